@@ -1,0 +1,139 @@
+/*
+ * cftft_b200.h -- C ABI of the B200-native truncated Fourier transform engine.
+ *
+ * Drop-in boundary for the reference's transform entry points
+ * (/root/reference/proj/include/cftft/transform.hpp), re-targeted at the
+ * large-coefficient rings of the BASELINE north star:
+ *
+ *   FERMAT      R = Z/(2^N+1), omega = 2, root order M = 2N   (Schoenhage-Strassen)
+ *   NEGACYCLIC  R = (Z/mZ)[y]/(y^K+1), omega = y, M = 2K      (Nussbaumer)
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.
+ *
+ * Element format (little-endian u64 words):
+ *   FERMAT      N/64 limbs followed by one top word; canonical value in
+ *               [0, 2^N] (top == 1 only for 2^N == -1, all limbs zero).
+ *   NEGACYCLIC  K words, each canonical in [0, m).
+ * Element i of a view lives at base + i * elem_stride_bytes; the stride must
+ * be a multiple of 16 and at least cftft_ring_element_bytes(ring).  This is
+ * the byte-level form of cftft::StridedView (view.hpp:14-51): a reference
+ * view (buffer, base, stride) maps to base_ptr = buffer + base*size and
+ * elem_stride_bytes = stride*size.
+ *
+ * Errors map 1:1 onto the reference's exceptions:
+ *   CFTFT_BAD_LENGTH      <- cftft::BadLength      (transform.hpp:16-20)
+ *   CFTFT_INVALID_PARAMS  <- cftft::InvalidParams  (transform.hpp:22-24)
+ * and are raised before any work is enqueued.  cftft_last_error() returns
+ * the message of the last failure on the calling thread.
+ */
+#ifndef CFTFT_B200_H
+#define CFTFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum cftft_status {
+  CFTFT_OK = 0,
+  CFTFT_BAD_LENGTH = 1,     /* L not a power of two in [2, M]               */
+  CFTFT_INVALID_PARAMS = 2, /* z, n, f outside the reference's contract      */
+  CFTFT_CUDA_ERROR = 3,     /* CUDA runtime failure (no GPU, launch error)  */
+  CFTFT_UNSUPPORTED = 4,    /* ring/stride the engine does not implement    */
+  CFTFT_NO_MEMORY = 5
+};
+
+enum cftft_ring_kind { CFTFT_RING_FERMAT = 1, CFTFT_RING_NEGACYCLIC = 2 };
+
+/* cftft::SplitPolicy (transform.hpp:27-30). */
+enum cftft_split_policy { CFTFT_BALANCED = 0, CFTFT_RADIX2 = 1 };
+
+/* cftft::TransformParams (transform.hpp:39-45). */
+typedef struct cftft_params {
+  uint64_t length;       /* L = 2^ell, 2 <= L <= M                    */
+  uint64_t twiddle_exp;  /* s: zeta = omega^s, reduced mod M on use   */
+  uint64_t input_count;  /* z                                         */
+  uint64_t output_count; /* n                                         */
+  int32_t want_next;     /* f (inverse transform only)                */
+} cftft_params;
+
+typedef struct cftft_ring cftft_ring;
+
+/* Ring contexts replace cftft::RingCtx (field.hpp:84-185).  For FERMAT,
+ * n_or_k = N (a power of two, >= 64) and modulus is ignored.  For
+ * NEGACYCLIC, n_or_k = K (a power of two) and modulus = m (odd, < 2^62).
+ * Immutable and shareable across threads once created. */
+int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** out);
+void cftft_ring_destroy(cftft_ring* ring);
+uint64_t cftft_ring_root_order(const cftft_ring* ring);    /* M */
+uint64_t cftft_ring_element_bytes(const cftft_ring* ring); /* minimal stride */
+
+/* Tuning/testing knob: caps the on-chip leaf size at 2^max_ell coefficients
+ * (default: the largest that fits the shared-memory budget).  Smaller caps
+ * force deeper Bailey decompositions (more waves); results are unchanged.
+ * Returns the cap in effect.  Must not race with transforms on the ring. */
+unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell);
+
+/* Forward truncated transform, in place over a DEVICE view
+ * (replaces cftft::cf_tft, transform.hpp:252-264).  On entry x[0..z) hold
+ * the coefficients (cells beyond are never read); on exit x[0..n) hold the
+ * first n transformed values in bit-reversed order; x[n..L) are unspecified.
+ * Asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * base_case_count (nullable) receives the reference's ButterflyStats count
+ * (transform.hpp:47-51), computed by schedule replay on the host. */
+int cftft_gpu_tft(const cftft_ring* ring, const cftft_params* params, void* dev_base,
+                  uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count,
+                  void* stream);
+
+/* Inverse truncated transform, in place over a DEVICE view
+ * (replaces cftft::cf_itft, transform.hpp:273-286).  On entry x[0..n) hold
+ * transformed values and x[n..z) hold L times the coefficients; on exit
+ * x[0..n) hold L times the coefficients and, if f = 1, x[n] holds the next
+ * transformed value. */
+int cftft_gpu_itft(const cftft_ring* ring, const cftft_params* params, void* dev_base,
+                   uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count,
+                   void* stream);
+
+/* Host-buffer forms: the same contract as cf_tft/cf_itft on a HOST view
+ * (synchronous, like the reference).  The engine stages x[0..z) to the GPU,
+ * transforms, and copies back x[0..n) (+ x[n] for f = 1).  Pinned host
+ * memory gives full PCIe bandwidth but is not required. */
+int cftft_tft_host(const cftft_ring* ring, const cftft_params* params, void* host_base,
+                   uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count);
+int cftft_itft_host(const cftft_ring* ring, const cftft_params* params, void* host_base,
+                    uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count);
+
+/* Pointwise ring products a[i] <- a[i] * b[i], i < count, on device views
+ * (the pointwise stage of cftft::poly_mul, polymul.hpp:73-77). */
+int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
+                        uint64_t elem_stride_bytes, void* stream);
+
+/* Scales x[0..count) by omega^e (e.g. 1/L = omega^(M - ell) in the Fermat
+ * ring, or the SS final 2^-k scale); device view, asynchronous. */
+int cftft_gpu_scale(const cftft_ring* ring, void* dev_base, uint64_t count,
+                    uint64_t elem_stride_bytes, uint64_t e, void* stream);
+
+/* Base-case counts of the reference recursion (data independent;
+ * verify.hpp:459-483), by host replay.  No GPU needed. */
+uint64_t cftft_tft_base_cases(uint64_t L, uint64_t z, uint64_t n, int policy);
+uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int policy);
+
+/* Launch statistics of the last transform issued on this thread: number of
+ * kernels enqueued (for bench.py's gpu_launches). */
+uint64_t cftft_last_launch_count(void);
+
+/* Debug: JSON description of the GPU schedule (leaves, waves, micro-ops) a
+ * transform would run.  Pure host code (no GPU).  Returns the number of
+ * bytes needed (including the terminating NUL); writes at most cap bytes. */
+size_t cftft_plan_dump(const cftft_ring* ring, int inverse, const cftft_params* params,
+                       int policy, char* buf, size_t cap);
+
+const char* cftft_last_error(void);
+const char* cftft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,500 @@
+// capi.cu -- the C ABI (include/cftft_b200.h) over the planner and the
+// sm_100a leaf kernels.  Host C++; no torch types anywhere.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/cftft_b200.h"
+#include "fermat_leaf.cuh"
+#include "negacyclic_leaf.cuh"
+#include "planner.hpp"
+
+using namespace cftft_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local u64 g_last_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(CFTFT_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_));    \
+  } while (0)
+
+constexpr size_t kSmemBudget = 200 * 1024;  // per-CTA dynamic shared memory we plan for
+
+// A plan resident on one device.
+struct DevicePlan {
+  Plan host;
+  void* dbuf = nullptr;
+  const DevClass* classes = nullptr;
+  const DevOp* ops = nullptr;
+  const u32* levels = nullptr;
+  const SymExp* stores = nullptr;
+  const DevLeaf* leaves = nullptr;
+  struct W {
+    u64 offset, count;
+    unsigned max_ell;
+  };
+  std::vector<W> waves;
+  ~DevicePlan() {
+    if (dbuf) cudaFree(dbuf);
+  }
+};
+
+using PlanKey = std::tuple<int, int, u64, u64, u64, u64, int, int>;  // dev, inv, L, s, z, n, f, policy
+
+}  // namespace
+
+struct cftft_ring {
+  int kind = 0;
+  u64 N = 0, K = 0, m = 0, M = 0;
+  u32 D = 0, C = 0;     // Fermat: u32 words / 128-bit chunks
+  u32 slot_bytes = 0;   // shared-memory bytes per slot
+  u64 elem_bytes = 0;   // minimal element stride
+  unsigned max_leaf_ell = 1;
+  unsigned max_leaf_fit = 1;
+  std::mutex mu;
+  std::map<PlanKey, std::unique_ptr<DevicePlan>> cache;
+  // staging buffer for the host-view entry points
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  CountReplay counts;
+  ~cftft_ring() {
+    if (stage) cudaFree(stage);
+  }
+};
+
+namespace {
+
+int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
+  const Plan& p = dp.host;
+  std::vector<DevClass> cls;
+  std::vector<DevOp> ops;
+  std::vector<u32> levels;
+  std::vector<SymExp> stores;
+  for (const auto& c : p.classes) {
+    DevClass d{};
+    d.L = 1u << c.key.ell;
+    d.nload = c.nload;
+    d.nstore = c.nstore;
+    d.nlevels = (u32)c.level_begin.size() - 1;
+    d.level_begin = (u32)levels.size();
+    d.store_begin = (u32)stores.size();
+    u32 op0 = (u32)ops.size();
+    for (u32 x : c.level_begin) levels.push_back(op0 + x);
+    ops.insert(ops.end(), c.ops.begin(), c.ops.end());
+    stores.insert(stores.end(), c.store_rot.begin(), c.store_rot.end());
+    cls.push_back(d);
+  }
+  std::vector<DevLeaf> leaves;
+  for (const auto& w : p.waves) {
+    dp.waves.push_back({(u64)leaves.size(), (u64)w.leaves.size(), w.max_ell});
+    leaves.insert(leaves.end(), w.leaves.begin(), w.leaves.end());
+  }
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t o_cls = 0, o_ops = al(o_cls + cls.size() * sizeof(DevClass));
+  size_t o_lev = al(o_ops + ops.size() * sizeof(DevOp));
+  size_t o_st = al(o_lev + levels.size() * sizeof(u32));
+  size_t o_lf = al(o_st + stores.size() * sizeof(SymExp));
+  size_t total = al(o_lf + leaves.size() * sizeof(DevLeaf)) + 256;
+  std::vector<std::uint8_t> h(total, 0);
+  std::memcpy(h.data() + o_cls, cls.data(), cls.size() * sizeof(DevClass));
+  std::memcpy(h.data() + o_ops, ops.data(), ops.size() * sizeof(DevOp));
+  std::memcpy(h.data() + o_lev, levels.data(), levels.size() * sizeof(u32));
+  std::memcpy(h.data() + o_st, stores.data(), stores.size() * sizeof(SymExp));
+  std::memcpy(h.data() + o_lf, leaves.data(), leaves.size() * sizeof(DevLeaf));
+  CUDA_TRY(cudaMalloc(&dp.dbuf, total));
+  CUDA_TRY(cudaMemcpyAsync(dp.dbuf, h.data(), total, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));  // h is a temporary
+  auto* b = static_cast<std::uint8_t*>(dp.dbuf);
+  dp.classes = reinterpret_cast<const DevClass*>(b + o_cls);
+  dp.ops = reinterpret_cast<const DevOp*>(b + o_ops);
+  dp.levels = reinterpret_cast<const u32*>(b + o_lev);
+  dp.stores = reinterpret_cast<const SymExp*>(b + o_st);
+  dp.leaves = reinterpret_cast<const DevLeaf*>(b + o_lf);
+  (void)R;
+  return CFTFT_OK;
+}
+
+RingShape shape_of(const cftft_ring* R) {
+  RingShape rs;
+  rs.fermat = (R->kind == CFTFT_RING_FERMAT);
+  rs.M = R->M;
+  rs.max_leaf_ell = R->max_leaf_ell;
+  return rs;
+}
+
+int get_plan(cftft_ring* R, bool inv, const cftft_params& p, int policy, cudaStream_t st,
+             DevicePlan** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  PlanKey key{dev, inv ? 1 : 0, p.length, p.twiddle_exp & (R->M - 1), p.input_count,
+              p.output_count, inv ? p.want_next : 0, policy};
+  std::lock_guard<std::mutex> g(R->mu);
+  auto it = R->cache.find(key);
+  if (it != R->cache.end()) {
+    *out = it->second.get();
+    return CFTFT_OK;
+  }
+  auto dp = std::make_unique<DevicePlan>();
+  Planner pl(shape_of(R));
+  dp->host = pl.build(inv, p.length, p.twiddle_exp, p.input_count, p.output_count,
+                      inv ? p.want_next : 0, policy);
+  int rc = upload(R, *dp, st);
+  if (rc) return rc;
+  *out = dp.get();
+  R->cache[key] = std::move(dp);
+  return CFTFT_OK;
+}
+
+int validate(const cftft_ring* R, bool inv, const cftft_params* p, int policy) {
+  if (!R || !p) return fail(CFTFT_INVALID_PARAMS, "null ring or params");
+  const u64 L = p->length;
+  if (L < 2 || (L & (L - 1)) != 0 || L > R->M)  // transform.hpp:241-243
+    return fail(CFTFT_BAD_LENGTH, "transform length " + std::to_string(L) +
+                                      " is not a power of two dividing the root order");
+  if (policy != CFTFT_BALANCED && policy != CFTFT_RADIX2)
+    return fail(CFTFT_INVALID_PARAMS, "unknown split policy");
+  if (!inv) {  // transform.hpp:255-259
+    if (p->input_count < 1 || p->input_count > L || p->output_count < 1 || p->output_count > L)
+      return fail(CFTFT_INVALID_PARAMS, "tft requires 1 <= z <= L and 1 <= n <= L");
+    if (p->want_next != 0) return fail(CFTFT_INVALID_PARAMS, "the forward transform takes no f flag");
+  } else {  // transform.hpp:276-281
+    if (p->want_next != 0 && p->want_next != 1) return fail(CFTFT_INVALID_PARAMS, "f must be 0 or 1");
+    const u64 nf = p->output_count + (u64)p->want_next;
+    if (p->input_count < 1 || p->input_count > L || nf < 1 || nf > L ||
+        p->input_count < p->output_count)
+      return fail(CFTFT_INVALID_PARAMS, "itft requires 1 <= z <= L, 1 <= n+f <= L and z >= n");
+  }
+  return CFTFT_OK;
+}
+
+int check_stride(const cftft_ring* R, u64 stride) {
+  if (stride < R->elem_bytes || (stride % 16) != 0)
+    return fail(CFTFT_UNSUPPORTED, "element stride must be a multiple of 16 and >= " +
+                                       std::to_string(R->elem_bytes) + " bytes");
+  return CFTFT_OK;
+}
+
+template <class K>
+int set_smem(K kernel) {
+  static bool done = false;
+  if (!done) {
+    CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSmemBudget));
+    done = true;
+  }
+  return CFTFT_OK;
+}
+
+int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
+                bool canonicalize) {
+  u64 launches = 0;
+  if (R->kind == CFTFT_RING_FERMAT) {
+    if (int rc = set_smem(fermat::leaf_kernel)) return rc;
+    fermat::Args A{};
+    A.data = base;
+    A.elem_bytes = stride;
+    A.classes = dp.classes;
+    A.ops = dp.ops;
+    A.levels = dp.levels;
+    A.stores = dp.stores;
+    A.N = R->N;
+    A.M = R->M;
+    A.D = R->D;
+    A.C = R->C;
+    A.slot_bytes = R->slot_bytes;
+    for (const auto& w : dp.waves) {
+      if (!w.count) continue;
+      A.leaves = dp.leaves + w.offset;
+      size_t smem = (size_t)R->slot_bytes << w.max_ell;
+      fermat::leaf_kernel<<<(unsigned)w.count, fermat::kThreads, smem, st>>>(A);
+      ++launches;
+    }
+    if (canonicalize && dp.host.final_count) {
+      u64 cnt = dp.host.final_count;
+      fermat::canonicalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, stride, cnt,
+                                                                                  R->D);
+      ++launches;
+    }
+  } else {
+    if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
+    negacyclic::Args A{};
+    A.data = base;
+    A.elem_bytes = stride;
+    A.classes = dp.classes;
+    A.ops = dp.ops;
+    A.levels = dp.levels;
+    A.stores = dp.stores;
+    A.K = R->K;
+    A.M = R->M;
+    A.m = R->m;
+    A.slot_bytes = R->slot_bytes;
+    for (const auto& w : dp.waves) {
+      if (!w.count) continue;
+      A.leaves = dp.leaves + w.offset;
+      size_t smem = (size_t)R->slot_bytes << w.max_ell;
+      negacyclic::leaf_kernel<<<(unsigned)w.count, negacyclic::kThreads, smem, st>>>(A);
+      ++launches;
+    }
+  }
+  g_last_launches = launches;
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* dev_base, u64 stride,
+              int policy, uint64_t* count, void* stream) {
+  if (int rc = validate(cR, inv, p, policy)) return rc;
+  if (int rc = check_stride(cR, stride)) return rc;
+  auto* R = const_cast<cftft_ring*>(cR);
+  if (count) {
+    std::lock_guard<std::mutex> g(R->mu);
+    *count = inv ? R->counts.itft(p->length, p->input_count, p->output_count, p->want_next, policy)
+                 : R->counts.tft(p->length, p->input_count, p->output_count, policy);
+  }
+  auto st = static_cast<cudaStream_t>(stream);
+  DevicePlan* dp = nullptr;
+  if (int rc = get_plan(R, inv, *p, policy, st, &dp)) return rc;
+  return launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), stride, st, true);
+}
+
+int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* host_base,
+                   u64 stride, int policy, uint64_t* count) {
+  if (int rc = validate(cR, inv, p, policy)) return rc;
+  if (int rc = check_stride(cR, stride)) return rc;
+  auto* R = const_cast<cftft_ring*>(cR);
+  const u64 L = p->length;
+  const size_t need = (size_t)L * stride;
+  {
+    std::lock_guard<std::mutex> g(R->mu);
+    if (R->stage_bytes < need) {
+      if (R->stage) cudaFree(R->stage);
+      R->stage = nullptr;
+      R->stage_bytes = 0;
+      CUDA_TRY(cudaMalloc(&R->stage, need));
+      R->stage_bytes = need;
+    }
+  }
+  const u64 in = p->input_count;
+  const u64 out = inv ? p->output_count + (u64)p->want_next : p->output_count;
+  const size_t eb = R->elem_bytes;
+  CUDA_TRY(cudaMemcpy2D(R->stage, stride, host_base, stride, eb, in, cudaMemcpyHostToDevice));
+  int rc = transform(R, inv, p, R->stage, stride, policy, count, nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy2D(host_base, stride, R->stage, stride, eb, out, cudaMemcpyDeviceToHost));
+  return CFTFT_OK;
+}
+
+void json_plan(std::ostringstream& os, const Plan& p) {
+  os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"L\":" << p.L << ",\"s\":" << p.s
+     << ",\"z\":" << p.z << ",\"n\":" << p.n << ",\"f\":" << p.f << ",\"final_count\":"
+     << p.final_count << ",\"classes\":[";
+  for (size_t c = 0; c < p.classes.size(); ++c) {
+    const auto& k = p.classes[c];
+    if (c) os << ",";
+    os << "{\"ell\":" << k.key.ell << ",\"inverse\":" << k.key.inverse << ",\"z\":" << k.key.z
+       << ",\"n\":" << k.key.n << ",\"f\":" << k.key.f << ",\"nload\":" << k.nload
+       << ",\"nstore\":" << k.nstore << ",\"levels\":[";
+    for (size_t l = 0; l < k.level_begin.size(); ++l) os << (l ? "," : "") << k.level_begin[l];
+    os << "],\"ops\":[";
+    for (size_t i = 0; i < k.ops.size(); ++i) {
+      const auto& o = k.ops[i];
+      os << (i ? "," : "") << "[" << (int)o.type << "," << o.a << "," << o.b << "," << o.ra << ","
+         << o.rb << "]";
+    }
+    os << "],\"store\":[";
+    for (size_t i = 0; i < k.store_rot.size(); ++i)
+      os << (i ? "," : "") << "[" << k.store_rot[i].a << "," << k.store_rot[i].b << "]";
+    os << "]}";
+  }
+  os << "],\"waves\":[";
+  for (size_t w = 0; w < p.waves.size(); ++w) {
+    os << (w ? "," : "") << "[";
+    const auto& lv = p.waves[w].leaves;
+    for (size_t i = 0; i < lv.size(); ++i)
+      os << (i ? "," : "") << "[" << lv[i].cls << "," << lv[i].base << "," << lv[i].stride << ","
+         << lv[i].s << "]";
+    os << "]";
+  }
+  os << "]}";
+}
+
+}  // namespace
+
+extern "C" {
+
+int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** out) {
+  if (!out) return fail(CFTFT_INVALID_PARAMS, "null out");
+  *out = nullptr;
+  auto R = std::make_unique<cftft_ring>();
+  R->kind = kind;
+  if (kind == CFTFT_RING_FERMAT) {
+    const u64 N = n_or_k;
+    if (N < 128 || (N & (N - 1)) != 0)
+      return fail(CFTFT_UNSUPPORTED, "Fermat ring needs N a power of two >= 128");
+    R->N = N;
+    R->M = 2 * N;
+    R->D = (u32)(N / 32);
+    R->C = R->D / 4;
+    const u32 pend = (R->C + 15) & ~15u;
+    R->slot_bytes = 4 * R->D + pend;
+    R->elem_bytes = ((N / 8 + 8) + 15) & ~u64(15);
+  } else if (kind == CFTFT_RING_NEGACYCLIC) {
+    const u64 K = n_or_k, m = modulus;
+    if (K < 2 || (K & (K - 1)) != 0 || K > 16384)
+      return fail(CFTFT_UNSUPPORTED, "negacyclic ring needs K a power of two in [2, 16384]");
+    if (m < 3 || (m & 1) == 0 || m >= (u64{1} << 62))
+      return fail(CFTFT_INVALID_PARAMS, "negacyclic modulus must be odd and < 2^62");
+    R->K = K;
+    R->m = m;
+    R->M = 2 * K;
+    R->slot_bytes = (u32)(8 * K);
+    R->elem_bytes = 8 * K;
+  } else {
+    return fail(CFTFT_UNSUPPORTED, "unknown ring kind");
+  }
+  // largest leaf whose slots fit the shared-memory budget (and the 16-bit slot ids)
+  unsigned lam = 1;
+  while (lam < 15 && ((size_t)R->slot_bytes << (lam + 1)) <= kSmemBudget) ++lam;
+  R->max_leaf_ell = lam;
+  R->max_leaf_fit = lam;
+  *out = R.release();
+  return CFTFT_OK;
+}
+
+void cftft_ring_destroy(cftft_ring* ring) { delete ring; }
+uint64_t cftft_ring_root_order(const cftft_ring* ring) { return ring ? ring->M : 0; }
+uint64_t cftft_ring_element_bytes(const cftft_ring* ring) { return ring ? ring->elem_bytes : 0; }
+
+unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell) {
+  if (!ring) return 0;
+  std::lock_guard<std::mutex> g(ring->mu);
+  unsigned cap = ring->max_leaf_fit;
+  unsigned v = max_ell == 0 ? cap : std::min(std::max(max_ell, 1u), cap);
+  if (v != ring->max_leaf_ell) {
+    ring->max_leaf_ell = v;
+    ring->cache.clear();
+  }
+  return v;
+}
+
+int cftft_gpu_tft(const cftft_ring* ring, const cftft_params* params, void* dev_base,
+                  uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count, void* stream) {
+  return transform(ring, false, params, dev_base, elem_stride_bytes, policy, base_case_count, stream);
+}
+
+int cftft_gpu_itft(const cftft_ring* ring, const cftft_params* params, void* dev_base,
+                   uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count, void* stream) {
+  return transform(ring, true, params, dev_base, elem_stride_bytes, policy, base_case_count, stream);
+}
+
+int cftft_tft_host(const cftft_ring* ring, const cftft_params* params, void* host_base,
+                   uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count) {
+  return host_transform(ring, false, params, host_base, elem_stride_bytes, policy, base_case_count);
+}
+
+int cftft_itft_host(const cftft_ring* ring, const cftft_params* params, void* host_base,
+                    uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count) {
+  return host_transform(ring, true, params, host_base, elem_stride_bytes, policy, base_case_count);
+}
+
+int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
+                        uint64_t elem_stride_bytes, void* stream) {
+  (void)ring;
+  (void)dev_a;
+  (void)dev_b;
+  (void)count;
+  (void)elem_stride_bytes;
+  (void)stream;
+  return fail(CFTFT_UNSUPPORTED, "pointwise products are not implemented yet");
+}
+
+int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
+                    uint64_t elem_stride_bytes, uint64_t e, void* stream) {
+  if (!cring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (int rc = check_stride(cring, elem_stride_bytes)) return rc;
+  if (count == 0) return CFTFT_OK;
+  auto* R = const_cast<cftft_ring*>(cring);
+  auto st = static_cast<cudaStream_t>(stream);
+  // A scale is a degenerate plan: one length-1 class (load, no ops, store
+  // with rotation e) and one leaf per element.
+  const u64 M = R->M;
+  PlanKey key{-1, 2, 1, e & (M - 1), count, 0, 0, 0};
+  DevicePlan* dp = nullptr;
+  {
+    std::lock_guard<std::mutex> g(R->mu);
+    auto it = R->cache.find(key);
+    if (it != R->cache.end()) {
+      dp = it->second.get();
+    } else {
+      auto np = std::make_unique<DevicePlan>();
+      LeafProgram lp;
+      lp.key = ClassKey{0, 0, 1, 1, 0};
+      lp.nload = 1;
+      lp.nstore = 1;
+      lp.level_begin = {0};
+      lp.store_rot = {SymExp{0, e & (M - 1)}};
+      np->host.classes.push_back(lp);
+      Wave w;
+      w.max_ell = 0;
+      for (u64 i = 0; i < count; ++i) w.leaves.push_back(DevLeaf{0, 0, i, 1, 0});
+      np->host.waves.push_back(std::move(w));
+      np->host.final_count = count;
+      if (int rc = upload(R, *np, st)) return rc;
+      dp = np.get();
+      R->cache[key] = std::move(np);
+    }
+  }
+  return launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, st, true);
+}
+
+uint64_t cftft_tft_base_cases(uint64_t L, uint64_t z, uint64_t n, int policy) {
+  CountReplay c;
+  return c.tft(L, z, n, policy);
+}
+uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int policy) {
+  CountReplay c;
+  return c.itft(L, z, n, f, policy);
+}
+
+uint64_t cftft_last_launch_count(void) { return g_last_launches; }
+
+size_t cftft_plan_dump(const cftft_ring* ring, int inverse, const cftft_params* params, int policy,
+                       char* buf, size_t cap) {
+  if (validate(ring, inverse != 0, params, policy)) return 0;
+  Planner pl(shape_of(ring));
+  Plan p = pl.build(inverse != 0, params->length, params->twiddle_exp, params->input_count,
+                    params->output_count, inverse ? params->want_next : 0, policy);
+  std::ostringstream os;
+  json_plan(os, p);
+  std::string s = os.str();
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return s.size() + 1;
+}
+
+const char* cftft_last_error(void) { return g_last_error.c_str(); }
+const char* cftft_version(void) { return "cftft-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,186 @@
+"""The C ABI and the host planner, on the CPU (no GPU calls).
+
+  * libcftft_b200.so loads and exports every symbol include/cftft_b200.h declares
+  * validation maps onto BadLength / InvalidParams before any GPU work
+  * the planner's base-case replay equals the reference's ButterflyStats at
+    the BASELINE shapes (tests/golden/counts.json)
+  * the GPU schedule (leaves, waves, micro-ops with pending rotations),
+    executed at the VALUE level with Python integers, reproduces the
+    definition of the TFT/ITFT: this pins the planner independently of the
+    kernels' limb arithmetic
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import random
+import re
+
+import pytest
+
+import bigint_model as bm
+import paper_0810_3203_b200 as cf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "cftft_b200.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(cftft_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = cf.lib()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert b"sm_100a" in lib.cftft_version()
+
+
+def test_ring_contexts():
+    f = cf.FermatRingCtx(32768)
+    assert f.root_order() == 65536
+    assert f.element_bytes == 4096 + 16
+    n = cf.NegacyclicRingCtx(1024, (1 << 61) + 15)
+    assert n.root_order() == 2048 and n.element_bytes == 8192
+    with pytest.raises(cf.Unsupported):
+        cf.FermatRingCtx(1000)
+    with pytest.raises(cf.InvalidParams):
+        cf.NegacyclicRingCtx(8, 96)  # even modulus
+
+
+def test_c_abi_validation_without_gpu():
+    lib = cf.lib()
+    ctx = cf.FermatRingCtx(128)  # M = 256
+
+    def call(L, z, n, f=0, inv=False, stride=None):
+        p = cf._Params(L, 0, z, n, f)
+        fn = lib.cftft_gpu_itft if inv else lib.cftft_gpu_tft
+        return fn(ctx._h, C.byref(p), None, stride or ctx.element_bytes, 0, None, None)
+
+    assert call(12, 1, 1) == 1
+    assert call(512, 1, 1) == 1  # exceeds the root order
+    assert call(8, 0, 1) == 2
+    assert call(8, 9, 1) == 2
+    assert call(8, 1, 0) == 2
+    assert call(8, 1, 1, f=1) == 2
+    assert call(8, 2, 3, inv=True) == 2
+    assert call(8, 1, 0, 0, inv=True) == 2
+    assert call(8, 8, 8, 1, inv=True) == 2
+    assert call(8, 8, 8, stride=24) == 4  # stride not a multiple of 16
+    with pytest.raises(cf.BadLength):
+        cf._validate(ctx, cf.TransformParams(12, 0, 1, 1), False, 12)
+    with pytest.raises(cf.InvalidParams):
+        cf._validate(ctx, cf.TransformParams(4, 0, 1, 1), False, 8)
+
+
+def test_base_case_counts_match_reference():
+    cases = json.load(open(os.path.join(GOLD, "counts.json")))
+    for c in cases:
+        if c["inverse"]:
+            got = cf.itft_base_cases(c["L"], c["z"], c["n"], c["f"], c["policy"])
+        else:
+            got = cf.tft_base_cases(c["L"], c["z"], c["n"], c["policy"])
+        assert got == c["count"], c
+
+
+def test_counts_full_transform_hits_ceiling():  # transform_test.cpp:342-351
+    for ell in range(1, 8):
+        L = 1 << ell
+        for pol in (0, 1):
+            assert 2 * cf.tft_base_cases(L, L, L, pol) == L * ell
+            assert 2 * cf.itft_base_cases(L, L, L, 0, pol) == L * ell
+
+
+def test_counts_respect_bounds():  # verify.hpp:507-553
+    for ell in range(1, 6):
+        L = 1 << ell
+        for z in range(1, L + 1):
+            for n in range(1, L + 1):
+                assert cf.tft_base_cases(L, z, n, 0) <= cf.tft_bound(L, n)
+            for n in range(0, z + 1):
+                for f in (0, 1):
+                    if 1 <= n + f <= L:
+                        assert cf.itft_base_cases(L, z, n, f, 1) <= cf.itft_bound(L, n, f)
+
+
+# ---- value-level execution of the GPU schedule ----------------------------------
+
+def run_plan_fermat(plan, N, vals):
+    P, M = (1 << N) + 1, 2 * N
+    x = dict(vals)
+    for wave in plan["waves"]:
+        for (cls, base, stride, s) in wave:
+            c = plan["classes"][cls]
+            slot = [None] * (1 << c["ell"])
+            for i in range(c["nload"]):
+                slot[i] = x[base + i * stride]
+            for (t, a, b, ra, rb) in c["ops"]:
+                r = (ra * s + rb) % M
+                if t == 4:
+                    slot[b] = slot[a]
+                    continue
+                A, B = slot[a], (slot[b] * pow(2, r, P)) % P
+                if t == 0:
+                    slot[a], slot[b] = (A + B) % P, (A - B) % P
+                elif t == 1:
+                    slot[a] = (A + B) % P
+                elif t == 2:
+                    slot[a] = (2 * A - B) % P
+                elif t == 3:
+                    slot[a], slot[b] = (2 * A - B) % P, (A - B) % P
+                else:
+                    raise AssertionError("negacyclic-only op in a Fermat plan")
+            for i in range(c["nstore"]):
+                ea, eb = c["store"][i]
+                x[base + i * stride] = (slot[i] * pow(2, (ea * s + eb) % M, P)) % P
+    return x
+
+
+def check_plan(ctx, N, rnd, trials):
+    fm = bm.FermatModel(N)
+    for _ in range(trials):
+        L = 1 << rnd.randint(1, 8)
+        z, n = rnd.randint(1, L), rnd.randint(1, L)
+        s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
+        a = [rnd.randrange((1 << N) + 1) for _ in range(z)]
+        want = fm.dft(L, s, a)
+        plan = cf.plan_dump(ctx, False, cf.TransformParams(L, s, z, n), pol)
+        x = run_plan_fermat(plan, N, {i: a[i] for i in range(z)})
+        assert [x[i] for i in range(n)] == want[:n], (N, L, z, n, s, pol)
+        n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+        if not 1 <= n2 + f <= L:
+            continue
+        vals = {i: want[i] for i in range(n2)}
+        vals.update({i: (L * a[i]) % fm.P for i in range(n2, z)})
+        plan = cf.plan_dump(ctx, True, cf.TransformParams(L, s, z, n2, f), pol)
+        x = run_plan_fermat(plan, N, vals)
+        assert [x[i] for i in range(n2)] == [(L * a[i]) % fm.P for i in range(n2)]
+        if f:
+            assert x[n2] == want[n2]
+
+
+@pytest.mark.parametrize("limit", [0, 1, 2, 3])
+def test_gpu_schedule_reproduces_definition(limit):
+    rnd = random.Random(limit)
+    for N in (128, 256):
+        ctx = cf.FermatRingCtx(N)
+        ctx.set_leaf_limit(limit)
+        check_plan(ctx, N, rnd, 40)
+
+
+def test_schedule_shape_config5():
+    """C5 (L=2^18, z=n=200000): top split 512x512, SMEM leaves of 8 -> 3 waves
+    per pass; only columns < z2' and rows < n1' are scheduled."""
+    ctx = cf.FermatRingCtx(131072)
+    assert ctx.set_leaf_limit(0) == 3
+    plan = cf.plan_dump(ctx, False, cf.TransformParams(1 << 18, 0, 200000, 200000))
+    assert len(plan["waves"]) == 6
+    # every column leaf of the first wave has stride 512*64 (top column stride x inner rows)
+    leaves0 = plan["waves"][0]
+    assert len(leaves0) == 512 * 64
+    assert all(lf[2] == 512 * 64 for lf in leaves0)

@@ -1,0 +1,203 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle,
+bit for bit, on seeded inputs.  Patterned on the reference's own suites
+(verify.hpp:85-173 oracle/inversion sweeps, transform_test.cpp:228-330)."""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from helpers import fermat_inputs, from_dev, negacyclic_inputs, random_modulus, to_dev
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_0810_3203_b200 as cf  # noqa: E402
+
+
+def _fermat_case(ctx, ring, N, L, z, n, s, pol, seed, inverse=False, f=0, special=False):
+    W = ctx.element_words
+    lim = N // 64
+    buf = fermat_inputs(N, L, z, W, seed, special=special)
+    want = buf.copy()
+    if inverse:
+        ring.itft(want, L, s, z, n, f, pol)
+    else:
+        ring.tft(want, L, s, z, n, pol)
+    dev = to_dev(buf)
+    view = cf.DeviceView(dev)
+    st = cf.ButterflyStats()
+    if inverse:
+        cf.cf_itft(ctx, cf.TransformParams(L, s, z, n, f), view, pol, st)
+    else:
+        cf.cf_tft(ctx, cf.TransformParams(L, s, z, n), view, pol, st)
+    got = from_dev(dev)
+    k = n + f if inverse else n
+    assert np.array_equal(got[:k, : lim + 1], want[:k, : lim + 1]), (N, L, z, n, f, s, pol, inverse)
+    ref_count = ring.itft(buf.copy(), L, s, z, n, f, pol) if inverse else ring.tft(buf.copy(), L, s, z, n, pol)
+    assert st.base_case_count == ref_count
+
+
+@pytest.mark.parametrize("N", [128, 256, 1024])
+@pytest.mark.parametrize("limit", [0, 1, 2, 3])
+def test_fermat_random_sweep(N, limit):
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_leaf_limit(limit)
+    ring = po.Ring.fermat(N)
+    rnd = random.Random(N * 10 + limit)
+    for trial in range(30):
+        L = 1 << rnd.randint(1, min(10, (2 * N).bit_length() - 1))
+        z, n = rnd.randint(1, L), rnd.randint(1, L)
+        s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
+        _fermat_case(ctx, ring, N, L, z, n, s, pol, seed=trial, special=(trial % 3 == 0))
+        n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+        if 1 <= n2 + f <= L:
+            _fermat_case(ctx, ring, N, L, z, n2, s, pol, seed=1000 + trial, inverse=True, f=f,
+                         special=(trial % 3 == 1))
+
+
+def test_fermat_exhaustive_small():
+    """Every (z, n) at L = 16, both policies (cf. verify.hpp:85-120)."""
+    N, L = 128, 16
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_leaf_limit(2)
+    ring = po.Ring.fermat(N)
+    for z in range(1, L + 1):
+        for n in range(1, L + 1):
+            for pol in (0, 1):
+                _fermat_case(ctx, ring, N, L, z, n, 37, pol, seed=z * 100 + n)
+        for n in range(0, z + 1):
+            for f in (0, 1):
+                if 1 <= n + f <= L:
+                    _fermat_case(ctx, ring, N, L, z, n, 5, 0, seed=z * 7 + n, inverse=True, f=f)
+
+
+def test_fermat_all_ones_and_minus_one():
+    """Inputs made only of 2^N-1 and 2^N (== -1): maximal carry chains."""
+    N, L = 1024, 64
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    W = ctx.element_words
+    lim = N // 64
+    buf = np.zeros((L, W), dtype=np.uint64)
+    for i in range(L):
+        if i % 2:
+            buf[i, :lim] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        else:
+            buf[i, lim] = 1
+    for inverse in (False, True):
+        want = buf.copy()
+        dev = to_dev(buf)
+        if inverse:
+            ring.itft(want, L, 3, L, L, 0, 0)
+            cf.cf_itft(ctx, cf.TransformParams(L, 3, L, L, 0), cf.DeviceView(dev))
+        else:
+            ring.tft(want, L, 3, L, L, 0)
+            cf.cf_tft(ctx, cf.TransformParams(L, 3, L, L), cf.DeviceView(dev))
+        got = from_dev(dev)
+        assert np.array_equal(got[:, : lim + 1], want[:, : lim + 1])
+
+
+def test_strided_view_leaves_surroundings_untouched():
+    """transform_test.cpp:292-313 restated on the device."""
+    N, L, stride, base = 256, 32, 3, 2
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    W = ctx.element_words
+    lim = N // 64
+    rows = base + (L - 1) * stride + 5
+    rng = np.random.default_rng(8)
+    full = np.zeros((rows, W), dtype=np.uint64)
+    full[:, :lim] = rng.integers(0, 1 << 64, size=(rows, lim), dtype=np.uint64, endpoint=False)
+    before = full.copy()
+    dev = to_dev(full)
+    view = cf.DeviceView(dev, base, stride, L)
+    cf.cf_tft(ctx, cf.TransformParams(L, 5, 20, 27), view)
+    after = from_dev(dev)
+    idx = [base + i * stride for i in range(L)]
+    mask = np.ones(rows, bool)
+    mask[idx] = False
+    assert np.array_equal(after[mask], before[mask])
+    # and the view cells match the oracle on a compact copy
+    want = before[idx].copy()
+    ring.tft(want, L, 5, 20, 27, 0)
+    assert np.array_equal(after[idx][:27, : lim + 1], want[:27, : lim + 1])
+
+
+def test_validation_errors():
+    """transform_test.cpp:360-390: errors are raised before any work."""
+    ctx = cf.FermatRingCtx(128)  # M = 256
+    dev = to_dev(np.zeros((8, ctx.element_words), dtype=np.uint64))
+    v = cf.DeviceView(dev)
+    with pytest.raises(cf.BadLength):
+        cf.cf_tft(ctx, cf.TransformParams(12, 0, 1, 1), cf.DeviceView(dev, 0, 1, 8))
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_tft(ctx, cf.TransformParams(8, 0, 0, 1), v)
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_tft(ctx, cf.TransformParams(8, 0, 9, 1), v)
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_tft(ctx, cf.TransformParams(8, 0, 1, 1, 1), v)
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_tft(ctx, cf.TransformParams(4, 0, 1, 1), v)  # view length 8 != L
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_itft(ctx, cf.TransformParams(8, 0, 2, 3), v)
+    with pytest.raises(cf.InvalidParams):
+        cf.cf_itft(ctx, cf.TransformParams(8, 0, 8, 8, 1), v)
+
+
+@pytest.mark.parametrize("K", [2, 8, 64, 1024])
+def test_negacyclic_random_sweep(K):
+    m = random_modulus(K)
+    ctx = cf.NegacyclicRingCtx(K, m)
+    ring = po.Ring.negacyclic(K, m)
+    rnd = random.Random(K)
+    W = ctx.element_words
+    for limit in (0, 2):
+        ctx.set_leaf_limit(limit)
+        for trial in range(12):
+            L = 1 << rnd.randint(1, min(11, (2 * K).bit_length() - 1))
+            z, n = rnd.randint(1, L), rnd.randint(1, L)
+            s, pol = rnd.randrange(2 * K), rnd.randint(0, 1)
+            buf = negacyclic_inputs(K, m, L, z, W, trial)
+            want = buf.copy()
+            ring.tft(want, L, s, z, n, pol)
+            dev = to_dev(buf)
+            cf.cf_tft(ctx, cf.TransformParams(L, s, z, n), cf.DeviceView(dev), pol)
+            assert np.array_equal(from_dev(dev)[:n, :K], want[:n, :K]), (K, L, z, n, s, pol)
+            n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+            if not 1 <= n2 + f <= L:
+                continue
+            buf = negacyclic_inputs(K, m, L, z, W, 100 + trial)
+            want = buf.copy()
+            ring.itft(want, L, s, z, n2, f, pol)
+            dev = to_dev(buf)
+            cf.cf_itft(ctx, cf.TransformParams(L, s, z, n2, f), cf.DeviceView(dev), pol)
+            assert np.array_equal(from_dev(dev)[: n2 + f, :K], want[: n2 + f, :K]), (K, L, z, n2, f)
+
+
+def test_c1_round_trip_bit_exact():
+    """BASELINE config 1: Z/(2^1024+1), L=2^10, z=n=700, zeta=1: bit-exact vs the
+    oracle, and ITFT(TFT(a)) = a after the 1/L = 2^(2048-10) scale."""
+    N, L, z = 1024, 1024, 700
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    W = ctx.element_words
+    lim = N // 64
+    buf = fermat_inputs(N, L, z, W, po.mix_seed(42, 1))
+    want = buf.copy()
+    ring.tft(want, L, 0, z, z, 0)
+    dev = to_dev(buf)
+    view = cf.DeviceView(dev)
+    cf.cf_tft(ctx, cf.TransformParams(L, 0, z, z), view)
+    got = from_dev(dev)
+    assert np.array_equal(got[:z, : lim + 1], want[:z, : lim + 1])
+    ring.itft(want, L, 0, z, z, 0, 0)
+    cf.cf_itft(ctx, cf.TransformParams(L, 0, z, z, 0), view)
+    assert np.array_equal(from_dev(dev)[:z, : lim + 1], want[:z, : lim + 1])
+    cf.scale(ctx, view, z, 2 * N - 10)
+    assert np.array_equal(from_dev(dev)[:z, : lim + 1], buf[:z, : lim + 1])
