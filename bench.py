@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- TFT+ITFT throughput (GB/s) on B200, against the host-CPU oracle.
+
+Default workload (BASELINE.json config 5, the metric's 1/2/4/8-GPU config):
+  R = Z/(2^131072+1) (16 KiB coefficients), L = 2^18, z = n = 200000, s = 0;
+  one step = cf_tft (z, n) followed by cf_itft (z = n, f = 0) in place: the
+  round trip over ~3.3 GB of coefficients (far larger than the 126 MB L2, so
+  no L2 flush is needed between steps).
+
+Metric: GB/s = (TFT bytes + ITFT bytes) / (TFT time + ITFT time), with the
+ALGORITHMIC bytes of a two-pass Bailey decomposition at the top-level split
+(SURVEY.md §8d):
+  TFT  bytes = B (z + 2 n1' z2' + n)
+  ITFT bytes = B [2 n1 L2 + sum_{u in [n2,z2')} (r(u) + n1 + f') + f'(z2' + n2 + f)
+                  + sum_{u < n2} (r(u) + n1 + 1)],   r(u) = z1 + [u < z2]
+  B = N/8 information bytes per coefficient.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--config C1|C2|C4|C5] [--no-cpu] [--no-e2e]
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (N bits, L, z, n, description)
+    "C1": (1024, 1 << 10, 700, 700, "Z/(2^1024+1), L=2^10, z=n=700"),
+    "C2": (32768, 1 << 16, 65535, 65535, "Z/(2^32768+1), L=2^16, z=n=65535 (largest C2 pair)"),
+    "C4": (65536, 1 << 17, 119999, 119999, "Z/(2^65536+1), L=2^17, z=n=119999 (C4 ITFT shape)"),
+    "C5": (131072, 1 << 18, 200000, 200000, "Z/(2^131072+1), L=2^18, z=n=200000"),
+}
+
+
+# ---------------------------------------------------------------------------
+def split(ell: int, policy: int = 0):
+    return (1, ell - 1) if policy else (ell // 2, ell - ell // 2)
+
+
+def tft_bytes(N: int, L: int, z: int, n: int) -> int:
+    B = N // 8
+    ell = L.bit_length() - 1
+    l1, l2 = split(ell)
+    cols = 1 << l2
+    n2, n1 = n & (cols - 1), n >> l2
+    n1c = n1 + (1 if n2 else 0)
+    z2, z1 = z & (cols - 1), z >> l2
+    z2e = cols if z1 else z2
+    return B * (z + 2 * n1c * z2e + n)
+
+
+def itft_bytes(N: int, L: int, z: int, n: int, f: int) -> int:
+    B = N // 8
+    ell = L.bit_length() - 1
+    l1, l2 = split(ell)
+    cols = 1 << l2
+    n2, n1 = n & (cols - 1), n >> l2
+    z2, z1 = z & (cols - 1), z >> l2
+    fm = 1 if n2 + f > 0 else 0
+    z2e = cols if z1 else z2
+
+    def r(u):
+        return z1 + (1 if u < z2 else 0)
+
+    tot = 2 * n1 * cols
+    tot += sum(r(u) + n1 + fm for u in range(n2, z2e))
+    tot += fm * (z2e + n2 + f)
+    tot += sum(r(u) + n1 + 1 for u in range(n2))
+    return B * tot
+
+
+def hbm_peak():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        try:
+            with open(p) as fh:
+                return float(json.load(fh)["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def load_traffic(cfg: str):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(cfg)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def make_input(N: int, L: int, z: int, W: int, seed: int):
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    buf = np.zeros((L, W), dtype=np.uint64)
+    lim = N // 64
+    step = 8192
+    for i in range(0, z, step):
+        k = min(step, z - i)
+        buf[i:i + k, :lim] = rng.integers(0, 1 << 64, size=(k, lim), dtype=np.uint64, endpoint=False)
+    return buf
+
+
+def cpu_round_trip(N, L, z, n, buf, threads):
+    """The oracle port (oracle/cftft_oracle.c) on the host: TFT then ITFT."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    ring = po.Ring.fermat(N)
+    t0 = time.perf_counter()
+    ring.tft(buf, L, 0, z, n, 0, threads=threads)
+    t1 = time.perf_counter()
+    ring.itft(buf, L, 0, n, n, 0, 0, threads=threads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, cfgname):
+    """--impl reference: the CPU implementation of the path on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    N, L, z, n, desc = CONFIGS[cfgname]
+    threads, model = cpu_info()
+    W = N // 64 + 2
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    po.build()
+    buf = make_input(N, L, z, W, po.mix_seed(42, 5))
+    byts = tft_bytes(N, L, z, n) + itft_bytes(N, L, n, n, 0)
+    times = []
+    for i in range(args.warmup + args.steps):
+        a, b = cpu_round_trip(N, L, z, n, buf, threads)
+        if i >= args.warmup:
+            times.append(a + b)
+    tot = sum(times)
+    gbs = byts * len(times) / tot / 1e9
+    line = {
+        "impl": "reference",
+        "metric": f"TFT+ITFT GB/s ({cfgname}: {desc})",
+        "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfgname, "ring": f"Z/(2^{N}+1)", "L": L, "z": z, "n": n},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"full {cfgname} TFT+ITFT round trip per step on {threads} threads "
+                                   f"({model}); oracle/cftft_oracle.c (the reference implements no "
+                                   f"Fermat ring, SPEC.md:13)"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+
+    if args.impl == "reference":
+        run_reference(args, args.config)
+        return
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_0810_3203_b200 as cf
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    N, L, z, n, desc = CONFIGS[args.config]
+    ctx = cf.FermatRingCtx(N)
+    W = ctx.element_words
+    host = make_input(N, L, z, W, po.mix_seed(42, 5 + rank))
+    dev = torch.from_numpy(host.view(np.int64)).cuda()
+    view = cf.DeviceView(dev)
+    stream = torch.cuda.current_stream()
+    pt = cf.TransformParams(L, 0, z, n)
+    pi = cf.TransformParams(L, 0, n, n, 0)
+    byts = tft_bytes(N, L, z, n) + itft_bytes(N, L, n, n, 0)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        cf.cf_tft(ctx, pt, view, stream=stream)
+        l1 = cf.last_launch_count()
+        if evs:
+            evs[1].record(stream)
+        cf.cf_itft(ctx, pi, view, stream=stream)
+        l2 = cf.last_launch_count()
+        if evs:
+            evs[2].record(stream)
+        return l1 + l2
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    g0.record(stream)
+    launches = 0
+    for k in range(args.steps):
+        launches += step(evs[k])
+    g1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    total_ms = g0.elapsed_time(g1)
+    t_tft = sum(e[0].elapsed_time(e[1]) for e in evs)
+    t_itft = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if dist is not None:
+        t = torch.tensor([total_ms, t_tft, t_itft], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, t_tft, t_itft = t.tolist()
+    ms_per_step = total_ms / args.steps
+    value = world * byts * args.steps / (total_ms / 1e3) / 1e9
+    kernel_gbs = byts * args.steps / ((t_tft + t_itft) / 1e3) / 1e9
+    peak, peak_kind = hbm_peak()
+
+    # ---- end to end through the public API with host buffers -----------------
+    e2e = None
+    if not args.no_e2e:
+        elem = ctx.element_bytes
+        pin_in = torch.from_numpy(host.view(np.int64)).pin_memory()
+        pin_out = torch.empty_like(pin_in).pin_memory()
+        ek = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ek):
+            dev[:z].copy_(pin_in[:z], non_blocking=True)
+            step()
+            pin_out[:n].copy_(dev[:n], non_blocking=True)
+            torch.cuda.synchronize()
+        barrier()
+        dt = (time.perf_counter() - t0) / ek
+        e2e = {"value": world * byts / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": z * elem,
+               "d2h_bytes_per_step": n * elem, "steps": ek,
+               "note": "pinned host -> HBM copy of the z inputs, TFT+ITFT, HBM -> pinned copy of the n outputs"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads, model = cpu_info()
+        po.build()
+        hb = make_input(N, L, z, W, po.mix_seed(42, 5))
+        a, b = cpu_round_trip(N, L, z, n, hb, threads)
+        cpu = {"value": byts / (a + b) / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"one full {args.config} TFT+ITFT round trip ({a:.1f}+{b:.1f} s) with the "
+                         f"oracle port on {threads} threads, {model}"}
+        del hb
+
+    if rank == 0:
+        line = {
+            "metric": f"TFT+ITFT GB/s ({args.config}: {desc})",
+            "value": value,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic: seeded uniform 64-bit limbs (numpy PCG64, seed mix_seed(42,5+rank))",
+            "config": {"workload": args.config, "ring": f"Z/(2^{N}+1)", "L": L, "z": z, "n": n,
+                       "coeff_bytes": N // 8, "algorithmic_bytes_per_step": byts,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (3.3 GB at C5) far exceed the 126 MB L2; no flush needed"
+                       if args.config == "C5" else "see DESIGN.md"},
+            "roofline": {"bound": "hbm", "achieved": kernel_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": kernel_gbs / peak, "peak_kind": peak_kind,
+                         "traffic": load_traffic(args.config),
+                         "kernel": "leaf_kernel waves (all kernels of the step)",
+                         "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
