@@ -46,13 +46,12 @@ struct DevicePlan {
   const DevClass* classes = nullptr;
   const DevOp* ops = nullptr;
   const u32* levels = nullptr;
-  const SymExp* stores = nullptr;
+  const SymExp* rots = nullptr;
   const DevLeaf* leaves = nullptr;
-  struct W {
-    u64 offset, count;
-    unsigned max_ell;
-  };
-  std::vector<W> waves;
+  const DevCounter* cmeta = nullptr;
+  u64 nleaves = 0;
+  u32 ncounters = 0;
+  unsigned max_ell = 0;
   ~DevicePlan() {
     if (dbuf) cudaFree(dbuf);
   }
@@ -88,7 +87,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   std::vector<DevClass> cls;
   std::vector<DevOp> ops;
   std::vector<u32> levels;
-  std::vector<SymExp> stores;
+  std::vector<SymExp> rots;
   for (const auto& c : p.classes) {
     DevClass d{};
     d.L = 1u << c.key.ell;
@@ -96,30 +95,39 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.nstore = c.nstore;
     d.nlevels = (u32)c.level_begin.size() - 1;
     d.level_begin = (u32)levels.size();
-    d.store_begin = (u32)stores.size();
     u32 op0 = (u32)ops.size();
     for (u32 x : c.level_begin) levels.push_back(op0 + x);
     ops.insert(ops.end(), c.ops.begin(), c.ops.end());
-    stores.insert(stores.end(), c.store_rot.begin(), c.store_rot.end());
+    d.pre_begin = (u32)rots.size();
+    rots.insert(rots.end(), c.pre.begin(), c.pre.end());
+    d.post_begin = (u32)rots.size();
+    rots.insert(rots.end(), c.post.begin(), c.post.end());
+    d.has_pre = c.has_pre ? 1 : 0;
     cls.push_back(d);
   }
-  std::vector<DevLeaf> leaves;
-  for (const auto& w : p.waves) {
-    dp.waves.push_back({(u64)leaves.size(), (u64)w.leaves.size(), w.max_ell});
-    leaves.insert(leaves.end(), w.leaves.begin(), w.leaves.end());
-  }
+  if (rots.empty()) rots.push_back(SymExp{});
+  if (levels.empty()) levels.push_back(0);
+  if (ops.empty()) ops.push_back(DevOp{});
+  const auto& leaves = p.leaves;
+  dp.nleaves = leaves.size();
+  dp.ncounters = (u32)p.counters.size();
+  std::vector<DevCounter> cm = p.counters;
+  if (cm.empty()) cm.push_back(DevCounter{0, kNoDep});
+  dp.max_ell = p.max_ell;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t o_cls = 0, o_ops = al(o_cls + cls.size() * sizeof(DevClass));
   size_t o_lev = al(o_ops + ops.size() * sizeof(DevOp));
-  size_t o_st = al(o_lev + levels.size() * sizeof(u32));
-  size_t o_lf = al(o_st + stores.size() * sizeof(SymExp));
-  size_t total = al(o_lf + leaves.size() * sizeof(DevLeaf)) + 256;
+  size_t o_rot = al(o_lev + levels.size() * sizeof(u32));
+  size_t o_lf = al(o_rot + rots.size() * sizeof(SymExp));
+  size_t o_cm = al(o_lf + leaves.size() * sizeof(DevLeaf));
+  size_t total = al(o_cm + cm.size() * sizeof(DevCounter)) + 256;
   std::vector<std::uint8_t> h(total, 0);
   std::memcpy(h.data() + o_cls, cls.data(), cls.size() * sizeof(DevClass));
   std::memcpy(h.data() + o_ops, ops.data(), ops.size() * sizeof(DevOp));
   std::memcpy(h.data() + o_lev, levels.data(), levels.size() * sizeof(u32));
-  std::memcpy(h.data() + o_st, stores.data(), stores.size() * sizeof(SymExp));
+  std::memcpy(h.data() + o_rot, rots.data(), rots.size() * sizeof(SymExp));
   std::memcpy(h.data() + o_lf, leaves.data(), leaves.size() * sizeof(DevLeaf));
+  std::memcpy(h.data() + o_cm, cm.data(), cm.size() * sizeof(DevCounter));
   CUDA_TRY(cudaMalloc(&dp.dbuf, total));
   CUDA_TRY(cudaMemcpyAsync(dp.dbuf, h.data(), total, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // h is a temporary
@@ -127,8 +135,9 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.classes = reinterpret_cast<const DevClass*>(b + o_cls);
   dp.ops = reinterpret_cast<const DevOp*>(b + o_ops);
   dp.levels = reinterpret_cast<const u32*>(b + o_lev);
-  dp.stores = reinterpret_cast<const SymExp*>(b + o_st);
+  dp.rots = reinterpret_cast<const SymExp*>(b + o_rot);
   dp.leaves = reinterpret_cast<const DevLeaf*>(b + o_lf);
+  dp.cmeta = reinterpret_cast<const DevCounter*>(b + o_cm);
   (void)R;
   return CFTFT_OK;
 }
@@ -138,6 +147,7 @@ RingShape shape_of(const cftft_ring* R) {
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
   rs.M = R->M;
   rs.max_leaf_ell = R->max_leaf_ell;
+  rs.elem_bytes = R->elem_bytes;
   return rs;
 }
 
@@ -204,56 +214,78 @@ int set_smem(K kernel) {
   return CFTFT_OK;
 }
 
+template <class K>
+int grid_for(K kernel, int threads, size_t smem, u64 nleaves, unsigned* grid) {
+  int dev = 0, sms = 0, per = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem));
+  if (per < 1) return fail(CFTFT_CUDA_ERROR, "leaf kernel does not fit on an SM");
+  u64 g = (u64)sms * (u64)per;
+  if (g > nleaves) g = nleaves;
+  *grid = (unsigned)std::max<u64>(g, 1);
+  return CFTFT_OK;
+}
+
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
   u64 launches = 0;
-  if (R->kind == CFTFT_RING_FERMAT) {
-    if (int rc = set_smem(fermat::leaf_kernel)) return rc;
-    fermat::Args A{};
-    A.data = base;
-    A.elem_bytes = stride;
-    A.classes = dp.classes;
-    A.ops = dp.ops;
-    A.levels = dp.levels;
-    A.stores = dp.stores;
-    A.N = R->N;
-    A.M = R->M;
-    A.D = R->D;
-    A.C = R->C;
-    A.slot_bytes = R->slot_bytes;
-    for (const auto& w : dp.waves) {
-      if (!w.count) continue;
-      A.leaves = dp.leaves + w.offset;
-      size_t smem = (size_t)R->slot_bytes << w.max_ell;
-      fermat::leaf_kernel<<<(unsigned)w.count, fermat::kThreads, smem, st>>>(A);
-      ++launches;
+  if (dp.nleaves) {
+    u32* counters = nullptr;
+    const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
+    CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
+    CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
+    const size_t smem = (size_t)R->slot_bytes << dp.max_ell;
+    unsigned grid = 1;
+    if (R->kind == CFTFT_RING_FERMAT) {
+      if (int rc = set_smem(fermat::leaf_kernel)) return rc;
+      if (int rc = grid_for(fermat::leaf_kernel, fermat::kThreads, smem, dp.nleaves, &grid)) return rc;
+      fermat::Args A{};
+      A.data = base;
+      A.elem_bytes = stride;
+      A.leaves = dp.leaves;
+      A.nleaves = dp.nleaves;
+      A.classes = dp.classes;
+      A.ops = dp.ops;
+      A.levels = dp.levels;
+      A.rots = dp.rots;
+      A.counters = counters;
+      A.cmeta = dp.cmeta;
+      A.N = R->N;
+      A.M = R->M;
+      A.D = R->D;
+      A.C = R->C;
+      A.slot_bytes = R->slot_bytes;
+      fermat::leaf_kernel<<<grid, fermat::kThreads, smem, st>>>(A);
+    } else {
+      if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
+      if (int rc = grid_for(negacyclic::leaf_kernel, negacyclic::kThreads, smem, dp.nleaves, &grid))
+        return rc;
+      negacyclic::Args A{};
+      A.data = base;
+      A.elem_bytes = stride;
+      A.leaves = dp.leaves;
+      A.nleaves = dp.nleaves;
+      A.classes = dp.classes;
+      A.ops = dp.ops;
+      A.levels = dp.levels;
+      A.rots = dp.rots;
+      A.counters = counters;
+      A.cmeta = dp.cmeta;
+      A.K = R->K;
+      A.M = R->M;
+      A.m = R->m;
+      A.slot_bytes = R->slot_bytes;
+      negacyclic::leaf_kernel<<<grid, negacyclic::kThreads, smem, st>>>(A);
     }
-    if (canonicalize && dp.host.final_count) {
-      u64 cnt = dp.host.final_count;
-      fermat::canonicalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, stride, cnt,
-                                                                                  R->D);
-      ++launches;
-    }
-  } else {
-    if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
-    negacyclic::Args A{};
-    A.data = base;
-    A.elem_bytes = stride;
-    A.classes = dp.classes;
-    A.ops = dp.ops;
-    A.levels = dp.levels;
-    A.stores = dp.stores;
-    A.K = R->K;
-    A.M = R->M;
-    A.m = R->m;
-    A.slot_bytes = R->slot_bytes;
-    for (const auto& w : dp.waves) {
-      if (!w.count) continue;
-      A.leaves = dp.leaves + w.offset;
-      size_t smem = (size_t)R->slot_bytes << w.max_ell;
-      negacyclic::leaf_kernel<<<(unsigned)w.count, negacyclic::kThreads, smem, st>>>(A);
-      ++launches;
-    }
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(counters, st));
+  }
+  if (R->kind == CFTFT_RING_FERMAT && canonicalize && dp.host.final_count) {
+    const u64 cnt = dp.host.final_count;
+    fermat::canonicalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, stride, cnt, R->D);
+    ++launches;
   }
   g_last_launches = launches;
   CUDA_TRY(cudaGetLastError());
@@ -306,7 +338,16 @@ int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* 
 void json_plan(std::ostringstream& os, const Plan& p) {
   os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"L\":" << p.L << ",\"s\":" << p.s
      << ",\"z\":" << p.z << ",\"n\":" << p.n << ",\"f\":" << p.f << ",\"final_count\":"
-     << p.final_count << ",\"classes\":[";
+     << p.final_count << ",\"counters\":[";
+  for (size_t i = 0; i < p.counters.size(); ++i)
+    os << (i ? "," : "") << "[" << p.counters[i].target << ","
+       << (p.counters[i].next == kNoDep ? -1 : (long long)p.counters[i].next) << "]";
+  os << "],\"classes\":[";
+  auto sym = [&](const std::vector<SymExp>& v) {
+    os << "[";
+    for (size_t i = 0; i < v.size(); ++i) os << (i ? "," : "") << "[" << v[i].a << "," << v[i].b << "]";
+    os << "]";
+  };
   for (size_t c = 0; c < p.classes.size(); ++c) {
     const auto& k = p.classes[c];
     if (c) os << ",";
@@ -317,22 +358,20 @@ void json_plan(std::ostringstream& os, const Plan& p) {
     os << "],\"ops\":[";
     for (size_t i = 0; i < k.ops.size(); ++i) {
       const auto& o = k.ops[i];
-      os << (i ? "," : "") << "[" << (int)o.type << "," << o.a << "," << o.b << "," << o.ra << ","
-         << o.rb << "]";
+      os << (i ? "," : "") << "[" << (int)o.type << "," << o.a << "," << o.b << "," << o.r << "]";
     }
-    os << "],\"store\":[";
-    for (size_t i = 0; i < k.store_rot.size(); ++i)
-      os << (i ? "," : "") << "[" << k.store_rot[i].a << "," << k.store_rot[i].b << "]";
-    os << "]}";
+    os << "],\"pre\":";
+    sym(k.pre);
+    os << ",\"post\":";
+    sym(k.post);
+    os << "}";
   }
-  os << "],\"waves\":[";
-  for (size_t w = 0; w < p.waves.size(); ++w) {
-    os << (w ? "," : "") << "[";
-    const auto& lv = p.waves[w].leaves;
-    for (size_t i = 0; i < lv.size(); ++i)
-      os << (i ? "," : "") << "[" << lv[i].cls << "," << lv[i].base << "," << lv[i].stride << ","
-         << lv[i].s << "]";
-    os << "]";
+  os << "],\"leaves\":[";
+  for (size_t i = 0; i < p.leaves.size(); ++i) {
+    const auto& lf = p.leaves[i];
+    os << (i ? "," : "") << "[" << lf.cls << "," << lf.base << "," << lf.stride << "," << lf.s << ","
+       << (lf.dep == kNoDep ? -1 : (long long)lf.dep) << "," << lf.dep_target << ","
+       << (lf.comp == kNoDep ? -1 : (long long)lf.comp) << "," << p.leaf_wave[i] << "]";
   }
   os << "]}";
 }
@@ -451,12 +490,19 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
       lp.nload = 1;
       lp.nstore = 1;
       lp.level_begin = {0};
-      lp.store_rot = {SymExp{0, e & (M - 1)}};
+      lp.pre = {SymExp{}};
+      lp.post = {SymExp{0, e & (M - 1)}};
       np->host.classes.push_back(lp);
-      Wave w;
-      w.max_ell = 0;
-      for (u64 i = 0; i < count; ++i) w.leaves.push_back(DevLeaf{0, 0, i, 1, 0});
-      np->host.waves.push_back(std::move(w));
+      for (u64 i = 0; i < count; ++i) {
+        DevLeaf lf{};
+        lf.cls = 0;
+        lf.dep = kNoDep;
+        lf.comp = kNoDep;
+        lf.base = i;
+        lf.stride = 1;
+        np->host.leaves.push_back(lf);
+      }
+      np->host.max_ell = 0;
       np->host.final_count = count;
       if (int rc = upload(R, *np, st)) return rc;
       dp = np.get();

@@ -4,22 +4,29 @@
 // (transform.hpp:154-239).  On the GPU the recursion is cut at "leaves":
 // sub-transforms small enough that all their coefficients sit in one CTA's
 // shared memory.  The planner
-//   (1) replays the reference recursion above the leaves, with the
-//       reference's own split at the top level and an SMEM-sized split
-//       below it (outputs are unique, so any inner split gives the same
-//       bits: transform_test.cpp:248-272), producing WAVES of independent
-//       leaves (all columns of a node before its rows; ITFT phases i..iv);
-//   (2) replays the reference recursion INSIDE a leaf symbolically in the
-//       leaf weight s, turning every base case (transform.hpp:94-150) into a
-//       micro-op on SMEM slots.  Multiplications by powers of omega are never
-//       executed eagerly: each slot carries a pending exponent P (its true
-//       value is omega^P * stored), so a butterfly applies exactly one
-//       relative rotation to one operand, and the leaf's store applies the
-//       final P of each output slot;
+//   (1) replays the reference recursion above the leaves -- the reference's
+//       own split at the top level, an SMEM-sized near-balanced split below
+//       it (outputs are unique, so any inner split gives the same bits;
+//       transform_test.cpp:248-272) -- and records, for every leaf, the one
+//       (node, phase) completion counter it must wait for and the counters
+//       it completes: within a node all columns finish before any row starts
+//       (TFT), and the ITFT's phases i..iv run in order (transform.hpp:215-238);
+//   (2) replays the reference recursion INSIDE a leaf with zeta = 1, turning
+//       every base case (transform.hpp:94-150) into a micro-op on SMEM slots.
+//       Multiplications by powers of omega are never executed eagerly: each
+//       slot carries a pending exponent P (true value = omega^P * stored), so
+//       a butterfly applies one relative rotation to one operand.  The leaf
+//       weight zeta = omega^s enters only as a pre-rotation of the ITFT's
+//       spectral inputs (x_j <- zeta^-j' x_j) and a post-rotation of the
+//       outputs (TFT: zeta^j'; ITFT: the f-output), because
+//       TFT_zeta(a)[j] = zeta^j' TFT_1(a)[j] (transform.hpp:288-311).  Inside
+//       a leaf of length L' every relative rotation is then a multiple of
+//       M/L' bits, i.e. whole 128-bit chunks for all BASELINE shapes;
 //   (3) groups micro-ops into dependency levels (ops in a level touch
-//       disjoint slots and run concurrently).
-// Leaf programs depend only on (kind, ell, z, n, f), so they are shared by
-// all leaves of a class; per-leaf data is (class, base, stride, s).
+//       disjoint slots and run concurrently);
+//   (4) orders leaves into a ticket list for one persistent launch: batches
+//       of top-level sub-transforms small enough to stay L2 resident are run
+//       level by level, so intermediate levels hit L2 instead of HBM.
 #pragma once
 
 #include <algorithm>
@@ -35,7 +42,7 @@ namespace cftft_b200 {
 using u64 = std::uint64_t;
 using u32 = std::uint32_t;
 
-// Exponent a*s + b of omega, symbolic in the leaf weight s (all mod M).
+// Exponent a*s + b of omega, symbolic in a leaf weight s (all mod M).
 struct SymExp {
   u64 a = 0, b = 0;
   SymExp operator+(const SymExp& o) const { return {a + o.a, b + o.b}; }
@@ -47,19 +54,20 @@ enum OpType : std::uint8_t {
   OP_ADD = 1,       // a <- a + R(b)
   OP_SUB2 = 2,      // a <- 2a - R(b)
   OP_SUB2DIFF = 3,  // a <- 2a - R(b);           b <- a - R(b)
-  OP_COPY = 4,      // b <- a   (verbatim, pending exponent set by planner)
+  OP_COPY = 4,      // b <- a   (verbatim; the planner sets b's pending exponent)
   OP_DBL = 5,       // a <- 2a             (negacyclic only)
   OP_HALF = 6,      // a <- a/2            (negacyclic only)
   OP_ADDHALF = 7,   // a <- (a + R(b))/2   (negacyclic only)
 };
 
-// One micro-op; R = multiplication by omega^(ra*s + rb).  Device layout.
+// One micro-op; R = multiplication by omega^r (r concrete, reduced mod M).
 struct DevOp {
   std::uint8_t type;
   std::uint8_t pad0;
   std::uint16_t a, b;
   std::uint16_t pad1;
-  u64 ra, rb;
+  u64 r;
+  u64 pad2;
 };
 static_assert(sizeof(DevOp) == 24, "DevOp layout");
 
@@ -70,17 +78,33 @@ struct DevClass {
   u32 nstore;       // slots [0, nstore) are stored back
   u32 nlevels;
   u32 level_begin;  // index into level table (nlevels + 1 entries)
-  u32 store_begin;  // index into store-rotation table (nstore entries)
+  u32 pre_begin;    // index into rotation table: nload pre-rotations
+  u32 post_begin;   // index into rotation table: nstore post-rotations
+  u32 has_pre;      // any nonzero pre-rotation coefficient
+};
+
+constexpr u32 kNoDep = 0xFFFFFFFFu;
+
+// Completion tracking: one counter per (node, phase) of the decomposition.
+// A counter counts finished children (leaves or whole sub-nodes) of its
+// phase; when it reaches `target` and the phase is its node's last, the node
+// is finished and the counter `next` (the parent's phase) is bumped in turn.
+struct DevCounter {
+  u32 target;
+  u32 next;  // kNoDep: none
 };
 
 struct DevLeaf {
   u32 cls;
-  u32 pad;
-  u64 base;    // view index of slot 0
-  u64 stride;  // view-index distance between slots
-  u64 s;       // leaf weight (omega exponent), reduced mod M
+  u32 dep;         // counter to wait for (kNoDep: none)
+  u32 dep_target;  // ... until it reaches this value
+  u32 comp;        // counter to bump when done (kNoDep: none)
+  u64 base;        // view index of slot 0
+  u64 stride;      // view-index distance between slots
+  u64 s;           // leaf weight (omega exponent), reduced mod M
+  u64 pad;
 };
-static_assert(sizeof(DevLeaf) == 32, "DevLeaf layout");
+static_assert(sizeof(DevLeaf) == 48, "DevLeaf layout");
 
 struct ClassKey {
   int inverse;
@@ -96,13 +120,10 @@ struct LeafProgram {
   ClassKey key;
   std::vector<DevOp> ops;          // sorted by level
   std::vector<u32> level_begin;    // nlevels + 1 offsets into ops
-  std::vector<SymExp> store_rot;   // final pending exponent per stored slot
+  std::vector<SymExp> pre;         // per loaded slot (a*s + b)
+  std::vector<SymExp> post;        // per stored slot
   u32 nload = 0, nstore = 0;
-};
-
-struct Wave {
-  std::vector<DevLeaf> leaves;
-  unsigned max_ell = 0;  // largest leaf in the wave (sizes shared memory)
+  bool has_pre = false;
 };
 
 struct Plan {
@@ -110,7 +131,10 @@ struct Plan {
   u64 L = 0, s = 0, z = 0, n = 0;
   int f = 0, policy = 0;
   std::vector<LeafProgram> classes;
-  std::vector<Wave> waves;
+  std::vector<DevLeaf> leaves;  // ticket order (topological)
+  std::vector<u32> leaf_wave;   // merged wave index of each leaf (debug / waves view)
+  std::vector<DevCounter> counters;
+  unsigned max_ell = 0;
   u64 final_count = 0;  // outputs [0, final_count) are canonicalised at the end
 };
 
@@ -119,7 +143,18 @@ struct RingShape {
   bool fermat = true;  // false: negacyclic
   u64 M = 0;           // root order
   unsigned max_leaf_ell = 3;
+  u64 elem_bytes = 0;          // bytes per coefficient (for L2 batching)
+  u64 l2_budget = 48ull << 20;  // bytes of L2 a batch may occupy
 };
+
+inline u64 bitrev(u64 j, unsigned ell) {
+  u64 r = 0;
+  for (unsigned i = 0; i < ell; ++i) {
+    r = (r << 1) | (j & 1);
+    j >>= 1;
+  }
+  return r;
+}
 
 // ---------------------------------------------------------------------------
 class Planner {
@@ -137,10 +172,28 @@ class Planner {
     p.policy = policy;
     class_index_.clear();
     classes_.clear();
-    std::vector<Wave> waves;
-    node(inverse, L, s, z, n, f, 0, 1, policy, true, waves);
-    p.waves = std::move(waves);
+    leaves_.clear();
+    keys_.clear();
+    counters_.clear();
+    max_ell_ = 0;
+    Ctx root;
+    root.dep = kNoDep;
+    root.dep_target = 0;
+    root.report = kNoDep;
+    node(inverse, L, s, z, n, f, 0, 1, policy, /*depth=*/0, root, /*wave0=*/0);
+    // ticket order: (top phase, batch, wave, top child, emission order)
+    std::vector<u32> idx(leaves_.size());
+    for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return keys_[x] < keys_[y]; });
+    p.leaves.reserve(idx.size());
+    p.leaf_wave.reserve(idx.size());
+    for (u32 i : idx) {
+      p.leaves.push_back(leaves_[i]);
+      p.leaf_wave.push_back(std::get<2>(keys_[i]));
+    }
     p.classes = std::move(classes_);
+    p.counters = std::move(counters_);
+    p.max_ell = max_ell_;
     p.final_count = inverse ? n + (u64)f : n;
     return p;
   }
@@ -162,103 +215,135 @@ class Planner {
       return;
     }
     unsigned lam = rs_.max_leaf_ell;
-    unsigned k = (ell + lam - 1) / lam;  // waves needed
+    unsigned k = (ell + lam - 1) / lam;  // levels needed
     l1 = (ell + k - 1) / k;
     if (l1 >= ell) l1 = ell - 1;
     if (l1 < 1) l1 = 1;
     l2 = ell - l1;
   }
 
-  static void merge_into(std::vector<Wave>& acc, std::vector<Wave>&& w) {
-    if (acc.size() < w.size()) acc.resize(w.size());
-    for (size_t i = 0; i < w.size(); ++i) {
-      auto& dst = acc[i].leaves;
-      dst.insert(dst.end(), w[i].leaves.begin(), w[i].leaves.end());
-      acc[i].max_ell = std::max(acc[i].max_ell, w[i].max_ell);
-    }
+  unsigned levels_of(unsigned ell) const {
+    unsigned lam = rs_.max_leaf_ell;
+    return ell <= lam ? 1 : (ell + lam - 1) / lam;
   }
 
-  static void append(std::vector<Wave>& out, std::vector<Wave>&& w) {
-    for (auto& x : w) out.push_back(std::move(x));
-  }
+  struct Ctx {
+    u32 dep = kNoDep, dep_target = 0;
+    u32 report = kNoDep;  // counter of the parent phase this subtree reports to
+    // top-level bookkeeping for ticket ordering
+    u32 top_phase = 0;
+    u64 top_batch = 0, top_child = 0;
+  };
 
-  // One node of the GPU decomposition.  base/stride are in view elements.
-  void node(bool inv, u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride, int policy,
-            bool top, std::vector<Wave>& out) {
+  using Key = std::tuple<u32, u64, u32, u64, u64>;  // phase, batch, wave, child, seq
+
+  // One node of the GPU decomposition (base/stride in view elements).
+  // Returns the number of leaves emitted and the number of waves (levels).
+  std::pair<u64, u32> node(bool inv, u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride,
+                           int policy, int depth, const Ctx& cx, u32 wave0) {
     const u64 M = rs_.M;
     s &= (M - 1);
     unsigned ell = ctz(L);
-    // A leaf when it fits on chip.  At the top level a transform that fits is
-    // still a single leaf (the leaf program replays the policy's recursion).
     if (ell <= rs_.max_leaf_ell) {
-      Wave w;
-      w.max_ell = ell;
       DevLeaf lf{};
       lf.cls = class_of(ClassKey{inv ? 1 : 0, ell, z, n, f}, policy);
+      lf.dep = cx.dep;
+      lf.dep_target = cx.dep_target;
+      lf.comp = cx.report;
       lf.base = base;
       lf.stride = stride;
       lf.s = s;
-      w.leaves.push_back(lf);
-      out.push_back(std::move(w));
-      return;
+      leaves_.push_back(lf);
+      keys_.push_back(Key{cx.top_phase, cx.top_batch, wave0, cx.top_child, (u64)keys_.size()});
+      max_ell_ = std::max(max_ell_, ell);
+      return {1, 1};
     }
     unsigned l1, l2;
-    split(ell, policy, top, l1, l2);
+    split(ell, policy, depth == 0, l1, l2);
     const u64 cols = u64{1} << l2, rows = u64{1} << l1;
     const u64 col_step = M >> ell;
     const u64 s_row = s << l1;
+
+    // a phase = list of child sub-transforms
+    struct Child {
+      u64 L, s, z, n;
+      int f;
+      u64 base, stride;
+    };
+    std::vector<std::vector<Child>> phases;
     if (!inv) {  // transform.hpp:154-186
       const u64 n2 = n & (cols - 1), n1 = n >> l2, n1c = n1 + (n2 ? 1 : 0);
       const u64 z2 = z & (cols - 1), z1 = z >> l2, z2e = z1 ? cols : z2;
-      std::vector<Wave> colw, roww;
-      for (u64 u = 0; u < z2e; ++u) {
-        std::vector<Wave> w;
-        node(false, rows, s + u * col_step, u < z2 ? z1 + 1 : z1, n1c, 0, base + u * stride,
-             stride * cols, policy, false, w);
-        merge_into(colw, std::move(w));
+      std::vector<Child> c, r;
+      for (u64 u = 0; u < z2e; ++u)
+        c.push_back({rows, s + u * col_step, u < z2 ? z1 + 1 : z1, n1c, 0, base + u * stride,
+                     stride * cols});
+      for (u64 u = 0; u < n1c; ++u)
+        r.push_back({cols, s_row, z2e, u < n1 ? cols : n2, 0, base + u * cols * stride, stride});
+      phases.push_back(std::move(c));
+      phases.push_back(std::move(r));
+    } else {  // transform.hpp:188-239
+      const u64 n2 = n & (cols - 1), n1 = n >> l2, z2 = z & (cols - 1), z1 = z >> l2;
+      const int fm = (n2 + (u64)f > 0) ? 1 : 0;
+      const u64 z2e = z1 ? cols : z2;
+      const u64 lo = std::min(n2, z2), hi = std::max(n2, z2);
+      std::vector<Child> p1, p2, p3, p4;
+      for (u64 u = 0; u < n1; ++u) p1.push_back({cols, s_row, cols, cols, 0, base + u * cols * stride, stride});
+      for (u64 u = n2; u < z2e; ++u)
+        p2.push_back({rows, s + u * col_step, u < hi ? z1 + 1 : z1, n1, fm, base + u * stride, stride * cols});
+      if (fm) p3.push_back({cols, s_row, z2e, n2, f, base + n1 * cols * stride, stride});
+      for (u64 u = 0; u < n2; ++u)
+        p4.push_back({rows, s + u * col_step, u < lo ? z1 + 1 : z1, n1 + 1, 0, base + u * stride, stride * cols});
+      for (auto* ph : {&p1, &p2, &p3, &p4})
+        if (!ph->empty()) phases.push_back(std::move(*ph));
+    }
+
+    u64 total = 0;
+    u32 wave = wave0;
+    u32 prev_counter = kNoDep;
+    u32 prev_target = 0;
+    u32 phase_index = 0;
+    for (auto& ph : phases) {
+      const u32 cid = (u32)counters_.size();
+      counters_.push_back(DevCounter{(u32)ph.size(), kNoDep});
+      Ctx c2;
+      if (phase_index == 0) {
+        c2.dep = cx.dep;
+        c2.dep_target = cx.dep_target;
+      } else {
+        c2.dep = prev_counter;
+        c2.dep_target = prev_target;
       }
-      for (u64 u = 0; u < n1c; ++u) {
-        std::vector<Wave> w;
-        node(false, cols, s_row, z2e, u < n1 ? cols : n2, 0, base + u * cols * stride, stride,
-             policy, false, w);
-        merge_into(roww, std::move(w));
+      c2.report = cid;
+      u32 maxw = 0;
+      // L2 batching of top-level children
+      u64 child_bytes = (u64{1} << ctz(ph.front().L)) * rs_.elem_bytes;
+      u64 batch = std::max<u64>(1, rs_.l2_budget / std::max<u64>(1, child_bytes));
+      for (u64 ci = 0; ci < ph.size(); ++ci) {
+        const Child& ch = ph[ci];
+        if (depth == 0) {
+          c2.top_phase = phase_index;
+          c2.top_batch = ci / batch;
+          c2.top_child = ci;
+        } else {
+          c2.top_phase = cx.top_phase;
+          c2.top_batch = cx.top_batch;
+          c2.top_child = cx.top_child;
+        }
+        u32 w0 = depth == 0 ? 0 : wave;
+        auto [k, w] = node(inv, ch.L, ch.s, ch.z, ch.n, ch.f, ch.base, ch.stride, policy, depth + 1,
+                           c2, w0);
+        total += k;
+        maxw = std::max(maxw, w);
       }
-      append(out, std::move(colw));
-      append(out, std::move(roww));
-      return;
+      prev_counter = cid;
+      prev_target = (u32)ph.size();
+      wave += maxw;
+      ++phase_index;
     }
-    // transform.hpp:188-239
-    const u64 n2 = n & (cols - 1), n1 = n >> l2, z2 = z & (cols - 1), z1 = z >> l2;
-    const int fm = (n2 + (u64)f > 0) ? 1 : 0;
-    const u64 z2e = z1 ? cols : z2;
-    const u64 lo = std::min(n2, z2), hi = std::max(n2, z2);
-    std::vector<Wave> ph1, ph2, ph3, ph4;
-    for (u64 u = 0; u < n1; ++u) {
-      std::vector<Wave> w;
-      node(true, cols, s_row, cols, cols, 0, base + u * cols * stride, stride, policy, false, w);
-      merge_into(ph1, std::move(w));
-    }
-    for (u64 u = n2; u < z2e; ++u) {
-      std::vector<Wave> w;
-      node(true, rows, s + u * col_step, u < hi ? z1 + 1 : z1, n1, fm, base + u * stride,
-           stride * cols, policy, false, w);
-      merge_into(ph2, std::move(w));
-    }
-    if (fm) {
-      std::vector<Wave> w;
-      node(true, cols, s_row, z2e, n2, f, base + n1 * cols * stride, stride, policy, false, w);
-      merge_into(ph3, std::move(w));
-    }
-    for (u64 u = 0; u < n2; ++u) {
-      std::vector<Wave> w;
-      node(true, rows, s + u * col_step, u < lo ? z1 + 1 : z1, n1 + 1, 0, base + u * stride,
-           stride * cols, policy, false, w);
-      merge_into(ph4, std::move(w));
-    }
-    append(out, std::move(ph1));
-    append(out, std::move(ph2));
-    append(out, std::move(ph3));
-    append(out, std::move(ph4));
+    // the node is finished when its last phase is: report to the parent phase
+    counters_[prev_counter].next = cx.report;
+    return {total, wave - wave0};
   }
 
   // ---- leaf programs -------------------------------------------------------
@@ -278,9 +363,10 @@ class Planner {
       u32 level;
     };
     std::vector<Raw> ops;
-    std::vector<u32> last;     // last level touching each slot
-    std::vector<SymExp> P;     // pending exponent per slot
-    void push(std::uint8_t type, u32 a, u32 b, SymExp r, bool two_slots) {
+    std::vector<u32> last;  // last level touching each slot
+    std::vector<u64> P;     // pending exponent per slot (concrete, zeta = 1)
+    u64 M = 0;
+    void push(std::uint8_t type, u32 a, u32 b, u64 r, bool two_slots) {
       u32 lv = last[a];
       if (two_slots) lv = std::max(lv, last[b]);
       lv += 1;
@@ -290,14 +376,12 @@ class Planner {
       op.type = type;
       op.a = (std::uint16_t)a;
       op.b = (std::uint16_t)b;
-      op.ra = r.a;
-      op.rb = r.b;
+      op.r = r & (M - 1);
       ops.push_back({op, lv});
     }
   };
 
-  // Symbolic twiddles: the leaf is called with s = 1*s + 0.
-  void leaf_tft(Emit& e, u64 L, SymExp s, u64 z, u64 n, u64 base, u64 stride, int policy) {
+  void leaf_tft(Emit& e, u64 L, u64 s, u64 z, u64 n, u64 base, u64 stride, int policy) {
     if (L == 2) {
       u32 i = (u32)base, j = (u32)(base + stride);
       if (n == 2) {
@@ -305,7 +389,7 @@ class Planner {
           e.push(OP_ADDSUB, i, j, e.P[j] - e.P[i], true);
           e.P[j] = e.P[i] + s;
         } else {  // x1 = zeta x0
-          e.push(OP_COPY, i, j, SymExp{}, true);
+          e.push(OP_COPY, i, j, 0, true);
           e.P[j] = e.P[i] + s;
         }
       } else if (z == 2) {  // x0 = x0 + x1
@@ -320,19 +404,15 @@ class Planner {
     const u64 z2 = z & (cols - 1), z1 = z >> l2, z2e = z1 ? cols : z2;
     const u64 col_step = rs_.M >> ell;
     for (u64 u = 0; u < z2; ++u)
-      leaf_tft(e, rows, s + SymExp{0, u * col_step}, z1 + 1, n1c, base + u * stride,
-               stride * cols, policy);
+      leaf_tft(e, rows, s + u * col_step, z1 + 1, n1c, base + u * stride, stride * cols, policy);
     for (u64 u = z2; u < z2e; ++u)
-      leaf_tft(e, rows, s + SymExp{0, u * col_step}, z1, n1c, base + u * stride, stride * cols,
-               policy);
-    const SymExp s_row{s.a << l1, s.b << l1};
-    for (u64 u = 0; u < n1; ++u)
-      leaf_tft(e, cols, s_row, z2e, cols, base + u * cols * stride, stride, policy);
+      leaf_tft(e, rows, s + u * col_step, z1, n1c, base + u * stride, stride * cols, policy);
+    const u64 s_row = s << l1;
+    for (u64 u = 0; u < n1; ++u) leaf_tft(e, cols, s_row, z2e, cols, base + u * cols * stride, stride, policy);
     if (n2 > 0) leaf_tft(e, cols, s_row, z2e, n2, base + n1 * cols * stride, stride, policy);
   }
 
-  void leaf_itft(Emit& e, u64 L, SymExp s, u64 z, u64 n, int f, u64 base, u64 stride,
-                 int policy) {
+  void leaf_itft(Emit& e, u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride, int policy) {
     const bool fermat = rs_.fermat;
     if (L == 2) {
       u32 i = (u32)base, j = (u32)(base + stride);
@@ -345,36 +425,36 @@ class Planner {
             e.push(OP_SUB2DIFF, i, j, e.P[j] - e.P[i], true);
             e.P[j] = e.P[i] + s;
           } else {  // (2x0, zeta x0)
-            e.push(OP_COPY, i, j, SymExp{}, true);
+            e.push(OP_COPY, i, j, 0, true);
             e.P[j] = e.P[i] + s;
             if (fermat)
-              e.P[i] = e.P[i] + SymExp{0, 1};
+              e.P[i] = e.P[i] + 1;
             else
-              e.push(OP_DBL, i, i, SymExp{}, false);
+              e.push(OP_DBL, i, i, 0, false);
           }
         } else {
           if (z == 2) {  // 2x0 - x1
             e.push(OP_SUB2, i, j, e.P[j] - e.P[i], true);
           } else {  // 2x0
             if (fermat)
-              e.P[i] = e.P[i] + SymExp{0, 1};
+              e.P[i] = e.P[i] + 1;
             else
-              e.push(OP_DBL, i, i, SymExp{}, false);
+              e.push(OP_DBL, i, i, 0, false);
           }
         }
       } else {  // n == 0: half(x0 + x1) or half(x0)
         if (z == 2) {
           if (fermat) {
             e.push(OP_ADD, i, j, e.P[j] - e.P[i], true);
-            e.P[i] = e.P[i] + SymExp{0, rs_.M - 1};
+            e.P[i] = e.P[i] + (rs_.M - 1);
           } else {
             e.push(OP_ADDHALF, i, j, e.P[j] - e.P[i], true);
           }
         } else {
           if (fermat)
-            e.P[i] = e.P[i] + SymExp{0, rs_.M - 1};
+            e.P[i] = e.P[i] + (rs_.M - 1);
           else
-            e.push(OP_HALF, i, i, SymExp{}, false);
+            e.push(OP_HALF, i, i, 0, false);
         }
       }
       return;
@@ -387,22 +467,17 @@ class Planner {
     const u64 z2e = z1 ? cols : z2;
     const u64 lo = std::min(n2, z2), hi = std::max(n2, z2);
     const u64 col_step = rs_.M >> ell;
-    const SymExp s_row{s.a << l1, s.b << l1};
-    for (u64 u = 0; u < n1; ++u)
-      leaf_itft(e, cols, s_row, cols, cols, 0, base + u * cols * stride, stride, policy);
+    const u64 s_row = s << l1;
+    for (u64 u = 0; u < n1; ++u) leaf_itft(e, cols, s_row, cols, cols, 0, base + u * cols * stride, stride, policy);
     for (u64 u = n2; u < hi; ++u)
-      leaf_itft(e, rows, s + SymExp{0, u * col_step}, z1 + 1, n1, fm, base + u * stride,
-                stride * cols, policy);
+      leaf_itft(e, rows, s + u * col_step, z1 + 1, n1, fm, base + u * stride, stride * cols, policy);
     for (u64 u = hi; u < z2e; ++u)
-      leaf_itft(e, rows, s + SymExp{0, u * col_step}, z1, n1, fm, base + u * stride,
-                stride * cols, policy);
+      leaf_itft(e, rows, s + u * col_step, z1, n1, fm, base + u * stride, stride * cols, policy);
     if (fm) leaf_itft(e, cols, s_row, z2e, n2, f, base + n1 * cols * stride, stride, policy);
     for (u64 u = 0; u < lo; ++u)
-      leaf_itft(e, rows, s + SymExp{0, u * col_step}, z1 + 1, n1 + 1, 0, base + u * stride,
-                stride * cols, policy);
+      leaf_itft(e, rows, s + u * col_step, z1 + 1, n1 + 1, 0, base + u * stride, stride * cols, policy);
     for (u64 u = lo; u < n2; ++u)
-      leaf_itft(e, rows, s + SymExp{0, u * col_step}, z1, n1 + 1, 0, base + u * stride,
-                stride * cols, policy);
+      leaf_itft(e, rows, s + u * col_step, z1, n1 + 1, 0, base + u * stride, stride * cols, policy);
   }
 
   static void split_ref(unsigned ell, int policy, unsigned& l1, unsigned& l2) {
@@ -418,12 +493,14 @@ class Planner {
   LeafProgram build_leaf(const ClassKey& k, int policy) {
     const u64 L = u64{1} << k.ell;
     Emit e;
+    e.M = rs_.M;
     e.last.assign(L, 0);
-    e.P.assign(L, SymExp{});
+    e.P.assign(L, 0);
+    // zeta = 1 inside the leaf; the weight is applied by pre/post rotations
     if (k.inverse)
-      leaf_itft(e, L, SymExp{1, 0}, k.z, k.n, k.f, 0, 1, policy);
+      leaf_itft(e, L, 0, k.z, k.n, k.f, 0, 1, policy);
     else
-      leaf_tft(e, L, SymExp{1, 0}, k.z, k.n, 0, 1, policy);
+      leaf_tft(e, L, 0, k.z, k.n, 0, 1, policy);
     LeafProgram prog;
     prog.key = k;
     prog.nload = (u32)k.z;
@@ -432,32 +509,41 @@ class Planner {
     for (auto& r : e.ops) nlev = std::max(nlev, r.level);
     std::stable_sort(e.ops.begin(), e.ops.end(),
                      [](const Emit::Raw& x, const Emit::Raw& y) { return x.level < y.level; });
-    prog.level_begin.assign(nlev + 1, 0);
     prog.ops.reserve(e.ops.size());
-    u32 cur = 1;
-    for (size_t i = 0; i < e.ops.size(); ++i) {
-      while (cur < e.ops[i].level) prog.level_begin[cur++] = (u32)i;
-      prog.ops.push_back(e.ops[i].op);
-    }
-    while (cur <= nlev) prog.level_begin[cur++] = (u32)e.ops.size();
-    prog.level_begin[0] = 0;
-    // level_begin[l] = first op of level l+1; entry nlev = total
-    std::vector<u32> lb(nlev + 1);
-    // recompute cleanly: lb[i] = first op index with level > i
+    for (auto& r : e.ops) prog.ops.push_back(r.op);
+    // level l (1-based) spans [level_begin[l-1], level_begin[l])
+    prog.level_begin.assign(nlev + 1, 0);
     size_t idx = 0;
     for (u32 l = 0; l <= nlev; ++l) {
       while (idx < e.ops.size() && e.ops[idx].level <= l) ++idx;
-      lb[l] = (u32)idx;
+      prog.level_begin[l] = (u32)idx;
     }
-    // lb[0] = 0 (no op has level 0); level l (1-based) spans [lb[l-1], lb[l])
-    prog.level_begin = std::move(lb);
-    prog.store_rot.assign(e.P.begin(), e.P.begin() + prog.nstore);
+    const u64 M = rs_.M;
+    prog.pre.assign(prog.nload, SymExp{});
+    prog.post.assign(prog.nstore, SymExp{});
+    for (u32 j = 0; j < prog.nstore; ++j) prog.post[j].b = e.P[j] & (M - 1);
+    if (!k.inverse) {
+      // TFT_zeta(a)[j] = zeta^{j'} TFT_1(a)[j]
+      for (u32 j = 0; j < prog.nstore; ++j) prog.post[j].a = bitrev(j, k.ell);
+    } else {
+      // spectral inputs x_j (j < n) are pre-rotated by zeta^{-j'}; the
+      // f-output is a spectral value: post-rotated by zeta^{n'}
+      for (u32 j = 0; j < prog.nload && j < k.n; ++j) {
+        prog.pre[j].a = (u64)0 - bitrev(j, k.ell);
+        if (bitrev(j, k.ell)) prog.has_pre = true;
+      }
+      if (k.f) prog.post[k.n].a = bitrev(k.n, k.ell);
+    }
     return prog;
   }
 
   RingShape rs_;
   std::map<ClassKey, u32> class_index_;
   std::vector<LeafProgram> classes_;
+  std::vector<DevLeaf> leaves_;
+  std::vector<Key> keys_;
+  std::vector<DevCounter> counters_;
+  unsigned max_ell_ = 0;
 };
 
 // ---------------------------------------------------------------------------

@@ -111,33 +111,45 @@ def test_counts_respect_bounds():  # verify.hpp:507-553
 # ---- value-level execution of the GPU schedule ----------------------------------
 
 def run_plan_fermat(plan, N, vals):
+    """Executes the ticket list at the value level, checking that every leaf's
+    dependency counter is complete when its ticket comes up."""
     P, M = (1 << N) + 1, 2 * N
     x = dict(vals)
-    for wave in plan["waves"]:
-        for (cls, base, stride, s) in wave:
-            c = plan["classes"][cls]
-            slot = [None] * (1 << c["ell"])
-            for i in range(c["nload"]):
-                slot[i] = x[base + i * stride]
-            for (t, a, b, ra, rb) in c["ops"]:
-                r = (ra * s + rb) % M
-                if t == 4:
-                    slot[b] = slot[a]
-                    continue
-                A, B = slot[a], (slot[b] * pow(2, r, P)) % P
-                if t == 0:
-                    slot[a], slot[b] = (A + B) % P, (A - B) % P
-                elif t == 1:
-                    slot[a] = (A + B) % P
-                elif t == 2:
-                    slot[a] = (2 * A - B) % P
-                elif t == 3:
-                    slot[a], slot[b] = (2 * A - B) % P, (A - B) % P
-                else:
-                    raise AssertionError("negacyclic-only op in a Fermat plan")
-            for i in range(c["nstore"]):
-                ea, eb = c["store"][i]
-                x[base + i * stride] = (slot[i] * pow(2, (ea * s + eb) % M, P)) % P
+    meta = plan["counters"]
+    counters = [0] * len(meta)
+    for (cls, base, stride, s, dep, target, comp, wave) in plan["leaves"]:
+        if dep >= 0:
+            assert counters[dep] >= target, "ticket order is not topological"
+        c = plan["classes"][cls]
+        slot = [None] * (1 << c["ell"])
+        for i in range(c["nload"]):
+            a, b = c["pre"][i]
+            slot[i] = (x[base + i * stride] * pow(2, (a * s + b) % M, P)) % P
+        for (t, a, b, r) in c["ops"]:
+            if t == 4:
+                slot[b] = slot[a]
+                continue
+            A, B = slot[a], (slot[b] * pow(2, r, P)) % P
+            if t == 0:
+                slot[a], slot[b] = (A + B) % P, (A - B) % P
+            elif t == 1:
+                slot[a] = (A + B) % P
+            elif t == 2:
+                slot[a] = (2 * A - B) % P
+            elif t == 3:
+                slot[a], slot[b] = (2 * A - B) % P, (A - B) % P
+            else:
+                raise AssertionError("negacyclic-only op in a Fermat plan")
+        for i in range(c["nstore"]):
+            ea, eb = c["post"][i]
+            x[base + i * stride] = (slot[i] * pow(2, (ea * s + eb) % M, P)) % P
+        k = comp
+        while k >= 0:  # leaf -> phase counter -> (node finished) -> parent phase ...
+            counters[k] += 1
+            tgt, nxt = meta[k]
+            if counters[k] != tgt:
+                break
+            k = nxt
     return x
 
 
@@ -174,13 +186,20 @@ def test_gpu_schedule_reproduces_definition(limit):
 
 
 def test_schedule_shape_config5():
-    """C5 (L=2^18, z=n=200000): top split 512x512, SMEM leaves of 8 -> 3 waves
-    per pass; only columns < z2' and rows < n1' are scheduled."""
+    """C5 (L=2^18, z=n=200000): top split 512x512, SMEM leaves of 8 -> three
+    levels per top-level pass; only columns < z2' and rows < n1' are scheduled;
+    the ticket list is L2-batched (whole columns, level by level)."""
     ctx = cf.FermatRingCtx(131072)
     assert ctx.set_leaf_limit(0) == 3
     plan = cf.plan_dump(ctx, False, cf.TransformParams(1 << 18, 0, 200000, 200000))
-    assert len(plan["waves"]) == 6
-    # every column leaf of the first wave has stride 512*64 (top column stride x inner rows)
-    leaves0 = plan["waves"][0]
-    assert len(leaves0) == 512 * 64
-    assert all(lf[2] == 512 * 64 for lf in leaves0)
+    leaves = plan["leaves"]
+    # columns: 64 inner columns + 6 full row-64 nodes (16 leaves) + a partial
+    # one (9); rows: 390 full rows (192 leaves) + the partial row n2=320 (144)
+    assert len(leaves) == 512 * (64 + 6 * 16 + 9) + 390 * 192 + 144
+    assert max(lf[7] for lf in leaves) == 2  # waves 0..2 within each top-level child
+    assert sum(1 for lf in leaves if lf[4] < 0) == 512 * 64  # only the first level is free
+    first = leaves[:64]
+    assert all(lf[7] == 0 and lf[2] == 512 * 64 for lf in first)
+    # within the first batch, level-1 leaves precede level-2 leaves
+    waves = [lf[7] for lf in leaves[: 3 * 64 * 6]]
+    assert waves == sorted(waves)
