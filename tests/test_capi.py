@@ -201,5 +201,7 @@ def test_schedule_shape_config5():
     first = leaves[:64]
     assert all(lf[7] == 0 and lf[2] == 512 * 64 for lf in first)
     # within the first batch, level-1 leaves precede level-2 leaves
-    waves = [lf[7] for lf in leaves[: 3 * 64 * 6]]
-    assert waves == sorted(waves)
+    per_col = 64 + 6 * 16 + 9
+    waves = [lf[7] for lf in leaves[: 5 * per_col]]  # first L2 batch: 5 columns (48 MiB budget)
+    assert waves == sorted(waves) and waves[0] == 0 and waves[-1] == 2
+    assert leaves[5 * per_col][7] == 0  # the next batch restarts at level 1
