@@ -255,6 +255,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.M = R->M;
       A.D = R->D;
       A.C = R->C;
+      A.logC = (u32)__builtin_ctz(R->C);
       A.slot_bytes = R->slot_bytes;
       fermat::leaf_kernel<<<grid, fermat::kThreads, smem, st>>>(A);
     } else {

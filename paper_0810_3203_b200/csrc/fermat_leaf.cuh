@@ -33,8 +33,6 @@ namespace fermat {
 constexpr int kThreads = 512;
 constexpr int kTasksPerThread = 4;
 
-typedef unsigned __int128 u128;
-
 struct Args {
   std::uint8_t* data;      // view element 0
   u64 elem_bytes;          // bytes between consecutive view elements
@@ -49,6 +47,7 @@ struct Args {
   u64 N, M;
   u32 D, C;                // u32 words, 128-bit chunks per element
   u32 slot_bytes;          // 4*D + pending bytes (16B aligned)
+  u32 logC;
 };
 
 __device__ __forceinline__ uint4* slot_chunks(std::uint8_t* sm, const Args& A, u32 s) {
@@ -58,43 +57,67 @@ __device__ __forceinline__ signed char* slot_pend(std::uint8_t* sm, const Args& 
   return reinterpret_cast<signed char*>(sm + (size_t)s * A.slot_bytes + 4u * A.D);
 }
 
-__device__ __forceinline__ u128 to128(uint4 v) {
-  return ((u128)v.w << 96) | ((u128)v.z << 64) | ((u128)v.y << 32) | (u128)v.x;
-}
-__device__ __forceinline__ uint4 from128(u128 x) {
-  return make_uint4((u32)x, (u32)(x >> 32), (u32)(x >> 64), (u32)(x >> 96));
-}
+// ---- 128-bit chunk arithmetic on u32 words with PTX carry chains -------------
 
-// value = lo + hi * 2^128
-struct Val {
-  u128 lo;
-  int hi;
+struct Ch {
+  u32 w[4];
 };
-__device__ __forceinline__ Val vadd(Val a, Val b) {
-  Val r;
-  r.lo = a.lo + b.lo;
-  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
-  return r;
+__device__ __forceinline__ Ch ld_ch(const uint4* p) {
+  const uint4 v = *p;
+  return Ch{{v.x, v.y, v.z, v.w}};
 }
-__device__ __forceinline__ Val vsub(Val a, Val b) {
-  Val r;
-  r.lo = a.lo - b.lo;
-  r.hi = a.hi - b.hi - (a.lo < b.lo ? 1 : 0);
-  return r;
+__device__ __forceinline__ void st_ch(uint4* p, const Ch& c) { *p = make_uint4(c.w[0], c.w[1], c.w[2], c.w[3]); }
+
+// r = a + b; returns the carry out (0/1)
+__device__ __forceinline__ int ch_add(Ch& r, const Ch& a, const Ch& b) {
+  u32 c;
+  asm("add.cc.u32 %0, %5, %9;\n\t"
+      "addc.cc.u32 %1, %6, %10;\n\t"
+      "addc.cc.u32 %2, %7, %11;\n\t"
+      "addc.cc.u32 %3, %8, %12;\n\t"
+      "addc.u32 %4, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]),
+        "r"(b.w[3]));
+  return (int)c;
 }
-__device__ __forceinline__ Val vneg(Val a) {
-  Val r;
-  r.lo = (u128)0 - a.lo;
-  r.hi = -a.hi - (a.lo != 0 ? 1 : 0);
-  return r;
+// r = a - b; returns the borrow as -1/0
+__device__ __forceinline__ int ch_sub(Ch& r, const Ch& a, const Ch& b) {
+  u32 c;
+  asm("sub.cc.u32 %0, %5, %9;\n\t"
+      "subc.cc.u32 %1, %6, %10;\n\t"
+      "subc.cc.u32 %2, %7, %11;\n\t"
+      "subc.cc.u32 %3, %8, %12;\n\t"
+      "subc.u32 %4, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]),
+        "r"(b.w[3]));
+  return (int)c;
 }
-// small signed p times 2^o, 0 <= o < 128
-__device__ __forceinline__ Val vsmall(int p, u32 o) {
-  Val r;
-  __int128 sp = (__int128)p;
-  r.lo = (u128)sp << o;
-  r.hi = o ? (int)(sp >> (128 - o)) : (p < 0 ? -1 : 0);
-  return r;
+// r += k (k small signed, sign-extended); returns the signed carry (-1/0/1)
+__device__ __forceinline__ int ch_add_small(Ch& r, int k) {
+  const u32 e = (u32)(k >> 31);
+  u32 c;
+  asm("add.cc.u32 %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, %6;\n\t"
+      "addc.cc.u32 %2, %2, %6;\n\t"
+      "addc.cc.u32 %3, %3, %6;\n\t"
+      "addc.u32 %4, %6, 0;"
+      : "+r"(r.w[0]), "+r"(r.w[1]), "+r"(r.w[2]), "+r"(r.w[3]), "=r"(c)
+      : "r"((u32)k), "r"(e));
+  return (int)c;
+}
+__device__ __forceinline__ Ch ch_not(const Ch& a) { return Ch{{~a.w[0], ~a.w[1], ~a.w[2], ~a.w[3]}}; }
+
+// A chunk value in "open" form: value = c + pb + adj * 2^128, with pb a small
+// signed integer at bit 0 of the chunk and adj the chunk's carry-out.
+struct Open {
+  Ch c;
+  int pb, adj;
+};
+__device__ __forceinline__ Open open_neg(const Open& x) {
+  // -(c + pb + adj 2^128) = ~c + 1 - 2^128 - pb - adj 2^128
+  return Open{ch_not(x.c), 1 - x.pb, -1 - x.adj};
 }
 
 // Rotation r (0 <= r < 2N) for windowed reads of omega^r * x.
@@ -105,55 +128,87 @@ struct Rot {
 __device__ __forceinline__ Rot make_rot(u64 r, u64 N) {
   Rot R;
   R.sigma = (r >= N) ? -1 : 1;
-  u64 t = (r >= N) ? r - N : r;
+  const u64 t = (r >= N) ? r - N : r;
   R.q = (u32)(t >> 7);
   R.o = (u32)(t & 127);
   return R;
 }
 
-// Exact value of output chunk i of omega^r * x (x a shared-memory slot),
-// including the one pending carry of x that lands inside it.
-__device__ __forceinline__ Val rot_chunk(const uint4* xc, const signed char* xp, const Rot& R,
-                                         u32 C, u32 i) {
+// 128-bit window [lo:hi] >> (128 - o) ... i.e. bits [128-o, 256-o) of hi:lo
+// (o in 1..127): the chunk of (hi:lo) << o that lands in the upper half.
+__device__ __forceinline__ Ch funnel_up(const Ch& lo, const Ch& hi, u32 o) {
+  u32 W[8] = {lo.w[0], lo.w[1], lo.w[2], lo.w[3], hi.w[0], hi.w[1], hi.w[2], hi.w[3]};
+  const u32 ow = o >> 5, ob = o & 31;
+  Ch r;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    // output word k of the upper half = bits [32(4+k) - o, ...) of W
+    const int hiw = 4 + k - (int)ow;  // word holding the high part
+    u32 h = 0, l = 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      if (x == hiw) h = W[x];
+      if (x == hiw - 1) l = W[x];
+    }
+    r.w[k] = ob ? __funnelshift_l(l, h, ob) : h;
+  }
+  return r;
+}
+
+// Chunk i of omega^r * x in open form (x a shared-memory slot), including the
+// one pending carry of x that lands inside it.
+__device__ __forceinline__ Open rot_chunk(const uint4* xc, const signed char* xp, const Rot& R,
+                                          u32 C, u32 i) {
   const u32 Cm = C - 1;
   const u32 j = (i - R.q) & Cm;  // source chunk of the upper part
-  const u32 jm = (j - 1) & Cm;   // source chunk of the lower part / landed pending
-  Val v;
+  const u32 jm = (j - 1) & Cm;   // lower part / landed pending (top of chunk jm)
+  Open v;
   if (R.o == 0) {
-    v.lo = to128(xc[j]);
-    v.hi = 0;
-    if (i < R.q) v = vneg(v);
-  } else {
-    const u128 up = to128(xc[j]) << R.o;
-    const u128 dn = to128(xc[jm]) >> (128 - R.o);
-    if (i > R.q) {
-      v.lo = up | dn;
-      v.hi = 0;
-    } else if (i < R.q) {
-      v.lo = up | dn;
-      v.hi = 0;
-      v = vneg(v);
-    } else {
-      Val a{up, 0}, b{dn, 0};
-      v = vsub(a, b);
-    }
+    // aligned: chunk j moves whole, its bottom pending (top of jm) with it
+    v.c = ld_ch(xc + j);
+    v.pb = (int)xp[jm];
+    v.adj = 0;
+    const bool neg = (i < R.q) != (R.sigma < 0);
+    if (i == R.q) v.pb = -v.pb;  // the element's top carry wraps: 2^N == -1
+    if (neg) v = open_neg(v);
+    return v;
   }
-  int p = xp[jm];
-  if (i <= R.q) p = -p;
-  v = vadd(v, vsmall(p, R.o));
-  if (R.sigma < 0) v = vneg(v);
+  const Ch lo = ld_ch(xc + jm), hi = ld_ch(xc + j);
+  const int p = (int)xp[jm];
+  // p * 2^o as a 160-bit signed value folded into the window
+  const u32 ow = R.o >> 5, ob = R.o & 31;
+  const long long pw = (long long)p * (1ll << ob);  // < 2^40 in magnitude
+  Ch P;
+  const u32 ext = (u32)(p >> 31);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    P.w[k] = ((u32)k < ow) ? 0u : ((u32)k == ow ? (u32)pw : ((u32)k == ow + 1 ? (u32)(pw >> 32) : ext));
+  }
+  const int ptop = (ow == 3) ? (int)(pw >> 32) : (int)ext;  // word 4 of p*2^o (sign extension)
+  if (i != R.q) {
+    v.c = funnel_up(lo, hi, R.o);
+    const int c = ch_add(v.c, v.c, P);
+    v.pb = 0;
+    v.adj = c + ptop;
+    const bool neg = (i < R.q) != (R.sigma < 0);
+    if (neg) v = open_neg(v);
+    return v;
+  }
+  // the chunk holding bit t: upper bits from chunk 0 (positive), lower bits
+  // from the top of chunk C-1 (wrapped, negative), and the wrapped top carry
+  Ch up = funnel_up(Ch{{0, 0, 0, 0}}, hi, R.o);
+  Ch dn = funnel_up(lo, Ch{{0, 0, 0, 0}}, R.o);
+  // value = up - dn - p*2^o
+  int c1 = ch_sub(v.c, up, dn);
+  int c2 = ch_sub(v.c, v.c, P);
+  v.pb = 0;
+  v.adj = c1 + c2 - ptop;
+  if (R.sigma < 0) v = open_neg(v);
   return v;
 }
 
-// Operand a, unrotated: chunk i plus its bottom pending carry.
-__device__ __forceinline__ Val plain_chunk(const uint4* ac, const signed char* ap, u32 C, u32 i) {
-  Val v{to128(ac[i]), 0};
-  int p = i ? (int)ap[i - 1] : -(int)ap[C - 1];
-  return vadd(v, vsmall(p, 0));
-}
-
 struct TaskOut {
-  uint4 w0, w1;
+  Ch w0, w1;
   signed char p0, p1;
   std::uint8_t mask;  // bit0: out0 -> slot a, bit1: out1 -> slot b
   std::uint16_t sa, sb;
@@ -169,50 +224,60 @@ __device__ __forceinline__ void run_op_task(std::uint8_t* sm, const Args& A, con
   const uint4* ac = slot_chunks(sm, A, op.a);
   const signed char* ap = slot_pend(sm, A, op.a);
   if (op.type == OP_COPY) {
-    T.w1 = ac[i];
+    T.w1 = ld_ch(ac + i);
     T.p1 = ap[i];
     T.mask = 2;
     return;
   }
   const Rot R = make_rot(op.r, A.N);
-  const Val b = rot_chunk(slot_chunks(sm, A, op.b), slot_pend(sm, A, op.b), R, C, i);
-  const Val a = plain_chunk(ac, ap, C, i);
-  Val y0, y1;
+  const Open b = rot_chunk(slot_chunks(sm, A, op.b), slot_pend(sm, A, op.b), R, C, i);
+  const Ch a = ld_ch(ac + i);
+  const int pa = i ? (int)ap[i - 1] : -(int)ap[C - 1];
+  // S = a + b, T = a - b (open form, exact)
+  Ch S, D;
+  int cs = ch_add(S, a, b.c);
+  cs += ch_add_small(S, pa + b.pb);
+  cs += b.adj;
+  int cd = ch_sub(D, a, b.c);
+  cd += ch_add_small(D, pa - b.pb);
+  cd -= b.adj;
   switch (op.type) {
     case OP_ADDSUB:
-      y0 = vadd(a, b);
-      y1 = vsub(a, b);
+      T.w0 = S;
+      T.p0 = (signed char)cs;
+      T.w1 = D;
+      T.p1 = (signed char)cd;
       T.mask = 3;
       break;
     case OP_ADD:
-      y0 = vadd(a, b);
+      T.w0 = S;
+      T.p0 = (signed char)cs;
       T.mask = 1;
       break;
-    case OP_SUB2:
-      y0 = vsub(vadd(a, a), b);
-      T.mask = 1;
-      break;
-    default:  // OP_SUB2DIFF
-      y1 = vsub(a, b);
-      y0 = vadd(a, y1);
-      T.mask = 3;
-      break;
-  }
-  T.w0 = from128(y0.lo);
-  T.p0 = (signed char)y0.hi;
-  if (T.mask & 2) {
-    T.w1 = from128(y1.lo);
-    T.p1 = (signed char)y1.hi;
+    default: {  // OP_SUB2 / OP_SUB2DIFF: out0 = a + (a - b)
+      Ch E;
+      int ce = ch_add(E, a, D);
+      ce += ch_add_small(E, pa);
+      T.w0 = E;
+      T.p0 = (signed char)(ce + cd);
+      if (op.type == OP_SUB2DIFF) {
+        T.w1 = D;
+        T.p1 = (signed char)cd;
+        T.mask = 3;
+      } else {
+        T.mask = 1;
+      }
+    }
   }
 }
 
 __device__ __forceinline__ void write_task(std::uint8_t* sm, const Args& A, const TaskOut& T) {
   if (T.mask & 1) {
-    slot_chunks(sm, A, T.sa)[T.chunk] = T.w0;
+    st_ch(slot_chunks(sm, A, T.sa) + T.chunk, T.w0);
     slot_pend(sm, A, T.sa)[T.chunk] = T.p0;
   }
   if (T.mask & 2) {
-    slot_chunks(sm, A, T.sb)[T.chunk] = T.w1;
+    st_ch(slot_chunks(sm, A, T.sb) + T.chunk, T.w1);
     slot_pend(sm, A, T.sb)[T.chunk] = T.p1;
   }
 }
@@ -238,18 +303,17 @@ __device__ __forceinline__ void rotate_slots(std::uint8_t* sm, const Args& A, u3
   for (u32 b0 = 0; b0 < ns; b0 += per_batch) {
     const u32 nb = min(ns - b0, per_batch);
     const u32 ntask = nb * C;
-    uint4 w[kTasksPerThread];
+    Ch w[kTasksPerThread];
     signed char p[kTasksPerThread];
 #pragma unroll
     for (int k = 0; k < kTasksPerThread; ++k) {
       const u32 t = tid + k * nthr;
       if (t < ntask) {
-        const u32 sl = s0 + b0 + t / C, i = t % C;
+        const u32 sl = s0 + b0 + (t >> A.logC), i = t & (C - 1);
         const u64 r = (rot[sl].a * s + rot[sl].b) & (A.M - 1);
-        const Rot R = make_rot(r, A.N);
-        Val v = rot_chunk(slot_chunks(sm, A, sl), slot_pend(sm, A, sl), R, C, i);
-        w[k] = from128(v.lo);
-        p[k] = (signed char)v.hi;
+        const Open v = rot_chunk(slot_chunks(sm, A, sl), slot_pend(sm, A, sl), make_rot(r, A.N), C, i);
+        w[k] = v.c;
+        p[k] = (signed char)(v.adj + ch_add_small(w[k], v.pb));
       }
     }
     __syncthreads();
@@ -257,8 +321,8 @@ __device__ __forceinline__ void rotate_slots(std::uint8_t* sm, const Args& A, u3
     for (int k = 0; k < kTasksPerThread; ++k) {
       const u32 t = tid + k * nthr;
       if (t < ntask) {
-        const u32 sl = s0 + b0 + t / C, i = t % C;
-        slot_chunks(sm, A, sl)[i] = w[k];
+        const u32 sl = s0 + b0 + (t >> A.logC), i = t & (C - 1);
+        st_ch(slot_chunks(sm, A, sl) + i, w[k]);
         slot_pend(sm, A, sl)[i] = p[k];
       }
     }
@@ -275,7 +339,7 @@ __device__ __forceinline__ void resolve_slots(std::uint8_t* sm, const Args& A, u
     const u32 nb = min(ns - b0, per_batch);
     const u32 ntask = nb * C;
     for (;;) {
-      u128 w[kTasksPerThread];
+      Ch w[kTasksPerThread];
       int e[kTasksPerThread];
       int any = 0;
 #pragma unroll
@@ -283,15 +347,11 @@ __device__ __forceinline__ void resolve_slots(std::uint8_t* sm, const Args& A, u
         const u32 t = tid + k * nthr;
         e[k] = 0;
         if (t < ntask) {
-          const u32 sl = b0 + t / C, i = t % C;
+          const u32 sl = b0 + (t >> A.logC), i = t & (C - 1);
           const signed char* pp = slot_pend(sm, A, sl);
           const int in = i ? (int)pp[i - 1] : 0;
-          w[k] = to128(slot_chunks(sm, A, sl)[i]);
-          const u128 old = w[k];
-          w[k] += (u128)(__int128)in;
-          int carry = 0;
-          if (in > 0 && w[k] < old) carry = 1;
-          if (in < 0 && w[k] > old) carry = -1;
+          w[k] = ld_ch(slot_chunks(sm, A, sl) + i);
+          const int carry = in ? ch_add_small(w[k], in) : 0;
           e[k] = (i == C - 1) ? (int)pp[C - 1] + carry : carry;
           if (i != C - 1 && carry != 0) any = 1;
         }
@@ -301,8 +361,8 @@ __device__ __forceinline__ void resolve_slots(std::uint8_t* sm, const Args& A, u
       for (int k = 0; k < kTasksPerThread; ++k) {
         const u32 t = tid + k * nthr;
         if (t < ntask) {
-          const u32 sl = b0 + t / C, i = t % C;
-          slot_chunks(sm, A, sl)[i] = from128(w[k]);
+          const u32 sl = b0 + (t >> A.logC), i = t & (C - 1);
+          st_ch(slot_chunks(sm, A, sl) + i, w[k]);
           slot_pend(sm, A, sl)[i] = (signed char)e[k];
         }
       }
@@ -370,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
           T[k].mask = 0;
           const u32 t = tid + k * nthr;
           if (t < ntask) {
-            const DevOp op = A.ops[ob + t / C];
-            run_op_task(sm, A, op, t % C, T[k]);
+            const DevOp op = A.ops[ob + (t >> A.logC)];
+            run_op_task(sm, A, op, t & (C - 1), T[k]);
           }
         }
         __syncthreads();
