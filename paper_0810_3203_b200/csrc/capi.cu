@@ -37,7 +37,8 @@ int fail(int code, const std::string& msg) {
       return fail(CFTFT_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_));    \
   } while (0)
 
-constexpr size_t kSmemBudget = 200 * 1024;  // per-CTA dynamic shared memory we plan for
+constexpr size_t kSmemBudget = 200 * 1024;  // per-CTA dynamic shared memory for leaf slots
+constexpr size_t kScratchBytes = 2048;       // Fermat carry scratch (threads x tasks per thread)
 
 // A plan resident on one device.
 struct DevicePlan {
@@ -208,7 +209,7 @@ int set_smem(K kernel) {
   static bool done = false;
   if (!done) {
     CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kSmemBudget));
+                                  (int)(kSmemBudget + kScratchBytes)));
     done = true;
   }
   return CFTFT_OK;
@@ -235,7 +236,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
-    const size_t smem = (size_t)R->slot_bytes << dp.max_ell;
+    const size_t slots_bytes = (size_t)R->slot_bytes << dp.max_ell;
+    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? kScratchBytes : 0);
     unsigned grid = 1;
     if (R->kind == CFTFT_RING_FERMAT) {
       if (int rc = set_smem(fermat::leaf_kernel)) return rc;
@@ -256,6 +258,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.D = R->D;
       A.C = R->C;
       A.logC = (u32)__builtin_ctz(R->C);
+      A.scratch_off = (u32)slots_bytes;
       A.slot_bytes = R->slot_bytes;
       fermat::leaf_kernel<<<grid, fermat::kThreads, smem, st>>>(A);
     } else {
@@ -388,8 +391,8 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   R->kind = kind;
   if (kind == CFTFT_RING_FERMAT) {
     const u64 N = n_or_k;
-    if (N < 128 || (N & (N - 1)) != 0)
-      return fail(CFTFT_UNSUPPORTED, "Fermat ring needs N a power of two >= 128");
+    if (N < 128 || (N & (N - 1)) != 0 || N > (u64{1} << 18))
+      return fail(CFTFT_UNSUPPORTED, "Fermat ring needs N a power of two in [128, 2^18]");
     R->N = N;
     R->M = 2 * N;
     R->D = (u32)(N / 32);
@@ -413,7 +416,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   }
   // largest leaf whose slots fit the shared-memory budget (and the 16-bit slot ids)
   unsigned lam = 1;
-  while (lam < 15 && ((size_t)R->slot_bytes << (lam + 1)) <= kSmemBudget) ++lam;
+  while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= kSmemBudget) ++lam;
   R->max_leaf_ell = lam;
   R->max_leaf_fit = lam;
   *out = R.release();

@@ -3,7 +3,7 @@
 // One persistent launch runs a whole transform.  Each CTA repeatedly takes a
 // ticket (a leaf: a sub-transform of <= 2^max_ell coefficients that fits in
 // shared memory), waits until the (node, phase) counter it depends on is
-// complete, runs the leaf, and bumps the counters it completes.  Tickets are
+// complete, runs the leaf, and bumps the counter it completes.  Tickets are
 // issued in a topological, L2-batched order by the planner.
 //
 // Element representation in shared memory ("chunked, carry-deferred"):
@@ -14,12 +14,13 @@
 //   the last chunk's pending carry sitting at 2^N == -1.  One thread computes
 //   one 128-bit output chunk of a butterfly from chunk i of operand a (plus
 //   a's pending carry from chunk i-1) and the matching window of the rotated
-//   operand b (plus the one pending carry of b landing inside it); its carry
-//   out becomes the new pending carry of chunk i.  No cross-thread carry
-//   propagation happens inside a leaf: carries are resolved once per stored
-//   slot (parallel sweeps in shared memory).
+//   operand b (plus the one pending carry of b landing inside it), with PTX
+//   add.cc/addc chains; its carry out becomes the new pending carry of chunk
+//   i.  No cross-thread carry propagation happens inside a leaf: carries are
+//   resolved once per stored slot, fused with the final rotation and the
+//   store to global memory.
 //
-// Global (HBM) element format between waves: N/64 u64 limbs "lo" plus a
+// Global (HBM) element format between levels: N/64 u64 limbs "lo" plus a
 // signed top word hi, value = lo + hi*2^N (== lo - hi).  Canonical inputs
 // (top in {0,1}) are a special case; the last step canonicalises.
 #pragma once
@@ -32,6 +33,7 @@ namespace fermat {
 
 constexpr int kThreads = 512;
 constexpr int kTasksPerThread = 4;
+constexpr u32 kMaxBatch = 256;  // ops (or slots) staged per batch
 
 struct Args {
   std::uint8_t* data;      // view element 0
@@ -43,30 +45,39 @@ struct Args {
   const u32* levels;       // absolute op offsets
   const SymExp* rots;      // pre/post rotation tables
   u32* counters;           // [0]: ticket; [1 + k]: (node, phase) completion counters
-  const DevCounter* cmeta;  // per-counter target and parent link
+  const DevCounter* cmeta; // per-counter target and parent link
   u64 N, M;
   u32 D, C;                // u32 words, 128-bit chunks per element
-  u32 slot_bytes;          // 4*D + pending bytes (16B aligned)
   u32 logC;
+  u32 slot_bytes;          // 4*D + pending bytes (16B aligned)
+  u32 scratch_off;         // byte offset of the carry scratch
 };
-
-__device__ __forceinline__ uint4* slot_chunks(std::uint8_t* sm, const Args& A, u32 s) {
-  return reinterpret_cast<uint4*>(sm + (size_t)s * A.slot_bytes);
-}
-__device__ __forceinline__ signed char* slot_pend(std::uint8_t* sm, const Args& A, u32 s) {
-  return reinterpret_cast<signed char*>(sm + (size_t)s * A.slot_bytes + 4u * A.D);
-}
 
 // ---- 128-bit chunk arithmetic on u32 words with PTX carry chains -------------
 
 struct Ch {
   u32 w[4];
 };
-__device__ __forceinline__ Ch ld_ch(const uint4* p) {
-  const uint4 v = *p;
-  return Ch{{v.x, v.y, v.z, v.w}};
+__device__ __forceinline__ Ch lds_ch(u32 addr) {
+  Ch c;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3])
+               : "r"(addr));
+  return c;
 }
-__device__ __forceinline__ void st_ch(uint4* p, const Ch& c) { *p = make_uint4(c.w[0], c.w[1], c.w[2], c.w[3]); }
+__device__ __forceinline__ void sts_ch(u32 addr, const Ch& c) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(c.w[0]), "r"(c.w[1]),
+               "r"(c.w[2]), "r"(c.w[3])
+               : "memory");
+}
+__device__ __forceinline__ int lds_s8(u32 addr) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_s8(u32 addr, int v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // r = a + b; returns the carry out (0/1)
 __device__ __forceinline__ int ch_add(Ch& r, const Ch& a, const Ch& b) {
@@ -107,7 +118,9 @@ __device__ __forceinline__ int ch_add_small(Ch& r, int k) {
       : "r"((u32)k), "r"(e));
   return (int)c;
 }
-__device__ __forceinline__ Ch ch_not(const Ch& a) { return Ch{{~a.w[0], ~a.w[1], ~a.w[2], ~a.w[3]}}; }
+__device__ __forceinline__ Ch ch_xor(const Ch& a, u32 m) {
+  return Ch{{a.w[0] ^ m, a.w[1] ^ m, a.w[2] ^ m, a.w[3] ^ m}};
+}
 
 // A chunk value in "open" form: value = c + pb + adj * 2^128, with pb a small
 // signed integer at bit 0 of the chunk and adj the chunk's carry-out.
@@ -115,176 +128,156 @@ struct Open {
   Ch c;
   int pb, adj;
 };
-__device__ __forceinline__ Open open_neg(const Open& x) {
-  // -(c + pb + adj 2^128) = ~c + 1 - 2^128 - pb - adj 2^128
-  return Open{ch_not(x.c), 1 - x.pb, -1 - x.adj};
+// conditional negation: -(c + pb + adj 2^128) = ~c + (1 - pb) + (-1 - adj) 2^128
+__device__ __forceinline__ Open open_cneg(const Open& x, bool neg) {
+  const u32 m = neg ? 0xFFFFFFFFu : 0u;
+  return Open{ch_xor(x.c, m), neg ? 1 - x.pb : x.pb, neg ? -1 - x.adj : x.adj};
 }
 
 // Rotation r (0 <= r < 2N) for windowed reads of omega^r * x.
 struct Rot {
-  int sigma;  // -1 when r >= N (2^N == -1)
   u32 q, o;   // t = r mod N = 128 q + o
+  u32 sneg;   // 1 when r >= N (2^N == -1)
 };
 __device__ __forceinline__ Rot make_rot(u64 r, u64 N) {
   Rot R;
-  R.sigma = (r >= N) ? -1 : 1;
-  const u64 t = (r >= N) ? r - N : r;
+  R.sneg = (r >= N) ? 1u : 0u;
+  const u64 t = R.sneg ? r - N : r;
   R.q = (u32)(t >> 7);
   R.o = (u32)(t & 127);
   return R;
 }
 
-// 128-bit window [lo:hi] >> (128 - o) ... i.e. bits [128-o, 256-o) of hi:lo
-// (o in 1..127): the chunk of (hi:lo) << o that lands in the upper half.
+// Upper 128 bits of (hi:lo) << o, 0 < o < 128.
 __device__ __forceinline__ Ch funnel_up(const Ch& lo, const Ch& hi, u32 o) {
-  u32 W[8] = {lo.w[0], lo.w[1], lo.w[2], lo.w[3], hi.w[0], hi.w[1], hi.w[2], hi.w[3]};
+  const u32 W[8] = {lo.w[0], lo.w[1], lo.w[2], lo.w[3], hi.w[0], hi.w[1], hi.w[2], hi.w[3]};
   const u32 ow = o >> 5, ob = o & 31;
   Ch r;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    // output word k of the upper half = bits [32(4+k) - o, ...) of W
-    const int hiw = 4 + k - (int)ow;  // word holding the high part
     u32 h = 0, l = 0;
 #pragma unroll
     for (int x = 0; x < 8; ++x) {
-      if (x == hiw) h = W[x];
-      if (x == hiw - 1) l = W[x];
+      if (x == 4 + k - (int)ow) h = W[x];
+      if (x == 3 + k - (int)ow) l = W[x];
     }
-    r.w[k] = ob ? __funnelshift_l(l, h, ob) : h;
+    r.w[k] = __funnelshift_l(l, h, ob);
   }
   return r;
 }
 
-// Chunk i of omega^r * x in open form (x a shared-memory slot), including the
-// one pending carry of x that lands inside it.
-__device__ __forceinline__ Open rot_chunk(const uint4* xc, const signed char* xp, const Rot& R,
-                                          u32 C, u32 i) {
-  const u32 Cm = C - 1;
+// Chunk i of omega^r * x in open form; x = (chunk base address, pending base
+// address) in shared memory.  Includes the one pending carry of x that lands
+// inside the chunk.
+__device__ __forceinline__ Open rot_chunk(u32 xw, u32 xp, const Rot& R, u32 Cm, u32 i) {
   const u32 j = (i - R.q) & Cm;  // source chunk of the upper part
   const u32 jm = (j - 1) & Cm;   // lower part / landed pending (top of chunk jm)
   Open v;
   if (R.o == 0) {
-    // aligned: chunk j moves whole, its bottom pending (top of jm) with it
-    v.c = ld_ch(xc + j);
-    v.pb = (int)xp[jm];
+    // aligned: chunk j moves whole, its bottom pending (top of chunk jm) with it
+    v.c = lds_ch(xw + 16 * j);
+    v.pb = lds_s8(xp + jm);
     v.adj = 0;
-    const bool neg = (i < R.q) != (R.sigma < 0);
     if (i == R.q) v.pb = -v.pb;  // the element's top carry wraps: 2^N == -1
-    if (neg) v = open_neg(v);
-    return v;
+    return open_cneg(v, ((i < R.q) ? 1u : 0u) != R.sneg);
   }
-  const Ch lo = ld_ch(xc + jm), hi = ld_ch(xc + j);
-  const int p = (int)xp[jm];
-  // p * 2^o as a 160-bit signed value folded into the window
+  const Ch lo = lds_ch(xw + 16 * jm), hi = lds_ch(xw + 16 * j);
+  const int p = lds_s8(xp + jm);
+  // p * 2^o as a 160-bit signed value P (+ ptop * 2^128)
   const u32 ow = R.o >> 5, ob = R.o & 31;
-  const long long pw = (long long)p * (1ll << ob);  // < 2^40 in magnitude
-  Ch P;
+  const long long pw = (long long)p * (1ll << ob);
   const u32 ext = (u32)(p >> 31);
+  Ch P;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 4; ++k)
     P.w[k] = ((u32)k < ow) ? 0u : ((u32)k == ow ? (u32)pw : ((u32)k == ow + 1 ? (u32)(pw >> 32) : ext));
-  }
-  const int ptop = (ow == 3) ? (int)(pw >> 32) : (int)ext;  // word 4 of p*2^o (sign extension)
+  const int ptop = (ow == 3) ? (int)(pw >> 32) : (int)ext;
   if (i != R.q) {
     v.c = funnel_up(lo, hi, R.o);
-    const int c = ch_add(v.c, v.c, P);
+    v.adj = ch_add(v.c, v.c, P) + ptop;
     v.pb = 0;
-    v.adj = c + ptop;
-    const bool neg = (i < R.q) != (R.sigma < 0);
-    if (neg) v = open_neg(v);
-    return v;
+    return open_cneg(v, ((i < R.q) ? 1u : 0u) != R.sneg);
   }
   // the chunk holding bit t: upper bits from chunk 0 (positive), lower bits
   // from the top of chunk C-1 (wrapped, negative), and the wrapped top carry
-  Ch up = funnel_up(Ch{{0, 0, 0, 0}}, hi, R.o);
-  Ch dn = funnel_up(lo, Ch{{0, 0, 0, 0}}, R.o);
-  // value = up - dn - p*2^o
-  int c1 = ch_sub(v.c, up, dn);
-  int c2 = ch_sub(v.c, v.c, P);
+  const Ch z{{0, 0, 0, 0}};
+  const Ch up = funnel_up(z, hi, R.o);
+  const Ch dn = funnel_up(lo, z, R.o);
+  const int c1 = ch_sub(v.c, up, dn);
+  const int c2 = ch_sub(v.c, v.c, P);
   v.pb = 0;
   v.adj = c1 + c2 - ptop;
-  if (R.sigma < 0) v = open_neg(v);
-  return v;
+  return open_cneg(v, R.sneg != 0);
 }
+
+// Per-op parameters staged in shared memory once per batch.
+struct OpT {
+  u32 aw, bw;  // smem addresses of slot a / slot b (pending arrays at +W4)
+  u32 q, o;
+  u32 sneg, type;
+};
 
 struct TaskOut {
   Ch w0, w1;
-  signed char p0, p1;
-  std::uint8_t mask;  // bit0: out0 -> slot a, bit1: out1 -> slot b
-  std::uint16_t sa, sb;
-  u32 chunk;
+  int p0, p1;
+  u32 d0, d1;  // smem chunk destinations
+  u32 mask;
 };
 
-__device__ __forceinline__ void run_op_task(std::uint8_t* sm, const Args& A, const DevOp& op, u32 i,
-                                            TaskOut& T) {
-  const u32 C = A.C;
-  T.sa = op.a;
-  T.sb = op.b;
-  T.chunk = i;
-  const uint4* ac = slot_chunks(sm, A, op.a);
-  const signed char* ap = slot_pend(sm, A, op.a);
-  if (op.type == OP_COPY) {
-    T.w1 = ld_ch(ac + i);
-    T.p1 = ap[i];
+__device__ __forceinline__ void run_op_task(const OpT& op, u32 W4, u32 Cm, u32 i, TaskOut& T) {
+  T.d0 = op.aw + 16 * i;
+  T.d1 = op.bw + 16 * i;
+  if (op.type == OP_COPY) {  // b <- a verbatim
+    T.w1 = lds_ch(op.aw + 16 * i);
+    T.p1 = lds_s8(op.aw + W4 + i);
     T.mask = 2;
     return;
   }
-  const Rot R = make_rot(op.r, A.N);
-  const Open b = rot_chunk(slot_chunks(sm, A, op.b), slot_pend(sm, A, op.b), R, C, i);
-  const Ch a = ld_ch(ac + i);
-  const int pa = i ? (int)ap[i - 1] : -(int)ap[C - 1];
-  // S = a + b, T = a - b (open form, exact)
+  const Rot R{op.q, op.o, op.sneg};
+  const Open b = rot_chunk(op.bw, op.bw + W4, R, Cm, i);
+  const Ch a = lds_ch(op.aw + 16 * i);
+  const int pa_raw = lds_s8(op.aw + W4 + ((i - 1) & Cm));
+  const int pa = i ? pa_raw : -pa_raw;
   Ch S, D;
   int cs = ch_add(S, a, b.c);
-  cs += ch_add_small(S, pa + b.pb);
-  cs += b.adj;
+  cs += ch_add_small(S, pa + b.pb) + b.adj;
   int cd = ch_sub(D, a, b.c);
-  cd += ch_add_small(D, pa - b.pb);
-  cd -= b.adj;
-  switch (op.type) {
-    case OP_ADDSUB:
-      T.w0 = S;
-      T.p0 = (signed char)cs;
-      T.w1 = D;
-      T.p1 = (signed char)cd;
-      T.mask = 3;
-      break;
-    case OP_ADD:
-      T.w0 = S;
-      T.p0 = (signed char)cs;
-      T.mask = 1;
-      break;
-    default: {  // OP_SUB2 / OP_SUB2DIFF: out0 = a + (a - b)
-      Ch E;
-      int ce = ch_add(E, a, D);
-      ce += ch_add_small(E, pa);
-      T.w0 = E;
-      T.p0 = (signed char)(ce + cd);
-      if (op.type == OP_SUB2DIFF) {
-        T.w1 = D;
-        T.p1 = (signed char)cd;
-        T.mask = 3;
-      } else {
-        T.mask = 1;
-      }
-    }
+  cd += ch_add_small(D, pa - b.pb) - b.adj;
+  if (op.type == OP_ADDSUB) {
+    T.w0 = S;
+    T.p0 = cs;
+    T.w1 = D;
+    T.p1 = cd;
+    T.mask = 3;
+  } else if (op.type == OP_ADD) {
+    T.w0 = S;
+    T.p0 = cs;
+    T.mask = 1;
+  } else {  // OP_SUB2 / OP_SUB2DIFF: out0 = a + (a - b)
+    Ch E;
+    int ce = ch_add(E, a, D);
+    ce += ch_add_small(E, pa);
+    T.w0 = E;
+    T.p0 = ce + cd;
+    T.w1 = D;
+    T.p1 = cd;
+    T.mask = (op.type == OP_SUB2DIFF) ? 3 : 1;
   }
 }
 
-__device__ __forceinline__ void write_task(std::uint8_t* sm, const Args& A, const TaskOut& T) {
+__device__ __forceinline__ void write_task(const TaskOut& T, u32 W4, u32 i) {
   if (T.mask & 1) {
-    st_ch(slot_chunks(sm, A, T.sa) + T.chunk, T.w0);
-    slot_pend(sm, A, T.sa)[T.chunk] = T.p0;
+    sts_ch(T.d0, T.w0);
+    sts_s8(T.d0 - 16 * i + W4 + i, T.p0);
   }
   if (T.mask & 2) {
-    st_ch(slot_chunks(sm, A, T.sb) + T.chunk, T.w1);
-    slot_pend(sm, A, T.sb)[T.chunk] = T.p1;
+    sts_ch(T.d1, T.w1);
+    sts_s8(T.d1 - 16 * i + W4 + i, T.p1);
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+__device__ __forceinline__ void cp_async16(u32 saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -294,88 +287,17 @@ __device__ __forceinline__ u32 ld_acquire(const u32* p) {
   return v;
 }
 
-// Rotates slots [s0, s0+ns) in place by rot[k] (k = slot) -- batched so that
-// every thread holds at most kTasksPerThread chunks.
-__device__ __forceinline__ void rotate_slots(std::uint8_t* sm, const Args& A, u32 s0, u32 ns,
-                                             const SymExp* rot, u64 s) {
-  const u32 C = A.C, tid = threadIdx.x, nthr = blockDim.x;
-  const u32 per_batch = max(1u, (nthr * kTasksPerThread) / C);
-  for (u32 b0 = 0; b0 < ns; b0 += per_batch) {
-    const u32 nb = min(ns - b0, per_batch);
-    const u32 ntask = nb * C;
-    Ch w[kTasksPerThread];
-    signed char p[kTasksPerThread];
-#pragma unroll
-    for (int k = 0; k < kTasksPerThread; ++k) {
-      const u32 t = tid + k * nthr;
-      if (t < ntask) {
-        const u32 sl = s0 + b0 + (t >> A.logC), i = t & (C - 1);
-        const u64 r = (rot[sl].a * s + rot[sl].b) & (A.M - 1);
-        const Open v = rot_chunk(slot_chunks(sm, A, sl), slot_pend(sm, A, sl), make_rot(r, A.N), C, i);
-        w[k] = v.c;
-        p[k] = (signed char)(v.adj + ch_add_small(w[k], v.pb));
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kTasksPerThread; ++k) {
-      const u32 t = tid + k * nthr;
-      if (t < ntask) {
-        const u32 sl = s0 + b0 + (t >> A.logC), i = t & (C - 1);
-        st_ch(slot_chunks(sm, A, sl) + i, w[k]);
-        slot_pend(sm, A, sl)[i] = p[k];
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Resolves the pending carries of slots [0, ns) into exact limbs (the top
-// pending carry stays: it is the element's signed top word).
-__device__ __forceinline__ void resolve_slots(std::uint8_t* sm, const Args& A, u32 ns) {
-  const u32 C = A.C, tid = threadIdx.x, nthr = blockDim.x;
-  const u32 per_batch = max(1u, (nthr * kTasksPerThread) / C);
-  for (u32 b0 = 0; b0 < ns; b0 += per_batch) {
-    const u32 nb = min(ns - b0, per_batch);
-    const u32 ntask = nb * C;
-    for (;;) {
-      Ch w[kTasksPerThread];
-      int e[kTasksPerThread];
-      int any = 0;
-#pragma unroll
-      for (int k = 0; k < kTasksPerThread; ++k) {
-        const u32 t = tid + k * nthr;
-        e[k] = 0;
-        if (t < ntask) {
-          const u32 sl = b0 + (t >> A.logC), i = t & (C - 1);
-          const signed char* pp = slot_pend(sm, A, sl);
-          const int in = i ? (int)pp[i - 1] : 0;
-          w[k] = ld_ch(slot_chunks(sm, A, sl) + i);
-          const int carry = in ? ch_add_small(w[k], in) : 0;
-          e[k] = (i == C - 1) ? (int)pp[C - 1] + carry : carry;
-          if (i != C - 1 && carry != 0) any = 1;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kTasksPerThread; ++k) {
-        const u32 t = tid + k * nthr;
-        if (t < ntask) {
-          const u32 sl = b0 + (t >> A.logC), i = t & (C - 1);
-          st_ch(slot_chunks(sm, A, sl) + i, w[k]);
-          slot_pend(sm, A, sl)[i] = (signed char)e[k];
-        }
-      }
-      if (!__syncthreads_or(any)) break;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
   extern __shared__ __align__(16) std::uint8_t sm[];
   __shared__ u32 s_ticket;
+  __shared__ OpT s_ops[kMaxBatch];
+  __shared__ Rot s_rot[kMaxBatch];
   const u32 tid = threadIdx.x, nthr = blockDim.x;
-  const u32 D = A.D, C = A.C;
+  const u32 C = A.C, Cm = C - 1, logC = A.logC;
+  const u32 smb = (u32)__cvta_generic_to_shared(sm);
+  const u32 SB = A.slot_bytes, W4 = 4 * A.D;
+  const u32 scr = smb + A.scratch_off;
+  const u32 per_batch = min(kMaxBatch, max(1u, (nthr * kTasksPerThread) >> logC));
 
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(&A.counters[0], 1u);
@@ -389,75 +311,169 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
       while (ld_acquire(c) < lf.dep_target) __nanosleep(64);
     }
     __syncthreads();
+    std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
+    const u64 gstride = lf.stride * A.elem_bytes;
 
-    // ---- load slots [0, nload) (L2 path: data may come from other CTAs) ----
+    // ---- load slots [0, nload) through L2 (written by other CTAs) -------------
     {
-      const u32 q16 = D / 4;
-      const u32 total = cl.nload * q16;
+      const u32 total = cl.nload << logC;
       for (u32 idx = tid; idx < total; idx += nthr) {
-        const u32 s = idx / q16, k = idx - s * q16;
-        const uint4* src =
-            reinterpret_cast<const uint4*>(A.data + (lf.base + (u64)s * lf.stride) * A.elem_bytes);
-        cp_async16(slot_chunks(sm, A, s) + k, src + k);
+        const u32 s = idx >> logC, k = idx & Cm;
+        cp_async16(smb + s * SB + 16 * k, gbase + s * gstride + 16 * (u64)k);
       }
-      for (u32 s = tid; s < cl.nload; s += nthr) {
-        const long long* top = reinterpret_cast<const long long*>(
-            A.data + (lf.base + (u64)s * lf.stride) * A.elem_bytes + A.N / 8);
-        const long long hi = __ldcg(top);
-        signed char* pp = slot_pend(sm, A, s);
-        pp[C - 1] = (signed char)hi;
-      }
-      const u32 ptotal = cl.nload * (C - 1);
-      for (u32 idx = tid; idx < ptotal; idx += nthr) {
-        const u32 s = idx / (C - 1), c = idx - s * (C - 1);
-        slot_pend(sm, A, s)[c] = 0;
+      for (u32 idx = tid; idx < total; idx += nthr) {
+        const u32 s = idx >> logC, c = idx & Cm;
+        int v = 0;
+        if (c == Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4));
+        sts_s8(smb + s * SB + W4 + c, v);
       }
       cp_async_wait_all();
     }
     __syncthreads();
-    if (cl.has_pre) rotate_slots(sm, A, 0, cl.nload, A.rots + cl.pre_begin, lf.s);
+
+    // ---- pre-rotations (ITFT spectral inputs), in place through registers ---
+    if (cl.has_pre) {
+      for (u32 b0 = 0; b0 < cl.nload; b0 += per_batch) {
+        const u32 nb = min(cl.nload - b0, per_batch);
+        for (u32 x = tid; x < nb; x += nthr) {
+          const SymExp P = A.rots[cl.pre_begin + b0 + x];
+          s_rot[x] = make_rot((P.a * lf.s + P.b) & (A.M - 1), A.N);
+        }
+        __syncthreads();
+        const u32 ntask = nb << logC;
+        Ch w[kTasksPerThread];
+        int p[kTasksPerThread];
+#pragma unroll
+        for (int k = 0; k < kTasksPerThread; ++k) {
+          const u32 t = tid + k * nthr;
+          if (t < ntask) {
+            const u32 x = t >> logC, i = t & Cm, sw = smb + (b0 + x) * SB;
+            const Open v = rot_chunk(sw, sw + W4, s_rot[x], Cm, i);
+            w[k] = v.c;
+            p[k] = v.adj + ch_add_small(w[k], v.pb);
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kTasksPerThread; ++k) {
+          const u32 t = tid + k * nthr;
+          if (t < ntask) {
+            const u32 i = t & Cm, sw = smb + (b0 + (t >> logC)) * SB;
+            sts_ch(sw + 16 * i, w[k]);
+            sts_s8(sw + W4 + i, p[k]);
+          }
+        }
+        __syncthreads();
+      }
+    }
 
     // ---- micro-op levels ------------------------------------------------------
-    const u32 ops_per_batch = max(1u, (nthr * kTasksPerThread) / C);
     for (u32 l = 0; l < cl.nlevels; ++l) {
       const u32 o0 = A.levels[cl.level_begin + l], o1 = A.levels[cl.level_begin + l + 1];
-      for (u32 ob = o0; ob < o1; ob += ops_per_batch) {
-        const u32 oe = min(o1, ob + ops_per_batch);
-        const u32 ntask = (oe - ob) * C;
+      for (u32 ob = o0; ob < o1; ob += per_batch) {
+        const u32 nb = min(o1 - ob, per_batch);
+        for (u32 x = tid; x < nb; x += nthr) {
+          const DevOp op = A.ops[ob + x];
+          const Rot R = make_rot(op.r, A.N);
+          s_ops[x] = OpT{smb + op.a * SB, smb + op.b * SB, R.q, R.o, R.sneg, op.type};
+        }
+        __syncthreads();
+        const u32 ntask = nb << logC;
         TaskOut T[kTasksPerThread];
 #pragma unroll
         for (int k = 0; k < kTasksPerThread; ++k) {
           T[k].mask = 0;
           const u32 t = tid + k * nthr;
-          if (t < ntask) {
-            const DevOp op = A.ops[ob + (t >> A.logC)];
-            run_op_task(sm, A, op, t & (C - 1), T[k]);
-          }
+          if (t < ntask) run_op_task(s_ops[t >> logC], W4, Cm, t & Cm, T[k]);
         }
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < kTasksPerThread; ++k)
-          if (T[k].mask) write_task(sm, A, T[k]);
+          if (T[k].mask) write_task(T[k], W4, (tid + k * nthr) & Cm);
         __syncthreads();
       }
     }
 
-    // ---- post-rotation, carry resolution, store --------------------------------
-    rotate_slots(sm, A, 0, cl.nstore, A.rots + cl.post_begin, lf.s);
-    resolve_slots(sm, A, cl.nstore);
-    {
-      const u32 q16 = D / 4;
-      const u32 total = cl.nstore * q16;
-      for (u32 idx = tid; idx < total; idx += nthr) {
-        const u32 s = idx / q16, k = idx - s * q16;
-        uint4* dst = reinterpret_cast<uint4*>(A.data + (lf.base + (u64)s * lf.stride) * A.elem_bytes);
-        __stcg(dst + k, slot_chunks(sm, A, s)[k]);
+    // ---- post-rotation + carry resolution + store, fused ------------------------
+    for (u32 b0 = 0; b0 < cl.nstore; b0 += per_batch) {
+      const u32 nb = min(cl.nstore - b0, per_batch);
+      for (u32 x = tid; x < nb; x += nthr) {
+        const SymExp P = A.rots[cl.post_begin + b0 + x];
+        s_rot[x] = make_rot((P.a * lf.s + P.b) & (A.M - 1), A.N);
       }
-      for (u32 s = tid; s < cl.nstore; s += nthr) {
-        long long* top = reinterpret_cast<long long*>(A.data + (lf.base + (u64)s * lf.stride) * A.elem_bytes +
-                                                      A.N / 8);
-        __stcg(top, (long long)slot_pend(sm, A, s)[C - 1]);
+      __syncthreads();
+      const u32 ntask = nb << logC;
+      Ch w[kTasksPerThread];
+      int top[kTasksPerThread];
+#pragma unroll
+      for (int k = 0; k < kTasksPerThread; ++k) {
+        const u32 t = tid + k * nthr;
+        if (t < ntask) {
+          const u32 x = t >> logC, i = t & Cm, sw = smb + (b0 + x) * SB;
+          const Open v = rot_chunk(sw, sw + W4, s_rot[x], Cm, i);
+          w[k] = v.c;
+          top[k] = v.adj + ch_add_small(w[k], v.pb);
+          sts_s8(scr + t, top[k]);
+        }
       }
+      __syncthreads();
+      // absorb the carry of the chunk below (one step); carries that ripple
+      // further (a chunk of all ones / all zeros) take the slow path
+      int rare = 0;
+#pragma unroll
+      for (int k = 0; k < kTasksPerThread; ++k) {
+        const u32 t = tid + k * nthr;
+        if (t < ntask) {
+          const u32 i = t & Cm;
+          const int in = i ? lds_s8(scr + t - 1) : 0;
+          const int e = in ? ch_add_small(w[k], in) : 0;
+          if (i == Cm) {
+            top[k] += e;
+          } else {
+            if (e) rare = 1;
+            top[k] = e;  // carry still owed to chunk i+1
+          }
+        }
+      }
+      if (__syncthreads_or(rare)) {
+        // sequential sweeps through shared memory (the slots are free now)
+        for (;;) {
+#pragma unroll
+          for (int k = 0; k < kTasksPerThread; ++k) {
+            const u32 t = tid + k * nthr;
+            if (t < ntask && (t & Cm) != Cm) sts_s8(scr + t, top[k]);
+          }
+          __syncthreads();
+          int any = 0;
+#pragma unroll
+          for (int k = 0; k < kTasksPerThread; ++k) {
+            const u32 t = tid + k * nthr;
+            if (t < ntask) {
+              const u32 i = t & Cm;
+              const int in = i ? lds_s8(scr + t - 1) : 0;
+              const int e = in ? ch_add_small(w[k], in) : 0;
+              if (i == Cm) {
+                top[k] += e;
+              } else {
+                if (e) any = 1;
+                top[k] = e;
+              }
+            }
+          }
+          if (!__syncthreads_or(any)) break;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kTasksPerThread; ++k) {
+        const u32 t = tid + k * nthr;
+        if (t < ntask) {
+          const u32 i = t & Cm;
+          std::uint8_t* g = gbase + (b0 + (t >> logC)) * gstride;
+          __stcg(reinterpret_cast<uint4*>(g) + i, make_uint4(w[k].w[0], w[k].w[1], w[k].w[2], w[k].w[3]));
+          if (i == Cm) __stcg(reinterpret_cast<long long*>(g + W4), (long long)top[k]);
+        }
+      }
+      __syncthreads();  // scratch and s_rot reuse
     }
     __threadfence();
     __syncthreads();
