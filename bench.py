@@ -235,6 +235,7 @@ def main():
     ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--leaf-limit", type=int, default=0, help="cap on-chip leaves at 2^k (tuning)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -262,6 +263,8 @@ def main():
 
     N, L, z, n, desc = CONFIGS[args.config]
     ctx = cf.FermatRingCtx(N)
+    if args.leaf_limit:
+        ctx.set_leaf_limit(args.leaf_limit)
     W = ctx.element_words
     host = make_input(N, L, z, W, po.mix_seed(42, 5 + rank))
     dev = torch.from_numpy(host.view(np.int64)).cuda()

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -37,8 +38,9 @@ int fail(int code, const std::string& msg) {
       return fail(CFTFT_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_));    \
   } while (0)
 
-constexpr size_t kSmemBudget = 200 * 1024;  // per-CTA dynamic shared memory for leaf slots
-constexpr size_t kScratchBytes = 2048;       // Fermat carry scratch (threads x tasks per thread)
+constexpr size_t kSmemBudget = 196 * 1024;  // per-CTA dynamic shared memory for leaf slots
+// Fermat carry scratch: one int per (thread x task) of a store batch
+inline size_t scratch_bytes(u32 cw) { return (size_t)fermat::kThreads * (fermat::kWordsPerThread / cw) * 4; }
 
 // A plan resident on one device.
 struct DevicePlan {
@@ -65,7 +67,8 @@ using PlanKey = std::tuple<int, int, u64, u64, u64, u64, int, int>;  // dev, inv
 struct cftft_ring {
   int kind = 0;
   u64 N = 0, K = 0, m = 0, M = 0;
-  u32 D = 0, C = 0;     // Fermat: u32 words / 128-bit chunks
+  u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
+  u32 CW = 16;
   u32 slot_bytes = 0;   // shared-memory bytes per slot
   u64 elem_bytes = 0;   // minimal element stride
   unsigned max_leaf_ell = 1;
@@ -206,12 +209,7 @@ int check_stride(const cftft_ring* R, u64 stride) {
 
 template <class K>
 int set_smem(K kernel) {
-  static bool done = false;
-  if (!done) {
-    CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kSmemBudget + kScratchBytes)));
-    done = true;
-  }
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
   return CFTFT_OK;
 }
 
@@ -237,11 +235,9 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
     const size_t slots_bytes = (size_t)R->slot_bytes << dp.max_ell;
-    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? kScratchBytes : 0);
+    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->CW) : 0);
     unsigned grid = 1;
     if (R->kind == CFTFT_RING_FERMAT) {
-      if (int rc = set_smem(fermat::leaf_kernel)) return rc;
-      if (int rc = grid_for(fermat::leaf_kernel, fermat::kThreads, smem, dp.nleaves, &grid)) return rc;
       fermat::Args A{};
       A.data = base;
       A.elem_bytes = stride;
@@ -258,9 +254,35 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.D = R->D;
       A.C = R->C;
       A.logC = (u32)__builtin_ctz(R->C);
-      A.scratch_off = (u32)slots_bytes;
       A.slot_bytes = R->slot_bytes;
-      fermat::leaf_kernel<<<grid, fermat::kThreads, smem, st>>>(A);
+      A.scratch_off = (u32)slots_bytes;
+      unsigned long long* prof = nullptr;
+      static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
+      if (profiling) {
+        CUDA_TRY(cudaMallocAsync((void**)&prof, 8 * fermat::PH_N, st));
+        CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * fermat::PH_N, st));
+      }
+      A.prof = prof;
+      auto go = [&](auto kernel) -> int {
+        if (int rc = set_smem(kernel)) return rc;
+        if (int rc = grid_for(kernel, fermat::kThreads, smem, dp.nleaves, &grid)) return rc;
+        kernel<<<grid, fermat::kThreads, smem, st>>>(A);
+        return CFTFT_OK;
+      };
+      int rc = R->CW == 16 ? go(fermat::leaf_kernel<16>) : R->CW == 8 ? go(fermat::leaf_kernel<8>)
+                                                                     : go(fermat::leaf_kernel<4>);
+      if (rc) return rc;
+      if (prof) {
+        unsigned long long h[fermat::PH_N];
+        CUDA_TRY(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        CUDA_TRY(cudaFreeAsync(prof, st));
+        unsigned long long tot = 0;
+        for (auto v : h) tot += v;
+        fprintf(stderr, "[cftft] leaves=%llu grid=%u phase cycles (%% of CTA time): wait %.1f load %.1f pre %.1f levels %.1f post %.1f store %.1f (total %.3g cyc/CTA)\n",
+                (unsigned long long)dp.nleaves, grid, 100.0 * h[0] / tot, 100.0 * h[1] / tot, 100.0 * h[2] / tot,
+                100.0 * h[3] / tot, 100.0 * h[4] / tot, 100.0 * h[5] / tot, (double)tot / grid);
+      }
     } else {
       if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
       if (int rc = grid_for(negacyclic::leaf_kernel, negacyclic::kThreads, smem, dp.nleaves, &grid))
@@ -396,9 +418,9 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
     R->N = N;
     R->M = 2 * N;
     R->D = (u32)(N / 32);
-    R->C = R->D / 4;
-    const u32 pend = (R->C + 15) & ~15u;
-    R->slot_bytes = 4 * R->D + pend;
+    R->CW = R->D >= 16 ? 16 : R->D;
+    R->C = R->D / R->CW;
+    R->slot_bytes = (4 * R->D + 4 * R->C + 15) & ~15u;
     R->elem_bytes = ((N / 8 + 8) + 15) & ~u64(15);
   } else if (kind == CFTFT_RING_NEGACYCLIC) {
     const u64 K = n_or_k, m = modulus;
@@ -416,7 +438,8 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   }
   // largest leaf whose slots fit the shared-memory budget (and the 16-bit slot ids)
   unsigned lam = 1;
-  while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= kSmemBudget) ++lam;
+  const size_t budget = kSmemBudget - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->CW) : 0);
+  while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= budget) ++lam;
   R->max_leaf_ell = lam;
   R->max_leaf_fit = lam;
   *out = R.release();

@@ -7,18 +7,18 @@
 // issued in a topological, L2-batched order by the planner.
 //
 // Element representation in shared memory ("chunked, carry-deferred"):
-//   D = N/32 u32 words in C = D/4 chunks of 128 bits, plus one signed 8-bit
-//   pending carry per chunk (the carry out of that chunk, not yet added to
-//   the next).  The value is
-//       sum_j (chunk_j + pend_j * 2^128) * 2^(128 j)   (mod 2^N + 1),
-//   the last chunk's pending carry sitting at 2^N == -1.  One thread computes
-//   one 128-bit output chunk of a butterfly from chunk i of operand a (plus
-//   a's pending carry from chunk i-1) and the matching window of the rotated
-//   operand b (plus the one pending carry of b landing inside it), with PTX
-//   add.cc/addc chains; its carry out becomes the new pending carry of chunk
-//   i.  No cross-thread carry propagation happens inside a leaf: carries are
-//   resolved once per stored slot, fused with the final rotation and the
-//   store to global memory.
+//   D = N/32 u32 words in C = D/CW chunks of CW words (CB = 32*CW bits), plus
+//   one signed 32-bit carry per chunk that sits ON TOP of the chunk:
+//       value = sum_j (chunk_j + top_j * 2^CB) * 2^(CB j)   (mod 2^N + 1),
+//   the last chunk's top sitting at 2^N == -1.  A butterfly output chunk is
+//   computed by one thread from chunk i of operand a and chunk i of the
+//   rotated operand b with ONE add.cc chain and ONE sub.cc chain; the tops
+//   just add (top0 = ta + tb + carry), so nothing ever crosses a chunk
+//   boundary inside a leaf.  A rotation by a whole number of chunks moves
+//   (chunk, top) pairs, negating those that wrap past 2^N; the negation costs
+//   nothing because it turns the add chain into a sub chain and vice versa.
+//   Tops grow by about one bit per level; they are folded into the limbs once
+//   per stored slot, fused with the final rotation and the store to HBM.
 //
 // Global (HBM) element format between levels: N/64 u64 limbs "lo" plus a
 // signed top word hi, value = lo + hi*2^N (== lo - hi).  Canonical inputs
@@ -32,8 +32,8 @@ namespace cftft_b200 {
 namespace fermat {
 
 constexpr int kThreads = 512;
-constexpr int kTasksPerThread = 4;
-constexpr u32 kMaxBatch = 256;  // ops (or slots) staged per batch
+constexpr u32 kMaxBatch = 256;    // ops (or slots) staged per batch
+constexpr u32 kWordsPerThread = 32;  // live words per thread per batch
 
 struct Args {
   std::uint8_t* data;      // view element 0
@@ -47,40 +47,102 @@ struct Args {
   u32* counters;           // [0]: ticket; [1 + k]: (node, phase) completion counters
   const DevCounter* cmeta; // per-counter target and parent link
   u64 N, M;
-  u32 D, C;                // u32 words, 128-bit chunks per element
+  u32 D, C;                // u32 words, chunks per element
   u32 logC;
-  u32 slot_bytes;          // 4*D + pending bytes (16B aligned)
+  u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
+  unsigned long long* prof;  // optional per-phase cycle totals (CFTFT_PROFILE=1)
 };
 
-// ---- 128-bit chunk arithmetic on u32 words with PTX carry chains -------------
+// Phase timing (debug): thread 0 of each CTA accumulates clock64 deltas.
+enum { PH_WAIT = 0, PH_LOAD, PH_PRE, PH_LEVELS, PH_POST, PH_STORE, PH_N };
+struct PhaseClock {
+  unsigned long long acc[PH_N];
+  unsigned long long t;
+  bool on;
+  __device__ void start(bool enable) {
+    on = enable;
+    for (int i = 0; i < PH_N; ++i) acc[i] = 0;
+    t = clock64();
+  }
+  __device__ void mark(int ph) {
+    if (!on) return;
+    const unsigned long long n = clock64();
+    acc[ph] += n - t;
+    t = n;
+  }
+  __device__ void flush(unsigned long long* out) {
+    if (!on) return;
+    for (int i = 0; i < PH_N; ++i) atomicAdd(out + i, acc[i]);
+  }
+};
 
+extern __shared__ __align__(16) std::uint8_t g_sm[];
+
+template <int CW>
 struct Ch {
-  u32 w[4];
+  u32 w[CW];
 };
-__device__ __forceinline__ Ch lds_ch(u32 addr) {
-  Ch c;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3])
-               : "r"(addr));
-  return c;
+
+// A slot stores its chunks PIECE-MAJOR and XOR-swizzled: 16-byte piece k of
+// chunk i lives at slot + (k*C + (i ^ (k & (C-1))))*16.  Lanes of a warp
+// (consecutive chunks, same k) touch distinct consecutive-ish 16-byte pieces,
+// and so do lanes copying consecutive pieces of one chunk: both the compute
+// accesses and the coalesced copies to/from HBM are bank-conflict free.
+__device__ __forceinline__ u32 piece_off(u32 slot, u32 i, u32 k, u32 C) {
+  return slot + ((k * C) + (i ^ (k & (C - 1)))) * 16;
 }
-__device__ __forceinline__ void sts_ch(u32 addr, const Ch& c) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(c.w[0]), "r"(c.w[1]),
-               "r"(c.w[2]), "r"(c.w[3])
-               : "memory");
+template <int CW>
+__device__ __forceinline__ void lds_ch(Ch<CW>& c, u32 slot, u32 i, u32 C) {
+#pragma unroll
+  for (int k = 0; k < CW; k += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(g_sm + piece_off(slot, i, k / 4, C));
+    c.w[k] = v.x;
+    c.w[k + 1] = v.y;
+    c.w[k + 2] = v.z;
+    c.w[k + 3] = v.w;
+  }
 }
-__device__ __forceinline__ int lds_s8(u32 addr) {
-  int v;
-  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
+template <int CW>
+__device__ __forceinline__ void sts_ch(u32 slot, u32 i, u32 C, const Ch<CW>& c) {
+#pragma unroll
+  for (int k = 0; k < CW; k += 4)
+    *reinterpret_cast<uint4*>(g_sm + piece_off(slot, i, k / 4, C)) =
+        make_uint4(c.w[k], c.w[k + 1], c.w[k + 2], c.w[k + 3]);
 }
-__device__ __forceinline__ void sts_s8(u32 addr, int v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+
+// X[m] = W[CW-1-OW+m] (m = 0..CW) of the window W = lo ++ hi.
+template <int CW, int OW>
+__device__ __forceinline__ void pick_window(u32 (&X)[CW + 1], const Ch<CW>& lo, const Ch<CW>& hi) {
+#pragma unroll
+  for (int m = 0; m <= CW; ++m) {
+    const int idx = CW - 1 - OW + m;
+    X[m] = idx < CW ? lo.w[idx] : hi.w[idx - CW];
+  }
 }
+template <int CW, int OW = 0>
+__device__ __forceinline__ void pick_window_rt(u32 (&X)[CW + 1], const Ch<CW>& lo, const Ch<CW>& hi, u32 ow) {
+  if constexpr (OW < CW) {
+    if (ow == OW)
+      pick_window<CW, OW>(X, lo, hi);
+    else
+      pick_window_rt<CW, OW + 1>(X, lo, hi, ow);
+  }
+}
+
+__device__ __forceinline__ int lds_i32(u32 off) { return *reinterpret_cast<const int*>(g_sm + off); }
+__device__ __forceinline__ void sts_i32(u32 off, int v) { *reinterpret_cast<int*>(g_sm + off) = v; }
+
+// ---- multi-word carry chains: ONE asm statement per chain (the carry flag
+// is invisible to the compiler, so a chain must never be split) -----------
+// (generated for CW = 4, 8, 16)
+template <int CW> __device__ int ch_add(Ch<CW>& r, const Ch<CW>& a, const Ch<CW>& b);
+template <int CW> __device__ int ch_sub(Ch<CW>& r, const Ch<CW>& a, const Ch<CW>& b);
+template <int CW> __device__ int ch_add_small(Ch<CW>& r, int k);
 
 // r = a + b; returns the carry out (0/1)
-__device__ __forceinline__ int ch_add(Ch& r, const Ch& a, const Ch& b) {
+template <>
+__device__ __forceinline__ int ch_add<4>(Ch<4>& r, const Ch<4>& a, const Ch<4>& b) {
   u32 c;
   asm("add.cc.u32 %0, %5, %9;\n\t"
       "addc.cc.u32 %1, %6, %10;\n\t"
@@ -88,12 +150,13 @@ __device__ __forceinline__ int ch_add(Ch& r, const Ch& a, const Ch& b) {
       "addc.cc.u32 %3, %8, %12;\n\t"
       "addc.u32 %4, 0, 0;"
       : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(c)
-      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]),
-        "r"(b.w[3]));
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
   return (int)c;
 }
+
 // r = a - b; returns the borrow as -1/0
-__device__ __forceinline__ int ch_sub(Ch& r, const Ch& a, const Ch& b) {
+template <>
+__device__ __forceinline__ int ch_sub<4>(Ch<4>& r, const Ch<4>& a, const Ch<4>& b) {
   u32 c;
   asm("sub.cc.u32 %0, %5, %9;\n\t"
       "subc.cc.u32 %1, %6, %10;\n\t"
@@ -101,12 +164,13 @@ __device__ __forceinline__ int ch_sub(Ch& r, const Ch& a, const Ch& b) {
       "subc.cc.u32 %3, %8, %12;\n\t"
       "subc.u32 %4, 0, 0;"
       : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(c)
-      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]),
-        "r"(b.w[3]));
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
   return (int)c;
 }
-// r += k (k small signed, sign-extended); returns the signed carry (-1/0/1)
-__device__ __forceinline__ int ch_add_small(Ch& r, int k) {
+
+// r += k (small signed, sign-extended); returns the signed carry out
+template <>
+__device__ __forceinline__ int ch_add_small<4>(Ch<4>& r, int k) {
   const u32 e = (u32)(k >> 31);
   u32 c;
   asm("add.cc.u32 %0, %0, %5;\n\t"
@@ -118,163 +182,231 @@ __device__ __forceinline__ int ch_add_small(Ch& r, int k) {
       : "r"((u32)k), "r"(e));
   return (int)c;
 }
-__device__ __forceinline__ Ch ch_xor(const Ch& a, u32 m) {
-  return Ch{{a.w[0] ^ m, a.w[1] ^ m, a.w[2] ^ m, a.w[3] ^ m}};
+
+// r = a + b; returns the carry out (0/1)
+template <>
+__device__ __forceinline__ int ch_add<8>(Ch<8>& r, const Ch<8>& a, const Ch<8>& b) {
+  u32 c;
+  asm("add.cc.u32 %0, %9, %17;\n\t"
+      "addc.cc.u32 %1, %10, %18;\n\t"
+      "addc.cc.u32 %2, %11, %19;\n\t"
+      "addc.cc.u32 %3, %12, %20;\n\t"
+      "addc.cc.u32 %4, %13, %21;\n\t"
+      "addc.cc.u32 %5, %14, %22;\n\t"
+      "addc.cc.u32 %6, %15, %23;\n\t"
+      "addc.cc.u32 %7, %16, %24;\n\t"
+      "addc.u32 %8, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]), "r"(a.w[7]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]));
+  return (int)c;
 }
 
-// A chunk value in "open" form: value = c + pb + adj * 2^128, with pb a small
-// signed integer at bit 0 of the chunk and adj the chunk's carry-out.
-struct Open {
-  Ch c;
-  int pb, adj;
-};
-// conditional negation: -(c + pb + adj 2^128) = ~c + (1 - pb) + (-1 - adj) 2^128
-__device__ __forceinline__ Open open_cneg(const Open& x, bool neg) {
-  const u32 m = neg ? 0xFFFFFFFFu : 0u;
-  return Open{ch_xor(x.c, m), neg ? 1 - x.pb : x.pb, neg ? -1 - x.adj : x.adj};
+// r = a - b; returns the borrow as -1/0
+template <>
+__device__ __forceinline__ int ch_sub<8>(Ch<8>& r, const Ch<8>& a, const Ch<8>& b) {
+  u32 c;
+  asm("sub.cc.u32 %0, %9, %17;\n\t"
+      "subc.cc.u32 %1, %10, %18;\n\t"
+      "subc.cc.u32 %2, %11, %19;\n\t"
+      "subc.cc.u32 %3, %12, %20;\n\t"
+      "subc.cc.u32 %4, %13, %21;\n\t"
+      "subc.cc.u32 %5, %14, %22;\n\t"
+      "subc.cc.u32 %6, %15, %23;\n\t"
+      "subc.cc.u32 %7, %16, %24;\n\t"
+      "subc.u32 %8, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]), "r"(a.w[7]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]));
+  return (int)c;
+}
+
+// r += k (small signed, sign-extended); returns the signed carry out
+template <>
+__device__ __forceinline__ int ch_add_small<8>(Ch<8>& r, int k) {
+  const u32 e = (u32)(k >> 31);
+  u32 c;
+  asm("add.cc.u32 %0, %0, %9;\n\t"
+      "addc.cc.u32 %1, %1, %10;\n\t"
+      "addc.cc.u32 %2, %2, %10;\n\t"
+      "addc.cc.u32 %3, %3, %10;\n\t"
+      "addc.cc.u32 %4, %4, %10;\n\t"
+      "addc.cc.u32 %5, %5, %10;\n\t"
+      "addc.cc.u32 %6, %6, %10;\n\t"
+      "addc.cc.u32 %7, %7, %10;\n\t"
+      "addc.u32 %8, %10, 0;"
+      : "+r"(r.w[0]), "+r"(r.w[1]), "+r"(r.w[2]), "+r"(r.w[3]), "+r"(r.w[4]), "+r"(r.w[5]), "+r"(r.w[6]), "+r"(r.w[7]), "=r"(c)
+      : "r"((u32)k), "r"(e));
+  return (int)c;
+}
+
+// r = a + b; returns the carry out (0/1)
+template <>
+__device__ __forceinline__ int ch_add<16>(Ch<16>& r, const Ch<16>& a, const Ch<16>& b) {
+  u32 c;
+  asm("add.cc.u32 %0, %17, %33;\n\t"
+      "addc.cc.u32 %1, %18, %34;\n\t"
+      "addc.cc.u32 %2, %19, %35;\n\t"
+      "addc.cc.u32 %3, %20, %36;\n\t"
+      "addc.cc.u32 %4, %21, %37;\n\t"
+      "addc.cc.u32 %5, %22, %38;\n\t"
+      "addc.cc.u32 %6, %23, %39;\n\t"
+      "addc.cc.u32 %7, %24, %40;\n\t"
+      "addc.cc.u32 %8, %25, %41;\n\t"
+      "addc.cc.u32 %9, %26, %42;\n\t"
+      "addc.cc.u32 %10, %27, %43;\n\t"
+      "addc.cc.u32 %11, %28, %44;\n\t"
+      "addc.cc.u32 %12, %29, %45;\n\t"
+      "addc.cc.u32 %13, %30, %46;\n\t"
+      "addc.cc.u32 %14, %31, %47;\n\t"
+      "addc.cc.u32 %15, %32, %48;\n\t"
+      "addc.u32 %16, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]), "=r"(r.w[8]), "=r"(r.w[9]), "=r"(r.w[10]), "=r"(r.w[11]), "=r"(r.w[12]), "=r"(r.w[13]), "=r"(r.w[14]), "=r"(r.w[15]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]), "r"(a.w[7]), "r"(a.w[8]), "r"(a.w[9]), "r"(a.w[10]), "r"(a.w[11]), "r"(a.w[12]), "r"(a.w[13]), "r"(a.w[14]), "r"(a.w[15]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]), "r"(b.w[8]), "r"(b.w[9]), "r"(b.w[10]), "r"(b.w[11]), "r"(b.w[12]), "r"(b.w[13]), "r"(b.w[14]), "r"(b.w[15]));
+  return (int)c;
+}
+
+// r = a - b; returns the borrow as -1/0
+template <>
+__device__ __forceinline__ int ch_sub<16>(Ch<16>& r, const Ch<16>& a, const Ch<16>& b) {
+  u32 c;
+  asm("sub.cc.u32 %0, %17, %33;\n\t"
+      "subc.cc.u32 %1, %18, %34;\n\t"
+      "subc.cc.u32 %2, %19, %35;\n\t"
+      "subc.cc.u32 %3, %20, %36;\n\t"
+      "subc.cc.u32 %4, %21, %37;\n\t"
+      "subc.cc.u32 %5, %22, %38;\n\t"
+      "subc.cc.u32 %6, %23, %39;\n\t"
+      "subc.cc.u32 %7, %24, %40;\n\t"
+      "subc.cc.u32 %8, %25, %41;\n\t"
+      "subc.cc.u32 %9, %26, %42;\n\t"
+      "subc.cc.u32 %10, %27, %43;\n\t"
+      "subc.cc.u32 %11, %28, %44;\n\t"
+      "subc.cc.u32 %12, %29, %45;\n\t"
+      "subc.cc.u32 %13, %30, %46;\n\t"
+      "subc.cc.u32 %14, %31, %47;\n\t"
+      "subc.cc.u32 %15, %32, %48;\n\t"
+      "subc.u32 %16, 0, 0;"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]), "=r"(r.w[8]), "=r"(r.w[9]), "=r"(r.w[10]), "=r"(r.w[11]), "=r"(r.w[12]), "=r"(r.w[13]), "=r"(r.w[14]), "=r"(r.w[15]), "=r"(c)
+      : "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]), "r"(a.w[7]), "r"(a.w[8]), "r"(a.w[9]), "r"(a.w[10]), "r"(a.w[11]), "r"(a.w[12]), "r"(a.w[13]), "r"(a.w[14]), "r"(a.w[15]), "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]), "r"(b.w[6]), "r"(b.w[7]), "r"(b.w[8]), "r"(b.w[9]), "r"(b.w[10]), "r"(b.w[11]), "r"(b.w[12]), "r"(b.w[13]), "r"(b.w[14]), "r"(b.w[15]));
+  return (int)c;
+}
+
+// r += k (small signed, sign-extended); returns the signed carry out
+template <>
+__device__ __forceinline__ int ch_add_small<16>(Ch<16>& r, int k) {
+  const u32 e = (u32)(k >> 31);
+  u32 c;
+  asm("add.cc.u32 %0, %0, %17;\n\t"
+      "addc.cc.u32 %1, %1, %18;\n\t"
+      "addc.cc.u32 %2, %2, %18;\n\t"
+      "addc.cc.u32 %3, %3, %18;\n\t"
+      "addc.cc.u32 %4, %4, %18;\n\t"
+      "addc.cc.u32 %5, %5, %18;\n\t"
+      "addc.cc.u32 %6, %6, %18;\n\t"
+      "addc.cc.u32 %7, %7, %18;\n\t"
+      "addc.cc.u32 %8, %8, %18;\n\t"
+      "addc.cc.u32 %9, %9, %18;\n\t"
+      "addc.cc.u32 %10, %10, %18;\n\t"
+      "addc.cc.u32 %11, %11, %18;\n\t"
+      "addc.cc.u32 %12, %12, %18;\n\t"
+      "addc.cc.u32 %13, %13, %18;\n\t"
+      "addc.cc.u32 %14, %14, %18;\n\t"
+      "addc.cc.u32 %15, %15, %18;\n\t"
+      "addc.u32 %16, %18, 0;"
+      : "+r"(r.w[0]), "+r"(r.w[1]), "+r"(r.w[2]), "+r"(r.w[3]), "+r"(r.w[4]), "+r"(r.w[5]), "+r"(r.w[6]), "+r"(r.w[7]), "+r"(r.w[8]), "+r"(r.w[9]), "+r"(r.w[10]), "+r"(r.w[11]), "+r"(r.w[12]), "+r"(r.w[13]), "+r"(r.w[14]), "+r"(r.w[15]), "=r"(c)
+      : "r"((u32)k), "r"(e));
+  return (int)c;
 }
 
 // Rotation r (0 <= r < 2N) for windowed reads of omega^r * x.
 struct Rot {
-  u32 q, o;   // t = r mod N = 128 q + o
+  u32 q, o;   // t = r mod N = CB q + o
   u32 sneg;   // 1 when r >= N (2^N == -1)
 };
+template <int CW>
 __device__ __forceinline__ Rot make_rot(u64 r, u64 N) {
+  constexpr u32 CB = 32 * CW;
   Rot R;
   R.sneg = (r >= N) ? 1u : 0u;
   const u64 t = R.sneg ? r - N : r;
-  R.q = (u32)(t >> 7);
-  R.o = (u32)(t & 127);
+  R.q = (u32)(t / CB);
+  R.o = (u32)(t % CB);
   return R;
 }
 
-// Upper 128 bits of (hi:lo) << o, 0 < o < 128.
-__device__ __forceinline__ Ch funnel_up(const Ch& lo, const Ch& hi, u32 o) {
-  const u32 W[8] = {lo.w[0], lo.w[1], lo.w[2], lo.w[3], hi.w[0], hi.w[1], hi.w[2], hi.w[3]};
+// p * 2^o (o < CB) as a (CW+1)-word signed value: words P and top ptop.
+template <int CW>
+__device__ __forceinline__ int small_shifted(Ch<CW>& P, int p, u32 o) {
   const u32 ow = o >> 5, ob = o & 31;
-  Ch r;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    u32 h = 0, l = 0;
-#pragma unroll
-    for (int x = 0; x < 8; ++x) {
-      if (x == 4 + k - (int)ow) h = W[x];
-      if (x == 3 + k - (int)ow) l = W[x];
-    }
-    r.w[k] = __funnelshift_l(l, h, ob);
-  }
-  return r;
-}
-
-// Chunk i of omega^r * x in open form; x = (chunk base address, pending base
-// address) in shared memory.  Includes the one pending carry of x that lands
-// inside the chunk.
-__device__ __forceinline__ Open rot_chunk(u32 xw, u32 xp, const Rot& R, u32 Cm, u32 i) {
-  const u32 j = (i - R.q) & Cm;  // source chunk of the upper part
-  const u32 jm = (j - 1) & Cm;   // lower part / landed pending (top of chunk jm)
-  Open v;
-  if (R.o == 0) {
-    // aligned: chunk j moves whole, its bottom pending (top of chunk jm) with it
-    v.c = lds_ch(xw + 16 * j);
-    v.pb = lds_s8(xp + jm);
-    v.adj = 0;
-    if (i == R.q) v.pb = -v.pb;  // the element's top carry wraps: 2^N == -1
-    return open_cneg(v, ((i < R.q) ? 1u : 0u) != R.sneg);
-  }
-  const Ch lo = lds_ch(xw + 16 * jm), hi = lds_ch(xw + 16 * j);
-  const int p = lds_s8(xp + jm);
-  // p * 2^o as a 160-bit signed value P (+ ptop * 2^128)
-  const u32 ow = R.o >> 5, ob = R.o & 31;
   const long long pw = (long long)p * (1ll << ob);
   const u32 ext = (u32)(p >> 31);
-  Ch P;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < CW; ++k)
     P.w[k] = ((u32)k < ow) ? 0u : ((u32)k == ow ? (u32)pw : ((u32)k == ow + 1 ? (u32)(pw >> 32) : ext));
-  const int ptop = (ow == 3) ? (int)(pw >> 32) : (int)ext;
-  if (i != R.q) {
-    v.c = funnel_up(lo, hi, R.o);
-    v.adj = ch_add(v.c, v.c, P) + ptop;
-    v.pb = 0;
-    return open_cneg(v, ((i < R.q) ? 1u : 0u) != R.sneg);
+  return (ow == CW - 1) ? (int)(pw >> 32) : (int)ext;
+}
+
+// Chunk i of omega^r * x as (B, tb, neg): value = (-1)^neg (B + tb 2^CB).
+// xw: smem offset of x's chunks, xt: of its tops.
+template <int CW>
+__device__ __forceinline__ bool rot_chunk(Ch<CW>& B, int& tb, u32 xw, u32 xt, const Rot& R, u32 Cm,
+                                          u32 i) {
+  const u32 C = Cm + 1;
+  const u32 j = (i - R.q) & Cm;
+  if (R.o == 0) {  // whole chunks: (chunk, top) pairs move together
+    lds_ch(B, xw, j, C);
+    tb = lds_i32(xt + 4 * j);
+    return ((i < R.q) ? 1u : 0u) != R.sneg;
   }
-  // the chunk holding bit t: upper bits from chunk 0 (positive), lower bits
-  // from the top of chunk C-1 (wrapped, negative), and the wrapped top carry
-  const Ch z{{0, 0, 0, 0}};
-  const Ch up = funnel_up(z, hi, R.o);
-  const Ch dn = funnel_up(lo, z, R.o);
-  const int c1 = ch_sub(v.c, up, dn);
-  const int c2 = ch_sub(v.c, v.c, P);
-  v.pb = 0;
-  v.adj = c1 + c2 - ptop;
-  return open_cneg(v, R.sneg != 0);
+  // unaligned: word g of the output takes source bits [32g - t, 32g + 32 - t)
+  // (mod N); words below t wrap past 2^N (negative).  Read the CW+1 source
+  // words of the window straight from shared memory.
+  const u32 jm = (j - 1) & Cm;
+  const u32 ow = R.o >> 5, sh = R.o & 31;
+  Ch<CW> lo, hi;
+  lds_ch(lo, xw, jm, C);
+  lds_ch(hi, xw, j, C);
+  u32 Wd[CW + 1];
+  pick_window_rt<CW>(Wd, lo, hi, ow);
+  Ch<CW> P;
+  const int ptop = small_shifted(P, lds_i32(xt + 4 * jm), R.o);  // jm's top lands at offset o
+  if (i != R.q) {
+#pragma unroll
+    for (int k = 0; k < CW; ++k) B.w[k] = __funnelshift_l(Wd[k], Wd[k + 1], sh);
+    tb = ch_add(B, B, P) + ptop;
+    return ((i < R.q) ? 1u : 0u) != R.sneg;
+  }
+  // the chunk holding bit t: words above t come from chunk 0 (positive),
+  // words below from the top of chunk C-1 and its top carry (wrapped: negative)
+  Ch<CW> up, dn;
+#pragma unroll
+  for (int k = 0; k < CW; ++k) {
+    const u32 v = __funnelshift_l(Wd[k], Wd[k + 1], sh);
+    const u32 mhi = ((u32)k > ow) ? 0xFFFFFFFFu : ((u32)k == ow ? (0xFFFFFFFFu << sh) : 0u);
+    up.w[k] = v & mhi;
+    dn.w[k] = v & ~mhi;
+  }
+  const int c1 = ch_sub(B, up, dn);
+  const int c2 = ch_sub(B, B, P);
+  tb = c1 + c2 - ptop;
+  return R.sneg != 0;
+}
+
+// Exact form of (-1)^neg (B + tb 2^CB): chunk W and top.
+template <int CW>
+__device__ __forceinline__ int exact_from(Ch<CW>& W, int tb, bool neg) {
+  if (!neg) return tb;
+  // -(B + tb 2^CB) = (~B + 1) - (tb + 1) 2^CB
+#pragma unroll
+  for (int k = 0; k < CW; ++k) W.w[k] = ~W.w[k];
+  return ch_add_small(W, 1) - tb - 1;
 }
 
 // Per-op parameters staged in shared memory once per batch.
 struct OpT {
-  u32 aw, bw;  // smem addresses of slot a / slot b (pending arrays at +W4)
+  u32 aw, bw;  // smem offsets of slot a / slot b (tops at +W4)
   u32 q, o;
   u32 sneg, type;
 };
-
-struct TaskOut {
-  Ch w0, w1;
-  int p0, p1;
-  u32 d0, d1;  // smem chunk destinations
-  u32 mask;
-};
-
-__device__ __forceinline__ void run_op_task(const OpT& op, u32 W4, u32 Cm, u32 i, TaskOut& T) {
-  T.d0 = op.aw + 16 * i;
-  T.d1 = op.bw + 16 * i;
-  if (op.type == OP_COPY) {  // b <- a verbatim
-    T.w1 = lds_ch(op.aw + 16 * i);
-    T.p1 = lds_s8(op.aw + W4 + i);
-    T.mask = 2;
-    return;
-  }
-  const Rot R{op.q, op.o, op.sneg};
-  const Open b = rot_chunk(op.bw, op.bw + W4, R, Cm, i);
-  const Ch a = lds_ch(op.aw + 16 * i);
-  const int pa_raw = lds_s8(op.aw + W4 + ((i - 1) & Cm));
-  const int pa = i ? pa_raw : -pa_raw;
-  Ch S, D;
-  int cs = ch_add(S, a, b.c);
-  cs += ch_add_small(S, pa + b.pb) + b.adj;
-  int cd = ch_sub(D, a, b.c);
-  cd += ch_add_small(D, pa - b.pb) - b.adj;
-  if (op.type == OP_ADDSUB) {
-    T.w0 = S;
-    T.p0 = cs;
-    T.w1 = D;
-    T.p1 = cd;
-    T.mask = 3;
-  } else if (op.type == OP_ADD) {
-    T.w0 = S;
-    T.p0 = cs;
-    T.mask = 1;
-  } else {  // OP_SUB2 / OP_SUB2DIFF: out0 = a + (a - b)
-    Ch E;
-    int ce = ch_add(E, a, D);
-    ce += ch_add_small(E, pa);
-    T.w0 = E;
-    T.p0 = ce + cd;
-    T.w1 = D;
-    T.p1 = cd;
-    T.mask = (op.type == OP_SUB2DIFF) ? 3 : 1;
-  }
-}
-
-__device__ __forceinline__ void write_task(const TaskOut& T, u32 W4, u32 i) {
-  if (T.mask & 1) {
-    sts_ch(T.d0, T.w0);
-    sts_s8(T.d0 - 16 * i + W4 + i, T.p0);
-  }
-  if (T.mask & 2) {
-    sts_ch(T.d1, T.w1);
-    sts_s8(T.d1 - 16 * i + W4 + i, T.p1);
-  }
-}
 
 __device__ __forceinline__ void cp_async16(u32 saddr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
@@ -287,146 +419,271 @@ __device__ __forceinline__ u32 ld_acquire(const u32* p) {
   return v;
 }
 
+// Leaf-program cache: the micro-ops / rotations of the current leaf class
+// live in shared memory, so consecutive leaves of one class (the common case)
+// never touch the class tables in global memory again.
+constexpr u32 kCacheOps = 256;
+constexpr u32 kCacheLev = 64;
+constexpr u32 kCacheRot = 512;  // pre + post rotations
+
+// Issues the cp.async loads of a leaf's input slots and initialises their
+// tops (the element's signed top word sits on top of the last chunk).
+template <int CW>
+__device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
+                                           u32 tid) {
+  constexpr u32 nthr = kThreads;
+  const u32 C = A.C, Cm = C - 1, logC = A.logC, SB = A.slot_bytes, W4 = 4 * A.D;
+  std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
+  const u64 gstride = lf.stride * A.elem_bytes;
+  const u32 q16 = A.D >> 2, lq = logC + (u32)__ffs(CW / 4) - 1;  // 16-byte pieces per slot
+  const u32 total = cl.nload << lq;
+  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
+  for (u32 idx = tid; idx < total; idx += nthr) {
+    const u32 s = idx >> lq, pp = idx & (q16 - 1);
+    const u32 i = pp >> lpc, k = pp & ((1u << lpc) - 1);
+    cp_async16(smem_base + piece_off(s * SB, i, k, C), gbase + s * gstride + 16 * (u64)pp);
+  }
+  const u32 ttot = cl.nload << logC;
+  for (u32 idx = tid; idx < ttot; idx += nthr) {
+    const u32 s = idx >> logC, c = idx & Cm;
+    int v = 0;
+    if (c == Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4));
+    sts_i32(s * SB + W4 + 4 * c, v);
+  }
+}
+
+template <int CW>
 __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
-  extern __shared__ __align__(16) std::uint8_t sm[];
-  __shared__ u32 s_ticket;
-  __shared__ OpT s_ops[kMaxBatch];
+  constexpr u32 CBY = 4 * CW;
+  constexpr int TPT = kWordsPerThread / CW;  // tasks per thread per batch
+  __shared__ u32 s_tk[2];
+  __shared__ DevLeaf s_lf[2];
+  __shared__ DevClass s_cl[2];
+  __shared__ int s_ready;  // next leaf's dependency already satisfied
+  __shared__ u32 s_cached;
+  __shared__ OpT s_ops[kCacheOps];
+  __shared__ u32 s_lev[kCacheLev + 1];
+  __shared__ SymExp s_crot[kCacheRot];
   __shared__ Rot s_rot[kMaxBatch];
-  const u32 tid = threadIdx.x, nthr = blockDim.x;
+  const u32 tid = threadIdx.x;
+  constexpr u32 nthr = kThreads;
   const u32 C = A.C, Cm = C - 1, logC = A.logC;
-  const u32 smb = (u32)__cvta_generic_to_shared(sm);
   const u32 SB = A.slot_bytes, W4 = 4 * A.D;
-  const u32 scr = smb + A.scratch_off;
-  const u32 per_batch = min(kMaxBatch, max(1u, (nthr * kTasksPerThread) >> logC));
+  const u32 scr = A.scratch_off;
+  const u32 smem_base = (u32)__cvta_generic_to_shared(g_sm);
+  const u32 per_batch = min(kMaxBatch, max(1u, (nthr * TPT) >> logC));
+  PhaseClock pc;
+  pc.start(tid == 0 && A.prof != nullptr);
+
+  // ---- prologue: first ticket, its descriptor, its loads ----------------------
+  if (tid == 0) {
+    const u32 t = atomicAdd(&A.counters[0], 1u);
+    s_tk[0] = t;
+    if (t < A.nleaves) {
+      s_lf[0] = A.leaves[t];
+      s_cl[0] = A.classes[s_lf[0].cls];
+      if (s_lf[0].dep != kNoDep)
+        while (ld_acquire(&A.counters[1 + s_lf[0].dep]) < s_lf[0].dep_target) __nanosleep(64);
+    }
+    s_cached = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  if (s_tk[0] < A.nleaves) issue_load<CW>(A, s_lf[0], s_cl[0], smem_base, tid);
+  u32 cur = 0;
 
   for (;;) {
-    if (tid == 0) s_ticket = atomicAdd(&A.counters[0], 1u);
-    __syncthreads();
-    const u32 ticket = s_ticket;
-    if (ticket >= A.nleaves) return;
-    const DevLeaf lf = A.leaves[ticket];
-    const DevClass cl = A.classes[lf.cls];
-    if (lf.dep != kNoDep && tid == 0) {
-      const u32* c = &A.counters[1 + lf.dep];
-      while (ld_acquire(c) < lf.dep_target) __nanosleep(64);
+    const u32 ticket = s_tk[cur];
+    if (ticket >= A.nleaves) break;
+    const DevLeaf lf = s_lf[cur];
+    const DevClass cl = s_cl[cur];
+    const u32 nxt = cur ^ 1;
+    // fetch the next ticket and descriptor now; they are consumed a leaf later
+    if (tid == 0) {
+      const u32 t = atomicAdd(&A.counters[0], 1u);
+      s_tk[nxt] = t;
+      s_ready = 0;
+      if (t < A.nleaves) {
+        s_lf[nxt] = A.leaves[t];
+        s_cl[nxt] = A.classes[s_lf[nxt].cls];
+        const DevLeaf& nl = s_lf[nxt];
+        s_ready = (nl.dep == kNoDep) || (ld_acquire(&A.counters[1 + nl.dep]) >= nl.dep_target);
+      }
     }
+    // leaf-program cache
+    const u32 nops = A.levels[cl.level_begin + cl.nlevels] - A.levels[cl.level_begin];
+    const bool cached = nops <= kCacheOps && cl.nlevels <= kCacheLev && cl.nload + cl.nstore <= kCacheRot;
+    if (cached && s_cached != lf.cls) {
+      const u32 op0 = A.levels[cl.level_begin];
+      for (u32 x = tid; x < nops; x += nthr) {
+        const DevOp op = A.ops[op0 + x];
+        const Rot R = make_rot<CW>(op.r, A.N);
+        s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
+      }
+      for (u32 x = tid; x <= cl.nlevels; x += nthr) s_lev[x] = A.levels[cl.level_begin + x] - op0;
+      for (u32 x = tid; x < cl.nload; x += nthr) s_crot[x] = A.rots[cl.pre_begin + x];
+      for (u32 x = tid; x < cl.nstore; x += nthr) s_crot[cl.nload + x] = A.rots[cl.post_begin + x];
+    }
+    cp_async_wait_all();
     __syncthreads();
+    if (tid == 0 && cached) s_cached = lf.cls;
+    pc.mark(PH_LOAD);
     std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
     const u64 gstride = lf.stride * A.elem_bytes;
-
-    // ---- load slots [0, nload) through L2 (written by other CTAs) -------------
-    {
-      const u32 total = cl.nload << logC;
-      for (u32 idx = tid; idx < total; idx += nthr) {
-        const u32 s = idx >> logC, k = idx & Cm;
-        cp_async16(smb + s * SB + 16 * k, gbase + s * gstride + 16 * (u64)k);
-      }
-      for (u32 idx = tid; idx < total; idx += nthr) {
-        const u32 s = idx >> logC, c = idx & Cm;
-        int v = 0;
-        if (c == Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4));
-        sts_s8(smb + s * SB + W4 + c, v);
-      }
-      cp_async_wait_all();
-    }
-    __syncthreads();
 
     // ---- pre-rotations (ITFT spectral inputs), in place through registers ---
     if (cl.has_pre) {
       for (u32 b0 = 0; b0 < cl.nload; b0 += per_batch) {
         const u32 nb = min(cl.nload - b0, per_batch);
         for (u32 x = tid; x < nb; x += nthr) {
-          const SymExp P = A.rots[cl.pre_begin + b0 + x];
-          s_rot[x] = make_rot((P.a * lf.s + P.b) & (A.M - 1), A.N);
+          const SymExp P = cached ? s_crot[b0 + x] : A.rots[cl.pre_begin + b0 + x];
+          s_rot[x] = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
         }
         __syncthreads();
         const u32 ntask = nb << logC;
-        Ch w[kTasksPerThread];
-        int p[kTasksPerThread];
+        Ch<CW> w[TPT];
+        int tp[TPT];
 #pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k) {
+        for (int k = 0; k < TPT; ++k) {
           const u32 t = tid + k * nthr;
           if (t < ntask) {
-            const u32 x = t >> logC, i = t & Cm, sw = smb + (b0 + x) * SB;
-            const Open v = rot_chunk(sw, sw + W4, s_rot[x], Cm, i);
-            w[k] = v.c;
-            p[k] = v.adj + ch_add_small(w[k], v.pb);
+            const u32 x = t >> logC, i = t & Cm, sw = (b0 + x) * SB;
+            const bool neg = rot_chunk<CW>(w[k], tp[k], sw, sw + W4, s_rot[x], Cm, i);
+            tp[k] = exact_from<CW>(w[k], tp[k], neg);
           }
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k) {
+        for (int k = 0; k < TPT; ++k) {
           const u32 t = tid + k * nthr;
           if (t < ntask) {
-            const u32 i = t & Cm, sw = smb + (b0 + (t >> logC)) * SB;
-            sts_ch(sw + 16 * i, w[k]);
-            sts_s8(sw + W4 + i, p[k]);
+            const u32 i = t & Cm, sw = (b0 + (t >> logC)) * SB;
+            sts_ch<CW>(sw, i, C, w[k]);
+            sts_i32(sw + W4 + 4 * i, tp[k]);
           }
         }
         __syncthreads();
       }
     }
+    pc.mark(PH_PRE);
 
     // ---- micro-op levels ------------------------------------------------------
     for (u32 l = 0; l < cl.nlevels; ++l) {
-      const u32 o0 = A.levels[cl.level_begin + l], o1 = A.levels[cl.level_begin + l + 1];
+      u32 o0, o1;
+      if (cached) {
+        o0 = s_lev[l];
+        o1 = s_lev[l + 1];
+      } else {
+        o0 = A.levels[cl.level_begin + l];
+        o1 = A.levels[cl.level_begin + l + 1];
+      }
       for (u32 ob = o0; ob < o1; ob += per_batch) {
         const u32 nb = min(o1 - ob, per_batch);
-        for (u32 x = tid; x < nb; x += nthr) {
-          const DevOp op = A.ops[ob + x];
-          const Rot R = make_rot(op.r, A.N);
-          s_ops[x] = OpT{smb + op.a * SB, smb + op.b * SB, R.q, R.o, R.sneg, op.type};
+        u32 sbase = ob;
+        if (!cached) {  // stage this batch's ops
+          for (u32 x = tid; x < nb; x += nthr) {
+            const DevOp op = A.ops[ob + x];
+            const Rot R = make_rot<CW>(op.r, A.N);
+            s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
+          }
+          __syncthreads();
+          sbase = 0;
         }
-        __syncthreads();
         const u32 ntask = nb << logC;
-        TaskOut T[kTasksPerThread];
+        // out0 goes to slot a in place right away (only this task reads a's
+        // chunk i); out1 goes to slot b after the barrier (b is read rotated)
+        Ch<CW> hold[TPT];
+        int htop[TPT];
+        u32 hdst[TPT];
 #pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k) {
-          T[k].mask = 0;
+        for (int k = 0; k < TPT; ++k) {
+          hdst[k] = 0xFFFFFFFFu;
           const u32 t = tid + k * nthr;
-          if (t < ntask) run_op_task(s_ops[t >> logC], W4, Cm, t & Cm, T[k]);
+          if (t >= ntask) continue;
+          const OpT op = s_ops[sbase + (t >> logC)];
+          const u32 i = t & Cm;
+          const u32 ta = op.aw + W4 + 4 * i;
+          Ch<CW> a;
+          lds_ch(a, op.aw, i, C);
+          const int pa = lds_i32(ta);
+          if (op.type == OP_COPY) {
+            hold[k] = a;
+            htop[k] = pa;
+            hdst[k] = op.bw;
+            continue;
+          }
+          Ch<CW> b;
+          int pb;
+          const bool neg = rot_chunk<CW>(b, pb, op.bw, op.bw + W4, Rot{op.q, op.o, op.sneg}, Cm, i);
+          Ch<CW> y0;
+          int t0, t1;
+          // y0 = a + s b, y1 = a - s b with s = (-1)^neg
+          if (!neg) {
+            t0 = ch_add(y0, a, b) + pa + pb;
+            t1 = ch_sub(hold[k], a, b) + pa - pb;
+          } else {
+            t0 = ch_sub(y0, a, b) + pa - pb;
+            t1 = ch_add(hold[k], a, b) + pa + pb;
+          }
+          if (op.type == OP_SUB2 || op.type == OP_SUB2DIFF) {  // y0 = a + y1 = 2a - s b
+            t0 = ch_add(y0, a, hold[k]) + pa + t1;
+          }
+          sts_ch<CW>(op.aw, i, C, y0);
+          sts_i32(ta, t0);
+          if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF) {
+            htop[k] = t1;
+            hdst[k] = op.bw;
+          }
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k)
-          if (T[k].mask) write_task(T[k], W4, (tid + k * nthr) & Cm);
+        for (int k = 0; k < TPT; ++k) {
+          if (hdst[k] != 0xFFFFFFFFu) {
+            const u32 i = (tid + k * nthr) & Cm;
+            sts_ch<CW>(hdst[k], i, C, hold[k]);
+            sts_i32(hdst[k] + W4 + 4 * i, htop[k]);
+          }
+        }
         __syncthreads();
       }
     }
+    pc.mark(PH_LEVELS);
 
     // ---- post-rotation + carry resolution + store, fused ------------------------
+    const bool have_next = s_tk[nxt] < A.nleaves;
+    bool next_issued = false;
     for (u32 b0 = 0; b0 < cl.nstore; b0 += per_batch) {
       const u32 nb = min(cl.nstore - b0, per_batch);
+      const bool last = b0 + nb >= cl.nstore;
       for (u32 x = tid; x < nb; x += nthr) {
-        const SymExp P = A.rots[cl.post_begin + b0 + x];
-        s_rot[x] = make_rot((P.a * lf.s + P.b) & (A.M - 1), A.N);
+        const SymExp P = cached ? s_crot[cl.nload + b0 + x] : A.rots[cl.post_begin + b0 + x];
+        s_rot[x] = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
       }
       __syncthreads();
       const u32 ntask = nb << logC;
-      Ch w[kTasksPerThread];
-      int top[kTasksPerThread];
+      Ch<CW> w[TPT];
+      int top[TPT];
 #pragma unroll
-      for (int k = 0; k < kTasksPerThread; ++k) {
+      for (int k = 0; k < TPT; ++k) {
         const u32 t = tid + k * nthr;
         if (t < ntask) {
-          const u32 x = t >> logC, i = t & Cm, sw = smb + (b0 + x) * SB;
-          const Open v = rot_chunk(sw, sw + W4, s_rot[x], Cm, i);
-          w[k] = v.c;
-          top[k] = v.adj + ch_add_small(w[k], v.pb);
-          sts_s8(scr + t, top[k]);
+          const u32 x = t >> logC, i = t & Cm, sw = (b0 + x) * SB;
+          const bool neg = rot_chunk<CW>(w[k], top[k], sw, sw + W4, s_rot[x], Cm, i);
+          top[k] = exact_from<CW>(w[k], top[k], neg);
+          sts_i32(scr + 4 * t, top[k]);
         }
       }
       __syncthreads();
-      // absorb the carry of the chunk below (one step); carries that ripple
+      pc.mark(PH_POST);
+      // fold in the top of the chunk below (one step); carries that ripple
       // further (a chunk of all ones / all zeros) take the slow path
       int rare = 0;
 #pragma unroll
-      for (int k = 0; k < kTasksPerThread; ++k) {
+      for (int k = 0; k < TPT; ++k) {
         const u32 t = tid + k * nthr;
         if (t < ntask) {
           const u32 i = t & Cm;
-          const int in = i ? lds_s8(scr + t - 1) : 0;
-          const int e = in ? ch_add_small(w[k], in) : 0;
+          const int in = i ? lds_i32(scr + 4 * (t - 1)) : 0;
+          const int e = in ? ch_add_small<CW>(w[k], in) : 0;
           if (i == Cm) {
             top[k] += e;
           } else {
@@ -436,22 +693,21 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
         }
       }
       if (__syncthreads_or(rare)) {
-        // sequential sweeps through shared memory (the slots are free now)
         for (;;) {
 #pragma unroll
-          for (int k = 0; k < kTasksPerThread; ++k) {
+          for (int k = 0; k < TPT; ++k) {
             const u32 t = tid + k * nthr;
-            if (t < ntask && (t & Cm) != Cm) sts_s8(scr + t, top[k]);
+            if (t < ntask && (t & Cm) != Cm) sts_i32(scr + 4 * t, top[k]);
           }
           __syncthreads();
           int any = 0;
 #pragma unroll
-          for (int k = 0; k < kTasksPerThread; ++k) {
+          for (int k = 0; k < TPT; ++k) {
             const u32 t = tid + k * nthr;
             if (t < ntask) {
               const u32 i = t & Cm;
-              const int in = i ? lds_s8(scr + t - 1) : 0;
-              const int e = in ? ch_add_small(w[k], in) : 0;
+              const int in = i ? lds_i32(scr + 4 * (t - 1)) : 0;
+              const int e = in ? ch_add_small<CW>(w[k], in) : 0;
               if (i == Cm) {
                 top[k] += e;
               } else {
@@ -463,23 +719,45 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
           if (!__syncthreads_or(any)) break;
         }
       }
+      // resolved chunks back into their (now free) slots, then a coalesced
+      // copy of whole elements to HBM (full 32-byte sectors per request)
 #pragma unroll
-      for (int k = 0; k < kTasksPerThread; ++k) {
+      for (int k = 0; k < TPT; ++k) {
         const u32 t = tid + k * nthr;
         if (t < ntask) {
-          const u32 i = t & Cm;
-          std::uint8_t* g = gbase + (b0 + (t >> logC)) * gstride;
-          __stcg(reinterpret_cast<uint4*>(g) + i, make_uint4(w[k].w[0], w[k].w[1], w[k].w[2], w[k].w[3]));
-          if (i == Cm) __stcg(reinterpret_cast<long long*>(g + W4), (long long)top[k]);
+          const u32 i = t & Cm, sw = (b0 + (t >> logC)) * SB;
+          sts_ch<CW>(sw, i, C, w[k]);
+          if (i == Cm) sts_i32(sw + W4, top[k]);
         }
       }
-      __syncthreads();  // scratch and s_rot reuse
+      __syncthreads();
+      {
+        const u32 q16 = A.D >> 2, lq = logC + (u32)__ffs(CW / 4) - 1;
+        constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
+        const u32 total = nb << lq;
+        for (u32 idx = tid; idx < total; idx += nthr) {
+          const u32 x = idx >> lq, pp = idx & (q16 - 1);
+          const u32 i = pp >> lpc, kk = pp & ((1u << lpc) - 1);
+          const uint4 v = *reinterpret_cast<const uint4*>(g_sm + piece_off((b0 + x) * SB, i, kk, C));
+          __stcg(reinterpret_cast<uint4*>(gbase + (b0 + x) * gstride) + pp, v);
+        }
+        for (u32 x = tid; x < nb; x += nthr)
+          __stcg(reinterpret_cast<long long*>(gbase + (b0 + x) * gstride + W4),
+                 (long long)lds_i32((b0 + x) * SB + W4));
+      }
+      __syncthreads();  // scratch, s_rot and slot reuse
+      // this leaf is out of shared memory: prefetch the next leaf's inputs now
+      // (if its dependency is already met) so they overlap our HBM stores
+      if (last && have_next && s_ready) {
+        issue_load<CW>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+        next_issued = true;
+      }
+      pc.mark(PH_STORE);
     }
-    __threadfence();
-    __syncthreads();
+    // publish completion: bump the phase counter; the last child of a node's
+    // last phase finishes the node and reports to the parent phase in turn
     if (tid == 0 && lf.comp != kNoDep) {
-      // bump the phase counter; the last child of a node's last phase
-      // finishes the node and reports to the parent phase in turn
+      __threadfence();
       u32 k = lf.comp;
       for (;;) {
         const u32 old = atomicAdd(&A.counters[1 + k], 1u);
@@ -489,7 +767,20 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
         k = cm.next;
       }
     }
+    if (have_next && !next_issued) {
+      if (tid == 0) {
+        const DevLeaf& nl = s_lf[nxt];
+        if (nl.dep != kNoDep)
+          while (ld_acquire(&A.counters[1 + nl.dep]) < nl.dep_target) __nanosleep(64);
+      }
+      __syncthreads();
+      issue_load<CW>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+    }
+    pc.mark(PH_WAIT);
+    cur = nxt;
   }
+  pc.mark(PH_WAIT);
+  pc.flush(A.prof);
 }
 
 // Final canonicalisation: value = lo + hi*2^N == lo - hi -> [0, 2^N].
