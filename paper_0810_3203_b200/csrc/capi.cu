@@ -40,7 +40,7 @@ int fail(int code, const std::string& msg) {
 
 constexpr size_t kSmemBudget = 196 * 1024;  // per-CTA dynamic shared memory for leaf slots
 // Fermat carry scratch: one int per (thread x task) of a store batch
-inline size_t scratch_bytes(u32 cw) { return (size_t)fermat::kThreads * (fermat::kWordsPerThread / cw) * 4; }
+inline size_t scratch_bytes(u32 nt) { return (size_t)nt * 4; }
 
 // A plan resident on one device.
 struct DevicePlan {
@@ -69,6 +69,7 @@ struct cftft_ring {
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
   u32 CW = 16;
+  u32 NT = 512;  // Fermat CTA size: 512 (1 CTA/SM) or 256 (2 CTAs/SM, half-size leaves)
   u32 slot_bytes = 0;   // shared-memory bytes per slot
   u64 elem_bytes = 0;   // minimal element stride
   unsigned max_leaf_ell = 1;
@@ -100,6 +101,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.nlevels = (u32)c.level_begin.size() - 1;
     d.level_begin = (u32)levels.size();
     u32 op0 = (u32)ops.size();
+    d.op_begin = op0;
+    d.nops = (u32)c.ops.size();
     for (u32 x : c.level_begin) levels.push_back(op0 + x);
     ops.insert(ops.end(), c.ops.begin(), c.ops.end());
     d.pre_begin = (u32)rots.size();
@@ -235,7 +238,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
     const size_t slots_bytes = (size_t)R->slot_bytes << dp.max_ell;
-    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->CW) : 0);
+    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
     unsigned grid = 1;
     if (R->kind == CFTFT_RING_FERMAT) {
       fermat::Args A{};
@@ -263,14 +266,15 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * fermat::PH_N, st));
       }
       A.prof = prof;
-      auto go = [&](auto kernel) -> int {
+      auto go = [&](auto kernel, int nt) -> int {
         if (int rc = set_smem(kernel)) return rc;
-        if (int rc = grid_for(kernel, fermat::kThreads, smem, dp.nleaves, &grid)) return rc;
-        kernel<<<grid, fermat::kThreads, smem, st>>>(A);
+        if (int rc = grid_for(kernel, nt, smem, dp.nleaves, &grid)) return rc;
+        kernel<<<grid, nt, smem, st>>>(A);
         return CFTFT_OK;
       };
-      int rc = R->CW == 16 ? go(fermat::leaf_kernel<16>) : R->CW == 8 ? go(fermat::leaf_kernel<8>)
-                                                                     : go(fermat::leaf_kernel<4>);
+      int rc = R->CW == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
+               : R->CW == 8 ? go(fermat::leaf_kernel<8, 512>, 512)
+                            : go(fermat::leaf_kernel<4, 512>, 512);
       if (rc) return rc;
       if (prof) {
         unsigned long long h[fermat::PH_N];
@@ -438,7 +442,12 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   }
   // largest leaf whose slots fit the shared-memory budget (and the 16-bit slot ids)
   unsigned lam = 1;
-  const size_t budget = kSmemBudget - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->CW) : 0);
+  if (kind == CFTFT_RING_FERMAT) {
+    const char* e = getenv("CFTFT_CTAS_PER_SM");
+    if (e && atoi(e) == 2 && R->CW == 16 && R->C <= 256) R->NT = 256;
+  }
+  const size_t per_cta = R->NT == 256 ? 96 * 1024 + scratch_bytes(R->NT) : kSmemBudget;
+  const size_t budget = per_cta - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
   while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= budget) ++lam;
   R->max_leaf_ell = lam;
   R->max_leaf_fit = lam;

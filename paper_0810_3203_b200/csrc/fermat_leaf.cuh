@@ -31,7 +31,7 @@
 namespace cftft_b200 {
 namespace fermat {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;  // default CTA size (the 2-CTA/SM variant uses 256)
 constexpr u32 kMaxBatch = 256;    // ops (or slots) staged per batch
 constexpr u32 kWordsPerThread = 32;  // live words per thread per batch
 
@@ -345,21 +345,14 @@ __device__ __forceinline__ int small_shifted(Ch<CW>& P, int p, u32 o) {
   return (ow == CW - 1) ? (int)(pw >> 32) : (int)ext;
 }
 
-// Chunk i of omega^r * x as (B, tb, neg): value = (-1)^neg (B + tb 2^CB).
-// xw: smem offset of x's chunks, xt: of its tops.
+// Unaligned part of rot_chunk (the rotation is not a whole number of
+// chunks): kept out of line so the hot aligned paths keep their registers.
+// word g of the output takes source bits [32g - t, 32g + 32 - t) (mod N);
+// words below t wrap past 2^N (negative).
 template <int CW>
-__device__ __forceinline__ bool rot_chunk(Ch<CW>& B, int& tb, u32 xw, u32 xt, const Rot& R, u32 Cm,
-                                          u32 i) {
+__device__ __noinline__ bool rot_chunk_unaligned(Ch<CW>& B, int& tb, u32 xw, u32 xt, Rot R, u32 Cm, u32 i) {
   const u32 C = Cm + 1;
   const u32 j = (i - R.q) & Cm;
-  if (R.o == 0) {  // whole chunks: (chunk, top) pairs move together
-    lds_ch(B, xw, j, C);
-    tb = lds_i32(xt + 4 * j);
-    return ((i < R.q) ? 1u : 0u) != R.sneg;
-  }
-  // unaligned: word g of the output takes source bits [32g - t, 32g + 32 - t)
-  // (mod N); words below t wrap past 2^N (negative).  Read the CW+1 source
-  // words of the window straight from shared memory.
   const u32 jm = (j - 1) & Cm;
   const u32 ow = R.o >> 5, sh = R.o & 31;
   Ch<CW> lo, hi;
@@ -391,6 +384,20 @@ __device__ __forceinline__ bool rot_chunk(Ch<CW>& B, int& tb, u32 xw, u32 xt, co
   return R.sneg != 0;
 }
 
+// Chunk i of omega^r * x as (B, tb, neg): value = (-1)^neg (B + tb 2^CB).
+// xw: smem offset of x's chunks, xt: of its tops.
+template <int CW>
+__device__ __forceinline__ bool rot_chunk(Ch<CW>& B, int& tb, u32 xw, u32 xt, const Rot& R, u32 Cm,
+                                          u32 i) {
+  if (R.o == 0) {  // whole chunks: (chunk, top) pairs move together
+    const u32 j = (i - R.q) & Cm;
+    lds_ch(B, xw, j, Cm + 1);
+    tb = lds_i32(xt + 4 * j);
+    return ((i < R.q) ? 1u : 0u) != R.sneg;
+  }
+  return rot_chunk_unaligned<CW>(B, tb, xw, xt, R, Cm, i);
+}
+
 // Exact form of (-1)^neg (B + tb 2^CB): chunk W and top.
 template <int CW>
 __device__ __forceinline__ int exact_from(Ch<CW>& W, int tb, bool neg) {
@@ -401,7 +408,7 @@ __device__ __forceinline__ int exact_from(Ch<CW>& W, int tb, bool neg) {
   return ch_add_small(W, 1) - tb - 1;
 }
 
-// Per-op parameters staged in shared memory once per batch.
+// Per-op parameters staged in shared memory.
 struct OpT {
   u32 aw, bw;  // smem offsets of slot a / slot b (tops at +W4)
   u32 q, o;
@@ -426,36 +433,97 @@ constexpr u32 kCacheOps = 256;
 constexpr u32 kCacheLev = 64;
 constexpr u32 kCacheRot = 512;  // pre + post rotations
 
-// Issues the cp.async loads of a leaf's input slots and initialises their
-// tops (the element's signed top word sits on top of the last chunk).
+// Chunk-i piece offsets (within a slot) for the thread's fixed chunk.
 template <int CW>
+struct Offs {
+  u32 o[CW / 4];
+  __device__ __forceinline__ void init(u32 i, u32 C) {
+#pragma unroll
+    for (int k = 0; k < CW / 4; ++k) o[k] = piece_off(0, i, k, C);
+  }
+};
+template <int CW>
+__device__ __forceinline__ void lds_at(Ch<CW>& c, u32 slot, const Offs<CW>& f) {
+#pragma unroll
+  for (int k = 0; k < CW; k += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(g_sm + slot + f.o[k / 4]);
+    c.w[k] = v.x;
+    c.w[k + 1] = v.y;
+    c.w[k + 2] = v.z;
+    c.w[k + 3] = v.w;
+  }
+}
+template <int CW>
+__device__ __forceinline__ void sts_at(u32 slot, const Offs<CW>& f, const Ch<CW>& c) {
+#pragma unroll
+  for (int k = 0; k < CW; k += 4)
+    *reinterpret_cast<uint4*>(g_sm + slot + f.o[k / 4]) = make_uint4(c.w[k], c.w[k + 1], c.w[k + 2], c.w[k + 3]);
+}
+
+// Moves whole elements between HBM and shared memory (piece-major swizzled
+// slots), 16 bytes per thread per step, coalesced on the HBM side.  Element
+// x of the range lives at g0 + x*gstride and in slot (s0 + x), x < nslots.
+// The per-thread piece positions are fixed, so the loop body is a couple of
+// adds (no division, no 64-bit multiply).
+template <int CW, bool kLoad, int NT>
+__device__ __forceinline__ void copy_slots(const Args& A, std::uint8_t* g0, u64 gstride, u32 s0, u32 nslots,
+                                           u32 smem_base, u32 tid) {
+  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
+  const u32 C = A.C, SB = A.slot_bytes;
+  const u32 lq = A.logC + lpc, q16 = 1u << lq;  // pieces per slot
+  if (q16 >= (u32)NT) {
+    // each thread copies pieces tid, tid+NT, ... of every slot
+    for (u32 pp = tid; pp < q16; pp += NT) {
+      const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
+      std::uint8_t* g = g0 + 16u * pp;
+      u32 so = s0 * SB + so0;
+      for (u32 x = 0; x < nslots; ++x, g += gstride, so += SB) {
+        if (kLoad)
+          cp_async16(smem_base + so, g);
+        else
+          __stcg(reinterpret_cast<uint4*>(g), *reinterpret_cast<const uint4*>(g_sm + so));
+      }
+    }
+  } else {
+    // NT/q16 slots side by side; each thread keeps one piece position
+    const u32 pp = tid & (q16 - 1), x0 = tid >> lq, step = (u32)NT >> lq;
+    const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
+    std::uint8_t* g = g0 + (u64)x0 * gstride + 16u * pp;
+    const u64 gstep = (u64)step * gstride;
+    u32 so = (s0 + x0) * SB + so0;
+    for (u32 x = x0; x < nslots; x += step, g += gstep, so += step * SB) {
+      if (kLoad)
+        cp_async16(smem_base + so, g);
+      else
+        __stcg(reinterpret_cast<uint4*>(g), *reinterpret_cast<const uint4*>(g_sm + so));
+    }
+  }
+}
+
+// Issues the cp.async loads of slots [s0, s1) of a leaf's inputs (s1 capped
+// at nload) and initialises their tops (the element's signed top word sits
+// on top of the last chunk).
+template <int CW, int NT>
 __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 tid) {
-  constexpr u32 nthr = kThreads;
-  const u32 C = A.C, Cm = C - 1, logC = A.logC, SB = A.slot_bytes, W4 = 4 * A.D;
+                                           u32 tid, u32 s0 = 0, u32 s1 = 0xFFFFFFFFu) {
+  const u32 Cm = A.C - 1, SB = A.slot_bytes, W4 = 4 * A.D;
+  s1 = min(s1, cl.nload);
+  if (s0 >= s1) return;
   std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
   const u64 gstride = lf.stride * A.elem_bytes;
-  const u32 q16 = A.D >> 2, lq = logC + (u32)__ffs(CW / 4) - 1;  // 16-byte pieces per slot
-  const u32 total = cl.nload << lq;
-  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
-  for (u32 idx = tid; idx < total; idx += nthr) {
-    const u32 s = idx >> lq, pp = idx & (q16 - 1);
-    const u32 i = pp >> lpc, k = pp & ((1u << lpc) - 1);
-    cp_async16(smem_base + piece_off(s * SB, i, k, C), gbase + s * gstride + 16 * (u64)pp);
-  }
-  const u32 ttot = cl.nload << logC;
-  for (u32 idx = tid; idx < ttot; idx += nthr) {
-    const u32 s = idx >> logC, c = idx & Cm;
+  copy_slots<CW, true, NT>(A, gbase + (u64)s0 * gstride, gstride, s0, s1 - s0, smem_base, tid);
+  const u32 ttot = (s1 - s0) << A.logC;
+  for (u32 idx = tid; idx < ttot; idx += NT) {
+    const u32 s = s0 + (idx >> A.logC), c = idx & Cm;
     int v = 0;
     if (c == Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4));
     sts_i32(s * SB + W4 + 4 * c, v);
   }
 }
 
-template <int CW>
-__global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
-  constexpr u32 CBY = 4 * CW;
-  constexpr int TPT = kWordsPerThread / CW;  // tasks per thread per batch
+template <int CW, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) leaf_kernel(Args A) {
+  constexpr int TPT = 2;  // ops per thread per round (each a CW-word chunk)
   __shared__ u32 s_tk[2];
   __shared__ DevLeaf s_lf[2];
   __shared__ DevClass s_cl[2];
@@ -466,12 +534,16 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
   __shared__ SymExp s_crot[kCacheRot];
   __shared__ Rot s_rot[kMaxBatch];
   const u32 tid = threadIdx.x;
-  constexpr u32 nthr = kThreads;
+  constexpr u32 nthr = NT;
   const u32 C = A.C, Cm = C - 1, logC = A.logC;
   const u32 SB = A.slot_bytes, W4 = 4 * A.D;
   const u32 scr = A.scratch_off;
   const u32 smem_base = (u32)__cvta_generic_to_shared(g_sm);
-  const u32 per_batch = min(kMaxBatch, max(1u, (nthr * TPT) >> logC));
+  // fixed thread geometry: chunk i of group g; G groups work side by side
+  const u32 i = tid & Cm, g = tid >> logC, G = nthr >> logC;
+  Offs<CW> fi;
+  fi.init(i, C);
+  const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
   PhaseClock pc;
   pc.start(tid == 0 && A.prof != nullptr);
 
@@ -488,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
     s_cached = 0xFFFFFFFFu;
   }
   __syncthreads();
-  if (s_tk[0] < A.nleaves) issue_load<CW>(A, s_lf[0], s_cl[0], smem_base, tid);
+  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, tid);
   u32 cur = 0;
 
   for (;;) {
@@ -510,11 +582,10 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
       }
     }
     // leaf-program cache
-    const u32 nops = A.levels[cl.level_begin + cl.nlevels] - A.levels[cl.level_begin];
-    const bool cached = nops <= kCacheOps && cl.nlevels <= kCacheLev && cl.nload + cl.nstore <= kCacheRot;
+    const bool cached = cl.nops <= kCacheOps && cl.nlevels <= kCacheLev && cl.nload + cl.nstore <= kCacheRot;
     if (cached && s_cached != lf.cls) {
-      const u32 op0 = A.levels[cl.level_begin];
-      for (u32 x = tid; x < nops; x += nthr) {
+      const u32 op0 = cl.op_begin;
+      for (u32 x = tid; x < cl.nops; x += nthr) {
         const DevOp op = A.ops[op0 + x];
         const Rot R = make_rot<CW>(op.r, A.N);
         s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
@@ -530,66 +601,52 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
     std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
     const u64 gstride = lf.stride * A.elem_bytes;
 
-    // ---- pre-rotations (ITFT spectral inputs), in place through registers ---
+    // ---- pre-rotations (ITFT spectral inputs), in place: G slots per round -------
     if (cl.has_pre) {
-      for (u32 b0 = 0; b0 < cl.nload; b0 += per_batch) {
-        const u32 nb = min(cl.nload - b0, per_batch);
-        for (u32 x = tid; x < nb; x += nthr) {
-          const SymExp P = cached ? s_crot[b0 + x] : A.rots[cl.pre_begin + b0 + x];
-          s_rot[x] = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
+      for (u32 b0 = 0; b0 < cl.nload; b0 += G) {
+        const u32 sl = b0 + g;
+        const bool act = sl < cl.nload;
+        Ch<CW> w;
+        int tp = 0;
+        if (act) {
+          const SymExp P = cached ? s_crot[sl] : A.rots[cl.pre_begin + sl];
+          const Rot R = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
+          const bool neg = rot_chunk<CW>(w, tp, sl * SB, sl * SB + W4, R, Cm, i);
+          tp = exact_from<CW>(w, tp, neg);
         }
         __syncthreads();
-        const u32 ntask = nb << logC;
-        Ch<CW> w[TPT];
-        int tp[TPT];
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          const u32 t = tid + k * nthr;
-          if (t < ntask) {
-            const u32 x = t >> logC, i = t & Cm, sw = (b0 + x) * SB;
-            const bool neg = rot_chunk<CW>(w[k], tp[k], sw, sw + W4, s_rot[x], Cm, i);
-            tp[k] = exact_from<CW>(w[k], tp[k], neg);
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < TPT; ++k) {
-          const u32 t = tid + k * nthr;
-          if (t < ntask) {
-            const u32 i = t & Cm, sw = (b0 + (t >> logC)) * SB;
-            sts_ch<CW>(sw, i, C, w[k]);
-            sts_i32(sw + W4 + 4 * i, tp[k]);
-          }
+        if (act) {
+          sts_at<CW>(sl * SB, fi, w);
+          sts_i32(sl * SB + ti, tp);
         }
         __syncthreads();
       }
     }
     pc.mark(PH_PRE);
 
-    // ---- micro-op levels ------------------------------------------------------
+    // ---- micro-op levels: each thread runs chunk i of up to TPT ops per round ----
     for (u32 l = 0; l < cl.nlevels; ++l) {
       u32 o0, o1;
       if (cached) {
         o0 = s_lev[l];
         o1 = s_lev[l + 1];
       } else {
-        o0 = A.levels[cl.level_begin + l];
-        o1 = A.levels[cl.level_begin + l + 1];
+        o0 = A.levels[cl.level_begin + l] - cl.op_begin;
+        o1 = A.levels[cl.level_begin + l + 1] - cl.op_begin;
       }
-      for (u32 ob = o0; ob < o1; ob += per_batch) {
-        const u32 nb = min(o1 - ob, per_batch);
+      for (u32 ob = o0; ob < o1; ob += G * TPT) {
+        const u32 nb = min(o1 - ob, G * TPT);
         u32 sbase = ob;
-        if (!cached) {  // stage this batch's ops
+        if (!cached) {  // stage this round's ops
           for (u32 x = tid; x < nb; x += nthr) {
-            const DevOp op = A.ops[ob + x];
+            const DevOp op = A.ops[cl.op_begin + ob + x];
             const Rot R = make_rot<CW>(op.r, A.N);
             s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
           }
           __syncthreads();
           sbase = 0;
         }
-        const u32 ntask = nb << logC;
-        // out0 goes to slot a in place right away (only this task reads a's
+        // out0 goes to slot a in place right away (only this thread reads a's
         // chunk i); out1 goes to slot b after the barrier (b is read rotated)
         Ch<CW> hold[TPT];
         int htop[TPT];
@@ -597,14 +654,12 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
 #pragma unroll
         for (int k = 0; k < TPT; ++k) {
           hdst[k] = 0xFFFFFFFFu;
-          const u32 t = tid + k * nthr;
-          if (t >= ntask) continue;
-          const OpT op = s_ops[sbase + (t >> logC)];
-          const u32 i = t & Cm;
-          const u32 ta = op.aw + W4 + 4 * i;
+          const u32 x = g + G * k;
+          if (x >= nb) continue;
+          const OpT op = s_ops[sbase + x];
           Ch<CW> a;
-          lds_ch(a, op.aw, i, C);
-          const int pa = lds_i32(ta);
+          lds_at(a, op.aw, fi);
+          const int pa = lds_i32(op.aw + ti);
           if (op.type == OP_COPY) {
             hold[k] = a;
             htop[k] = pa;
@@ -613,7 +668,15 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
           }
           Ch<CW> b;
           int pb;
-          const bool neg = rot_chunk<CW>(b, pb, op.bw, op.bw + W4, Rot{op.q, op.o, op.sneg}, Cm, i);
+          bool neg;
+          if (op.o == 0) {  // whole-chunk rotation: the common case inside a leaf
+            const u32 j = (i - op.q) & Cm;
+            lds_ch(b, op.bw, j, C);
+            pb = lds_i32(op.bw + W4 + 4 * j);
+            neg = ((i < op.q) ? 1u : 0u) != op.sneg;
+          } else {
+            neg = rot_chunk<CW>(b, pb, op.bw, op.bw + W4, Rot{op.q, op.o, op.sneg}, Cm, i);
+          }
           Ch<CW> y0;
           int t0, t1;
           // y0 = a + s b, y1 = a - s b with s = (-1)^neg
@@ -627,8 +690,8 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
           if (op.type == OP_SUB2 || op.type == OP_SUB2DIFF) {  // y0 = a + y1 = 2a - s b
             t0 = ch_add(y0, a, hold[k]) + pa + t1;
           }
-          sts_ch<CW>(op.aw, i, C, y0);
-          sts_i32(ta, t0);
+          sts_at<CW>(op.aw, fi, y0);
+          sts_i32(op.aw + ti, t0);
           if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF) {
             htop[k] = t1;
             hdst[k] = op.bw;
@@ -638,9 +701,8 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
 #pragma unroll
         for (int k = 0; k < TPT; ++k) {
           if (hdst[k] != 0xFFFFFFFFu) {
-            const u32 i = (tid + k * nthr) & Cm;
-            sts_ch<CW>(hdst[k], i, C, hold[k]);
-            sts_i32(hdst[k] + W4 + 4 * i, htop[k]);
+            sts_at<CW>(hdst[k], fi, hold[k]);
+            sts_i32(hdst[k] + ti, htop[k]);
           }
         }
         __syncthreads();
@@ -648,108 +710,82 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
     }
     pc.mark(PH_LEVELS);
 
-    // ---- post-rotation + carry resolution + store, fused ------------------------
+    // ---- post-rotation + carry resolution + store: G slots per round -------------
     const bool have_next = s_tk[nxt] < A.nleaves;
     bool next_issued = false;
-    for (u32 b0 = 0; b0 < cl.nstore; b0 += per_batch) {
-      const u32 nb = min(cl.nstore - b0, per_batch);
+    for (u32 b0 = 0; b0 < cl.nstore; b0 += G) {
+      const u32 nb = min(cl.nstore - b0, G);
       const bool last = b0 + nb >= cl.nstore;
-      for (u32 x = tid; x < nb; x += nthr) {
-        const SymExp P = cached ? s_crot[cl.nload + b0 + x] : A.rots[cl.post_begin + b0 + x];
-        s_rot[x] = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
-      }
-      __syncthreads();
-      const u32 ntask = nb << logC;
-      Ch<CW> w[TPT];
-      int top[TPT];
-#pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        const u32 t = tid + k * nthr;
-        if (t < ntask) {
-          const u32 x = t >> logC, i = t & Cm, sw = (b0 + x) * SB;
-          const bool neg = rot_chunk<CW>(w[k], top[k], sw, sw + W4, s_rot[x], Cm, i);
-          top[k] = exact_from<CW>(w[k], top[k], neg);
-          sts_i32(scr + 4 * t, top[k]);
+      const u32 sl = b0 + g;
+      const bool act = g < nb;
+      Ch<CW> w;
+      int top = 0;
+      if (act) {
+        const SymExp P = cached ? s_crot[cl.nload + sl] : A.rots[cl.post_begin + sl];
+        const Rot R = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
+        bool neg;
+        if (R.o == 0) {
+          const u32 j = (i - R.q) & Cm;
+          lds_ch(w, sl * SB, j, C);
+          top = lds_i32(sl * SB + W4 + 4 * j);
+          neg = ((i < R.q) ? 1u : 0u) != R.sneg;
+        } else {
+          neg = rot_chunk<CW>(w, top, sl * SB, sl * SB + W4, R, Cm, i);
         }
+        top = exact_from<CW>(w, top, neg);
+        sts_i32(scr + 4 * tid, top);
       }
       __syncthreads();
       pc.mark(PH_POST);
       // fold in the top of the chunk below (one step); carries that ripple
       // further (a chunk of all ones / all zeros) take the slow path
       int rare = 0;
-#pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        const u32 t = tid + k * nthr;
-        if (t < ntask) {
-          const u32 i = t & Cm;
-          const int in = i ? lds_i32(scr + 4 * (t - 1)) : 0;
-          const int e = in ? ch_add_small<CW>(w[k], in) : 0;
-          if (i == Cm) {
-            top[k] += e;
-          } else {
-            if (e) rare = 1;
-            top[k] = e;  // carry still owed to chunk i+1
-          }
+      if (act) {
+        const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
+        const int e = in ? ch_add_small<CW>(w, in) : 0;
+        if (i == Cm) {
+          top += e;
+        } else {
+          if (e) rare = 1;
+          top = e;  // carry still owed to chunk i+1
         }
       }
       if (__syncthreads_or(rare)) {
         for (;;) {
-#pragma unroll
-          for (int k = 0; k < TPT; ++k) {
-            const u32 t = tid + k * nthr;
-            if (t < ntask && (t & Cm) != Cm) sts_i32(scr + 4 * t, top[k]);
-          }
+          if (act && i != Cm) sts_i32(scr + 4 * tid, top);
           __syncthreads();
           int any = 0;
-#pragma unroll
-          for (int k = 0; k < TPT; ++k) {
-            const u32 t = tid + k * nthr;
-            if (t < ntask) {
-              const u32 i = t & Cm;
-              const int in = i ? lds_i32(scr + 4 * (t - 1)) : 0;
-              const int e = in ? ch_add_small<CW>(w[k], in) : 0;
-              if (i == Cm) {
-                top[k] += e;
-              } else {
-                if (e) any = 1;
-                top[k] = e;
-              }
+          if (act) {
+            const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
+            const int e = in ? ch_add_small<CW>(w, in) : 0;
+            if (i == Cm) {
+              top += e;
+            } else {
+              if (e) any = 1;
+              top = e;
             }
           }
           if (!__syncthreads_or(any)) break;
         }
       }
-      // resolved chunks back into their (now free) slots, then a coalesced
-      // copy of whole elements to HBM (full 32-byte sectors per request)
-#pragma unroll
-      for (int k = 0; k < TPT; ++k) {
-        const u32 t = tid + k * nthr;
-        if (t < ntask) {
-          const u32 i = t & Cm, sw = (b0 + (t >> logC)) * SB;
-          sts_ch<CW>(sw, i, C, w[k]);
-          if (i == Cm) sts_i32(sw + W4, top[k]);
-        }
+      // resolved chunks back into their (free) slots, then a coalesced copy
+      // of whole elements to HBM (full 32-byte sectors per request)
+      if (act) {
+        sts_at<CW>(sl * SB, fi, w);
+        if (i == Cm) sts_i32(sl * SB + W4, top);
       }
       __syncthreads();
-      {
-        const u32 q16 = A.D >> 2, lq = logC + (u32)__ffs(CW / 4) - 1;
-        constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
-        const u32 total = nb << lq;
-        for (u32 idx = tid; idx < total; idx += nthr) {
-          const u32 x = idx >> lq, pp = idx & (q16 - 1);
-          const u32 i = pp >> lpc, kk = pp & ((1u << lpc) - 1);
-          const uint4 v = *reinterpret_cast<const uint4*>(g_sm + piece_off((b0 + x) * SB, i, kk, C));
-          __stcg(reinterpret_cast<uint4*>(gbase + (b0 + x) * gstride) + pp, v);
-        }
-        for (u32 x = tid; x < nb; x += nthr)
-          __stcg(reinterpret_cast<long long*>(gbase + (b0 + x) * gstride + W4),
-                 (long long)lds_i32((b0 + x) * SB + W4));
-      }
-      __syncthreads();  // scratch, s_rot and slot reuse
-      // this leaf is out of shared memory: prefetch the next leaf's inputs now
-      // (if its dependency is already met) so they overlap our HBM stores
-      if (last && have_next && s_ready) {
-        issue_load<CW>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+      copy_slots<CW, false, NT>(A, gbase + (u64)b0 * gstride, gstride, b0, nb, smem_base, tid);
+      for (u32 x = tid; x < nb; x += nthr)
+        __stcg(reinterpret_cast<long long*>(gbase + (b0 + x) * gstride + W4),
+               (long long)lds_i32((b0 + x) * SB + W4));
+      __syncthreads();  // scratch and slot reuse
+      // slots [0, b0 + nb) are out of shared memory now: if the next leaf's
+      // dependency is already met, stream its inputs into them while we keep
+      // computing and storing the remaining slots
+      if (have_next && s_ready) {
+        const u32 lo = b0 == 0 ? 0 : b0, hi = last ? 0xFFFFFFFFu : b0 + nb;
+        issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, lo, hi);
         next_issued = true;
       }
       pc.mark(PH_STORE);
@@ -774,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 1) leaf_kernel(Args A) {
           while (ld_acquire(&A.counters[1 + nl.dep]) < nl.dep_target) __nanosleep(64);
       }
       __syncthreads();
-      issue_load<CW>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
     }
     pc.mark(PH_WAIT);
     cur = nxt;

@@ -81,6 +81,8 @@ struct DevClass {
   u32 pre_begin;    // index into rotation table: nload pre-rotations
   u32 post_begin;   // index into rotation table: nstore post-rotations
   u32 has_pre;      // any nonzero pre-rotation coefficient
+  u32 op_begin;     // first op of the class in the op table
+  u32 nops;         // number of ops
 };
 
 constexpr u32 kNoDep = 0xFFFFFFFFu;
