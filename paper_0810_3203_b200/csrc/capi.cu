@@ -266,6 +266,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * fermat::PH_N, st));
       }
       A.prof = prof;
+      static const u32 dbg = getenv("CFTFT_DEBUG_SKIP") ? (u32)atoi(getenv("CFTFT_DEBUG_SKIP")) : 0u;
+      A.debug_skip = dbg;
       auto go = [&](auto kernel, int nt) -> int {
         if (int rc = set_smem(kernel)) return rc;
         if (int rc = grid_for(kernel, nt, smem, dp.nleaves, &grid)) return rc;
@@ -273,7 +275,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         return CFTFT_OK;
       };
       int rc = R->CW == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
-               : R->CW == 8 ? go(fermat::leaf_kernel<8, 512>, 512)
+               : R->CW == 8 ? (R->NT == 1024 ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
                             : go(fermat::leaf_kernel<4, 512>, 512);
       if (rc) return rc;
       if (prof) {
@@ -445,6 +447,13 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   if (kind == CFTFT_RING_FERMAT) {
     const char* e = getenv("CFTFT_CTAS_PER_SM");
     if (e && atoi(e) == 2 && R->CW == 16 && R->C <= 256) R->NT = 256;
+    const char* wv = getenv("CFTFT_WIDE");  // experiment: 1024 threads, 256-bit chunks
+    if (wv && atoi(wv) == 1 && R->D >= 16) {
+      R->CW = 8;
+      R->C = R->D / 8;
+      R->slot_bytes = (4 * R->D + 4 * R->C + 15) & ~15u;
+      R->NT = 1024;
+    }
   }
   const size_t per_cta = R->NT == 256 ? 96 * 1024 + scratch_bytes(R->NT) : kSmemBudget;
   const size_t budget = per_cta - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);

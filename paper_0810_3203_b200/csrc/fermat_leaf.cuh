@@ -52,6 +52,7 @@ struct Args {
   u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
   unsigned long long* prof;  // optional per-phase cycle totals (CFTFT_PROFILE=1)
+  u32 debug_skip;            // perf experiments only (CFTFT_DEBUG_SKIP): 1 = levels, 2 = post maths
 };
 
 // Phase timing (debug): thread 0 of each CTA accumulates clock64 deltas.
@@ -522,7 +523,7 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
 }
 
 template <int CW, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) leaf_kernel(Args A) {
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args A) {
   constexpr int TPT = 2;  // ops per thread per round (each a CW-word chunk)
   __shared__ u32 s_tk[2];
   __shared__ DevLeaf s_lf[2];
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) leaf_kernel(Args A) {
     pc.mark(PH_PRE);
 
     // ---- micro-op levels: each thread runs chunk i of up to TPT ops per round ----
-    for (u32 l = 0; l < cl.nlevels; ++l) {
+    for (u32 l = 0; l < ((A.debug_skip & 1) ? 0u : cl.nlevels); ++l) {
       u32 o0, o1;
       if (cached) {
         o0 = s_lev[l];
@@ -720,7 +721,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) leaf_kernel(Args A) {
       const bool act = g < nb;
       Ch<CW> w;
       int top = 0;
-      if (act) {
+      if (act && (A.debug_skip & 2)) {
+        lds_at(w, sl * SB, fi);
+        sts_i32(scr + 4 * tid, 0);
+      } else if (act) {
         const SymExp P = cached ? s_crot[cl.nload + sl] : A.rots[cl.post_begin + sl];
         const Rot R = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
         bool neg;
@@ -774,26 +778,26 @@ __global__ void __launch_bounds__(NT, 512 / NT) leaf_kernel(Args A) {
         sts_at<CW>(sl * SB, fi, w);
         if (i == Cm) sts_i32(sl * SB + W4, top);
       }
-      __syncthreads();
-      copy_slots<CW, false, NT>(A, gbase + (u64)b0 * gstride, gstride, b0, nb, smem_base, tid);
-      for (u32 x = tid; x < nb; x += nthr)
-        __stcg(reinterpret_cast<long long*>(gbase + (b0 + x) * gstride + W4),
-               (long long)lds_i32((b0 + x) * SB + W4));
-      __syncthreads();  // scratch and slot reuse
-      // slots [0, b0 + nb) are out of shared memory now: if the next leaf's
-      // dependency is already met, stream its inputs into them while we keep
-      // computing and storing the remaining slots
-      if (have_next && s_ready) {
-        const u32 lo = b0 == 0 ? 0 : b0, hi = last ? 0xFFFFFFFFu : b0 + nb;
-        issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, lo, hi);
-        next_issued = true;
-      }
+      __syncthreads();  // scratch reuse
       pc.mark(PH_STORE);
+      (void)last;
     }
+    // the whole leaf is resolved in shared memory: one coalesced copy to HBM
+    copy_slots<CW, false, NT>(A, gbase, gstride, 0, cl.nstore, smem_base, tid);
+    for (u32 x = tid; x < cl.nstore; x += nthr)
+      __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4), (long long)lds_i32(x * SB + W4));
+    __syncthreads();  // slot reuse
+    // this leaf is out of shared memory: if the next leaf's dependency is
+    // already met, stream its inputs in now so they overlap our HBM stores
+    if (have_next && s_ready) {
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+      next_issued = true;
+    }
+    pc.mark(PH_STORE);
     // publish completion: bump the phase counter; the last child of a node's
     // last phase finishes the node and reports to the parent phase in turn
     if (tid == 0 && lf.comp != kNoDep) {
-      __threadfence();
+      if (!(A.debug_skip & 4)) __threadfence();
       u32 k = lf.comp;
       for (;;) {
         const u32 old = atomicAdd(&A.counters[1 + k], 1u);
