@@ -226,6 +226,103 @@ def run_reference(args, cfgname):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, local):
+    """N GPUs: one config-5 transform partitioned over the ranks (column slabs
+    -> NCCL all-to-all -> row slabs).  Strong scaling."""
+    import numpy as np
+    import torch
+
+    from paper_0810_3203_b200.dist import DistTFT, GpuEngine
+
+    W = ctx.element_words
+    eng = GpuEngine(ctx)
+    M = 2 * N
+    fwd = DistTFT(eng, M, L, 0, z, n)
+    inv = DistTFT(eng, M, L, 0, n, n, 0)
+    g = fwd.g
+    rows_local = g.L1 * g.width(rank)
+    # this rank's column slab: seeded uniform limbs in rows < z1 + 1 (inputs)
+    rng = np.random.default_rng(po.mix_seed(42, 5 + rank))
+    host = np.zeros((rows_local, W), dtype=np.uint64)
+    live = min(rows_local, (g.z1 + 1) * g.width(rank))
+    host[:live, : N // 64] = rng.integers(0, 1 << 64, size=(live, N // 64), dtype=np.uint64, endpoint=False)
+    col = torch.from_numpy(host.view(np.int64)).cuda()
+    stream = torch.cuda.current_stream()
+    byts = tft_bytes(N, L, z, n) + itft_bytes(N, L, n, n, 0)
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        rows = fwd.tft(col)
+        inv.itft(rows, col)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = eng.launches
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = t.item()
+    value = byts * args.steps / (total_ms / 1e3) / 1e9
+    peak, peak_kind = hbm_peak()
+    # bytes this rank sends over NVLink per step (the two transposes + phase iii)
+    elem = ctx.element_bytes
+    xfer = (g.nrows(rank) * g.width(rank) * (world - 1) + g.zrows * g.width(rank) * (world - 1) // world) * elem
+    e2e = None
+    if not args.no_e2e:
+        pin = torch.from_numpy(host.view(np.int64)).pin_memory()
+        pout = torch.empty_like(pin).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        ek = max(1, min(args.steps, 3))
+        for _ in range(ek):
+            col.copy_(pin, non_blocking=True)
+            step()
+            pout.copy_(col, non_blocking=True)
+            torch.cuda.synchronize()
+        barrier()
+        tt = torch.tensor([(time.perf_counter() - t0) / ek], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": byts / tt.item() / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(pin.numel() * 8),
+               "d2h_bytes_per_step": int(pout.numel() * 8), "steps": ek,
+               "note": "per rank: pinned column slab in, round trip, column slab out"}
+    if rank == 0:
+        line = {
+            "metric": f"TFT+ITFT GB/s ({args.config}: {desc})",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: seeded uniform 64-bit limbs per rank slab (numpy PCG64)",
+            "config": {"workload": args.config, "ring": f"Z/(2^{N}+1)", "L": L, "z": z, "n": n,
+                       "coeff_bytes": N // 8, "algorithmic_bytes_per_step": byts,
+                       "parallelism": f"column/row slabs over {world} GPUs, NCCL all-to-all transpose",
+                       "l2": "inputs far exceed L2"},
+            "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
+                         "frac": value / world / peak, "peak_kind": peak_kind, "traffic": None,
+                         "per": "GPU", "nvlink_bytes_per_gpu_per_step": xfer,
+                         "nvlink_gbs_per_gpu": xfer / (total_ms / args.steps / 1e3) / 1e9,
+                         "nvlink_peak_gbs": 770.0},
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": eng.launches - l0,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -236,6 +333,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--leaf-limit", type=int, default=0, help="cap on-chip leaves at 2^k (tuning)")
+    ap.add_argument("--force-dist", action="store_true", help="use the multi-GPU path even on 1 rank (testing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -251,9 +349,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_dist:
         import torch.distributed as dist
 
+        if world == 1 and "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_0810_3203_b200 as cf
@@ -266,6 +366,9 @@ def main():
     if args.leaf_limit:
         ctx.set_leaf_limit(args.leaf_limit)
     W = ctx.element_words
+    if world > 1 or args.force_dist:
+        run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, local)
+        return
     host = make_input(N, L, z, W, po.mix_seed(42, 5 + rank))
     dev = torch.from_numpy(host.view(np.int64)).cuda()
     view = cf.DeviceView(dev)

@@ -105,6 +105,28 @@ int cftft_tft_host(const cftft_ring* ring, const cftft_params* params, void* hos
 int cftft_itft_host(const cftft_ring* ring, const cftft_params* params, void* host_base,
                     uint64_t elem_stride_bytes, int policy, uint64_t* base_case_count);
 
+/* One independent sub-transform of a batch (cftft_gpu_batch): a TFT or ITFT
+ * of `length` elements of the device view, element i at view index
+ * base + i*stride (the Bailey columns / rows of a distributed transform). */
+typedef struct cftft_subtransform {
+  uint64_t length, twiddle_exp, input_count, output_count;
+  int32_t want_next;
+  int32_t pad;
+  uint64_t base, stride;
+} cftft_subtransform;
+
+/* Runs `count` independent sub-transforms (all forward, or all inverse) of
+ * the view [dev_base, elem_stride_bytes] in ONE launch.  Outputs are left in
+ * the engine's lazy element format (limbs + signed top word) unless
+ * canonicalize != 0; cftft_gpu_canonicalize finishes them later.  Used by the
+ * multi-GPU column and row passes. */
+int cftft_gpu_batch(const cftft_ring* ring, int inverse, const cftft_subtransform* items, uint64_t count,
+                    void* dev_base, uint64_t elem_stride_bytes, int policy, int canonicalize, void* stream);
+
+/* Canonicalises x[0..count) (lazy engine format -> [0, 2^N]); Fermat only. */
+int cftft_gpu_canonicalize(const cftft_ring* ring, void* dev_base, uint64_t count,
+                           uint64_t elem_stride_bytes, void* stream);
+
 /* Pointwise ring products a[i] <- a[i] * b[i], i < count, on device views
  * (the pointwise stage of cftft::poly_mul, polymul.hpp:73-77). */
 int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,

@@ -82,6 +82,12 @@ class _Params(C.Structure):
                 ("output_count", C.c_uint64), ("want_next", C.c_int32)]
 
 
+class _Sub(C.Structure):
+    _fields_ = [("length", C.c_uint64), ("twiddle_exp", C.c_uint64), ("input_count", C.c_uint64),
+                ("output_count", C.c_uint64), ("want_next", C.c_int32), ("pad", C.c_int32),
+                ("base", C.c_uint64), ("stride", C.c_uint64)]
+
+
 _lib = None
 
 
@@ -107,6 +113,8 @@ def lib():
         for f in ("cftft_tft_host", "cftft_itft_host"):
             getattr(L, f).argtypes = [vp, P, vp, u64, C.c_int, C.POINTER(u64)]
         L.cftft_gpu_pointwise.argtypes = [vp, vp, vp, u64, u64, vp]
+        L.cftft_gpu_batch.argtypes = [vp, C.c_int, C.POINTER(_Sub), u64, vp, u64, C.c_int, C.c_int, vp]
+        L.cftft_gpu_canonicalize.argtypes = [vp, vp, u64, u64, vp]
         L.cftft_gpu_scale.argtypes = [vp, vp, u64, u64, u64, vp]
         L.cftft_tft_base_cases.argtypes = [u64, u64, u64, C.c_int]
         L.cftft_tft_base_cases.restype = u64
@@ -343,3 +351,26 @@ def plan_dump(ctx, inverse: bool, params: TransformParams, policy=SplitPolicy.ba
     buf = C.create_string_buffer(need)
     lib().cftft_plan_dump(ctx._h, 1 if inverse else 0, C.byref(p), int(policy), buf, need)
     return json.loads(buf.value.decode())
+
+
+def run_batch(ctx, inverse: bool, subs, slab, policy=SplitPolicy.balanced, canonicalize: bool = False,
+              stream=None) -> None:
+    """Runs independent sub-transforms (objects with L, s, z, n, f, base,
+    stride; indices into the slab's rows) in ONE launch on the slab's GPU."""
+    subs = list(subs)
+    if not subs:
+        return
+    arr = (_Sub * len(subs))()
+    for k, x in enumerate(subs):
+        arr[k] = _Sub(x.L, x.s % (1 << 64), x.z, x.n, x.f, 0, x.base, x.stride)
+    _check(lib().cftft_gpu_batch(ctx._h, 1 if inverse else 0, arr, len(subs), C.c_void_p(slab.data_ptr()),
+                                 slab.shape[1] * 8, int(policy), 1 if canonicalize else 0,
+                                 C.c_void_p(_stream_ptr(stream))))
+
+
+def canonicalize(ctx, slab, count: int, stream=None) -> None:
+    """Lazy engine format -> canonical residues for rows [0, count) of the slab."""
+    if count <= 0:
+        return
+    _check(lib().cftft_gpu_canonicalize(ctx._h, C.c_void_p(slab.data_ptr()), count, slab.shape[1] * 8,
+                                        C.c_void_p(_stream_ptr(stream))))

@@ -557,6 +557,77 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   return launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, st, true);
 }
 
+int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransform* items, uint64_t count,
+                    void* dev_base, uint64_t elem_stride_bytes, int policy, int canonicalize, void* stream) {
+  if (!cring || (!items && count)) return fail(CFTFT_INVALID_PARAMS, "null ring or items");
+  if (int rc = check_stride(cring, elem_stride_bytes)) return rc;
+  if (count == 0) return CFTFT_OK;
+  auto* R = const_cast<cftft_ring*>(cring);
+  std::vector<Planner::Item> v;
+  v.reserve(count);
+  for (u64 k = 0; k < count; ++k) {
+    const cftft_subtransform& it = items[k];
+    cftft_params p{it.length, it.twiddle_exp, it.input_count, it.output_count, it.want_next};
+    if (int rc = validate(R, inverse != 0, &p, policy)) return rc;
+    if (it.stride == 0) return fail(CFTFT_INVALID_PARAMS, "sub-transform stride must be >= 1");
+    v.push_back(Planner::Item{it.length, it.twiddle_exp & (R->M - 1), it.input_count, it.output_count,
+                              inverse ? it.want_next : 0, it.base, it.stride});
+  }
+  auto st = static_cast<cudaStream_t>(stream);
+  // batches are planned per call (the multi-GPU passes reuse one shape many
+  // times; the planner is fast) and cached by a content hash
+  u64 h = 1469598103934665603ull;
+  auto mix = [&](u64 x) { h = (h ^ x) * 1099511628211ull; };
+  mix(inverse ? 1 : 0);
+  mix((u64)policy);
+  for (const auto& it : v) {
+    mix(it.L); mix(it.s); mix(it.z); mix(it.n); mix((u64)it.f); mix(it.base); mix(it.stride);
+  }
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  PlanKey key{dev, 3 + (inverse ? 1 : 0), h, count, v[0].L, v[0].base, policy, -1};
+  DevicePlan* dp = nullptr;
+  {
+    std::lock_guard<std::mutex> g(R->mu);
+    auto itc = R->cache.find(key);
+    if (itc != R->cache.end()) {
+      dp = itc->second.get();
+    } else {
+      auto np = std::make_unique<DevicePlan>();
+      Planner pl(shape_of(R));
+      np->host = pl.build_batch(inverse != 0, v, policy);
+      if (int rc = upload(R, *np, st)) return rc;
+      dp = np.get();
+      R->cache[key] = std::move(np);
+    }
+  }
+  int rc = launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, st, false);
+  if (rc || !canonicalize || R->kind != CFTFT_RING_FERMAT) return rc;
+  for (u64 k = 0; k < count; ++k) {
+    const u64 outs = v[k].n + (u64)v[k].f;
+    std::uint8_t* b = static_cast<std::uint8_t*>(dev_base) + v[k].base * elem_stride_bytes;
+    if (v[k].stride == 1) {
+      fermat::canonicalize_kernel<<<(unsigned)((outs + 255) / 256), 256, 0, st>>>(b, elem_stride_bytes, outs, R->D);
+    } else {
+      fermat::canonicalize_kernel<<<(unsigned)((outs + 255) / 256), 256, 0, st>>>(
+          b, elem_stride_bytes * v[k].stride, outs, R->D);
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int cftft_gpu_canonicalize(const cftft_ring* ring, void* dev_base, uint64_t count, uint64_t elem_stride_bytes,
+                           void* stream) {
+  if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  if (ring->kind != CFTFT_RING_FERMAT || count == 0) return CFTFT_OK;
+  fermat::canonicalize_kernel<<<(unsigned)((count + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, count, ring->D);
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
 uint64_t cftft_tft_base_cases(uint64_t L, uint64_t z, uint64_t n, int policy) {
   CountReplay c;
   return c.tft(L, z, n, policy);

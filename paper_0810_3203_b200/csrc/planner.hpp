@@ -163,6 +163,49 @@ class Planner {
  public:
   explicit Planner(const RingShape& rs) : rs_(rs) {}
 
+  // Independent sub-transforms in one schedule (one launch): the building
+  // block of the multi-GPU column / row passes.
+  struct Item {
+    u64 L, s, z, n;
+    int f;
+    u64 base, stride;
+  };
+  Plan build_batch(bool inverse, const std::vector<Item>& items, int policy) {
+    Plan p;
+    p.inverse = inverse;
+    p.policy = policy;
+    class_index_.clear();
+    classes_.clear();
+    leaves_.clear();
+    keys_.clear();
+    counters_.clear();
+    max_ell_ = 0;
+    u64 item_bytes = items.empty() ? 1 : (items[0].L * std::max<u64>(1, rs_.elem_bytes));
+    u64 batch = std::max<u64>(1, rs_.l2_budget / std::max<u64>(1, item_bytes));
+    for (size_t k = 0; k < items.size(); ++k) {
+      const Item& it = items[k];
+      Ctx c;
+      c.dep = kNoDep;
+      c.report = kNoDep;
+      c.top_phase = 0;
+      c.top_batch = k / batch;
+      c.top_child = k;
+      node(inverse, it.L, it.s, it.z, it.n, it.f, it.base, it.stride, policy, /*depth=*/1, c, 0);
+    }
+    std::vector<u32> idx(leaves_.size());
+    for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return keys_[x] < keys_[y]; });
+    for (u32 i : idx) {
+      p.leaves.push_back(leaves_[i]);
+      p.leaf_wave.push_back(std::get<2>(keys_[i]));
+    }
+    p.classes = std::move(classes_);
+    p.counters = std::move(counters_);
+    p.max_ell = max_ell_;
+    p.final_count = 0;  // caller canonicalises
+    return p;
+  }
+
   Plan build(bool inverse, u64 L, u64 s, u64 z, u64 n, int f, int policy) {
     Plan p;
     p.inverse = inverse;
@@ -206,7 +249,7 @@ class Planner {
   // Split for a node: the reference's policy at the top (transform.hpp:83-87),
   // an SMEM-sized near-balanced split below it.
   void split(unsigned ell, int policy, bool top, unsigned& l1, unsigned& l2) const {
-    if (top) {
+    if (top || policy_everywhere_) {
       if (policy == 1) {
         l1 = 1;
         l2 = ell - 1;
@@ -540,6 +583,7 @@ class Planner {
   }
 
   RingShape rs_;
+  bool policy_everywhere_ = false;
   std::map<ClassKey, u32> class_index_;
   std::vector<LeafProgram> classes_;
   std::vector<DevLeaf> leaves_;

@@ -201,3 +201,50 @@ def test_c1_round_trip_bit_exact():
     assert np.array_equal(from_dev(dev)[:z, : lim + 1], want[:z, : lim + 1])
     cf.scale(ctx, view, z, 2 * N - 10)
     assert np.array_equal(from_dev(dev)[:z, : lim + 1], buf[:z, : lim + 1])
+
+
+def _dist_single_rank(N, L, z, n):
+    """The distributed path (column slab -> batched GPU column pass -> NCCL
+    all-to-all -> row pass, and the ITFT back) on a one-rank NCCL group."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_0810_3203_b200.dist import DistTFT, GpuEngine
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    W = ctx.element_words
+    lim = N // 64
+    full = fermat_inputs(N, L, z, W, 77)
+    full[z:] = 0
+    want = full.copy()
+    ring.tft(want, L, 0, z, n)
+    fwd = DistTFT(GpuEngine(ctx), ring.M, L, 0, z, n)
+    g = fwd.g
+    col = to_dev(full)  # one rank: the column slab is the row-major array itself
+    rows = fwd.tft(col)
+    got = from_dev(rows)
+    assert np.array_equal(got[:n, : lim + 1], want[:n, : lim + 1])
+    inv = DistTFT(GpuEngine(ctx), ring.M, L, 0, n, n, 0)
+    back = torch.zeros_like(col)
+    inv.itft(rows, back)
+    b = from_dev(back)
+    exp = full.copy()
+    ring_scale = po.Ring.fermat(N)
+    for i in range(n):
+        exp[i, : lim + 1] = ring_scale.twiddle(L.bit_length() - 1, full[i, : lim + 1])
+    assert np.array_equal(b[:n, : lim + 1], exp[:n, : lim + 1])
+    assert g.L1 * g.L2 == L
+
+
+def test_dist_path_on_one_gpu():
+    _dist_single_rank(1024, 1024, 700, 700)
+    _dist_single_rank(4096, 4096, 3000, 3100)
