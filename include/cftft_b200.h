@@ -128,9 +128,16 @@ int cftft_gpu_canonicalize(const cftft_ring* ring, void* dev_base, uint64_t coun
                            uint64_t elem_stride_bytes, void* stream);
 
 /* Pointwise ring products a[i] <- a[i] * b[i], i < count, on device views
- * (the pointwise stage of cftft::poly_mul, polymul.hpp:73-77). */
+ * with the same element stride (the pointwise stage of cftft::poly_mul,
+ * polymul.hpp:73-77).  Inputs and outputs canonical.  Fermat rings need
+ * 512 <= N <= 2^17. */
 int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
                         uint64_t elem_stride_bytes, void* stream);
+
+/* Negacyclic rings: x[i] <- c * x[i] word-wise mod m (e.g. poly_mul's final
+ * L^-1 scale, polymul.hpp:82-87). */
+int cftft_gpu_mul_scalar(const cftft_ring* ring, void* dev_base, uint64_t count, uint64_t elem_stride_bytes,
+                         uint64_t c, void* stream);
 
 /* Scales x[0..count) by omega^e (e.g. 1/L = omega^(M - ell) in the Fermat
  * ring, or the SS final 2^-k scale); device view, asynchronous. */

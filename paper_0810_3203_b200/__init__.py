@@ -113,6 +113,7 @@ def lib():
         for f in ("cftft_tft_host", "cftft_itft_host"):
             getattr(L, f).argtypes = [vp, P, vp, u64, C.c_int, C.POINTER(u64)]
         L.cftft_gpu_pointwise.argtypes = [vp, vp, vp, u64, u64, vp]
+        L.cftft_gpu_mul_scalar.argtypes = [vp, vp, u64, u64, u64, vp]
         L.cftft_gpu_batch.argtypes = [vp, C.c_int, C.POINTER(_Sub), u64, vp, u64, C.c_int, C.c_int, vp]
         L.cftft_gpu_canonicalize.argtypes = [vp, vp, u64, u64, vp]
         L.cftft_gpu_scale.argtypes = [vp, vp, u64, u64, u64, vp]

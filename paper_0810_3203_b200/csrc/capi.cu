@@ -17,6 +17,7 @@
 #include "../../include/cftft_b200.h"
 #include "fermat_leaf.cuh"
 #include "negacyclic_leaf.cuh"
+#include "pointwise.cuh"
 #include "planner.hpp"
 
 using namespace cftft_b200;
@@ -76,12 +77,15 @@ struct cftft_ring {
   unsigned max_leaf_fit = 1;
   std::mutex mu;
   std::map<PlanKey, std::unique_ptr<DevicePlan>> cache;
+  // Goldilocks twiddle tables of the Fermat pointwise multiplier
+  u64* ntt_tw = nullptr;
   // staging buffer for the host-view entry points
   void* stage = nullptr;
   size_t stage_bytes = 0;
   CountReplay counts;
   ~cftft_ring() {
     if (stage) cudaFree(stage);
+    if (ntt_tw) cudaFree(ntt_tw);
   }
 };
 
@@ -500,15 +504,102 @@ int cftft_itft_host(const cftft_ring* ring, const cftft_params* params, void* ho
   return host_transform(ring, true, params, host_base, elem_stride_bytes, policy, base_case_count);
 }
 
-int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
+namespace {
+typedef unsigned __int128 hu128;
+constexpr u64 kGold = 0xFFFFFFFF00000001ull;
+u64 gmul(u64 a, u64 b) { return (u64)((hu128)a * b % kGold); }
+u64 gpow(u64 a, u64 e) {
+  u64 r = 1;
+  while (e) {
+    if (e & 1) r = gmul(r, a);
+    a = gmul(a, a);
+    e >>= 1;
+  }
+  return r;
+}
+// Twiddle table layout (see pointwise.cuh): [psi^i, i<n] [omega^j, j<n/2]
+// [unused n/2] [psi^-i / n, i<n] [omega^-j, j<n/2]
+int ensure_ntt_tables(cftft_ring* R, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(R->mu);
+  if (R->ntt_tw) return CFTFT_OK;
+  const u64 n = R->N / 16;
+  // the reference's root search over Goldilocks (field.hpp:170-177): 7^((p-1)/2^32)
+  const u64 w32 = gpow(7, (kGold - 1) >> 32);
+  const u64 psi = gpow(w32, (u64{1} << 32) / (2 * n));  // order 2n
+  const u64 om = gmul(psi, psi);                         // order n
+  const u64 psi_inv = gpow(psi, kGold - 2), om_inv = gpow(om, kGold - 2), n_inv = gpow(n % kGold, kGold - 2);
+  std::vector<u64> h((size_t)(3 * n + n / 2), 0);
+  u64 x = 1, y = n_inv;
+  for (u64 i = 0; i < n; ++i) {
+    h[i] = x;
+    h[2 * n + i] = y;
+    x = gmul(x, psi);
+    y = gmul(y, psi_inv);
+  }
+  x = 1, y = 1;
+  for (u64 j = 0; j < n / 2; ++j) {
+    h[n + j] = x;
+    h[3 * n + j] = y;
+    x = gmul(x, om);
+    y = gmul(y, om_inv);
+  }
+  CUDA_TRY(cudaMalloc((void**)&R->ntt_tw, h.size() * 8));
+  CUDA_TRY(cudaMemcpyAsync(R->ntt_tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return CFTFT_OK;
+}
+}  // namespace
+
+int cftft_gpu_pointwise(const cftft_ring* cring, void* dev_a, const void* dev_b, uint64_t count,
                         uint64_t elem_stride_bytes, void* stream) {
-  (void)ring;
-  (void)dev_a;
-  (void)dev_b;
-  (void)count;
-  (void)elem_stride_bytes;
-  (void)stream;
-  return fail(CFTFT_UNSUPPORTED, "pointwise products are not implemented yet");
+  if (!cring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (int rc = check_stride(cring, elem_stride_bytes)) return rc;
+  if (count == 0) return CFTFT_OK;
+  if (count > 0x7FFFFFFFull) return fail(CFTFT_UNSUPPORTED, "too many products for one launch");
+  auto* R = const_cast<cftft_ring*>(cring);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (R->kind == CFTFT_RING_NEGACYCLIC) {
+    const size_t smem = 24 * R->K;
+    CUDA_TRY(cudaFuncSetAttribute(pointwise::nega_pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    pointwise::nega_pointwise_kernel<<<(unsigned)count, 256, smem, st>>>(
+        static_cast<std::uint8_t*>(dev_a), static_cast<const std::uint8_t*>(dev_b), elem_stride_bytes, (u32)R->K,
+        R->m, 1);
+    g_last_launches = 1;
+    CUDA_TRY(cudaGetLastError());
+    return CFTFT_OK;
+  }
+  if (R->N < 512 || R->N > (u64{1} << 17))
+    return fail(CFTFT_UNSUPPORTED, "Fermat pointwise products need 512 <= N <= 2^17");
+  if (int rc = ensure_ntt_tables(R, st)) return rc;
+  pointwise::FermatMulArgs A{};
+  A.a = static_cast<std::uint8_t*>(dev_a);
+  A.b = static_cast<const std::uint8_t*>(dev_b);
+  A.stride = elem_stride_bytes;
+  A.D16 = (u32)(R->N / 16);
+  A.logn = (u32)__builtin_ctz(A.D16);
+  A.D32 = R->D;
+  A.tw = R->ntt_tw;
+  const size_t smem = (size_t)3 * A.D16 * 8;
+  CUDA_TRY(cudaFuncSetAttribute(pointwise::fermat_pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  pointwise::fermat_pointwise_kernel<<<(unsigned)count, 512, smem, st>>>(A);
+  g_last_launches = 1;
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int cftft_gpu_mul_scalar(const cftft_ring* ring, void* dev_base, uint64_t count, uint64_t elem_stride_bytes,
+                         uint64_t c, void* stream) {
+  if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (ring->kind != CFTFT_RING_NEGACYCLIC) return fail(CFTFT_UNSUPPORTED, "mul_scalar is for negacyclic rings");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  if (count == 0) return CFTFT_OK;
+  const u64 total = count * ring->K;
+  pointwise::nega_scale_kernel<<<(unsigned)((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, count, (u32)ring->K, ring->m, c % ring->m);
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
 }
 
 int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
