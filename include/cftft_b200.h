@@ -76,6 +76,14 @@ uint64_t cftft_ring_element_bytes(const cftft_ring* ring); /* minimal stride */
  * Returns the cap in effect.  Must not race with transforms on the ring. */
 unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell);
 
+/* Fermat rings: leaf layout.  lane_words = 0 runs every leaf on whole
+ * coefficients; 4, 8 or 16 enables coset leaves over lanes of that many
+ * 32-bit words (a leaf whose rotations are whole lanes works
+ * on one residue class of lanes of many coefficients, carries kept per
+ * lane); -1 (the default) picks the lane width per transform length.
+ * Results are bit-identical in every mode. */
+int cftft_ring_set_coset(cftft_ring* ring, int lane_words);
+
 /* Forward truncated transform, in place over a DEVICE view
  * (replaces cftft::cf_tft, transform.hpp:252-264).  On entry x[0..z) hold
  * the coefficients (cells beyond are never read); on exit x[0..n) hold the

@@ -216,6 +216,26 @@ class Ring:
             raise OracleError(rc)
         return c.value
 
+    def tft_at(self, buf: np.ndarray, base: int, stride: int, L, s, z, n, policy=BALANCED):
+        """In place on the strided view buf[base + i * stride], i < L (element
+        rows of a 2-D buffer): the sub-transforms of a Bailey decomposition."""
+        W = buf.shape[1]
+        ptr = C.cast(buf.ctypes.data + 8 * W * base, U64P)
+        c = C.c_uint64(0)
+        rc = lib().or_tft(C.byref(self.r), L, s % (1 << 64), z, n, ptr, W * stride, policy, C.byref(c), 1)
+        if rc:
+            raise OracleError(rc)
+        return c.value
+
+    def itft_at(self, buf: np.ndarray, base: int, stride: int, L, s, z, n, f=0, policy=BALANCED):
+        W = buf.shape[1]
+        ptr = C.cast(buf.ctypes.data + 8 * W * base, U64P)
+        c = C.c_uint64(0)
+        rc = lib().or_itft(C.byref(self.r), L, s % (1 << 64), z, n, f, ptr, W * stride, policy, C.byref(c), 1)
+        if rc:
+            raise OracleError(rc)
+        return c.value
+
     def dft_naive(self, L, s, coeffs: np.ndarray) -> np.ndarray:
         coeffs = np.ascontiguousarray(coeffs, np.uint64)
         out = np.zeros((L, self.words), dtype=np.uint64)

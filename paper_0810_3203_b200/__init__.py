@@ -108,6 +108,7 @@ def lib():
         L.cftft_ring_element_bytes.restype = u64
         L.cftft_ring_set_leaf_limit.argtypes = [vp, C.c_uint]
         L.cftft_ring_set_leaf_limit.restype = C.c_uint
+        L.cftft_ring_set_coset.argtypes = [vp, C.c_int]
         for f in ("cftft_gpu_tft", "cftft_gpu_itft"):
             getattr(L, f).argtypes = [vp, P, vp, u64, C.c_int, C.POINTER(u64), vp]
         for f in ("cftft_tft_host", "cftft_itft_host"):
@@ -179,6 +180,11 @@ class FermatRingCtx(_Ring):
     def __init__(self, N: int):
         self.N = N
         super().__init__(N, 0)
+
+    def set_coset(self, lane_words: int) -> None:
+        """Leaf layout: 0 = whole-coefficient leaves only; 4/8/16 = coset leaves
+        over lanes of that many 32-bit words; -1 = automatic (default)."""
+        _check(lib().cftft_ring_set_coset(self._h, lane_words))
 
 
 class NegacyclicRingCtx(_Ring):

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -56,6 +57,9 @@ struct DevicePlan {
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
+  // Fermat geometry of this plan: chunk (lane) width, chunks per element,
+  // whole-leaf slot bytes, tops-array interleave
+  u32 cw = 16, C = 0, slot_bytes = 0, logS = 0;
   ~DevicePlan() {
     if (dbuf) cudaFree(dbuf);
   }
@@ -67,6 +71,8 @@ using PlanKey = std::tuple<int, int, u64, u64, u64, u64, int, int>;  // dev, inv
 
 struct cftft_ring {
   int kind = 0;
+  int coset_cw = -1;          // Fermat coset leaves: -1 auto, 0 off, 4/8/16 lane words
+  unsigned leaf_limit = 0;    // cftft_ring_set_leaf_limit (0: none)
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
   u32 CW = 16;
@@ -114,6 +120,14 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.post_begin = (u32)rots.size();
     rots.insert(rots.end(), c.post.begin(), c.post.end());
     d.has_pre = c.has_pre ? 1 : 0;
+    d.kind = c.kind;
+    d.cs = c.cs ? c.cs : dp.C;
+    d.m = c.m;
+    d.step = c.step;
+    d.slot_bytes = c.slot_bytes ? c.slot_bytes : dp.slot_bytes;
+    d.inverse = (u32)c.key.inverse;
+    d.spec_n = c.key.inverse ? (u32)c.key.n : 0;
+    d.fslot = (c.key.inverse && c.key.f) ? (u32)c.key.n : 0xFFFFFFFFu;
     cls.push_back(d);
   }
   if (rots.empty()) rots.push_back(SymExp{});
@@ -153,12 +167,61 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   return CFTFT_OK;
 }
 
-RingShape shape_of(const cftft_ring* R) {
+// Planning geometry of one transform of length L.  Fermat: coset leaves use
+// lanes of `cw` words, chosen so that the reference's top-level split yields
+// sub-transforms whose internal rotations are whole lanes (M / sqrt(L) bits).
+RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   RingShape rs;
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
   rs.M = R->M;
   rs.max_leaf_ell = R->max_leaf_ell;
   rs.elem_bytes = R->elem_bytes;
+  u32 cw = R->CW, C = R->C, sb = R->slot_bytes;
+  if (rs.fermat) {
+    const bool on = R->coset_cw > 0 || (R->coset_cw < 0 && R->N >= 4096 && R->NT == 512);
+    if (on && L >= 4) {
+      if (R->coset_cw > 0) {
+        cw = (u32)R->coset_cw;
+      } else {
+        const unsigned ell = (unsigned)__builtin_ctzll(L);
+        const u64 lnode = u64{1} << (ell - ell / 2);
+        u64 lane = R->M / lnode;
+        cw = (u32)std::min<u64>(16, std::max<u64>(4, lane / 32));
+      }
+      if (cw > R->D) cw = R->D;
+      C = R->D / cw;
+      sb = (4 * R->D + 4 * C + 15) & ~15u;
+      const size_t budget = kSmemBudget - scratch_bytes(R->NT);
+      unsigned lam = 1;
+      while (lam < 10 && ((size_t)sb << (lam + 1)) <= budget) ++lam;
+      if (R->leaf_limit) lam = std::min(lam, R->leaf_limit);
+      rs.max_leaf_ell = lam;
+      rs.lane_bits = 32ull * cw;
+      rs.slot_budget = budget;
+      unsigned cl = 0;
+      for (unsigned e = 1; e <= 6; ++e) {
+        const u64 cs = u64{1} << (e - 1);
+        const u64 slot = (cs * 4 * cw + cs * 4 + 15) & ~u64(15);
+        if ((u64{1} << e) <= 2ull * C && (u64{1} << e) * slot <= budget) cl = e;
+      }
+      if (R->leaf_limit) cl = std::min(cl, std::max(1u, R->leaf_limit));
+      rs.coset_max_ell = cl;
+      if (!cl) rs.lane_bits = 0;
+    }
+  }
+  rs.C = C;
+  rs.slot_bytes = sb;
+  if (dp) {
+    dp->cw = cw;
+    dp->C = C;
+    dp->slot_bytes = sb;
+    u32 logS = 0;
+    if (rs.lane_bits) {
+      const u64 S = std::max<u64>(1, (2ull * C) >> rs.coset_max_ell);
+      logS = (u32)__builtin_ctzll(S);
+    }
+    dp->logS = logS;
+  }
   return rs;
 }
 
@@ -175,9 +238,13 @@ int get_plan(cftft_ring* R, bool inv, const cftft_params& p, int policy, cudaStr
     return CFTFT_OK;
   }
   auto dp = std::make_unique<DevicePlan>();
-  Planner pl(shape_of(R));
-  dp->host = pl.build(inv, p.length, p.twiddle_exp, p.input_count, p.output_count,
-                      inv ? p.want_next : 0, policy);
+  Planner pl(shape_of(R, p.length, dp.get()));
+  try {
+    dp->host = pl.build(inv, p.length, p.twiddle_exp, p.input_count, p.output_count,
+                        inv ? p.want_next : 0, policy);
+  } catch (const std::exception& ex) {
+    return fail(CFTFT_UNSUPPORTED, ex.what());
+  }
   int rc = upload(R, *dp, st);
   if (rc) return rc;
   *out = dp.get();
@@ -241,9 +308,12 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
-    const size_t slots_bytes = (size_t)R->slot_bytes << dp.max_ell;
+    const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
+                                   ? std::max<size_t>(dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell)
+                                   : (size_t)R->slot_bytes << dp.max_ell;
     const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
     unsigned grid = 1;
+    short* tops = nullptr;
     if (R->kind == CFTFT_RING_FERMAT) {
       fermat::Args A{};
       A.data = base;
@@ -259,10 +329,19 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.N = R->N;
       A.M = R->M;
       A.D = R->D;
-      A.C = R->C;
-      A.logC = (u32)__builtin_ctz(R->C);
-      A.slot_bytes = R->slot_bytes;
+      A.C = dp.C;
+      A.logC = (u32)__builtin_ctz(dp.C);
+      A.slot_bytes = dp.slot_bytes;
       A.scratch_off = (u32)slots_bytes;
+      A.lanes = dp.C;
+      A.logLanes = (u32)__builtin_ctz(dp.C);
+      A.logS = dp.logS;
+      if (dp.host.coset) {
+        const size_t tb = (size_t)dp.host.extent * dp.C * sizeof(short);
+        CUDA_TRY(cudaMallocAsync((void**)&tops, tb, st));
+        CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
+      }
+      A.T = tops;
       unsigned long long* prof = nullptr;
       static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
       if (profiling) {
@@ -278,10 +357,21 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         kernel<<<grid, nt, smem, st>>>(A);
         return CFTFT_OK;
       };
-      int rc = R->CW == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
-               : R->CW == 8 ? (R->NT == 1024 ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
+      int rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
+               : dp.cw == 8 ? (R->NT == 1024 ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
                             : go(fermat::leaf_kernel<4, 512>, 512);
       if (rc) return rc;
+      if (tops) {
+        // carry-save lanes of the outputs (a batch: of every element it touched)
+        // back to the canonical element format
+        const u64 cnt = dp.host.final_count ? dp.host.final_count : dp.host.extent;
+        if (cnt) {
+          fermat::cs_fold_kernel<<<(unsigned)cnt, 256, 0, st>>>(base, stride, tops, dp.C, dp.cw,
+                                                               (u32)__builtin_ctz(dp.C), dp.logS, R->D, 0, 1);
+          ++launches;
+        }
+        CUDA_TRY(cudaFreeAsync(tops, st));
+      }
       if (prof) {
         unsigned long long h[fermat::PH_N];
         CUDA_TRY(cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -318,7 +408,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(counters, st));
   }
-  if (R->kind == CFTFT_RING_FERMAT && canonicalize && dp.host.final_count) {
+  if (R->kind == CFTFT_RING_FERMAT && canonicalize && dp.host.final_count && !dp.host.coset) {
     const u64 cnt = dp.host.final_count;
     fermat::canonicalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(base, stride, cnt, R->D);
     ++launches;
@@ -371,8 +461,9 @@ int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* 
   return CFTFT_OK;
 }
 
-void json_plan(std::ostringstream& os, const Plan& p) {
-  os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"L\":" << p.L << ",\"s\":" << p.s
+void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
+  os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"lane_bits\":" << lane_bits << ",\"coset\":" << (p.coset ? 1 : 0)
+     << ",\"L\":" << p.L << ",\"s\":" << p.s
      << ",\"z\":" << p.z << ",\"n\":" << p.n << ",\"f\":" << p.f << ",\"final_count\":"
      << p.final_count << ",\"counters\":[";
   for (size_t i = 0; i < p.counters.size(); ++i)
@@ -389,7 +480,8 @@ void json_plan(std::ostringstream& os, const Plan& p) {
     if (c) os << ",";
     os << "{\"ell\":" << k.key.ell << ",\"inverse\":" << k.key.inverse << ",\"z\":" << k.key.z
        << ",\"n\":" << k.key.n << ",\"f\":" << k.key.f << ",\"nload\":" << k.nload
-       << ",\"nstore\":" << k.nstore << ",\"levels\":[";
+       << ",\"nstore\":" << k.nstore << ",\"kind\":" << k.kind << ",\"step\":" << k.step
+       << ",\"m\":" << k.m << ",\"cs\":" << k.cs << ",\"levels\":[";
     for (size_t l = 0; l < k.level_begin.size(); ++l) os << (l ? "," : "") << k.level_begin[l];
     os << "],\"ops\":[";
     for (size_t i = 0; i < k.ops.size(); ++i) {
@@ -407,7 +499,8 @@ void json_plan(std::ostringstream& os, const Plan& p) {
     const auto& lf = p.leaves[i];
     os << (i ? "," : "") << "[" << lf.cls << "," << lf.base << "," << lf.stride << "," << lf.s << ","
        << (lf.dep == kNoDep ? -1 : (long long)lf.dep) << "," << lf.dep_target << ","
-       << (lf.comp == kNoDep ? -1 : (long long)lf.comp) << "," << p.leaf_wave[i] << "]";
+       << (lf.comp == kNoDep ? -1 : (long long)lf.comp) << "," << p.leaf_wave[i] << "," << lf.tpre << ","
+       << lf.tpost << "," << lf.c0 << "]";
   }
   os << "]}";
 }
@@ -477,11 +570,26 @@ unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell) {
   std::lock_guard<std::mutex> g(ring->mu);
   unsigned cap = ring->max_leaf_fit;
   unsigned v = max_ell == 0 ? cap : std::min(std::max(max_ell, 1u), cap);
-  if (v != ring->max_leaf_ell) {
+  const unsigned lim = max_ell == 0 ? 0u : std::max(max_ell, 1u);
+  if (v != ring->max_leaf_ell || lim != ring->leaf_limit) {
     ring->max_leaf_ell = v;
+    ring->leaf_limit = lim;
     ring->cache.clear();
   }
   return v;
+}
+
+int cftft_ring_set_coset(cftft_ring* ring, int lane_words) {
+  if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (ring->kind != CFTFT_RING_FERMAT) return lane_words == 0 ? CFTFT_OK : fail(CFTFT_UNSUPPORTED, "coset leaves are for Fermat rings");
+  if (lane_words != -1 && lane_words != 0 && lane_words != 4 && lane_words != 8 && lane_words != 16)
+    return fail(CFTFT_INVALID_PARAMS, "lane_words must be -1 (auto), 0 (off), 4, 8 or 16");
+  std::lock_guard<std::mutex> g(ring->mu);
+  if (ring->coset_cw != lane_words) {
+    ring->coset_cw = lane_words;
+    ring->cache.clear();
+  }
+  return CFTFT_OK;
 }
 
 int cftft_gpu_tft(const cftft_ring* ring, const cftft_params* params, void* dev_base,
@@ -640,6 +748,9 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
       }
       np->host.max_ell = 0;
       np->host.final_count = count;
+      np->cw = R->CW;
+      np->C = R->C;
+      np->slot_bytes = R->slot_bytes;
       if (int rc = upload(R, *np, st)) return rc;
       dp = np.get();
       R->cache[key] = std::move(np);
@@ -685,8 +796,12 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
       dp = itc->second.get();
     } else {
       auto np = std::make_unique<DevicePlan>();
-      Planner pl(shape_of(R));
-      np->host = pl.build_batch(inverse != 0, v, policy);
+      Planner pl(shape_of(R, v[0].L, np.get()));
+      try {
+        np->host = pl.build_batch(inverse != 0, v, policy);
+      } catch (const std::exception& ex) {
+        return fail(CFTFT_UNSUPPORTED, ex.what());
+      }
       if (int rc = upload(R, *np, st)) return rc;
       dp = np.get();
       R->cache[key] = std::move(np);
@@ -733,11 +848,18 @@ uint64_t cftft_last_launch_count(void) { return g_last_launches; }
 size_t cftft_plan_dump(const cftft_ring* ring, int inverse, const cftft_params* params, int policy,
                        char* buf, size_t cap) {
   if (validate(ring, inverse != 0, params, policy)) return 0;
-  Planner pl(shape_of(ring));
-  Plan p = pl.build(inverse != 0, params->length, params->twiddle_exp, params->input_count,
-                    params->output_count, inverse ? params->want_next : 0, policy);
+  DevicePlan geo;
+  const RingShape rs = shape_of(ring, params->length, &geo);
+  Planner pl(rs);
+  Plan p;
+  try {
+    p = pl.build(inverse != 0, params->length, params->twiddle_exp, params->input_count,
+                 params->output_count, inverse ? params->want_next : 0, policy);
+  } catch (const std::exception&) {
+    return 0;
+  }
   std::ostringstream os;
-  json_plan(os, p);
+  json_plan(os, p, rs.lane_bits);
   std::string s = os.str();
   if (buf && cap) {
     size_t k = std::min(cap - 1, s.size());

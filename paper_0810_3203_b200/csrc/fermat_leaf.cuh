@@ -51,6 +51,9 @@ struct Args {
   u32 logC;
   u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
+  short* T;                // carry-save tops, [view element][lane] (nullptr: not in use)
+  u32 lanes, logLanes;     // lanes (chunks) per element
+  u32 logS;                // tops-array lane interleave
   unsigned long long* prof;  // optional per-phase cycle totals (CFTFT_PROFILE=1)
   u32 debug_skip;            // perf experiments only (CFTFT_DEBUG_SKIP): 1 = levels, 2 = post maths
 };
@@ -461,17 +464,73 @@ __device__ __forceinline__ void sts_at(u32 slot, const Offs<CW>& f, const Ch<CW>
     *reinterpret_cast<uint4*>(g_sm + slot + f.o[k / 4]) = make_uint4(c.w[k], c.w[k + 1], c.w[k + 2], c.w[k + 3]);
 }
 
+// Per-leaf geometry (from the leaf's class and ticket).
+struct Geo {
+  u32 C, Cm, logC;  // chunks per slot
+  u32 SB, W4;       // slot bytes, offset of the tops within a slot
+  u32 coset;        // coset leaf
+  u32 m, logm, step, c0;
+};
+__device__ __forceinline__ Geo geo_of(const DevClass& cl, const DevLeaf& lf, u32 CW) {
+  Geo g;
+  g.C = cl.cs;
+  g.Cm = cl.cs - 1;
+  g.logC = __ffs(cl.cs) - 1;
+  g.SB = cl.slot_bytes;
+  g.W4 = cl.cs * CW * 4;
+  g.coset = cl.kind;
+  g.m = cl.m;
+  g.logm = __ffs(cl.m) - 1;
+  g.step = cl.step;
+  g.c0 = lf.c0;
+  return g;
+}
+// element lane of slot chunk j
+__device__ __forceinline__ u32 lane_of(const Geo& g, u32 j) {
+  return g.coset ? g.c0 + (j & (g.m - 1)) + g.step * (j >> g.logm) : j;
+}
+// tops-array index of lane p (lanes interleaved by S = 2^logS, so that the
+// lanes of one coset are contiguous)
+__device__ __forceinline__ u32 tops_ix(const Args& A, u32 p) {
+  return ((p & ((1u << A.logS) - 1)) << (A.logLanes - A.logS)) | (p >> A.logS);
+}
+
+// Pre / post rotation (omega exponent) of slot k of a leaf.
+__device__ __forceinline__ u64 pre_exp(const Args& A, const DevClass& cl, const DevLeaf& lf, const SymExp& P, u32 k) {
+  return (P.a * lf.s + P.b + (k < cl.spec_n ? lf.tpre : 0)) & (A.M - 1);
+}
+__device__ __forceinline__ u64 post_exp(const Args& A, const DevClass& cl, const DevLeaf& lf, const SymExp& P,
+                                        u32 k) {
+  const bool tp = cl.inverse ? (k == cl.fslot) : true;
+  return (P.a * lf.s + P.b + (tp ? lf.tpost : 0)) & (A.M - 1);
+}
+
+// Rotation of a micro-op: bits for whole leaves; for coset leaves the lane
+// rotation r/lane (a multiple of the step) moves chunk j to j + m r/(lane step)
+// in the slot's negacyclic ring of C chunks.
+template <int CW>
+__device__ __forceinline__ Rot op_rot(const Args& A, const Geo& g, u64 r) {
+  if (!g.coset) return make_rot<CW>(r, A.N);
+  constexpr u32 CB = 32 * CW;
+  const u32 qv = (u32)((r / CB) / g.step) * g.m;
+  Rot R;
+  R.sneg = qv >= g.C ? 1u : 0u;
+  R.q = qv - (R.sneg ? g.C : 0u);
+  R.o = 0;
+  return R;
+}
+
 // Moves whole elements between HBM and shared memory (piece-major swizzled
 // slots), 16 bytes per thread per step, coalesced on the HBM side.  Element
 // x of the range lives at g0 + x*gstride and in slot (s0 + x), x < nslots.
 // The per-thread piece positions are fixed, so the loop body is a couple of
 // adds (no division, no 64-bit multiply).
 template <int CW, bool kLoad, int NT>
-__device__ __forceinline__ void copy_slots(const Args& A, std::uint8_t* g0, u64 gstride, u32 s0, u32 nslots,
+__device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 gstride, u32 s0, u32 nslots,
                                            u32 smem_base, u32 tid) {
   constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
-  const u32 C = A.C, SB = A.slot_bytes;
-  const u32 lq = A.logC + lpc, q16 = 1u << lq;  // pieces per slot
+  const u32 C = G.C, SB = G.SB;
+  const u32 lq = G.logC + lpc, q16 = 1u << lq;  // pieces per slot
   if (q16 >= (u32)NT) {
     // each thread copies pieces tid, tid+NT, ... of every slot
     for (u32 pp = tid; pp < q16; pp += NT) {
@@ -501,30 +560,72 @@ __device__ __forceinline__ void copy_slots(const Args& A, std::uint8_t* g0, u64 
   }
 }
 
+// Lane rotations of a coset leaf's slots, staged per ticket buffer: the
+// pre-rotation (lanes, < 2C) of each loaded slot.
+constexpr u32 kMaxSlots = 64;
+
 // Issues the cp.async loads of slots [s0, s1) of a leaf's inputs (s1 capped
-// at nload) and initialises their tops (the element's signed top word sits
-// on top of the last chunk).
+// at nload) and initialises their tops: the tops array (carry-save lanes,
+// when in use) plus the element's signed top word on top of lane C-1.  Coset
+// leaves gather their lanes through the slot's pre-rotation (negated lanes
+// are fixed up once the data has landed).
 template <int CW, int NT>
 __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 tid, u32 s0 = 0, u32 s1 = 0xFFFFFFFFu) {
-  const u32 Cm = A.C - 1, SB = A.slot_bytes, W4 = 4 * A.D;
+                                           u32 tid, u32* rho, u32 s0 = 0, u32 s1 = 0xFFFFFFFFu) {
+  const Geo G = geo_of(cl, lf, CW);
   s1 = min(s1, cl.nload);
   if (s0 >= s1) return;
-  std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
-  const u64 gstride = lf.stride * A.elem_bytes;
-  copy_slots<CW, true, NT>(A, gbase + (u64)s0 * gstride, gstride, s0, s1 - s0, smem_base, tid);
-  const u32 ttot = (s1 - s0) << A.logC;
+  const u64 eb = A.elem_bytes;
+  std::uint8_t* const gbase = A.data + lf.base * eb;
+  const u64 gstride = lf.stride * eb;
+  const u32 CL = A.lanes, CLm = CL - 1;
+  const u32 W4e = 4 * A.D;  // element top word offset
+  if (!G.coset) {
+    copy_slots<CW, true, NT>(G, gbase + (u64)s0 * gstride, gstride, s0, s1 - s0, smem_base, tid);
+    const u32 ttot = (s1 - s0) << G.logC;
+    for (u32 idx = tid; idx < ttot; idx += NT) {
+      const u32 s = s0 + (idx >> G.logC), c = idx & G.Cm;
+      const u64 e = lf.base + (u64)s * lf.stride;
+      int v = 0;
+      if (c == G.Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4e));
+      if (A.T) v += (int)__ldcg(A.T + e * CL + tops_ix(A, c));
+      sts_i32(s * G.SB + G.W4 + 4 * c, v);
+    }
+    return;
+  }
+  // coset leaf: per-slot lane pre-rotations first
+  constexpr u32 CB = 32 * CW;
+  for (u32 k = s0 + tid; k < s1; k += NT) {
+    const SymExp P = A.rots[cl.pre_begin + k];
+    rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
+  }
+  __syncthreads();
+  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
+  const u32 lq = G.logC + lpc;
+  const u32 tot = (s1 - s0) << lq;
+  for (u32 idx = tid; idx < tot; idx += NT) {
+    const u32 k = s0 + (idx >> lq), rem = idx & ((1u << lq) - 1);
+    const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
+    const u32 src = (lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1);
+    const u32 ln = src & CLm;
+    cp_async16(smem_base + piece_off(k * G.SB, j, q, G.C), gbase + (u64)k * gstride + (u64)ln * (CB / 8) + 16u * q);
+  }
+  const u32 ttot = (s1 - s0) << G.logC;
   for (u32 idx = tid; idx < ttot; idx += NT) {
-    const u32 s = s0 + (idx >> A.logC), c = idx & Cm;
-    int v = 0;
-    if (c == Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4));
-    sts_i32(s * SB + W4 + 4 * c, v);
+    const u32 k = s0 + (idx >> G.logC), j = idx & G.Cm;
+    const u32 src = (lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1);
+    const u32 ln = src & CLm;
+    const u64 e = lf.base + (u64)k * lf.stride;
+    int v = (int)__ldcg(A.T + e * CL + tops_ix(A, ln));
+    if (ln == CLm) v += (int)__ldcg(reinterpret_cast<const long long*>(gbase + (u64)k * gstride + W4e));
+    sts_i32(k * G.SB + G.W4 + 4 * j, v);
   }
 }
 
 template <int CW, int NT>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args A) {
   constexpr int TPT = 2;  // ops per thread per round (each a CW-word chunk)
+  constexpr u32 CB = 32 * CW;
   __shared__ u32 s_tk[2];
   __shared__ DevLeaf s_lf[2];
   __shared__ DevClass s_cl[2];
@@ -533,18 +634,13 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   __shared__ OpT s_ops[kCacheOps];
   __shared__ u32 s_lev[kCacheLev + 1];
   __shared__ SymExp s_crot[kCacheRot];
-  __shared__ Rot s_rot[kMaxBatch];
+  __shared__ u32 s_rho[2][kMaxSlots];
   const u32 tid = threadIdx.x;
   constexpr u32 nthr = NT;
-  const u32 C = A.C, Cm = C - 1, logC = A.logC;
-  const u32 SB = A.slot_bytes, W4 = 4 * A.D;
+  const u32 CL = A.lanes, CLm = CL - 1;
+  const u32 W4e = 4 * A.D;
   const u32 scr = A.scratch_off;
   const u32 smem_base = (u32)__cvta_generic_to_shared(g_sm);
-  // fixed thread geometry: chunk i of group g; G groups work side by side
-  const u32 i = tid & Cm, g = tid >> logC, G = nthr >> logC;
-  Offs<CW> fi;
-  fi.init(i, C);
-  const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
   PhaseClock pc;
   pc.start(tid == 0 && A.prof != nullptr);
 
@@ -561,7 +657,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     s_cached = 0xFFFFFFFFu;
   }
   __syncthreads();
-  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, tid);
+  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, tid, s_rho[0]);
   u32 cur = 0;
 
   for (;;) {
@@ -569,6 +665,13 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     if (ticket >= A.nleaves) break;
     const DevLeaf lf = s_lf[cur];
     const DevClass cl = s_cl[cur];
+    const Geo G = geo_of(cl, lf, CW);
+    const u32 C = G.C, Cm = G.Cm, logC = G.logC, SB = G.SB, W4 = G.W4;
+    // fixed thread geometry for this leaf: chunk i of group g; NG groups side by side
+    const u32 i = tid & Cm, g = tid >> logC, NG = nthr >> logC;
+    Offs<CW> fi;
+    fi.init(i, C);
+    const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
     const u32 nxt = cur ^ 1;
     // fetch the next ticket and descriptor now; they are consumed a leaf later
     if (tid == 0) {
@@ -588,7 +691,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       const u32 op0 = cl.op_begin;
       for (u32 x = tid; x < cl.nops; x += nthr) {
         const DevOp op = A.ops[op0 + x];
-        const Rot R = make_rot<CW>(op.r, A.N);
+        const Rot R = op_rot<CW>(A, G, op.r);
         s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
       }
       for (u32 x = tid; x <= cl.nlevels; x += nthr) s_lev[x] = A.levels[cl.level_begin + x] - op0;
@@ -602,16 +705,35 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
     const u64 gstride = lf.stride * A.elem_bytes;
 
-    // ---- pre-rotations (ITFT spectral inputs), in place: G slots per round -------
-    if (cl.has_pre) {
-      for (u32 b0 = 0; b0 < cl.nload; b0 += G) {
+    if (G.coset) {
+      // ---- coset leaf: negate the lanes that wrapped past 2^N on the way in --------
+      bool any = false;
+      for (u32 k = 0; k < cl.nload; ++k) any |= (s_rho[cur][k] != 0);
+      if (any) {
+        for (u32 idx = tid; idx < (cl.nload << logC); idx += nthr) {
+          const u32 k = idx >> logC, j = idx & Cm;
+          const u32 src = (lane_of(G, j) + 2 * CL - s_rho[cur][k]) & (2 * CL - 1);
+          if (src >= CL) {
+            Ch<CW> w;
+            lds_ch(w, k * SB, j, C);
+            int tp = lds_i32(k * SB + W4 + 4 * j);
+            tp = exact_from<CW>(w, tp, true);
+            sts_ch(k * SB, j, C, w);
+            sts_i32(k * SB + W4 + 4 * j, tp);
+          }
+        }
+        __syncthreads();
+      }
+    } else if (cl.has_pre || lf.tpre) {
+      // ---- pre-rotations (ITFT spectral inputs), in place: NG slots per round -------
+      for (u32 b0 = 0; b0 < cl.nload; b0 += NG) {
         const u32 sl = b0 + g;
         const bool act = sl < cl.nload;
         Ch<CW> w;
         int tp = 0;
         if (act) {
           const SymExp P = cached ? s_crot[sl] : A.rots[cl.pre_begin + sl];
-          const Rot R = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
+          const Rot R = make_rot<CW>(pre_exp(A, cl, lf, P, sl), A.N);
           const bool neg = rot_chunk<CW>(w, tp, sl * SB, sl * SB + W4, R, Cm, i);
           tp = exact_from<CW>(w, tp, neg);
         }
@@ -635,13 +757,13 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         o0 = A.levels[cl.level_begin + l] - cl.op_begin;
         o1 = A.levels[cl.level_begin + l + 1] - cl.op_begin;
       }
-      for (u32 ob = o0; ob < o1; ob += G * TPT) {
-        const u32 nb = min(o1 - ob, G * TPT);
+      for (u32 ob = o0; ob < o1; ob += NG * TPT) {
+        const u32 nb = min(o1 - ob, NG * TPT);
         u32 sbase = ob;
         if (!cached) {  // stage this round's ops
           for (u32 x = tid; x < nb; x += nthr) {
             const DevOp op = A.ops[cl.op_begin + ob + x];
-            const Rot R = make_rot<CW>(op.r, A.N);
+            const Rot R = op_rot<CW>(A, G, op.r);
             s_ops[x] = OpT{op.a * SB, op.b * SB, R.q, R.o, R.sneg, op.type};
           }
           __syncthreads();
@@ -655,7 +777,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
 #pragma unroll
         for (int k = 0; k < TPT; ++k) {
           hdst[k] = 0xFFFFFFFFu;
-          const u32 x = g + G * k;
+          const u32 x = g + NG * k;
           if (x >= nb) continue;
           const OpT op = s_ops[sbase + x];
           Ch<CW> a;
@@ -711,86 +833,145 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     }
     pc.mark(PH_LEVELS);
 
-    // ---- post-rotation + carry resolution + store: G slots per round -------------
     const bool have_next = s_tk[nxt] < A.nleaves;
     bool next_issued = false;
-    for (u32 b0 = 0; b0 < cl.nstore; b0 += G) {
-      const u32 nb = min(cl.nstore - b0, G);
-      const bool last = b0 + nb >= cl.nstore;
-      const u32 sl = b0 + g;
-      const bool act = g < nb;
-      Ch<CW> w;
-      int top = 0;
-      if (act && (A.debug_skip & 2)) {
-        lds_at(w, sl * SB, fi);
-        sts_i32(scr + 4 * tid, 0);
-      } else if (act) {
-        const SymExp P = cached ? s_crot[cl.nload + sl] : A.rots[cl.post_begin + sl];
-        const Rot R = make_rot<CW>((P.a * lf.s + P.b) & (A.M - 1), A.N);
-        bool neg;
-        if (R.o == 0) {
-          const u32 j = (i - R.q) & Cm;
-          lds_ch(w, sl * SB, j, C);
-          top = lds_i32(sl * SB + W4 + 4 * j);
-          neg = ((i < R.q) ? 1u : 0u) != R.sneg;
-        } else {
-          neg = rot_chunk<CW>(w, top, sl * SB, sl * SB + W4, R, Cm, i);
+    if (G.coset) {
+      // ---- coset leaf: lanes out through the post-rotation, carry-save -------------
+      // (1) per chunk: negate wrapped lanes in place, write the tops array, and
+      //     clear the element top word where this ticket owns lane C-1
+      for (u32 idx = tid; idx < (cl.nstore << logC); idx += nthr) {
+        const u32 k = idx >> logC, j = idx & Cm;
+        const SymExp P = cached ? s_crot[cl.nload + k] : A.rots[cl.post_begin + k];
+        const u32 rho = (u32)(post_exp(A, cl, lf, P, k) / CB);
+        const u32 dst = (lane_of(G, j) + rho) & (2 * CL - 1);
+        const u32 d = dst & CLm;
+        int tp = lds_i32(k * SB + W4 + 4 * j);
+        if (dst >= CL) {
+          Ch<CW> w;
+          lds_ch(w, k * SB, j, C);
+          tp = exact_from<CW>(w, tp, true);
+          sts_ch(k * SB, j, C, w);
         }
-        top = exact_from<CW>(w, top, neg);
-        sts_i32(scr + 4 * tid, top);
+        const u64 e = lf.base + (u64)k * lf.stride;
+        __stcg(A.T + e * CL + tops_ix(A, d), (short)tp);
+        if (j == 0) {
+          // the ticket that read lane C-1 (or, for an output-only slot, writes it)
+          // folded the element top word into its lane tops: clear it
+          const u32 pstar = k < cl.nload ? ((CLm + s_rho[cur][k]) & CLm) : ((CLm + 2 * CL - rho) & CLm);
+          if (((pstar & (G.step - 1)) - G.c0) < G.m)
+            __stcg(reinterpret_cast<long long*>(gbase + (u64)k * gstride + W4e), 0ll);
+        }
       }
       __syncthreads();
-      pc.mark(PH_POST);
-      // fold in the top of the chunk below (one step); carries that ripple
-      // further (a chunk of all ones / all zeros) take the slow path
-      int rare = 0;
-      if (act) {
-        const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
-        const int e = in ? ch_add_small<CW>(w, in) : 0;
-        if (i == Cm) {
-          top += e;
-        } else {
-          if (e) rare = 1;
-          top = e;  // carry still owed to chunk i+1
+      // (2) coalesced copy of the lanes to their rotated positions
+      {
+        constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
+        const u32 lq = logC + lpc;
+        const u32 tot = cl.nstore << lq;
+        for (u32 idx = tid; idx < tot; idx += nthr) {
+          const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
+          const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
+          const SymExp P = cached ? s_crot[cl.nload + k] : A.rots[cl.post_begin + k];
+          const u32 rho = (u32)(post_exp(A, cl, lf, P, k) / CB);
+          const u32 d = (lane_of(G, j) + rho) & CLm;
+          __stcg(reinterpret_cast<uint4*>(gbase + (u64)k * gstride + (u64)d * (CB / 8) + 16u * q),
+                 *reinterpret_cast<const uint4*>(g_sm + piece_off(k * SB, j, q, C)));
         }
       }
-      if (__syncthreads_or(rare)) {
-        for (;;) {
-          if (act && i != Cm) sts_i32(scr + 4 * tid, top);
-          __syncthreads();
-          int any = 0;
-          if (act) {
-            const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
-            const int e = in ? ch_add_small<CW>(w, in) : 0;
-            if (i == Cm) {
-              top += e;
-            } else {
-              if (e) any = 1;
-              top = e;
-            }
-          }
-          if (!__syncthreads_or(any)) break;
-        }
-      }
-      // resolved chunks back into their (free) slots, then a coalesced copy
-      // of whole elements to HBM (full 32-byte sectors per request)
-      if (act) {
-        sts_at<CW>(sl * SB, fi, w);
-        if (i == Cm) sts_i32(sl * SB + W4, top);
-      }
-      __syncthreads();  // scratch reuse
+      __syncthreads();  // slot reuse
       pc.mark(PH_STORE);
-      (void)last;
+    } else {
+      // ---- post-rotation + carry resolution + store: NG slots per round ------------
+      for (u32 b0 = 0; b0 < cl.nstore; b0 += NG) {
+        const u32 nb = min(cl.nstore - b0, NG);
+        const u32 sl = b0 + g;
+        const bool act = g < nb;
+        Ch<CW> w;
+        int top = 0;
+        if (act && (A.debug_skip & 2)) {
+          lds_at(w, sl * SB, fi);
+          sts_i32(scr + 4 * tid, 0);
+        } else if (act) {
+          const SymExp P = cached ? s_crot[cl.nload + sl] : A.rots[cl.post_begin + sl];
+          const Rot R = make_rot<CW>(post_exp(A, cl, lf, P, sl), A.N);
+          bool neg;
+          if (R.o == 0) {
+            const u32 j = (i - R.q) & Cm;
+            lds_ch(w, sl * SB, j, C);
+            top = lds_i32(sl * SB + W4 + 4 * j);
+            neg = ((i < R.q) ? 1u : 0u) != R.sneg;
+          } else {
+            neg = rot_chunk<CW>(w, top, sl * SB, sl * SB + W4, R, Cm, i);
+          }
+          top = exact_from<CW>(w, top, neg);
+          sts_i32(scr + 4 * tid, top);
+        }
+        __syncthreads();
+        pc.mark(PH_POST);
+        // fold in the top of the chunk below (one step); carries that ripple
+        // further (a chunk of all ones / all zeros) take the slow path
+        int rare = 0;
+        if (act) {
+          const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
+          const int e = in ? ch_add_small<CW>(w, in) : 0;
+          if (i == Cm) {
+            top += e;
+          } else {
+            if (e) rare = 1;
+            top = e;  // carry still owed to chunk i+1
+          }
+        }
+        if (__syncthreads_or(rare)) {
+          for (;;) {
+            if (act && i != Cm) sts_i32(scr + 4 * tid, top);
+            __syncthreads();
+            int any = 0;
+            if (act) {
+              const int in = i ? lds_i32(scr + 4 * (tid - 1)) : 0;
+              const int e = in ? ch_add_small<CW>(w, in) : 0;
+              if (i == Cm) {
+                top += e;
+              } else {
+                if (e) any = 1;
+                top = e;
+              }
+            }
+            if (!__syncthreads_or(any)) break;
+          }
+        }
+        // resolved chunks back into their (free) slots, then a coalesced copy
+        // of whole elements to HBM (full 32-byte sectors per request)
+        if (act) {
+          sts_at<CW>(sl * SB, fi, w);
+          if (i == Cm) sts_i32(sl * SB + W4, top);
+        }
+        __syncthreads();  // scratch reuse
+        pc.mark(PH_STORE);
+      }
+      // the whole leaf is resolved in shared memory: one coalesced copy to HBM
+      copy_slots<CW, false, NT>(G, gbase, gstride, 0, cl.nstore, smem_base, tid);
+      for (u32 x = tid; x < cl.nstore; x += nthr)
+        __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4e), (long long)lds_i32(x * SB + W4));
+      if (A.T) {  // element format out: the lanes carry no tops
+        if ((CL & 7) == 0) {
+          const u32 per = CL / 8;  // 16-byte groups of int16 tops per element
+          for (u32 x = tid; x < cl.nstore * per; x += nthr) {
+            const u32 k = x / per, q = x - k * per;
+            __stcg(reinterpret_cast<uint4*>(A.T + (lf.base + (u64)k * lf.stride) * CL) + q, make_uint4(0, 0, 0, 0));
+          }
+        } else {
+          for (u32 x = tid; x < cl.nstore * CL; x += nthr) {
+            const u32 k = x / CL, q = x - k * CL;
+            A.T[(lf.base + (u64)k * lf.stride) * CL + q] = 0;
+          }
+        }
+      }
+      __syncthreads();  // slot reuse
     }
-    // the whole leaf is resolved in shared memory: one coalesced copy to HBM
-    copy_slots<CW, false, NT>(A, gbase, gstride, 0, cl.nstore, smem_base, tid);
-    for (u32 x = tid; x < cl.nstore; x += nthr)
-      __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4), (long long)lds_i32(x * SB + W4));
-    __syncthreads();  // slot reuse
     // this leaf is out of shared memory: if the next leaf's dependency is
     // already met, stream its inputs in now so they overlap our HBM stores
     if (have_next && s_ready) {
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, s_rho[nxt]);
       next_issued = true;
     }
     pc.mark(PH_STORE);
@@ -814,7 +995,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           while (ld_acquire(&A.counters[1 + nl.dep]) < nl.dep_target) __nanosleep(64);
       }
       __syncthreads();
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, s_rho[nxt]);
     }
     pc.mark(PH_WAIT);
     cur = nxt;
@@ -824,11 +1005,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
 }
 
 // Final canonicalisation: value = lo + hi*2^N == lo - hi -> [0, 2^N].
-// Thread per element; carry chains beyond word 0 are rare, handled serially.
-__global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 count, u32 D) {
-  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= count) return;
-  std::uint8_t* el = data + e * elem_bytes;
+// Carry chains beyond word 0 are rare, handled serially.
+__device__ void canon_element(std::uint8_t* el, u32 D) {
   long long* topp = reinterpret_cast<long long*>(el + (u64)D * 4);
   long long hi = *topp;
   if (hi == 0) return;
@@ -874,6 +1052,81 @@ __global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 coun
     }
   }
   *topp = top;
+}
+
+// Thread per element.
+__global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 count, u32 D) {
+  u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  canon_element(data + e * elem_bytes, D);
+}
+
+// Carry-save lanes -> canonical element format, one CTA per element: lane p
+// takes the top of lane p-1 (lane 0 takes minus the top of lane C-1 and the
+// element top word: 2^N == -1).  Only word 0 of a lane is touched unless a
+// carry ripples; lanes whose carry-in is zero are not touched at all.
+__global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const short* T, u32 CL, u32 CW,
+                                                      u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride) {
+  __shared__ int s_pend[1024];
+  const u64 e = idx0 + (u64)blockIdx.x * istride;
+  std::uint8_t* el = data + e * eb;
+  const short* Te = T + e * CL;
+  long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
+  u32* w = reinterpret_cast<u32*>(el);
+  auto tix = [&](u32 p) { return ((p & ((1u << logS) - 1)) << (logLanes - logS)) | (p >> logS); };
+  // pass 1: every lane takes its carry-in
+  for (u32 p = threadIdx.x; p < CL; p += blockDim.x) {
+    long long cin;
+    if (p) {
+      cin = Te[tix(p - 1)];
+    } else {
+      cin = -((long long)Te[tix(CL - 1)] + *hip);
+    }
+    int co = 0;
+    if (cin) {
+      u32* lw = w + (u64)p * CW;
+      long long v = (long long)lw[0] + cin;
+      lw[0] = (u32)v;
+      long long c = v >> 32;
+      for (u32 k = 1; k < CW && c; ++k) {
+        v = (long long)lw[k] + c;
+        lw[k] = (u32)v;
+        c = v >> 32;
+      }
+      co = (int)c;
+    }
+    s_pend[p] = co;
+  }
+  // carries out of a lane are rare (a lane of all ones / all zeros): settle
+  // them serially, the top lane's going to the element top word
+  int any = 0;
+  for (u32 p = threadIdx.x; p < CL; p += blockDim.x) any |= s_pend[p];
+  if (!__syncthreads_or(any)) {
+    if (threadIdx.x == 0) *hip = 0;  // lo is canonical: every lane in [0, 2^lane)
+    return;
+  }
+  if (threadIdx.x == 0) {
+    long long h = 0;
+    for (u32 p = 0; p < CL; ++p) {
+      long long c = s_pend[p];
+      if (!c) continue;
+      for (u32 q = p + 1; c; ++q) {
+        if (q == CL) {
+          h += c;
+          break;
+        }
+        u32* lw = w + (u64)q * CW;
+        for (u32 k = 0; k < CW && c; ++k) {
+          long long v = (long long)lw[k] + c;
+          lw[k] = (u32)v;
+          c = v >> 32;
+        }
+      }
+    }
+    // value = lo + h 2^N; the lane-0 term already took the old element top
+    *hip = h;
+    canon_element(el, D);
+  }
 }
 
 }  // namespace fermat

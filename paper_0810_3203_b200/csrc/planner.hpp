@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -83,6 +84,20 @@ struct DevClass {
   u32 has_pre;      // any nonzero pre-rotation coefficient
   u32 op_begin;     // first op of the class in the op table
   u32 nops;         // number of ops
+  // leaf geometry (Fermat).  A leaf works on `cs` chunks of every slot:
+  //   whole leaves (kind 0): cs = C, all lanes, any rotation, carries resolved
+  //     at the store (element format out);
+  //   coset leaves (kind 1): the lanes p == c0 .. c0+m-1 (mod step) of every
+  //     slot, step = (M >> ell) / lane_bits; lane-aligned rotations only,
+  //     carry-save format out (lanes + per-lane tops).
+  u32 kind;
+  u32 cs;          // chunks per slot in shared memory
+  u32 m;           // cosets per ticket (coset leaves)
+  u32 step;        // coset step in lanes (coset leaves)
+  u32 slot_bytes;  // shared-memory bytes per slot
+  u32 inverse;     // ITFT program: tpre goes to pre slots < spec_n, tpost to post slot fslot;
+  u32 spec_n;      // TFT program: tpost goes to every post slot
+  u32 fslot;
 };
 
 constexpr u32 kNoDep = 0xFFFFFFFFu;
@@ -104,17 +119,24 @@ struct DevLeaf {
   u64 base;        // view index of slot 0
   u64 stride;      // view-index distance between slots
   u64 s;           // leaf weight (omega exponent), reduced mod M
-  u64 pad;
+  // extra rotations of a leaf on the boundary of a factored node (see
+  // Planner::node): added to the pre-rotation of the ITFT's spectral inputs
+  // (tpre) and to the post-rotation of the TFT's outputs / the ITFT's f-output
+  // (tpost); 0 elsewhere
+  u64 tpre, tpost;
+  u32 c0;          // coset leaves: first coset of this ticket
+  u32 pad;
 };
-static_assert(sizeof(DevLeaf) == 48, "DevLeaf layout");
+static_assert(sizeof(DevLeaf) == 64, "DevLeaf layout");
 
 struct ClassKey {
   int inverse;
   unsigned ell;
   u64 z, n;
   int f;
+  int kind = 0;  // 0 whole, 1 coset
   bool operator<(const ClassKey& o) const {
-    return std::tie(inverse, ell, z, n, f) < std::tie(o.inverse, o.ell, o.z, o.n, o.f);
+    return std::tie(inverse, ell, z, n, f, kind) < std::tie(o.inverse, o.ell, o.z, o.n, o.f, o.kind);
   }
 };
 
@@ -126,6 +148,8 @@ struct LeafProgram {
   std::vector<SymExp> post;        // per stored slot
   u32 nload = 0, nstore = 0;
   bool has_pre = false;
+  // geometry (DevClass)
+  u32 kind = 0, cs = 0, m = 1, step = 1, slot_bytes = 0;
 };
 
 struct Plan {
@@ -138,6 +162,9 @@ struct Plan {
   std::vector<DevCounter> counters;
   unsigned max_ell = 0;
   u64 final_count = 0;  // outputs [0, final_count) are canonicalised at the end
+  u64 max_slot_area = 0;  // shared-memory bytes of the largest leaf
+  bool coset = false;     // some leaves write carry-save lanes (tops array in use)
+  u64 extent = 0;         // view indices [0, extent) touched (tops array rows)
 };
 
 // Ring-dependent planning parameters.
@@ -147,6 +174,13 @@ struct RingShape {
   unsigned max_leaf_ell = 3;
   u64 elem_bytes = 0;          // bytes per coefficient (for L2 batching)
   u64 l2_budget = 48ull << 20;  // bytes of L2 a batch may occupy
+  // whole-leaf geometry (Fermat): chunks per element and slot bytes
+  u32 C = 0;
+  u32 slot_bytes = 0;
+  // coset mode (Fermat): lanes of lane_bits bits (= chunks), 0 = off
+  u64 lane_bits = 0;
+  unsigned coset_max_ell = 0;
+  u64 slot_budget = 0;  // shared-memory bytes available for a leaf's slots
 };
 
 inline u64 bitrev(u64 j, unsigned ell) {
@@ -174,12 +208,7 @@ class Planner {
     Plan p;
     p.inverse = inverse;
     p.policy = policy;
-    class_index_.clear();
-    classes_.clear();
-    leaves_.clear();
-    keys_.clear();
-    counters_.clear();
-    max_ell_ = 0;
+    reset();
     u64 item_bytes = items.empty() ? 1 : (items[0].L * std::max<u64>(1, rs_.elem_bytes));
     u64 batch = std::max<u64>(1, rs_.l2_budget / std::max<u64>(1, item_bytes));
     for (size_t k = 0; k < items.size(); ++k) {
@@ -190,18 +219,9 @@ class Planner {
       c.top_phase = 0;
       c.top_batch = k / batch;
       c.top_child = k;
-      node(inverse, it.L, it.s, it.z, it.n, it.f, it.base, it.stride, policy, /*depth=*/1, c, 0);
+      node(inverse, it.L, it.s, it.z, it.n, it.f, it.base, it.stride, policy, /*depth=*/1, c, 0, Bnd{});
     }
-    std::vector<u32> idx(leaves_.size());
-    for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return keys_[x] < keys_[y]; });
-    for (u32 i : idx) {
-      p.leaves.push_back(leaves_[i]);
-      p.leaf_wave.push_back(std::get<2>(keys_[i]));
-    }
-    p.classes = std::move(classes_);
-    p.counters = std::move(counters_);
-    p.max_ell = max_ell_;
+    finish(p);
     p.final_count = 0;  // caller canonicalises
     return p;
   }
@@ -215,18 +235,35 @@ class Planner {
     p.n = n;
     p.f = f;
     p.policy = policy;
-    class_index_.clear();
-    classes_.clear();
-    leaves_.clear();
-    keys_.clear();
-    counters_.clear();
-    max_ell_ = 0;
+    reset();
     Ctx root;
     root.dep = kNoDep;
     root.dep_target = 0;
     root.report = kNoDep;
-    node(inverse, L, s, z, n, f, 0, 1, policy, /*depth=*/0, root, /*wave0=*/0);
-    // ticket order: (top phase, batch, wave, top child, emission order)
+    node(inverse, L, s, z, n, f, 0, 1, policy, /*depth=*/0, root, /*wave0=*/0, Bnd{});
+    finish(p);
+    p.final_count = inverse ? n + (u64)f : n;
+    return p;
+  }
+
+ private:
+  static unsigned ctz(u64 x) { return (unsigned)__builtin_ctzll(x); }
+
+  void reset() {
+    class_index_.clear();
+    classes_.clear();
+    progs_.clear();
+    leaves_.clear();
+    keys_.clear();
+    counters_.clear();
+    max_ell_ = 0;
+    max_area_ = 0;
+    coset_used_ = false;
+    extent_ = 0;
+  }
+
+  // ticket order: (top phase, batch, wave, top child, emission order)
+  void finish(Plan& p) {
     std::vector<u32> idx(leaves_.size());
     for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return keys_[x] < keys_[y]; });
@@ -239,12 +276,10 @@ class Planner {
     p.classes = std::move(classes_);
     p.counters = std::move(counters_);
     p.max_ell = max_ell_;
-    p.final_count = inverse ? n + (u64)f : n;
-    return p;
+    p.max_slot_area = max_area_;
+    p.coset = coset_used_;
+    p.extent = extent_;
   }
-
- private:
-  static unsigned ctz(u64 x) { return (unsigned)__builtin_ctzll(x); }
 
   // Split for a node: the reference's policy at the top (transform.hpp:83-87),
   // an SMEM-sized near-balanced split below it.
@@ -260,16 +295,12 @@ class Planner {
       return;
     }
     unsigned lam = rs_.max_leaf_ell;
+    if (rs_.fermat && rs_.lane_bits) lam = std::max(lam, rs_.coset_max_ell);
     unsigned k = (ell + lam - 1) / lam;  // levels needed
     l1 = (ell + k - 1) / k;
     if (l1 >= ell) l1 = ell - 1;
     if (l1 < 1) l1 = 1;
     l2 = ell - l1;
-  }
-
-  unsigned levels_of(unsigned ell) const {
-    unsigned lam = rs_.max_leaf_ell;
-    return ell <= lam ? 1 : (ell + lam - 1) / lam;
   }
 
   struct Ctx {
@@ -280,31 +311,76 @@ class Planner {
     u64 top_batch = 0, top_child = 0;
   };
 
+  // A "factored" node: the first node on a path whose internal rotations
+  // (multiples of M/L) are whole lanes.  Its weight zeta = omega^sigma is
+  // taken out -- TFT_zeta = diag(zeta^[j]) TFT_1 and ITFT_zeta = ITFT_1 after
+  // x_j <- zeta^-[j] x_j (j < n), with the f-output times zeta^[n]
+  // (transform.hpp:288-311) -- so every leaf inside runs with a lane-aligned
+  // weight and only the leaves on the node's boundary carry the (possibly
+  // unaligned) rotations zeta^[j].
+  struct Bnd {
+    bool active = false;
+    u64 sigma = 0;
+    unsigned ell = 0;
+    u64 base = 0, stride = 1;
+    bool out = false;  // TFT: this sub-node's outputs are the node's outputs
+    bool in = false;   // ITFT: its spectral inputs are the node's spectral inputs
+    bool fo = false;   // ITFT: its f-output is the node's f-output
+  };
+
   using Key = std::tuple<u32, u64, u32, u64, u64>;  // phase, batch, wave, child, seq
 
   // One node of the GPU decomposition (base/stride in view elements).
-  // Returns the number of leaves emitted and the number of waves (levels).
+  // Returns the number of completion events it reports to cx.report and the
+  // number of waves (leaf levels) it spans.
   std::pair<u64, u32> node(bool inv, u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride,
-                           int policy, int depth, const Ctx& cx, u32 wave0) {
+                           int policy, int depth, const Ctx& cx, u32 wave0, Bnd bnd) {
     const u64 M = rs_.M;
     s &= (M - 1);
     unsigned ell = ctz(L);
-    if (ell <= rs_.max_leaf_ell) {
+    extent_ = std::max(extent_, base + (L - 1) * stride + 1);
+    const bool coset_on = rs_.fermat && rs_.lane_bits != 0;
+    if (coset_on && !bnd.active && (M >> ell) % rs_.lane_bits == 0) {
+      bnd.active = true;
+      bnd.sigma = s;
+      bnd.ell = ell;
+      bnd.base = base;
+      bnd.stride = stride;
+      bnd.out = !inv;
+      bnd.in = inv;
+      bnd.fo = inv && f;
+      s = 0;
+    }
+    if (bnd.active) {
+      u64 units = 0;
+      if (try_leaf(inv, L, s, z, n, f, base, stride, policy, cx, wave0, bnd, units)) return {units, 1};
+    } else if (ell <= rs_.max_leaf_ell) {
       DevLeaf lf{};
-      lf.cls = class_of(ClassKey{inv ? 1 : 0, ell, z, n, f}, policy);
-      lf.dep = cx.dep;
-      lf.dep_target = cx.dep_target;
-      lf.comp = cx.report;
-      lf.base = base;
-      lf.stride = stride;
       lf.s = s;
-      leaves_.push_back(lf);
-      keys_.push_back(Key{cx.top_phase, cx.top_batch, wave0, cx.top_child, (u64)keys_.size()});
-      max_ell_ = std::max(max_ell_, ell);
+      emit_whole(inv, ell, z, n, f, base, stride, policy, cx, wave0, lf);
       return {1, 1};
     }
     unsigned l1, l2;
-    split(ell, policy, depth == 0, l1, l2);
+    if (bnd.active) {
+      const bool unal = (bnd.sigma % rs_.lane_bits) != 0;
+      if (unal && ((!inv && bnd.out) || (inv && bnd.in))) {
+        // the boundary rows (TFT: last level, ITFT: first level) carry
+        // unaligned rotations: make them whole leaves
+        l2 = std::min(rs_.max_leaf_ell, ell - 1);
+        l1 = ell - l2;
+      } else {
+        const unsigned lam = std::max(1u, rs_.coset_max_ell);
+        const unsigned k = std::max(2u, (ell + lam - 1) / lam);
+        l1 = (ell + k - 1) / k;
+        if (l1 >= ell) l1 = ell - 1;
+        l2 = ell - l1;
+      }
+    } else if (coset_on && depth > 0) {
+      l1 = ell / 2;
+      l2 = ell - l1;
+    } else {
+      split(ell, policy, depth == 0, l1, l2);
+    }
     const u64 cols = u64{1} << l2, rows = u64{1} << l1;
     const u64 col_step = M >> ell;
     const u64 s_row = s << l1;
@@ -314,7 +390,10 @@ class Planner {
       u64 L, s, z, n;
       int f;
       u64 base, stride;
+      Bnd b;
     };
+    Bnd colb = bnd, rowb = bnd;
+    colb.out = colb.in = colb.fo = false;  // columns never touch the node boundary
     std::vector<std::vector<Child>> phases;
     if (!inv) {  // transform.hpp:154-186
       const u64 n2 = n & (cols - 1), n1 = n >> l2, n1c = n1 + (n2 ? 1 : 0);
@@ -322,9 +401,9 @@ class Planner {
       std::vector<Child> c, r;
       for (u64 u = 0; u < z2e; ++u)
         c.push_back({rows, s + u * col_step, u < z2 ? z1 + 1 : z1, n1c, 0, base + u * stride,
-                     stride * cols});
+                     stride * cols, colb});
       for (u64 u = 0; u < n1c; ++u)
-        r.push_back({cols, s_row, z2e, u < n1 ? cols : n2, 0, base + u * cols * stride, stride});
+        r.push_back({cols, s_row, z2e, u < n1 ? cols : n2, 0, base + u * cols * stride, stride, rowb});
       phases.push_back(std::move(c));
       phases.push_back(std::move(r));
     } else {  // transform.hpp:188-239
@@ -332,25 +411,30 @@ class Planner {
       const int fm = (n2 + (u64)f > 0) ? 1 : 0;
       const u64 z2e = z1 ? cols : z2;
       const u64 lo = std::min(n2, z2), hi = std::max(n2, z2);
+      Bnd r1 = bnd;  // phase i rows: full rows of node spectral inputs, no f-output
+      r1.fo = false;
+      Bnd r3 = bnd;  // phase iii row: its first n2 inputs and its f-output are the node's
       std::vector<Child> p1, p2, p3, p4;
-      for (u64 u = 0; u < n1; ++u) p1.push_back({cols, s_row, cols, cols, 0, base + u * cols * stride, stride});
+      for (u64 u = 0; u < n1; ++u)
+        p1.push_back({cols, s_row, cols, cols, 0, base + u * cols * stride, stride, r1});
       for (u64 u = n2; u < z2e; ++u)
-        p2.push_back({rows, s + u * col_step, u < hi ? z1 + 1 : z1, n1, fm, base + u * stride, stride * cols});
-      if (fm) p3.push_back({cols, s_row, z2e, n2, f, base + n1 * cols * stride, stride});
+        p2.push_back({rows, s + u * col_step, u < hi ? z1 + 1 : z1, n1, fm, base + u * stride, stride * cols,
+                      colb});
+      if (fm) p3.push_back({cols, s_row, z2e, n2, f, base + n1 * cols * stride, stride, r3});
       for (u64 u = 0; u < n2; ++u)
-        p4.push_back({rows, s + u * col_step, u < lo ? z1 + 1 : z1, n1 + 1, 0, base + u * stride, stride * cols});
+        p4.push_back({rows, s + u * col_step, u < lo ? z1 + 1 : z1, n1 + 1, 0, base + u * stride, stride * cols,
+                      colb});
       for (auto* ph : {&p1, &p2, &p3, &p4})
         if (!ph->empty()) phases.push_back(std::move(*ph));
     }
 
-    u64 total = 0;
     u32 wave = wave0;
     u32 prev_counter = kNoDep;
     u32 prev_target = 0;
     u32 phase_index = 0;
     for (auto& ph : phases) {
       const u32 cid = (u32)counters_.size();
-      counters_.push_back(DevCounter{(u32)ph.size(), kNoDep});
+      counters_.push_back(DevCounter{0, kNoDep});
       Ctx c2;
       if (phase_index == 0) {
         c2.dep = cx.dep;
@@ -361,6 +445,7 @@ class Planner {
       }
       c2.report = cid;
       u32 maxw = 0;
+      u64 units = 0;
       // L2 batching of top-level children
       u64 child_bytes = (u64{1} << ctz(ph.front().L)) * rs_.elem_bytes;
       u64 batch = std::max<u64>(1, rs_.l2_budget / std::max<u64>(1, child_bytes));
@@ -377,25 +462,159 @@ class Planner {
         }
         u32 w0 = depth == 0 ? 0 : wave;
         auto [k, w] = node(inv, ch.L, ch.s, ch.z, ch.n, ch.f, ch.base, ch.stride, policy, depth + 1,
-                           c2, w0);
-        total += k;
+                           c2, w0, ch.b);
+        units += k;
         maxw = std::max(maxw, w);
       }
+      counters_[cid].target = (u32)units;
       prev_counter = cid;
-      prev_target = (u32)ph.size();
+      prev_target = (u32)units;
       wave += maxw;
       ++phase_index;
     }
     // the node is finished when its last phase is: report to the parent phase
     counters_[prev_counter].next = cx.report;
-    return {total, wave - wave0};
+    return {1, wave - wave0};
+  }
+
+  // Boundary rotations of a leaf inside a factored node (see Bnd): leaf slot k
+  // sits at node position j = rb + k * 2^a, so zeta^[j] = omega^(t + [k] s2)
+  // with t = sigma [rb] and s2 = sigma 2^(ell_node - a - ell_leaf).
+  void boundary(const Bnd& bnd, bool inv, unsigned ell, u64 base, u64 stride, DevLeaf& lf) const {
+    const u64 M = rs_.M;
+    if (!bnd.active) return;
+    const bool tft_out = !inv && bnd.out;
+    const bool itft_b = inv && (bnd.in || bnd.fo);
+    if (!tft_out && !itft_b) return;
+    const u64 rb = (base - bnd.base) / bnd.stride, rt = stride / bnd.stride;
+    const unsigned a = ctz(rt);
+    const u64 s2 = (bnd.sigma << (bnd.ell - a - ell)) & (M - 1);
+    const u64 t = (bnd.sigma * bitrev(rb, bnd.ell)) & (M - 1);
+    // boundary leaves have a zero weight of their own inside the factored node
+    if (lf.s != 0) throw std::logic_error("planner: boundary leaf with a nonzero weight");
+    lf.s = s2;
+    if (tft_out) lf.tpost = t;
+    if (inv && bnd.in) lf.tpre = (M - t) & (M - 1);
+    if (inv && bnd.fo) lf.tpost = t;
+  }
+
+  // A leaf inside a factored node: a coset leaf when every rotation it
+  // performs is lane aligned, else a whole leaf when it fits; false: split.
+  bool try_leaf(bool inv, u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride, int policy,
+                const Ctx& cx, u32 wave0, const Bnd& bnd, u64& units) {
+    const unsigned ell = ctz(L);
+    DevLeaf lf{};
+    lf.s = s;
+    boundary(bnd, inv, ell, base, stride, lf);
+    if (coset_fits(ell)) {
+      const ClassKey key{inv ? 1 : 0, ell, z, n, f, 1};
+      const LeafProgram& prog = program(key, policy);
+      if (aligned(prog, inv, ell, lf)) {
+        units = emit_coset(key, policy, base, stride, cx, wave0, lf);
+        return true;
+      }
+    }
+    if (ell <= rs_.max_leaf_ell) {
+      emit_whole(inv, ell, z, n, f, base, stride, policy, cx, wave0, lf);
+      units = 1;
+      return true;
+    }
+    return false;
+  }
+
+  u64 lanes2() const { return rs_.M / rs_.lane_bits; }  // 2C
+  u32 coset_slot_bytes(u64 cs) const { return (u32)((cs * (rs_.lane_bits / 8) + cs * 4 + 15) & ~u64(15)); }
+
+  bool coset_fits(unsigned ell) const {
+    if (!rs_.lane_bits || ell > rs_.coset_max_ell || ell < 1) return false;
+    if ((u64{1} << ell) > lanes2()) return false;  // step >= 1
+    const u64 cs = u64{1} << (ell - 1);
+    return (u64{1} << ell) * coset_slot_bytes(cs) <= rs_.slot_budget;
+  }
+
+  // every op rotation a multiple of the coset step, every pre/post rotation a
+  // whole number of lanes
+  bool aligned(const LeafProgram& prog, bool inv, unsigned ell, const DevLeaf& lf) const {
+    const u64 M = rs_.M, inner = M >> ell, lb = rs_.lane_bits;
+    for (const auto& op : prog.ops)
+      if (op.type != OP_COPY && (op.r % inner) != 0) return false;
+    for (u32 k = 0; k < prog.nload; ++k) {
+      u64 r = prog.pre[k].a * lf.s + prog.pre[k].b + ((inv && k < prog.key.n) ? lf.tpre : 0);
+      if ((r & (M - 1)) % lb) return false;
+    }
+    for (u32 k = 0; k < prog.nstore; ++k) {
+      const bool tp = inv ? (prog.key.f && k == prog.key.n) : true;
+      u64 r = prog.post[k].a * lf.s + prog.post[k].b + (tp ? lf.tpost : 0);
+      if ((r & (M - 1)) % lb) return false;
+    }
+    return true;
+  }
+
+  void push_leaf(const DevLeaf& lf, const Ctx& cx, u32 wave0) {
+    leaves_.push_back(lf);
+    keys_.push_back(Key{cx.top_phase, cx.top_batch, wave0, cx.top_child, (u64)keys_.size()});
+  }
+
+  void emit_whole(bool inv, unsigned ell, u64 z, u64 n, int f, u64 base, u64 stride, int policy, const Ctx& cx,
+                  u32 wave0, DevLeaf lf) {
+    lf.cls = class_of(ClassKey{inv ? 1 : 0, ell, z, n, f, 0}, policy);
+    lf.dep = cx.dep;
+    lf.dep_target = cx.dep_target;
+    lf.comp = cx.report;
+    lf.base = base;
+    lf.stride = stride;
+    lf.c0 = 0;
+    push_leaf(lf, cx, wave0);
+    max_ell_ = std::max(max_ell_, ell);
+  }
+
+  u64 emit_coset(const ClassKey& key, int policy, u64 base, u64 stride, const Ctx& cx, u32 wave0, DevLeaf lf) {
+    lf.cls = class_of(key, policy);
+    const LeafProgram& c = classes_[lf.cls];
+    lf.dep = cx.dep;
+    lf.dep_target = cx.dep_target;
+    lf.comp = cx.report;
+    lf.base = base;
+    lf.stride = stride;
+    const u64 groups = c.step / c.m;
+    for (u64 g = 0; g < groups; ++g) {
+      lf.c0 = (u32)(g * c.m);
+      push_leaf(lf, cx, wave0);
+    }
+    coset_used_ = true;
+    return groups;
   }
 
   // ---- leaf programs -------------------------------------------------------
+  const LeafProgram& program(ClassKey k, int policy) {
+    k.kind = 0;
+    auto it = progs_.find(k);
+    if (it == progs_.end()) it = progs_.emplace(k, build_leaf(k, policy)).first;
+    return it->second;
+  }
+
   u32 class_of(const ClassKey& k, int policy) {
     auto it = class_index_.find(k);
     if (it != class_index_.end()) return it->second;
-    LeafProgram prog = build_leaf(k, policy);
+    LeafProgram prog = program(k, policy);
+    prog.key = k;
+    const u64 L = u64{1} << k.ell;
+    prog.kind = (u32)k.kind;
+    if (k.kind == 1) {
+      prog.step = (u32)(lanes2() >> k.ell);
+      const u64 cl = u64{1} << (k.ell - 1);  // lanes per coset
+      u64 m = 1;
+      while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.slot_budget) m *= 2;
+      prog.m = (u32)m;
+      prog.cs = (u32)(m * cl);
+      prog.slot_bytes = coset_slot_bytes(prog.cs);
+    } else {
+      prog.step = 1;
+      prog.m = 1;
+      prog.cs = rs_.C;
+      prog.slot_bytes = rs_.slot_bytes;
+    }
+    max_area_ = std::max<u64>(max_area_, L * prog.slot_bytes);
     u32 id = (u32)classes_.size();
     classes_.push_back(std::move(prog));
     class_index_[k] = id;
@@ -585,11 +804,15 @@ class Planner {
   RingShape rs_;
   bool policy_everywhere_ = false;
   std::map<ClassKey, u32> class_index_;
+  std::map<ClassKey, LeafProgram> progs_;
   std::vector<LeafProgram> classes_;
   std::vector<DevLeaf> leaves_;
   std::vector<Key> keys_;
   std::vector<DevCounter> counters_;
   unsigned max_ell_ = 0;
+  u64 max_area_ = 0;
+  bool coset_used_ = false;
+  u64 extent_ = 0;
 };
 
 // ---------------------------------------------------------------------------

@@ -112,20 +112,29 @@ def test_counts_respect_bounds():  # verify.hpp:507-553
 
 def run_plan_fermat(plan, N, vals):
     """Executes the ticket list at the value level, checking that every leaf's
-    dependency counter is complete when its ticket comes up."""
+    dependency counter is complete when its ticket comes up.  Coset leaves
+    (one ticket per group of lane cosets) are run once, at their first ticket;
+    every rotation they perform must be a whole number of lanes."""
     P, M = (1 << N) + 1, 2 * N
+    lane = plan.get("lane_bits", 0)
     x = dict(vals)
     meta = plan["counters"]
     counters = [0] * len(meta)
-    for (cls, base, stride, s, dep, target, comp, wave) in plan["leaves"]:
+    for (cls, base, stride, s, dep, target, comp, wave, tpre, tpost, c0) in plan["leaves"]:
         if dep >= 0:
             assert counters[dep] >= target, "ticket order is not topological"
         c = plan["classes"][cls]
+        inv, cn, cf_ = c["inverse"], c["n"], c["f"]
+        coset = c["kind"] == 1
+        run = not coset or c0 == 0
         slot = [None] * (1 << c["ell"])
-        for i in range(c["nload"]):
+        for i in range(c["nload"] if run else 0):
             a, b = c["pre"][i]
-            slot[i] = (x[base + i * stride] * pow(2, (a * s + b) % M, P)) % P
-        for (t, a, b, r) in c["ops"]:
+            e = (a * s + b + (tpre if inv and i < cn else 0)) % M
+            assert not coset or e % lane == 0
+            slot[i] = (x[base + i * stride] * pow(2, e, P)) % P
+        for (t, a, b, r) in (c["ops"] if run else []):
+            assert not coset or t == 4 or r % (M >> c["ell"]) == 0
             if t == 4:
                 slot[b] = slot[a]
                 continue
@@ -140,9 +149,12 @@ def run_plan_fermat(plan, N, vals):
                 slot[a], slot[b] = (2 * A - B) % P, (A - B) % P
             else:
                 raise AssertionError("negacyclic-only op in a Fermat plan")
-        for i in range(c["nstore"]):
+        for i in range(c["nstore"] if run else 0):
             ea, eb = c["post"][i]
-            x[base + i * stride] = (slot[i] * pow(2, (ea * s + eb) % M, P)) % P
+            tp = (tpost if cf_ and i == cn else 0) if inv else tpost
+            e = (ea * s + eb + tp) % M
+            assert not coset or e % lane == 0
+            x[base + i * stride] = (slot[i] * pow(2, e, P)) % P
         k = comp
         while k >= 0:  # leaf -> phase counter -> (node finished) -> parent phase ...
             counters[k] += 1
@@ -185,11 +197,24 @@ def test_gpu_schedule_reproduces_definition(limit):
         check_plan(ctx, N, rnd, 40)
 
 
+@pytest.mark.parametrize("limit", [0, 2, 3])
+def test_coset_schedule_reproduces_definition(limit):
+    """Coset leaves: factored nodes (zeta taken out), lane-aligned leaves as
+    coset tickets, boundary leaves with their extra rotations."""
+    rnd = random.Random(100 + limit)
+    for N, cw in ((512, 4), (1024, 4), (2048, 8)):
+        ctx = cf.FermatRingCtx(N)
+        ctx.set_coset(cw)
+        ctx.set_leaf_limit(limit)
+        check_plan(ctx, N, rnd, 25)
+
+
 def test_schedule_shape_config5():
     """C5 (L=2^18, z=n=200000): top split 512x512, SMEM leaves of 8 -> three
     levels per top-level pass; only columns < z2' and rows < n1' are scheduled;
     the ticket list is L2-batched (whole columns, level by level)."""
     ctx = cf.FermatRingCtx(131072)
+    ctx.set_coset(0)
     assert ctx.set_leaf_limit(0) == 3
     plan = cf.plan_dump(ctx, False, cf.TransformParams(1 << 18, 0, 200000, 200000))
     leaves = plan["leaves"]

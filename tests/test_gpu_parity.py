@@ -248,3 +248,52 @@ def _dist_single_rank(N, L, z, n):
 def test_dist_path_on_one_gpu():
     _dist_single_rank(1024, 1024, 700, 700)
     _dist_single_rank(4096, 4096, 3000, 3100)
+
+
+# ---- coset leaves (carry-save lanes) ---------------------------------------------
+
+@pytest.mark.parametrize("N,cw", [(1024, 4), (2048, 8), (4096, 4), (8192, 16)])
+@pytest.mark.parametrize("limit", [0, 2, 3])
+def test_fermat_coset_sweep(N, cw, limit):
+    """Factored nodes, coset tickets, boundary rotations and the carry-save
+    fold, against the oracle on random shapes and twiddles."""
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_coset(cw)
+    ctx.set_leaf_limit(limit)
+    ring = po.Ring.fermat(N)
+    rnd = random.Random(N * 7 + cw + limit)
+    for trial in range(16):
+        L = 1 << rnd.randint(2, min(10, (2 * N).bit_length() - 1))
+        z, n = rnd.randint(1, L), rnd.randint(1, L)
+        s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
+        _fermat_case(ctx, ring, N, L, z, n, s, pol, seed=trial, special=(trial % 3 == 0))
+        n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+        if 1 <= n2 + f <= L:
+            _fermat_case(ctx, ring, N, L, z, n2, s, pol, seed=500 + trial, inverse=True, f=f,
+                         special=(trial % 3 == 1))
+
+
+def test_fermat_coset_exhaustive_small():
+    """Every (z, n) at L = 32 with coset leaves forced (cf. verify.hpp:85-120)."""
+    N, L = 1024, 32
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_coset(4)
+    ctx.set_leaf_limit(2)
+    ring = po.Ring.fermat(N)
+    for z in range(1, L + 1):
+        for n in range(1, L + 1, 3):
+            _fermat_case(ctx, ring, N, L, z, n, 11, 0, seed=z * 100 + n, special=(z % 5 == 0))
+        for n in range(0, z + 1, 2):
+            for f in (0, 1):
+                if 1 <= n + f <= L:
+                    _fermat_case(ctx, ring, N, L, z, n, 3, 0, seed=z * 7 + n, inverse=True, f=f)
+
+
+@pytest.mark.parametrize("N,L,z,n", [(32768, 4096, 3000, 3000), (65536, 2048, 1500, 1700), (131072, 1024, 700, 700)])
+def test_fermat_coset_large_elements(N, L, z, n):
+    """BASELINE-sized coefficients (automatic coset mode), TFT and ITFT vs the oracle."""
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    _fermat_case(ctx, ring, N, L, z, n, 0, 0, seed=N + z)
+    _fermat_case(ctx, ring, N, L, min(z, n), min(z, n), 0, 0, seed=N + n, inverse=True, f=0)
+    _fermat_case(ctx, ring, N, L, z, n // 2, 5, 1, seed=N + 1, inverse=True, f=1)
