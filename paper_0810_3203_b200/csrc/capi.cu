@@ -186,11 +186,13 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         const unsigned ell = (unsigned)__builtin_ctzll(L);
         const u64 lnode = u64{1} << (ell - ell / 2);
         u64 lane = R->M / lnode;
-        cw = (u32)std::min<u64>(16, std::max<u64>(4, lane / 32));
+        // lanes of <= 8 words keep a 64-coefficient coset ticket within one of
+        // the two ticket buffers
+        cw = (u32)std::min<u64>(8, std::max<u64>(4, lane / 32));
       }
       if (cw > R->D) cw = R->D;
       C = R->D / cw;
-      sb = (4 * R->D + 4 * C + 15) & ~15u;
+      sb = fermat_slot_bytes(C, 4 * cw);
       const size_t budget = kSmemBudget - scratch_bytes(R->NT);
       unsigned lam = 1;
       while (lam < 10 && ((size_t)sb << (lam + 1)) <= budget) ++lam;
@@ -201,8 +203,8 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       unsigned cl = 0;
       for (unsigned e = 1; e <= 6; ++e) {
         const u64 cs = u64{1} << (e - 1);
-        const u64 slot = (cs * 4 * cw + cs * 4 + 15) & ~u64(15);
-        if ((u64{1} << e) <= 2ull * C && (u64{1} << e) * slot <= budget) cl = e;
+        const u64 slot = fermat_slot_bytes(cs, 4 * cw);
+        if ((u64{1} << e) <= 2ull * C && (u64{1} << e) * slot <= budget / 2) cl = e;
       }
       if (R->leaf_limit) cl = std::min(cl, std::max(1u, R->leaf_limit));
       rs.coset_max_ell = cl;
@@ -308,8 +310,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
+    // Fermat: two ticket buffers of `half` bytes each (a big ticket spans both)
+    const size_t half = ((kSmemBudget - scratch_bytes(R->NT)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
-                                   ? std::max<size_t>(dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell)
+                                   ? std::max<size_t>({dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell, 2 * half})
                                    : (size_t)R->slot_bytes << dp.max_ell;
     const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
     unsigned grid = 1;
@@ -342,6 +346,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
       }
       A.T = tops;
+      A.half = (u32)half;
       unsigned long long* prof = nullptr;
       static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
       if (profiling) {
@@ -523,7 +528,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
     R->D = (u32)(N / 32);
     R->CW = R->D >= 16 ? 16 : R->D;
     R->C = R->D / R->CW;
-    R->slot_bytes = (4 * R->D + 4 * R->C + 15) & ~15u;
+    R->slot_bytes = fermat_slot_bytes(R->C, 4 * R->CW);
     R->elem_bytes = ((N / 8 + 8) + 15) & ~u64(15);
   } else if (kind == CFTFT_RING_NEGACYCLIC) {
     const u64 K = n_or_k, m = modulus;
@@ -548,7 +553,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
     if (wv && atoi(wv) == 1 && R->D >= 16) {
       R->CW = 8;
       R->C = R->D / 8;
-      R->slot_bytes = (4 * R->D + 4 * R->C + 15) & ~15u;
+      R->slot_bytes = fermat_slot_bytes(R->C, 4 * R->CW);
       R->NT = 1024;
     }
   }
@@ -739,6 +744,7 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
       np->host.classes.push_back(lp);
       for (u64 i = 0; i < count; ++i) {
         DevLeaf lf{};
+        lf.lbar = kNoDep;
         lf.cls = 0;
         lf.dep = kNoDep;
         lf.comp = kNoDep;

@@ -52,6 +52,7 @@ struct Args {
   u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
   short* T;                // carry-save tops, [view element][lane] (nullptr: not in use)
+  u32 half;                // bytes of one of the two ticket buffers (double buffering)
   u32 lanes, logLanes;     // lanes (chunks) per element
   u32 logS;                // tops-array lane interleave
   unsigned long long* prof;  // optional per-phase cycle totals (CFTFT_PROFILE=1)
@@ -423,6 +424,15 @@ __device__ __forceinline__ void cp_async16(u32 saddr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async4(u32 saddr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(u32 saddr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ u32 ld_acquire(const u32* p) {
   u32 v;
@@ -467,7 +477,7 @@ __device__ __forceinline__ void sts_at(u32 slot, const Offs<CW>& f, const Ch<CW>
 // Per-leaf geometry (from the leaf's class and ticket).
 struct Geo {
   u32 C, Cm, logC;  // chunks per slot
-  u32 SB, W4;       // slot bytes, offset of the tops within a slot
+  u32 SB, W4, HO;   // slot bytes, offsets of the tops and of the element top word
   u32 coset;        // coset leaf
   u32 m, logm, step, c0;
 };
@@ -478,6 +488,7 @@ __device__ __forceinline__ Geo geo_of(const DevClass& cl, const DevLeaf& lf, u32
   g.logC = __ffs(cl.cs) - 1;
   g.SB = cl.slot_bytes;
   g.W4 = cl.cs * CW * 4;
+  g.HO = g.W4 + ((4 * cl.cs + 7) & ~7u);
   g.coset = cl.kind;
   g.m = cl.m;
   g.logm = __ffs(cl.m) - 1;
@@ -527,7 +538,7 @@ __device__ __forceinline__ Rot op_rot(const Args& A, const Geo& g, u64 r) {
 // adds (no division, no 64-bit multiply).
 template <int CW, bool kLoad, int NT>
 __device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 gstride, u32 s0, u32 nslots,
-                                           u32 smem_base, u32 tid) {
+                                           u32 smem_base, u32 boff, u32 tid) {
   constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
   const u32 C = G.C, SB = G.SB;
   const u32 lq = G.logC + lpc, q16 = 1u << lq;  // pieces per slot
@@ -536,7 +547,7 @@ __device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 g
     for (u32 pp = tid; pp < q16; pp += NT) {
       const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
       std::uint8_t* g = g0 + 16u * pp;
-      u32 so = s0 * SB + so0;
+      u32 so = boff + s0 * SB + so0;
       for (u32 x = 0; x < nslots; ++x, g += gstride, so += SB) {
         if (kLoad)
           cp_async16(smem_base + so, g);
@@ -550,7 +561,7 @@ __device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 g
     const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
     std::uint8_t* g = g0 + (u64)x0 * gstride + 16u * pp;
     const u64 gstep = (u64)step * gstride;
-    u32 so = (s0 + x0) * SB + so0;
+    u32 so = boff + (s0 + x0) * SB + so0;
     for (u32 x = x0; x < nslots; x += step, g += gstep, so += step * SB) {
       if (kLoad)
         cp_async16(smem_base + so, g);
@@ -560,66 +571,92 @@ __device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 g
   }
 }
 
-// Lane rotations of a coset leaf's slots, staged per ticket buffer: the
-// pre-rotation (lanes, < 2C) of each loaded slot.
+// Slot layout (both leaf kinds): C chunks (piece-major, swizzled), then one
+// int32 top per chunk at W4, then the element's 64-bit top word at W4 + 4C.
 constexpr u32 kMaxSlots = 64;
 
-// Issues the cp.async loads of slots [s0, s1) of a leaf's inputs (s1 capped
-// at nload) and initialises their tops: the tops array (carry-save lanes,
-// when in use) plus the element's signed top word on top of lane C-1.  Coset
-// leaves gather their lanes through the slot's pre-rotation (negated lanes
-// are fixed up once the data has landed).
+// Issues the loads of a ticket into the slot buffer at `boff`, all as
+// cp.async in one commit group: the data chunks (coset tickets gather their
+// lanes through the slot's lane pre-rotation), the 4-byte word of the tops
+// array that holds each chunk's carry-save top (when in use), and each
+// slot's element top word.  fixup() turns these into int32 tops once landed.
 template <int CW, int NT>
 __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 tid, u32* rho, u32 s0 = 0, u32 s1 = 0xFFFFFFFFu) {
+                                           u32 boff, u32 tid, u32* rho) {
   const Geo G = geo_of(cl, lf, CW);
-  s1 = min(s1, cl.nload);
-  if (s0 >= s1) return;
-  const u64 eb = A.elem_bytes;
-  std::uint8_t* const gbase = A.data + lf.base * eb;
-  const u64 gstride = lf.stride * eb;
-  const u32 CL = A.lanes, CLm = CL - 1;
-  const u32 W4e = 4 * A.D;  // element top word offset
-  if (!G.coset) {
-    copy_slots<CW, true, NT>(G, gbase + (u64)s0 * gstride, gstride, s0, s1 - s0, smem_base, tid);
-    const u32 ttot = (s1 - s0) << G.logC;
-    for (u32 idx = tid; idx < ttot; idx += NT) {
-      const u32 s = s0 + (idx >> G.logC), c = idx & G.Cm;
-      const u64 e = lf.base + (u64)s * lf.stride;
-      int v = 0;
-      if (c == G.Cm) v = (int)__ldcg(reinterpret_cast<const long long*>(gbase + s * gstride + W4e));
-      if (A.T) v += (int)__ldcg(A.T + e * CL + tops_ix(A, c));
-      sts_i32(s * G.SB + G.W4 + 4 * c, v);
+  const u32 nl = cl.nload;
+  if (nl) {
+    constexpr u32 CB = 32 * CW;
+    constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
+    const u64 eb = A.elem_bytes;
+    std::uint8_t* const gbase = A.data + lf.base * eb;
+    const u64 gstride = lf.stride * eb;
+    const u32 CL = A.lanes;
+    const u32 sb = smem_base + boff;
+    if (G.coset) {
+      for (u32 k = tid; k < nl; k += NT) {
+        const SymExp P = A.rots[cl.pre_begin + k];
+        rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
+      }
+      __syncthreads();
+      const u32 lq = G.logC + lpc;
+      const u32 tot = nl << lq;
+      for (u32 idx = tid; idx < tot; idx += NT) {
+        const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
+        const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
+        const u32 ln = (lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1);
+        cp_async16(sb + piece_off(k * G.SB, j, q, G.C), gbase + (u64)k * gstride + (u64)ln * (CB / 8) + 16u * q);
+      }
+    } else {
+      copy_slots<CW, true, NT>(G, gbase, gstride, 0, nl, smem_base, boff, tid);
     }
-    return;
+    if (A.T) {
+      const u32 tt = nl << G.logC;
+      for (u32 idx = tid; idx < tt; idx += NT) {
+        const u32 k = idx >> G.logC, j = idx & G.Cm;
+        const u32 ln = G.coset ? ((lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1)) : j;
+        const u64 e = lf.base + (u64)k * lf.stride;
+        cp_async4(sb + k * G.SB + G.W4 + 4 * j, A.T + e * CL + (tops_ix(A, ln) & ~1u));
+      }
+    }
+    for (u32 k = tid; k < nl; k += NT)
+      cp_async8(sb + k * G.SB + G.HO, gbase + (u64)k * gstride + 4ull * A.D);
   }
-  // coset leaf: per-slot lane pre-rotations first
-  constexpr u32 CB = 32 * CW;
-  for (u32 k = s0 + tid; k < s1; k += NT) {
-    const SymExp P = A.rots[cl.pre_begin + k];
-    rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
+  cp_async_commit();
+}
+
+// Once a ticket's loads have landed: int32 tops from the tops-array words and
+// the element top word (on lane C-1), and coset lanes that wrapped past 2^N
+// negated in place.
+template <int CW, int NT>
+__device__ __forceinline__ void fixup(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 boff, u32 tid,
+                                      const u32* rho) {
+  const Geo G = geo_of(cl, lf, CW);
+  const u32 CL = A.lanes;
+  const u32 tt = cl.nload << G.logC;
+  for (u32 idx = tid; idx < tt; idx += NT) {
+    const u32 k = idx >> G.logC, j = idx & G.Cm;
+    const u32 src = G.coset ? ((lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1)) : j;
+    const u32 ln = src & (CL - 1);
+    const u32 so = boff + k * G.SB;
+    int top = 0;
+    if (A.T) {
+      const u32 raw = *reinterpret_cast<const u32*>(g_sm + so + G.W4 + 4 * j);
+      top = (tops_ix(A, ln) & 1u) ? (int)(short)(raw >> 16) : (int)(short)(raw & 0xFFFFu);
+    }
+    if (ln == CL - 1) top += (int)*reinterpret_cast<const long long*>(g_sm + so + G.HO);
+    if (src >= CL) {
+      Ch<CW> w;
+      lds_ch(w, so, j, G.C);
+      top = exact_from<CW>(w, top, true);
+      sts_ch(so, j, G.C, w);
+    }
+    sts_i32(so + G.W4 + 4 * j, top);
   }
-  __syncthreads();
-  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
-  const u32 lq = G.logC + lpc;
-  const u32 tot = (s1 - s0) << lq;
-  for (u32 idx = tid; idx < tot; idx += NT) {
-    const u32 k = s0 + (idx >> lq), rem = idx & ((1u << lq) - 1);
-    const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
-    const u32 src = (lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1);
-    const u32 ln = src & CLm;
-    cp_async16(smem_base + piece_off(k * G.SB, j, q, G.C), gbase + (u64)k * gstride + (u64)ln * (CB / 8) + 16u * q);
-  }
-  const u32 ttot = (s1 - s0) << G.logC;
-  for (u32 idx = tid; idx < ttot; idx += NT) {
-    const u32 k = s0 + (idx >> G.logC), j = idx & G.Cm;
-    const u32 src = (lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1);
-    const u32 ln = src & CLm;
-    const u64 e = lf.base + (u64)k * lf.stride;
-    int v = (int)__ldcg(A.T + e * CL + tops_ix(A, ln));
-    if (ln == CLm) v += (int)__ldcg(reinterpret_cast<const long long*>(gbase + (u64)k * gstride + W4e));
-    sts_i32(k * G.SB + G.W4 + 4 * j, v);
-  }
+}
+
+__device__ __forceinline__ bool small_ticket(const Args& A, const DevClass& cl) {
+  return cl.L * cl.slot_bytes <= A.half;
 }
 
 template <int CW, int NT>
@@ -629,12 +666,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   __shared__ u32 s_tk[2];
   __shared__ DevLeaf s_lf[2];
   __shared__ DevClass s_cl[2];
+  __shared__ u32 s_boff[2];
   __shared__ int s_ready;  // next leaf's dependency already satisfied
   __shared__ u32 s_cached;
   __shared__ OpT s_ops[kCacheOps];
   __shared__ u32 s_lev[kCacheLev + 1];
   __shared__ SymExp s_crot[kCacheRot];
-  __shared__ u32 s_rho[2][kMaxSlots];
+  __shared__ u32 s_rho[2][kMaxSlots];  // coset: lane pre-rotation per loaded slot
+  __shared__ u32 s_rhp[kMaxSlots];     // coset: lane post-rotation per stored slot
   const u32 tid = threadIdx.x;
   constexpr u32 nthr = NT;
   const u32 CL = A.lanes, CLm = CL - 1;
@@ -648,6 +687,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   if (tid == 0) {
     const u32 t = atomicAdd(&A.counters[0], 1u);
     s_tk[0] = t;
+    s_boff[0] = 0;
     if (t < A.nleaves) {
       s_lf[0] = A.leaves[t];
       s_cl[0] = A.classes[s_lf[0].cls];
@@ -657,7 +697,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     s_cached = 0xFFFFFFFFu;
   }
   __syncthreads();
-  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, tid, s_rho[0]);
+  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, 0, tid, s_rho[0]);
   u32 cur = 0;
 
   for (;;) {
@@ -665,6 +705,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     if (ticket >= A.nleaves) break;
     const DevLeaf lf = s_lf[cur];
     const DevClass cl = s_cl[cur];
+    const u32 boff = s_boff[cur];
     const Geo G = geo_of(cl, lf, CW);
     const u32 C = G.C, Cm = G.Cm, logC = G.logC, SB = G.SB, W4 = G.W4;
     // fixed thread geometry for this leaf: chunk i of group g; NG groups side by side
@@ -673,7 +714,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     fi.init(i, C);
     const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
     const u32 nxt = cur ^ 1;
-    // fetch the next ticket and descriptor now; they are consumed a leaf later
+    // fetch the next ticket and descriptor now
     if (tid == 0) {
       const u32 t = atomicAdd(&A.counters[0], 1u);
       s_tk[nxt] = t;
@@ -684,6 +725,16 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         const DevLeaf& nl = s_lf[nxt];
         s_ready = (nl.dep == kNoDep) || (ld_acquire(&A.counters[1 + nl.dep]) >= nl.dep_target);
       }
+    }
+    __syncthreads();
+    const bool have_next = s_tk[nxt] < A.nleaves;
+    // double buffering: a small next ticket whose inputs are ready streams into
+    // the other buffer while this one computes
+    bool prefetched = false;
+    if (have_next && s_ready && small_ticket(A, cl) && small_ticket(A, s_cl[nxt])) {
+      if (tid == 0) s_boff[nxt] = boff ^ A.half;
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt]);
+      prefetched = true;
     }
     // leaf-program cache
     const bool cached = cl.nops <= kCacheOps && cl.nlevels <= kCacheLev && cl.nload + cl.nstore <= kCacheRot;
@@ -698,34 +749,27 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       for (u32 x = tid; x < cl.nload; x += nthr) s_crot[x] = A.rots[cl.pre_begin + x];
       for (u32 x = tid; x < cl.nstore; x += nthr) s_crot[cl.nload + x] = A.rots[cl.post_begin + x];
     }
-    cp_async_wait_all();
+    if (G.coset) {
+      for (u32 k = tid; k < cl.nstore; k += nthr) {
+        const SymExp P = A.rots[cl.post_begin + k];
+        s_rhp[k] = (u32)(post_exp(A, cl, lf, P, k) / CB);
+      }
+    }
+    if (prefetched)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
     __syncthreads();
     if (tid == 0 && cached) s_cached = lf.cls;
+    if (tid == 0 && lf.lbar != kNoDep) atomicAdd(&A.counters[1 + lf.lbar], 1u);  // inputs are in
     pc.mark(PH_LOAD);
+    fixup<CW, NT>(A, lf, cl, boff, tid, s_rho[cur]);
+    __syncthreads();
     std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
     const u64 gstride = lf.stride * A.elem_bytes;
 
-    if (G.coset) {
-      // ---- coset leaf: negate the lanes that wrapped past 2^N on the way in --------
-      bool any = false;
-      for (u32 k = 0; k < cl.nload; ++k) any |= (s_rho[cur][k] != 0);
-      if (any) {
-        for (u32 idx = tid; idx < (cl.nload << logC); idx += nthr) {
-          const u32 k = idx >> logC, j = idx & Cm;
-          const u32 src = (lane_of(G, j) + 2 * CL - s_rho[cur][k]) & (2 * CL - 1);
-          if (src >= CL) {
-            Ch<CW> w;
-            lds_ch(w, k * SB, j, C);
-            int tp = lds_i32(k * SB + W4 + 4 * j);
-            tp = exact_from<CW>(w, tp, true);
-            sts_ch(k * SB, j, C, w);
-            sts_i32(k * SB + W4 + 4 * j, tp);
-          }
-        }
-        __syncthreads();
-      }
-    } else if (cl.has_pre || lf.tpre) {
-      // ---- pre-rotations (ITFT spectral inputs), in place: NG slots per round -------
+    if (!G.coset && (cl.has_pre || lf.tpre)) {
+      // ---- pre-rotations (whole tickets), in place: NG slots per round --------------
       for (u32 b0 = 0; b0 < cl.nload; b0 += NG) {
         const u32 sl = b0 + g;
         const bool act = sl < cl.nload;
@@ -734,13 +778,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         if (act) {
           const SymExp P = cached ? s_crot[sl] : A.rots[cl.pre_begin + sl];
           const Rot R = make_rot<CW>(pre_exp(A, cl, lf, P, sl), A.N);
-          const bool neg = rot_chunk<CW>(w, tp, sl * SB, sl * SB + W4, R, Cm, i);
+          const u32 so = boff + sl * SB;
+          const bool neg = rot_chunk<CW>(w, tp, so, so + W4, R, Cm, i);
           tp = exact_from<CW>(w, tp, neg);
         }
         __syncthreads();
         if (act) {
-          sts_at<CW>(sl * SB, fi, w);
-          sts_i32(sl * SB + ti, tp);
+          sts_at<CW>(boff + sl * SB, fi, w);
+          sts_i32(boff + sl * SB + ti, tp);
         }
         __syncthreads();
       }
@@ -779,7 +824,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           hdst[k] = 0xFFFFFFFFu;
           const u32 x = g + NG * k;
           if (x >= nb) continue;
-          const OpT op = s_ops[sbase + x];
+          OpT op = s_ops[sbase + x];
+          op.aw += boff;
+          op.bw += boff;
           Ch<CW> a;
           lds_at(a, op.aw, fi);
           const int pa = lds_i32(op.aw + ti);
@@ -833,24 +880,29 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     }
     pc.mark(PH_LEVELS);
 
-    const bool have_next = s_tk[nxt] < A.nleaves;
-    bool next_issued = false;
     if (G.coset) {
-      // ---- coset leaf: lanes out through the post-rotation, carry-save -------------
+      if (lf.lbar != kNoDep) {  // every ticket of this leaf has read its lanes
+        if (tid == 0) {
+          const u32 tgt = A.cmeta[lf.lbar].target;
+          while (ld_acquire(&A.counters[1 + lf.lbar]) < tgt) __nanosleep(32);
+        }
+        __syncthreads();
+      }
+      // ---- coset ticket: lanes out through the post-rotation, carry-save -----------
       // (1) per chunk: negate wrapped lanes in place, write the tops array, and
       //     clear the element top word where this ticket owns lane C-1
       for (u32 idx = tid; idx < (cl.nstore << logC); idx += nthr) {
         const u32 k = idx >> logC, j = idx & Cm;
-        const SymExp P = cached ? s_crot[cl.nload + k] : A.rots[cl.post_begin + k];
-        const u32 rho = (u32)(post_exp(A, cl, lf, P, k) / CB);
+        const u32 rho = s_rhp[k];
         const u32 dst = (lane_of(G, j) + rho) & (2 * CL - 1);
         const u32 d = dst & CLm;
-        int tp = lds_i32(k * SB + W4 + 4 * j);
+        const u32 so = boff + k * SB;
+        int tp = lds_i32(so + W4 + 4 * j);
         if (dst >= CL) {
           Ch<CW> w;
-          lds_ch(w, k * SB, j, C);
+          lds_ch(w, so, j, C);
           tp = exact_from<CW>(w, tp, true);
-          sts_ch(k * SB, j, C, w);
+          sts_ch(so, j, C, w);
         }
         const u64 e = lf.base + (u64)k * lf.stride;
         __stcg(A.T + e * CL + tops_ix(A, d), (short)tp);
@@ -871,11 +923,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         for (u32 idx = tid; idx < tot; idx += nthr) {
           const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
           const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
-          const SymExp P = cached ? s_crot[cl.nload + k] : A.rots[cl.post_begin + k];
-          const u32 rho = (u32)(post_exp(A, cl, lf, P, k) / CB);
-          const u32 d = (lane_of(G, j) + rho) & CLm;
+          const u32 d = (lane_of(G, j) + s_rhp[k]) & CLm;
           __stcg(reinterpret_cast<uint4*>(gbase + (u64)k * gstride + (u64)d * (CB / 8) + 16u * q),
-                 *reinterpret_cast<const uint4*>(g_sm + piece_off(k * SB, j, q, C)));
+                 *reinterpret_cast<const uint4*>(g_sm + piece_off(boff + k * SB, j, q, C)));
         }
       }
       __syncthreads();  // slot reuse
@@ -886,10 +936,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         const u32 nb = min(cl.nstore - b0, NG);
         const u32 sl = b0 + g;
         const bool act = g < nb;
+        const u32 so = boff + sl * SB;
         Ch<CW> w;
         int top = 0;
         if (act && (A.debug_skip & 2)) {
-          lds_at(w, sl * SB, fi);
+          lds_at(w, so, fi);
           sts_i32(scr + 4 * tid, 0);
         } else if (act) {
           const SymExp P = cached ? s_crot[cl.nload + sl] : A.rots[cl.post_begin + sl];
@@ -897,11 +948,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           bool neg;
           if (R.o == 0) {
             const u32 j = (i - R.q) & Cm;
-            lds_ch(w, sl * SB, j, C);
-            top = lds_i32(sl * SB + W4 + 4 * j);
+            lds_ch(w, so, j, C);
+            top = lds_i32(so + W4 + 4 * j);
             neg = ((i < R.q) ? 1u : 0u) != R.sneg;
           } else {
-            neg = rot_chunk<CW>(w, top, sl * SB, sl * SB + W4, R, Cm, i);
+            neg = rot_chunk<CW>(w, top, so, so + W4, R, Cm, i);
           }
           top = exact_from<CW>(w, top, neg);
           sts_i32(scr + 4 * tid, top);
@@ -942,16 +993,16 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         // resolved chunks back into their (free) slots, then a coalesced copy
         // of whole elements to HBM (full 32-byte sectors per request)
         if (act) {
-          sts_at<CW>(sl * SB, fi, w);
-          if (i == Cm) sts_i32(sl * SB + W4, top);
+          sts_at<CW>(so, fi, w);
+          if (i == Cm) sts_i32(so + W4, top);
         }
         __syncthreads();  // scratch reuse
         pc.mark(PH_STORE);
       }
       // the whole leaf is resolved in shared memory: one coalesced copy to HBM
-      copy_slots<CW, false, NT>(G, gbase, gstride, 0, cl.nstore, smem_base, tid);
+      copy_slots<CW, false, NT>(G, gbase, gstride, 0, cl.nstore, smem_base, boff, tid);
       for (u32 x = tid; x < cl.nstore; x += nthr)
-        __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4e), (long long)lds_i32(x * SB + W4));
+        __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4e), (long long)lds_i32(boff + x * SB + W4));
       if (A.T) {  // element format out: the lanes carry no tops
         if ((CL & 7) == 0) {
           const u32 per = CL / 8;  // 16-byte groups of int16 tops per element
@@ -968,12 +1019,6 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       }
       __syncthreads();  // slot reuse
     }
-    // this leaf is out of shared memory: if the next leaf's dependency is
-    // already met, stream its inputs in now so they overlap our HBM stores
-    if (have_next && s_ready) {
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, s_rho[nxt]);
-      next_issued = true;
-    }
     pc.mark(PH_STORE);
     // publish completion: bump the phase counter; the last child of a node's
     // last phase finishes the node and reports to the parent phase in turn
@@ -988,14 +1033,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         k = cm.next;
       }
     }
-    if (have_next && !next_issued) {
+    if (have_next && !prefetched) {
       if (tid == 0) {
         const DevLeaf& nl = s_lf[nxt];
         if (nl.dep != kNoDep)
           while (ld_acquire(&A.counters[1 + nl.dep]) < nl.dep_target) __nanosleep(64);
+        s_boff[nxt] = 0;
       }
       __syncthreads();
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, tid, s_rho[nxt]);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt]);
     }
     pc.mark(PH_WAIT);
     cur = nxt;

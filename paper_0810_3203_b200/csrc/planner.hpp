@@ -125,7 +125,10 @@ struct DevLeaf {
   // (tpost); 0 elsewhere
   u64 tpre, tpost;
   u32 c0;          // coset leaves: first coset of this ticket
-  u32 pad;
+  // coset leaves of several tickets, in place: counter of tickets whose
+  // inputs are in shared memory; no ticket stores before all have loaded
+  // (their lane sets differ between load and store)
+  u32 lbar;
 };
 static_assert(sizeof(DevLeaf) == 64, "DevLeaf layout");
 
@@ -182,6 +185,12 @@ struct RingShape {
   unsigned coset_max_ell = 0;
   u64 slot_budget = 0;  // shared-memory bytes available for a leaf's slots
 };
+
+// Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
+// the element's 64-bit top word; 16-byte aligned.
+inline u32 fermat_slot_bytes(u64 cs, u64 lane_bytes) {
+  return (u32)((cs * lane_bytes + ((cs * 4 + 7) & ~u64(7)) + 8 + 15) & ~u64(15));
+}
 
 inline u64 bitrev(u64 j, unsigned ell) {
   u64 r = 0;
@@ -523,13 +532,14 @@ class Planner {
   }
 
   u64 lanes2() const { return rs_.M / rs_.lane_bits; }  // 2C
-  u32 coset_slot_bytes(u64 cs) const { return (u32)((cs * (rs_.lane_bits / 8) + cs * 4 + 15) & ~u64(15)); }
+  u32 coset_slot_bytes(u64 cs) const { return fermat_slot_bytes(cs, rs_.lane_bits / 8); }
 
+  // coset tickets must fit one of the two ticket buffers (double buffering)
   bool coset_fits(unsigned ell) const {
     if (!rs_.lane_bits || ell > rs_.coset_max_ell || ell < 1) return false;
     if ((u64{1} << ell) > lanes2()) return false;  // step >= 1
     const u64 cs = u64{1} << (ell - 1);
-    return (u64{1} << ell) * coset_slot_bytes(cs) <= rs_.slot_budget;
+    return (u64{1} << ell) * coset_slot_bytes(cs) <= rs_.slot_budget / 2;
   }
 
   // every op rotation a multiple of the coset step, every pre/post rotation a
@@ -558,6 +568,7 @@ class Planner {
   void emit_whole(bool inv, unsigned ell, u64 z, u64 n, int f, u64 base, u64 stride, int policy, const Ctx& cx,
                   u32 wave0, DevLeaf lf) {
     lf.cls = class_of(ClassKey{inv ? 1 : 0, ell, z, n, f, 0}, policy);
+    lf.lbar = kNoDep;
     lf.dep = cx.dep;
     lf.dep_target = cx.dep_target;
     lf.comp = cx.report;
@@ -577,6 +588,11 @@ class Planner {
     lf.base = base;
     lf.stride = stride;
     const u64 groups = c.step / c.m;
+    lf.lbar = kNoDep;
+    if (groups > 1) {
+      lf.lbar = (u32)counters_.size();
+      counters_.push_back(DevCounter{(u32)groups, kNoDep});
+    }
     for (u64 g = 0; g < groups; ++g) {
       lf.c0 = (u32)(g * c.m);
       push_leaf(lf, cx, wave0);
@@ -604,7 +620,8 @@ class Planner {
       prog.step = (u32)(lanes2() >> k.ell);
       const u64 cl = u64{1} << (k.ell - 1);  // lanes per coset
       u64 m = 1;
-      while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.slot_budget) m *= 2;
+      while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.slot_budget / 2)
+        m *= 2;
       prog.m = (u32)m;
       prog.cs = (u32)(m * cl);
       prog.slot_bytes = coset_slot_bytes(prog.cs);
