@@ -54,6 +54,8 @@ struct DevicePlan {
   const SymExp* rots = nullptr;
   const DevLeaf* leaves = nullptr;
   const DevCounter* cmeta = nullptr;
+  const u64* locbits = nullptr;
+  const u64* shadow_finals = nullptr;
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
@@ -145,7 +147,9 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   size_t o_rot = al(o_lev + levels.size() * sizeof(u32));
   size_t o_lf = al(o_rot + rots.size() * sizeof(SymExp));
   size_t o_cm = al(o_lf + leaves.size() * sizeof(DevLeaf));
-  size_t total = al(o_cm + cm.size() * sizeof(DevCounter)) + 256;
+  size_t o_lb = al(o_cm + cm.size() * sizeof(DevCounter));
+  size_t o_sf = al(o_lb + p.locbits.size() * sizeof(u64));
+  size_t total = al(o_sf + p.shadow_finals.size() * sizeof(u64)) + 256;
   std::vector<std::uint8_t> h(total, 0);
   std::memcpy(h.data() + o_cls, cls.data(), cls.size() * sizeof(DevClass));
   std::memcpy(h.data() + o_ops, ops.data(), ops.size() * sizeof(DevOp));
@@ -153,6 +157,9 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   std::memcpy(h.data() + o_rot, rots.data(), rots.size() * sizeof(SymExp));
   std::memcpy(h.data() + o_lf, leaves.data(), leaves.size() * sizeof(DevLeaf));
   std::memcpy(h.data() + o_cm, cm.data(), cm.size() * sizeof(DevCounter));
+  if (!p.locbits.empty()) std::memcpy(h.data() + o_lb, p.locbits.data(), p.locbits.size() * sizeof(u64));
+  if (!p.shadow_finals.empty())
+    std::memcpy(h.data() + o_sf, p.shadow_finals.data(), p.shadow_finals.size() * sizeof(u64));
   CUDA_TRY(cudaMalloc(&dp.dbuf, total));
   CUDA_TRY(cudaMemcpyAsync(dp.dbuf, h.data(), total, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // h is a temporary
@@ -163,6 +170,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.rots = reinterpret_cast<const SymExp*>(b + o_rot);
   dp.leaves = reinterpret_cast<const DevLeaf*>(b + o_lf);
   dp.cmeta = reinterpret_cast<const DevCounter*>(b + o_cm);
+  dp.locbits = reinterpret_cast<const u64*>(b + o_lb);
+  dp.shadow_finals = reinterpret_cast<const u64*>(b + o_sf);
   (void)R;
   return CFTFT_OK;
 }
@@ -180,8 +189,11 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   if (rs.fermat) {
     const bool on = R->coset_cw > 0 || (R->coset_cw < 0 && R->N >= 4096 && R->NT == 512);
     if (on && L >= 4) {
+      static const int env_cw = getenv("CFTFT_COSET_CW") ? atoi(getenv("CFTFT_COSET_CW")) : 0;
       if (R->coset_cw > 0) {
         cw = (u32)R->coset_cw;
+      } else if (env_cw == 4 || env_cw == 8 || env_cw == 16) {
+        cw = (u32)env_cw;
       } else {
         const unsigned ell = (unsigned)__builtin_ctzll(L);
         const u64 lnode = u64{1} << (ell - ell / 2);
@@ -193,7 +205,7 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       if (cw > R->D) cw = R->D;
       C = R->D / cw;
       sb = fermat_slot_bytes(C, 4 * cw);
-      const size_t budget = kSmemBudget - scratch_bytes(R->NT);
+      const size_t budget = kSmemBudget - scratch_bytes(1024);
       unsigned lam = 1;
       while (lam < 10 && ((size_t)sb << (lam + 1)) <= budget) ++lam;
       if (R->leaf_limit) lam = std::min(lam, R->leaf_limit);
@@ -213,6 +225,10 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   }
   rs.C = C;
   rs.slot_bytes = sb;
+  static const int env_ov = getenv("CFTFT_OVERLAP") ? atoi(getenv("CFTFT_OVERLAP")) : 0;
+  rs.wave_overlap = (u32)std::max(0, env_ov);
+  static const int env_l2 = getenv("CFTFT_L2MB") ? atoi(getenv("CFTFT_L2MB")) : 0;
+  if (env_l2 > 0) rs.l2_budget = (u64)env_l2 << 20;
   if (dp) {
     dp->cw = cw;
     dp->C = C;
@@ -302,20 +318,39 @@ int grid_for(K kernel, int threads, size_t smem, u64 nleaves, unsigned* grid) {
   return CFTFT_OK;
 }
 
+// Per-launch scratch (counters, tops arrays, the shadow buffer) comes from the
+// device's stream-ordered pool; keep freed blocks cached instead of returning
+// them to the driver at every synchronisation.
+int keep_pool() {
+  static std::mutex m;
+  static std::vector<int> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(m);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return CFTFT_OK;
+  cudaMemPool_t pool;
+  CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  u64 thr = ~u64{0};
+  CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done.push_back(dev);
+  return CFTFT_OK;
+}
+
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
   u64 launches = 0;
+  if (int rc = keep_pool()) return rc;
   if (dp.nleaves) {
     u32* counters = nullptr;
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
     // Fermat: two ticket buffers of `half` bytes each (a big ticket spans both)
-    const size_t half = ((kSmemBudget - scratch_bytes(R->NT)) / 2) & ~size_t(15);
+    const size_t half = ((kSmemBudget - scratch_bytes(1024)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
                                    ? std::max<size_t>({dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell, 2 * half})
                                    : (size_t)R->slot_bytes << dp.max_ell;
-    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
+    const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(1024) : 0);
     unsigned grid = 1;
     short* tops = nullptr;
     if (R->kind == CFTFT_RING_FERMAT) {
@@ -340,12 +375,17 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.lanes = dp.C;
       A.logLanes = (u32)__builtin_ctz(dp.C);
       A.logS = dp.logS;
+      std::uint8_t* shadow = nullptr;
       if (dp.host.coset) {
-        const size_t tb = (size_t)dp.host.extent * dp.C * sizeof(short);
+        const size_t tb = 2 * (size_t)dp.host.extent * dp.C * sizeof(short);
         CUDA_TRY(cudaMallocAsync((void**)&tops, tb, st));
         CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
+        CUDA_TRY(cudaMallocAsync((void**)&shadow, (size_t)dp.host.extent * stride, st));
       }
       A.T = tops;
+      A.data2 = shadow;
+      A.tloc = (u64)dp.host.extent * dp.C;
+      A.locbits = dp.locbits;
       A.half = (u32)half;
       unsigned long long* prof = nullptr;
       static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
@@ -363,10 +403,16 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         return CFTFT_OK;
       };
       int rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
-               : dp.cw == 8 ? (R->NT == 1024 ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
+               : dp.cw == 8 ? (getenv("CFTFT_NT1024") ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
                             : go(fermat::leaf_kernel<4, 512>, 512);
       if (rc) return rc;
       if (tops) {
+        if (!dp.host.shadow_finals.empty()) {
+          fermat::shadow_copy_kernel<<<(unsigned)dp.host.shadow_finals.size(), 256, 0, st>>>(
+              base, shadow, stride, tops, A.tloc, dp.C, dp.shadow_finals, R->D);
+          ++launches;
+        }
+        CUDA_TRY(cudaFreeAsync(shadow, st));
         // carry-save lanes of the outputs (a batch: of every element it touched)
         // back to the canonical element format
         const u64 cnt = dp.host.final_count ? dp.host.final_count : dp.host.extent;
@@ -505,8 +551,12 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
     os << (i ? "," : "") << "[" << lf.cls << "," << lf.base << "," << lf.stride << "," << lf.s << ","
        << (lf.dep == kNoDep ? -1 : (long long)lf.dep) << "," << lf.dep_target << ","
        << (lf.comp == kNoDep ? -1 : (long long)lf.comp) << "," << p.leaf_wave[i] << "," << lf.tpre << ","
-       << lf.tpost << "," << lf.c0 << "]";
+       << lf.tpost << "," << lf.c0 << "," << (lf.locoff == kNoDep ? -1 : (long long)lf.locoff) << "]";
   }
+  os << "],\"locbits\":[";
+  for (size_t i = 0; i < p.locbits.size(); ++i) os << (i ? "," : "") << p.locbits[i];
+  os << "],\"shadow_finals\":[";
+  for (size_t i = 0; i < p.shadow_finals.size(); ++i) os << (i ? "," : "") << p.shadow_finals[i];
   os << "]}";
 }
 
@@ -744,7 +794,7 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
       np->host.classes.push_back(lp);
       for (u64 i = 0; i < count; ++i) {
         DevLeaf lf{};
-        lf.lbar = kNoDep;
+        lf.locoff = kNoDep;
         lf.cls = 0;
         lf.dep = kNoDep;
         lf.comp = kNoDep;

@@ -51,7 +51,10 @@ struct Args {
   u32 logC;
   u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
-  short* T;                // carry-save tops, [view element][lane] (nullptr: not in use)
+  short* T;                // carry-save tops, [buffer][view element][lane] (nullptr: not in use)
+  std::uint8_t* data2;     // shadow buffer (same element stride), coset plans
+  u64 tloc;                // tops entries per buffer
+  const u64* locbits;      // per-slot buffer bits (DevLeaf::locoff)
   u32 half;                // bytes of one of the two ticket buffers (double buffering)
   u32 lanes, logLanes;     // lanes (chunks) per element
   u32 logS;                // tops-array lane interleave
@@ -536,19 +539,33 @@ __device__ __forceinline__ Rot op_rot(const Args& A, const Geo& g, u64 r) {
 // x of the range lives at g0 + x*gstride and in slot (s0 + x), x < nslots.
 // The per-thread piece positions are fixed, so the loop body is a couple of
 // adds (no division, no 64-bit multiply).
+constexpr u32 kMaskWords = 16;  // per-slot buffer bits of up to 1024 slots
+__device__ __forceinline__ u32 in_buf(const u64* m, u32 k) { return (u32)(m[2 * (k >> 6)] >> (k & 63)) & 1u; }
+__device__ __forceinline__ u32 out_buf(const u64* m, u32 k) { return (u32)(m[2 * (k >> 6) + 1] >> (k & 63)) & 1u; }
+__device__ __forceinline__ std::uint8_t* elem_ptr(const Args& A, u32 buf, u64 e) {
+  return (buf ? A.data2 : A.data) + e * A.elem_bytes;
+}
+__device__ __forceinline__ short* tops_row(const Args& A, u32 buf, u64 e) {
+  return A.T + (buf ? A.tloc : 0) + e * A.lanes;
+}
+
 template <int CW, bool kLoad, int NT>
-__device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 gstride, u32 s0, u32 nslots,
+__device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const DevLeaf& lf, const u64* locm, u32 nslots,
                                            u32 smem_base, u32 boff, u32 tid) {
   constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
   const u32 C = G.C, SB = G.SB;
   const u32 lq = G.logC + lpc, q16 = 1u << lq;  // pieces per slot
+  auto slot_ptr = [&](u32 x) {
+    const u32 b = kLoad ? in_buf(locm, x) : out_buf(locm, x);
+    return elem_ptr(A, b, lf.base + (u64)x * lf.stride);
+  };
   if (q16 >= (u32)NT) {
     // each thread copies pieces tid, tid+NT, ... of every slot
     for (u32 pp = tid; pp < q16; pp += NT) {
       const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
-      std::uint8_t* g = g0 + 16u * pp;
-      u32 so = boff + s0 * SB + so0;
-      for (u32 x = 0; x < nslots; ++x, g += gstride, so += SB) {
+      u32 so = boff + so0;
+      for (u32 x = 0; x < nslots; ++x, so += SB) {
+        std::uint8_t* g = slot_ptr(x) + 16u * pp;
         if (kLoad)
           cp_async16(smem_base + so, g);
         else
@@ -559,10 +576,9 @@ __device__ __forceinline__ void copy_slots(const Geo& G, std::uint8_t* g0, u64 g
     // NT/q16 slots side by side; each thread keeps one piece position
     const u32 pp = tid & (q16 - 1), x0 = tid >> lq, step = (u32)NT >> lq;
     const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
-    std::uint8_t* g = g0 + (u64)x0 * gstride + 16u * pp;
-    const u64 gstep = (u64)step * gstride;
-    u32 so = boff + (s0 + x0) * SB + so0;
-    for (u32 x = x0; x < nslots; x += step, g += gstep, so += step * SB) {
+    u32 so = boff + x0 * SB + so0;
+    for (u32 x = x0; x < nslots; x += step, so += step * SB) {
+      std::uint8_t* g = slot_ptr(x) + 16u * pp;
       if (kLoad)
         cp_async16(smem_base + so, g);
       else
@@ -582,45 +598,49 @@ constexpr u32 kMaxSlots = 64;
 // slot's element top word.  fixup() turns these into int32 tops once landed.
 template <int CW, int NT>
 __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 boff, u32 tid, u32* rho) {
+                                           u32 boff, u32 tid, u32* rho, u64* locm) {
   const Geo G = geo_of(cl, lf, CW);
   const u32 nl = cl.nload;
+  constexpr u32 CB = 32 * CW;
+  // stage the ticket's per-slot buffer bits and (coset) lane pre-rotations
+  const u32 span = max(cl.nload, cl.nstore), nw = (span + 63) >> 6;
+  for (u32 x = tid; x < 2 * kMaskWords; x += NT)
+    locm[x] = (lf.locoff != kNoDep && x < 2 * nw) ? A.locbits[lf.locoff + x] : 0ull;
+  if (G.coset) {
+    for (u32 k = tid; k < nl; k += NT) {
+      const SymExp P = A.rots[cl.pre_begin + k];
+      rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
+    }
+  }
+  __syncthreads();
   if (nl) {
-    constexpr u32 CB = 32 * CW;
     constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
-    const u64 eb = A.elem_bytes;
-    std::uint8_t* const gbase = A.data + lf.base * eb;
-    const u64 gstride = lf.stride * eb;
     const u32 CL = A.lanes;
     const u32 sb = smem_base + boff;
     if (G.coset) {
-      for (u32 k = tid; k < nl; k += NT) {
-        const SymExp P = A.rots[cl.pre_begin + k];
-        rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
-      }
-      __syncthreads();
       const u32 lq = G.logC + lpc;
       const u32 tot = nl << lq;
       for (u32 idx = tid; idx < tot; idx += NT) {
         const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
         const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
         const u32 ln = (lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1);
-        cp_async16(sb + piece_off(k * G.SB, j, q, G.C), gbase + (u64)k * gstride + (u64)ln * (CB / 8) + 16u * q);
+        std::uint8_t* g = elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
+        cp_async16(sb + piece_off(k * G.SB, j, q, G.C), g + (u64)ln * (CB / 8) + 16u * q);
       }
     } else {
-      copy_slots<CW, true, NT>(G, gbase, gstride, 0, nl, smem_base, boff, tid);
+      copy_slots<CW, true, NT>(A, G, lf, locm, nl, smem_base, boff, tid);
     }
     if (A.T) {
       const u32 tt = nl << G.logC;
       for (u32 idx = tid; idx < tt; idx += NT) {
         const u32 k = idx >> G.logC, j = idx & G.Cm;
         const u32 ln = G.coset ? ((lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1)) : j;
-        const u64 e = lf.base + (u64)k * lf.stride;
-        cp_async4(sb + k * G.SB + G.W4 + 4 * j, A.T + e * CL + (tops_ix(A, ln) & ~1u));
+        const short* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
+        cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, ln) & ~1u));
       }
     }
     for (u32 k = tid; k < nl; k += NT)
-      cp_async8(sb + k * G.SB + G.HO, gbase + (u64)k * gstride + 4ull * A.D);
+      cp_async8(sb + k * G.SB + G.HO, elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride) + 4ull * A.D);
   }
   cp_async_commit();
 }
@@ -673,6 +693,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   __shared__ u32 s_lev[kCacheLev + 1];
   __shared__ SymExp s_crot[kCacheRot];
   __shared__ u32 s_rho[2][kMaxSlots];  // coset: lane pre-rotation per loaded slot
+  __shared__ u64 s_loc[2][2 * kMaskWords];  // per-slot buffer bits
   __shared__ u32 s_rhp[kMaxSlots];     // coset: lane post-rotation per stored slot
   const u32 tid = threadIdx.x;
   constexpr u32 nthr = NT;
@@ -697,7 +718,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     s_cached = 0xFFFFFFFFu;
   }
   __syncthreads();
-  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, 0, tid, s_rho[0]);
+  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, 0, tid, s_rho[0], s_loc[0]);
   u32 cur = 0;
 
   for (;;) {
@@ -714,7 +735,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     fi.init(i, C);
     const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
     const u32 nxt = cur ^ 1;
-    // fetch the next ticket and descriptor now
+    // fetch the next ticket now; when small and ready, prefetch it into the
+    // other buffer so its loads overlap this ticket's work
+    bool prefetched = false;
     if (tid == 0) {
       const u32 t = atomicAdd(&A.counters[0], 1u);
       s_tk[nxt] = t;
@@ -728,12 +751,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     }
     __syncthreads();
     const bool have_next = s_tk[nxt] < A.nleaves;
-    // double buffering: a small next ticket whose inputs are ready streams into
-    // the other buffer while this one computes
-    bool prefetched = false;
     if (have_next && s_ready && small_ticket(A, cl) && small_ticket(A, s_cl[nxt])) {
       if (tid == 0) s_boff[nxt] = boff ^ A.half;
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt]);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt], s_loc[nxt]);
       prefetched = true;
     }
     // leaf-program cache
@@ -761,12 +781,10 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       cp_async_wait<0>();
     __syncthreads();
     if (tid == 0 && cached) s_cached = lf.cls;
-    if (tid == 0 && lf.lbar != kNoDep) atomicAdd(&A.counters[1 + lf.lbar], 1u);  // inputs are in
     pc.mark(PH_LOAD);
     fixup<CW, NT>(A, lf, cl, boff, tid, s_rho[cur]);
     __syncthreads();
-    std::uint8_t* const gbase = A.data + lf.base * A.elem_bytes;
-    const u64 gstride = lf.stride * A.elem_bytes;
+    const u64* const locm = s_loc[cur];
 
     if (!G.coset && (cl.has_pre || lf.tpre)) {
       // ---- pre-rotations (whole tickets), in place: NG slots per round --------------
@@ -881,13 +899,6 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     pc.mark(PH_LEVELS);
 
     if (G.coset) {
-      if (lf.lbar != kNoDep) {  // every ticket of this leaf has read its lanes
-        if (tid == 0) {
-          const u32 tgt = A.cmeta[lf.lbar].target;
-          while (ld_acquire(&A.counters[1 + lf.lbar]) < tgt) __nanosleep(32);
-        }
-        __syncthreads();
-      }
       // ---- coset ticket: lanes out through the post-rotation, carry-save -----------
       // (1) per chunk: negate wrapped lanes in place, write the tops array, and
       //     clear the element top word where this ticket owns lane C-1
@@ -905,13 +916,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           sts_ch(so, j, C, w);
         }
         const u64 e = lf.base + (u64)k * lf.stride;
-        __stcg(A.T + e * CL + tops_ix(A, d), (short)tp);
+        const u32 ob = out_buf(locm, k);
+        __stcg(tops_row(A, ob, e) + tops_ix(A, d), (short)tp);
         if (j == 0) {
-          // the ticket that read lane C-1 (or, for an output-only slot, writes it)
-          // folded the element top word into its lane tops: clear it
+          // one ticket per slot (the one that read lane C-1, or for an output-
+          // only slot writes it) sets the output's element top word to zero:
+          // the value now lives in the lanes and their tops
           const u32 pstar = k < cl.nload ? ((CLm + s_rho[cur][k]) & CLm) : ((CLm + 2 * CL - rho) & CLm);
           if (((pstar & (G.step - 1)) - G.c0) < G.m)
-            __stcg(reinterpret_cast<long long*>(gbase + (u64)k * gstride + W4e), 0ll);
+            __stcg(reinterpret_cast<long long*>(elem_ptr(A, ob, e) + W4e), 0ll);
         }
       }
       __syncthreads();
@@ -924,7 +937,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
           const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
           const u32 d = (lane_of(G, j) + s_rhp[k]) & CLm;
-          __stcg(reinterpret_cast<uint4*>(gbase + (u64)k * gstride + (u64)d * (CB / 8) + 16u * q),
+          std::uint8_t* g = elem_ptr(A, out_buf(locm, k), lf.base + (u64)k * lf.stride);
+          __stcg(reinterpret_cast<uint4*>(g + (u64)d * (CB / 8) + 16u * q),
                  *reinterpret_cast<const uint4*>(g_sm + piece_off(boff + k * SB, j, q, C)));
         }
       }
@@ -1000,20 +1014,22 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         pc.mark(PH_STORE);
       }
       // the whole leaf is resolved in shared memory: one coalesced copy to HBM
-      copy_slots<CW, false, NT>(G, gbase, gstride, 0, cl.nstore, smem_base, boff, tid);
+      copy_slots<CW, false, NT>(A, G, lf, locm, cl.nstore, smem_base, boff, tid);
       for (u32 x = tid; x < cl.nstore; x += nthr)
-        __stcg(reinterpret_cast<long long*>(gbase + x * gstride + W4e), (long long)lds_i32(boff + x * SB + W4));
+        __stcg(reinterpret_cast<long long*>(elem_ptr(A, out_buf(locm, x), lf.base + (u64)x * lf.stride) + W4e),
+               (long long)lds_i32(boff + x * SB + W4));
       if (A.T) {  // element format out: the lanes carry no tops
         if ((CL & 7) == 0) {
           const u32 per = CL / 8;  // 16-byte groups of int16 tops per element
           for (u32 x = tid; x < cl.nstore * per; x += nthr) {
             const u32 k = x / per, q = x - k * per;
-            __stcg(reinterpret_cast<uint4*>(A.T + (lf.base + (u64)k * lf.stride) * CL) + q, make_uint4(0, 0, 0, 0));
+            __stcg(reinterpret_cast<uint4*>(tops_row(A, out_buf(locm, k), lf.base + (u64)k * lf.stride)) + q,
+                   make_uint4(0, 0, 0, 0));
           }
         } else {
           for (u32 x = tid; x < cl.nstore * CL; x += nthr) {
             const u32 k = x / CL, q = x - k * CL;
-            A.T[(lf.base + (u64)k * lf.stride) * CL + q] = 0;
+            tops_row(A, out_buf(locm, k), lf.base + (u64)k * lf.stride)[q] = 0;
           }
         }
       }
@@ -1041,7 +1057,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         s_boff[nxt] = 0;
       }
       __syncthreads();
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt]);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt], s_loc[nxt]);
     }
     pc.mark(PH_WAIT);
     cur = nxt;
@@ -1105,6 +1121,18 @@ __global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 coun
   u64 e = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= count) return;
   canon_element(data + e * elem_bytes, D);
+}
+
+// Outputs the schedule left in the shadow buffer: element (lanes, top word)
+// and its tops row back to the caller's view.
+__global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2, u64 eb, short* T, u64 tloc, u32 CL,
+                                   const u64* idx, u32 D) {
+  const u64 e = idx[blockIdx.x];
+  const uint4* src = reinterpret_cast<const uint4*>(data2 + e * eb);
+  uint4* dst = reinterpret_cast<uint4*>(data + e * eb);
+  const u32 pieces = (4 * D + 8 + 15) / 16;
+  for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) dst[x] = __ldcg(src + x);
+  for (u32 x = threadIdx.x; x < CL; x += blockDim.x) T[e * CL + x] = T[tloc + e * CL + x];
 }
 
 // Carry-save lanes -> canonical element format, one CTA per element: lane p

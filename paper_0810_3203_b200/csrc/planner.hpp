@@ -125,10 +125,12 @@ struct DevLeaf {
   // (tpost); 0 elsewhere
   u64 tpre, tpost;
   u32 c0;          // coset leaves: first coset of this ticket
-  // coset leaves of several tickets, in place: counter of tickets whose
-  // inputs are in shared memory; no ticket stores before all have loaded
-  // (their lane sets differ between load and store)
-  u32 lbar;
+  // Buffer of each slot (plans with coset leaves): the tickets of one coset
+  // leaf read and write different lanes of the same coefficients, so a coset
+  // leaf reads each slot from one of two buffers (the caller's view, a shadow
+  // copy) and writes it to the other.  locbits[locoff + 2w] / [+ 2w + 1]: bit
+  // k%64 of word w = slot k's input / output buffer.  kNoDep: all in the view.
+  u32 locoff;
 };
 static_assert(sizeof(DevLeaf) == 64, "DevLeaf layout");
 
@@ -168,6 +170,8 @@ struct Plan {
   u64 max_slot_area = 0;  // shared-memory bytes of the largest leaf
   bool coset = false;     // some leaves write carry-save lanes (tops array in use)
   u64 extent = 0;         // view indices [0, extent) touched (tops array rows)
+  std::vector<u64> locbits;        // per-slot buffer bits (see DevLeaf::locoff)
+  std::vector<u64> shadow_finals;  // outputs the schedule leaves in the shadow buffer
 };
 
 // Ring-dependent planning parameters.
@@ -176,7 +180,9 @@ struct RingShape {
   u64 M = 0;           // root order
   unsigned max_leaf_ell = 3;
   u64 elem_bytes = 0;          // bytes per coefficient (for L2 batching)
-  u64 l2_budget = 48ull << 20;  // bytes of L2 a batch may occupy
+  // bytes of top-level sub-transforms per ticket-order batch: the engine is
+  // issue bound, so batches favour parallelism over L2 residency
+  u64 l2_budget = 512ull << 20;
   // whole-leaf geometry (Fermat): chunks per element and slot bytes
   u32 C = 0;
   u32 slot_bytes = 0;
@@ -184,6 +190,7 @@ struct RingShape {
   u64 lane_bits = 0;
   unsigned coset_max_ell = 0;
   u64 slot_budget = 0;  // shared-memory bytes available for a leaf's slots
+  u32 wave_overlap = 0;  // waves by which consecutive L2 batches overlap in the ticket order
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -230,7 +237,10 @@ class Planner {
       c.top_child = k;
       node(inverse, it.L, it.s, it.z, it.n, it.f, it.base, it.stride, policy, /*depth=*/1, c, 0, Bnd{});
     }
-    finish(p);
+    std::vector<u64> finals;
+    for (const Item& it : items)
+      for (u64 k = 0; k < it.n + (u64)(inverse ? it.f : 0); ++k) finals.push_back(it.base + k * it.stride);
+    finish(p, finals);
     p.final_count = 0;  // caller canonicalises
     return p;
   }
@@ -250,8 +260,10 @@ class Planner {
     root.dep_target = 0;
     root.report = kNoDep;
     node(inverse, L, s, z, n, f, 0, 1, policy, /*depth=*/0, root, /*wave0=*/0, Bnd{});
-    finish(p);
     p.final_count = inverse ? n + (u64)f : n;
+    std::vector<u64> finals(p.final_count);
+    for (u64 k = 0; k < p.final_count; ++k) finals[k] = k;
+    finish(p, finals);
     return p;
   }
 
@@ -271,11 +283,92 @@ class Planner {
     extent_ = 0;
   }
 
-  // ticket order: (top phase, batch, wave, top child, emission order)
-  void finish(Plan& p) {
+  // Buffers of every slot (plans with coset leaves).  A coset leaf reads each
+  // slot from one buffer and writes it to the other; a whole leaf (one
+  // ticket) may read and write either.  Backward over the leaves (emission
+  // order is topological), whole leaves pick the output buffer that brings
+  // the element back to the caller's view after the coset leaves that
+  // follow; forward, the actual buffers are assigned.  Outputs that still end
+  // in the shadow buffer (an odd run of coset leaves from the inputs) are
+  // listed for the final fold to copy back.
+  void assign_buffers(Plan& p, const std::vector<u64>& finals) {
+    const size_t nt = leaves_.size();
+    std::vector<size_t> gs;
+    for (size_t t = 0; t < nt; ++t) {
+      if (t > 0) {
+        const DevLeaf &a = leaves_[t - 1], &b = leaves_[t];
+        if (classes_[b.cls].kind == 1 && a.cls == b.cls && a.base == b.base && a.stride == b.stride && b.c0 != 0)
+          continue;
+      }
+      gs.push_back(t);
+    }
+    constexpr std::uint8_t ANY = 2;
+    std::vector<std::uint8_t> req(extent_, ANY);
+    for (u64 e : finals) req[e] = 0;
+    std::vector<std::vector<u64>> pref(gs.size());
+    for (size_t gi = gs.size(); gi-- > 0;) {
+      const DevLeaf& lf = leaves_[gs[gi]];
+      const LeafProgram& c = classes_[lf.cls];
+      const u32 nl = c.nload, ns = c.nstore, span = std::max(nl, ns);
+      pref[gi].assign((span + 63) / 64, 0);
+      for (u32 k = 0; k < span; ++k) {
+        const u64 e = lf.base + (u64)k * lf.stride;
+        if (k < ns) {
+          const std::uint8_t want = req[e] == ANY ? 0 : req[e];
+          if (c.kind == 0) {
+            if (want) pref[gi][k / 64] |= u64{1} << (k % 64);
+            req[e] = ANY;
+          } else {
+            req[e] = k < nl ? (std::uint8_t)(1 - want) : ANY;
+          }
+        } else {
+          req[e] = ANY;
+        }
+      }
+    }
+    std::vector<std::uint8_t> loc(extent_, 0);
+    p.locbits.clear();
+    for (size_t gi = 0; gi < gs.size(); ++gi) {
+      const size_t t0 = gs[gi], t1 = gi + 1 < gs.size() ? gs[gi + 1] : nt;
+      const DevLeaf& lf = leaves_[t0];
+      const LeafProgram& c = classes_[lf.cls];
+      const u32 nl = c.nload, ns = c.nstore, span = std::max(nl, ns), nw = (span + 63) / 64;
+      const u32 off = (u32)p.locbits.size();
+      p.locbits.resize(off + 2 * (size_t)nw, 0);
+      for (u32 k = 0; k < nl; ++k)
+        if (loc[lf.base + (u64)k * lf.stride]) p.locbits[off + 2 * (k / 64)] |= u64{1} << (k % 64);
+      for (u32 k = 0; k < ns; ++k) {
+        const u64 e = lf.base + (u64)k * lf.stride;
+        const std::uint8_t o = c.kind == 1 ? (std::uint8_t)(1 - loc[e]) : (std::uint8_t)((pref[gi][k / 64] >> (k % 64)) & 1);
+        if (o) p.locbits[off + 2 * (k / 64) + 1] |= u64{1} << (k % 64);
+        loc[e] = o;
+      }
+      for (size_t t = t0; t < t1; ++t) leaves_[t].locoff = off;
+    }
+    p.shadow_finals.clear();
+    for (u64 e : finals)
+      if (loc[e]) p.shadow_finals.push_back(e);
+  }
+
+  // ticket order: (top phase, batch, wave, top child, emission order), with
+  // the waves of consecutive L2 batches overlapped by `overlap` waves: batch
+  // b's wave w is ranked at w + (W - overlap) b (W = waves per batch), so the
+  // next batch's first waves fill the CTAs that the tail of a batch (its few
+  // late tickets) leaves idle.  Any such order is topological: batches are
+  // independent, and each keeps its own wave order.
+  void finish(Plan& p, const std::vector<u64>& finals) {
+    if (coset_used_) assign_buffers(p, finals);
     std::vector<u32> idx(leaves_.size());
     for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return keys_[x] < keys_[y]; });
+    u32 W = 1;
+    for (const auto& k : keys_) W = std::max(W, std::get<2>(k) + 1);
+    const u32 ov = std::min(W - 1, rs_.wave_overlap);
+    auto rank = [&](u32 x) {
+      const auto& k = keys_[x];
+      return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k) + (u64)(W - ov) * std::get<1>(k), std::get<1>(k),
+                             std::get<3>(k), std::get<4>(k));
+    };
+    std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return rank(x) < rank(y); });
     p.leaves.reserve(idx.size());
     p.leaf_wave.reserve(idx.size());
     for (u32 i : idx) {
@@ -568,7 +661,7 @@ class Planner {
   void emit_whole(bool inv, unsigned ell, u64 z, u64 n, int f, u64 base, u64 stride, int policy, const Ctx& cx,
                   u32 wave0, DevLeaf lf) {
     lf.cls = class_of(ClassKey{inv ? 1 : 0, ell, z, n, f, 0}, policy);
-    lf.lbar = kNoDep;
+    lf.locoff = kNoDep;
     lf.dep = cx.dep;
     lf.dep_target = cx.dep_target;
     lf.comp = cx.report;
@@ -588,11 +681,7 @@ class Planner {
     lf.base = base;
     lf.stride = stride;
     const u64 groups = c.step / c.m;
-    lf.lbar = kNoDep;
-    if (groups > 1) {
-      lf.lbar = (u32)counters_.size();
-      counters_.push_back(DevCounter{(u32)groups, kNoDep});
-    }
+    lf.locoff = kNoDep;
     for (u64 g = 0; g < groups; ++g) {
       lf.c0 = (u32)(g * c.m);
       push_leaf(lf, cx, wave0);

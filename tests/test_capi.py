@@ -117,10 +117,17 @@ def run_plan_fermat(plan, N, vals):
     every rotation they perform must be a whole number of lanes."""
     P, M = (1 << N) + 1, 2 * N
     lane = plan.get("lane_bits", 0)
-    x = dict(vals)
+    bits = plan.get("locbits", [])
+    x = {(0, e): v for e, v in vals.items()}  # (buffer, element) -> value
+
+    def buf(locoff, k, out):
+        if locoff < 0:
+            return 0
+        return (bits[locoff + 2 * (k // 64) + (1 if out else 0)] >> (k % 64)) & 1
+
     meta = plan["counters"]
     counters = [0] * len(meta)
-    for (cls, base, stride, s, dep, target, comp, wave, tpre, tpost, c0) in plan["leaves"]:
+    for (cls, base, stride, s, dep, target, comp, wave, tpre, tpost, c0, locoff) in plan["leaves"]:
         if dep >= 0:
             assert counters[dep] >= target, "ticket order is not topological"
         c = plan["classes"][cls]
@@ -132,7 +139,7 @@ def run_plan_fermat(plan, N, vals):
             a, b = c["pre"][i]
             e = (a * s + b + (tpre if inv and i < cn else 0)) % M
             assert not coset or e % lane == 0
-            slot[i] = (x[base + i * stride] * pow(2, e, P)) % P
+            slot[i] = (x[(buf(locoff, i, False), base + i * stride)] * pow(2, e, P)) % P
         for (t, a, b, r) in (c["ops"] if run else []):
             assert not coset or t == 4 or r % (M >> c["ell"]) == 0
             if t == 4:
@@ -154,7 +161,10 @@ def run_plan_fermat(plan, N, vals):
             tp = (tpost if cf_ and i == cn else 0) if inv else tpost
             e = (ea * s + eb + tp) % M
             assert not coset or e % lane == 0
-            x[base + i * stride] = (slot[i] * pow(2, e, P)) % P
+            ob = buf(locoff, i, True)
+            if coset and i < c["nload"]:
+                assert ob != buf(locoff, i, False), "a coset leaf must not write the buffer it reads"
+            x[(ob, base + i * stride)] = (slot[i] * pow(2, e, P)) % P
         k = comp
         while k >= 0:  # leaf -> phase counter -> (node finished) -> parent phase ...
             counters[k] += 1
@@ -162,7 +172,8 @@ def run_plan_fermat(plan, N, vals):
             if counters[k] != tgt:
                 break
             k = nxt
-    return x
+    shadow = set(plan.get("shadow_finals", []))
+    return {e: x[(1 if e in shadow else 0, e)] for (b, e) in x if b == 0 or e in shadow}
 
 
 def check_plan(ctx, N, rnd, trials):
@@ -227,6 +238,7 @@ def test_schedule_shape_config5():
     assert all(lf[7] == 0 and lf[2] == 512 * 64 for lf in first)
     # within the first batch, level-1 leaves precede level-2 leaves
     per_col = 64 + 6 * 16 + 9
-    waves = [lf[7] for lf in leaves[: 5 * per_col]]  # first L2 batch: 5 columns (48 MiB budget)
+    batch = (512 << 20) // (512 * ctx.element_bytes)  # columns per ticket-order batch (512 MiB budget)
+    waves = [lf[7] for lf in leaves[: batch * per_col]]
     assert waves == sorted(waves) and waves[0] == 0 and waves[-1] == 2
-    assert leaves[5 * per_col][7] == 0  # the next batch restarts at level 1
+    assert leaves[batch * per_col][7] == 0  # the next batch restarts at level 1
