@@ -203,6 +203,7 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         cw = (u32)std::min<u64>(8, std::max<u64>(4, lane / 32));
       }
       if (cw > R->D) cw = R->D;
+      while (R->D / cw > 512 && cw < 16) cw *= 2;  // a CTA covers one chunk per thread of a coefficient
       C = R->D / cw;
       sb = fermat_slot_bytes(C, 4 * cw);
       const size_t budget = kSmemBudget - scratch_bytes(1024);
@@ -386,6 +387,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.data2 = shadow;
       A.tloc = (u64)dp.host.extent * dp.C;
       A.locbits = dp.locbits;
+      A.nclasses = (u32)dp.host.classes.size();
       A.half = (u32)half;
       unsigned long long* prof = nullptr;
       static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
@@ -430,9 +432,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaFreeAsync(prof, st));
         unsigned long long tot = 0;
         for (auto v : h) tot += v;
-        fprintf(stderr, "[cftft] leaves=%llu grid=%u phase cycles (%% of CTA time): wait %.1f load %.1f pre %.1f levels %.1f post %.1f store %.1f (total %.3g cyc/CTA)\n",
-                (unsigned long long)dp.nleaves, grid, 100.0 * h[0] / tot, 100.0 * h[1] / tot, 100.0 * h[2] / tot,
-                100.0 * h[3] / tot, 100.0 * h[4] / tot, 100.0 * h[5] / tot, (double)tot / grid);
+        fprintf(stderr, "[cftft] leaves=%llu grid=%u phase cycles (%% of CTA time): wait %.1f issue %.1f cache %.1f load %.1f pre %.1f levels %.1f post %.1f store %.1f (total %.3g cyc/CTA)\n",
+                (unsigned long long)dp.nleaves, grid, 100.0 * h[0] / tot, 100.0 * h[6] / tot, 100.0 * h[7] / tot,
+                100.0 * h[1] / tot, 100.0 * h[2] / tot, 100.0 * h[3] / tot, 100.0 * h[4] / tot, 100.0 * h[5] / tot,
+                (double)tot / grid);
       }
     } else {
       if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;

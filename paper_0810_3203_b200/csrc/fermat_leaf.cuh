@@ -55,6 +55,7 @@ struct Args {
   std::uint8_t* data2;     // shadow buffer (same element stride), coset plans
   u64 tloc;                // tops entries per buffer
   const u64* locbits;      // per-slot buffer bits (DevLeaf::locoff)
+  u32 nclasses;
   u32 half;                // bytes of one of the two ticket buffers (double buffering)
   u32 lanes, logLanes;     // lanes (chunks) per element
   u32 logS;                // tops-array lane interleave
@@ -63,7 +64,7 @@ struct Args {
 };
 
 // Phase timing (debug): thread 0 of each CTA accumulates clock64 deltas.
-enum { PH_WAIT = 0, PH_LOAD, PH_PRE, PH_LEVELS, PH_POST, PH_STORE, PH_N };
+enum { PH_WAIT = 0, PH_LOAD, PH_PRE, PH_LEVELS, PH_POST, PH_STORE, PH_ISSUE, PH_CACHE, PH_N };
 struct PhaseClock {
   unsigned long long acc[PH_N];
   unsigned long long t;
@@ -590,6 +591,7 @@ __device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const De
 // Slot layout (both leaf kinds): C chunks (piece-major, swizzled), then one
 // int32 top per chunk at W4, then the element's 64-bit top word at W4 + 4C.
 constexpr u32 kMaxSlots = 64;
+constexpr u32 kClassTab = 48;
 
 // Issues the loads of a ticket into the slot buffer at `boff`, all as
 // cp.async in one commit group: the data chunks (coset tickets gather their
@@ -598,11 +600,12 @@ constexpr u32 kMaxSlots = 64;
 // slot's element top word.  fixup() turns these into int32 tops once landed.
 template <int CW, int NT>
 __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 boff, u32 tid, u32* rho, u64* locm) {
+                                           u32 boff, u32 tid, u32* rho, u64* locm, std::uint8_t** sp) {
   const Geo G = geo_of(cl, lf, CW);
   const u32 nl = cl.nload;
   constexpr u32 CB = 32 * CW;
-  // stage the ticket's per-slot buffer bits and (coset) lane pre-rotations
+  // stage the ticket's per-slot buffer bits, (coset) lane pre-rotations and
+  // input element pointers
   const u32 span = max(cl.nload, cl.nstore), nw = (span + 63) >> 6;
   for (u32 x = tid; x < 2 * kMaskWords; x += NT)
     locm[x] = (lf.locoff != kNoDep && x < 2 * nw) ? A.locbits[lf.locoff + x] : 0ull;
@@ -610,6 +613,8 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
     for (u32 k = tid; k < nl; k += NT) {
       const SymExp P = A.rots[cl.pre_begin + k];
       rho[k] = (u32)(pre_exp(A, cl, lf, P, k) / CB);
+      const u32 b = (lf.locoff != kNoDep) ? (u32)(A.locbits[lf.locoff + 2 * (k >> 6)] >> (k & 63)) & 1u : 0u;
+      sp[k] = elem_ptr(A, b, lf.base + (u64)k * lf.stride);
     }
   }
   __syncthreads();
@@ -618,29 +623,45 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
     const u32 CL = A.lanes;
     const u32 sb = smem_base + boff;
     if (G.coset) {
-      const u32 lq = G.logC + lpc;
-      const u32 tot = nl << lq;
-      for (u32 idx = tid; idx < tot; idx += NT) {
-        const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
-        const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
-        const u32 ln = (lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1);
-        std::uint8_t* g = elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
-        cp_async16(sb + piece_off(k * G.SB, j, q, G.C), g + (u64)ln * (CB / 8) + 16u * q);
+      // thread -> fixed piece position (chunk j, piece q); slots strided
+      const u32 lq = G.logC + lpc, P = 1u << lq;
+      for (u32 pp = tid & (P - 1); pp < ((A.debug_skip & 16) ? 0u : P); pp += NT) {
+        const u32 j = pp >> lpc, q = pp & ((1u << lpc) - 1);
+        const u32 lj = lane_of(G, j) + 2 * CL;
+        const u32 so0 = piece_off(0, j, q, G.C);
+        const u32 kstep = NT > P ? NT / P : 1u;
+        for (u32 k = NT > P ? tid / P : 0u; k < nl; k += kstep) {
+          const u32 ln = (lj - rho[k]) & (CL - 1);
+          cp_async16(sb + k * G.SB + so0, sp[k] + (u64)ln * (CB / 8) + 16u * q);
+        }
       }
+      if (A.T && !(A.debug_skip & 8)) {
+        const u32 Pc = G.C;
+        for (u32 j = tid & (Pc - 1); j < Pc; j += NT) {
+          const u32 lj = lane_of(G, j) + 2 * CL;
+          const u32 kstep = NT > Pc ? NT / Pc : 1u;
+          for (u32 k = NT > Pc ? tid / Pc : 0u; k < nl; k += kstep) {
+            const u32 ln = (lj - rho[k]) & (CL - 1);
+            const u32 b = in_buf(locm, k);
+            const short* tr = A.T + (b ? A.tloc : 0) + (lf.base + (u64)k * lf.stride) * CL;
+            cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, ln) & ~1u));
+          }
+        }
+      }
+      for (u32 k = tid; k < nl; k += NT) cp_async8(sb + k * G.SB + G.HO, sp[k] + 4ull * A.D);
     } else {
       copy_slots<CW, true, NT>(A, G, lf, locm, nl, smem_base, boff, tid);
-    }
-    if (A.T) {
-      const u32 tt = nl << G.logC;
-      for (u32 idx = tid; idx < tt; idx += NT) {
-        const u32 k = idx >> G.logC, j = idx & G.Cm;
-        const u32 ln = G.coset ? ((lane_of(G, j) + 2 * CL - rho[k]) & (CL - 1)) : j;
-        const short* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
-        cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, ln) & ~1u));
+      if (A.T) {
+        const u32 tt = nl << G.logC;
+        for (u32 idx = tid; idx < tt; idx += NT) {
+          const u32 k = idx >> G.logC, j = idx & G.Cm;
+          const short* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
+          cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, j) & ~1u));
+        }
       }
+      for (u32 k = tid; k < nl; k += NT)
+        cp_async8(sb + k * G.SB + G.HO, elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride) + 4ull * A.D);
     }
-    for (u32 k = tid; k < nl; k += NT)
-      cp_async8(sb + k * G.SB + G.HO, elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride) + 4ull * A.D);
   }
   cp_async_commit();
 }
@@ -653,25 +674,28 @@ __device__ __forceinline__ void fixup(const Args& A, const DevLeaf& lf, const De
                                       const u32* rho) {
   const Geo G = geo_of(cl, lf, CW);
   const u32 CL = A.lanes;
-  const u32 tt = cl.nload << G.logC;
-  for (u32 idx = tid; idx < tt; idx += NT) {
-    const u32 k = idx >> G.logC, j = idx & G.Cm;
-    const u32 src = G.coset ? ((lane_of(G, j) + 2 * CL - rho[k]) & (2 * CL - 1)) : j;
-    const u32 ln = src & (CL - 1);
-    const u32 so = boff + k * G.SB;
-    int top = 0;
-    if (A.T) {
-      const u32 raw = *reinterpret_cast<const u32*>(g_sm + so + G.W4 + 4 * j);
-      top = (tops_ix(A, ln) & 1u) ? (int)(short)(raw >> 16) : (int)(short)(raw & 0xFFFFu);
+  const u32 Pc = G.C, nl = cl.nload;
+  const u32 kstep = NT > Pc ? NT / Pc : 1u;
+  for (u32 j = tid & (Pc - 1); j < Pc; j += NT) {
+    const u32 lj = G.coset ? lane_of(G, j) + 2 * CL : j;
+    for (u32 k = NT > Pc ? tid / Pc : 0u; k < nl; k += kstep) {
+      const u32 src = G.coset ? ((lj - rho[k]) & (2 * CL - 1)) : j;
+      const u32 ln = src & (CL - 1);
+      const u32 so = boff + k * G.SB;
+      int top = 0;
+      if (A.T) {
+        const u32 raw = *reinterpret_cast<const u32*>(g_sm + so + G.W4 + 4 * j);
+        top = (tops_ix(A, ln) & 1u) ? (int)(short)(raw >> 16) : (int)(short)(raw & 0xFFFFu);
+      }
+      if (ln == CL - 1) top += (int)*reinterpret_cast<const long long*>(g_sm + so + G.HO);
+      if (src >= CL) {
+        Ch<CW> w;
+        lds_ch(w, so, j, G.C);
+        top = exact_from<CW>(w, top, true);
+        sts_ch(so, j, G.C, w);
+      }
+      sts_i32(so + G.W4 + 4 * j, top);
     }
-    if (ln == CL - 1) top += (int)*reinterpret_cast<const long long*>(g_sm + so + G.HO);
-    if (src >= CL) {
-      Ch<CW> w;
-      lds_ch(w, so, j, G.C);
-      top = exact_from<CW>(w, top, true);
-      sts_ch(so, j, G.C, w);
-    }
-    sts_i32(so + G.W4 + 4 * j, top);
   }
 }
 
@@ -683,18 +707,24 @@ template <int CW, int NT>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args A) {
   constexpr int TPT = 2;  // ops per thread per round (each a CW-word chunk)
   constexpr u32 CB = 32 * CW;
-  __shared__ u32 s_tk[2];
-  __shared__ DevLeaf s_lf[2];
-  __shared__ DevClass s_cl[2];
-  __shared__ u32 s_boff[2];
-  __shared__ int s_ready;  // next leaf's dependency already satisfied
+  // ticket descriptors, a ring of three: the current ticket, the next one
+  // (prefetched into the other buffer when its inputs are ready), and the one
+  // after it, whose descriptor tid 0 fetches while the current one computes
+  __shared__ u32 s_tk[3];
+  __shared__ DevLeaf s_lf[3];
+  __shared__ DevClass s_cl[3];
+  __shared__ u32 s_boff[3];
+  __shared__ int s_ready[3];  // dependency already satisfied (as last checked)
   __shared__ u32 s_cached;
   __shared__ OpT s_ops[kCacheOps];
   __shared__ u32 s_lev[kCacheLev + 1];
   __shared__ SymExp s_crot[kCacheRot];
-  __shared__ u32 s_rho[2][kMaxSlots];  // coset: lane pre-rotation per loaded slot
-  __shared__ u64 s_loc[2][2 * kMaskWords];  // per-slot buffer bits
+  __shared__ u32 s_rho[3][kMaxSlots];  // coset: lane pre-rotation per loaded slot
+  __shared__ u64 s_loc[3][2 * kMaskWords];  // per-slot buffer bits
+  __shared__ std::uint8_t* s_sp[3][kMaxSlots];  // coset: input element pointer per slot
+  __shared__ std::uint8_t* s_op[kMaxSlots];     // coset: output element pointer per slot
   __shared__ u32 s_rhp[kMaxSlots];     // coset: lane post-rotation per stored slot
+  __shared__ DevClass s_ctab[kClassTab];  // the plan's first kClassTab classes
   const u32 tid = threadIdx.x;
   constexpr u32 nthr = NT;
   const u32 CL = A.lanes, CLm = CL - 1;
@@ -704,21 +734,32 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   PhaseClock pc;
   pc.start(tid == 0 && A.prof != nullptr);
 
-  // ---- prologue: first ticket, its descriptor, its loads ----------------------
-  if (tid == 0) {
+  auto dep_met = [&](const DevLeaf& l) {
+    return (l.dep == kNoDep) || (ld_acquire(&A.counters[1 + l.dep]) >= l.dep_target);
+  };
+  auto fetch = [&](u32 r) {  // tid 0 only
     const u32 t = atomicAdd(&A.counters[0], 1u);
-    s_tk[0] = t;
-    s_boff[0] = 0;
+    s_tk[r] = t;
+    s_ready[r] = 0;
     if (t < A.nleaves) {
-      s_lf[0] = A.leaves[t];
-      s_cl[0] = A.classes[s_lf[0].cls];
-      if (s_lf[0].dep != kNoDep)
-        while (ld_acquire(&A.counters[1 + s_lf[0].dep]) < s_lf[0].dep_target) __nanosleep(64);
+      s_lf[r] = A.leaves[t];
+      s_cl[r] = A.classes[s_lf[r].cls];
+      s_ready[r] = dep_met(s_lf[r]);
     }
+  };
+
+  for (u32 x = tid; x < min(A.nclasses, kClassTab); x += NT) s_ctab[x] = A.classes[x];
+  // ---- prologue: first two tickets, the first one's loads -------------------
+  if (tid == 0) {
+    fetch(0);
+    s_boff[0] = 0;
+    if (s_tk[0] < A.nleaves)
+      while (!dep_met(s_lf[0])) __nanosleep(64);
+    fetch(1);
     s_cached = 0xFFFFFFFFu;
   }
   __syncthreads();
-  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, 0, tid, s_rho[0], s_loc[0]);
+  if (s_tk[0] < A.nleaves) issue_load<CW, NT>(A, s_lf[0], s_cl[0], smem_base, 0, tid, s_rho[0], s_loc[0], s_sp[0]);
   u32 cur = 0;
 
   for (;;) {
@@ -734,27 +775,28 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     Offs<CW> fi;
     fi.init(i, C);
     const u32 ti = W4 + 4 * i;  // offset of chunk i's top within a slot
-    const u32 nxt = cur ^ 1;
-    // fetch the next ticket now; when small and ready, prefetch it into the
-    // other buffer so its loads overlap this ticket's work
-    bool prefetched = false;
-    if (tid == 0) {
-      const u32 t = atomicAdd(&A.counters[0], 1u);
-      s_tk[nxt] = t;
-      s_ready = 0;
-      if (t < A.nleaves) {
-        s_lf[nxt] = A.leaves[t];
-        s_cl[nxt] = A.classes[s_lf[nxt].cls];
-        const DevLeaf& nl = s_lf[nxt];
-        s_ready = (nl.dep == kNoDep) || (ld_acquire(&A.counters[1 + nl.dep]) >= nl.dep_target);
-      }
-    }
-    __syncthreads();
+    const u32 nxt = cur == 2 ? 0 : cur + 1, nn = nxt == 2 ? 0 : nxt + 1;
     const bool have_next = s_tk[nxt] < A.nleaves;
-    if (have_next && s_ready && small_ticket(A, cl) && small_ticket(A, s_cl[nxt])) {
+    // the descriptor after next: its ticket number is claimed now, its leaf is
+    // read once the prefetch is issued; everyone reads it next iteration
+    u32 tnn = 0xFFFFFFFFu;
+    if (tid == 0 && have_next) tnn = atomicAdd(&A.counters[0], 1u);
+    // the next ticket streams into the other buffer while this one computes
+    bool prefetched = false;
+    if (have_next && s_ready[nxt] && small_ticket(A, cl) && small_ticket(A, s_cl[nxt])) {
       if (tid == 0) s_boff[nxt] = boff ^ A.half;
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt], s_loc[nxt]);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt], s_loc[nxt], s_sp[nxt]);
       prefetched = true;
+    }
+    pc.mark(PH_ISSUE);
+    if (tid == 0 && have_next) {
+      s_tk[nn] = tnn;
+      s_ready[nn] = 0;  // checked at the end of this iteration
+      if (tnn < A.nleaves) {
+        s_lf[nn] = A.leaves[tnn];
+        const u32 c = s_lf[nn].cls;
+        s_cl[nn] = c < kClassTab ? s_ctab[c] : A.classes[c];
+      }
     }
     // leaf-program cache
     const bool cached = cl.nops <= kCacheOps && cl.nlevels <= kCacheLev && cl.nload + cl.nstore <= kCacheRot;
@@ -773,8 +815,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       for (u32 k = tid; k < cl.nstore; k += nthr) {
         const SymExp P = A.rots[cl.post_begin + k];
         s_rhp[k] = (u32)(post_exp(A, cl, lf, P, k) / CB);
+        const u32 b = (lf.locoff != kNoDep) ? (u32)(A.locbits[lf.locoff + 2 * (k >> 6) + 1] >> (k & 63)) & 1u : 0u;
+        s_op[k] = elem_ptr(A, b, lf.base + (u64)k * lf.stride);
       }
     }
+    pc.mark(PH_CACHE);
     if (prefetched)
       cp_async_wait<1>();
     else
@@ -931,15 +976,17 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
       // (2) coalesced copy of the lanes to their rotated positions
       {
         constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
-        const u32 lq = logC + lpc;
-        const u32 tot = cl.nstore << lq;
-        for (u32 idx = tid; idx < tot; idx += nthr) {
-          const u32 k = idx >> lq, rem = idx & ((1u << lq) - 1);
-          const u32 j = rem >> lpc, q = rem & ((1u << lpc) - 1);
-          const u32 d = (lane_of(G, j) + s_rhp[k]) & CLm;
-          std::uint8_t* g = elem_ptr(A, out_buf(locm, k), lf.base + (u64)k * lf.stride);
-          __stcg(reinterpret_cast<uint4*>(g + (u64)d * (CB / 8) + 16u * q),
-                 *reinterpret_cast<const uint4*>(g_sm + piece_off(boff + k * SB, j, q, C)));
+        const u32 lq = logC + lpc, P = 1u << lq;
+        const u32 kstep = nthr > P ? nthr / P : 1u;
+        for (u32 pp = tid & (P - 1); pp < P; pp += nthr) {
+          const u32 j = pp >> lpc, q = pp & ((1u << lpc) - 1);
+          const u32 lj = lane_of(G, j);
+          const u32 so0 = piece_off(0, j, q, C);
+          for (u32 k = nthr > P ? tid / P : 0u; k < cl.nstore; k += kstep) {
+            const u32 d = (lj + s_rhp[k]) & CLm;
+            __stcg(reinterpret_cast<uint4*>(s_op[k] + (u64)d * (CB / 8) + 16u * q),
+                   *reinterpret_cast<const uint4*>(g_sm + boff + k * SB + so0));
+          }
         }
       }
       __syncthreads();  // slot reuse
@@ -1051,14 +1098,15 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     }
     if (have_next && !prefetched) {
       if (tid == 0) {
-        const DevLeaf& nl = s_lf[nxt];
-        if (nl.dep != kNoDep)
-          while (ld_acquire(&A.counters[1 + nl.dep]) < nl.dep_target) __nanosleep(64);
+        while (!dep_met(s_lf[nxt])) __nanosleep(64);
         s_boff[nxt] = 0;
       }
       __syncthreads();
-      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt], s_loc[nxt]);
+      issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt], s_loc[nxt], s_sp[nxt]);
     }
+    // refresh the readiness of the ticket after next (prefetch decision)
+    if (tid == 0 && have_next && s_tk[nn] < A.nleaves && !s_ready[nn]) s_ready[nn] = dep_met(s_lf[nn]);
+    __syncthreads();
     pc.mark(PH_WAIT);
     cur = nxt;
   }
