@@ -353,7 +353,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
                                    : (size_t)R->slot_bytes << dp.max_ell;
     const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(1024) : 0);
     unsigned grid = 1;
-    short* tops = nullptr;
+    int* tops = nullptr;
     if (R->kind == CFTFT_RING_FERMAT) {
       fermat::Args A{};
       A.data = base;
@@ -378,7 +378,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.logS = dp.logS;
       std::uint8_t* shadow = nullptr;
       if (dp.host.coset) {
-        const size_t tb = 2 * (size_t)dp.host.extent * dp.C * sizeof(short);
+        const size_t tb = 2 * (size_t)dp.host.extent * dp.C * sizeof(int);
         CUDA_TRY(cudaMallocAsync((void**)&tops, tb, st));
         CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
         CUDA_TRY(cudaMallocAsync((void**)&shadow, (size_t)dp.host.extent * stride, st));

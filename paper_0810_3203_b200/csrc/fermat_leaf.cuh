@@ -51,7 +51,7 @@ struct Args {
   u32 logC;
   u32 slot_bytes;          // 4*D + 4*C (16B aligned)
   u32 scratch_off;         // byte offset of the carry scratch
-  short* T;                // carry-save tops, [buffer][view element][lane] (nullptr: not in use)
+  int* T;                  // carry-save tops, [buffer][view element][lane] (nullptr: not in use)
   std::uint8_t* data2;     // shadow buffer (same element stride), coset plans
   u64 tloc;                // tops entries per buffer
   const u64* locbits;      // per-slot buffer bits (DevLeaf::locoff)
@@ -546,7 +546,7 @@ __device__ __forceinline__ u32 out_buf(const u64* m, u32 k) { return (u32)(m[2 *
 __device__ __forceinline__ std::uint8_t* elem_ptr(const Args& A, u32 buf, u64 e) {
   return (buf ? A.data2 : A.data) + e * A.elem_bytes;
 }
-__device__ __forceinline__ short* tops_row(const Args& A, u32 buf, u64 e) {
+__device__ __forceinline__ int* tops_row(const Args& A, u32 buf, u64 e) {
   return A.T + (buf ? A.tloc : 0) + e * A.lanes;
 }
 
@@ -643,8 +643,8 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
           for (u32 k = NT > Pc ? tid / Pc : 0u; k < nl; k += kstep) {
             const u32 ln = (lj - rho[k]) & (CL - 1);
             const u32 b = in_buf(locm, k);
-            const short* tr = A.T + (b ? A.tloc : 0) + (lf.base + (u64)k * lf.stride) * CL;
-            cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, ln) & ~1u));
+            const int* tr = A.T + (b ? A.tloc : 0) + (lf.base + (u64)k * lf.stride) * CL;
+            cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, ln));
           }
         }
       }
@@ -655,8 +655,8 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
         const u32 tt = nl << G.logC;
         for (u32 idx = tid; idx < tt; idx += NT) {
           const u32 k = idx >> G.logC, j = idx & G.Cm;
-          const short* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
-          cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + (tops_ix(A, j) & ~1u));
+          const int* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
+          cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, j));
         }
       }
       for (u32 k = tid; k < nl; k += NT)
@@ -683,15 +683,15 @@ __device__ __forceinline__ void fixup(const Args& A, const DevLeaf& lf, const De
       const u32 ln = src & (CL - 1);
       const u32 so = boff + k * G.SB;
       int top = 0;
-      if (A.T) {
-        const u32 raw = *reinterpret_cast<const u32*>(g_sm + so + G.W4 + 4 * j);
-        top = (tops_ix(A, ln) & 1u) ? (int)(short)(raw >> 16) : (int)(short)(raw & 0xFFFFu);
-      }
-      if (ln == CL - 1) top += (int)*reinterpret_cast<const long long*>(g_sm + so + G.HO);
-      if (src >= CL) {
+      if (A.T) top = *reinterpret_cast<const int*>(g_sm + so + G.W4 + 4 * j);
+      // the element's top word hi sits at 2^N == -1: fold -hi into lane 0
+      // right here, so no lane top ever accumulates it
+      const int hi = ln == 0 ? (int)*reinterpret_cast<const long long*>(g_sm + so + G.HO) : 0;
+      if (hi != 0 || src >= CL) {
         Ch<CW> w;
         lds_ch(w, so, j, G.C);
-        top = exact_from<CW>(w, top, true);
+        if (hi) top += ch_add_small<CW>(w, -hi);
+        if (src >= CL) top = exact_from<CW>(w, top, true);
         sts_ch(so, j, G.C, w);
       }
       sts_i32(so + G.W4 + 4 * j, top);
@@ -962,12 +962,13 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         }
         const u64 e = lf.base + (u64)k * lf.stride;
         const u32 ob = out_buf(locm, k);
-        __stcg(tops_row(A, ob, e) + tops_ix(A, d), (short)tp);
+        __stcg(tops_row(A, ob, e) + tops_ix(A, d), tp);
         if (j == 0) {
-          // one ticket per slot (the one that read lane C-1, or for an output-
-          // only slot writes it) sets the output's element top word to zero:
-          // the value now lives in the lanes and their tops
-          const u32 pstar = k < cl.nload ? ((CLm + s_rho[cur][k]) & CLm) : ((CLm + 2 * CL - rho) & CLm);
+          // one ticket per slot (the one that read lane 0, which took the
+          // element top word, or for an output-only slot writes lane 0) sets
+          // the output's element top word to zero: the value now lives in the
+          // lanes and their tops
+          const u32 pstar = k < cl.nload ? (s_rho[cur][k] & CLm) : ((2 * CL - rho) & CLm);
           if (((pstar & (G.step - 1)) - G.c0) < G.m)
             __stcg(reinterpret_cast<long long*>(elem_ptr(A, ob, e) + W4e), 0ll);
         }
@@ -1066,8 +1067,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         __stcg(reinterpret_cast<long long*>(elem_ptr(A, out_buf(locm, x), lf.base + (u64)x * lf.stride) + W4e),
                (long long)lds_i32(boff + x * SB + W4));
       if (A.T) {  // element format out: the lanes carry no tops
-        if ((CL & 7) == 0) {
-          const u32 per = CL / 8;  // 16-byte groups of int16 tops per element
+        if ((CL & 3) == 0) {
+          const u32 per = CL / 4;  // 16-byte groups of int32 tops per element
           for (u32 x = tid; x < cl.nstore * per; x += nthr) {
             const u32 k = x / per, q = x - k * per;
             __stcg(reinterpret_cast<uint4*>(tops_row(A, out_buf(locm, k), lf.base + (u64)k * lf.stride)) + q,
@@ -1173,7 +1174,7 @@ __global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 coun
 
 // Outputs the schedule left in the shadow buffer: element (lanes, top word)
 // and its tops row back to the caller's view.
-__global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2, u64 eb, short* T, u64 tloc, u32 CL,
+__global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2, u64 eb, int* T, u64 tloc, u32 CL,
                                    const u64* idx, u32 D) {
   const u64 e = idx[blockIdx.x];
   const uint4* src = reinterpret_cast<const uint4*>(data2 + e * eb);
@@ -1187,12 +1188,12 @@ __global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2
 // takes the top of lane p-1 (lane 0 takes minus the top of lane C-1 and the
 // element top word: 2^N == -1).  Only word 0 of a lane is touched unless a
 // carry ripples; lanes whose carry-in is zero are not touched at all.
-__global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const short* T, u32 CL, u32 CW,
+__global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const int* T, u32 CL, u32 CW,
                                                       u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride) {
   __shared__ int s_pend[1024];
   const u64 e = idx0 + (u64)blockIdx.x * istride;
   std::uint8_t* el = data + e * eb;
-  const short* Te = T + e * CL;
+  const int* Te = T + e * CL;
   long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
   u32* w = reinterpret_cast<u32*>(el);
   auto tix = [&](u32 p) { return ((p & ((1u << logS) - 1)) << (logLanes - logS)) | (p >> logS); };
