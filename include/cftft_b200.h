@@ -76,6 +76,12 @@ uint64_t cftft_ring_element_bytes(const cftft_ring* ring); /* minimal stride */
  * Returns the cap in effect.  Must not race with transforms on the ring. */
 unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell);
 
+/* Validation only (transform.hpp:241-286: length, then counts), no work. */
+int cftft_validate(const cftft_ring* ring, int inverse, const cftft_params* params, int policy);
+
+/* cudaStreamSynchronize for callers that do not include the CUDA runtime. */
+int cftft_stream_synchronize(void* stream);
+
 /* Fermat rings: leaf layout.  lane_words = 0 runs every leaf on whole
  * coefficients; 4, 8 or 16 enables coset leaves over lanes of that many
  * 32-bit words (a leaf whose rotations are whole lanes works

@@ -61,3 +61,22 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build_library(force=True, verbose=True))
+
+
+API_TEST_SRC = os.path.join(os.path.dirname(PKG), "tests", "cpp", "api_test.cpp")
+API_TEST = os.path.join(LIBDIR, "api_test")
+
+
+def build_api_test(force: bool = False) -> str:
+    """The C++ host-API test program (tests/cpp/api_test.cpp), linked against
+    the in-tree library with an $ORIGIN rpath."""
+    if not force and os.path.exists(API_TEST) and os.path.getmtime(API_TEST) >= max(
+            os.path.getmtime(API_TEST_SRC), os.path.getmtime(LIB)):
+        return API_TEST
+    cmd = [_nvcc(), "-std=c++17", "-O2", "-o", API_TEST + ".tmp", API_TEST_SRC, "-L", LIBDIR, "-lcftft_b200",
+           "-Xlinker", "-rpath=$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("api_test build failed:\n" + r.stdout + r.stderr)
+    os.replace(API_TEST + ".tmp", API_TEST)
+    return API_TEST

@@ -637,6 +637,15 @@ unsigned cftft_ring_set_leaf_limit(cftft_ring* ring, unsigned max_ell) {
   return v;
 }
 
+int cftft_validate(const cftft_ring* ring, int inverse, const cftft_params* params, int policy) {
+  return validate(ring, inverse != 0, params, policy);
+}
+
+int cftft_stream_synchronize(void* stream) {
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return CFTFT_OK;
+}
+
 int cftft_ring_set_coset(cftft_ring* ring, int lane_words) {
   if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
   if (ring->kind != CFTFT_RING_FERMAT) return lane_words == 0 ? CFTFT_OK : fail(CFTFT_UNSUPPORTED, "coset leaves are for Fermat rings");
