@@ -213,6 +213,10 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       rs.max_leaf_ell = lam;
       rs.lane_bits = 32ull * cw;
       rs.slot_budget = budget;
+      // per-ticket fixed costs outweigh the overlap two half-size buffers buy:
+      // coset tickets fill the shared memory (CFTFT_HALFTICKETS=1: half, double buffered)
+      static const bool half = getenv("CFTFT_HALFTICKETS") != nullptr;
+      rs.ticket_budget = half ? budget / 2 : budget;
       unsigned cl = 0;
       for (unsigned e = 1; e <= 6; ++e) {
         const u64 cs = u64{1} << (e - 1);

@@ -191,6 +191,7 @@ struct RingShape {
   unsigned coset_max_ell = 0;
   u64 slot_budget = 0;  // shared-memory bytes available for a leaf's slots
   u32 wave_overlap = 0;  // waves by which consecutive L2 batches overlap in the ticket order
+  u64 ticket_budget = 0;  // shared-memory bytes a coset ticket may fill (default: one of two buffers)
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -709,7 +710,7 @@ class Planner {
       prog.step = (u32)(lanes2() >> k.ell);
       const u64 cl = u64{1} << (k.ell - 1);  // lanes per coset
       u64 m = 1;
-      while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.slot_budget / 2)
+      while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.ticket_budget)
         m *= 2;
       prog.m = (u32)m;
       prog.cs = (u32)(m * cl);
