@@ -110,6 +110,16 @@ class ClockSampler:
         self.idx = gpu_index
         self.rows = []
         self.proc = None
+        self.lo, self.hi = 0, None
+
+    # started before the warm-up (nvidia-smi's start-up perturbs the GPU);
+    # only the samples between begin() and end() are reported
+    def begin(self):
+        self.lo = len(self.rows)
+
+    def end(self):
+        time.sleep(0.12)
+        self.hi = len(self.rows)
 
     def start(self):
         try:
@@ -136,7 +146,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = self.rows[self.lo:self.hi] if self.hi is not None and self.hi > self.lo else self.rows[self.lo:]
+        for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = float(r[2])
@@ -308,19 +319,21 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
         rows = fwd.tft(col)
         inv.itft(rows, col)
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = eng.launches
     barrier()
+    sampler.begin()
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     barrier()
+    sampler.end()
     clocks = sampler.stop()
     t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -432,37 +445,50 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    host_ms = []
+
     def step(evs=None):
         if evs:
             evs[0].record(stream)
+        h0 = time.perf_counter()
         cf.cf_tft(ctx, pt, view, stream=stream)
+        h1 = time.perf_counter()
         l1 = cf.last_launch_count()
         if evs:
             evs[1].record(stream)
+        h2 = time.perf_counter()
         cf.cf_itft(ctx, pi, view, stream=stream)
+        h3 = time.perf_counter()
         l2 = cf.last_launch_count()
         if evs:
             evs[2].record(stream)
+        host_ms.append((round(1e3 * (h1 - h0), 2), round(1e3 * (h3 - h2), 2)))
         return l1 + l2
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    sampler.begin()
     g0.record(stream)
     launches = 0
     for k in range(args.steps):
         launches += step(evs[k])
     g1.record(stream)
     barrier()
+    sampler.end()
     clocks = sampler.stop()
     total_ms = g0.elapsed_time(g1)
     t_tft = sum(e[0].elapsed_time(e[1]) for e in evs)
     t_itft = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if os.environ.get("CFTFT_BENCH_DEBUG"):
+        print("per-step tft ms", [round(e[0].elapsed_time(e[1]), 2) for e in evs],
+              "itft ms", [round(e[1].elapsed_time(e[2]), 2) for e in evs], "host ms (tft, itft)", host_ms,
+              file=sys.stderr)
     if dist is not None:
         t = torch.tensor([total_ms, t_tft, t_itft], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

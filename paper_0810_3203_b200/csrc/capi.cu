@@ -2,6 +2,7 @@
 // sm_100a leaf kernels.  Host C++; no torch types anywhere.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -90,10 +91,26 @@ struct cftft_ring {
   // staging buffer for the host-view entry points
   void* stage = nullptr;
   size_t stage_bytes = 0;
+  // coset-plan scratch (shadow buffer, tops arrays), one per stream: reused
+  // across launches on that stream (stream order makes reuse safe; a
+  // stream-ordered pool allocation of 4 GB can cost the host tens of ms)
+  struct Scratch {
+    int dev = -1;
+    void* stream = nullptr;
+    void* shadow = nullptr;
+    size_t shadow_bytes = 0;
+    void* tops = nullptr;
+    size_t tops_bytes = 0;
+  };
+  std::vector<Scratch> scratch;
   CountReplay counts;
   ~cftft_ring() {
     if (stage) cudaFree(stage);
     if (ntt_tw) cudaFree(ntt_tw);
+    for (auto& sc : scratch) {
+      if (sc.shadow) cudaFree(sc.shadow);
+      if (sc.tops) cudaFree(sc.tops);
+    }
   }
 };
 
@@ -304,18 +321,47 @@ int check_stride(const cftft_ring* R, u64 stride) {
   return CFTFT_OK;
 }
 
+// Kernel attributes and occupancy are set / queried once per (device,
+// kernel): touching a kernel's attributes while an earlier launch of it runs
+// can stall the host until that launch ends.
+struct KernelInfo {
+  int dev;
+  const void* fn;
+  int threads;
+  size_t smem;
+  int per;
+};
+inline std::mutex g_kmu;
+inline std::vector<KernelInfo> g_kinfo;
+
 template <class K>
 int set_smem(K kernel) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_kmu);
+  for (const auto& k : g_kinfo)
+    if (k.dev == dev && k.fn == (const void*)kernel && k.threads == -1) return CFTFT_OK;
   CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget));
+  g_kinfo.push_back(KernelInfo{dev, (const void*)kernel, -1, 0, 0});
   return CFTFT_OK;
 }
 
 template <class K>
 int grid_for(K kernel, int threads, size_t smem, u64 nleaves, unsigned* grid) {
-  int dev = 0, sms = 0, per = 0;
+  int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
+  int per = -1, sms = 0;
+  {
+    std::lock_guard<std::mutex> g(g_kmu);
+    for (const auto& k : g_kinfo)
+      if (k.dev == dev && k.fn == (const void*)kernel && k.threads == threads && k.smem == smem) per = k.per;
+  }
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem));
+  if (per < 0) {
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem));
+    std::lock_guard<std::mutex> g(g_kmu);
+    g_kinfo.push_back(KernelInfo{dev, (const void*)kernel, threads, smem, per});
+  }
   if (per < 1) return fail(CFTFT_CUDA_ERROR, "leaf kernel does not fit on an SM");
   u64 g = (u64)sms * (u64)per;
   if (g > nleaves) g = nleaves;
@@ -341,15 +387,31 @@ int keep_pool() {
   return CFTFT_OK;
 }
 
+// CFTFT_HOST_TRACE=1: host-side time of each step of a launch (stderr)
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  HostTrace() : on(getenv("CFTFT_HOST_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[cftft host] %-14s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
   u64 launches = 0;
+  HostTrace ht;
   if (int rc = keep_pool()) return rc;
+  ht.mark("pool");
   if (dp.nleaves) {
     u32* counters = nullptr;
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
+    ht.mark("counters");
     // Fermat: two ticket buffers of `half` bytes each (a big ticket spans both)
     const size_t half = ((kSmemBudget - scratch_bytes(1024)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
@@ -383,9 +445,40 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       std::uint8_t* shadow = nullptr;
       if (dp.host.coset) {
         const size_t tb = 2 * (size_t)dp.host.extent * dp.C * sizeof(int);
-        CUDA_TRY(cudaMallocAsync((void**)&tops, tb, st));
+        const size_t sb = (size_t)dp.host.extent * stride;
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> g(R->mu);
+        cftft_ring::Scratch* sc = nullptr;
+        for (auto& x : R->scratch)
+          if (x.dev == dev && x.stream == (void*)st) sc = &x;
+        if (!sc) {
+          R->scratch.push_back(cftft_ring::Scratch{});
+          sc = &R->scratch.back();
+          sc->dev = dev;
+          sc->stream = (void*)st;
+        }
+        if (sc->tops_bytes < tb || sc->shadow_bytes < sb) {
+          CUDA_TRY(cudaStreamSynchronize(st));  // the old buffers may still be in use
+          if (sc->tops_bytes < tb) {
+            if (sc->tops) cudaFree(sc->tops);
+            sc->tops = nullptr;
+            sc->tops_bytes = 0;
+            CUDA_TRY(cudaMalloc(&sc->tops, tb));
+            sc->tops_bytes = tb;
+          }
+          if (sc->shadow_bytes < sb) {
+            if (sc->shadow) cudaFree(sc->shadow);
+            sc->shadow = nullptr;
+            sc->shadow_bytes = 0;
+            CUDA_TRY(cudaMalloc(&sc->shadow, sb));
+            sc->shadow_bytes = sb;
+          }
+        }
+        tops = static_cast<int*>(sc->tops);
+        shadow = static_cast<std::uint8_t*>(sc->shadow);
+        ht.mark("scratch");
         CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
-        CUDA_TRY(cudaMallocAsync((void**)&shadow, (size_t)dp.host.extent * stride, st));
       }
       A.T = tops;
       A.data2 = shadow;
@@ -405,7 +498,9 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       auto go = [&](auto kernel, int nt) -> int {
         if (int rc = set_smem(kernel)) return rc;
         if (int rc = grid_for(kernel, nt, smem, dp.nleaves, &grid)) return rc;
+        ht.mark("attrs");
         kernel<<<grid, nt, smem, st>>>(A);
+        ht.mark("launch");
         return CFTFT_OK;
       };
       int rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
@@ -418,7 +513,6 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
               base, shadow, stride, tops, A.tloc, dp.C, dp.shadow_finals, R->D);
           ++launches;
         }
-        CUDA_TRY(cudaFreeAsync(shadow, st));
         // carry-save lanes of the outputs (a batch: of every element it touched)
         // back to the canonical element format
         const u64 cnt = dp.host.final_count ? dp.host.final_count : dp.host.extent;
@@ -427,7 +521,6 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
                                                                (u32)__builtin_ctz(dp.C), dp.logS, R->D, 0, 1);
           ++launches;
         }
-        CUDA_TRY(cudaFreeAsync(tops, st));
       }
       if (prof) {
         unsigned long long h[fermat::PH_N];
