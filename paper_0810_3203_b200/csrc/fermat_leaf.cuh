@@ -551,8 +551,8 @@ __device__ __forceinline__ int* tops_row(const Args& A, u32 buf, u64 e) {
 }
 
 template <int CW, bool kLoad, int NT>
-__device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const DevLeaf& lf, const u64* locm, u32 nslots,
-                                           u32 smem_base, u32 boff, u32 tid) {
+__device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const DevLeaf& lf, const u64* locm, u32 k0,
+                                           u32 k1, u32 smem_base, u32 boff, u32 tid) {
   constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);  // log2 pieces per chunk
   const u32 C = G.C, SB = G.SB;
   const u32 lq = G.logC + lpc, q16 = 1u << lq;  // pieces per slot
@@ -564,8 +564,8 @@ __device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const De
     // each thread copies pieces tid, tid+NT, ... of every slot
     for (u32 pp = tid; pp < q16; pp += NT) {
       const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
-      u32 so = boff + so0;
-      for (u32 x = 0; x < nslots; ++x, so += SB) {
+      u32 so = boff + k0 * SB + so0;
+      for (u32 x = k0; x < k1; ++x, so += SB) {
         std::uint8_t* g = slot_ptr(x) + 16u * pp;
         if (kLoad)
           cp_async16(smem_base + so, g);
@@ -577,8 +577,8 @@ __device__ __forceinline__ void copy_slots(const Args& A, const Geo& G, const De
     // NT/q16 slots side by side; each thread keeps one piece position
     const u32 pp = tid & (q16 - 1), x0 = tid >> lq, step = (u32)NT >> lq;
     const u32 so0 = piece_off(0, pp >> lpc, pp & ((1u << lpc) - 1), C);
-    u32 so = boff + x0 * SB + so0;
-    for (u32 x = x0; x < nslots; x += step, so += step * SB) {
+    u32 so = boff + (k0 + x0) * SB + so0;
+    for (u32 x = k0 + x0; x < k1; x += step, so += step * SB) {
       std::uint8_t* g = slot_ptr(x) + 16u * pp;
       if (kLoad)
         cp_async16(smem_base + so, g);
@@ -598,14 +598,14 @@ constexpr u32 kClassTab = 48;
 // lanes through the slot's lane pre-rotation), the 4-byte word of the tops
 // array that holds each chunk's carry-save top (when in use), and each
 // slot's element top word.  fixup() turns these into int32 tops once landed.
+// Stages a ticket's per-slot buffer bits, (coset) lane pre-rotations and
+// input element pointers in shared memory; ends with a barrier.
 template <int CW, int NT>
-__device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
-                                           u32 boff, u32 tid, u32* rho, u64* locm, std::uint8_t** sp) {
+__device__ __forceinline__ void stage_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 tid, u32* rho,
+                                           u64* locm, std::uint8_t** sp) {
   const Geo G = geo_of(cl, lf, CW);
   const u32 nl = cl.nload;
   constexpr u32 CB = 32 * CW;
-  // stage the ticket's per-slot buffer bits, (coset) lane pre-rotations and
-  // input element pointers
   const u32 span = max(cl.nload, cl.nstore), nw = (span + 63) >> 6;
   for (u32 x = tid; x < 2 * kMaskWords; x += NT)
     locm[x] = (lf.locoff != kNoDep && x < 2 * nw) ? A.locbits[lf.locoff + x] : 0ull;
@@ -618,51 +618,70 @@ __device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, con
     }
   }
   __syncthreads();
-  if (nl) {
-    constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
-    const u32 CL = A.lanes;
-    const u32 sb = smem_base + boff;
-    if (G.coset) {
-      // thread -> fixed piece position (chunk j, piece q); slots strided
-      const u32 lq = G.logC + lpc, P = 1u << lq;
-      for (u32 pp = tid & (P - 1); pp < ((A.debug_skip & 16) ? 0u : P); pp += NT) {
-        const u32 j = pp >> lpc, q = pp & ((1u << lpc) - 1);
-        const u32 lj = lane_of(G, j) + 2 * CL;
-        const u32 so0 = piece_off(0, j, q, G.C);
-        const u32 kstep = NT > P ? NT / P : 1u;
-        for (u32 k = NT > P ? tid / P : 0u; k < nl; k += kstep) {
-          const u32 ln = (lj - rho[k]) & (CL - 1);
-          cp_async16(sb + k * G.SB + so0, sp[k] + (u64)ln * (CB / 8) + 16u * q);
-        }
+}
+
+// Issues the cp.async loads of slots [k0, k1) of a staged ticket into the
+// slot buffer at `boff`: the data chunks (coset tickets gather their lanes
+// through the slot's lane pre-rotation), the tops-array word of each chunk
+// (when in use), each slot's element top word.  fixup() finishes them.
+template <int CW, int NT>
+__device__ __forceinline__ void issue_slots(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
+                                            u32 boff, u32 tid, const u32* rho, const u64* locm,
+                                            std::uint8_t* const* sp, u32 k0, u32 k1) {
+  const Geo G = geo_of(cl, lf, CW);
+  k1 = min(k1, cl.nload);
+  if (k0 >= k1) return;
+  constexpr u32 CB = 32 * CW;
+  constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
+  const u32 CL = A.lanes;
+  const u32 sb = smem_base + boff;
+  if (G.coset) {
+    // thread -> fixed piece position (chunk j, piece q); slots strided
+    const u32 lq = G.logC + lpc, P = 1u << lq;
+    const u32 kstep = NT > P ? NT / P : 1u;
+    for (u32 pp = tid & (P - 1); pp < ((A.debug_skip & 16) ? 0u : P); pp += NT) {
+      const u32 j = pp >> lpc, q = pp & ((1u << lpc) - 1);
+      const u32 lj = lane_of(G, j) + 2 * CL;
+      const u32 so0 = piece_off(0, j, q, G.C);
+      for (u32 k = k0 + (NT > P ? tid / P : 0u); k < k1; k += kstep) {
+        const u32 ln = (lj - rho[k]) & (CL - 1);
+        cp_async16(sb + k * G.SB + so0, sp[k] + (u64)ln * (CB / 8) + 16u * q);
       }
-      if (A.T && !(A.debug_skip & 8)) {
-        const u32 Pc = G.C;
-        for (u32 j = tid & (Pc - 1); j < Pc; j += NT) {
-          const u32 lj = lane_of(G, j) + 2 * CL;
-          const u32 kstep = NT > Pc ? NT / Pc : 1u;
-          for (u32 k = NT > Pc ? tid / Pc : 0u; k < nl; k += kstep) {
-            const u32 ln = (lj - rho[k]) & (CL - 1);
-            const u32 b = in_buf(locm, k);
-            const int* tr = A.T + (b ? A.tloc : 0) + (lf.base + (u64)k * lf.stride) * CL;
-            cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, ln));
-          }
-        }
-      }
-      for (u32 k = tid; k < nl; k += NT) cp_async8(sb + k * G.SB + G.HO, sp[k] + 4ull * A.D);
-    } else {
-      copy_slots<CW, true, NT>(A, G, lf, locm, nl, smem_base, boff, tid);
-      if (A.T) {
-        const u32 tt = nl << G.logC;
-        for (u32 idx = tid; idx < tt; idx += NT) {
-          const u32 k = idx >> G.logC, j = idx & G.Cm;
-          const int* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
-          cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, j));
-        }
-      }
-      for (u32 k = tid; k < nl; k += NT)
-        cp_async8(sb + k * G.SB + G.HO, elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride) + 4ull * A.D);
     }
+    if (A.T && !(A.debug_skip & 8)) {
+      const u32 Pc = G.C;
+      const u32 kstep = NT > Pc ? NT / Pc : 1u;
+      for (u32 j = tid & (Pc - 1); j < Pc; j += NT) {
+        const u32 lj = lane_of(G, j) + 2 * CL;
+        for (u32 k = k0 + (NT > Pc ? tid / Pc : 0u); k < k1; k += kstep) {
+          const u32 ln = (lj - rho[k]) & (CL - 1);
+          const u32 b = in_buf(locm, k);
+          const int* tr = A.T + (b ? A.tloc : 0) + (lf.base + (u64)k * lf.stride) * CL;
+          cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, ln));
+        }
+      }
+    }
+    for (u32 k = k0 + tid; k < k1; k += NT) cp_async8(sb + k * G.SB + G.HO, sp[k] + 4ull * A.D);
+  } else {
+    copy_slots<CW, true, NT>(A, G, lf, locm, k0, k1, smem_base, boff, tid);
+    if (A.T) {
+      const u32 tt = (k1 - k0) << G.logC;
+      for (u32 idx = tid; idx < tt; idx += NT) {
+        const u32 k = k0 + (idx >> G.logC), j = idx & G.Cm;
+        const int* tr = tops_row(A, in_buf(locm, k), lf.base + (u64)k * lf.stride);
+        cp_async4(sb + k * G.SB + G.W4 + 4 * j, tr + tops_ix(A, j));
+      }
+    }
+    for (u32 k = k0 + tid; k < k1; k += NT)
+      cp_async8(sb + k * G.SB + G.HO, elem_ptr(A, in_buf(locm, k), lf.base + (u64)k * lf.stride) + 4ull * A.D);
   }
+}
+
+template <int CW, int NT>
+__device__ __forceinline__ void issue_load(const Args& A, const DevLeaf& lf, const DevClass& cl, u32 smem_base,
+                                           u32 boff, u32 tid, u32* rho, u64* locm, std::uint8_t** sp) {
+  stage_load<CW, NT>(A, lf, cl, tid, rho, locm, sp);
+  issue_slots<CW, NT>(A, lf, cl, smem_base, boff, tid, rho, locm, sp, 0, cl.nload);
   cp_async_commit();
 }
 
@@ -782,7 +801,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     u32 tnn = 0xFFFFFFFFu;
     if (tid == 0 && have_next) tnn = atomicAdd(&A.counters[0], 1u);
     // the next ticket streams into the other buffer while this one computes
-    bool prefetched = false;
+    bool prefetched = false, rolled = false;
     if (have_next && s_ready[nxt] && small_ticket(A, cl) && small_ticket(A, s_cl[nxt])) {
       if (tid == 0) s_boff[nxt] = boff ^ A.half;
       issue_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, boff ^ A.half, tid, s_rho[nxt], s_loc[nxt], s_sp[nxt]);
@@ -974,8 +993,11 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         }
       }
       __syncthreads();
-      // (2) coalesced copy of the lanes to their rotated positions
-      {
+      // (2) coalesced copy of the lanes to their rotated positions.  When the
+      //     next ticket is ready and lands in this buffer, the copy runs in two
+      //     halves: the next ticket's loads stream into the freed first half
+      //     while the second half is stored.
+      auto store_range = [&](u32 k0, u32 k1) {
         constexpr u32 lpc = CW == 16 ? 2 : (CW == 8 ? 1 : 0);
         const u32 lq = logC + lpc, P = 1u << lq;
         const u32 kstep = nthr > P ? nthr / P : 1u;
@@ -983,14 +1005,31 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
           const u32 j = pp >> lpc, q = pp & ((1u << lpc) - 1);
           const u32 lj = lane_of(G, j);
           const u32 so0 = piece_off(0, j, q, C);
-          for (u32 k = nthr > P ? tid / P : 0u; k < cl.nstore; k += kstep) {
+          for (u32 k = k0 + (nthr > P ? tid / P : 0u); k < k1; k += kstep) {
             const u32 d = (lj + s_rhp[k]) & CLm;
             __stcg(reinterpret_cast<uint4*>(s_op[k] + (u64)d * (CB / 8) + 16u * q),
                    *reinterpret_cast<const uint4*>(g_sm + boff + k * SB + so0));
           }
         }
+      };
+      if (have_next && !prefetched && boff == 0 && s_ready[nxt] && cl.nstore >= 2) {
+        const u32 h = cl.nstore / 2;
+        store_range(0, h);
+        __syncthreads();
+        if (tid == 0) s_boff[nxt] = 0;
+        stage_load<CW, NT>(A, s_lf[nxt], s_cl[nxt], tid, s_rho[nxt], s_loc[nxt], s_sp[nxt]);
+        const u32 h2 = (h * SB) / s_cl[nxt].slot_bytes;
+        issue_slots<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt], s_loc[nxt], s_sp[nxt], 0, h2);
+        store_range(h, cl.nstore);
+        __syncthreads();
+        issue_slots<CW, NT>(A, s_lf[nxt], s_cl[nxt], smem_base, 0, tid, s_rho[nxt], s_loc[nxt], s_sp[nxt], h2,
+                            0xFFFFFFFFu);
+        cp_async_commit();
+        rolled = true;
+      } else {
+        store_range(0, cl.nstore);
+        __syncthreads();  // slot reuse
       }
-      __syncthreads();  // slot reuse
       pc.mark(PH_STORE);
     } else {
       // ---- post-rotation + carry resolution + store: NG slots per round ------------
@@ -1062,7 +1101,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         pc.mark(PH_STORE);
       }
       // the whole leaf is resolved in shared memory: one coalesced copy to HBM
-      copy_slots<CW, false, NT>(A, G, lf, locm, cl.nstore, smem_base, boff, tid);
+      copy_slots<CW, false, NT>(A, G, lf, locm, 0, cl.nstore, smem_base, boff, tid);
       for (u32 x = tid; x < cl.nstore; x += nthr)
         __stcg(reinterpret_cast<long long*>(elem_ptr(A, out_buf(locm, x), lf.base + (u64)x * lf.stride) + W4e),
                (long long)lds_i32(boff + x * SB + W4));
@@ -1097,7 +1136,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         k = cm.next;
       }
     }
-    if (have_next && !prefetched) {
+    if (have_next && !prefetched && !rolled) {
       if (tid == 0) {
         while (!dep_met(s_lf[nxt])) __nanosleep(64);
         s_boff[nxt] = 0;
