@@ -20,6 +20,7 @@
 #include "fermat_leaf.cuh"
 #include "negacyclic_leaf.cuh"
 #include "pointwise.cuh"
+#include "wave_coset.cuh"
 #include "planner.hpp"
 
 using namespace cftft_b200;
@@ -57,6 +58,8 @@ struct DevicePlan {
   const DevCounter* cmeta = nullptr;
   const u64* locbits = nullptr;
   const u64* shadow_finals = nullptr;
+  const u32* wave_ops = nullptr;
+  const u32* wave_slots = nullptr;
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
@@ -75,6 +78,7 @@ using PlanKey = std::tuple<int, int, u64, u64, u64, u64, int, int>;  // dev, inv
 struct cftft_ring {
   int kind = 0;
   int coset_cw = -1;          // Fermat coset leaves: -1 auto, 0 off, 4/8/16 lane words
+  int wave = -1;              // Fermat wave engine: -1 auto, 0 off, 1 on
   unsigned leaf_limit = 0;    // cftft_ring_set_leaf_limit (0: none)
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
@@ -147,6 +151,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.inverse = (u32)c.key.inverse;
     d.spec_n = c.key.inverse ? (u32)c.key.n : 0;
     d.fslot = (c.key.inverse && c.key.f) ? (u32)c.key.n : 0xFFFFFFFFu;
+    d.wop_begin = cls.size() < p.wave_op_begin.size() ? p.wave_op_begin[cls.size()] : 0;
     cls.push_back(d);
   }
   if (rots.empty()) rots.push_back(SymExp{});
@@ -166,7 +171,9 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   size_t o_cm = al(o_lf + leaves.size() * sizeof(DevLeaf));
   size_t o_lb = al(o_cm + cm.size() * sizeof(DevCounter));
   size_t o_sf = al(o_lb + p.locbits.size() * sizeof(u64));
-  size_t total = al(o_sf + p.shadow_finals.size() * sizeof(u64)) + 256;
+  size_t o_wo = al(o_sf + p.shadow_finals.size() * sizeof(u64));
+  size_t o_ws = al(o_wo + p.wave_ops.size() * sizeof(u32));
+  size_t total = al(o_ws + p.wave_slots.size() * sizeof(u32)) + 256;
   std::vector<std::uint8_t> h(total, 0);
   std::memcpy(h.data() + o_cls, cls.data(), cls.size() * sizeof(DevClass));
   std::memcpy(h.data() + o_ops, ops.data(), ops.size() * sizeof(DevOp));
@@ -177,6 +184,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   if (!p.locbits.empty()) std::memcpy(h.data() + o_lb, p.locbits.data(), p.locbits.size() * sizeof(u64));
   if (!p.shadow_finals.empty())
     std::memcpy(h.data() + o_sf, p.shadow_finals.data(), p.shadow_finals.size() * sizeof(u64));
+  if (!p.wave_ops.empty()) std::memcpy(h.data() + o_wo, p.wave_ops.data(), p.wave_ops.size() * sizeof(u32));
+  if (!p.wave_slots.empty()) std::memcpy(h.data() + o_ws, p.wave_slots.data(), p.wave_slots.size() * sizeof(u32));
   CUDA_TRY(cudaMalloc(&dp.dbuf, total));
   CUDA_TRY(cudaMemcpyAsync(dp.dbuf, h.data(), total, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // h is a temporary
@@ -189,6 +198,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.cmeta = reinterpret_cast<const DevCounter*>(b + o_cm);
   dp.locbits = reinterpret_cast<const u64*>(b + o_lb);
   dp.shadow_finals = reinterpret_cast<const u64*>(b + o_sf);
+  dp.wave_ops = reinterpret_cast<const u32*>(b + o_wo);
+  dp.wave_slots = reinterpret_cast<const u32*>(b + o_ws);
   (void)R;
   return CFTFT_OK;
 }
@@ -241,6 +252,13 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         if ((u64{1} << e) <= 2ull * C && (u64{1} << e) * slot <= budget / 2) cl = e;
       }
       if (R->leaf_limit) cl = std::min(cl, std::max(1u, R->leaf_limit));
+      static const int env_wave = getenv("CFTFT_WAVE") ? atoi(getenv("CFTFT_WAVE")) : -1;
+      const int wave = R->wave >= 0 ? R->wave : (env_wave >= 0 ? env_wave : 0);
+      if (wave && cw == 8) {
+        rs.wave_engine = true;
+        cl = std::min(cl, 3u);
+        rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
+      }
       rs.coset_max_ell = cl;
       if (!cl) rs.lane_bits = 0;
     }
@@ -256,7 +274,7 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
     dp->C = C;
     dp->slot_bytes = sb;
     u32 logS = 0;
-    if (rs.lane_bits) {
+    if (rs.lane_bits && !rs.wave_engine) {
       const u64 S = std::max<u64>(1, (2ull * C) >> rs.coset_max_ell);
       logS = (u32)__builtin_ctzll(S);
     }
@@ -485,6 +503,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.tloc = (u64)dp.host.extent * dp.C;
       A.locbits = dp.locbits;
       A.nclasses = (u32)dp.host.classes.size();
+      A.no_deps = 0;
       A.half = (u32)half;
       unsigned long long* prof = nullptr;
       static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
@@ -503,9 +522,59 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         ht.mark("launch");
         return CFTFT_OK;
       };
-      int rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
-               : dp.cw == 8 ? (getenv("CFTFT_NT1024") ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
-                            : go(fermat::leaf_kernel<4, 512>, 512);
+      int rc = 0;
+      if (!dp.host.waves.empty()) {
+        // wave engine: one launch per range of independent tickets, in order;
+        // coset ranges on the warp-level kernel, whole ranges on the leaf kernel
+        A.no_deps = 1;
+        fermat::WaveArgs W{};
+        W.classes = dp.classes;
+        W.ops = dp.ops;
+        W.rots = dp.rots;
+        W.data = base;
+        W.data2 = A.data2;
+        W.elem_bytes = stride;
+        W.T = tops;
+        W.tloc = A.tloc;
+        W.locbits = dp.locbits;
+        W.wops = dp.wave_ops;
+        W.wslots = dp.wave_slots;
+        W.lanes = dp.C;
+        W.D = R->D;
+        W.M = R->M;
+        const size_t wsmem = (size_t)fermat::kWaveWarps * fermat::wave_tile_words<8>() * 4;
+        static bool wave_attr = false;
+        if (!wave_attr) {
+          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)wsmem));
+          wave_attr = true;
+        }
+        int dev = 0, sms = 0, per = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8>,
+                                                               32 * fermat::kWaveWarps, wsmem));
+        for (const auto& wr : dp.host.waves) {
+          if (wr[2] == 1) {
+            W.leaves = dp.leaves + wr[0];
+            W.nleaves = (u32)wr[1];
+            const unsigned g = (unsigned)std::min<u64>(wr[1], (u64)sms * std::max(per, 1));
+            fermat::coset_wave_kernel<8><<<g, 32 * fermat::kWaveWarps, wsmem, st>>>(W);
+          } else {
+            CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(u32), st));  // ticket counter of this range
+            A.leaves = dp.leaves + wr[0];
+            A.nleaves = wr[1];
+            rc = go(fermat::leaf_kernel<8, 512>, 512);
+            if (rc) return rc;
+          }
+          ++launches;
+        }
+        launches -= 1;  // counted once more below
+      } else {
+        rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
+             : dp.cw == 8 ? (getenv("CFTFT_NT1024") ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
+                          : go(fermat::leaf_kernel<4, 512>, 512);
+      }
       if (rc) return rc;
       if (tops) {
         if (!dp.host.shadow_finals.empty()) {

@@ -56,6 +56,7 @@ struct Args {
   u64 tloc;                // tops entries per buffer
   const u64* locbits;      // per-slot buffer bits (DevLeaf::locoff)
   u32 nclasses;
+  u32 no_deps;             // launch order already separates dependent tickets (wave engine)
   u32 half;                // bytes of one of the two ticket buffers (double buffering)
   u32 lanes, logLanes;     // lanes (chunks) per element
   u32 logS;                // tops-array lane interleave
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
   pc.start(tid == 0 && A.prof != nullptr);
 
   auto dep_met = [&](const DevLeaf& l) {
-    return (l.dep == kNoDep) || (ld_acquire(&A.counters[1 + l.dep]) >= l.dep_target);
+    return A.no_deps || (l.dep == kNoDep) || (ld_acquire(&A.counters[1 + l.dep]) >= l.dep_target);
   };
   auto fetch = [&](u32 r) {  // tid 0 only
     const u32 t = atomicAdd(&A.counters[0], 1u);
@@ -1125,7 +1126,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     pc.mark(PH_STORE);
     // publish completion: bump the phase counter; the last child of a node's
     // last phase finishes the node and reports to the parent phase in turn
-    if (tid == 0 && lf.comp != kNoDep) {
+    if (tid == 0 && lf.comp != kNoDep && !A.no_deps) {
       if (!(A.debug_skip & 4)) __threadfence();
       u32 k = lf.comp;
       for (;;) {

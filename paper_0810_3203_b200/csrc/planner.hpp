@@ -30,6 +30,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -98,6 +99,7 @@ struct DevClass {
   u32 inverse;     // ITFT program: tpre goes to pre slots < spec_n, tpost to post slot fslot;
   u32 spec_n;      // TFT program: tpost goes to every post slot
   u32 fslot;
+  u32 wop_begin;   // wave engine, coset classes: first packed op in Plan::wave_ops
 };
 
 constexpr u32 kNoDep = 0xFFFFFFFFu;
@@ -172,6 +174,16 @@ struct Plan {
   u64 extent = 0;         // view indices [0, extent) touched (tops array rows)
   std::vector<u64> locbits;        // per-slot buffer bits (see DevLeaf::locoff)
   std::vector<u64> shadow_finals;  // outputs the schedule leaves in the shadow buffer
+  // wave engine: ticket ranges of mutually independent leaves, launched in
+  // order; {first ticket, count, kind (0 whole, 1 coset)}
+  std::vector<std::array<u64, 3>> waves;
+  // wave engine, coset classes: micro-ops packed as type | a << 4 | b << 8 |
+  // q << 12, q the rotation in coset positions (class order, see wop_begin)
+  std::vector<u32> wave_ops;
+  std::vector<u32> wave_op_begin;  // per class
+  // wave engine, coset tickets: per slot {pre lanes | in-buffer << 31,
+  // post lanes | out-buffer << 31}, at DevLeaf::c0 (reused as the offset)
+  std::vector<u32> wave_slots;
 };
 
 // Ring-dependent planning parameters.
@@ -192,6 +204,9 @@ struct RingShape {
   u64 slot_budget = 0;  // shared-memory bytes available for a leaf's slots
   u32 wave_overlap = 0;  // waves by which consecutive L2 batches overlap in the ticket order
   u64 ticket_budget = 0;  // shared-memory bytes a coset ticket may fill (default: one of two buffers)
+  // wave engine: leaves of <= 8 coefficients, one launch per independent wave;
+  // coset leaves run on the warp-level kernel (csrc/wave_coset.cuh)
+  bool wave_engine = false;
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -351,6 +366,50 @@ class Planner {
       if (loc[e]) p.shadow_finals.push_back(e);
   }
 
+  // Host-side precomputation for the warp-level kernel: packed micro-ops per
+  // coset class and per-slot lane rotations / buffers per coset ticket.
+  void wave_tables(Plan& p) {
+    const u64 M = rs_.M, lb = rs_.lane_bits;
+    p.wave_ops.clear();
+    p.wave_op_begin.assign(classes_.size(), 0);
+    for (size_t c = 0; c < classes_.size(); ++c) {
+      const LeafProgram& cl = classes_[c];
+      p.wave_op_begin[c] = (u32)p.wave_ops.size();
+      if (cl.kind != 1) continue;
+      for (const auto& op : cl.ops) {
+        const u64 q = op.type == OP_COPY ? 0 : (op.r / lb) / cl.step;
+        p.wave_ops.push_back((u32)op.type | ((u32)op.a << 4) | ((u32)op.b << 8) | ((u32)q << 12));
+      }
+    }
+    p.wave_slots.clear();
+    for (auto& lf : leaves_) {
+      const LeafProgram& cl = classes_[lf.cls];
+      if (cl.kind != 1) continue;
+      const u32 off = (u32)p.wave_slots.size();
+      const u32 span = std::max(cl.nload, cl.nstore);
+      for (u32 k = 0; k < span; ++k) {
+        const bool inv = cl.key.inverse != 0;
+        u32 pre = 0, post = 0;
+        if (k < cl.nload) {
+          const u64 r = (cl.pre[k].a * lf.s + cl.pre[k].b + ((inv && k < cl.key.n) ? lf.tpre : 0)) & (M - 1);
+          pre = (u32)(r / lb);
+        }
+        if (k < cl.nstore) {
+          const bool tp = inv ? (cl.key.f && k == cl.key.n) : true;
+          const u64 r = (cl.post[k].a * lf.s + cl.post[k].b + (tp ? lf.tpost : 0)) & (M - 1);
+          post = (u32)(r / lb);
+        }
+        if (lf.locoff != kNoDep) {
+          if ((p.locbits[lf.locoff + 2 * (k / 64)] >> (k % 64)) & 1) pre |= 1u << 31;
+          if ((p.locbits[lf.locoff + 2 * (k / 64) + 1] >> (k % 64)) & 1) post |= 1u << 31;
+        }
+        p.wave_slots.push_back(pre);
+        p.wave_slots.push_back(post);
+      }
+      lf.c0 = off;
+    }
+  }
+
   // ticket order: (top phase, batch, wave, top child, emission order), with
   // the waves of consecutive L2 batches overlapped by `overlap` waves: batch
   // b's wave w is ranked at w + (W - overlap) b (W = waves per batch), so the
@@ -359,6 +418,7 @@ class Planner {
   // independent, and each keeps its own wave order.
   void finish(Plan& p, const std::vector<u64>& finals) {
     if (coset_used_) assign_buffers(p, finals);
+    if (rs_.wave_engine) wave_tables(p);
     std::vector<u32> idx(leaves_.size());
     for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
     u32 W = 1;
@@ -366,10 +426,24 @@ class Planner {
     const u32 ov = std::min(W - 1, rs_.wave_overlap);
     auto rank = [&](u32 x) {
       const auto& k = keys_[x];
+      if (rs_.wave_engine)  // (top phase, wave, kind): every range is independent
+        return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k), (u64)classes_[leaves_[x].cls].kind,
+                               std::get<3>(k), std::get<4>(k));
       return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k) + (u64)(W - ov) * std::get<1>(k), std::get<1>(k),
                              std::get<3>(k), std::get<4>(k));
     };
     std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return rank(x) < rank(y); });
+    p.waves.clear();
+    if (rs_.wave_engine) {
+      for (size_t t = 0; t < idx.size(); ++t) {
+        const auto& k = keys_[idx[t]];
+        const u64 kind = classes_[leaves_[idx[t]].cls].kind;
+        if (t == 0 || std::get<0>(keys_[idx[t - 1]]) != std::get<0>(k) ||
+            std::get<2>(keys_[idx[t - 1]]) != std::get<2>(k) || p.waves.back()[2] != kind)
+          p.waves.push_back({(u64)t, 0, kind});
+        p.waves.back()[1] += 1;
+      }
+    }
     p.leaves.reserve(idx.size());
     p.leaf_wave.reserve(idx.size());
     for (u32 i : idx) {
@@ -712,6 +786,7 @@ class Planner {
       u64 m = 1;
       while (m * 2 <= prog.step && m * 2 * cl <= 512 && L * coset_slot_bytes(m * 2 * cl) <= rs_.ticket_budget)
         m *= 2;
+      if (rs_.wave_engine) m = prog.step;  // one ticket per leaf: the warp kernel covers all cosets
       prog.m = (u32)m;
       prog.cs = (u32)(m * cl);
       prog.slot_bytes = coset_slot_bytes(prog.cs);

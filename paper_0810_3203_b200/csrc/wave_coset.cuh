@@ -1,0 +1,213 @@
+// wave_coset.cuh -- warp-level engine for small coset leaves (2^lambda <= 8
+// coefficients), one launch per wave of independent leaves.
+//
+// A coset leaf's rotations are whole multiples of its coset step (planner.hpp,
+// DevClass), so lane p of every output depends only on the lanes
+// p' == p (mod step) of its inputs.  Here one warp owns 2^cb cosets x C'
+// positions (cb = 6 - lambda, C' = 2^(lambda-1)): lane l holds the 256-bit
+// chunk of element lane  c + step * pos  (c = coset, pos = l >> cb) of every
+// slot of the leaf.  A butterfly reads its own chunk of `a` and the chunk of
+// the rotated `b` from the lane (pos - q) of the same coset -- a permutation
+// inside the warp -- so the whole leaf runs with __syncwarp only: no CTA
+// barriers, no tickets, no dependency counters (launch order separates the
+// waves).  Chunks live in a per-warp shared-memory tile [slot][word][lane]
+// (conflict-free: a warp always touches 32 distinct lanes of one row).
+//
+// Formats are the persistent engine's (fermat_leaf.cuh): carry-save lanes
+// with an int32 top per lane in the tops array, the coefficient's top word
+// folded into lane 0 by the lane that reads it, the two-buffer ping-pong of
+// DevLeaf::locoff, the pre / post rotations of DevClass / DevLeaf.
+#pragma once
+
+#include "fermat_leaf.cuh"
+
+namespace cftft_b200 {
+namespace fermat {
+
+struct WaveArgs {
+  const DevLeaf* leaves;  // this wave's coset tickets (one per leaf)
+  u32 nleaves;
+  const DevClass* classes;
+  const DevOp* ops;
+  const SymExp* rots;
+  std::uint8_t* data;   // caller's view
+  std::uint8_t* data2;  // shadow buffer
+  u64 elem_bytes;
+  int* T;               // tops, [buffer][element][lane] (natural lane order)
+  u64 tloc;
+  const u64* locbits;
+  const u32* wops;      // packed micro-ops (Plan::wave_ops)
+  const u32* wslots;    // per-slot {pre, post} lane rotations | buffer bits (Plan::wave_slots)
+  u32 lanes;            // lanes per coefficient (C)
+  u32 D;                // u32 words per coefficient
+  u64 M;
+};
+
+constexpr int kWaveWarps = 8;
+
+// per warp: 8 slots x 32 lanes x a 16-byte aligned row of CW words + top
+// (+ pad); rows 48 bytes apart keep 16-byte lane accesses conflict free
+template <int CW>
+__host__ __device__ constexpr u32 wave_row_words() {
+  return (CW + 1 + 3) & ~3u;
+}
+template <int CW>
+__host__ __device__ constexpr u32 wave_tile_words() {
+  return 8u * 32u * wave_row_words<CW>() + 16u;  // + the slots' top words (8 x u64)
+}
+
+template <int CW>
+__global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A) {
+  extern __shared__ __align__(16) u32 wsm[];
+  constexpr u32 CB = 32 * CW;
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u32* const tile = wsm + warp * wave_tile_words<CW>();
+  const u32 CL = A.lanes;
+  const u64 Mm = A.M - 1;
+  constexpr u32 RR = wave_row_words<CW>();
+  auto row = [&](u32 slot, u32 l) -> u32* { return tile + (slot * 32u + l) * RR; };
+  long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * RR);  // per slot top word
+  auto ld = [&](Ch<CW>& c, u32 slot, u32 l) -> int {
+    const u32* r = row(slot, l);
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(r + 4 * q);
+      c.w[4 * q] = v.x;
+      c.w[4 * q + 1] = v.y;
+      c.w[4 * q + 2] = v.z;
+      c.w[4 * q + 3] = v.w;
+    }
+    return (int)r[CW];
+  };
+  auto st = [&](u32 slot, u32 l, const Ch<CW>& c, int top) {
+    u32* r = row(slot, l);
+#pragma unroll
+    for (int q = 0; q < CW / 4; ++q)
+      *reinterpret_cast<uint4*>(r + 4 * q) = make_uint4(c.w[4 * q], c.w[4 * q + 1], c.w[4 * q + 2], c.w[4 * q + 3]);
+    r[CW] = (u32)top;
+  };
+  const u32 tile_s = (u32)__cvta_generic_to_shared(tile);
+
+  for (u32 t = blockIdx.x; t < A.nleaves; t += gridDim.x) {
+    const DevLeaf lf = A.leaves[t];
+    const DevClass cl = A.classes[lf.cls];
+    const u32 ell = 31 - __clz(cl.L);
+    const u32 cp = 1u << (ell - 1);   // positions per coset
+    const u32 cb = 6 - ell;           // coset bits of the lane index
+    const u32 cmask = (1u << cb) - 1;
+    const u32 step = cl.step;
+    const u32 groups = max(1u, step >> cb);
+    for (u32 g = warp; g < groups; g += kWaveWarps) {
+      const u32 c = (g << cb) + (lane & cmask);
+      const u32 pos = lane >> cb;
+      const bool act = c < step && pos < cp;
+      const u32 L0 = c + step * pos;  // this lane's element lane (frame)
+
+      // ---- load: gather through the pre-rotation (all slots in flight at
+      //      once), then fold the top word and negate wrapped lanes
+      u32 wrapped = 0, lane0 = 0;  // per-slot bit masks of this lane
+      const u32* const sl = A.wslots + lf.c0;  // {pre, post} per slot
+      for (u32 k = 0; k < cl.nload; ++k) {
+        if (!act) break;
+        const u32 pre = sl[2 * k];
+        const u32 src = (L0 + 2 * CL - (pre & 0x7FFFFFFFu)) & (2 * CL - 1);
+        const u32 ln = src & (CL - 1);
+        const u32 ib = pre >> 31;
+        const u64 e = lf.base + (u64)k * lf.stride;
+        const std::uint8_t* el = (ib ? A.data2 : A.data) + e * A.elem_bytes;
+        const u32 so = tile_s + (k * 32u + lane) * RR * 4u;
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q) cp_async16(so + 16u * q, el + (u64)ln * (CB / 8) + 16u * q);
+        if (A.T) cp_async4(so + 4u * CW, A.T + (ib ? A.tloc : 0) + e * CL + ln);
+        if (ln == 0) {
+          cp_async8(tile_s + (8u * 32u * RR) * 4u + 8u * k, el + 4ull * A.D);
+          lane0 |= 1u << k;
+        }
+        if (src >= CL) wrapped |= 1u << k;
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      for (u32 k = 0; k < cl.nload; ++k) {
+        if (!act) break;
+        const bool has_hi = (lane0 >> k) & 1u, neg = (wrapped >> k) & 1u;
+        int top = A.T ? (int)row(k, lane)[CW] : 0;
+        if (!A.T) row(k, lane)[CW] = 0;
+        if (!has_hi && !neg) continue;
+        Ch<CW> w;
+        ld(w, k, lane);
+        if (has_hi) {
+          const int hi = (int)hiw[k];
+          if (hi) top += ch_add_small<CW>(w, -hi);
+        }
+        if (neg) top = exact_from<CW>(w, top, true);
+        st(k, lane, w, top);
+      }
+      __syncwarp();
+      // ---- the leaf program: every lane runs every micro-op on its chunk
+      for (u32 o = 0; o < cl.nops; ++o) {
+        const u32 wop = A.wops[cl.wop_begin + o];
+        struct {
+          u32 type, a, b, q;
+        } op{wop & 15u, (wop >> 4) & 15u, (wop >> 8) & 15u, wop >> 12};
+        Ch<CW> a, b, y0, y1;
+        int pa = 0, pb = 0, t0 = 0, t1 = 0;
+        if (act) {
+          pa = ld(a, op.a, lane);
+          if (op.type == OP_COPY) {
+            y1 = a;
+            t1 = pa;
+          } else {
+            const u32 qv = op.q;  // positions, < 2 cp
+            const u32 sneg = qv >= cp ? 1u : 0u;
+            const u32 qq = qv - (sneg ? cp : 0u);
+            const u32 pl = (((pos - qq) & (cp - 1)) << cb) | (lane & cmask);
+            const bool neg = ((pos < qq) ? 1u : 0u) != sneg;
+            pb = ld(b, op.b, pl);
+            // y0 = a + s b, y1 = a - s b with s = (-1)^neg
+            if (!neg) {
+              t0 = ch_add(y0, a, b) + pa + pb;
+              t1 = ch_sub(y1, a, b) + pa - pb;
+            } else {
+              t0 = ch_sub(y0, a, b) + pa - pb;
+              t1 = ch_add(y1, a, b) + pa + pb;
+            }
+            if (op.type == OP_SUB2 || op.type == OP_SUB2DIFF) t0 = ch_add(y0, a, y1) + pa + t1;
+          }
+        }
+        __syncwarp();
+        if (act) {
+          if (op.type != OP_COPY) st(op.a, lane, y0, t0);
+          if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF || op.type == OP_COPY) st(op.b, lane, y1, t1);
+        }
+        __syncwarp();
+      }
+
+      // ---- store: scatter through the post-rotation, carry-save out
+      for (u32 k = 0; k < cl.nstore; ++k) {
+        if (!act) break;
+        const u32 post = sl[2 * k + 1];
+        const u32 dst = (L0 + (post & 0x7FFFFFFFu)) & (2 * CL - 1);
+        const u32 d = dst & (CL - 1);
+        const u32 ob = post >> 31;
+        const u64 e = lf.base + (u64)k * lf.stride;
+        std::uint8_t* el = (ob ? A.data2 : A.data) + e * A.elem_bytes;
+        Ch<CW> w;
+        int top = ld(w, k, lane);
+        if (dst >= CL) top = exact_from<CW>(w, top, true);
+        uint4* gp = reinterpret_cast<uint4*>(el + (u64)d * (CB / 8));
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q)
+          __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
+        __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
+        // the lane that took the top word (source lane 0), or for an
+        // output-only slot the lane writing lane 0, clears the output's
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sl[2 * k] & 0x7FFFFFFFu)) & (CL - 1)) == 0 : d == 0;
+        if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace fermat
+}  // namespace cftft_b200
