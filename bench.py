@@ -553,7 +553,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": kernel_gbs, "peak": peak, "unit": "GB/s",
                          "frac": kernel_gbs / peak, "peak_kind": peak_kind,
                          "traffic": load_traffic(args.config),
-                         "kernel": "leaf_kernel waves (all kernels of the step)",
+                         "kernel": "coset_wave_kernel + leaf_kernel waves (all kernels of the step)",
                          "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -60,6 +60,7 @@ struct DevicePlan {
   const u64* shadow_finals = nullptr;
   const u32* wave_ops = nullptr;
   const u32* wave_slots = nullptr;
+  const u32* final_rot = nullptr;
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
@@ -173,7 +174,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   size_t o_sf = al(o_lb + p.locbits.size() * sizeof(u64));
   size_t o_wo = al(o_sf + p.shadow_finals.size() * sizeof(u64));
   size_t o_ws = al(o_wo + p.wave_ops.size() * sizeof(u32));
-  size_t total = al(o_ws + p.wave_slots.size() * sizeof(u32)) + 256;
+  size_t o_fr = al(o_ws + p.wave_slots.size() * sizeof(u32));
+  size_t total = al(o_fr + p.final_rot.size() * sizeof(u32)) + 256;
   std::vector<std::uint8_t> h(total, 0);
   std::memcpy(h.data() + o_cls, cls.data(), cls.size() * sizeof(DevClass));
   std::memcpy(h.data() + o_ops, ops.data(), ops.size() * sizeof(DevOp));
@@ -186,6 +188,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     std::memcpy(h.data() + o_sf, p.shadow_finals.data(), p.shadow_finals.size() * sizeof(u64));
   if (!p.wave_ops.empty()) std::memcpy(h.data() + o_wo, p.wave_ops.data(), p.wave_ops.size() * sizeof(u32));
   if (!p.wave_slots.empty()) std::memcpy(h.data() + o_ws, p.wave_slots.data(), p.wave_slots.size() * sizeof(u32));
+  if (!p.final_rot.empty()) std::memcpy(h.data() + o_fr, p.final_rot.data(), p.final_rot.size() * sizeof(u32));
   CUDA_TRY(cudaMalloc(&dp.dbuf, total));
   CUDA_TRY(cudaMemcpyAsync(dp.dbuf, h.data(), total, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // h is a temporary
@@ -200,6 +203,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.shadow_finals = reinterpret_cast<const u64*>(b + o_sf);
   dp.wave_ops = reinterpret_cast<const u32*>(b + o_wo);
   dp.wave_slots = reinterpret_cast<const u32*>(b + o_ws);
+  dp.final_rot = p.final_rot.empty() ? nullptr : reinterpret_cast<const u32*>(b + o_fr);
   (void)R;
   return CFTFT_OK;
 }
@@ -253,9 +257,10 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       }
       if (R->leaf_limit) cl = std::min(cl, std::max(1u, R->leaf_limit));
       static const int env_wave = getenv("CFTFT_WAVE") ? atoi(getenv("CFTFT_WAVE")) : -1;
-      const int wave = R->wave >= 0 ? R->wave : (env_wave >= 0 ? env_wave : 0);
+      const int wave = R->wave >= 0 ? R->wave : (env_wave >= 0 ? env_wave : 1);
       if (wave && cw == 8) {
         rs.wave_engine = true;
+        rs.wave_unaligned = getenv("CFTFT_WAVE_ALIGNED") == nullptr;
         cl = std::min(cl, 3u);
         rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
       }
@@ -527,6 +532,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         // wave engine: one launch per range of independent tickets, in order;
         // coset ranges on the warp-level kernel, whole ranges on the leaf kernel
         A.no_deps = 1;
+        A.xpre = dp.wave_slots;
         fermat::WaveArgs W{};
         W.classes = dp.classes;
         W.ops = dp.ops;
@@ -585,9 +591,18 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         // carry-save lanes of the outputs (a batch: of every element it touched)
         // back to the canonical element format
         const u64 cnt = dp.host.final_count ? dp.host.final_count : dp.host.extent;
+        // (with the sub-lane rotations the outputs' last writers deferred)
         if (cnt) {
-          fermat::cs_fold_kernel<<<(unsigned)cnt, 256, 0, st>>>(base, stride, tops, dp.C, dp.cw,
-                                                               (u32)__builtin_ctz(dp.C), dp.logS, R->D, 0, 1);
+          const size_t fsm = dp.final_rot ? (size_t)R->D * 4 : 0;
+          static size_t fattr = 0;
+          if (fsm > 48 * 1024 && fsm > fattr) {
+            CUDA_TRY(cudaFuncSetAttribute(fermat::cs_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)fsm));
+            fattr = fsm;
+          }
+          fermat::cs_fold_kernel<<<(unsigned)cnt, 256, fsm, st>>>(base, stride, tops, dp.C, dp.cw,
+                                                                 (u32)__builtin_ctz(dp.C), dp.logS, R->D, 0, 1,
+                                                                 dp.final_rot);
           ++launches;
         }
       }
@@ -683,6 +698,7 @@ int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* 
 
 void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
   os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"lane_bits\":" << lane_bits << ",\"coset\":" << (p.coset ? 1 : 0)
+     << ",\"wave\":" << (p.waves.empty() ? 0 : 1)
      << ",\"L\":" << p.L << ",\"s\":" << p.s
      << ",\"z\":" << p.z << ",\"n\":" << p.n << ",\"f\":" << p.f << ",\"final_count\":"
      << p.final_count << ",\"counters\":[";
@@ -726,6 +742,15 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
   for (size_t i = 0; i < p.locbits.size(); ++i) os << (i ? "," : "") << p.locbits[i];
   os << "],\"shadow_finals\":[";
   for (size_t i = 0; i < p.shadow_finals.size(); ++i) os << (i ? "," : "") << p.shadow_finals[i];
+  os << "],\"wave_slots\":[";
+  for (size_t i = 0; i < p.wave_slots.size(); ++i) os << (i ? "," : "") << p.wave_slots[i];
+  os << "],\"final_rot\":[";  // {element, bits} pairs
+  bool first_fr = true;
+  for (size_t i = 0; i < p.final_rot.size(); ++i)
+    if (p.final_rot[i]) {
+      os << (first_fr ? "" : ",") << i << "," << p.final_rot[i];
+      first_fr = false;
+    }
   os << "]}";
 }
 

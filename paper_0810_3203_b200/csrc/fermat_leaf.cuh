@@ -62,6 +62,7 @@ struct Args {
   u32 logS;                // tops-array lane interleave
   unsigned long long* prof;  // optional per-phase cycle totals (CFTFT_PROFILE=1)
   u32 debug_skip;            // perf experiments only (CFTFT_DEBUG_SKIP): 1 = levels, 2 = post maths
+  const u32* xpre;           // wave engine: deferred pre-rotation bits of whole tickets (DevLeaf::c0 - 1)
 };
 
 // Phase timing (debug): thread 0 of each CTA accumulates clock64 deltas.
@@ -851,7 +852,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
     __syncthreads();
     const u64* const locm = s_loc[cur];
 
-    if (!G.coset && (cl.has_pre || lf.tpre)) {
+    const u32* const xp = (!G.coset && A.xpre && lf.c0) ? A.xpre + (lf.c0 - 1) : nullptr;
+    if (!G.coset && (cl.has_pre || lf.tpre || xp)) {
       // ---- pre-rotations (whole tickets), in place: NG slots per round --------------
       for (u32 b0 = 0; b0 < cl.nload; b0 += NG) {
         const u32 sl = b0 + g;
@@ -860,7 +862,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 512 / NT) leaf_kernel(Args
         int tp = 0;
         if (act) {
           const SymExp P = cached ? s_crot[sl] : A.rots[cl.pre_begin + sl];
-          const Rot R = make_rot<CW>(pre_exp(A, cl, lf, P, sl), A.N);
+          const u64 r = pre_exp(A, cl, lf, P, sl) + (xp ? xp[sl] : 0u);
+          const Rot R = make_rot<CW>(r & (A.M - 1), A.N);
           const u32 so = boff + sl * SB;
           const bool neg = rot_chunk<CW>(w, tp, so, so + W4, R, Cm, i);
           tp = exact_from<CW>(w, tp, neg);
@@ -1228,14 +1231,24 @@ __global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2
 // takes the top of lane p-1 (lane 0 takes minus the top of lane C-1 and the
 // element top word: 2^N == -1).  Only word 0 of a lane is touched unless a
 // carry ripples; lanes whose carry-in is zero are not touched at all.
+//
+// frot (wave engine): per element, a sub-lane rotation 2^o its last writer
+// deferred (Plan::final_rot), applied here after the fold: x = lo + h 2^N
+// times 2^o is (lo << o mod 2^N) - S with S = (lo >> (N - o)) + h 2^o, a
+// number of about o bits -- the shifted words in parallel, then S subtracted
+// serially (the borrow stops after a few words unless a run of zero words).
+// Dynamic shared memory: 4 D bytes when frot is set.
 __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const int* T, u32 CL, u32 CW,
-                                                      u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride) {
+                                                      u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride,
+                                                      const u32* frot) {
   __shared__ int s_pend[1024];
+  extern __shared__ u32 s_old[];  // D words (frot only)
   const u64 e = idx0 + (u64)blockIdx.x * istride;
   std::uint8_t* el = data + e * eb;
   const int* Te = T + e * CL;
   long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
   u32* w = reinterpret_cast<u32*>(el);
+  const u32 o = frot ? frot[e] : 0u;
   auto tix = [&](u32 p) { return ((p & ((1u << logS) - 1)) << (logLanes - logS)) | (p >> logS); };
   // pass 1: every lane takes its carry-in
   for (u32 p = threadIdx.x; p < CL; p += blockDim.x) {
@@ -1266,9 +1279,7 @@ __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb
   for (u32 p = threadIdx.x; p < CL; p += blockDim.x) any |= s_pend[p];
   if (!__syncthreads_or(any)) {
     if (threadIdx.x == 0) *hip = 0;  // lo is canonical: every lane in [0, 2^lane)
-    return;
-  }
-  if (threadIdx.x == 0) {
+  } else if (threadIdx.x == 0) {
     long long h = 0;
     for (u32 p = 0; p < CL; ++p) {
       long long c = s_pend[p];
@@ -1290,6 +1301,35 @@ __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb
     *hip = h;
     canon_element(el, D);
   }
+  if (!o) return;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < D; i += blockDim.x) s_old[i] = w[i];
+  __syncthreads();
+  const u32 ws = o >> 5, b = o & 31;
+  for (u32 i = threadIdx.x; i < D; i += blockDim.x) {
+    const u32 x0 = i >= ws ? s_old[i - ws] : 0u;
+    const u32 x1 = i >= ws + 1 ? s_old[i - ws - 1] : 0u;
+    w[i] = b ? (x0 << b) | (x1 >> (32 - b)) : x0;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const u32 N = 32 * D, nT = (o + 31) >> 5;
+  const long long h = *hip;
+  __int128 acc = 0;
+  for (u32 i = 0; i < D; ++i) {
+    acc += w[i];
+    if (i < nT) {  // word i of lo >> (N - o)
+      const u32 st = N - o + 32 * i, q = st >> 5, sh = st & 31;
+      const u32 lo0 = s_old[q], lo1 = q + 1 < D ? s_old[q + 1] : 0u;
+      acc -= sh ? (lo0 >> sh) | (lo1 << (32 - sh)) : lo0;
+    }
+    if (i == ws) acc -= (__int128)h << b;
+    w[i] = (u32)acc;
+    acc >>= 32;
+    if (i + 1 >= nT && i >= ws && acc == 0) break;
+  }
+  *hip = (long long)acc;
+  if (acc) canon_element(el, D);
 }
 
 }  // namespace fermat

@@ -181,9 +181,14 @@ struct Plan {
   // q << 12, q the rotation in coset positions (class order, see wop_begin)
   std::vector<u32> wave_ops;
   std::vector<u32> wave_op_begin;  // per class
-  // wave engine, coset tickets: per slot {pre lanes | in-buffer << 31,
-  // post lanes | out-buffer << 31}, at DevLeaf::c0 (reused as the offset)
+  // wave engine, coset tickets: per slot {pre bits | in-buffer << 31,
+  // post lanes | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
+  // whole tickets with deferred rotations on their inputs: per loaded slot
+  // the extra pre-rotation bits, at DevLeaf::c0 - 1 (c0 = 0: none)
   std::vector<u32> wave_slots;
+  // outputs whose last writer deferred a sub-lane rotation: bits per view
+  // element [0, extent), applied by the final fold (empty: none)
+  std::vector<u32> final_rot;
 };
 
 // Ring-dependent planning parameters.
@@ -207,6 +212,7 @@ struct RingShape {
   // wave engine: leaves of <= 8 coefficients, one launch per independent wave;
   // coset leaves run on the warp-level kernel (csrc/wave_coset.cuh)
   bool wave_engine = false;
+  bool wave_unaligned = true;  // coset leaves may take unaligned pre-rotations (warp kernel)
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -367,8 +373,18 @@ class Planner {
   }
 
   // Host-side precomputation for the warp-level kernel: packed micro-ops per
-  // coset class and per-slot lane rotations / buffers per coset ticket.
-  void wave_tables(Plan& p) {
+  // coset class and per-slot rotations / buffers per coset ticket.
+  //
+  // Deferred rotations: a coset leaf applies the whole-lane part q of a
+  // post-rotation by r = q*lane + o bits and leaves 2^o pending on the
+  // element; the element's next reader (emission order is topological, and
+  // every element is read by at most one later leaf) adds o to its
+  // pre-rotation -- any bits on the warp kernel, a per-slot table on the whole
+  // leaf kernel -- and outputs still pending at the end are rotated after the
+  // fold.  2^o commutes with everything in between: the element is only
+  // copied between buffers.  (A slot read but not written keeps its value,
+  // and so its pending rotation.)
+  void wave_tables(Plan& p, const std::vector<u64>& finals) {
     const u64 M = rs_.M, lb = rs_.lane_bits;
     p.wave_ops.clear();
     p.wave_op_begin.assign(classes_.size(), 0);
@@ -382,22 +398,35 @@ class Planner {
       }
     }
     p.wave_slots.clear();
+    p.final_rot.clear();
+    std::vector<u32> pend(extent_, 0);
     for (auto& lf : leaves_) {
       const LeafProgram& cl = classes_[lf.cls];
-      if (cl.kind != 1) continue;
+      const bool inv = cl.key.inverse != 0;
+      if (cl.kind != 1) {
+        bool any = false;
+        for (u32 k = 0; k < cl.nload; ++k) any |= pend[lf.base + (u64)k * lf.stride] != 0;
+        if (any) {
+          lf.c0 = (u32)p.wave_slots.size() + 1;
+          for (u32 k = 0; k < cl.nload; ++k) p.wave_slots.push_back(pend[lf.base + (u64)k * lf.stride]);
+        }
+        for (u32 k = 0; k < cl.nstore; ++k) pend[lf.base + (u64)k * lf.stride] = 0;
+        continue;
+      }
       const u32 off = (u32)p.wave_slots.size();
       const u32 span = std::max(cl.nload, cl.nstore);
       for (u32 k = 0; k < span; ++k) {
-        const bool inv = cl.key.inverse != 0;
+        const u64 e = lf.base + (u64)k * lf.stride;
         u32 pre = 0, post = 0;
         if (k < cl.nload) {
-          const u64 r = (cl.pre[k].a * lf.s + cl.pre[k].b + ((inv && k < cl.key.n) ? lf.tpre : 0)) & (M - 1);
-          pre = (u32)(r / lb);
+          const u64 r = cl.pre[k].a * lf.s + cl.pre[k].b + ((inv && k < cl.key.n) ? lf.tpre : 0) + pend[e];
+          pre = (u32)(r & (M - 1));  // bits: the warp kernel takes unaligned pre-rotations
         }
         if (k < cl.nstore) {
           const bool tp = inv ? (cl.key.f && k == cl.key.n) : true;
           const u64 r = (cl.post[k].a * lf.s + cl.post[k].b + (tp ? lf.tpost : 0)) & (M - 1);
           post = (u32)(r / lb);
+          pend[e] = (u32)(r % lb);
         }
         if (lf.locoff != kNoDep) {
           if ((p.locbits[lf.locoff + 2 * (k / 64)] >> (k % 64)) & 1) pre |= 1u << 31;
@@ -408,6 +437,11 @@ class Planner {
       }
       lf.c0 = off;
     }
+    for (u64 e : finals)
+      if (pend[e]) {
+        if (p.final_rot.empty()) p.final_rot.assign(extent_, 0);
+        p.final_rot[e] = pend[e];
+      }
   }
 
   // ticket order: (top phase, batch, wave, top child, emission order), with
@@ -418,7 +452,7 @@ class Planner {
   // independent, and each keeps its own wave order.
   void finish(Plan& p, const std::vector<u64>& finals) {
     if (coset_used_) assign_buffers(p, finals);
-    if (rs_.wave_engine) wave_tables(p);
+    if (rs_.wave_engine) wave_tables(p, finals);
     std::vector<u32> idx(leaves_.size());
     for (u32 i = 0; i < idx.size(); ++i) idx[i] = i;
     u32 W = 1;
@@ -540,7 +574,7 @@ class Planner {
     unsigned l1, l2;
     if (bnd.active) {
       const bool unal = (bnd.sigma % rs_.lane_bits) != 0;
-      if (unal && ((!inv && bnd.out) || (inv && bnd.in))) {
+      if (unal && !(rs_.wave_engine && rs_.wave_unaligned) && ((!inv && bnd.out) || (inv && bnd.in))) {
         // the boundary rows (TFT: last level, ITFT: first level) carry
         // unaligned rotations: make them whole leaves
         l2 = std::min(rs_.max_leaf_ell, ell - 1);
@@ -716,11 +750,13 @@ class Planner {
     const u64 M = rs_.M, inner = M >> ell, lb = rs_.lane_bits;
     for (const auto& op : prog.ops)
       if (op.type != OP_COPY && (op.r % inner) != 0) return false;
-    for (u32 k = 0; k < prog.nload; ++k) {
+    for (u32 k = 0; k < prog.nload && !(rs_.wave_engine && rs_.wave_unaligned); ++k) {  // the warp kernel takes any pre-rotation
       u64 r = prog.pre[k].a * lf.s + prog.pre[k].b + ((inv && k < prog.key.n) ? lf.tpre : 0);
       if ((r & (M - 1)) % lb) return false;
     }
-    for (u32 k = 0; k < prog.nstore; ++k) {
+    // the warp kernel applies the lane part of a post-rotation and defers the
+    // sub-lane rest to the next reader of the element (see wave_tables)
+    for (u32 k = 0; k < prog.nstore && !(rs_.wave_engine && rs_.wave_unaligned); ++k) {
       const bool tp = inv ? (prog.key.f && k == prog.key.n) : true;
       u64 r = prog.post[k].a * lf.s + prog.post[k].b + (tp ? lf.tpost : 0);
       if ((r & (M - 1)) % lb) return false;

@@ -53,7 +53,9 @@ __host__ __device__ constexpr u32 wave_row_words() {
 }
 template <int CW>
 __host__ __device__ constexpr u32 wave_tile_words() {
-  return 8u * 32u * wave_row_words<CW>() + 16u;  // + the slots' top words (8 x u64)
+  // rows, the slots' top words (8 x u64), and the extra rows of unaligned
+  // rotations (8 slots x 4 positions)
+  return 8u * 32u * wave_row_words<CW>() + 16u + 8u * 4u * wave_row_words<CW>();
 }
 
 template <int CW>
@@ -67,6 +69,8 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
   constexpr u32 RR = wave_row_words<CW>();
   auto row = [&](u32 slot, u32 l) -> u32* { return tile + (slot * 32u + l) * RR; };
   long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * RR);  // per slot top word
+  u32* const xtile = tile + 8u * 32u * RR + 16u;  // extra rows: [slot][position]
+  auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * 4u + p) * RR; };
   auto ld = [&](Ch<CW>& c, u32 slot, u32 l) -> int {
     const u32* r = row(slot, l);
 #pragma unroll
@@ -105,44 +109,110 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
 
       // ---- load: gather through the pre-rotation (all slots in flight at
       //      once), then fold the top word and negate wrapped lanes
-      u32 wrapped = 0, lane0 = 0;  // per-slot bit masks of this lane
-      const u32* const sl = A.wslots + lf.c0;  // {pre, post} per slot
+      // A pre-rotation by r = q*lane + o bits reads source lane L0 - q ("A");
+      // when o != 0 the output lane also takes the top o bits of lane
+      // L0 - q - 1 ("B") -- the A of the previous lane of this warp, or, for a
+      // warp's first coset, an extra row this lane loads itself.
+      u32 wrapA = 0, wrapB = 0, zeroA = 0, zeroB = 0, unal = 0;  // per-slot bit masks
+      const u32* const sl = A.wslots + lf.c0;  // {pre bits | in-buffer, post lanes | out-buffer} per slot
+      const bool first = (lane & cmask) == 0;
       for (u32 k = 0; k < cl.nload; ++k) {
         if (!act) break;
-        const u32 pre = sl[2 * k];
-        const u32 src = (L0 + 2 * CL - (pre & 0x7FFFFFFFu)) & (2 * CL - 1);
-        const u32 ln = src & (CL - 1);
+        const u32 pre = sl[2 * k], r = pre & 0x7FFFFFFFu;
+        const u32 q = r / CB, o = r % CB;
+        const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
+        const u32 lnA = srcA & (CL - 1);
         const u32 ib = pre >> 31;
         const u64 e = lf.base + (u64)k * lf.stride;
         const std::uint8_t* el = (ib ? A.data2 : A.data) + e * A.elem_bytes;
+        const int* tr = A.T ? A.T + (ib ? A.tloc : 0) + e * CL : nullptr;
         const u32 so = tile_s + (k * 32u + lane) * RR * 4u;
 #pragma unroll
-        for (int q = 0; q < CW / 4; ++q) cp_async16(so + 16u * q, el + (u64)ln * (CB / 8) + 16u * q);
-        if (A.T) cp_async4(so + 4u * CW, A.T + (ib ? A.tloc : 0) + e * CL + ln);
-        if (ln == 0) {
-          cp_async8(tile_s + (8u * 32u * RR) * 4u + 8u * k, el + 4ull * A.D);
-          lane0 |= 1u << k;
+        for (int x = 0; x < CW / 4; ++x) cp_async16(so + 16u * x, el + (u64)lnA * (CB / 8) + 16u * x);
+        if (tr) cp_async4(so + 4u * CW, tr + lnA);
+        if (lane == 0) cp_async8(tile_s + (8u * 32u * RR) * 4u + 8u * k, el + 4ull * A.D);
+        if (lnA == 0) zeroA |= 1u << k;
+        if (srcA >= CL) wrapA |= 1u << k;
+        if (o) {
+          unal |= 1u << k;
+          const u32 srcB = (srcA + 2 * CL - 1) & (2 * CL - 1);
+          const u32 lnB = srcB & (CL - 1);
+          if (lnB == 0) zeroB |= 1u << k;
+          if (srcB >= CL) wrapB |= 1u << k;
+          if (first) {
+            const u32 xo = (u32)__cvta_generic_to_shared(xrow(k, pos));
+#pragma unroll
+            for (int x = 0; x < CW / 4; ++x) cp_async16(xo + 16u * x, el + (u64)lnB * (CB / 8) + 16u * x);
+            if (tr) cp_async4(xo + 4u * CW, tr + lnB);
+          }
         }
-        if (src >= CL) wrapped |= 1u << k;
       }
       cp_async_wait_all();
       __syncwarp();
-      for (u32 k = 0; k < cl.nload; ++k) {
-        if (!act) break;
-        const bool has_hi = (lane0 >> k) & 1u, neg = (wrapped >> k) & 1u;
-        int top = A.T ? (int)row(k, lane)[CW] : 0;
-        if (!A.T) row(k, lane)[CW] = 0;
-        if (!has_hi && !neg) continue;
+      // rows -> true carry-save values of their source lanes: the coefficient's
+      // top word folded into (every copy of) source lane 0, wrapped lanes negated
+      auto settle = [&](u32* rw, u32 k, bool zero, bool neg) {
+        int top = A.T ? (int)rw[CW] : 0;
+        if (!A.T) rw[CW] = 0;
+        if (!zero && !neg) return;
         Ch<CW> w;
-        ld(w, k, lane);
-        if (has_hi) {
+#pragma unroll
+        for (int x = 0; x < CW; ++x) w.w[x] = rw[x];
+        if (zero) {
           const int hi = (int)hiw[k];
           if (hi) top += ch_add_small<CW>(w, -hi);
         }
         if (neg) top = exact_from<CW>(w, top, true);
-        st(k, lane, w, top);
+#pragma unroll
+        for (int x = 0; x < CW; ++x) rw[x] = w.w[x];
+        rw[CW] = (u32)top;
+      };
+      for (u32 k = 0; k < cl.nload; ++k) {
+        if (!act) break;
+        settle(row(k, lane), k, (zeroA >> k) & 1u, (wrapA >> k) & 1u);
+        if (((unal >> k) & 1u) && first) settle(xrow(k, pos), k, (zeroB >> k) & 1u, (wrapB >> k) & 1u);
       }
       __syncwarp();
+      // unaligned slots: lane L0 = bits [Λ - o, 2Λ - o) of (B ++ A) plus B's top at bit o
+      for (u32 k = 0; k < cl.nload; ++k) {
+        const u32 o = (sl[2 * k] & 0x7FFFFFFFu) % CB;  // uniform across the warp
+        if (o == 0) continue;
+        Ch<CW> out;
+        int otop = 0;
+        if (act) {
+          Ch<CW> a, b;
+          ld(a, k, lane);
+          const u32* br = first ? xrow(k, pos) : row(k, lane - 1);
+#pragma unroll
+          for (int x = 0; x < CW; ++x) b.w[x] = br[x];
+          const int tb = (int)br[CW];
+          u32 X[CW + 1];
+          pick_window_rt<CW>(X, b, a, o >> 5);
+#pragma unroll
+          for (int x = 0; x < CW; ++x) out.w[x] = __funnelshift_l(X[x], X[x + 1], o & 31);
+          Ch<CW> P;
+          const int ptop = small_shifted<CW>(P, tb, o);
+          otop = ch_add(out, out, P) + ptop;
+          if (L0 == 0) {
+            // Lane 0's B is lane C-1's A seen through 2^N == -1: the split of
+            // -v must be -(split of v), and floor(-v 2^o / 2^Λ) is one short
+            // of that whenever v's low Λ-o bits (the part lane C-1 keeps) are
+            // nonzero (negation preserves that).
+            const u32 nb = CB - o;
+            u32 nz = 0;
+#pragma unroll
+            for (int x = 0; x < CW; ++x) {
+              const u32 lo = 32u * x;
+              const u32 m = lo + 32u <= nb ? ~0u : (lo < nb ? (1u << (nb - lo)) - 1u : 0u);
+              nz |= b.w[x] & m;
+            }
+            if (nz) otop += ch_add_small<CW>(out, 1);
+          }
+        }
+        __syncwarp();
+        if (act) st(k, lane, out, otop);
+        __syncwarp();
+      }
       // ---- the leaf program: every lane runs every micro-op on its chunk
       for (u32 o = 0; o < cl.nops; ++o) {
         const u32 wop = A.wops[cl.wop_begin + o];
@@ -201,7 +271,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
         __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
-        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sl[2 * k] & 0x7FFFFFFFu)) & (CL - 1)) == 0 : d == 0;
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sl[2 * k] & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
         if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
       }
       __syncwarp();

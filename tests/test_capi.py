@@ -127,18 +127,23 @@ def run_plan_fermat(plan, N, vals):
 
     meta = plan["counters"]
     counters = [0] * len(meta)
+    wplan, ws = plan.get("wave", 0), plan.get("wave_slots", [])
     for (cls, base, stride, s, dep, target, comp, wave, tpre, tpost, c0, locoff) in plan["leaves"]:
         if dep >= 0:
             assert counters[dep] >= target, "ticket order is not topological"
         c = plan["classes"][cls]
         inv, cn, cf_ = c["inverse"], c["n"], c["f"]
         coset = c["kind"] == 1
-        run = not coset or c0 == 0
+        run = not coset or c0 == 0 or plan.get("wave", 0)  # wave plans: one ticket per leaf (c0 = slot table)
         slot = [None] * (1 << c["ell"])
         for i in range(c["nload"] if run else 0):
             a, b = c["pre"][i]
             e = (a * s + b + (tpre if inv and i < cn else 0)) % M
-            assert not coset or e % lane == 0
+            if wplan and coset:  # the ticket's table: any bits, deferred rotations included
+                e = ws[c0 + 2 * i] & 0x7FFFFFFF
+            elif wplan and c0 > 0:  # a whole ticket reading elements with deferred rotations
+                e = (e + ws[c0 - 1 + i]) % M
+            assert not coset or e % lane == 0 or wplan
             slot[i] = (x[(buf(locoff, i, False), base + i * stride)] * pow(2, e, P)) % P
         for (t, a, b, r) in (c["ops"] if run else []):
             assert not coset or t == 4 or r % (M >> c["ell"]) == 0
@@ -160,6 +165,8 @@ def run_plan_fermat(plan, N, vals):
             ea, eb = c["post"][i]
             tp = (tpost if cf_ and i == cn else 0) if inv else tpost
             e = (ea * s + eb + tp) % M
+            if wplan and coset:  # whole lanes; the sub-lane rest goes to the next reader
+                e = (ws[c0 + 2 * i + 1] & 0x7FFFFFFF) * lane
             assert not coset or e % lane == 0
             ob = buf(locoff, i, True)
             if coset and i < c["nload"]:
@@ -173,7 +180,11 @@ def run_plan_fermat(plan, N, vals):
                 break
             k = nxt
     shadow = set(plan.get("shadow_finals", []))
-    return {e: x[(1 if e in shadow else 0, e)] for (b, e) in x if b == 0 or e in shadow}
+    out = {e: x[(1 if e in shadow else 0, e)] for (b, e) in x if b == 0 or e in shadow}
+    fr = plan.get("final_rot", [])
+    for e, o in zip(fr[::2], fr[1::2]):  # rotations deferred past the last writer
+        out[e] = (out[e] * pow(2, o, P)) % P
+    return out
 
 
 def check_plan(ctx, N, rnd, trials):
