@@ -548,7 +548,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         W.lanes = dp.C;
         W.D = R->D;
         W.M = R->M;
-        const size_t wsmem = (size_t)fermat::kWaveWarps * fermat::wave_tile_words<8>() * 4;
+        static const int wwarps = std::min(fermat::kWaveWarps, std::max(1, getenv("CFTFT_WAVE_WARPS")
+                                                                               ? atoi(getenv("CFTFT_WAVE_WARPS"))
+                                                                               : fermat::kWaveWarps));
+        const size_t wsmem = (size_t)wwarps * fermat::wave_tile_words<8>() * 4;
         static bool wave_attr = false;
         if (!wave_attr) {
           CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -558,14 +561,14 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         int dev = 0, sms = 0, per = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8>,
-                                                               32 * fermat::kWaveWarps, wsmem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8>, 32 * wwarps, wsmem));
         for (const auto& wr : dp.host.waves) {
           if (wr[2] == 1) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];
-            const unsigned g = (unsigned)std::min<u64>(wr[1], (u64)sms * std::max(per, 1));
-            fermat::coset_wave_kernel<8><<<g, 32 * fermat::kWaveWarps, wsmem, st>>>(W);
+            W.gpl = (u32)std::max<u64>(1, wr[3]);
+            const unsigned g = (unsigned)std::min<u64>((wr[1] * W.gpl + wwarps - 1) / wwarps, (u64)sms * std::max(per, 1));
+            fermat::coset_wave_kernel<8><<<g, 32 * wwarps, wsmem, st>>>(W);
           } else {
             CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(u32), st));  // ticket counter of this range
             A.leaves = dp.leaves + wr[0];

@@ -175,8 +175,9 @@ struct Plan {
   std::vector<u64> locbits;        // per-slot buffer bits (see DevLeaf::locoff)
   std::vector<u64> shadow_finals;  // outputs the schedule leaves in the shadow buffer
   // wave engine: ticket ranges of mutually independent leaves, launched in
-  // order; {first ticket, count, kind (0 whole, 1 coset)}
-  std::vector<std::array<u64, 3>> waves;
+  // order; {first ticket, count, kind (0 whole, 1 coset), coset ranges: the
+  // most warp groups of lane cosets a ticket of the range has}
+  std::vector<std::array<u64, 4>> waves;
   // wave engine, coset classes: micro-ops packed as type | a << 4 | b << 8 |
   // q << 12, q the rotation in coset positions (class order, see wop_begin)
   std::vector<u32> wave_ops;
@@ -474,8 +475,13 @@ class Planner {
         const u64 kind = classes_[leaves_[idx[t]].cls].kind;
         if (t == 0 || std::get<0>(keys_[idx[t - 1]]) != std::get<0>(k) ||
             std::get<2>(keys_[idx[t - 1]]) != std::get<2>(k) || p.waves.back()[2] != kind)
-          p.waves.push_back({(u64)t, 0, kind});
+          p.waves.push_back({(u64)t, 0, kind, 0});
         p.waves.back()[1] += 1;
+        if (kind == 1) {  // a warp takes 2^(6 - ell) cosets of all positions (wave_coset.cuh)
+          const LeafProgram& c = classes_[leaves_[idx[t]].cls];
+          const u64 groups = std::max<u64>(1, (u64)c.step >> (6 - c.key.ell));
+          p.waves.back()[3] = std::max(p.waves.back()[3], groups);
+        }
       }
     }
     p.leaves.reserve(idx.size());

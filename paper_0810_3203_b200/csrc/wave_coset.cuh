@@ -41,59 +41,95 @@ struct WaveArgs {
   u32 lanes;            // lanes per coefficient (C)
   u32 D;                // u32 words per coefficient
   u64 M;
+  u32 gpl;              // work items per ticket: its most warp groups (Plan::waves)
 };
 
-constexpr int kWaveWarps = 8;
+constexpr int kWaveWarps = 4;  // warps per CTA, at most (the launch may use fewer)
 
-// per warp: 8 slots x 32 lanes x a 16-byte aligned row of CW words + top
-// (+ pad); rows 48 bytes apart keep 16-byte lane accesses conflict free
+// per warp: data rows [slot][lane] of CW words, their 16-byte halves swapped
+// on lanes with bit 2 set (so the 8 lanes of a 16-byte access phase hit 32
+// distinct banks); tops [slot][lane]; the slots' top words; extra rows of
+// unaligned rotations [slot][position] (CW words + top, padded to 16 bytes)
 template <int CW>
-__host__ __device__ constexpr u32 wave_row_words() {
+__host__ __device__ constexpr u32 wave_xrow_words() {
   return (CW + 1 + 3) & ~3u;
 }
 template <int CW>
 __host__ __device__ constexpr u32 wave_tile_words() {
-  // rows, the slots' top words (8 x u64), and the extra rows of unaligned
-  // rotations (8 slots x 4 positions)
-  return 8u * 32u * wave_row_words<CW>() + 16u + 8u * 4u * wave_row_words<CW>();
+  return 8u * 32u * CW + 8u * 32u + 16u + 8u * 4u * wave_xrow_words<CW>();
 }
 
 template <int CW>
-__global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A) {
+__global__ void __launch_bounds__(32 * kWaveWarps, 5) coset_wave_kernel(WaveArgs A) {
+  static_assert(CW == 8, "the wave engine runs 256-bit lanes");
   extern __shared__ __align__(16) u32 wsm[];
   constexpr u32 CB = 32 * CW;
-  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr u32 XR = wave_xrow_words<CW>();
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   u32* const tile = wsm + warp * wave_tile_words<CW>();
   const u32 CL = A.lanes;
-  const u64 Mm = A.M - 1;
-  constexpr u32 RR = wave_row_words<CW>();
-  auto row = [&](u32 slot, u32 l) -> u32* { return tile + (slot * 32u + l) * RR; };
-  long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * RR);  // per slot top word
-  u32* const xtile = tile + 8u * 32u * RR + 16u;  // extra rows: [slot][position]
-  auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * 4u + p) * RR; };
-  auto ld = [&](Ch<CW>& c, u32 slot, u32 l) -> int {
-    const u32* r = row(slot, l);
+  auto rowp = [&](u32 slot, u32 l) -> u32* { return tile + (slot * 32u + l) * CW; };
+  int* const tops = reinterpret_cast<int*>(tile + 8u * 32u * CW);
+  long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * CW + 256u);  // per slot top word
+  u32* const xtile = tile + 8u * 32u * CW + 256u + 16u;  // extra rows: [slot][position]
+  auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * 4u + p) * XR; };
+  auto swz = [](u32 l) -> u32 { return (l >> 2) & 1u; };
+  auto ldw = [&](Ch<CW>& c, const u32* r, u32 sw) {
 #pragma unroll
-    for (int q = 0; q < CW / 4; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(r + 4 * q);
+    for (u32 q = 0; q < CW / 4; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(r + 4 * (q ^ sw));
       c.w[4 * q] = v.x;
       c.w[4 * q + 1] = v.y;
       c.w[4 * q + 2] = v.z;
       c.w[4 * q + 3] = v.w;
     }
-    return (int)r[CW];
+  };
+  auto stw = [&](u32* r, u32 sw, const Ch<CW>& c) {
+#pragma unroll
+    for (u32 q = 0; q < CW / 4; ++q)
+      *reinterpret_cast<uint4*>(r + 4 * (q ^ sw)) =
+          make_uint4(c.w[4 * q], c.w[4 * q + 1], c.w[4 * q + 2], c.w[4 * q + 3]);
+  };
+  auto ld = [&](Ch<CW>& c, u32 slot, u32 l) -> int {
+    ldw(c, rowp(slot, l), swz(l));
+    return tops[slot * 32u + l];
   };
   auto st = [&](u32 slot, u32 l, const Ch<CW>& c, int top) {
-    u32* r = row(slot, l);
-#pragma unroll
-    for (int q = 0; q < CW / 4; ++q)
-      *reinterpret_cast<uint4*>(r + 4 * q) = make_uint4(c.w[4 * q], c.w[4 * q + 1], c.w[4 * q + 2], c.w[4 * q + 3]);
-    r[CW] = (u32)top;
+    stw(rowp(slot, l), swz(l), c);
+    tops[slot * 32u + l] = top;
   };
   const u32 tile_s = (u32)__cvta_generic_to_shared(tile);
 
-  for (u32 t = blockIdx.x; t < A.nleaves; t += gridDim.x) {
-    const DevLeaf lf = A.leaves[t];
+  // descriptors one ticket ahead: the next ticket's load overlaps this one
+  struct Desc {
+    u64 base, stride;
+    u32 cls, c0;
+  };
+  auto fetch = [&](u32 t) {
+    Desc d{0, 0, 0, 0};
+    if (t < A.nleaves) {
+      const DevLeaf* p = A.leaves + t;
+      d.base = p->base;
+      d.stride = p->stride;
+      d.cls = p->cls;
+      d.c0 = p->c0;
+    }
+    return d;
+  };
+  // work items (ticket, warp group), gpl per ticket: a contiguous run per
+  // CTA, dealt round-robin to its warps -- the CTA's warps stream adjacent
+  // cosets of the same coefficients at once (DRAM locality), consecutive
+  // items of a warp mostly share a ticket (descriptor and tables)
+  const u64 gpl = A.gpl, items = (u64)A.nleaves * gpl;
+  const u64 c1i = (blockIdx.x + 1ull) * items / gridDim.x;
+  u64 i = blockIdx.x * items / gridDim.x + warp;
+  Desc lf_next = fetch(i < c1i ? (u32)(i / gpl) : A.nleaves);
+  while (i < c1i) {
+    const u32 t = (u32)(i / gpl);
+    const Desc lf = lf_next;
+    const u64 tend = c1i < (t + 1ull) * gpl ? c1i : (t + 1ull) * gpl;
+    const u64 inext = i + (tend - i + nwarps - 1) / nwarps * nwarps;  // this warp's first item past t
+    lf_next = fetch(inext < c1i ? (u32)(inext / gpl) : A.nleaves);
     const DevClass cl = A.classes[lf.cls];
     const u32 ell = 31 - __clz(cl.L);
     const u32 cp = 1u << (ell - 1);   // positions per coset
@@ -101,7 +137,15 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
     const u32 cmask = (1u << cb) - 1;
     const u32 step = cl.step;
     const u32 groups = max(1u, step >> cb);
-    for (u32 g = warp; g < groups; g += kWaveWarps) {
+    // the ticket's slot table and the class's first 32 packed ops, one word
+    // per lane, broadcast by shuffles (no dependent global loads in the loops)
+    const u32 span = max(cl.nload, cl.nstore);
+    const u32 slv = lane < 2 * span ? A.wslots[lf.c0 + lane] : 0u;
+    const u32 opv0 = lane < cl.nops ? A.wops[cl.wop_begin + lane] : 0u;
+    auto SL = [&](u32 i) { return __shfl_sync(0xffffffffu, slv, (int)i); };
+    for (; i < tend; i += nwarps) {
+      const u32 g = (u32)(i - (u64)t * gpl);
+      if (g >= groups) continue;
       const u32 c = (g << cb) + (lane & cmask);
       const u32 pos = lane >> cb;
       const bool act = c < step && pos < cp;
@@ -114,11 +158,11 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
       // L0 - q - 1 ("B") -- the A of the previous lane of this warp, or, for a
       // warp's first coset, an extra row this lane loads itself.
       u32 wrapA = 0, wrapB = 0, zeroA = 0, zeroB = 0, unal = 0;  // per-slot bit masks
-      const u32* const sl = A.wslots + lf.c0;  // {pre bits | in-buffer, post lanes | out-buffer} per slot
+      // slot table: {pre bits | in-buffer << 31, post lanes | out-buffer << 31}
       const bool first = (lane & cmask) == 0;
       for (u32 k = 0; k < cl.nload; ++k) {
-        if (!act) break;
-        const u32 pre = sl[2 * k], r = pre & 0x7FFFFFFFu;
+        const u32 pre = SL(2 * k), r = pre & 0x7FFFFFFFu;
+        if (!act) continue;
         const u32 q = r / CB, o = r % CB;
         const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
         const u32 lnA = srcA & (CL - 1);
@@ -126,11 +170,11 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
         const u64 e = lf.base + (u64)k * lf.stride;
         const std::uint8_t* el = (ib ? A.data2 : A.data) + e * A.elem_bytes;
         const int* tr = A.T ? A.T + (ib ? A.tloc : 0) + e * CL : nullptr;
-        const u32 so = tile_s + (k * 32u + lane) * RR * 4u;
+        const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
-        for (int x = 0; x < CW / 4; ++x) cp_async16(so + 16u * x, el + (u64)lnA * (CB / 8) + 16u * x);
-        if (tr) cp_async4(so + 4u * CW, tr + lnA);
-        if (lane == 0) cp_async8(tile_s + (8u * 32u * RR) * 4u + 8u * k, el + 4ull * A.D);
+        for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
+        if (tr) cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + lnA);
+        if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
         if (o) {
@@ -151,41 +195,44 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
       __syncwarp();
       // rows -> true carry-save values of their source lanes: the coefficient's
       // top word folded into (every copy of) source lane 0, wrapped lanes negated
-      auto settle = [&](u32* rw, u32 k, bool zero, bool neg) {
-        int top = A.T ? (int)rw[CW] : 0;
-        if (!A.T) rw[CW] = 0;
+      auto settle = [&](u32* rw, u32 sw, int* tp, u32 k, bool zero, bool neg) {
+        int top = A.T ? *tp : 0;
+        if (!A.T) *tp = 0;
         if (!zero && !neg) return;
         Ch<CW> w;
-#pragma unroll
-        for (int x = 0; x < CW; ++x) w.w[x] = rw[x];
+        ldw(w, rw, sw);
         if (zero) {
           const int hi = (int)hiw[k];
           if (hi) top += ch_add_small<CW>(w, -hi);
         }
         if (neg) top = exact_from<CW>(w, top, true);
-#pragma unroll
-        for (int x = 0; x < CW; ++x) rw[x] = w.w[x];
-        rw[CW] = (u32)top;
+        stw(rw, sw, w);
+        *tp = top;
       };
       for (u32 k = 0; k < cl.nload; ++k) {
         if (!act) break;
-        settle(row(k, lane), k, (zeroA >> k) & 1u, (wrapA >> k) & 1u);
-        if (((unal >> k) & 1u) && first) settle(xrow(k, pos), k, (zeroB >> k) & 1u, (wrapB >> k) & 1u);
+        settle(rowp(k, lane), swz(lane), tops + k * 32u + lane, k, (zeroA >> k) & 1u, (wrapA >> k) & 1u);
+        if (((unal >> k) & 1u) && first)
+          settle(xrow(k, pos), 0u, reinterpret_cast<int*>(xrow(k, pos) + CW), k, (zeroB >> k) & 1u,
+                 (wrapB >> k) & 1u);
       }
       __syncwarp();
       // unaligned slots: lane L0 = bits [Λ - o, 2Λ - o) of (B ++ A) plus B's top at bit o
       for (u32 k = 0; k < cl.nload; ++k) {
-        const u32 o = (sl[2 * k] & 0x7FFFFFFFu) % CB;  // uniform across the warp
+        const u32 o = (SL(2 * k) & 0x7FFFFFFFu) % CB;  // uniform across the warp
         if (o == 0) continue;
         Ch<CW> out;
         int otop = 0;
         if (act) {
           Ch<CW> a, b;
           ld(a, k, lane);
-          const u32* br = first ? xrow(k, pos) : row(k, lane - 1);
-#pragma unroll
-          for (int x = 0; x < CW; ++x) b.w[x] = br[x];
-          const int tb = (int)br[CW];
+          int tb;
+          if (first) {
+            ldw(b, xrow(k, pos), 0u);
+            tb = (int)xrow(k, pos)[CW];
+          } else {
+            tb = ld(b, k, lane - 1);
+          }
           u32 X[CW + 1];
           pick_window_rt<CW>(X, b, a, o >> 5);
 #pragma unroll
@@ -214,8 +261,10 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
         __syncwarp();
       }
       // ---- the leaf program: every lane runs every micro-op on its chunk
+      u32 opv = opv0;
       for (u32 o = 0; o < cl.nops; ++o) {
-        const u32 wop = A.wops[cl.wop_begin + o];
+        if (o && (o & 31) == 0) opv = o + lane < cl.nops ? A.wops[cl.wop_begin + o + lane] : 0u;
+        const u32 wop = __shfl_sync(0xffffffffu, opv, (int)(o & 31));
         struct {
           u32 type, a, b, q;
         } op{wop & 15u, (wop >> 4) & 15u, (wop >> 8) & 15u, wop >> 12};
@@ -254,8 +303,8 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
 
       // ---- store: scatter through the post-rotation, carry-save out
       for (u32 k = 0; k < cl.nstore; ++k) {
-        if (!act) break;
-        const u32 post = sl[2 * k + 1];
+        const u32 post = SL(2 * k + 1), prek = SL(2 * k);
+        if (!act) continue;
         const u32 dst = (L0 + (post & 0x7FFFFFFFu)) & (2 * CL - 1);
         const u32 d = dst & (CL - 1);
         const u32 ob = post >> 31;
@@ -271,7 +320,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps) coset_wave_kernel(WaveArgs A)
         __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
-        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sl[2 * k] & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (prek & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
         if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
       }
       __syncwarp();
