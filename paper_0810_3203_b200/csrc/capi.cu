@@ -153,6 +153,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.spec_n = c.key.inverse ? (u32)c.key.n : 0;
     d.fslot = (c.key.inverse && c.key.f) ? (u32)c.key.n : 0xFFFFFFFFu;
     d.wop_begin = cls.size() < p.wave_op_begin.size() ? p.wave_op_begin[cls.size()] : 0;
+    d.wnet = cls.size() < p.wave_net.size() ? p.wave_net[cls.size()] : 0;
     cls.push_back(d);
   }
   if (rots.empty()) rots.push_back(SymExp{});

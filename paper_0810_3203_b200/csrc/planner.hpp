@@ -100,6 +100,8 @@ struct DevClass {
   u32 spec_n;      // TFT program: tpost goes to every post slot
   u32 fslot;
   u32 wop_begin;   // wave engine, coset classes: first packed op in Plan::wave_ops
+  u32 wnet;        // wave engine: 0 generic ops, 1 / 2 the full 8-point network with
+                   // butterfly spans 4,2,1 / 1,2,4 (ADDSUB only; run in registers)
 };
 
 constexpr u32 kNoDep = 0xFFFFFFFFu;
@@ -182,6 +184,7 @@ struct Plan {
   // q << 12, q the rotation in coset positions (class order, see wop_begin)
   std::vector<u32> wave_ops;
   std::vector<u32> wave_op_begin;  // per class
+  std::vector<u32> wave_net;       // per class, DevClass::wnet
   // wave engine, coset tickets: per slot {pre bits | in-buffer << 31,
   // post lanes | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
   // whole tickets with deferred rotations on their inputs: per loaded slot
@@ -389,10 +392,12 @@ class Planner {
     const u64 M = rs_.M, lb = rs_.lane_bits;
     p.wave_ops.clear();
     p.wave_op_begin.assign(classes_.size(), 0);
+    p.wave_net.assign(classes_.size(), 0);
     for (size_t c = 0; c < classes_.size(); ++c) {
       const LeafProgram& cl = classes_[c];
       p.wave_op_begin[c] = (u32)p.wave_ops.size();
       if (cl.kind != 1) continue;
+      p.wave_net[c] = full_network(cl);
       for (const auto& op : cl.ops) {
         const u64 q = op.type == OP_COPY ? 0 : (op.r / lb) / cl.step;
         p.wave_ops.push_back((u32)op.type | ((u32)op.a << 4) | ((u32)op.b << 8) | ((u32)q << 12));
@@ -443,6 +448,24 @@ class Planner {
         if (p.final_rot.empty()) p.final_rot.assign(extent_, 0);
         p.final_rot[e] = pend[e];
       }
+  }
+
+  // 1 / 2: the class is the full 8-point network with butterfly spans 4,2,1
+  // (the TFT's) / 1,2,4 (the ITFT's), every op an ADDSUB in level order --
+  // the warp kernel then runs it in registers; 0: anything else
+  static u32 full_network(const LeafProgram& cl) {
+    if (cl.key.ell != 3 || cl.nload != 8 || cl.nstore != 8 || cl.ops.size() != 12) return 0;
+    for (u32 net = 1; net <= 2; ++net) {
+      bool ok = true;
+      for (u32 o = 0; o < 12 && ok; ++o) {
+        const u32 lvl = o >> 2, j = o & 3, h = net == 1 ? (4u >> lvl) : (1u << lvl);
+        const u32 a = (j / h) * 2 * h + (j % h);
+        const DevOp& op = cl.ops[o];
+        ok = op.type == OP_ADDSUB && op.a == a && op.b == a + h;
+      }
+      if (ok) return net;
+    }
+    return 0;
   }
 
   // ticket order: (top phase, batch, wave, top child, emission order), with

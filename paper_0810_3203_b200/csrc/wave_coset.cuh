@@ -60,7 +60,7 @@ __host__ __device__ constexpr u32 wave_tile_words() {
 }
 
 template <int CW>
-__global__ void __launch_bounds__(32 * kWaveWarps, 5) coset_wave_kernel(WaveArgs A) {
+__global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs A) {
   static_assert(CW == 8, "the wave engine runs 256-bit lanes");
   extern __shared__ __align__(16) u32 wsm[];
   constexpr u32 CB = 32 * CW;
@@ -260,6 +260,122 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 5) coset_wave_kernel(WaveArgs
         if (act) st(k, lane, out, otop);
         __syncwarp();
       }
+      // ---- store: scatter through the post-rotation, carry-save out
+      auto store_slot = [&](u32 k, Ch<CW>& w, int top, u32 post, u32 prek) {
+        const u32 dst = (L0 + (post & 0x7FFFFFFFu)) & (2 * CL - 1);
+        const u32 d = dst & (CL - 1);
+        const u32 ob = post >> 31;
+        const u64 e = lf.base + (u64)k * lf.stride;
+        std::uint8_t* el = (ob ? A.data2 : A.data) + e * A.elem_bytes;
+        if (dst >= CL) top = exact_from<CW>(w, top, true);
+        uint4* gp = reinterpret_cast<uint4*>(el + (u64)d * (CB / 8));
+#pragma unroll
+        for (int q = 0; q < CW / 4; ++q)
+          __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
+        __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
+        // the lane that took the top word (source lane 0), or for an
+        // output-only slot the lane writing lane 0, clears the output's
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (prek & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
+        if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
+      };
+
+      if (cl.wnet) {
+        // ---- the full 8-point network in registers: a butterfly's b comes
+        //      from the lane `q` positions back in the same coset (a shuffle,
+        //      none when q = 0).  Rows are lane-private from here on (no
+        //      __syncwarp): the span-4 level runs pairwise through the rows,
+        //      the two 4-point halves in registers, and outputs go straight
+        //      from registers to global memory.
+        auto bfly = [&](Ch<CW>& a, int& ta, Ch<CW>& b, int& tb, u32 oi) {
+          const u32 qv = __shfl_sync(0xffffffffu, opv0, (int)oi) >> 12;
+          Ch<CW> y0;
+          int t0;
+          if (qv == 0) {  // warp-uniform
+            t0 = ch_add(y0, a, b) + ta + tb;
+            Ch<CW> y1;
+            tb = ch_sub(y1, a, b) + ta - tb;
+            b = y1;
+          } else {
+            const u32 sneg = qv >= cp ? 1u : 0u;
+            const u32 qq = qv - (sneg ? cp : 0u);
+            const u32 pl = (((pos - qq) & (cp - 1)) << cb) | (lane & cmask);
+            const bool neg = ((pos < qq) ? 1u : 0u) != sneg;
+            Ch<CW> bp;
+#pragma unroll
+            for (int w = 0; w < CW; ++w) bp.w[w] = __shfl_sync(0xffffffffu, b.w[w], (int)pl);
+            const int tbp = __shfl_sync(0xffffffffu, tb, (int)pl);
+            if (!neg) {
+              t0 = ch_add(y0, a, bp) + ta + tbp;
+              tb = ch_sub(b, a, bp) + ta - tbp;
+            } else {
+              t0 = ch_sub(y0, a, bp) + ta - tbp;
+              tb = ch_add(b, a, bp) + ta + tbp;
+            }
+          }
+          a = y0;
+          ta = t0;
+        };
+        // span-4 level (op 0..3 or 8..11): pairs (j, j + 4) through the rows
+        auto span4 = [&](u32 o0, bool out) {
+#pragma unroll 1
+          for (u32 j = 0; j < 4; ++j) {
+            Ch<CW> a, b;
+            int ta = ld(a, j, lane), tb = ld(b, j + 4, lane);
+            bfly(a, ta, b, tb, o0 + j);
+            if (out) {
+              const u32 pa = SL(2 * j + 1), ra = SL(2 * j), pb = SL(2 * j + 9), rb = SL(2 * j + 8);
+              if (act) {
+                store_slot(j, a, ta, pa, ra);
+                store_slot(j + 4, b, tb, pb, rb);
+              }
+            } else {
+              st(j, lane, a, ta);
+              st(j + 4, lane, b, tb);
+            }
+          }
+        };
+        // a 4-point half (slots 4h..4h+3): spans 1,2 (DIT: ops 2h, 2h+1 then
+        // 4+2h, 5+2h) or 2,1 (DIF: ops 4+2h, 5+2h then 8+2h, 9+2h)
+        auto half4 = [&](u32 h, bool dit, bool out) {
+          Ch<CW> x[4];
+          int tx[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tx[k] = ld(x[k], 4 * h + k, lane);
+          if (dit) {
+            bfly(x[0], tx[0], x[1], tx[1], 2 * h);
+            bfly(x[2], tx[2], x[3], tx[3], 2 * h + 1);
+            bfly(x[0], tx[0], x[2], tx[2], 4 + 2 * h);
+            bfly(x[1], tx[1], x[3], tx[3], 5 + 2 * h);
+          } else {
+            bfly(x[0], tx[0], x[2], tx[2], 4 + 2 * h);
+            bfly(x[1], tx[1], x[3], tx[3], 5 + 2 * h);
+            bfly(x[0], tx[0], x[1], tx[1], 8 + 2 * h);
+            bfly(x[2], tx[2], x[3], tx[3], 9 + 2 * h);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const u32 sk = 4 * h + k;
+            if (out) {
+              const u32 post = SL(2 * sk + 1), prek = SL(2 * sk);
+              if (act) store_slot(sk, x[k], tx[k], post, prek);
+            } else {
+              st(sk, lane, x[k], tx[k]);
+            }
+          }
+        };
+        if (cl.wnet == 1) {  // DIF: span 4, then the halves
+          span4(0, false);
+          half4(0, false, true);
+          half4(1, false, true);
+        } else {  // DIT: the halves, then span 4
+          half4(0, true, false);
+          half4(1, true, false);
+          span4(8, true);
+        }
+        __syncwarp();
+        continue;
+      }
+
       // ---- the leaf program: every lane runs every micro-op on its chunk
       u32 opv = opv0;
       for (u32 o = 0; o < cl.nops; ++o) {
@@ -301,27 +417,12 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 5) coset_wave_kernel(WaveArgs
         __syncwarp();
       }
 
-      // ---- store: scatter through the post-rotation, carry-save out
       for (u32 k = 0; k < cl.nstore; ++k) {
         const u32 post = SL(2 * k + 1), prek = SL(2 * k);
         if (!act) continue;
-        const u32 dst = (L0 + (post & 0x7FFFFFFFu)) & (2 * CL - 1);
-        const u32 d = dst & (CL - 1);
-        const u32 ob = post >> 31;
-        const u64 e = lf.base + (u64)k * lf.stride;
-        std::uint8_t* el = (ob ? A.data2 : A.data) + e * A.elem_bytes;
         Ch<CW> w;
-        int top = ld(w, k, lane);
-        if (dst >= CL) top = exact_from<CW>(w, top, true);
-        uint4* gp = reinterpret_cast<uint4*>(el + (u64)d * (CB / 8));
-#pragma unroll
-        for (int q = 0; q < CW / 4; ++q)
-          __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
-        __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
-        // the lane that took the top word (source lane 0), or for an
-        // output-only slot the lane writing lane 0, clears the output's
-        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (prek & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
-        if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
+        const int top = ld(w, k, lane);
+        store_slot(k, w, top, post, prek);
       }
       __syncwarp();
     }
