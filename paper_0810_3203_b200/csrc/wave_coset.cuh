@@ -33,7 +33,7 @@ struct WaveArgs {
   std::uint8_t* data;   // caller's view
   std::uint8_t* data2;  // shadow buffer
   u64 elem_bytes;
-  int* T;               // tops, [buffer][element][lane] (natural lane order)
+  int* T;               // tops, [buffer][element][lane] (natural lane order); always set (coset plans)
   u64 tloc;
   const u64* locbits;
   const u32* wops;      // packed micro-ops (Plan::wave_ops)
@@ -54,9 +54,18 @@ template <int CW>
 __host__ __device__ constexpr u32 wave_xrow_words() {
   return (CW + 1 + 3) & ~3u;
 }
+// per ticket and slot: source / destination element and tops row (buffer
+// resolved), the slot's pre / post entry of Plan::wave_slots
+struct WaveSlot {
+  const std::uint8_t* in;
+  const int* tin;
+  std::uint8_t* out;
+  int* tout;
+  u32 pre, post, pad0, pad1;
+};
 template <int CW>
 __host__ __device__ constexpr u32 wave_tile_words() {
-  return 8u * 32u * CW + 8u * 32u + 16u + 8u * 4u * wave_xrow_words<CW>();
+  return 8u * 32u * CW + 8u * 32u + 16u + 8u * 4u * wave_xrow_words<CW>() + 8u * (sizeof(WaveSlot) / 4);
 }
 
 template <int CW>
@@ -73,6 +82,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
   long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * CW + 256u);  // per slot top word
   u32* const xtile = tile + 8u * 32u * CW + 256u + 16u;  // extra rows: [slot][position]
   auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * 4u + p) * XR; };
+  WaveSlot* const si = reinterpret_cast<WaveSlot*>(xtile + 8u * 4u * XR);
   auto swz = [](u32 l) -> u32 { return (l >> 2) & 1u; };
   auto ldw = [&](Ch<CW>& c, const u32* r, u32 sw) {
 #pragma unroll
@@ -140,9 +150,24 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
     // the ticket's slot table and the class's first 32 packed ops, one word
     // per lane, broadcast by shuffles (no dependent global loads in the loops)
     const u32 span = max(cl.nload, cl.nstore);
-    const u32 slv = lane < 2 * span ? A.wslots[lf.c0 + lane] : 0u;
     const u32 opv0 = lane < cl.nops ? A.wops[cl.wop_begin + lane] : 0u;
-    auto SL = [&](u32 i) { return __shfl_sync(0xffffffffu, slv, (int)i); };
+    // the ticket's slots, resolved once (lane k: slot k) and read back by
+    // broadcast; the previous ticket's groups are done with the table
+    __syncwarp();
+    if (lane < span) {
+      const u32 pre = A.wslots[lf.c0 + 2 * lane], post = A.wslots[lf.c0 + 2 * lane + 1];
+      const u64 e = lf.base + (u64)lane * lf.stride;
+      WaveSlot w;
+      w.in = (pre >> 31 ? A.data2 : A.data) + e * A.elem_bytes;
+      w.tin = A.T + (pre >> 31 ? A.tloc : 0) + e * CL;
+      w.out = (post >> 31 ? A.data2 : A.data) + e * A.elem_bytes;
+      w.tout = A.T + (post >> 31 ? A.tloc : 0) + e * CL;
+      w.pre = pre;
+      w.post = post;
+      w.pad0 = w.pad1 = 0;
+      si[lane] = w;
+    }
+    __syncwarp();
     for (; i < tend; i += nwarps) {
       const u32 g = (u32)(i - (u64)t * gpl);
       if (g >= groups) continue;
@@ -161,19 +186,17 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       // slot table: {pre bits | in-buffer << 31, post lanes | out-buffer << 31}
       const bool first = (lane & cmask) == 0;
       for (u32 k = 0; k < cl.nload; ++k) {
-        const u32 pre = SL(2 * k), r = pre & 0x7FFFFFFFu;
-        if (!act) continue;
+        if (!act) break;
+        const u32 r = si[k].pre & 0x7FFFFFFFu;
         const u32 q = r / CB, o = r % CB;
         const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
         const u32 lnA = srcA & (CL - 1);
-        const u32 ib = pre >> 31;
-        const u64 e = lf.base + (u64)k * lf.stride;
-        const std::uint8_t* el = (ib ? A.data2 : A.data) + e * A.elem_bytes;
-        const int* tr = A.T ? A.T + (ib ? A.tloc : 0) + e * CL : nullptr;
+        const std::uint8_t* el = si[k].in;
+        const int* tr = si[k].tin;
         const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
         for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
-        if (tr) cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + lnA);
+        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + lnA);
         if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
@@ -187,7 +210,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             const u32 xo = (u32)__cvta_generic_to_shared(xrow(k, pos));
 #pragma unroll
             for (int x = 0; x < CW / 4; ++x) cp_async16(xo + 16u * x, el + (u64)lnB * (CB / 8) + 16u * x);
-            if (tr) cp_async4(xo + 4u * CW, tr + lnB);
+            cp_async4(xo + 4u * CW, tr + lnB);
           }
         }
       }
@@ -196,8 +219,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       // rows -> true carry-save values of their source lanes: the coefficient's
       // top word folded into (every copy of) source lane 0, wrapped lanes negated
       auto settle = [&](u32* rw, u32 sw, int* tp, u32 k, bool zero, bool neg) {
-        int top = A.T ? *tp : 0;
-        if (!A.T) *tp = 0;
+        int top = *tp;
         if (!zero && !neg) return;
         Ch<CW> w;
         ldw(w, rw, sw);
@@ -219,7 +241,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       __syncwarp();
       // unaligned slots: lane L0 = bits [Λ - o, 2Λ - o) of (B ++ A) plus B's top at bit o
       for (u32 k = 0; k < cl.nload; ++k) {
-        const u32 o = (SL(2 * k) & 0x7FFFFFFFu) % CB;  // uniform across the warp
+        const u32 o = (si[k].pre & 0x7FFFFFFFu) % CB;  // uniform across the warp
         if (o == 0) continue;
         Ch<CW> out;
         int otop = 0;
@@ -261,21 +283,20 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         __syncwarp();
       }
       // ---- store: scatter through the post-rotation, carry-save out
-      auto store_slot = [&](u32 k, Ch<CW>& w, int top, u32 post, u32 prek) {
-        const u32 dst = (L0 + (post & 0x7FFFFFFFu)) & (2 * CL - 1);
+      auto store_slot = [&](u32 k, Ch<CW>& w, int top) {
+        const WaveSlot* sk = si + k;
+        const u32 dst = (L0 + (sk->post & 0x7FFFFFFFu)) & (2 * CL - 1);
         const u32 d = dst & (CL - 1);
-        const u32 ob = post >> 31;
-        const u64 e = lf.base + (u64)k * lf.stride;
-        std::uint8_t* el = (ob ? A.data2 : A.data) + e * A.elem_bytes;
+        std::uint8_t* el = sk->out;
         if (dst >= CL) top = exact_from<CW>(w, top, true);
         uint4* gp = reinterpret_cast<uint4*>(el + (u64)d * (CB / 8));
 #pragma unroll
         for (int q = 0; q < CW / 4; ++q)
           __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
-        __stcg(A.T + (ob ? A.tloc : 0) + e * CL + d, top);
+        __stcg(sk->tout + d, top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
-        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (prek & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
         if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
       };
 
@@ -323,10 +344,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             int ta = ld(a, j, lane), tb = ld(b, j + 4, lane);
             bfly(a, ta, b, tb, o0 + j);
             if (out) {
-              const u32 pa = SL(2 * j + 1), ra = SL(2 * j), pb = SL(2 * j + 9), rb = SL(2 * j + 8);
               if (act) {
-                store_slot(j, a, ta, pa, ra);
-                store_slot(j + 4, b, tb, pb, rb);
+                store_slot(j, a, ta);
+                store_slot(j + 4, b, tb);
               }
             } else {
               st(j, lane, a, ta);
@@ -356,8 +376,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           for (int k = 0; k < 4; ++k) {
             const u32 sk = 4 * h + k;
             if (out) {
-              const u32 post = SL(2 * sk + 1), prek = SL(2 * sk);
-              if (act) store_slot(sk, x[k], tx[k], post, prek);
+              if (act) store_slot(sk, x[k], tx[k]);
             } else {
               st(sk, lane, x[k], tx[k]);
             }
@@ -418,11 +437,10 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       }
 
       for (u32 k = 0; k < cl.nstore; ++k) {
-        const u32 post = SL(2 * k + 1), prek = SL(2 * k);
-        if (!act) continue;
+        if (!act) break;
         Ch<CW> w;
         const int top = ld(w, k, lane);
-        store_slot(k, w, top, post, prek);
+        store_slot(k, w, top);
       }
       __syncwarp();
     }
