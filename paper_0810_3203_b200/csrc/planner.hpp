@@ -186,7 +186,7 @@ struct Plan {
   std::vector<u32> wave_op_begin;  // per class
   std::vector<u32> wave_net;       // per class, DevClass::wnet
   // wave engine, coset tickets: per slot {pre bits | in-buffer << 31,
-  // post lanes | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
+  // post lanes | final output << 30 | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
   // whole tickets with deferred rotations on their inputs: per loaded slot
   // the extra pre-rotation bits, at DevLeaf::c0 - 1 (c0 = 0: none)
   std::vector<u32> wave_slots;
@@ -406,6 +406,7 @@ class Planner {
     p.wave_slots.clear();
     p.final_rot.clear();
     std::vector<u32> pend(extent_, 0);
+    std::vector<u64> last(extent_, ~u64{0});  // wave_slots index of the element's last coset write
     for (auto& lf : leaves_) {
       const LeafProgram& cl = classes_[lf.cls];
       const bool inv = cl.key.inverse != 0;
@@ -416,7 +417,10 @@ class Planner {
           lf.c0 = (u32)p.wave_slots.size() + 1;
           for (u32 k = 0; k < cl.nload; ++k) p.wave_slots.push_back(pend[lf.base + (u64)k * lf.stride]);
         }
-        for (u32 k = 0; k < cl.nstore; ++k) pend[lf.base + (u64)k * lf.stride] = 0;
+        for (u32 k = 0; k < cl.nstore; ++k) {
+          pend[lf.base + (u64)k * lf.stride] = 0;
+          last[lf.base + (u64)k * lf.stride] = ~u64{0};
+        }
         continue;
       }
       const u32 off = (u32)p.wave_slots.size();
@@ -433,6 +437,7 @@ class Planner {
           const u64 r = (cl.post[k].a * lf.s + cl.post[k].b + (tp ? lf.tpost : 0)) & (M - 1);
           post = (u32)(r / lb);
           pend[e] = (u32)(r % lb);
+          last[e] = p.wave_slots.size() + 1;
         }
         if (lf.locoff != kNoDep) {
           if ((p.locbits[lf.locoff + 2 * (k / 64)] >> (k % 64)) & 1) pre |= 1u << 31;
@@ -443,11 +448,15 @@ class Planner {
       }
       lf.c0 = off;
     }
-    for (u64 e : finals)
+    for (u64 e : finals) {
       if (pend[e]) {
         if (p.final_rot.empty()) p.final_rot.assign(extent_, 0);
         p.final_rot[e] = pend[e];
       }
+      // the last writer of an output absorbs lane tops into the next lane
+      // where the warp holds both (wave_coset.cuh, store_slot)
+      if (last[e] != ~u64{0}) p.wave_slots[last[e]] |= 1u << 30;
+    }
   }
 
   // 1 / 2: the class is the full 8-point network with butterfly spans 4,2,1

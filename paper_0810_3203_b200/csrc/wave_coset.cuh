@@ -283,12 +283,27 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         __syncwarp();
       }
       // ---- store: scatter through the post-rotation, carry-save out
+      // (called by every lane of the warp)
       auto store_slot = [&](u32 k, Ch<CW>& w, int top) {
         const WaveSlot* sk = si + k;
-        const u32 dst = (L0 + (sk->post & 0x7FFFFFFFu)) & (2 * CL - 1);
+        const u32 post = sk->post;
+        const u32 dst = (L0 + (post & 0x3FFFFFFFu)) & (2 * CL - 1);
         const u32 d = dst & (CL - 1);
         std::uint8_t* el = sk->out;
         if (dst >= CL) top = exact_from<CW>(w, top, true);
+        if (post & (1u << 30)) {
+          // a final output (warp-uniform): output lane d takes the top of
+          // lane d-1 (lane 0: minus lane C-1's, 2^N == -1) from the warp lane
+          // before it when that lane holds it -- the final fold then only
+          // touches lanes at warp-group edges and rare carries
+          const int up = __shfl_up_sync(0xffffffffu, top, 1);
+          const bool takes = (lane & cmask) != 0;
+          const bool gives = (lane & cmask) != cmask && c + 1 < step;
+          const int cin = takes ? (d == 0 ? -up : up) : 0;
+          const int co = cin ? ch_add_small<CW>(w, cin) : 0;
+          top = co + (gives ? 0 : top);
+        }
+        if (!act) return;
         uint4* gp = reinterpret_cast<uint4*>(el + (u64)d * (CB / 8));
 #pragma unroll
         for (int q = 0; q < CW / 4; ++q)
@@ -344,10 +359,8 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             int ta = ld(a, j, lane), tb = ld(b, j + 4, lane);
             bfly(a, ta, b, tb, o0 + j);
             if (out) {
-              if (act) {
-                store_slot(j, a, ta);
-                store_slot(j + 4, b, tb);
-              }
+              store_slot(j, a, ta);
+              store_slot(j + 4, b, tb);
             } else {
               st(j, lane, a, ta);
               st(j + 4, lane, b, tb);
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           for (int k = 0; k < 4; ++k) {
             const u32 sk = 4 * h + k;
             if (out) {
-              if (act) store_slot(sk, x[k], tx[k]);
+              store_slot(sk, x[k], tx[k]);
             } else {
               st(sk, lane, x[k], tx[k]);
             }
@@ -437,7 +450,6 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       }
 
       for (u32 k = 0; k < cl.nstore; ++k) {
-        if (!act) break;
         Ch<CW> w;
         const int top = ld(w, k, lane);
         store_slot(k, w, top);

@@ -166,7 +166,7 @@ def run_plan_fermat(plan, N, vals):
             tp = (tpost if cf_ and i == cn else 0) if inv else tpost
             e = (ea * s + eb + tp) % M
             if wplan and coset:  # whole lanes; the sub-lane rest goes to the next reader
-                e = (ws[c0 + 2 * i + 1] & 0x7FFFFFFF) * lane
+                e = (ws[c0 + 2 * i + 1] & 0x3FFFFFFF) * lane
             assert not coset or e % lane == 0
             ob = buf(locoff, i, True)
             if coset and i < c["nload"]:
