@@ -154,6 +154,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
     // the ticket's slots, resolved once (lane k: slot k) and read back by
     // broadcast; the previous ticket's groups are done with the table
     __syncwarp();
+    const u32 pre_l = lane < cl.nload ? A.wslots[lf.c0 + 2 * lane] : 0u;
+    // any unaligned pre-rotation in the ticket (warp-uniform)
+    const bool tunal = __any_sync(0xffffffffu, ((pre_l & 0x7FFFFFFFu) % CB) != 0);
     if (lane < span) {
       const u32 pre = A.wslots[lf.c0 + 2 * lane], post = A.wslots[lf.c0 + 2 * lane + 1];
       const u64 e = lf.base + (u64)lane * lf.stride;
@@ -185,8 +188,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       u32 wrapA = 0, wrapB = 0, zeroA = 0, zeroB = 0, unal = 0;  // per-slot bit masks
       // slot table: {pre bits | in-buffer << 31, post lanes | out-buffer << 31}
       const bool first = (lane & cmask) == 0;
-      for (u32 k = 0; k < cl.nload; ++k) {
-        if (!act) break;
+#pragma unroll
+      for (u32 k = 0; k < 8; ++k) {
+        if (!act || k >= cl.nload) break;
         const u32 r = si[k].pre & 0x7FFFFFFFu;
         const u32 q = r / CB, o = r % CB;
         const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
@@ -216,6 +220,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       }
       cp_async_wait_all();
       __syncwarp();
+      // full networks without unaligned pre-rotations settle their rows as
+      // they first read them into registers (no separate pass)
+      const bool fused = cl.wnet && !tunal;
       // rows -> true carry-save values of their source lanes: the coefficient's
       // top word folded into (every copy of) source lane 0, wrapped lanes negated
       auto settle = [&](u32* rw, u32 sw, int* tp, u32 k, bool zero, bool neg) {
@@ -231,7 +238,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         stw(rw, sw, w);
         *tp = top;
       };
-      for (u32 k = 0; k < cl.nload; ++k) {
+      for (u32 k = 0; k < (fused ? 0u : cl.nload); ++k) {
         if (!act) break;
         settle(rowp(k, lane), swz(lane), tops + k * 32u + lane, k, (zeroA >> k) & 1u, (wrapA >> k) & 1u);
         if (((unal >> k) & 1u) && first)
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       }
       __syncwarp();
       // unaligned slots: lane L0 = bits [Λ - o, 2Λ - o) of (B ++ A) plus B's top at bit o
-      for (u32 k = 0; k < cl.nload; ++k) {
+      for (u32 k = 0; k < (tunal ? cl.nload : 0u); ++k) {
         const u32 o = (si[k].pre & 0x7FFFFFFFu) % CB;  // uniform across the warp
         if (o == 0) continue;
         Ch<CW> out;
@@ -352,11 +359,23 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           ta = t0;
         };
         // span-4 level (op 0..3 or 8..11): pairs (j, j + 4) through the rows
-        auto span4 = [&](u32 o0, bool out) {
+        // a row read into registers; `fresh` (fused settle): first read of the slot
+        auto ldx = [&](Ch<CW>& c, u32 k, bool fresh) -> int {
+          int top = ld(c, k, lane);
+          if (fresh) {
+            if ((zeroA >> k) & 1u) {
+              const int hi = (int)hiw[k];
+              if (hi) top += ch_add_small<CW>(c, -hi);
+            }
+            if ((wrapA >> k) & 1u) top = exact_from<CW>(c, top, true);
+          }
+          return top;
+        };
+        auto span4 = [&](u32 o0, bool out, bool fresh) {
 #pragma unroll 1
           for (u32 j = 0; j < 4; ++j) {
             Ch<CW> a, b;
-            int ta = ld(a, j, lane), tb = ld(b, j + 4, lane);
+            int ta = ldx(a, j, fresh), tb = ldx(b, j + 4, fresh);
             bfly(a, ta, b, tb, o0 + j);
             if (out) {
               store_slot(j, a, ta);
@@ -369,11 +388,11 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         };
         // a 4-point half (slots 4h..4h+3): spans 1,2 (DIT: ops 2h, 2h+1 then
         // 4+2h, 5+2h) or 2,1 (DIF: ops 4+2h, 5+2h then 8+2h, 9+2h)
-        auto half4 = [&](u32 h, bool dit, bool out) {
+        auto half4 = [&](u32 h, bool dit, bool out, bool fresh) {
           Ch<CW> x[4];
           int tx[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) tx[k] = ld(x[k], 4 * h + k, lane);
+          for (int k = 0; k < 4; ++k) tx[k] = ldx(x[k], 4 * h + k, fresh);
           if (dit) {
             bfly(x[0], tx[0], x[1], tx[1], 2 * h);
             bfly(x[2], tx[2], x[3], tx[3], 2 * h + 1);
@@ -396,13 +415,13 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           }
         };
         if (cl.wnet == 1) {  // DIF: span 4, then the halves
-          span4(0, false);
-          half4(0, false, true);
-          half4(1, false, true);
+          span4(0, false, fused);
+          half4(0, false, true, false);
+          half4(1, false, true, false);
         } else {  // DIT: the halves, then span 4
-          half4(0, true, false);
-          half4(1, true, false);
-          span4(8, true);
+          half4(0, true, false, fused);
+          half4(1, true, false, fused);
+          span4(8, true, false);
         }
         __syncwarp();
         continue;
