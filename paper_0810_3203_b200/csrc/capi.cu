@@ -721,7 +721,8 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
     os << "{\"ell\":" << k.key.ell << ",\"inverse\":" << k.key.inverse << ",\"z\":" << k.key.z
        << ",\"n\":" << k.key.n << ",\"f\":" << k.key.f << ",\"nload\":" << k.nload
        << ",\"nstore\":" << k.nstore << ",\"kind\":" << k.kind << ",\"step\":" << k.step
-       << ",\"m\":" << k.m << ",\"cs\":" << k.cs << ",\"levels\":[";
+       << ",\"m\":" << k.m << ",\"cs\":" << k.cs
+       << ",\"wnet\":" << (c < p.wave_net.size() ? p.wave_net[c] : 0u) << ",\"levels\":[";
     for (size_t l = 0; l < k.level_begin.size(); ++l) os << (l ? "," : "") << k.level_begin[l];
     os << "],\"ops\":[";
     for (size_t i = 0; i < k.ops.size(); ++i) {

@@ -459,18 +459,35 @@ class Planner {
     }
   }
 
-  // 1 / 2: the class is the full 8-point network with butterfly spans 4,2,1
-  // (the TFT's) / 1,2,4 (the ITFT's), every op an ADDSUB in level order --
-  // the warp kernel then runs it in registers; 0: anything else
+  // 1 / 2: the class runs as the full 8-point network of ADDSUB butterflies
+  // with spans 4,2,1 (the TFT's) / 1,2,4 (the ITFT's) in level order -- the
+  // warp kernel then keeps it in registers; 0: anything else.  Truncated
+  // programs (z or n < 8) qualify when every op is an ADDSUB on the network's
+  // pairs, a COPY into a slot that still holds a truncated (zero) input, or an
+  // ADD whose b is never read again: with the missing inputs read as zeros
+  // and outputs >= n not stored, the ADDSUB network computes the same values.
   static u32 full_network(const LeafProgram& cl) {
-    if (cl.key.ell != 3 || cl.nload != 8 || cl.nstore != 8 || cl.ops.size() != 12) return 0;
+    if (cl.key.ell != 3 || cl.ops.size() != 12 || cl.nload == 0) return 0;
     for (u32 net = 1; net <= 2; ++net) {
       bool ok = true;
+      bool zero[8];
+      for (u32 k = 0; k < 8; ++k) zero[k] = k >= cl.nload;
       for (u32 o = 0; o < 12 && ok; ++o) {
         const u32 lvl = o >> 2, j = o & 3, h = net == 1 ? (4u >> lvl) : (1u << lvl);
         const u32 a = (j / h) * 2 * h + (j % h);
         const DevOp& op = cl.ops[o];
-        ok = op.type == OP_ADDSUB && op.a == a && op.b == a + h;
+        ok = op.a == a && op.b == a + h;
+        if (!ok) break;
+        if (op.type == OP_COPY) {
+          ok = zero[op.b];
+        } else if (op.type == OP_ADD) {
+          for (u32 o2 = o + 1; o2 < 12 && ok; ++o2) ok = cl.ops[o2].a != op.b && cl.ops[o2].b != op.b;
+          ok = ok && op.b >= cl.nstore;
+        } else {
+          ok = op.type == OP_ADDSUB;
+        }
+        const bool z = zero[op.a] && zero[op.b];
+        zero[op.a] = zero[op.b] = z;
       }
       if (ok) return net;
     }

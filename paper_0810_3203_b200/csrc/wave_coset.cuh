@@ -360,7 +360,13 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         };
         // span-4 level (op 0..3 or 8..11): pairs (j, j + 4) through the rows
         // a row read into registers; `fresh` (fused settle): first read of the slot
-        auto ldx = [&](Ch<CW>& c, u32 k, bool fresh) -> int {
+        // first: the slot's first read (slots >= nload are truncated inputs: zero)
+        auto ldx = [&](Ch<CW>& c, u32 k, bool first, bool fresh) -> int {
+          if (first && k >= cl.nload) {  // warp-uniform
+#pragma unroll
+            for (int w = 0; w < CW; ++w) c.w[w] = 0;
+            return 0;
+          }
           int top = ld(c, k, lane);
           if (fresh) {
             if ((zeroA >> k) & 1u) {
@@ -371,15 +377,15 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           }
           return top;
         };
-        auto span4 = [&](u32 o0, bool out, bool fresh) {
+        auto span4 = [&](u32 o0, bool out, bool first, bool fresh) {
 #pragma unroll 1
           for (u32 j = 0; j < 4; ++j) {
             Ch<CW> a, b;
-            int ta = ldx(a, j, fresh), tb = ldx(b, j + 4, fresh);
+            int ta = ldx(a, j, first, fresh), tb = ldx(b, j + 4, first, fresh);
             bfly(a, ta, b, tb, o0 + j);
             if (out) {
-              store_slot(j, a, ta);
-              store_slot(j + 4, b, tb);
+              if (j < cl.nstore) store_slot(j, a, ta);
+              if (j + 4 < cl.nstore) store_slot(j + 4, b, tb);
             } else {
               st(j, lane, a, ta);
               st(j + 4, lane, b, tb);
@@ -388,11 +394,11 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         };
         // a 4-point half (slots 4h..4h+3): spans 1,2 (DIT: ops 2h, 2h+1 then
         // 4+2h, 5+2h) or 2,1 (DIF: ops 4+2h, 5+2h then 8+2h, 9+2h)
-        auto half4 = [&](u32 h, bool dit, bool out, bool fresh) {
+        auto half4 = [&](u32 h, bool dit, bool out, bool first, bool fresh) {
           Ch<CW> x[4];
           int tx[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) tx[k] = ldx(x[k], 4 * h + k, fresh);
+          for (int k = 0; k < 4; ++k) tx[k] = ldx(x[k], 4 * h + k, first, fresh);
           if (dit) {
             bfly(x[0], tx[0], x[1], tx[1], 2 * h);
             bfly(x[2], tx[2], x[3], tx[3], 2 * h + 1);
@@ -408,20 +414,20 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           for (int k = 0; k < 4; ++k) {
             const u32 sk = 4 * h + k;
             if (out) {
-              store_slot(sk, x[k], tx[k]);
+              if (sk < cl.nstore) store_slot(sk, x[k], tx[k]);
             } else {
               st(sk, lane, x[k], tx[k]);
             }
           }
         };
         if (cl.wnet == 1) {  // DIF: span 4, then the halves
-          span4(0, false, fused);
-          half4(0, false, true, false);
-          half4(1, false, true, false);
+          span4(0, false, true, fused);
+          half4(0, false, true, false, false);
+          half4(1, false, true, false, false);
         } else {  // DIT: the halves, then span 4
-          half4(0, true, false, fused);
-          half4(1, true, false, fused);
-          span4(8, true, false);
+          half4(0, true, false, true, fused);
+          half4(1, true, false, true, fused);
+          span4(8, true, false, false);
         }
         __syncwarp();
         continue;

@@ -145,7 +145,14 @@ def run_plan_fermat(plan, N, vals):
                 e = (e + ws[c0 - 1 + i]) % M
             assert not coset or e % lane == 0 or wplan
             slot[i] = (x[(buf(locoff, i, False), base + i * stride)] * pow(2, e, P)) % P
-        for (t, a, b, r) in (c["ops"] if run else []):
+        ops = c["ops"]
+        if c.get("wnet"):
+            # the warp kernel runs these as the full ADDSUB network (spans 4,2,1
+            # or 1,2,4) on zero-filled truncated inputs, storing outputs < n
+            for i in range(c["nload"], 8):
+                slot[i] = 0
+            ops = [(0, a, b, r) for (t, a, b, r) in ops]
+        for (t, a, b, r) in (ops if run else []):
             assert not coset or t == 4 or r % (M >> c["ell"]) == 0
             if t == 4:
                 slot[b] = slot[a]
