@@ -90,6 +90,12 @@ int cftft_stream_synchronize(void* stream);
  * Results are bit-identical in every mode. */
 int cftft_ring_set_coset(cftft_ring* ring, int lane_words);
 
+/* Fermat rings with coset leaves: 1 runs leaves of up to 64 coefficients on
+ * the CTA-level radix-64 kernel (three passes over the data at L = 2^18
+ * instead of six), 0 the radix-8 warp engine, -1 (default) follows the
+ * environment variable CFTFT_WIDE (unset: 0).  Bit-identical results. */
+int cftft_ring_set_wide(cftft_ring* ring, int wide);
+
 /* Forward truncated transform, in place over a DEVICE view
  * (replaces cftft::cf_tft, transform.hpp:252-264).  On entry x[0..z) hold
  * the coefficients (cells beyond are never read); on exit x[0..n) hold the

@@ -109,6 +109,7 @@ def lib():
         L.cftft_ring_set_leaf_limit.argtypes = [vp, C.c_uint]
         L.cftft_ring_set_leaf_limit.restype = C.c_uint
         L.cftft_ring_set_coset.argtypes = [vp, C.c_int]
+        L.cftft_ring_set_wide.argtypes = [vp, C.c_int]
         for f in ("cftft_gpu_tft", "cftft_gpu_itft"):
             getattr(L, f).argtypes = [vp, P, vp, u64, C.c_int, C.POINTER(u64), vp]
         for f in ("cftft_tft_host", "cftft_itft_host"):
@@ -185,6 +186,11 @@ class FermatRingCtx(_Ring):
         """Leaf layout: 0 = whole-coefficient leaves only; 4/8/16 = coset leaves
         over lanes of that many 32-bit words; -1 = automatic (default)."""
         _check(lib().cftft_ring_set_coset(self._h, lane_words))
+
+    def set_wide(self, wide: int) -> None:
+        """Radix-64 coset leaves on the CTA kernel: 1 on, 0 off (radix-8 warp
+        engine), -1 = environment CFTFT_WIDE (default off)."""
+        _check(lib().cftft_ring_set_wide(self._h, wide))
 
 
 class NegacyclicRingCtx(_Ring):

@@ -21,6 +21,7 @@
 #include "negacyclic_leaf.cuh"
 #include "pointwise.cuh"
 #include "wave_coset.cuh"
+#include "wave_wide.cuh"
 #include "planner.hpp"
 
 using namespace cftft_b200;
@@ -80,6 +81,7 @@ struct cftft_ring {
   int kind = 0;
   int coset_cw = -1;          // Fermat coset leaves: -1 auto, 0 off, 4/8/16 lane words
   int wave = -1;              // Fermat wave engine: -1 auto, 0 off, 1 on
+  int wide = -1;              // radix-64 coset leaves (coset_wide_kernel): -1 env CFTFT_WIDE (default off), 0, 1
   unsigned leaf_limit = 0;    // cftft_ring_set_leaf_limit (0: none)
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
@@ -262,7 +264,12 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       if (wave && cw == 8) {
         rs.wave_engine = true;
         rs.wave_unaligned = getenv("CFTFT_WAVE_ALIGNED") == nullptr;
-        cl = std::min(cl, 3u);
+        // radix-64 coset leaves on the CTA kernel (CFTFT_WIDE=0: radix 8 only)
+        // (measured slower than the radix-8 engine so far: opt-in)
+        static const int env_wide = getenv("CFTFT_WIDE") ? atoi(getenv("CFTFT_WIDE")) : 0;
+        const int wide = R->wide >= 0 ? R->wide : env_wide;
+        rs.wide = wide != 0 && cl >= 6 && (R->M >> 6) % rs.lane_bits == 0;
+        cl = std::min(cl, rs.wide ? 6u : 3u);
         rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
       }
       rs.coset_max_ell = cl;
@@ -280,7 +287,9 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
     dp->C = C;
     dp->slot_bytes = sb;
     u32 logS = 0;
-    if (rs.lane_bits && !rs.wave_engine) {
+    if (rs.lane_bits && (!rs.wave_engine || rs.wide)) {
+      // the lanes of one coset of the largest coset leaves are contiguous in
+      // the tops arrays (wide plans: one coset per warp row)
       const u64 S = std::max<u64>(1, (2ull * C) >> rs.coset_max_ell);
       logS = (u32)__builtin_ctzll(S);
     }
@@ -545,6 +554,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         W.tloc = A.tloc;
         W.locbits = dp.locbits;
         W.wops = dp.wave_ops;
+        W.levels = dp.levels;
+        W.logS = dp.logS;
+        W.debug = dbg;
+        W.logLanes = (u32)__builtin_ctz(dp.C);
         W.wslots = dp.wave_slots;
         W.lanes = dp.C;
         W.D = R->D;
@@ -563,8 +576,26 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8>, 32 * wwarps, wsmem));
+        const size_t xsmem = (size_t)fermat::wide_tile_words<8>() * 4;
+        int xper = 0;
+        if (dp.host.wide) {
+          static bool wide_attr = false;
+          if (!wide_attr) {
+            CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wide_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)xsmem));
+            wide_attr = true;
+          }
+          CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, fermat::coset_wide_kernel<8>,
+                                                                 32 * fermat::kWideWarps, xsmem));
+        }
         for (const auto& wr : dp.host.waves) {
-          if (wr[2] == 1) {
+          if (wr[2] == 2) {
+            W.leaves = dp.leaves + wr[0];
+            W.nleaves = (u32)wr[1];
+            W.gpl = (u32)std::max<u64>(1, wr[3]);
+            const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms * std::max(xper, 1));
+            fermat::coset_wide_kernel<8><<<g, 32 * fermat::kWideWarps, xsmem, st>>>(W);
+          } else if (wr[2] == 1) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];
             W.gpl = (u32)std::max<u64>(1, wr[3]);
@@ -702,7 +733,11 @@ int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* 
 
 void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
   os << "{\"inverse\":" << (p.inverse ? 1 : 0) << ",\"lane_bits\":" << lane_bits << ",\"coset\":" << (p.coset ? 1 : 0)
-     << ",\"wave\":" << (p.waves.empty() ? 0 : 1)
+     << ",\"wave\":" << (p.waves.empty() ? 0 : 1);
+  os << ",\"waves\":[";
+  for (size_t w = 0; w < p.waves.size(); ++w)
+    os << (w ? "," : "") << "[" << p.waves[w][0] << "," << p.waves[w][1] << "," << p.waves[w][2] << "," << p.waves[w][3] << "]";
+  os << "]"
      << ",\"L\":" << p.L << ",\"s\":" << p.s
      << ",\"z\":" << p.z << ",\"n\":" << p.n << ",\"f\":" << p.f << ",\"final_count\":"
      << p.final_count << ",\"counters\":[";
@@ -722,7 +757,14 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
        << ",\"n\":" << k.key.n << ",\"f\":" << k.key.f << ",\"nload\":" << k.nload
        << ",\"nstore\":" << k.nstore << ",\"kind\":" << k.kind << ",\"step\":" << k.step
        << ",\"m\":" << k.m << ",\"cs\":" << k.cs
-       << ",\"wnet\":" << (c < p.wave_net.size() ? p.wave_net[c] : 0u) << ",\"levels\":[";
+       << ",\"wnet\":" << (c < p.wave_net.size() ? p.wave_net[c] : 0u);
+    if (c < p.wave_net.size() && p.wave_net[c] && k.key.ell == 6) {
+      // the radix-64 network's rotations (coset positions), (stage, warp, op)
+      os << ",\"net\":[";
+      for (u32 i = 0; i < 192; ++i) os << (i ? "," : "") << (p.wave_ops[p.wave_op_begin[c] + i] >> 16);
+      os << "]";
+    }
+    os << ",\"levels\":[";
     for (size_t l = 0; l < k.level_begin.size(); ++l) os << (l ? "," : "") << k.level_begin[l];
     os << "],\"ops\":[";
     for (size_t i = 0; i < k.ops.size(); ++i) {
@@ -850,6 +892,17 @@ int cftft_ring_set_coset(cftft_ring* ring, int lane_words) {
   std::lock_guard<std::mutex> g(ring->mu);
   if (ring->coset_cw != lane_words) {
     ring->coset_cw = lane_words;
+    ring->cache.clear();
+  }
+  return CFTFT_OK;
+}
+
+int cftft_ring_set_wide(cftft_ring* ring, int wide) {
+  if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (wide < -1 || wide > 1) return fail(CFTFT_INVALID_PARAMS, "wide must be -1 (environment), 0 or 1");
+  std::lock_guard<std::mutex> g(ring->mu);
+  if (ring->wide != wide) {
+    ring->wide = wide;
     ring->cache.clear();
   }
   return CFTFT_OK;

@@ -180,8 +180,8 @@ struct Plan {
   // order; {first ticket, count, kind (0 whole, 1 coset), coset ranges: the
   // most warp groups of lane cosets a ticket of the range has}
   std::vector<std::array<u64, 4>> waves;
-  // wave engine, coset classes: micro-ops packed as type | a << 4 | b << 8 |
-  // q << 12, q the rotation in coset positions (class order, see wop_begin)
+  // wave engine, coset classes: micro-ops packed as type | a << 4 | b << 10 |
+  // q << 16, q the rotation in coset positions (class order, see wop_begin)
   std::vector<u32> wave_ops;
   std::vector<u32> wave_op_begin;  // per class
   std::vector<u32> wave_net;       // per class, DevClass::wnet
@@ -193,6 +193,7 @@ struct Plan {
   // outputs whose last writer deferred a sub-lane rotation: bits per view
   // element [0, extent), applied by the final fold (empty: none)
   std::vector<u32> final_rot;
+  bool wide = false;  // some waves run on coset_wide_kernel (kind 2)
 };
 
 // Ring-dependent planning parameters.
@@ -217,6 +218,10 @@ struct RingShape {
   // coset leaves run on the warp-level kernel (csrc/wave_coset.cuh)
   bool wave_engine = false;
   bool wave_unaligned = true;  // coset leaves may take unaligned pre-rotations (warp kernel)
+  // wave engine with coset leaves of up to 64 coefficients: leaves of 2^4..2^6
+  // run on the CTA kernel (csrc/wave_wide.cuh); the top-level split leaves
+  // row nodes of 2^(6k) coefficients (three radix-64 passes at L = 2^18)
+  bool wide = false;
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -397,10 +402,21 @@ class Planner {
       const LeafProgram& cl = classes_[c];
       p.wave_op_begin[c] = (u32)p.wave_ops.size();
       if (cl.kind != 1) continue;
-      p.wave_net[c] = full_network(cl);
+      if (cl.key.ell >= 4) {
+        // CTA kernel: the radix-64 network's rotations per (stage, warp, op),
+        // or the class's micro-ops
+        std::vector<u32> net;
+        p.wave_net[c] = wide_network(cl, M, net);
+        if (p.wave_net[c]) {
+          p.wave_ops.insert(p.wave_ops.end(), net.begin(), net.end());
+          continue;
+        }
+      } else {
+        p.wave_net[c] = full_network(cl);
+      }
       for (const auto& op : cl.ops) {
         const u64 q = op.type == OP_COPY ? 0 : (op.r / lb) / cl.step;
-        p.wave_ops.push_back((u32)op.type | ((u32)op.a << 4) | ((u32)op.b << 8) | ((u32)q << 12));
+        p.wave_ops.push_back((u32)op.type | ((u32)op.a << 4) | ((u32)op.b << 10) | ((u32)q << 16));
       }
     }
     p.wave_slots.clear();
@@ -459,6 +475,112 @@ class Planner {
     }
   }
 
+  // launch kind of a leaf class in the wave engine: 0 whole (leaf_kernel),
+  // 1 coset leaf of <= 8 coefficients (coset_wave_kernel), 2 coset leaf of
+  // 16..64 coefficients (coset_wide_kernel)
+  static u32 wave_kind(const LeafProgram& cl) {
+    if (cl.kind != 1) return 0;
+    return cl.key.ell >= 4 ? 2u : 1u;
+  }
+
+  // 1 / 2: the 64-slot class runs as the radix-2 DIF (spans 32..1, the TFT's)
+  // / DIT (spans 1..32, the ITFT's) network of ADDSUB butterflies, as two
+  // stages of eight 8-point networks in registers (coset_wide_kernel); 0:
+  // anything else.  `net` gets the rotation (coset positions << 16) of every
+  // butterfly, ordered (stage, warp, op) with ops in the 8-point network order
+  // of wave_coset.cuh.  Truncated programs qualify when every op lies on a
+  // network pair in network order and the network -- missing inputs read as
+  // zeros, butterflies the program skips run with rotation 0, outputs >= n
+  // not stored -- reproduces the program exactly: both are evaluated over
+  // Z[x]/(x^32+1) (x = the leaf's rotation unit, x^32 = -1) on random inputs.
+  static u32 wide_network(const LeafProgram& cl, u64 M, std::vector<u32>& net) {
+    if (cl.key.ell != 6 || cl.nload == 0 || cl.ops.empty()) return 0;
+    const u64 unit = M >> 6;
+    using V = std::array<long long, 32>;
+    auto rot = [](const V& v, u64 q) {  // x^q v
+      V r{};
+      for (u32 d = 0; d < 32; ++d) {
+        const u64 t = d + q;
+        const bool neg = ((t / 32) & 1) != 0;
+        r[t % 32] = neg ? -v[d] : v[d];
+      }
+      return r;
+    };
+    auto ilog = [](u32 h) { u32 l = 0; while ((1u << l) < h) ++l; return l; };
+    for (u32 kind = 1; kind <= 2; ++kind) {
+      int qn[6][32];
+      for (auto& row : qn)
+        for (int& q : row) q = -1;
+      std::array<int, 64> last;
+      last.fill(-1);
+      bool ok = true;
+      for (const DevOp& op : cl.ops) {
+        const u32 a = op.a, b = op.b, h = b - a;
+        if (op.type > OP_COPY || b <= a || b >= 64 || (h & (h - 1)) || (a & h)) { ok = false; break; }
+        const int lvl = kind == 1 ? 5 - (int)ilog(h) : (int)ilog(h);
+        if (last[a] >= lvl || last[b] >= lvl) { ok = false; break; }
+        last[a] = last[b] = lvl;
+        if (op.type != OP_COPY && op.r % unit) { ok = false; break; }
+        const u32 j = (a / (2 * h)) * h + a % h;
+        qn[lvl][j] = op.type == OP_COPY ? 0 : (int)((op.r / unit) % 64);
+      }
+      if (!ok) continue;
+      // exact evaluation: the program, then the network
+      std::vector<V> x0(64), x1;
+      u64 seed = 0x9E3779B97F4A7C15ull * (cl.key.z * 131 + cl.key.n * 7 + kind);
+      for (u32 k = 0; k < 64; ++k)
+        for (u32 d = 0; d < 32; ++d) {
+          seed = seed * 6364136223846793005ull + 1442695040888963407ull;
+          x0[k][d] = k < cl.nload ? (long long)((seed >> 33) % 2001) - 1000 : 0;
+        }
+      x1 = x0;
+      for (const DevOp& op : cl.ops) {
+        V& A = x1[op.a];
+        V& B = x1[op.b];
+        if (op.type == OP_COPY) { B = A; continue; }
+        const V rb = rot(B, (op.r / unit) % 64);
+        V s0, s1;
+        for (u32 d = 0; d < 32; ++d) {
+          s0[d] = (op.type == OP_SUB2 || op.type == OP_SUB2DIFF ? 2 * A[d] - rb[d] : A[d] + rb[d]);
+          s1[d] = A[d] - rb[d];
+        }
+        A = s0;
+        if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF) B = s1;
+      }
+      std::vector<V> y = x0;
+      for (int lvl = 0; lvl < 6; ++lvl) {
+        const u32 h = kind == 1 ? (32u >> lvl) : (1u << lvl);
+        for (u32 j = 0; j < 32; ++j) {
+          const u32 a = (j / h) * 2 * h + j % h;
+          const V rb = rot(y[a + h], (u64)std::max(0, qn[lvl][j]));
+          for (u32 d = 0; d < 32; ++d) {
+            const long long av = y[a][d];
+            y[a][d] = av + rb[d];
+            y[a + h][d] = av - rb[d];
+          }
+        }
+      }
+      for (u32 k = 0; k < cl.nstore && ok; ++k) ok = y[k] == x1[k];
+      if (!ok) continue;
+      net.assign(2 * 8 * 12, 0);
+      for (u32 st = 0; st < 2; ++st)
+        for (u32 w = 0; w < 8; ++w)
+          for (u32 o = 0; o < 12; ++o) {
+            const u32 ll = o / 4, jj = o % 4;
+            const u32 hl = kind == 1 ? (4u >> ll) : (1u << ll);
+            const u32 al = (jj / hl) * 2 * hl + jj % hl;
+            // stage slots: DIF stage 0 / DIT stage 1 take w + 8i, the others 8w + i
+            const bool strided = (kind == 1) == (st == 0);
+            const u32 a = strided ? w + 8 * al : 8 * w + al, h = strided ? 8 * hl : hl;
+            const u32 lvl = 3 * st + ll;
+            const u32 j = (a / (2 * h)) * h + a % h;
+            net[(st * 8 + w) * 12 + o] = (u32)std::max(0, qn[lvl][j]) << 16;
+          }
+      return kind;
+    }
+    return 0;
+  }
+
   // 1 / 2: the class runs as the full 8-point network of ADDSUB butterflies
   // with spans 4,2,1 (the TFT's) / 1,2,4 (the ITFT's) in level order -- the
   // warp kernel then keeps it in registers; 0: anything else.  Truncated
@@ -511,22 +633,24 @@ class Planner {
     auto rank = [&](u32 x) {
       const auto& k = keys_[x];
       if (rs_.wave_engine)  // (top phase, wave, kind): every range is independent
-        return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k), (u64)classes_[leaves_[x].cls].kind,
+        return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k), (u64)wave_kind(classes_[leaves_[x].cls]),
                                std::get<3>(k), std::get<4>(k));
       return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k) + (u64)(W - ov) * std::get<1>(k), std::get<1>(k),
                              std::get<3>(k), std::get<4>(k));
     };
     std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return rank(x) < rank(y); });
     p.waves.clear();
+    p.wide = false;
     if (rs_.wave_engine) {
       for (size_t t = 0; t < idx.size(); ++t) {
         const auto& k = keys_[idx[t]];
-        const u64 kind = classes_[leaves_[idx[t]].cls].kind;
+        const u64 kind = wave_kind(classes_[leaves_[idx[t]].cls]);
         if (t == 0 || std::get<0>(keys_[idx[t - 1]]) != std::get<0>(k) ||
             std::get<2>(keys_[idx[t - 1]]) != std::get<2>(k) || p.waves.back()[2] != kind)
           p.waves.push_back({(u64)t, 0, kind, 0});
         p.waves.back()[1] += 1;
-        if (kind == 1) {  // a warp takes 2^(6 - ell) cosets of all positions (wave_coset.cuh)
+        if (kind == 2) p.wide = true;
+        if (kind >= 1) {  // a warp row takes 2^(6 - ell) cosets of all positions (wave_coset.cuh, wave_wide.cuh)
           const LeafProgram& c = classes_[leaves_[idx[t]].cls];
           const u64 groups = std::max<u64>(1, (u64)c.step >> (6 - c.key.ell));
           p.waves.back()[3] = std::max(p.waves.back()[3], groups);
@@ -550,6 +674,13 @@ class Planner {
   // Split for a node: the reference's policy at the top (transform.hpp:83-87),
   // an SMEM-sized near-balanced split below it.
   void split(unsigned ell, int policy, bool top, unsigned& l1, unsigned& l2) const {
+    if (top && rs_.wide && !policy_everywhere_ && ell > 6) {
+      // any split gives the same outputs (transform_test.cpp:248-272): the
+      // row nodes get 2^(6k) coefficients (radix-64 passes), the columns the rest
+      l1 = ell - 6 * ((ell - 1) / 6);
+      l2 = ell - l1;
+      return;
+    }
     if (top || policy_everywhere_) {
       if (policy == 1) {
         l1 = 1;
@@ -887,7 +1018,9 @@ class Planner {
       prog.cs = rs_.C;
       prog.slot_bytes = rs_.slot_bytes;
     }
-    max_area_ = std::max<u64>(max_area_, L * prog.slot_bytes);
+    // shared memory of the persistent leaf kernel (the wave engine runs coset
+    // classes on its own kernels)
+    if (!(rs_.wave_engine && k.kind == 1)) max_area_ = std::max<u64>(max_area_, L * prog.slot_bytes);
     u32 id = (u32)classes_.size();
     classes_.push_back(std::move(prog));
     class_index_[k] = id;

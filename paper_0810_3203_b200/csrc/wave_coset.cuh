@@ -37,12 +37,65 @@ struct WaveArgs {
   u64 tloc;
   const u64* locbits;
   const u32* wops;      // packed micro-ops (Plan::wave_ops)
+  const u32* levels;    // class level tables (absolute op indices; coset_wide_kernel)
   const u32* wslots;    // per-slot {pre, post} lane rotations | buffer bits (Plan::wave_slots)
   u32 lanes;            // lanes per coefficient (C)
   u32 D;                // u32 words per coefficient
   u64 M;
   u32 gpl;              // work items per ticket: its most warp groups (Plan::waves)
+  u32 logS, logLanes;   // tops-array lane interleave (fermat_leaf.cuh, tops_ix)
+  u32 debug;            // CFTFT_DEBUG_SKIP bits (experiments; results wrong when set)
 };
+__device__ __forceinline__ u32 wave_tix(const WaveArgs& A, u32 p) {
+  return ((p & ((1u << A.logS) - 1)) << (A.logLanes - A.logS)) | (p >> A.logS);
+}
+
+
+// y0 = a + s b, y1 = a - s b with s = (-1)^neg varying per lane, branch-free:
+// -(B + tb 2^CB) = (B ^ ~0) + 1 + (tb ^ ~0) 2^CB, so with x = B ^ m, tx = tb ^ m
+// (m = neg ? ~0 : 0), y0 = a + x + neg and y1 = a - x - neg as carry chains
+// with a carry / borrow in.
+__device__ __forceinline__ void ch_pm8(Ch<8>& y0, int& t0, Ch<8>& y1, int& t1, const Ch<8>& a, int ta,
+                                       const Ch<8>& b, int tb, bool neg) {
+  const u32 m = neg ? ~0u : 0u, ci = neg ? 1u : 0u;
+  Ch<8> x;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) x.w[w] = b.w[w] ^ m;
+  const int tx = tb ^ (int)m;
+  u32 c0, c1, d0, d1;
+  asm("add.cc.u32 %9, %10, -1;\n\t"
+      "addc.cc.u32 %0, %11, %19;\n\t"
+      "addc.cc.u32 %1, %12, %20;\n\t"
+      "addc.cc.u32 %2, %13, %21;\n\t"
+      "addc.cc.u32 %3, %14, %22;\n\t"
+      "addc.cc.u32 %4, %15, %23;\n\t"
+      "addc.cc.u32 %5, %16, %24;\n\t"
+      "addc.cc.u32 %6, %17, %25;\n\t"
+      "addc.cc.u32 %7, %18, %26;\n\t"
+      "addc.u32 %8, 0, 0;"
+      : "=r"(y0.w[0]), "=r"(y0.w[1]), "=r"(y0.w[2]), "=r"(y0.w[3]), "=r"(y0.w[4]), "=r"(y0.w[5]), "=r"(y0.w[6]),
+        "=r"(y0.w[7]), "=r"(c0), "=r"(d0)
+      : "r"(ci), "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]),
+        "r"(a.w[7]), "r"(x.w[0]), "r"(x.w[1]), "r"(x.w[2]), "r"(x.w[3]), "r"(x.w[4]), "r"(x.w[5]), "r"(x.w[6]),
+        "r"(x.w[7]));
+  asm("sub.cc.u32 %9, 0, %10;\n\t"
+      "subc.cc.u32 %0, %11, %19;\n\t"
+      "subc.cc.u32 %1, %12, %20;\n\t"
+      "subc.cc.u32 %2, %13, %21;\n\t"
+      "subc.cc.u32 %3, %14, %22;\n\t"
+      "subc.cc.u32 %4, %15, %23;\n\t"
+      "subc.cc.u32 %5, %16, %24;\n\t"
+      "subc.cc.u32 %6, %17, %25;\n\t"
+      "subc.cc.u32 %7, %18, %26;\n\t"
+      "subc.u32 %8, 0, 0;"
+      : "=r"(y1.w[0]), "=r"(y1.w[1]), "=r"(y1.w[2]), "=r"(y1.w[3]), "=r"(y1.w[4]), "=r"(y1.w[5]), "=r"(y1.w[6]),
+        "=r"(y1.w[7]), "=r"(c1), "=r"(d1)
+      : "r"(ci), "r"(a.w[0]), "r"(a.w[1]), "r"(a.w[2]), "r"(a.w[3]), "r"(a.w[4]), "r"(a.w[5]), "r"(a.w[6]),
+        "r"(a.w[7]), "r"(x.w[0]), "r"(x.w[1]), "r"(x.w[2]), "r"(x.w[3]), "r"(x.w[4]), "r"(x.w[5]), "r"(x.w[6]),
+        "r"(x.w[7]));
+  t0 = ta + tx + (int)c0;
+  t1 = ta - tx + (int)c1;
+}
 
 constexpr int kWaveWarps = 4;  // warps per CTA, at most (the launch may use fewer)
 
@@ -200,7 +253,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
         for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
-        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + lnA);
+        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + wave_tix(A, lnA));
         if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
@@ -214,7 +267,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             const u32 xo = (u32)__cvta_generic_to_shared(xrow(k, pos));
 #pragma unroll
             for (int x = 0; x < CW / 4; ++x) cp_async16(xo + 16u * x, el + (u64)lnB * (CB / 8) + 16u * x);
-            cp_async4(xo + 4u * CW, tr + lnB);
+            cp_async4(xo + 4u * CW, tr + wave_tix(A, lnB));
           }
         }
       }
@@ -315,7 +368,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
 #pragma unroll
         for (int q = 0; q < CW / 4; ++q)
           __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
-        __stcg(sk->tout + d, top);
+        __stcg(sk->tout + wave_tix(A, d), top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
         const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
@@ -330,7 +383,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         //      the two 4-point halves in registers, and outputs go straight
         //      from registers to global memory.
         auto bfly = [&](Ch<CW>& a, int& ta, Ch<CW>& b, int& tb, u32 oi) {
-          const u32 qv = __shfl_sync(0xffffffffu, opv0, (int)oi) >> 12;
+          const u32 qv = __shfl_sync(0xffffffffu, opv0, (int)oi) >> 16;
           Ch<CW> y0;
           int t0;
           if (qv == 0) {  // warp-uniform
@@ -347,13 +400,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
 #pragma unroll
             for (int w = 0; w < CW; ++w) bp.w[w] = __shfl_sync(0xffffffffu, b.w[w], (int)pl);
             const int tbp = __shfl_sync(0xffffffffu, tb, (int)pl);
-            if (!neg) {
-              t0 = ch_add(y0, a, bp) + ta + tbp;
-              tb = ch_sub(b, a, bp) + ta - tbp;
-            } else {
-              t0 = ch_sub(y0, a, bp) + ta - tbp;
-              tb = ch_add(b, a, bp) + ta + tbp;
-            }
+            ch_pm8(y0, t0, b, tb, a, ta, bp, tbp, neg);
           }
           a = y0;
           ta = t0;
@@ -440,7 +487,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         const u32 wop = __shfl_sync(0xffffffffu, opv, (int)(o & 31));
         struct {
           u32 type, a, b, q;
-        } op{wop & 15u, (wop >> 4) & 15u, (wop >> 8) & 15u, wop >> 12};
+        } op{wop & 15u, (wop >> 4) & 63u, (wop >> 10) & 63u, wop >> 16};
         Ch<CW> a, b, y0, y1;
         int pa = 0, pb = 0, t0 = 0, t1 = 0;
         if (act) {
@@ -456,13 +503,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             const bool neg = ((pos < qq) ? 1u : 0u) != sneg;
             pb = ld(b, op.b, pl);
             // y0 = a + s b, y1 = a - s b with s = (-1)^neg
-            if (!neg) {
-              t0 = ch_add(y0, a, b) + pa + pb;
-              t1 = ch_sub(y1, a, b) + pa - pb;
-            } else {
-              t0 = ch_sub(y0, a, b) + pa - pb;
-              t1 = ch_add(y1, a, b) + pa + pb;
-            }
+            ch_pm8(y0, t0, y1, t1, a, pa, b, pb, neg);
             if (op.type == OP_SUB2 || op.type == OP_SUB2DIFF) t0 = ch_add(y0, a, y1) + pa + t1;
           }
         }

@@ -146,7 +146,22 @@ def run_plan_fermat(plan, N, vals):
             assert not coset or e % lane == 0 or wplan
             slot[i] = (x[(buf(locoff, i, False), base + i * stride)] * pow(2, e, P)) % P
         ops = c["ops"]
-        if c.get("wnet"):
+        if c.get("net"):
+            # the CTA kernel's radix-64 network (wave_wide.cuh): two stages of
+            # eight 8-point networks, (stage, warp, op) -> butterfly
+            for i in range(c["nload"], 64):
+                slot[i] = 0
+            ops, unit, dif = [], M >> 6, c["wnet"] == 1
+            for st in range(2):
+                for w in range(8):
+                    for o in range(12):
+                        ll, jj = divmod(o, 4)
+                        hl = (4 >> ll) if dif else (1 << ll)
+                        al = (jj // hl) * 2 * hl + jj % hl
+                        strided = dif == (st == 0)
+                        a, h = (w + 8 * al, 8 * hl) if strided else (8 * w + al, hl)
+                        ops.append((0, a, a + h, c["net"][(st * 8 + w) * 12 + o] * unit))
+        elif c.get("wnet"):
             # the warp kernel runs these as the full ADDSUB network (spans 4,2,1
             # or 1,2,4) on zero-filled truncated inputs, storing outputs < n
             for i in range(c["nload"], 8):
@@ -194,10 +209,10 @@ def run_plan_fermat(plan, N, vals):
     return out
 
 
-def check_plan(ctx, N, rnd, trials):
+def check_plan(ctx, N, rnd, trials, lmin=1, lmax=8):
     fm = bm.FermatModel(N)
     for _ in range(trials):
-        L = 1 << rnd.randint(1, 8)
+        L = 1 << rnd.randint(lmin, lmax)
         z, n = rnd.randint(1, L), rnd.randint(1, L)
         s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
         a = [rnd.randrange((1 << N) + 1) for _ in range(z)]
@@ -224,6 +239,28 @@ def test_gpu_schedule_reproduces_definition(limit):
         ctx = cf.FermatRingCtx(N)
         ctx.set_leaf_limit(limit)
         check_plan(ctx, N, rnd, 40)
+
+
+def test_wide_schedule_reproduces_definition():
+    """Radix-64 coset leaves (coset_wide_kernel): the reshaped top split, the
+    full 64-point networks (incl. truncated TFT leaves on zero-filled inputs)
+    and the generic 16..64-slot programs."""
+    rnd = random.Random(7)
+    N = 8192
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_wide(1)
+    seen = set()
+    for _ in range(14):
+        L = 1 << rnd.randint(6, 9)
+        z, n = rnd.randint(1, L), rnd.randint(1, L)
+        s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
+        for inv in (False, True):
+            plan = cf.plan_dump(ctx, inv, cf.TransformParams(L, s, z, n if not inv else min(n, z)), pol)
+            for c in plan["classes"]:
+                if c["kind"] == 1 and c["ell"] >= 4:
+                    seen.add("net" if c.get("net") else "generic")
+    check_plan(ctx, N, random.Random(8), 10, 6, 9)
+    assert seen == {"net", "generic"}, seen
 
 
 @pytest.mark.parametrize("limit", [0, 2, 3])

@@ -98,11 +98,14 @@ def test_c2_itft_sweep(c2):
                 del dev
 
 
-def test_c5_full_transform_and_round_trip():
+@pytest.mark.parametrize("wide", [0, 1])
+def test_c5_full_transform_and_round_trip(wide):
     """C5: Z/(2^131072+1), L = 2^18, z = n = 200000: GPU TFT bit-exact vs the
-    oracle, GPU ITFT of it = L * a, base-case counts as pinned."""
+    oracle, GPU ITFT of it = L * a, base-case counts as pinned (radix-8 warp
+    engine and radix-64 CTA engine)."""
     N, L, z = 131072, 1 << 18, 200000
     ctx = cf.FermatRingCtx(N)
+    ctx.set_wide(wide)
     ring = po.Ring.fermat(N)
     lim = N // 64
     a = _limbs(N, L, z, ctx.element_words, po.mix_seed(42, 5))

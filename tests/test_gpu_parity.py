@@ -297,3 +297,23 @@ def test_fermat_coset_large_elements(N, L, z, n):
     _fermat_case(ctx, ring, N, L, z, n, 0, 0, seed=N + z)
     _fermat_case(ctx, ring, N, L, min(z, n), min(z, n), 0, 0, seed=N + n, inverse=True, f=0)
     _fermat_case(ctx, ring, N, L, z, n // 2, 5, 1, seed=N + 1, inverse=True, f=1)
+
+
+@pytest.mark.parametrize("N", [8192, 32768])
+def test_fermat_wide_sweep(N):
+    """Radix-64 coset leaves on the CTA kernel (set_wide(1)): full 64-point
+    networks, truncated TFT networks, generic 16..64-slot programs, unaligned
+    pre-rotations from deferred twiddles, against the oracle."""
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_wide(1)
+    ring = po.Ring.fermat(N)
+    rnd = random.Random(N + 64)
+    for trial in range(10):
+        L = 1 << rnd.randint(6, 11)
+        z, n = rnd.randint(1, L), rnd.randint(1, L)
+        s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
+        _fermat_case(ctx, ring, N, L, z, n, s, pol, seed=trial, special=(trial % 3 == 0))
+        n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+        if 1 <= n2 + f <= L:
+            _fermat_case(ctx, ring, N, L, z, n2, s, pol, seed=700 + trial, inverse=True, f=f,
+                         special=(trial % 3 == 1))
