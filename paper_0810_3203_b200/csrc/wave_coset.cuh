@@ -97,6 +97,43 @@ __device__ __forceinline__ void ch_pm8(Ch<8>& y0, int& t0, Ch<8>& y1, int& t1, c
   t1 = ta - tx + (int)c1;
 }
 
+
+// Sub-lane part of a rotation by o = 32 OW + sh bits (0 < o < 256), for one
+// lane of the result: bits [256 - o, 512 - o) of (B ++ A) -- A the source
+// lane, B the lane below it -- plus B's top tb shifted to bit o; returns the
+// result's top.  One specialisation per word offset OW (o is warp-uniform):
+// the window and the shifted top are compile-time register picks.
+template <int OW>
+__device__ __forceinline__ int unal_ow8(Ch<8>& out, const Ch<8>& b, const Ch<8>& a, int tb, u32 sh) {
+  u32 W[16];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    W[m] = b.w[m];
+    W[8 + m] = a.w[m];
+  }
+#pragma unroll
+  for (int x = 0; x < 8; ++x) out.w[x] = __funnelshift_l(W[7 - OW + x], W[8 - OW + x], sh);
+  const long long pw = (long long)tb * (1ll << sh);  // |tb| < 2^31: fits
+  const u32 lo = (u32)pw, hi = (u32)((unsigned long long)pw >> 32), ext = (u32)(tb >> 31);
+  Ch<8> P;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) P.w[k] = k < OW ? 0u : (k == OW ? lo : (k == OW + 1 ? hi : ext));
+  return ch_add<8>(out, out, P) + (OW == 7 ? (int)hi : (int)ext);
+}
+__device__ __forceinline__ int unal_combine8(Ch<8>& out, const Ch<8>& b, const Ch<8>& a, int tb, u32 o) {
+  const u32 sh = o & 31;
+  switch (o >> 5) {
+    case 0: return unal_ow8<0>(out, b, a, tb, sh);
+    case 1: return unal_ow8<1>(out, b, a, tb, sh);
+    case 2: return unal_ow8<2>(out, b, a, tb, sh);
+    case 3: return unal_ow8<3>(out, b, a, tb, sh);
+    case 4: return unal_ow8<4>(out, b, a, tb, sh);
+    case 5: return unal_ow8<5>(out, b, a, tb, sh);
+    case 6: return unal_ow8<6>(out, b, a, tb, sh);
+    default: return unal_ow8<7>(out, b, a, tb, sh);
+  }
+}
+
 constexpr int kWaveWarps = 4;  // warps per CTA, at most (the launch may use fewer)
 
 // per warp: data rows [slot][lane] of CW words, their 16-byte halves swapped
@@ -315,13 +352,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           } else {
             tb = ld(b, k, lane - 1);
           }
-          u32 X[CW + 1];
-          pick_window_rt<CW>(X, b, a, o >> 5);
-#pragma unroll
-          for (int x = 0; x < CW; ++x) out.w[x] = __funnelshift_l(X[x], X[x + 1], o & 31);
-          Ch<CW> P;
-          const int ptop = small_shifted<CW>(P, tb, o);
-          otop = ch_add(out, out, P) + ptop;
+          otop = unal_combine8(out, b, a, tb, o);
           if (L0 == 0) {
             // Lane 0's B is lane C-1's A seen through 2^N == -1: the split of
             // -v must be -(split of v), and floor(-v 2^o / 2^Λ) is one short

@@ -241,13 +241,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
             } else {
               tb = ld(b, k, lane - 1);
             }
-            u32 X[CW + 1];
-            pick_window_rt<CW>(X, b, a, o >> 5);
-#pragma unroll
-            for (int x = 0; x < CW; ++x) out.w[x] = __funnelshift_l(X[x], X[x + 1], o & 31);
-            Ch<CW> P;
-            const int ptop = small_shifted<CW>(P, tb, o);
-            otop = ch_add(out, out, P) + ptop;
+            otop = unal_combine8(out, b, a, tb, o);
             if (L0 == 0) {
               // lane 0's B is lane C-1's A seen through 2^N == -1 (wave_coset.cuh)
               const u32 nbits = CB - o;
