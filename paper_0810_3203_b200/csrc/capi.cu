@@ -568,14 +568,16 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         const size_t wsmem = (size_t)wwarps * fermat::wave_tile_words<8>() * 4;
         static bool wave_attr = false;
         if (!wave_attr) {
-          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)wsmem));
+          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
           wave_attr = true;
         }
         int dev = 0, sms = 0, per = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8>, 32 * wwarps, wsmem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8, false>, 32 * wwarps, wsmem));
         const size_t xsmem = (size_t)fermat::wide_tile_words<8>() * 4;
         int xper = 0;
         if (dp.host.wide) {
@@ -600,7 +602,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.nleaves = (u32)wr[1];
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             const unsigned g = (unsigned)std::min<u64>((wr[1] * W.gpl + wwarps - 1) / wwarps, (u64)sms * std::max(per, 1));
-            fermat::coset_wave_kernel<8><<<g, 32 * wwarps, wsmem, st>>>(W);
+            if (W.logS)
+              fermat::coset_wave_kernel<8, true><<<g, 32 * wwarps, wsmem, st>>>(W);
+            else
+              fermat::coset_wave_kernel<8, false><<<g, 32 * wwarps, wsmem, st>>>(W);
           } else {
             CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(u32), st));  // ticket counter of this range
             A.leaves = dp.leaves + wr[0];

@@ -158,8 +158,11 @@ __host__ __device__ constexpr u32 wave_tile_words() {
   return 8u * 32u * CW + 8u * 32u + 16u + 8u * 4u * wave_xrow_words<CW>() + 8u * (sizeof(WaveSlot) / 4);
 }
 
-template <int CW>
+// TIX: the tops arrays are lane-interleaved (wide plans, A.logS > 0); the
+// radix-8 plans keep natural lane order and skip the index mapping
+template <int CW, bool TIX>
 __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs A) {
+  auto tix = [&](u32 p) -> u32 { return TIX ? wave_tix(A, p) : p; };
   static_assert(CW == 8, "the wave engine runs 256-bit lanes");
   extern __shared__ __align__(16) u32 wsm[];
   constexpr u32 CB = 32 * CW;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
         for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
-        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + wave_tix(A, lnA));
+        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + tix(lnA));
         if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             const u32 xo = (u32)__cvta_generic_to_shared(xrow(k, pos));
 #pragma unroll
             for (int x = 0; x < CW / 4; ++x) cp_async16(xo + 16u * x, el + (u64)lnB * (CB / 8) + 16u * x);
-            cp_async4(xo + 4u * CW, tr + wave_tix(A, lnB));
+            cp_async4(xo + 4u * CW, tr + tix(lnB));
           }
         }
       }
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
 #pragma unroll
         for (int q = 0; q < CW / 4; ++q)
           __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
-        __stcg(sk->tout + wave_tix(A, d), top);
+        __stcg(sk->tout + tix(d), top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
         const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
