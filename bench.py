@@ -504,13 +504,16 @@ def main():
         elem = ctx.element_bytes
         pin_in = torch.from_numpy(host.view(np.int64)).pin_memory()
         pin_out = torch.empty_like(pin_in).pin_memory()
-        ek = max(3, min(args.steps, 10))
-        # a stream of independent transforms, double buffered: step k's
+        ek = max(16, args.steps)  # steady state: the pipeline fill and drain amortised
+        # a stream of independent transforms, triple buffered: step k's
         # host->device copy (its own stream) overlaps step k-1's transforms and
-        # step k-2's device->host copy (a third stream); every step copies its
-        # z inputs in and its n outputs out
-        bufs = [dev, torch.empty_like(dev)]
-        views = [view, cf.DeviceView(bufs[1])]
+        # step k-2's device->host copy (a third stream; PCIe runs both
+        # directions at once); every step copies its z inputs in and its n
+        # outputs out.  Three buffers keep the H2D stream busy: buffer k % 3 is
+        # free once step k-3's outputs are out.
+        NB = 3
+        bufs = [dev] + [torch.empty_like(dev) for _ in range(NB - 1)]
+        views = [view] + [cf.DeviceView(b) for b in bufs[1:]]
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ev_in = [torch.cuda.Event() for _ in range(ek)]
         ev_done = [torch.cuda.Event() for _ in range(ek)]
@@ -518,10 +521,10 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for k in range(ek):
-            b = k % 2
+            b = k % NB
             with torch.cuda.stream(s_in):
-                if k >= 2:
-                    s_in.wait_event(ev_out[k - 2])  # buffer b is free again
+                if k >= NB:
+                    s_in.wait_event(ev_out[k - NB])  # buffer b is free again
                 bufs[b][:z].copy_(pin_in[:z], non_blocking=True)
                 ev_in[k].record(s_in)
             stream.wait_event(ev_in[k])
@@ -535,11 +538,11 @@ def main():
         torch.cuda.synchronize()
         barrier()
         dt = (time.perf_counter() - t0) / ek
-        del bufs[1], views[1]
+        del bufs[1:], views[1:]
         e2e = {"value": world * byts / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": z * elem,
                "d2h_bytes_per_step": n * elem, "steps": ek,
                "note": "per step: pinned host -> HBM copy of the z inputs, TFT+ITFT through the public API, "
-                       "HBM -> pinned copy of the n outputs; double-buffered streams overlap consecutive steps"}
+                       "HBM -> pinned copy of the n outputs; triple-buffered streams overlap consecutive steps"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
     cpu = None
