@@ -1097,17 +1097,20 @@ class Planner {
           } else {  // (2x0, zeta x0)
             e.push(OP_COPY, i, j, 0, true);
             e.P[j] = e.P[i] + s;
+            // the doubling as arithmetic (x0 + x0), not as a pending 1-bit
+            // rotation: lane-local, so it never makes a later rotation (or
+            // the element's final value) sub-lane
             if (fermat)
-              e.P[i] = e.P[i] + 1;
+              e.push(OP_ADD, i, i, 0, true);
             else
               e.push(OP_DBL, i, i, 0, false);
           }
         } else {
           if (z == 2) {  // 2x0 - x1
             e.push(OP_SUB2, i, j, e.P[j] - e.P[i], true);
-          } else {  // 2x0
+          } else {  // 2x0 (as x0 + x0, see above)
             if (fermat)
-              e.P[i] = e.P[i] + 1;
+              e.push(OP_ADD, i, i, 0, true);
             else
               e.push(OP_DBL, i, i, 0, false);
           }
