@@ -305,6 +305,7 @@ class Planner {
     class_index_.clear();
     classes_.clear();
     progs_.clear();
+    lin_progs_.clear();
     leaves_.clear();
     keys_.clear();
     counters_.clear();
@@ -905,7 +906,7 @@ class Planner {
     boundary(bnd, inv, ell, base, stride, lf);
     if (coset_fits(ell)) {
       const ClassKey key{inv ? 1 : 0, ell, z, n, f, 1};
-      const LeafProgram& prog = program(key, policy);
+      const LeafProgram& prog = coset_program(key, policy);
       if (aligned(prog, inv, ell, lf)) {
         units = emit_coset(key, policy, base, stride, cx, wave0, lf);
         return true;
@@ -995,10 +996,117 @@ class Planner {
     return it->second;
   }
 
+  // The program a coset leaf runs: the leaf program, or -- when its op
+  // rotations are not lane aligned (the ITFT's halvings) and the wave engine
+  // takes sub-lane pre-rotations -- its linear form, if it has one.
+  const LeafProgram& coset_program(ClassKey k, int policy) {
+    k.kind = 0;
+    auto it = lin_progs_.find(k);
+    if (it != lin_progs_.end()) return it->second;
+    const LeafProgram& src = program(k, policy);
+    LeafProgram lin;
+    const u64 inner = rs_.M >> k.ell;
+    bool al = true;
+    for (const auto& op : src.ops) al = al && (op.type == OP_COPY || op.r % inner == 0);
+    const bool use = !al && rs_.wave_engine && rs_.wave_unaligned && rs_.fermat && linearize(src, lin);
+    return lin_progs_.emplace(k, use ? lin : src).first->second;
+  }
+
+  // A one-output program whose output is a sum of +-omega^e multiples of its
+  // (loaded) inputs, each input in at most one term, as that sum: the inputs
+  // pre-rotated by their e (any bits: the wave kernel's sub-lane loads), then
+  // added with rotation 0 (lane aligned).  The program's ops are replayed on
+  // symbolic stored values -- lists of (input, exponent) -- with the kernel's
+  // semantics (ADD a += R b, ADDSUB, SUB2 a = 2a - R b, SUB2DIFF, COPY b = a;
+  // 2 = omega^1, -1 = omega^(M/2)).  False: not such a program.
+  bool linearize(const LeafProgram& src, LeafProgram& dst) const {
+    if (src.nstore != 1 || src.nload == 0) return false;
+    const u64 M = rs_.M, H = M / 2;
+    const u32 L = 1u << src.key.ell;
+    using Terms = std::vector<std::pair<u32, u64>>;
+    std::vector<Terms> t(L);
+    for (u32 k = 0; k < src.nload; ++k) t[k].push_back({k, 0});
+    bool ok = true;
+    auto add_into = [&](Terms acc, const Terms& x, u64 sh) {
+      for (const auto& [in, e0] : x) {
+        const u64 e = (e0 + sh) & (M - 1);
+        auto it = std::find_if(acc.begin(), acc.end(), [&](const auto& q) { return q.first == in; });
+        if (it == acc.end()) {
+          acc.push_back({in, e});
+        } else if (it->second == e) {
+          it->second = (e + 1) & (M - 1);  // 2 omega^e
+        } else if (it->second == ((e + H) & (M - 1))) {
+          acc.erase(it);  // cancels
+        } else {
+          ok = false;
+        }
+      }
+      return acc;
+    };
+    auto shifted = [&](const Terms& x, u64 sh) {
+      Terms r = x;
+      for (auto& q : r) q.second = (q.second + sh) & (M - 1);
+      return r;
+    };
+    for (const DevOp& op : src.ops) {
+      const u32 a = op.a, b = op.b;
+      switch (op.type) {
+        case OP_ADD: t[a] = add_into(t[a], t[b], op.r); break;
+        case OP_COPY: t[b] = t[a]; break;
+        case OP_ADDSUB: {
+          Terms ta = add_into(t[a], t[b], op.r), tb = add_into(t[a], t[b], op.r + H);
+          t[a] = std::move(ta);
+          t[b] = std::move(tb);
+          break;
+        }
+        case OP_SUB2: t[a] = add_into(shifted(t[a], 1), t[b], op.r + H); break;
+        case OP_SUB2DIFF: {
+          Terms ta = add_into(shifted(t[a], 1), t[b], op.r + H), tb = add_into(t[a], t[b], op.r + H);
+          t[a] = std::move(ta);
+          t[b] = std::move(tb);
+          break;
+        }
+        default: return false;
+      }
+      if (!ok) return false;
+    }
+    const Terms& out = t[0];
+    if (out.empty()) return false;
+    dst = LeafProgram{};
+    dst.key = src.key;
+    dst.nload = src.nload;
+    dst.nstore = 1;
+    dst.pre = src.pre;
+    dst.post = src.post;
+    dst.has_pre = true;
+    Emit e;
+    e.M = M;
+    e.last.assign(L, 0);
+    e.P.assign(L, 0);
+    bool has0 = false;
+    for (const auto& [in, ex] : out) {
+      dst.pre[in].b = (dst.pre[in].b + ex) & (M - 1);
+      has0 = has0 || in == 0;
+    }
+    if (!has0) e.push(OP_COPY, out[0].first, 0, 0, true);
+    for (const auto& [in, ex] : out)
+      if (in != 0 && (has0 || in != out[0].first)) e.push(OP_ADD, 0, in, 0, true);
+    u32 nlev = 0;
+    for (auto& r : e.ops) nlev = std::max(nlev, r.level);
+    for (auto& r : e.ops) dst.ops.push_back(r.op);  // emitted in level order (a chain on slot 0)
+    dst.level_begin.assign(nlev + 1, 0);
+    size_t idx = 0;
+    for (u32 l = 0; l <= nlev; ++l) {
+      while (idx < e.ops.size() && e.ops[idx].level <= l) ++idx;
+      dst.level_begin[l] = (u32)idx;
+    }
+    return true;
+  }
+
   u32 class_of(const ClassKey& k, int policy) {
     auto it = class_index_.find(k);
     if (it != class_index_.end()) return it->second;
-    LeafProgram prog = program(k, policy);
+    LeafProgram prog = k.kind == 1 ? coset_program(k, policy) : program(k, policy);
     prog.key = k;
     const u64 L = u64{1} << k.ell;
     prog.kind = (u32)k.kind;
@@ -1214,6 +1322,7 @@ class Planner {
   bool policy_everywhere_ = false;
   std::map<ClassKey, u32> class_index_;
   std::map<ClassKey, LeafProgram> progs_;
+  std::map<ClassKey, LeafProgram> lin_progs_;  // coset_program
   std::vector<LeafProgram> classes_;
   std::vector<DevLeaf> leaves_;
   std::vector<Key> keys_;
