@@ -17,10 +17,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "ncu launches rc=$?"
 for w in tft itft; do
   timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:"leaf_kernel|coset_wave" --csv --log-file gpurun_out/traffic_${TAG}_c5_$w.csv python tools/prof_one.py C5 $w \
+    -k regex:"leaf_kernel|coset_wave|fold" --csv --log-file gpurun_out/traffic_${TAG}_c5_$w.csv python tools/prof_one.py C5 $w \
     > gpurun_out/ncu_traffic_${TAG}_$w.log 2>&1; echo "ncu traffic $w rc=$?"
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:leaf_kernel -c 1 -f -o gpurun_out/full_${TAG}_c5tft \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:coset_wave -s 3 -c 1 -f -o gpurun_out/full_${TAG}_c5tft_unal \
   python tools/prof_one.py C5 tft > gpurun_out/ncu_full_${TAG}.log 2>&1; echo "ncu full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:coset_wave -c 1 -f -o gpurun_out/full_${TAG}_c5tft_wave \
   python tools/prof_one.py C5 tft > gpurun_out/ncu_full_wave_${TAG}.log 2>&1; echo "ncu full wave rc=$?"
