@@ -511,7 +511,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         tops = static_cast<int*>(sc->tops);
         shadow = static_cast<std::uint8_t*>(sc->shadow);
         ht.mark("scratch");
-        CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
+        // wave plans load no tops of elements they have not written (Plan::tops_clear)
+        if (dp.host.tops_clear) CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
       }
       A.T = tops;
       A.data2 = shadow;

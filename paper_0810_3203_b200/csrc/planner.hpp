@@ -185,8 +185,9 @@ struct Plan {
   std::vector<u32> wave_ops;
   std::vector<u32> wave_op_begin;  // per class
   std::vector<u32> wave_net;       // per class, DevClass::wnet
-  // wave engine, coset tickets: per slot {pre bits | in-buffer << 31,
+  // wave engine, coset tickets: per slot {pre bits | fresh << 30 | in-buffer << 31,
   // post lanes | final output << 30 | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
+  // fresh: the element was never written by the plan before (its tops are zero, not loaded);
   // whole tickets with deferred rotations on their inputs: per loaded slot
   // the extra pre-rotation bits, at DevLeaf::c0 - 1 (c0 = 0: none)
   std::vector<u32> wave_slots;
@@ -194,6 +195,9 @@ struct Plan {
   // element [0, extent), applied by the final fold (empty: none)
   std::vector<u32> final_rot;
   bool wide = false;  // some waves run on coset_wide_kernel (kind 2)
+  // the tops arrays must start zeroed: some kernel reads the tops of an
+  // element the plan has not written (wave plans: whole leaves only)
+  bool tops_clear = true;
 };
 
 // Ring-dependent planning parameters.
@@ -273,6 +277,7 @@ class Planner {
       for (u64 k = 0; k < it.n + (u64)(inverse ? it.f : 0); ++k) finals.push_back(it.base + k * it.stride);
     finish(p, finals);
     p.final_count = 0;  // caller canonicalises
+    p.tops_clear = true;  // the fold visits every element in [0, extent), written or not
     return p;
   }
 
@@ -424,12 +429,16 @@ class Planner {
     p.final_rot.clear();
     std::vector<u32> pend(extent_, 0);
     std::vector<u64> last(extent_, ~u64{0});  // wave_slots index of the element's last coset write
+    std::vector<std::uint8_t> written(extent_, 0);  // tops rows valid (written by a leaf)
+    p.tops_clear = false;
     for (auto& lf : leaves_) {
       const LeafProgram& cl = classes_[lf.cls];
       const bool inv = cl.key.inverse != 0;
       if (cl.kind != 1) {
         bool any = false;
         for (u32 k = 0; k < cl.nload; ++k) any |= pend[lf.base + (u64)k * lf.stride] != 0;
+        for (u32 k = 0; k < cl.nload; ++k) p.tops_clear = p.tops_clear || !written[lf.base + (u64)k * lf.stride];
+        for (u32 k = 0; k < cl.nstore; ++k) written[lf.base + (u64)k * lf.stride] = 1;  // tops rows zeroed
         if (any) {
           lf.c0 = (u32)p.wave_slots.size() + 1;
           for (u32 k = 0; k < cl.nload; ++k) p.wave_slots.push_back(pend[lf.base + (u64)k * lf.stride]);
@@ -448,7 +457,9 @@ class Planner {
         if (k < cl.nload) {
           const u64 r = cl.pre[k].a * lf.s + cl.pre[k].b + ((inv && k < cl.key.n) ? lf.tpre : 0) + pend[e];
           pre = (u32)(r & (M - 1));  // bits: the warp kernel takes unaligned pre-rotations
+          if (!written[e]) pre |= 1u << 30;
         }
+        if (k < cl.nstore) written[e] = 1;
         if (k < cl.nstore) {
           const bool tp = inv ? (cl.key.f && k == cl.key.n) : true;
           const u64 r = (cl.post[k].a * lf.s + cl.post[k].b + (tp ? lf.tpost : 0)) & (M - 1);

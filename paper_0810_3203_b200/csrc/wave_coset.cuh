@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
     __syncwarp();
     const u32 pre_l = lane < cl.nload ? A.wslots[lf.c0 + 2 * lane] : 0u;
     // any unaligned pre-rotation in the ticket (warp-uniform)
-    const bool tunal = __any_sync(0xffffffffu, ((pre_l & 0x7FFFFFFFu) % CB) != 0);
+    const bool tunal = __any_sync(0xffffffffu, ((pre_l & 0x3FFFFFFFu) % CB) != 0);
     if (lane < span) {
       const u32 pre = A.wslots[lf.c0 + 2 * lane], post = A.wslots[lf.c0 + 2 * lane + 1];
       const u64 e = lf.base + (u64)lane * lf.stride;
@@ -284,16 +284,20 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
 #pragma unroll
       for (u32 k = 0; k < 8; ++k) {
         if (!act || k >= cl.nload) break;
-        const u32 r = si[k].pre & 0x7FFFFFFFu;
+        const u32 r = si[k].pre & 0x3FFFFFFFu;
         const u32 q = r / CB, o = r % CB;
         const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
         const u32 lnA = srcA & (CL - 1);
         const std::uint8_t* el = si[k].in;
         const int* tr = si[k].tin;
+        const bool fresh = (si[k].pre >> 30) & 1u;  // never written: tops are zero
         const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
         for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
-        cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + tix(lnA));
+        if (fresh)
+          tops[k * 32u + lane] = 0;
+        else
+          cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + tix(lnA));
         if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
@@ -307,7 +311,10 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             const u32 xo = (u32)__cvta_generic_to_shared(xrow(k, pos));
 #pragma unroll
             for (int x = 0; x < CW / 4; ++x) cp_async16(xo + 16u * x, el + (u64)lnB * (CB / 8) + 16u * x);
-            cp_async4(xo + 4u * CW, tr + tix(lnB));
+            if (fresh)
+              xrow(k, pos)[CW] = 0u;
+            else
+              cp_async4(xo + 4u * CW, tr + tix(lnB));
           }
         }
       }
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       __syncwarp();
       // unaligned slots: lane L0 = bits [Λ - o, 2Λ - o) of (B ++ A) plus B's top at bit o
       for (u32 k = 0; k < (tunal ? cl.nload : 0u); ++k) {
-        const u32 o = (si[k].pre & 0x7FFFFFFFu) % CB;  // uniform across the warp
+        const u32 o = (si[k].pre & 0x3FFFFFFFu) % CB;  // uniform across the warp
         if (o == 0) continue;
         Ch<CW> out;
         int otop = 0;
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         __stcg(sk->tout + tix(d), top);
         // the lane that took the top word (source lane 0), or for an
         // output-only slot the lane writing lane 0, clears the output's
-        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
+        const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x3FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
         if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
       };
 

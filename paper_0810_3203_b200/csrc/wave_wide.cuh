@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
     for (u32 i = 0; i < per; ++i) {
       const u32 k = own(i);
       if (k >= cl.nload) continue;  // (warp-uniform)
-      const u32 r = si[k].pre & 0x7FFFFFFFu;
+      const u32 r = si[k].pre & 0x3FFFFFFFu;
       const u32 q = r / CB, o = r % CB;
       if (o) unal |= 1u << i;
       if (!act) continue;
@@ -149,7 +149,10 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
       const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
       for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
-      cp_async4(tile_s + (64u * 32u * CW + k * 32u + lane) * 4u, si[k].tin + wave_tix(A, lnA));
+      if ((si[k].pre >> 30) & 1u)  // never written: tops are zero
+        tops[k * 32u + lane] = 0;
+      else
+        cp_async4(tile_s + (64u * 32u * CW + k * 32u + lane) * 4u, si[k].tin + wave_tix(A, lnA));
       if (lane == 0) cp_async8(tile_s + (64u * 32u * CW + 64u * 32u) * 4u + 8u * k, el + 4ull * A.D);
       if (lnA == 0) zeroA |= 1u << i;
       if (srcA >= CL) wrapA |= 1u << i;
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
         const u32 i = i0 + j;
         if (i >= per || !((unal >> i) & 1u) || !act || !first || (A.debug & 64)) continue;
         const u32 k = own(i);
-        const u32 r = si[k].pre & 0x7FFFFFFFu;
+        const u32 r = si[k].pre & 0x3FFFFFFFu;
         const u32 q = r / CB;
         const u32 srcA = (L0 + 2 * CL - q) & (2 * CL - 1);
         const u32 srcB = (srcA + 2 * CL - 1) & (2 * CL - 1);
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
           nb[j].w[4 * x + 2] = v.z;
           nb[j].w[4 * x + 3] = v.w;
         }
-        nbt[j] = __ldcg(si[k].tin + wave_tix(A, lnB));
+        nbt[j] = ((si[k].pre >> 30) & 1u) ? 0 : __ldcg(si[k].tin + wave_tix(A, lnB));
         if (lnB == 0) nbz |= 1u << i;
         if (srcB >= CL) nbw |= 1u << i;
       }
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
           const u32 i = i0 + j;
           if (i >= per || !((unal >> i) & 1u)) continue;  // (warp-uniform)
           const u32 k = own(i);
-          const u32 o = (si[k].pre & 0x7FFFFFFFu) % CB;
+          const u32 o = (si[k].pre & 0x3FFFFFFFu) % CB;
           Ch<CW> out;
           int otop = 0;
           if (act) {
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, 2) coset_wide_kernel(WaveArgs
       for (int q = 0; q < CW / 4; ++q)
         __stcg(gp + q, make_uint4(w.w[4 * q], w.w[4 * q + 1], w.w[4 * q + 2], w.w[4 * q + 3]));
       __stcg(sk->tout + wave_tix(A, d), top);
-      const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x7FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
+      const bool owner = k < cl.nload ? ((L0 + 2 * CL - (sk->pre & 0x3FFFFFFFu) / CB) & (CL - 1)) == 0 : d == 0;
       if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
     };
 

@@ -140,7 +140,7 @@ def run_plan_fermat(plan, N, vals):
             a, b = c["pre"][i]
             e = (a * s + b + (tpre if inv and i < cn else 0)) % M
             if wplan and coset:  # the ticket's table: any bits, deferred rotations included
-                e = ws[c0 + 2 * i] & 0x7FFFFFFF
+                e = ws[c0 + 2 * i] & 0x3FFFFFFF
             elif wplan and c0 > 0:  # a whole ticket reading elements with deferred rotations
                 e = (e + ws[c0 - 1 + i]) % M
             assert not coset or e % lane == 0 or wplan
