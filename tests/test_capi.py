@@ -297,3 +297,32 @@ def test_schedule_shape_config5():
     waves = [lf[7] for lf in leaves[: batch * per_col]]
     assert waves == sorted(waves) and waves[0] == 0 and waves[-1] == 2
     assert leaves[batch * per_col][7] == 0  # the next batch restarts at level 1
+
+
+def test_linear_form_and_doubling_leaves():
+    """One-output ITFT leaves whose halvings make op rotations sub-lane run in
+    their linear form (inputs pre-rotated by any bits, aligned adds) as coset
+    leaves; doublings are arithmetic (no deferred final rotations).  The plans
+    are evaluated against the transform's definition."""
+    N = 2048
+    ctx = cf.FermatRingCtx(N)
+    ctx.set_coset(8)
+    fm = bm.FermatModel(N)
+    rnd = random.Random(21)
+    seen_linear = 0
+    for L, z, n, f in ((64, 64, 1, 0), (64, 50, 33, 0), (128, 100, 65, 1), (256, 256, 129, 0)):
+        s = rnd.randrange(2 * N)
+        a = [rnd.randrange((1 << N) + 1) for _ in range(z)]
+        want = fm.dft(L, s, a)
+        plan = cf.plan_dump(ctx, True, cf.TransformParams(L, s, z, n, f))
+        assert plan.get("final_rot", []) == []
+        for c in plan["classes"]:
+            if c["kind"] == 1 and c["nstore"] == 1 and c["ops"] and all(t in (1, 4) and r == 0 for (t, a_, b_, r) in c["ops"]):
+                seen_linear += 1
+        vals = {i: want[i] for i in range(n)}
+        vals.update({i: (L * a[i]) % fm.P for i in range(n, z)})
+        x = run_plan_fermat(plan, N, vals)
+        assert [x[i] for i in range(n)] == [(L * a[i]) % fm.P for i in range(n)]
+        if f:
+            assert x[n] == want[n]
+    assert seen_linear > 0
