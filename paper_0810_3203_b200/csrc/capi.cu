@@ -59,6 +59,7 @@ struct DevicePlan {
   const DevCounter* cmeta = nullptr;
   const u64* locbits = nullptr;
   const u64* shadow_finals = nullptr;
+  const u64* fold_list = nullptr;
   const u32* wave_ops = nullptr;
   const u32* wave_slots = nullptr;
   const u32* final_rot = nullptr;
@@ -175,7 +176,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   size_t o_cm = al(o_lf + leaves.size() * sizeof(DevLeaf));
   size_t o_lb = al(o_cm + cm.size() * sizeof(DevCounter));
   size_t o_sf = al(o_lb + p.locbits.size() * sizeof(u64));
-  size_t o_wo = al(o_sf + p.shadow_finals.size() * sizeof(u64));
+  size_t o_fl = al(o_sf + p.shadow_finals.size() * sizeof(u64));
+  size_t o_wo = al(o_fl + p.fold_list.size() * sizeof(u64));
   size_t o_ws = al(o_wo + p.wave_ops.size() * sizeof(u32));
   size_t o_fr = al(o_ws + p.wave_slots.size() * sizeof(u32));
   size_t total = al(o_fr + p.final_rot.size() * sizeof(u32)) + 256;
@@ -189,6 +191,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   if (!p.locbits.empty()) std::memcpy(h.data() + o_lb, p.locbits.data(), p.locbits.size() * sizeof(u64));
   if (!p.shadow_finals.empty())
     std::memcpy(h.data() + o_sf, p.shadow_finals.data(), p.shadow_finals.size() * sizeof(u64));
+  if (!p.fold_list.empty()) std::memcpy(h.data() + o_fl, p.fold_list.data(), p.fold_list.size() * sizeof(u64));
   if (!p.wave_ops.empty()) std::memcpy(h.data() + o_wo, p.wave_ops.data(), p.wave_ops.size() * sizeof(u32));
   if (!p.wave_slots.empty()) std::memcpy(h.data() + o_ws, p.wave_slots.data(), p.wave_slots.size() * sizeof(u32));
   if (!p.final_rot.empty()) std::memcpy(h.data() + o_fr, p.final_rot.data(), p.final_rot.size() * sizeof(u32));
@@ -204,6 +207,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.cmeta = reinterpret_cast<const DevCounter*>(b + o_cm);
   dp.locbits = reinterpret_cast<const u64*>(b + o_lb);
   dp.shadow_finals = reinterpret_cast<const u64*>(b + o_sf);
+  dp.fold_list = reinterpret_cast<const u64*>(b + o_fl);
   dp.wave_ops = reinterpret_cast<const u32*>(b + o_wo);
   dp.wave_slots = reinterpret_cast<const u32*>(b + o_ws);
   dp.final_rot = p.final_rot.empty() ? nullptr : reinterpret_cast<const u32*>(b + o_fr);
@@ -624,26 +628,32 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       }
       if (rc) return rc;
       if (tops) {
-        if (!dp.host.shadow_finals.empty()) {
-          fermat::shadow_copy_kernel<<<(unsigned)dp.host.shadow_finals.size(), 256, 0, st>>>(
-              base, shadow, stride, tops, A.tloc, dp.C, dp.shadow_finals, R->D);
-          ++launches;
-        }
-        // carry-save lanes of the outputs (a batch: of every element it touched)
-        // back to the canonical element format
-        const u64 cnt = dp.host.final_count ? dp.host.final_count : dp.host.extent;
+        // carry-save lanes of the outputs back to the canonical element format
         // (with the sub-lane rotations the outputs' last writers deferred)
-        if (cnt) {
-          const size_t fsm = dp.final_rot ? (size_t)R->D * 4 : 0;
-          static size_t fattr = 0;
-          if (fsm > 48 * 1024 && fsm > fattr) {
-            CUDA_TRY(cudaFuncSetAttribute(fermat::cs_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)fsm));
-            fattr = fsm;
+        const size_t fsm = dp.final_rot ? (size_t)R->D * 4 : 0;
+        static size_t fattr = 0;
+        if (fsm > 48 * 1024 && fsm > fattr) {
+          CUDA_TRY(cudaFuncSetAttribute(fermat::cs_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)fsm));
+          fattr = fsm;
+        }
+        const u32 logC = (u32)__builtin_ctz(dp.C);
+        if (dp.host.use_fold_list) {
+          // listed outputs in place, the shadow buffer's from there into place
+          if (!dp.host.fold_list.empty()) {
+            fermat::cs_fold_kernel<<<(unsigned)dp.host.fold_list.size(), 256, fsm, st>>>(
+                base, stride, tops, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot, dp.fold_list, nullptr);
+            ++launches;
           }
-          fermat::cs_fold_kernel<<<(unsigned)cnt, 256, fsm, st>>>(base, stride, tops, dp.C, dp.cw,
-                                                                 (u32)__builtin_ctz(dp.C), dp.logS, R->D, 0, 1,
-                                                                 dp.final_rot);
+          if (!dp.host.shadow_finals.empty()) {
+            fermat::cs_fold_kernel<<<(unsigned)dp.host.shadow_finals.size(), 256, fsm, st>>>(
+                base, stride, tops + A.tloc, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot,
+                dp.shadow_finals, shadow);
+            ++launches;
+          }
+        } else if (dp.host.final_count) {
+          fermat::cs_fold_kernel<<<(unsigned)dp.host.final_count, 256, fsm, st>>>(
+              base, stride, tops, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot, nullptr, nullptr);
           ++launches;
         }
       }

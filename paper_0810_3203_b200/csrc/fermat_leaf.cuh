@@ -1238,13 +1238,24 @@ __global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2
 // number of about o bits -- the shifted words in parallel, then S subtracted
 // serially (the borrow stops after a few words unless a run of zero words).
 // Dynamic shared memory: 4 D bytes when frot is set.
+//
+// idx (optional): the element of CTA b is idx[b] (else idx0 + b istride);
+// src (optional): the element lives in this buffer (the shadow copy; T then
+// points at that buffer's tops) -- it is copied into place first.
 __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const int* T, u32 CL, u32 CW,
                                                       u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride,
-                                                      const u32* frot) {
+                                                      const u32* frot, const u64* idx, const std::uint8_t* src) {
   __shared__ int s_pend[1024];
   extern __shared__ u32 s_old[];  // D words (frot only)
-  const u64 e = idx0 + (u64)blockIdx.x * istride;
+  const u64 e = idx ? idx[blockIdx.x] : idx0 + (u64)blockIdx.x * istride;
   std::uint8_t* el = data + e * eb;
+  if (src) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + e * eb);
+    uint4* d4 = reinterpret_cast<uint4*>(el);
+    const u32 pieces = (4 * D + 8 + 15) / 16;
+    for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) d4[x] = __ldcg(s4 + x);
+    __syncthreads();
+  }
   const int* Te = T + e * CL;
   long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
   u32* w = reinterpret_cast<u32*>(el);

@@ -176,6 +176,10 @@ struct Plan {
   u64 extent = 0;         // view indices [0, extent) touched (tops array rows)
   std::vector<u64> locbits;        // per-slot buffer bits (see DevLeaf::locoff)
   std::vector<u64> shadow_finals;  // outputs the schedule leaves in the shadow buffer
+  // the fold visits listed outputs (fold_list in place, shadow_finals from the
+  // shadow buffer into place) instead of the index range [0, final_count)
+  bool use_fold_list = false;
+  std::vector<u64> fold_list;
   // wave engine: ticket ranges of mutually independent leaves, launched in
   // order; {first ticket, count, kind (0 whole, 1 coset), coset ranges: the
   // most warp groups of lane cosets a ticket of the range has}
@@ -277,7 +281,7 @@ class Planner {
       for (u64 k = 0; k < it.n + (u64)(inverse ? it.f : 0); ++k) finals.push_back(it.base + k * it.stride);
     finish(p, finals);
     p.final_count = 0;  // caller canonicalises
-    p.tops_clear = true;  // the fold visits every element in [0, extent), written or not
+    fold_lists(p, finals, true);
     return p;
   }
 
@@ -300,11 +304,25 @@ class Planner {
     std::vector<u64> finals(p.final_count);
     for (u64 k = 0; k < p.final_count; ++k) finals[k] = k;
     finish(p, finals);
+    fold_lists(p, finals, false);
     return p;
   }
 
  private:
   static unsigned ctz(u64 x) { return (unsigned)__builtin_ctzll(x); }
+
+  // Which outputs the fold visits, and from where: a batch folds its outputs
+  // only (not every element in [0, extent)); outputs left in the shadow buffer
+  // are folded from there straight into place (no separate copy back).
+  static void fold_lists(Plan& p, const std::vector<u64>& finals, bool batch) {
+    if (!p.coset || (!batch && p.shadow_finals.empty())) return;
+    p.use_fold_list = true;
+    std::vector<u64> sh = p.shadow_finals;
+    std::sort(sh.begin(), sh.end());
+    p.fold_list.clear();
+    for (u64 e : finals)
+      if (!std::binary_search(sh.begin(), sh.end(), e)) p.fold_list.push_back(e);
+  }
 
   void reset() {
     class_index_.clear();
