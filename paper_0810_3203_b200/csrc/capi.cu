@@ -273,7 +273,11 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         static const int env_wide = getenv("CFTFT_WIDE") ? atoi(getenv("CFTFT_WIDE")) : 0;
         const int wide = R->wide >= 0 ? R->wide : env_wide;
         rs.wide = wide != 0 && cl >= 6 && (R->M >> 6) % rs.lane_bits == 0;
-        cl = std::min(cl, rs.wide ? 6u : 3u);
+        // coset leaves of 16 coefficients on 16-slot warp tiles (CFTFT_R16=1; measured slower,
+        // profiles/r01_experiments.md: the tiles halve the warps per SM)
+        static const int env_r16 = getenv("CFTFT_R16") ? atoi(getenv("CFTFT_R16")) : 0;
+        rs.r16 = !rs.wide && env_r16 != 0 && cl >= 4;
+        cl = std::min(cl, rs.wide ? 6u : (rs.r16 ? 4u : 3u));
         rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
       }
       rs.coset_max_ell = cl;
@@ -302,6 +306,22 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   return rs;
 }
 
+// Radix-16 plans (RingShape::r16) against their radix-8 alternative: the
+// one whose leaves move fewer bytes (partial ITFT leaves of 16 coefficients
+// are often not lane aligned and split into 4-point leaves).
+template <class F>
+Plan best_plan(const RingShape& rs, F build) {
+  Planner pa(rs);
+  Plan a = build(pa);
+  if (!rs.r16) return a;
+  RingShape r8 = rs;
+  r8.r16 = false;
+  r8.coset_max_ell = std::min(r8.coset_max_ell, 3u);
+  Planner pb(r8);
+  Plan b = build(pb);
+  return plan_cost(a, rs.elem_bytes) <= plan_cost(b, rs.elem_bytes) ? std::move(a) : std::move(b);
+}
+
 int get_plan(cftft_ring* R, bool inv, const cftft_params& p, int policy, cudaStream_t st,
              DevicePlan** out) {
   int dev = 0;
@@ -315,10 +335,12 @@ int get_plan(cftft_ring* R, bool inv, const cftft_params& p, int policy, cudaStr
     return CFTFT_OK;
   }
   auto dp = std::make_unique<DevicePlan>();
-  Planner pl(shape_of(R, p.length, dp.get()));
+  const RingShape rs = shape_of(R, p.length, dp.get());
   try {
-    dp->host = pl.build(inv, p.length, p.twiddle_exp, p.input_count, p.output_count,
-                        inv ? p.want_next : 0, policy);
+    dp->host = best_plan(rs, [&](Planner& pl) {
+      return pl.build(inv, p.length, p.twiddle_exp, p.input_count, p.output_count, inv ? p.want_next : 0,
+                      policy);
+    });
   } catch (const std::exception& ex) {
     return fail(CFTFT_UNSUPPORTED, ex.what());
   }
@@ -571,18 +593,26 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
                                                                                ? atoi(getenv("CFTFT_WAVE_WARPS"))
                                                                                : fermat::kWaveWarps));
         const size_t wsmem = (size_t)wwarps * fermat::wave_tile_words<8>() * 4;
+        const size_t wsmem16 = (size_t)wwarps * fermat::wave_tile_words<8, 16>() * 4;
         static bool wave_attr = false;
         if (!wave_attr) {
           CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
           CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, false, 16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem16));
+          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, true, 16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem16));
           wave_attr = true;
         }
         int dev = 0, sms = 0, per = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8, false>, 32 * wwarps, wsmem));
+        int per16 = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per16, fermat::coset_wave_kernel<8, false, 16>,
+                                                               32 * wwarps, wsmem16));
         const size_t xsmem = (size_t)fermat::wide_tile_words<8>() * 4;
         int xper = 0;
         if (dp.host.wide) {
@@ -602,6 +632,15 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms * std::max(xper, 1));
             fermat::coset_wide_kernel<8><<<g, 32 * fermat::kWideWarps, xsmem, st>>>(W);
+          } else if (wr[2] == 3) {  // 16-slot warp tiles
+            W.leaves = dp.leaves + wr[0];
+            W.nleaves = (u32)wr[1];
+            W.gpl = (u32)std::max<u64>(1, wr[3]);
+            const unsigned g = (unsigned)std::min<u64>((wr[1] * W.gpl + wwarps - 1) / wwarps, (u64)sms * std::max(per16, 1));
+            if (W.logS)
+              fermat::coset_wave_kernel<8, true, 16><<<g, 32 * wwarps, wsmem16, st>>>(W);
+            else
+              fermat::coset_wave_kernel<8, false, 16><<<g, 32 * wwarps, wsmem16, st>>>(W);
           } else if (wr[2] == 1) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];
@@ -774,10 +813,12 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
        << ",\"nstore\":" << k.nstore << ",\"kind\":" << k.kind << ",\"step\":" << k.step
        << ",\"m\":" << k.m << ",\"cs\":" << k.cs
        << ",\"wnet\":" << (c < p.wave_net.size() ? p.wave_net[c] : 0u);
-    if (c < p.wave_net.size() && p.wave_net[c] && k.key.ell == 6) {
-      // the radix-64 network's rotations (coset positions), (stage, warp, op)
+    if (c < p.wave_net.size() && p.wave_net[c] && (k.key.ell == 6 || k.key.ell == 4)) {
+      // the radix-64 network's rotations (coset positions), (stage, warp, op);
+      // the 16-slot network's in the warp kernel's op order
+      const u32 nn = k.key.ell == 6 ? 192u : 32u;
       os << ",\"net\":[";
-      for (u32 i = 0; i < 192; ++i) os << (i ? "," : "") << (p.wave_ops[p.wave_op_begin[c] + i] >> 16);
+      for (u32 i = 0; i < nn; ++i) os << (i ? "," : "") << (p.wave_ops[p.wave_op_begin[c] + i] >> 16);
       os << "]";
     }
     os << ",\"levels\":[";
@@ -1129,9 +1170,9 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
       dp = itc->second.get();
     } else {
       auto np = std::make_unique<DevicePlan>();
-      Planner pl(shape_of(R, v[0].L, np.get()));
+      const RingShape rs = shape_of(R, v[0].L, np.get());
       try {
-        np->host = pl.build_batch(inverse != 0, v, policy);
+        np->host = best_plan(rs, [&](Planner& pl) { return pl.build_batch(inverse != 0, v, policy); });
       } catch (const std::exception& ex) {
         return fail(CFTFT_UNSUPPORTED, ex.what());
       }
@@ -1183,11 +1224,12 @@ size_t cftft_plan_dump(const cftft_ring* ring, int inverse, const cftft_params* 
   if (validate(ring, inverse != 0, params, policy)) return 0;
   DevicePlan geo;
   const RingShape rs = shape_of(ring, params->length, &geo);
-  Planner pl(rs);
   Plan p;
   try {
-    p = pl.build(inverse != 0, params->length, params->twiddle_exp, params->input_count,
-                 params->output_count, inverse ? params->want_next : 0, policy);
+    p = best_plan(rs, [&](Planner& pl) {
+      return pl.build(inverse != 0, params->length, params->twiddle_exp, params->input_count,
+                      params->output_count, inverse ? params->want_next : 0, policy);
+    });
   } catch (const std::exception&) {
     return 0;
   }

@@ -153,14 +153,17 @@ struct WaveSlot {
   int* tout;
   u32 pre, post, pad0, pad1;
 };
-template <int CW>
+// per warp, S slots (8, or 16 for radix-16 leaves): rows [S][32] x CW words,
+// tops [S][32], top words [S] (u64), extra rows [S][S/2], slot table [S]
+template <int CW, int S = 8>
 __host__ __device__ constexpr u32 wave_tile_words() {
-  return 8u * 32u * CW + 8u * 32u + 16u + 8u * 4u * wave_xrow_words<CW>() + 8u * (sizeof(WaveSlot) / 4);
+  return (u32)S * 32u * CW + (u32)S * 32u + 2u * S + (u32)S * (S / 2) * wave_xrow_words<CW>() +
+         (u32)S * (sizeof(WaveSlot) / 4);
 }
 
 // TIX: the tops arrays are lane-interleaved (wide plans, A.logS > 0); the
 // radix-8 plans keep natural lane order and skip the index mapping
-template <int CW, bool TIX>
+template <int CW, bool TIX, int S = 8>
 __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs A) {
   auto tix = [&](u32 p) -> u32 { return TIX ? wave_tix(A, p) : p; };
   static_assert(CW == 8, "the wave engine runs 256-bit lanes");
@@ -168,14 +171,15 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
   constexpr u32 CB = 32 * CW;
   constexpr u32 XR = wave_xrow_words<CW>();
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  u32* const tile = wsm + warp * wave_tile_words<CW>();
+  u32* const tile = wsm + warp * wave_tile_words<CW, S>();
   const u32 CL = A.lanes;
   auto rowp = [&](u32 slot, u32 l) -> u32* { return tile + (slot * 32u + l) * CW; };
-  int* const tops = reinterpret_cast<int*>(tile + 8u * 32u * CW);
-  long long* const hiw = reinterpret_cast<long long*>(tile + 8u * 32u * CW + 256u);  // per slot top word
-  u32* const xtile = tile + 8u * 32u * CW + 256u + 16u;  // extra rows: [slot][position]
-  auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * 4u + p) * XR; };
-  WaveSlot* const si = reinterpret_cast<WaveSlot*>(xtile + 8u * 4u * XR);
+  constexpr u32 TW = (u32)S * 32u * CW;  // tops follow the rows
+  int* const tops = reinterpret_cast<int*>(tile + TW);
+  long long* const hiw = reinterpret_cast<long long*>(tile + TW + S * 32u);  // per slot top word
+  u32* const xtile = tile + TW + S * 32u + 2u * S;  // extra rows: [slot][position]
+  auto xrow = [&](u32 slot, u32 p) -> u32* { return xtile + (slot * (S / 2) + p) * XR; };
+  WaveSlot* const si = reinterpret_cast<WaveSlot*>(xtile + (u32)S * (S / 2) * XR);
   auto swz = [](u32 l) -> u32 { return (l >> 2) & 1u; };
   auto ldw = [&](Ch<CW>& c, const u32* r, u32 sw) {
 #pragma unroll
@@ -243,7 +247,9 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
     // the ticket's slot table and the class's first 32 packed ops, one word
     // per lane, broadcast by shuffles (no dependent global loads in the loops)
     const u32 span = max(cl.nload, cl.nstore);
-    const u32 opv0 = lane < cl.nops ? A.wops[cl.wop_begin + lane] : 0u;
+    // (a 16-slot network's table has 32 rotations whatever the class's op count)
+    const u32 nwo = (cl.wnet && cl.L == 16) ? 32u : cl.nops;
+    const u32 opv0 = lane < nwo ? A.wops[cl.wop_begin + lane] : 0u;
     // the ticket's slots, resolved once (lane k: slot k) and read back by
     // broadcast; the previous ticket's groups are done with the table
     __syncwarp();
@@ -282,7 +288,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
       // slot table: {pre bits | in-buffer << 31, post lanes | out-buffer << 31}
       const bool first = (lane & cmask) == 0;
 #pragma unroll
-      for (u32 k = 0; k < 8; ++k) {
+      for (u32 k = 0; k < (u32)S; ++k) {
         if (!act || k >= cl.nload) break;
         const u32 r = si[k].pre & 0x3FFFFFFFu;
         const u32 q = r / CB, o = r % CB;
@@ -297,8 +303,8 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         if (fresh)
           tops[k * 32u + lane] = 0;
         else
-          cp_async4(tile_s + (8u * 32u * CW + k * 32u + lane) * 4u, tr + tix(lnA));
-        if (lane == 0) cp_async8(tile_s + (8u * 32u * CW + 256u) * 4u + 8u * k, el + 4ull * A.D);
+          cp_async4(tile_s + (TW + k * 32u + lane) * 4u, tr + tix(lnA));
+        if (lane == 0) cp_async8(tile_s + (TW + S * 32u) * 4u + 8u * k, el + 4ull * A.D);
         if (lnA == 0) zeroA |= 1u << k;
         if (srcA >= CL) wrapA |= 1u << k;
         if (o) {
@@ -465,42 +471,45 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
           }
           return top;
         };
-        auto span4 = [&](u32 o0, bool out, bool first, bool fresh) {
+        // np pairs (b0 + j, b0 + j + sp), ops o0 + j, through the rows
+        auto spanp = [&](u32 np, u32 sp, u32 b0, u32 o0, bool out, bool first, bool fresh) {
 #pragma unroll 1
-          for (u32 j = 0; j < 4; ++j) {
+          for (u32 j = 0; j < np; ++j) {
             Ch<CW> a, b;
-            int ta = ldx(a, j, first, fresh), tb = ldx(b, j + 4, first, fresh);
+            const u32 ka = b0 + j, kb = ka + sp;
+            int ta = ldx(a, ka, first, fresh), tb = ldx(b, kb, first, fresh);
             bfly(a, ta, b, tb, o0 + j);
             if (out) {
-              if (j < cl.nstore) store_slot(j, a, ta);
-              if (j + 4 < cl.nstore) store_slot(j + 4, b, tb);
+              if (ka < cl.nstore) store_slot(ka, a, ta);
+              if (kb < cl.nstore) store_slot(kb, b, tb);
             } else {
-              st(j, lane, a, ta);
-              st(j + 4, lane, b, tb);
+              st(ka, lane, a, ta);
+              st(kb, lane, b, tb);
             }
           }
         };
-        // a 4-point half (slots 4h..4h+3): spans 1,2 (DIT: ops 2h, 2h+1 then
-        // 4+2h, 5+2h) or 2,1 (DIF: ops 4+2h, 5+2h then 8+2h, 9+2h)
-        auto half4 = [&](u32 h, bool dit, bool out, bool first, bool fresh) {
+        // a 4-point half (slots b0+4h..b0+4h+3) of the 8-point network whose
+        // ops start at ob: spans 1,2 (DIT: ops 2h, 2h+1 then 4+2h, 5+2h) or
+        // 2,1 (DIF: ops 4+2h, 5+2h then 8+2h, 9+2h)
+        auto half4 = [&](u32 b0, u32 ob, u32 h, bool dit, bool out, bool first, bool fresh) {
           Ch<CW> x[4];
           int tx[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) tx[k] = ldx(x[k], 4 * h + k, first, fresh);
+          for (int k = 0; k < 4; ++k) tx[k] = ldx(x[k], b0 + 4 * h + k, first, fresh);
           if (dit) {
-            bfly(x[0], tx[0], x[1], tx[1], 2 * h);
-            bfly(x[2], tx[2], x[3], tx[3], 2 * h + 1);
-            bfly(x[0], tx[0], x[2], tx[2], 4 + 2 * h);
-            bfly(x[1], tx[1], x[3], tx[3], 5 + 2 * h);
+            bfly(x[0], tx[0], x[1], tx[1], ob + 2 * h);
+            bfly(x[2], tx[2], x[3], tx[3], ob + 2 * h + 1);
+            bfly(x[0], tx[0], x[2], tx[2], ob + 4 + 2 * h);
+            bfly(x[1], tx[1], x[3], tx[3], ob + 5 + 2 * h);
           } else {
-            bfly(x[0], tx[0], x[2], tx[2], 4 + 2 * h);
-            bfly(x[1], tx[1], x[3], tx[3], 5 + 2 * h);
-            bfly(x[0], tx[0], x[1], tx[1], 8 + 2 * h);
-            bfly(x[2], tx[2], x[3], tx[3], 9 + 2 * h);
+            bfly(x[0], tx[0], x[2], tx[2], ob + 4 + 2 * h);
+            bfly(x[1], tx[1], x[3], tx[3], ob + 5 + 2 * h);
+            bfly(x[0], tx[0], x[1], tx[1], ob + 8 + 2 * h);
+            bfly(x[2], tx[2], x[3], tx[3], ob + 9 + 2 * h);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const u32 sk = 4 * h + k;
+            const u32 sk = b0 + 4 * h + k;
             if (out) {
               if (sk < cl.nstore) store_slot(sk, x[k], tx[k]);
             } else {
@@ -508,14 +517,32 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             }
           }
         };
-        if (cl.wnet == 1) {  // DIF: span 4, then the halves
-          span4(0, false, true, fused);
-          half4(0, false, true, false, false);
-          half4(1, false, true, false, false);
-        } else {  // DIT: the halves, then span 4
-          half4(0, true, false, true, fused);
-          half4(1, true, false, true, fused);
-          span4(8, true, false, false);
+        // the 8-point network of slots b0..b0+7, ops ob..ob+11
+        auto net8 = [&](u32 b0, u32 ob, bool dif, bool out, bool first, bool fresh) {
+          if (dif) {  // span 4, then the halves
+            spanp(4, 4, b0, ob, false, first, fresh);
+            half4(b0, ob, 0, false, out, false, false);
+            half4(b0, ob, 1, false, out, false, false);
+          } else {  // the halves, then span 4
+            half4(b0, ob, 0, true, false, first, fresh);
+            half4(b0, ob, 1, true, false, first, fresh);
+            spanp(4, 4, b0, ob + 8, out, false, false);
+          }
+        };
+        if (S == 16 && cl.L == 16) {
+          // 16 slots (Planner::network16 op order): DIF = span 8, then the
+          // 8-point networks of slots 0-7 and 8-15; DIT = those, then span 8
+          if (cl.wnet == 1) {
+            spanp(8, 8, 0, 0, false, true, fused);
+            net8(0, 8, true, true, false, false);
+            net8(8, 20, true, true, false, false);
+          } else {
+            net8(0, 0, false, false, true, fused);
+            net8(8, 12, false, false, true, fused);
+            spanp(8, 8, 0, 24, true, false, false);
+          }
+        } else {
+          net8(0, 0, cl.wnet == 1, true, true, fused);
         }
         __syncwarp();
         continue;

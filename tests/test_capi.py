@@ -146,7 +146,29 @@ def run_plan_fermat(plan, N, vals):
             assert not coset or e % lane == 0 or wplan
             slot[i] = (x[(buf(locoff, i, False), base + i * stride)] * pow(2, e, P)) % P
         ops = c["ops"]
-        if c.get("net"):
+        if c.get("net") and c["ell"] == 4:
+            # the warp kernel's 16-slot network (wave_coset.cuh): DIF = span 8
+            # then the 8-point networks of slots 0-7, 8-15; DIT the reverse
+            for i in range(c["nload"], 16):
+                slot[i] = 0
+            ops, unit, dif, net = [], M >> 4, c["wnet"] == 1, c["net"]
+
+            def net8(hh, o0):
+                for o in range(12):
+                    ll, jj = divmod(o, 4)
+                    hl = (4 >> ll) if dif else (1 << ll)
+                    al = (jj // hl) * 2 * hl + jj % hl
+                    ops.append((0, 8 * hh + al, 8 * hh + al + hl, net[o0 + o] * unit))
+
+            if dif:
+                ops += [(0, j, j + 8, net[j] * unit) for j in range(8)]
+                net8(0, 8)
+                net8(1, 20)
+            else:
+                net8(0, 0)
+                net8(1, 12)
+                ops += [(0, j, j + 8, net[24 + j] * unit) for j in range(8)]
+        elif c.get("net"):
             # the CTA kernel's radix-64 network (wave_wide.cuh): two stages of
             # eight 8-point networks, (stage, warp, op) -> butterfly
             for i in range(c["nload"], 64):
@@ -326,3 +348,22 @@ def test_linear_form_and_doubling_leaves():
         if f:
             assert x[n] == want[n]
     assert seen_linear > 0
+
+
+def test_radix16_schedule_reproduces_definition():
+    """Opt-in radix-16 warp tiles (CFTFT_R16=1): 16-point networks, the
+    wave-minimising splits and the plan choice, evaluated in a subprocess
+    (the switch is read once per process)."""
+    import subprocess
+    import sys
+    code = (
+        "import random, sys; sys.path.insert(0, 'tests'); sys.path.insert(0, 'oracle');"
+        "import test_capi as t; import paper_0810_3203_b200 as cf;"
+        "ctx = cf.FermatRingCtx(8192);"
+        "d = cf.plan_dump(ctx, False, cf.TransformParams(1 << 9, 0, 500, 500, 0));"
+        "assert any(c['ell'] == 4 and c.get('net') for c in d['classes']), 'no 16-point network';"
+        "t.check_plan(ctx, 8192, random.Random(16), 8, 5, 9)"
+    )
+    env = dict(os.environ, CFTFT_R16="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
