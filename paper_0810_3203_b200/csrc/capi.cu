@@ -897,7 +897,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   if (kind == CFTFT_RING_FERMAT) {
     const char* e = getenv("CFTFT_CTAS_PER_SM");
     if (e && atoi(e) == 2 && R->CW == 16 && R->C <= 256) R->NT = 256;
-    const char* wv = getenv("CFTFT_WIDE");  // experiment: 1024 threads, 256-bit chunks
+    const char* wv = getenv("CFTFT_WHOLE1024");  // experiment: whole leaves, 1024 threads, 256-bit chunks
     if (wv && atoi(wv) == 1 && R->D >= 16) {
       R->CW = 8;
       R->C = R->D / 8;
