@@ -197,7 +197,7 @@ int main() {
     printf("%-34s CTAs/SM %d  %7.3f ms  %7.1f GB/s (r+w, data+tops)  %s\n", name, per, best, bytes / best / 1e6,
            cudaGetErrorString(cudaGetLastError()));
   };
-  for (int per : {4, 8}) {
+  for (int per : {2, 3, 4}) {
     run(pattern<0>, "cp.async 16B -> smem -> stcg", per);
     run(pattern<1>, "TMA bulk 256B runs (mbarrier)", per);
     run(pattern<2>, "ld.global.v4 -> regs -> stcg", per);
