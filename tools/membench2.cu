@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) pattern(const uint8_t* A, uint
                                                           uint64_t nitems, uint32_t nelem) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* tile = sm + warp * (8 * 32 * 32 + 8 * 32 * 4 + 64);
+  uint8_t* tile = sm + warp * (8 * 32 * 32 + 8 * 32 * 4 + 64 + (V == 5 ? 8 * 32 * 32 : 0));
   uint64_t* bar = reinterpret_cast<uint64_t*>(tile + 8 * 32 * 32 + 8 * 32 * 4);
   const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
@@ -94,6 +94,44 @@ __global__ void __launch_bounds__(32 * kWarps, 4) pattern(const uint8_t* A, uint
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
       __syncwarp();
+    } else if (V == 5) {
+      // cp.async 16 B/lane in (as V0), rows copied by the lanes into a
+      // separate staging area, TMA bulk runs out; the staging area is only
+      // waited for before its next reuse
+      uint8_t* stage = tile + 8 * 32 * 32 + 8 * 32 * 4 + 64;
+      const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint64_t e = (e0 + 64ull * k) % nelem;
+        const uint8_t* src = A + e * kElem + (uint64_t)L0 * 32;
+        cp16(tile_s + (k * 32 + lane) * 32, src);
+        cp16(tile_s + (k * 32 + lane) * 32 + 16, src + 16);
+        cp4(tile_s + 8 * 32 * 32 + (k * 32 + lane) * 4, TA + e * kLanes + L0);
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncwarp();
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint64_t e = (e0 + 64ull * k) % nelem;
+        const uint4* s = reinterpret_cast<const uint4*>(tile + (k * 32 + lane) * 32);
+        uint4* d = reinterpret_cast<uint4*>(stage + ((k * 4 + pos) * 8 + (lane & 7)) * 32);
+        d[0] = s[0];
+        d[1] = s[1];
+        __stcg(TB + e * kLanes + L0, reinterpret_cast<const int*>(tile + 8 * 32 * 32)[k * 32 + lane]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      {
+        const uint32_t k = lane >> 2, p = lane & 3;
+        const uint64_t e = (e0 + 64ull * k) % nelem;
+        const uint32_t l0 = (uint32_t)g * 8 + kStep * p;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;\n" ::"l"(B + e * kElem + (uint64_t)l0 * 32),
+                     "r"(stage_s + (k * 4 + p) * 256)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
     } else if (V == 3 || V == 4) {
       // data runs by TMA (lane j: slot j >> 2, position j & 3), tops by cp.async 4 B per lane
       const uint32_t k = lane >> 2, p = lane & 3;
@@ -164,6 +202,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) pattern(const uint8_t* A, uint
       }
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 int main() {
@@ -175,7 +214,7 @@ int main() {
   cudaMalloc(&TA, (size_t)nelem * kLanes * 4);
   cudaMalloc(&TB, (size_t)nelem * kLanes * 4);
   const uint64_t nitems = (uint64_t)nelem / 8 * 16;  // every lane of every element once
-  const size_t smem = kWarps * (8 * 32 * 32 + 8 * 32 * 4 + 64);
+  const size_t smem = kWarps * (8 * 32 * 32 + 8 * 32 * 4 + 64 + 8 * 32 * 32);
   const double bytes = 2.0 * nitems * 8 * 32 * 36;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -203,6 +242,7 @@ int main() {
     run(pattern<2>, "ld.global.v4 -> regs -> stcg", per);
     run(pattern<3>, "TMA data + cp.async tops, stcg out", per);
     run(pattern<4>, "TMA data + cp.async tops, TMA out", per);
+    run(pattern<5>, "cp.async in, staging + TMA out", per);
   }
   cudaMemcpy(B, A, (size_t)nelem * kElem, cudaMemcpyDeviceToDevice);
   cudaEvent_t a, b;
