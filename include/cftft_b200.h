@@ -45,7 +45,12 @@ enum cftft_status {
   CFTFT_NO_MEMORY = 5
 };
 
-enum cftft_ring_kind { CFTFT_RING_FERMAT = 1, CFTFT_RING_NEGACYCLIC = 2 };
+/* CFTFT_RING_PRIME: the reference's own ring, Z/pZ for an odd prime p < 2^64
+ * with 2^m | p - 1 and omega the reference's root of order M = 2^m
+ * (field.hpp:84-185; Goldilocks p = 2^64 - 2^32 + 1, m = 32 by default):
+ * cftft_ring_create(CFTFT_RING_PRIME, m, p, &ring), m <= 32; one u64 word
+ * per coefficient, element stride a multiple of 8 bytes. */
+enum cftft_ring_kind { CFTFT_RING_FERMAT = 1, CFTFT_RING_NEGACYCLIC = 2, CFTFT_RING_PRIME = 3 };
 
 /* cftft::SplitPolicy (transform.hpp:27-30). */
 enum cftft_split_policy { CFTFT_BALANCED = 0, CFTFT_RADIX2 = 1 };

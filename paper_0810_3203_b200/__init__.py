@@ -37,7 +37,8 @@ __all__ = [
     "SplitPolicy", "TransformParams", "ButterflyStats", "BadLength", "InvalidParams",
     "CudaError", "Unsupported", "FermatRingCtx", "NegacyclicRingCtx", "DeviceView",
     "cf_tft", "cf_itft", "cf_tft_host", "cf_itft_host", "bit_reverse", "tft_bound",
-    "itft_bound", "tft_base_cases", "itft_base_cases", "lib", "last_launch_count", "plan_dump",
+    "itft_bound", "tft_base_cases", "itft_base_cases", "lib", "last_launch_count", "plan_dump", "PrimeRingCtx",
+    "GOLDILOCKS",
     "scale",
 ]
 
@@ -201,6 +202,26 @@ class NegacyclicRingCtx(_Ring):
     def __init__(self, K: int, m: int):
         self.K, self.m = K, m
         super().__init__(K, m)
+
+
+GOLDILOCKS = 0xFFFFFFFF00000001
+
+
+class PrimeRingCtx(_Ring):
+    """The reference's own ring: Z/pZ with omega its root of order M = 2^m
+    (RingCtx(p, m), field.hpp:84-185; Goldilocks and m = 32 by default).
+
+    Element = one u64 word in [0, p); views of shape (E, 1)."""
+
+    kind = 3
+
+    def __init__(self, m: int = 32, p: int = GOLDILOCKS):
+        self.m, self.p = m, p
+        super().__init__(m, p)
+
+    @property
+    def element_words(self) -> int:
+        return 1
 
 
 class DeviceView:

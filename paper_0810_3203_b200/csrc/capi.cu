@@ -19,6 +19,7 @@
 #include "../../include/cftft_b200.h"
 #include "fermat_leaf.cuh"
 #include "negacyclic_leaf.cuh"
+#include "prime_leaf.cuh"
 #include "pointwise.cuh"
 #include "wave_coset.cuh"
 #include "wave_wide.cuh"
@@ -96,6 +97,10 @@ struct cftft_ring {
   std::map<PlanKey, std::unique_ptr<DevicePlan>> cache;
   // Goldilocks twiddle tables of the Fermat pointwise multiplier
   u64* ntt_tw = nullptr;
+  // prime rings: p (in m), -p^-1 mod 2^64, omega, two-level Montgomery tables
+  u64 pinv = 0, omega = 0;
+  u32 lo_bits = 0;
+  u64* prime_tw = nullptr;  // [2^lo_bits] omega^i R, then [M / 2^lo_bits] omega^(i 2^lo_bits) R
   // staging buffer for the host-view entry points
   void* stage = nullptr;
   size_t stage_bytes = 0;
@@ -115,6 +120,7 @@ struct cftft_ring {
   ~cftft_ring() {
     if (stage) cudaFree(stage);
     if (ntt_tw) cudaFree(ntt_tw);
+    if (prime_tw) cudaFree(prime_tw);
     for (auto& sc : scratch) {
       if (sc.shadow) cudaFree(sc.shadow);
       if (sc.tops) cudaFree(sc.tops);
@@ -374,6 +380,10 @@ int validate(const cftft_ring* R, bool inv, const cftft_params* p, int policy) {
 }
 
 int check_stride(const cftft_ring* R, u64 stride) {
+  if (R->kind == CFTFT_RING_PRIME) {
+    if (stride < 8 || (stride % 8) != 0) return fail(CFTFT_UNSUPPORTED, "element stride must be a multiple of 8 bytes");
+    return CFTFT_OK;
+  }
   if (stride < R->elem_bytes || (stride % 16) != 0)
     return fail(CFTFT_UNSUPPORTED, "element stride must be a multiple of 16 and >= " +
                                        std::to_string(R->elem_bytes) + " bytes");
@@ -458,6 +468,28 @@ struct HostTrace {
     t = n;
   }
 };
+
+// Prime rings: the two-level Montgomery tables of omega's powers (omega^i R
+// mod p, i < 2^lo_bits; omega^(i 2^lo_bits) R mod p), built once per ring.
+int ensure_prime_tables(cftft_ring* R, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(R->mu);
+  if (R->prime_tw) return CFTFT_OK;
+  const u64 p = R->m, lo = u64{1} << R->lo_bits, hi = R->M >> R->lo_bits;
+  auto mulp = [p](u64 a, u64 b) { return (u64)((unsigned __int128)a * b % p); };
+  const u64 Rm = (u64)(((unsigned __int128)1 << 64) % p);  // 2^64 mod p
+  std::vector<u64> h(lo + hi);
+  u64 w = 1 % p;
+  for (u64 i = 0; i < lo; ++i, w = mulp(w, R->omega)) h[i] = mulp(w, Rm);
+  const u64 step = w;  // omega^lo
+  u64 v = 1 % p;
+  for (u64 i = 0; i < hi; ++i, v = mulp(v, step)) h[lo + i] = mulp(v, Rm);
+  u64* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, h.size() * sizeof(u64)));
+  CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(u64), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  R->prime_tw = d;
+  return CFTFT_OK;
+}
 
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
@@ -708,6 +740,29 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
                 100.0 * h[1] / tot, 100.0 * h[2] / tot, 100.0 * h[3] / tot, 100.0 * h[4] / tot, 100.0 * h[5] / tot,
                 (double)tot / grid);
       }
+    } else if (R->kind == CFTFT_RING_PRIME) {
+      if (int rc = ensure_prime_tables(R, st)) return rc;
+      if (int rc = set_smem(prime::leaf_kernel)) return rc;
+      if (int rc = grid_for(prime::leaf_kernel, prime::kThreads, smem, dp.nleaves, &grid)) return rc;
+      prime::Args A{};
+      A.data = base;
+      A.elem_bytes = stride;
+      A.leaves = dp.leaves;
+      A.nleaves = dp.nleaves;
+      A.classes = dp.classes;
+      A.ops = dp.ops;
+      A.levels = dp.levels;
+      A.rots = dp.rots;
+      A.counters = counters;
+      A.cmeta = dp.cmeta;
+      A.M = R->M;
+      A.p = R->m;
+      A.pinv = R->pinv;
+      A.lo_bits = R->lo_bits;
+      A.tw_lo = R->prime_tw;
+      A.tw_hi = R->prime_tw + (size_t{1} << R->lo_bits);
+      A.slot_bytes = R->slot_bytes;
+      prime::leaf_kernel<<<grid, prime::kThreads, smem, st>>>(A);
     } else {
       if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
       if (int rc = grid_for(negacyclic::leaf_kernel, negacyclic::kThreads, smem, dp.nleaves, &grid))
@@ -889,6 +944,37 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
     R->M = 2 * K;
     R->slot_bytes = (u32)(8 * K);
     R->elem_bytes = 8 * K;
+  } else if (kind == CFTFT_RING_PRIME) {
+    // the reference's RingCtx(p, m) (field.hpp:84-185), m <= 32 on the GPU
+    const u64 m = n_or_k, p = modulus;
+    if (m < 1 || m > 32) return fail(CFTFT_UNSUPPORTED, "prime ring: two-adicity m must be in [1, 32]");
+    if (p < 3 || (p & 1) == 0 || ((p - 1) & ((u64{1} << m) - 1)) != 0)
+      return fail(CFTFT_INVALID_PARAMS, "prime ring: p must be odd with 2^m | p - 1");
+    auto mulp = [p](u64 a, u64 b) { return (u64)((unsigned __int128)a * b % p); };
+    auto powp = [&](u64 a, u64 e) {
+      u64 r = 1 % p;
+      for (; e; e >>= 1, a = mulp(a, a))
+        if (e & 1) r = mulp(r, a);
+      return r;
+    };
+    const u64 M = u64{1} << m;
+    // smallest g in 2, 3, 5, 7, ... whose (p-1)/2^m power has order 2^m (field.hpp:170-177)
+    u64 omega = 0;
+    for (u64 g = 2; g < 1024 && !omega; g = (g == 2) ? 3 : g + 2) {
+      const u64 w = powp(g % p, (p - 1) >> m);
+      if (powp(w, M / 2) == p - 1) omega = w;
+    }
+    if (!omega) return fail(CFTFT_INVALID_PARAMS, "prime ring: no root of order 2^m (is p prime?)");
+    u64 inv = 1;  // p^-1 mod 2^64 by Newton's iteration
+    for (int i = 0; i < 7; ++i) inv *= 2 - p * inv;
+    R->m = p;
+    R->K = m;
+    R->M = M;
+    R->omega = omega;
+    R->pinv = (u64)0 - inv;
+    R->lo_bits = (u32)std::min<u64>(m, 16);
+    R->slot_bytes = 8;
+    R->elem_bytes = 8;
   } else {
     return fail(CFTFT_UNSUPPORTED, "unknown ring kind");
   }
