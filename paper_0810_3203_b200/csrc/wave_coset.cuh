@@ -134,6 +134,13 @@ __device__ __forceinline__ int unal_combine8(Ch<8>& out, const Ch<8>& b, const C
   }
 }
 
+
+// cp.async of 16 bytes with an L2 prefetch-size hint (a warp row reads runs
+// of 8 consecutive 32-byte lanes: the first miss brings in the whole run)
+__device__ __forceinline__ void cp_async16_l2(u32 saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+
 constexpr int kWaveWarps = 4;  // warps per CTA, at most (the launch may use fewer)
 
 // per warp: data rows [slot][lane] of CW words, their 16-byte halves swapped
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
         const bool fresh = (si[k].pre >> 30) & 1u;  // never written: tops are zero
         const u32 so = tile_s + (k * 32u + lane) * CW * 4u, sw = swz(lane);
 #pragma unroll
-        for (u32 x = 0; x < CW / 4; ++x) cp_async16(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
+        for (u32 x = 0; x < CW / 4; ++x) cp_async16_l2(so + 16u * (x ^ sw), el + (u64)lnA * (CB / 8) + 16u * x);
         if (fresh)
           tops[k * 32u + lane] = 0;
         else
