@@ -61,6 +61,7 @@ struct DevicePlan {
   const u64* locbits = nullptr;
   const u64* shadow_finals = nullptr;
   const u64* fold_list = nullptr;
+  const u32* groups = nullptr;
   const u32* wave_ops = nullptr;
   const u32* wave_slots = nullptr;
   const u32* final_rot = nullptr;
@@ -183,7 +184,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   size_t o_lb = al(o_cm + cm.size() * sizeof(DevCounter));
   size_t o_sf = al(o_lb + p.locbits.size() * sizeof(u64));
   size_t o_fl = al(o_sf + p.shadow_finals.size() * sizeof(u64));
-  size_t o_wo = al(o_fl + p.fold_list.size() * sizeof(u64));
+  size_t o_gr = al(o_fl + p.fold_list.size() * sizeof(u64));
+  size_t o_wo = al(o_gr + p.groups.size() * sizeof(u32));
   size_t o_ws = al(o_wo + p.wave_ops.size() * sizeof(u32));
   size_t o_fr = al(o_ws + p.wave_slots.size() * sizeof(u32));
   size_t total = al(o_fr + p.final_rot.size() * sizeof(u32)) + 256;
@@ -198,6 +200,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   if (!p.shadow_finals.empty())
     std::memcpy(h.data() + o_sf, p.shadow_finals.data(), p.shadow_finals.size() * sizeof(u64));
   if (!p.fold_list.empty()) std::memcpy(h.data() + o_fl, p.fold_list.data(), p.fold_list.size() * sizeof(u64));
+  if (!p.groups.empty()) std::memcpy(h.data() + o_gr, p.groups.data(), p.groups.size() * sizeof(u32));
   if (!p.wave_ops.empty()) std::memcpy(h.data() + o_wo, p.wave_ops.data(), p.wave_ops.size() * sizeof(u32));
   if (!p.wave_slots.empty()) std::memcpy(h.data() + o_ws, p.wave_slots.data(), p.wave_slots.size() * sizeof(u32));
   if (!p.final_rot.empty()) std::memcpy(h.data() + o_fr, p.final_rot.data(), p.final_rot.size() * sizeof(u32));
@@ -214,6 +217,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.locbits = reinterpret_cast<const u64*>(b + o_lb);
   dp.shadow_finals = reinterpret_cast<const u64*>(b + o_sf);
   dp.fold_list = reinterpret_cast<const u64*>(b + o_fl);
+  dp.groups = p.groups.empty() ? nullptr : reinterpret_cast<const u32*>(b + o_gr);
   dp.wave_ops = reinterpret_cast<const u32*>(b + o_wo);
   dp.wave_slots = reinterpret_cast<const u32*>(b + o_ws);
   dp.final_rot = p.final_rot.empty() ? nullptr : reinterpret_cast<const u32*>(b + o_fr);
@@ -227,6 +231,8 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
 RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   RingShape rs;
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
+  static const int env_grp = getenv("CFTFT_PRIME_GROUP") ? atoi(getenv("CFTFT_PRIME_GROUP")) : 16;
+  if (R->kind == CFTFT_RING_PRIME) rs.group = (u32)std::min(16, std::max(1, env_grp));  // adjacent u64 coefficients per ticket
   rs.M = R->M;
   rs.max_leaf_ell = R->max_leaf_ell;
   rs.elem_bytes = R->elem_bytes;
@@ -507,7 +513,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     const size_t half = ((kSmemBudget - scratch_bytes(1024)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
                                    ? std::max<size_t>({dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell, 2 * half})
-                                   : (size_t)R->slot_bytes << dp.max_ell;
+                                   : ((size_t)R->slot_bytes << dp.max_ell) * (R->kind == CFTFT_RING_PRIME ? 16 : 1);  // prime: grouped leaves
     const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(1024) : 0);
     unsigned grid = 1;
     int* tops = nullptr;
@@ -762,6 +768,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.tw_lo = R->prime_tw;
       A.tw_hi = R->prime_tw + (size_t{1} << R->lo_bits);
       A.slot_bytes = R->slot_bytes;
+      A.groups = dp.groups;
+      A.nleaves = dp.groups ? dp.host.groups.size() / 2 : dp.nleaves;  // tickets
       prime::leaf_kernel<<<grid, prime::kThreads, smem, st>>>(A);
     } else {
       if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;

@@ -180,6 +180,9 @@ struct Plan {
   // shadow buffer into place) instead of the index range [0, final_count)
   bool use_fold_list = false;
   std::vector<u64> fold_list;
+  // small-coefficient plans: tickets are groups {first leaf, count} of
+  // consecutive leaves (Planner::group_leaves); empty: one leaf per ticket
+  std::vector<u32> groups;
   // wave engine: ticket ranges of mutually independent leaves, launched in
   // order; {first ticket, count, kind (0 whole, 1 coset), coset ranges: the
   // most warp groups of lane cosets a ticket of the range has}
@@ -206,7 +209,10 @@ struct Plan {
 
 // Ring-dependent planning parameters.
 struct RingShape {
-  bool fermat = true;  // false: negacyclic
+  bool fermat = true;  // false: negacyclic (or prime)
+  // prime rings (one u64 per coefficient): up to this many identical leaves
+  // on adjacent coefficients share a ticket (Planner::group_leaves)
+  u32 group = 1;
   u64 M = 0;           // root order
   unsigned max_leaf_ell = 3;
   u64 elem_bytes = 0;          // bytes per coefficient (for L2 batching)
@@ -779,8 +785,10 @@ class Planner {
       if (rs_.wave_engine)  // (top phase, wave, kind): every range is independent
         return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k), (u64)wave_kind(classes_[leaves_[x].cls]),
                                std::get<3>(k), std::get<4>(k));
+      // (grouped small-coefficient plans: a wave's leaves are independent --
+      // ordered by element address, adjacent columns become consecutive tickets)
       return std::make_tuple(std::get<0>(k), (u64)std::get<2>(k) + (u64)(W - ov) * std::get<1>(k), std::get<1>(k),
-                             std::get<3>(k), std::get<4>(k));
+                             rs_.group > 1 ? leaves_[x].base : std::get<3>(k), std::get<4>(k));
     };
     std::stable_sort(idx.begin(), idx.end(), [&](u32 x, u32 y) { return rank(x) < rank(y); });
     p.waves.clear();
@@ -807,12 +815,36 @@ class Planner {
       p.leaves.push_back(leaves_[i]);
       p.leaf_wave.push_back(std::get<2>(keys_[i]));
     }
+    if (rs_.group > 1 && !rs_.wave_engine) group_leaves(p);
     p.classes = std::move(classes_);
     p.counters = std::move(counters_);
     p.max_ell = max_ell_;
     p.max_slot_area = max_area_;
     p.coset = coset_used_;
     p.extent = extent_;
+  }
+
+  // Small coefficients (one u64): consecutive leaves of one class on adjacent
+  // coefficients (base, base + 1, ...: the columns u, u+1, ... of one phase,
+  // same stride) share a ticket of up to rs_.group leaves, so that a slot
+  // access covers whole 32-byte sectors (PAPER.md:837-839 processes several
+  // columns at once for the same reason).  Each member keeps its own weight,
+  // dependency and completion counter.
+  void group_leaves(Plan& p) const {
+    p.groups.clear();
+    for (size_t t = 0; t < p.leaves.size();) {
+      const DevLeaf& g = p.leaves[t];
+      size_t n = 1;
+      while (n < rs_.group && t + n < p.leaves.size()) {
+        const DevLeaf& x = p.leaves[t + n];
+        if (x.cls != g.cls || x.stride != g.stride || x.base != g.base + n || p.leaf_wave[t + n] != p.leaf_wave[t])
+          break;
+        ++n;
+      }
+      p.groups.push_back((u32)t);
+      p.groups.push_back((u32)n);
+      t += n;
+    }
   }
 
   // Split for a node: the reference's policy at the top (transform.hpp:83-87),

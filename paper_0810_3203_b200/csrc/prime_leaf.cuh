@@ -36,6 +36,7 @@ struct Args {
   const u64* tw_hi;    // omega^(i 2^lo_bits) 2^64 mod p
   u32 lo_bits;
   u32 slot_bytes;
+  const u32* groups;  // tickets = {first leaf, count} (Plan::groups), or null: one leaf each
 };
 
 __device__ __forceinline__ u64 addp(u64 a, u64 b, u64 p) {
@@ -66,6 +67,7 @@ __device__ __forceinline__ u32 ld_acquire(const u32* c) {
 __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
   extern __shared__ __align__(16) std::uint8_t sm[];
   __shared__ u32 s_ticket;
+  __shared__ u64 s_w[32];  // weights of the ticket's leaves
   const u32 tid = threadIdx.x, nthr = blockDim.x;
   const u64 p = A.p, pinv = A.pinv;
   const u64 lomask = (u64{1} << A.lo_bits) - 1;
@@ -83,42 +85,54 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
     __syncthreads();
     const u32 ticket = s_ticket;
     if (ticket >= A.nleaves) return;
-    const DevLeaf lf = A.leaves[ticket];
+    // a ticket is G >= 1 leaves on adjacent coefficients (Planner::group_leaves):
+    // leaf j starts at base + j, with its own weight, dependency and counter;
+    // slot k of leaf j sits at k G + j
+    const u32 first = A.groups ? A.groups[2 * ticket] : ticket;
+    const u32 G = A.groups ? A.groups[2 * ticket + 1] : 1u;
+    const DevLeaf lf = A.leaves[first];
     const DevClass cl = A.classes[lf.cls];
-    if (lf.dep != kNoDep && tid == 0) {
-      const u32* c = &A.counters[1 + lf.dep];
-      while (ld_acquire(c) < lf.dep_target) __nanosleep(64);
+    if (tid < G) {
+      const DevLeaf lj = A.leaves[first + tid];
+      s_w[tid] = lj.s;
+      if (lj.dep != kNoDep) {
+        const u32* c = &A.counters[1 + lj.dep];
+        while (ld_acquire(c) < lj.dep_target) __nanosleep(64);
+      }
     }
     __syncthreads();
-
+    auto wt = [&](u32 j) -> u64 { return s_w[j] & (A.M - 1); };
     // load through the pre-rotations (the ITFT's spectral inputs)
-    for (u32 k = tid; k < cl.nload; k += nthr) {
-      const u64 v = __ldcg(reinterpret_cast<const u64*>(A.data + (lf.base + (u64)k * lf.stride) * A.elem_bytes));
+    for (u32 idx = tid; idx < cl.nload * G; idx += nthr) {
+      const u32 k = idx / G, j = idx - k * G;
+      const u64 v = __ldcg(reinterpret_cast<const u64*>(A.data + (lf.base + j + (u64)k * lf.stride) * A.elem_bytes));
       if (cl.has_pre) {
         const SymExp P = A.rots[cl.pre_begin + k];
-        slot[k] = twiddle(v, (P.a * lf.s + P.b) & (A.M - 1));
+        slot[idx] = twiddle(v, (P.a * wt(j) + P.b) & (A.M - 1));
       } else {
-        slot[k] = v;
+        slot[idx] = v;
       }
     }
     __syncthreads();
 
-    const u32 ops_per_batch = nthr * kTasksPerThread;
+    // tasks = (op, leaf j), j fastest
+    const u32 tasks_per_batch = nthr * kTasksPerThread;
     for (u32 l = 0; l < cl.nlevels; ++l) {
       const u32 o0 = A.levels[cl.level_begin + l], o1 = A.levels[cl.level_begin + l + 1];
-      for (u32 ob = o0; ob < o1; ob += ops_per_batch) {
-        const u32 oe = min(o1, ob + ops_per_batch);
+      const u32 ntasks = (o1 - o0) * G;
+      for (u32 tb = 0; tb < ntasks; tb += tasks_per_batch) {
         u64 v0[kTasksPerThread], v1[kTasksPerThread];
         u32 sa[kTasksPerThread], sb[kTasksPerThread], mask[kTasksPerThread];
 #pragma unroll
         for (int k = 0; k < kTasksPerThread; ++k) {
           mask[k] = 0;
-          const u32 o = ob + tid + k * nthr;
-          if (o >= oe) continue;
-          const DevOp op = A.ops[o];
-          sa[k] = op.a;
-          sb[k] = op.b;
-          const u64 a = slot[op.a];
+          const u32 task = tb + tid + k * nthr;
+          if (task >= ntasks) continue;
+          const u32 oi = task / G, j = task - oi * G;
+          const DevOp op = A.ops[o0 + oi];
+          sa[k] = op.a * G + j;
+          sb[k] = op.b * G + j;
+          const u64 a = slot[sa[k]];
           switch (op.type) {
             case OP_COPY:
               v1[k] = a;
@@ -133,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
               mask[k] = 1;
               break;
             default: {
-              const u64 b = twiddle(slot[op.b], op.r);
+              const u64 b = twiddle(slot[sb[k]], op.r);
               switch (op.type) {
                 case OP_ADDSUB:
                   v0[k] = addp(a, b, p);
@@ -174,17 +188,18 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
     }
 
     // store through the post-rotations
-    for (u32 k = tid; k < cl.nstore; k += nthr) {
+    for (u32 idx = tid; idx < cl.nstore * G; idx += nthr) {
+      const u32 k = idx / G, j = idx - k * G;
       const SymExp P = A.rots[cl.post_begin + k];
-      u64* dst = reinterpret_cast<u64*>(A.data + (lf.base + (u64)k * lf.stride) * A.elem_bytes);
-      __stcg(dst, twiddle(slot[k], (P.a * lf.s + P.b) & (A.M - 1)));
+      u64* dst = reinterpret_cast<u64*>(A.data + (lf.base + j + (u64)k * lf.stride) * A.elem_bytes);
+      __stcg(dst, twiddle(slot[idx], (P.a * wt(j) + P.b) & (A.M - 1)));
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0 && lf.comp != kNoDep) {
-      // bump the phase counter; the last child of a node's last phase
+    if (tid < G && A.leaves[first + tid].comp != kNoDep) {
+      // bump the leaf's phase counter; the last child of a node's last phase
       // finishes the node and reports to the parent phase in turn
-      u32 k = lf.comp;
+      u32 k = A.leaves[first + tid].comp;
       for (;;) {
         const u32 old = atomicAdd(&A.counters[1 + k], 1u);
         const DevCounter cm = A.cmeta[k];
