@@ -409,13 +409,139 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
     dist.destroy_process_group()
 
 
+PRIME_CONFIG = ("G", 1 << 22, 3_000_000, "Z/pZ Goldilocks (the reference's own ring), L=2^22, z=n=3000000")
+
+
+def run_prime(args) -> None:
+    """--config G: the reference's own ring (RingCtx(p, m), Goldilocks) on the
+    GPU, against the UNMODIFIED reference cf_tft / cf_itft (oracle/_ref, one
+    host core) -- not a BASELINE config; a same-ring comparison with the
+    reference itself.  Rank 0 only (other ranks exit)."""
+    import ctypes as C
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    name, L, z, desc = PRIME_CONFIG
+    n = z
+    P, m = 0xFFFFFFFF00000001, 32
+    byts = tft_bytes(64, L, z, n) + itft_bytes(64, L, n, n, 0)  # 8 bytes per coefficient
+    rng = np.random.default_rng(po.mix_seed(42, 7))
+    host = np.zeros((L, 1), dtype=np.uint64)
+    host[:z, 0] = rng.integers(0, P, size=z, dtype=np.uint64)
+
+    def reference_once():
+        buf = np.ascontiguousarray(host.copy())
+        ptr = buf.ctypes.data_as(po.U64P)
+        c = C.c_uint64(0)
+        t = time.perf_counter()
+        po.ref().ref_tft(P, m, L, 0, z, n, ptr, L, 0, 1, 0, C.byref(c))
+        po.ref().ref_itft(P, m, L, 0, n, n, 0, ptr, L, 0, 1, 0, C.byref(c))
+        return time.perf_counter() - t
+
+    def oracle_once():
+        ring = po.Ring.prime(P, m)
+        buf = host.copy()
+        t = time.perf_counter()
+        ring.tft(buf, L, 0, z, n)
+        ring.itft(buf, L, 0, n, n, 0)
+        return time.perf_counter() - t
+
+    kind = "reference" if po.ref_available() else "port"
+    cpu_once = reference_once if kind == "reference" else oracle_once
+    sample = ("the whole TFT+ITFT, unmodified reference cf_tft/cf_itft (oracle/_ref, built from "
+              "/root/reference/proj/include) on 1 host core" if kind == "reference"
+              else "the whole TFT+ITFT, oracle port on 1 host core (oracle/_ref absent)")
+    common = {"unit": "GB/s", "n_gpus": 1, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+              "dtype": "u64", "data": "synthetic: seeded uniform residues mod p (numpy PCG64)",
+              "metric": f"TFT+ITFT GB/s ({name}: {desc})"}
+    cfg = {"workload": name, "ring": "Z/pZ, p = 2^64 - 2^32 + 1, omega of order 2^32", "L": L, "z": z, "n": n,
+           "coeff_bytes": 8, "algorithmic_bytes_per_step": byts, "parallelism": "single GPU",
+           "l2": "inputs 24 MB: L2-resident between steps (no flush); see DESIGN.md"}
+    if args.impl == "reference":
+        for _ in range(args.warmup):
+            cpu_once()
+        ts = [cpu_once() for _ in range(max(1, args.steps))]
+        v = byts * len(ts) / sum(ts) / 1e9
+        print(json.dumps({"impl": "reference", **common, "value": v, "steps": len(ts), "warmup": args.warmup,
+                          "ms_per_step": 1e3 * sum(ts) / len(ts), "config": cfg,
+                          "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample},
+                          "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+
+    import paper_0810_3203_b200 as cf
+
+    ctx = cf.PrimeRingCtx(m, P)
+    dev = torch.from_numpy(host.view(np.int64)).cuda()
+    view = cf.DeviceView(dev)
+    pt, pi = cf.TransformParams(L, 0, z, n), cf.TransformParams(L, 0, n, n, 0)
+    for _ in range(max(3, args.warmup)):
+        cf.cf_tft(ctx, pt, view)
+        cf.cf_itft(ctx, pi, view)
+    sampler = ClockSampler(0)
+    sampler.start()
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    sampler.begin()
+    e[0].record()
+    launches = 0
+    for _ in range(args.steps):
+        cf.cf_tft(ctx, pt, view)
+        launches += cf.last_launch_count()
+        e[1].record()
+        cf.cf_itft(ctx, pi, view)
+        launches += cf.last_launch_count()
+    e[2].record()
+    torch.cuda.synchronize()
+    sampler.end()
+    clocks = sampler.stop()
+    total = e[0].elapsed_time(e[2])
+    value = byts * args.steps / (total / 1e3) / 1e9
+    peak, peak_kind = hbm_peak()
+    # end to end: pinned inputs in, transforms, outputs out, every step
+    pin_in = torch.from_numpy(host.view(np.int64)).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ek = max(8, args.steps)
+    for _ in range(ek):
+        dev[:z].copy_(pin_in[:z], non_blocking=True)
+        cf.cf_tft(ctx, pt, view)
+        cf.cf_itft(ctx, pi, view)
+        pin_out[:n].copy_(dev[:n], non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / ek
+    cpu = None
+    if not args.no_cpu:
+        cpu_once()
+        ct = cpu_once()
+        cpu = {"value": byts / ct / 1e9, "unit": "GB/s", "cores": 1, "kind": kind, "sample": sample}
+    print(json.dumps({**common, "value": value, "steps": args.steps, "warmup": max(3, args.warmup),
+                      "ms_per_step": total / args.steps, "config": cfg,
+                      "roofline": {"bound": "hbm", "achieved": value, "peak": peak, "unit": "GB/s",
+                                   "frac": value / peak, "peak_kind": peak_kind, "traffic": None,
+                                   "kernel": "prime::leaf_kernel (all kernels of the step)"},
+                      "cpu_baseline": cpu,
+                      "e2e": {"value": byts / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": z * 8,
+                              "d2h_bytes_per_step": n * 8, "steps": ek,
+                              "note": "per step: pinned host -> HBM copy of the z inputs, TFT+ITFT, HBM -> pinned "
+                                      "copy of the n outputs (serial)"},
+                      "gpu_launches": launches, "clocks": clocks}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS) + ["G"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--leaf-limit", type=int, default=0, help="cap on-chip leaves at 2^k (tuning)")
@@ -423,6 +549,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
+    if args.config == "G":  # the reference's own ring, against the reference itself
+        run_prime(args)
+        return
     if args.impl == "reference":
         run_reference(args, args.config)
         return
