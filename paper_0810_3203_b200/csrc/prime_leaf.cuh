@@ -17,7 +17,7 @@
 namespace cftft_b200 {
 namespace prime {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kTasksPerThread = 4;
 
 struct Args {
