@@ -1103,7 +1103,10 @@ int ensure_ntt_tables(cftft_ring* R, cudaStream_t st) {
   const u64 psi = gpow(w32, (u64{1} << 32) / (2 * n));  // order 2n
   const u64 om = gmul(psi, psi);                         // order n
   const u64 psi_inv = gpow(psi, kGold - 2), om_inv = gpow(om, kGold - 2), n_inv = gpow(n % kGold, kGold - 2);
-  std::vector<u64> h((size_t)(3 * n + n / 2), 0);
+  // [0, n) psi^i, [n, 3n/2) omega^j, [2n, 3n) psi^-i / n, [3n, 7n/2) omega^-j, then per-stage
+  // twiddles for the NTT levels (level ls: omega^(j 2^ls), j < n >> (ls+1), at n - (n >> ls)):
+  // forward at 7n/2, inverse at 9n/2 -- contiguous per level, so a warp's reads coalesce
+  std::vector<u64> h((size_t)(11 * n / 2), 0);
   u64 x = 1, y = n_inv;
   for (u64 i = 0; i < n; ++i) {
     h[i] = x;
@@ -1117,6 +1120,16 @@ int ensure_ntt_tables(cftft_ring* R, cudaStream_t st) {
     h[3 * n + j] = y;
     x = gmul(x, om);
     y = gmul(y, om_inv);
+  }
+  for (u64 ls = 0, off = 0; (n >> (ls + 1)) >= 1; off += n >> (ls + 1), ++ls) {
+    const u64 sf = gpow(om, u64{1} << ls), si = gpow(om_inv, u64{1} << ls);
+    u64 a = 1, b = 1;
+    for (u64 j = 0; j < (n >> (ls + 1)); ++j) {
+      h[7 * n / 2 + off + j] = a;
+      h[9 * n / 2 + off + j] = b;
+      a = gmul(a, sf);
+      b = gmul(b, si);
+    }
   }
   CUDA_TRY(cudaMalloc((void**)&R->ntt_tw, h.size() * 8));
   CUDA_TRY(cudaMemcpyAsync(R->ntt_tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
@@ -1155,7 +1168,7 @@ int cftft_gpu_pointwise(const cftft_ring* cring, void* dev_a, const void* dev_b,
   A.logn = (u32)__builtin_ctz(A.D16);
   A.D32 = R->D;
   A.tw = R->ntt_tw;
-  const size_t smem = (size_t)3 * A.D16 * 8;
+  const size_t smem = (size_t)2 * A.D16 * 8;
   CUDA_TRY(cudaFuncSetAttribute(pointwise::fermat_pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem));
   pointwise::fermat_pointwise_kernel<<<(unsigned)count, 512, smem, st>>>(A);

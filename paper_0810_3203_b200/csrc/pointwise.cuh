@@ -130,26 +130,32 @@ struct FermatMulArgs {
 // In-place cyclic NTT of length n in shared memory: DIF (natural -> bit
 // reversed) for the forward transform, DIT (bit reversed -> natural) for the
 // inverse; w = omega_n^j table (n/2 entries) in shared memory.
-__device__ __forceinline__ void ntt_dif(u64* x, const u64* w, u32 n, u32 logn) {
+// ws: per-level twiddle tables in global memory (level ls: omega^(j 2^ls),
+// j < n >> (ls+1), at n - (n >> ls)) -- contiguous in j, so a warp's reads
+// coalesce (the strided w[j << ls] of one table was a 32-way shared-memory
+// bank conflict in the middle levels).
+__device__ __forceinline__ void ntt_dif(u64* x, const u64* ws, u32 n, u32 logn) {
   for (u32 h = n >> 1, ls = 0; h >= 1; h >>= 1, ++ls) {
     const u32 lh = logn - 1 - ls;
+    const u64* w = ws + (n - (n >> ls));
     for (u32 t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
       const u32 grp = t >> lh, j = t & (h - 1);
       const u32 i0 = grp * 2 * h + j, i1 = i0 + h;
       const u64 u = x[i0], v = x[i1];
       x[i0] = g_add(u, v);
-      x[i1] = g_mul(g_sub(u, v), w[j << ls]);
+      x[i1] = g_mul(g_sub(u, v), __ldg(w + j));
     }
     __syncthreads();
   }
 }
-__device__ __forceinline__ void ntt_dit(u64* x, const u64* w, u32 n, u32 logn) {
+__device__ __forceinline__ void ntt_dit(u64* x, const u64* ws, u32 n, u32 logn) {
   for (u32 h = 1, ls = logn - 1; h < n; h <<= 1, --ls) {
     const u32 lh = logn - 1 - ls;
+    const u64* w = ws + (n - (n >> ls));
     for (u32 t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
       const u32 grp = t >> lh, j = t & (h - 1);
       const u32 i0 = grp * 2 * h + j, i1 = i0 + h;
-      const u64 u = x[i0], v = g_mul(x[i1], w[j << ls]);
+      const u64 u = x[i0], v = g_mul(x[i1], __ldg(w + j));
       x[i0] = g_add(u, v);
       x[i1] = g_sub(u, v);
     }
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
   const u32 n = A.D16;
   u64* xa = s_f;
   u64* xb = s_f + n;
-  u64* w = s_f + 2 * n;          // omega^j, n/2 entries
-  u64* wi = w + n / 2;           // omega^-j
+  const u64* w = A.tw + 7 * (u64)n / 2;   // per-level omega^(j 2^ls) (ntt_dif)
+  const u64* wi = A.tw + 9 * (u64)n / 2;  // per-level omega^-(j 2^ls) (ntt_dit)
   std::uint8_t* ea = A.a + (u64)blockIdx.x * A.stride;
   const std::uint8_t* eb = A.b + (u64)blockIdx.x * A.stride;
   const u64* psi = A.tw;                 // psi^i
@@ -225,10 +231,6 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
     }
     __syncthreads();  // all reads of a done before anything is written
   } else {
-    for (u32 j = threadIdx.x; j < n / 2; j += blockDim.x) {
-      w[j] = A.tw[n + j];
-      wi[j] = A.tw[2 * n + n + j];
-    }
     for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
       xa[i] = g_mul((u64)da[i], psi[i]);
       xb[i] = g_mul((u64)db[i], psi[i]);

@@ -12,8 +12,9 @@ from helpers import random_modulus, to_dev  # noqa: E402
 from paper_0810_3203_b200 import polymul as pm  # noqa: E402
 
 
-def timed(fn, reps=3):
-    fn()
+def timed(fn, reps=5, warm=5):
+    for _ in range(warm):  # clocks ramp from idle: warm up before timing
+        fn()
     torch.cuda.synchronize()
     best = 1e9
     for _ in range(reps):
