@@ -103,7 +103,9 @@ def nussbaumer_negacyclic_mul(f: torch.Tensor, g: torch.Tensor, m: int, K: int, 
     in R[z] with R = (Z/mZ)[y]/(y^K+1) (TFT length L = 2s, omega = y), and
     recombine h_j = C_j + y C_{j+s}."""
     assert f.numel() == K * s and g.numel() == K * s
-    ctx = NegacyclicRingCtx(K, m)
+    ctx = _RINGS.get(("negacyclic", K, m))
+    if ctx is None:
+        ctx = _RINGS[("negacyclic", K, m)] = NegacyclicRingCtx(K, m)
     A = f.view(K, s).t().contiguous()  # A[j][k] = f[j + s k]
     B = g.view(K, s).t().contiguous()
     Cz = poly_mul(ctx, A, B, s, s, policy, stats)  # 2s - 1 elements of R
@@ -119,6 +121,19 @@ def nussbaumer_negacyclic_mul(f: torch.Tensor, g: torch.Tensor, m: int, K: int, 
 
 # ---------------------------------------------------------------------------
 # config 4: Schoenhage-Strassen
+
+
+_RINGS: dict = {}
+
+
+def _fermat_ring(N: int) -> "FermatRingCtx":
+    """One ring context per N, kept: a ring owns its plan cache and scratch
+    (the reference's callers likewise build a RingCtx once, field.hpp:84-100),
+    so repeated products re-plan nothing."""
+    r = _RINGS.get(("fermat", N))
+    if r is None:
+        r = _RINGS[("fermat", N)] = FermatRingCtx(N)
+    return r
 
 
 def ss_ring_bits(L: int, out_bits: int) -> int:
@@ -143,7 +158,7 @@ def ss_mul(F: torch.Tensor, G: torch.Tensor, coeff_bits: int, policy=SplitPolicy
         L <<= 1
     out_bits = 2 * coeff_bits + (min(zf, zg)).bit_length()
     N = ss_ring_bits(L, out_bits)
-    ctx = FermatRingCtx(N)
+    ctx = _fermat_ring(N)
     W = ctx.element_words
     limbs = F.shape[1]
     A = torch.zeros((zf, W), dtype=torch.int64, device=F.device)
