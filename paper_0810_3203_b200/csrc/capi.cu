@@ -1197,6 +1197,20 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   if (count == 0) return CFTFT_OK;
   auto* R = const_cast<cftft_ring*>(cring);
   auto st = static_cast<cudaStream_t>(stream);
+  if (R->kind == CFTFT_RING_FERMAT && (u64)R->D * 12 <= 200 * 1024) {
+    // one CTA per element: word-parallel shift, serial borrow (rotate_kernel)
+    const size_t sm = (size_t)R->D * 12;
+    static size_t rattr = 0;
+    if (sm > 48 * 1024 && sm > rattr) {
+      CUDA_TRY(cudaFuncSetAttribute(fermat::rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      rattr = sm;
+    }
+    fermat::rotate_kernel<<<(unsigned)count, 256, sm, st>>>(static_cast<std::uint8_t*>(dev_base), elem_stride_bytes,
+                                                            e, R->D);
+    CUDA_TRY(cudaGetLastError());
+    g_last_launches = 1;
+    return CFTFT_OK;
+  }
   // A scale is a degenerate plan: one length-1 class (load, no ops, store
   // with rotation e) and one leaf per element.
   const u64 M = R->M;

@@ -1215,6 +1215,120 @@ __global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 coun
   canon_element(data + e * elem_bytes, D);
 }
 
+// x <- x * 2^e mod 2^N + 1 for `count` canonical elements (x in [0, 2^N],
+// the top word 1 only for 2^N == -1): one CTA per element.  With t = e mod N,
+// x 2^t = (lo << t mod 2^N) - (lo >> (N - t)) - top 2^t: the shifted words in
+// parallel, the borrow chain serially (canon_element), then a negation when
+// e mod 2N >= N (2^N == -1).  poly_mul's 1/L = 2^(2N - ell) (polymul.hpp:82-87).
+__global__ void __launch_bounds__(256) rotate_kernel(std::uint8_t* base, u64 stride, u64 e, u32 D) {
+  extern __shared__ u32 s_x[];  // lo (D words), difference (D), borrow generate flags (D)
+  u32* const s_d = s_x + D;
+  u32* const s_b = s_x + 2 * D;
+  std::uint8_t* el = base + (u64)blockIdx.x * stride;
+  u32* w = reinterpret_cast<u32*>(el);
+  long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
+  const u64 N = 32ull * D;
+  e %= 2 * N;
+  const bool neg = e >= N;
+  const u64 t = neg ? e - N : e;
+  const u32 ws = (u32)(t >> 5), b = (u32)(t & 31);
+  const u32 nT = (u32)((t + 31) >> 5);
+  const long long top = *hip;
+  for (u32 i = threadIdx.x; i < D; i += blockDim.x) s_x[i] = w[i];
+  __syncthreads();
+  if (top != 0) {
+    // x = 2^N == -1 (lo = 0): x 2^t = -2^t = (2^N - 2^t) - 2^N, or 2^N for t = 0
+    for (u32 i = threadIdx.x; i < D; i += blockDim.x)
+      w[i] = t == 0 ? 0u : i < ws ? 0u : (i == ws ? (0xFFFFFFFFu << b) : 0xFFFFFFFFu);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *hip = t ? -1 : 1;
+      canon_element(el, D);
+    }
+  } else {
+    // d = A - S word by word: A = lo << t mod 2^N, S = lo >> (N - t) (t bits);
+    // the borrows by a block scan of (generate, propagate) over word chunks
+    const u32 per = (D + blockDim.x - 1) / blockDim.x;
+    const u32 i0 = min(D, threadIdx.x * per), i1 = min(D, i0 + per);
+    u32 G = 0, P = 1;
+    for (u32 i = i0; i < i1; ++i) {
+      const u32 x0 = i >= ws ? s_x[i - ws] : 0u;
+      const u32 x1 = i >= ws + 1 ? s_x[i - ws - 1] : 0u;
+      const u32 a = b ? (x0 << b) | (x1 >> (32 - b)) : x0;
+      u32 sv = 0;
+      if (i < nT) {
+        const u64 st = N - t + 32ull * i;
+        const u32 q = (u32)(st >> 5), sh = (u32)(st & 31);
+        const u32 l0 = q < D ? s_x[q] : 0u, l1 = q + 1 < D ? s_x[q + 1] : 0u;
+        sv = sh ? (l0 >> sh) | (l1 << (32 - sh)) : l0;
+      }
+      const u32 d = a - sv, g = a < sv, pr = d == 0;
+      s_d[i] = d;
+      s_b[i] = g;
+      G = g | (pr & G);
+      P &= pr;
+    }
+    // inclusive scan: (lower, upper) -> (upper.G | upper.P & lower.G, both P)
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (u32 o = 1; o < 32; o <<= 1) {
+      const u32 g2 = __shfl_up_sync(0xFFFFFFFFu, G, o), p2 = __shfl_up_sync(0xFFFFFFFFu, P, o);
+      if (lane >= o) {
+        G = G | (P & g2);
+        P &= p2;
+      }
+    }
+    __shared__ u32 s_wg[32], s_wp[32];
+    if (lane == 31) {
+      s_wg[warp] = G;
+      s_wp[warp] = P;
+    }
+    __syncthreads();
+    u32 pre = 0;  // borrow out of all earlier warps
+    for (u32 k = 0; k < warp; ++k) pre = s_wg[k] | (s_wp[k] & pre);
+    const u32 ex = __shfl_up_sync(0xFFFFFFFFu, G | (P & pre), 1);  // inclusive through lane - 1
+    u32 bin = lane ? ex : pre;
+    for (u32 i = i0; i < i1; ++i) {
+      const u32 d = s_d[i];
+      s_d[i] = d - bin;
+      bin = s_b[i] | (d == 0 && bin);
+    }
+    __shared__ u32 s_out;
+    if (threadIdx.x == blockDim.x - 1) s_out = bin;  // borrow out of the top word
+    __syncthreads();
+    const long long out = s_out;
+    for (u32 i = threadIdx.x; i < D; i += blockDim.x) w[i] = s_d[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *hip = -out;  // value = lo - out 2^N
+      canon_element(el, D);
+    }
+  }
+  if (!neg) return;
+  __syncthreads();
+  // -x = 2^N + 1 - x (x canonical): 0 -> 0, 2^N -> 1, else ~lo + 2
+  const long long h = *hip;
+  int nz = 0;
+  for (u32 i = threadIdx.x; i < D; i += blockDim.x) nz |= w[i] != 0;
+  nz = __syncthreads_or(nz);
+  if (h) {
+    for (u32 i = threadIdx.x; i < D; i += blockDim.x) w[i] = i == 0 ? 1u : 0u;
+    if (threadIdx.x == 0) *hip = 0;
+    return;
+  }
+  if (!nz) return;
+  for (u32 i = threadIdx.x; i < D; i += blockDim.x) w[i] = ~w[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 c = 2;
+    for (u32 i = 0; i < D && c; ++i) {
+      const u64 v = (u64)w[i] + c;
+      w[i] = (u32)v;
+      c = v >> 32;
+    }
+    *hip = c ? 1 : 0;  // only for x = 1: ~1 + 2 = 2^N
+  }
+}
+
 // Outputs the schedule left in the shadow buffer: element (lanes, top word)
 // and its tops row back to the caller's view.
 __global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2, u64 eb, int* T, u64 tloc, u32 CL,

@@ -317,3 +317,38 @@ def test_fermat_wide_sweep(N):
         if 1 <= n2 + f <= L:
             _fermat_case(ctx, ring, N, L, z, n2, s, pol, seed=700 + trial, inverse=True, f=f,
                          special=(trial % 3 == 1))
+
+
+@pytest.mark.parametrize("N", [128, 1024, 65536])
+def test_fermat_scale_exponents(N):
+    """cf.scale (x 2^e mod 2^N + 1, poly_mul's 1/L, polymul.hpp:82-87) against
+    Python integers: random and edge values (0, 1, 2^N == -1, all-ones, single
+    high bit) under exponents on and around 0, N and 2N, and random ones."""
+    ctx = cf.FermatRingCtx(N)
+    W, lim = ctx.element_words, N // 64
+    rng = np.random.default_rng(N)
+    count = 48
+    mod = (1 << N) + 1
+    exps = [0, 1, 31, 32, 33, N - 1, N, N + 1, N + 32, 2 * N - 1, 2 * N - 10, 2 * N, 5 * N + 3]
+    exps += [int(x) for x in rng.integers(0, 4 * N, size=4)]
+    for e in exps:
+        buf = np.zeros((count, W), dtype=np.uint64)
+        buf[:, :lim] = rng.integers(0, 1 << 63, size=(count, lim), dtype=np.uint64) * 2 + rng.integers(
+            0, 2, size=(count, lim), dtype=np.uint64
+        )
+        buf[0, :] = 0
+        buf[1, :] = 0
+        buf[1, 0] = 1
+        buf[2, :] = 0
+        buf[2, lim] = 1  # 2^N
+        buf[3, :lim] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        buf[4, :lim] = 0
+        buf[4, lim - 1] = np.uint64(1 << 63)
+        vals = [sum(int(buf[i, j]) << (64 * j) for j in range(lim)) + (int(buf[i, lim]) << N) for i in range(count)]
+        dev = to_dev(buf)
+        cf.scale(ctx, cf.DeviceView(dev), count, e)
+        got = from_dev(dev)
+        for i in range(count):
+            want = vals[i] * pow(2, e, mod) % mod
+            have = sum(int(got[i, j]) << (64 * j) for j in range(lim)) + (int(got[i, lim]) << N)
+            assert int(got[i, lim]) in (0, 1) and have == want, (N, e, i)
