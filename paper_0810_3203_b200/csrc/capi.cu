@@ -709,7 +709,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         // (with the sub-lane rotations the outputs' last writers deferred)
         const size_t fsm = dp.final_rot ? (size_t)R->D * 4 : 0;
         static size_t fattr = 0;
-        if (fsm > 48 * 1024 && fsm > fattr) {
+        if (fsm > 40 * 1024 && fsm > fattr) {
           CUDA_TRY(cudaFuncSetAttribute(fermat::cs_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)fsm));
           fattr = fsm;
@@ -1198,10 +1198,10 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   auto* R = const_cast<cftft_ring*>(cring);
   auto st = static_cast<cudaStream_t>(stream);
   if (R->kind == CFTFT_RING_FERMAT && (u64)R->D * 12 <= 200 * 1024) {
-    // one CTA per element: word-parallel shift, serial borrow (rotate_kernel)
+    // one CTA per element: word-parallel shift, block-scan borrows (rotate_kernel)
     const size_t sm = (size_t)R->D * 12;
     static size_t rattr = 0;
-    if (sm > 48 * 1024 && sm > rattr) {
+    if (sm > 40 * 1024 && sm > rattr) {  // with the static scan scratch
       CUDA_TRY(cudaFuncSetAttribute(fermat::rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       rattr = sm;
     }

@@ -1398,33 +1398,72 @@ __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb
     }
     s_pend[p] = co;
   }
-  // carries out of a lane are rare (a lane of all ones / all zeros): settle
-  // them serially, the top lane's going to the element top word
+  // carries out of a lane come from a lane of all ones / all zeros (sparse
+  // values: every high lane).  A lane passes carry x in {-1, 0, 1} on as
+  // own + [x = 1, lane all ones] - [x = -1, lane all zeros]; those maps are
+  // composed by a block scan over per-thread lane chunks, then every lane
+  // takes its carry; the top lane's goes to the element top word
   int any = 0;
   for (u32 p = threadIdx.x; p < CL; p += blockDim.x) any |= s_pend[p];
   if (!__syncthreads_or(any)) {
     if (threadIdx.x == 0) *hip = 0;  // lo is canonical: every lane in [0, 2^lane)
-  } else if (threadIdx.x == 0) {
-    long long h = 0;
-    for (u32 p = 0; p < CL; ++p) {
-      long long c = s_pend[p];
-      if (!c) continue;
-      for (u32 q = p + 1; c; ++q) {
-        if (q == CL) {
-          h += c;
-          break;
-        }
-        u32* lw = w + (u64)q * CW;
+  } else {
+    // map m: 2-bit fields m(x) + 1 at bit 2 (x + 1); identity 0x24
+    auto apply = [](u32 m, int x) { return (int)((m >> (2 * (x + 1))) & 3u) - 1; };
+    auto compose = [&](u32 lo, u32 up) {  // up after lo
+      u32 r = 0;
+      for (int x = -1; x <= 1; ++x) r |= (u32)(apply(up, apply(lo, x)) + 1) << (2 * (x + 1));
+      return r;
+    };
+    const u32 per = (CL + blockDim.x - 1) / blockDim.x;
+    const u32 p0 = min(CL, threadIdx.x * per), p1 = min(CL, p0 + per);
+    u32 M = 0x24;
+    for (u32 p = p0; p < p1; ++p) {
+      const u32* lw = w + (u64)p * CW;
+      u32 and_ = 0xFFFFFFFFu, or_ = 0;
+      for (u32 k = 0; k < CW; ++k) {
+        and_ &= lw[k];
+        or_ |= lw[k];
+      }
+      const int own = s_pend[p];
+      const int fm = own - (or_ == 0 ? 1 : 0), fp = own + (and_ == 0xFFFFFFFFu ? 1 : 0);
+      M = compose(M, (u32)(fm + 1) | ((u32)(own + 1) << 2) | ((u32)(fp + 1) << 4));
+    }
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (u32 d = 1; d < 32; d <<= 1) {
+      const u32 m2 = __shfl_up_sync(0xFFFFFFFFu, M, d);
+      if (lane >= d) M = compose(m2, M);
+    }
+    __shared__ u32 s_wm[32];
+    if (lane == 31) s_wm[warp] = M;
+    __syncthreads();
+    int pre = 0;  // carry into this warp's first lane
+    for (u32 k = 0; k < warp; ++k) pre = apply(s_wm[k], pre);
+    const int incl = apply(M, pre);
+    const int up = __shfl_up_sync(0xFFFFFFFFu, incl, 1);
+    int x = lane ? up : pre;
+    for (u32 p = p0; p < p1; ++p) {
+      if (x) {
+        u32* lw = w + (u64)p * CW;
+        long long c = x;
         for (u32 k = 0; k < CW && c; ++k) {
-          long long v = (long long)lw[k] + c;
+          const long long v = (long long)lw[k] + c;
           lw[k] = (u32)v;
           c = v >> 32;
         }
+        x = s_pend[p] + (int)c;
+      } else {
+        x = s_pend[p];
       }
     }
-    // value = lo + h 2^N; the lane-0 term already took the old element top
-    *hip = h;
-    canon_element(el, D);
+    __shared__ int s_h;
+    if (threadIdx.x == blockDim.x - 1) s_h = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // value = lo + h 2^N; the lane-0 term already took the old element top
+      *hip = s_h;
+      canon_element(el, D);
+    }
   }
   if (!o) return;
   __syncthreads();

@@ -352,3 +352,37 @@ def test_fermat_scale_exponents(N):
             want = vals[i] * pow(2, e, mod) % mod
             have = sum(int(got[i, j]) << (64 * j) for j in range(lim)) + (int(got[i, lim]) << N)
             assert int(got[i, lim]) in (0, 1) and have == want, (N, e, i)
+
+
+@pytest.mark.parametrize("N", [256, 4096])
+def test_fermat_sparse_values_carry_chains(N):
+    """Small and sparse coefficients (0, 1, 2^N == -1, a few low bits): the
+    outputs of the ITFT are mostly zero lanes, so the fold's carries run
+    across whole elements in both directions -- TFT and ITFT against the
+    oracle, then ITFT(TFT(a)) = L a (transform.hpp:266-272)."""
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    W, lim = ctx.element_words, N // 64
+    rng = np.random.default_rng(N + 3)
+    for L, z in ((64, 64), (512, 300)):
+        buf = np.zeros((L, W), dtype=np.uint64)
+        buf[:z, 0] = rng.integers(0, 1 << 20, size=z, dtype=np.uint64)
+        buf[: z : 7, 0] = 0
+        buf[1:z:11, 0] = 0
+        buf[1:z:11, lim] = 1  # 2^N
+        buf[2:z:13, 0] = 1
+        want = buf.copy()
+        ring.tft(want, L, 0, z, z, 0)
+        dev = to_dev(buf)
+        view = cf.DeviceView(dev)
+        cf.cf_tft(ctx, cf.TransformParams(L, 0, z, z), view)
+        assert np.array_equal(from_dev(dev)[:z, : lim + 1], want[:z, : lim + 1]), (N, L, z)
+        ring.itft(want, L, 0, z, z, 0, 0)
+        cf.cf_itft(ctx, cf.TransformParams(L, 0, z, z, 0), view)
+        got = from_dev(dev)
+        assert np.array_equal(got[:z, : lim + 1], want[:z, : lim + 1]), (N, L, z, "itft")
+        mod = (1 << N) + 1
+        for i in range(z):
+            a = int(buf[i, 0]) + (int(buf[i, lim]) << N)
+            have = sum(int(got[i, j]) << (64 * j) for j in range(lim)) + (int(got[i, lim]) << N)
+            assert have == (L * a) % mod, (N, L, i)
