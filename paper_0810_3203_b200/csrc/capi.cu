@@ -1199,7 +1199,7 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   auto st = static_cast<cudaStream_t>(stream);
   if (R->kind == CFTFT_RING_FERMAT && (u64)R->D * 12 <= 200 * 1024) {
     // one CTA per element: word-parallel shift, block-scan borrows (rotate_kernel)
-    const size_t sm = (size_t)R->D * 12;
+    const size_t sm = (size_t)R->D * 12 + 128;  // + borrow masks of a small ring
     static size_t rattr = 0;
     if (sm > 40 * 1024 && sm > rattr) {  // with the static scan scratch
       CUDA_TRY(cudaFuncSetAttribute(fermat::rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

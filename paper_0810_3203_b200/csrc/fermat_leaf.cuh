@@ -1218,10 +1218,10 @@ __global__ void canonicalize_kernel(std::uint8_t* data, u64 elem_bytes, u64 coun
 // x <- x * 2^e mod 2^N + 1 for `count` canonical elements (x in [0, 2^N],
 // the top word 1 only for 2^N == -1): one CTA per element.  With t = e mod N,
 // x 2^t = (lo << t mod 2^N) - (lo >> (N - t)) - top 2^t: the shifted words in
-// parallel, the borrow chain serially (canon_element), then a negation when
-// e mod 2N >= N (2^N == -1).  poly_mul's 1/L = 2^(2N - ell) (polymul.hpp:82-87).
+// parallel, the borrow chain by a block scan; for e mod 2N >= N (2^N == -1)
+// the difference is taken the other way round.  poly_mul's 1/L = 2^(2N - ell) (polymul.hpp:82-87).
 __global__ void __launch_bounds__(256) rotate_kernel(std::uint8_t* base, u64 stride, u64 e, u32 D) {
-  extern __shared__ u32 s_x[];  // lo (D words), difference (D), borrow generate flags (D)
+  extern __shared__ u32 s_x[];  // lo (D words), difference (D), borrow masks (<= D)
   u32* const s_d = s_x + D;
   u32* const s_b = s_x + 2 * D;
   std::uint8_t* el = base + (u64)blockIdx.x * stride;
@@ -1246,54 +1246,61 @@ __global__ void __launch_bounds__(256) rotate_kernel(std::uint8_t* base, u64 str
       canon_element(el, D);
     }
   } else {
-    // d = A - S word by word: A = lo << t mod 2^N, S = lo >> (N - t) (t bits);
-    // the borrows by a block scan of (generate, propagate) over word chunks
-    const u32 per = (D + blockDim.x - 1) / blockDim.x;
-    const u32 i0 = min(D, threadIdx.x * per), i1 = min(D, i0 + per);
-    u32 G = 0, P = 1;
-    for (u32 i = i0; i < i1; ++i) {
-      const u32 x0 = i >= ws ? s_x[i - ws] : 0u;
-      const u32 x1 = i >= ws + 1 ? s_x[i - ws - 1] : 0u;
-      const u32 a = b ? (x0 << b) | (x1 >> (32 - b)) : x0;
-      u32 sv = 0;
-      if (i < nT) {
-        const u64 st = N - t + 32ull * i;
-        const u32 q = (u32)(st >> 5), sh = (u32)(st & 31);
-        const u32 l0 = q < D ? s_x[q] : 0u, l1 = q + 1 < D ? s_x[q + 1] : 0u;
-        sv = sh ? (l0 >> sh) | (l1 << (32 - sh)) : l0;
+    // d = A - S word by word: A = lo << t mod 2^N, S = lo >> (N - t) (t bits).
+    // Borrows: each warp owns a contiguous segment, 32 words a step; within a
+    // step the borrow-in bits are the carries of (g | p) + g + cin (g: word
+    // borrows, p: word is zero), across warps a scan of segment maps.
+    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const u32 seg = ((D + nw * 32 - 1) / (nw * 32)) * 32, steps = seg >> 5;
+    u32* const s_g = s_b;              // D / 32 + steps * nw masks
+    u32* const s_p = s_b + steps * nw;  // (fits in the D-word flag area)
+    u32 c0 = 0, c1 = 1;  // segment borrow out for borrow in 0 / 1
+    for (u32 k = 0; k < steps; ++k) {
+      const u32 i = warp * seg + k * 32 + lane;
+      u32 g = 0, pr = 1;
+      if (i < D) {
+        const u32 x0 = i >= ws ? s_x[i - ws] : 0u;
+        const u32 x1 = i >= ws + 1 ? s_x[i - ws - 1] : 0u;
+        const u32 a = b ? (x0 << b) | (x1 >> (32 - b)) : x0;
+        u32 sv = 0;
+        if (i < nT) {
+          const u64 st = N - t + 32ull * i;
+          const u32 q = (u32)(st >> 5), sh = (u32)(st & 31);
+          const u32 l0 = q < D ? s_x[q] : 0u, l1 = q + 1 < D ? s_x[q + 1] : 0u;
+          sv = sh ? (l0 >> sh) | (l1 << (32 - sh)) : l0;
+        }
+        // e mod 2N >= N: x 2^e = -(A - S) = S - A
+        const u32 d = neg ? sv - a : a - sv;
+        s_d[i] = d;
+        g = neg ? sv < a : a < sv;
+        pr = d == 0;
       }
-      const u32 d = a - sv, g = a < sv, pr = d == 0;
-      s_d[i] = d;
-      s_b[i] = g;
-      G = g | (pr & G);
-      P &= pr;
-    }
-    // inclusive scan: (lower, upper) -> (upper.G | upper.P & lower.G, both P)
-    const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (u32 o = 1; o < 32; o <<= 1) {
-      const u32 g2 = __shfl_up_sync(0xFFFFFFFFu, G, o), p2 = __shfl_up_sync(0xFFFFFFFFu, P, o);
-      if (lane >= o) {
-        G = G | (P & g2);
-        P &= p2;
+      const u32 gm = __ballot_sync(0xFFFFFFFFu, g), pm = __ballot_sync(0xFFFFFFFFu, pr);
+      if (lane == 0) {
+        s_g[warp * steps + k] = gm;
+        s_p[warp * steps + k] = pm;
       }
+      c0 = (u32)(((u64)(gm | pm) + gm + c0) >> 32);
+      c1 = (u32)(((u64)(gm | pm) + gm + c1) >> 32);
     }
-    __shared__ u32 s_wg[32], s_wp[32];
-    if (lane == 31) {
-      s_wg[warp] = G;
-      s_wp[warp] = P;
+    __shared__ u32 s_c0[32], s_c1[32];
+    if (lane == 0) {
+      s_c0[warp] = c0;
+      s_c1[warp] = c1;
     }
     __syncthreads();
-    u32 pre = 0;  // borrow out of all earlier warps
-    for (u32 k = 0; k < warp; ++k) pre = s_wg[k] | (s_wp[k] & pre);
-    const u32 ex = __shfl_up_sync(0xFFFFFFFFu, G | (P & pre), 1);  // inclusive through lane - 1
-    u32 bin = lane ? ex : pre;
-    for (u32 i = i0; i < i1; ++i) {
-      const u32 d = s_d[i];
-      s_d[i] = d - bin;
-      bin = s_b[i] | (d == 0 && bin);
+    u32 c = 0;
+    for (u32 k = 0; k < warp; ++k) c = c ? s_c1[k] : s_c0[k];
+    for (u32 k = 0; k < steps; ++k) {
+      const u32 i = warp * seg + k * 32 + lane;
+      const u32 gm = s_g[warp * steps + k], am = gm | s_p[warp * steps + k];
+      const u64 sum = (u64)am + gm + c;
+      const u32 bin = (((u32)sum ^ am ^ gm) >> lane) & 1u;
+      c = (u32)(sum >> 32);
+      if (i < D) s_d[i] -= bin;
     }
     __shared__ u32 s_out;
-    if (threadIdx.x == blockDim.x - 1) s_out = bin;  // borrow out of the top word
+    if (threadIdx.x == blockDim.x - 1) s_out = c;  // borrow out of the top word
     __syncthreads();
     const long long out = s_out;
     for (u32 i = threadIdx.x; i < D; i += blockDim.x) w[i] = s_d[i];
@@ -1303,7 +1310,7 @@ __global__ void __launch_bounds__(256) rotate_kernel(std::uint8_t* base, u64 str
       canon_element(el, D);
     }
   }
-  if (!neg) return;
+  if (!neg || top == 0) return;  // (the sign is in the difference above)
   __syncthreads();
   // -x = 2^N + 1 - x (x canonical): 0 -> 0, 2^N -> 1, else ~lo + 2
   const long long h = *hip;
