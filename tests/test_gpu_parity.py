@@ -246,8 +246,14 @@ def _dist_single_rank(N, L, z, n):
 
 
 def test_dist_path_on_one_gpu():
-    _dist_single_rank(1024, 1024, 700, 700)
-    _dist_single_rank(4096, 4096, 3000, 3100)
+    import torch.distributed as dist
+
+    try:
+        _dist_single_rank(1024, 1024, 700, 700)
+        _dist_single_rank(4096, 4096, 3000, 3100)
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
 
 
 # ---- coset leaves (carry-save lanes) ---------------------------------------------
