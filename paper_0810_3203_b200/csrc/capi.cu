@@ -23,6 +23,7 @@
 #include "pointwise.cuh"
 #include "wave_coset.cuh"
 #include "wave_wide.cuh"
+#include "wave_tma.cuh"
 #include "planner.hpp"
 
 using namespace cftft_b200;
@@ -65,6 +66,12 @@ struct DevicePlan {
   const u32* wave_ops = nullptr;
   const u32* wave_slots = nullptr;
   const u32* final_rot = nullptr;
+  // per wave: 1 when every leaf is a radix-64 network class the TMA kernel runs
+  std::vector<std::uint8_t> tma_wave;
+  std::vector<u64> tma_desc_off;  // per wave: first descriptor in tma_descs
+  void* tma_descs = nullptr;      // fermat::TmaLeafDesc per leaf of the TMA waves
+  std::uint8_t* tma_lay = nullptr;  // coset-major layout bits per wave_slots entry (inside tma_descs)
+  u32 tma_step = 0;
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
@@ -73,6 +80,7 @@ struct DevicePlan {
   u32 cw = 16, C = 0, slot_bytes = 0, logS = 0;
   ~DevicePlan() {
     if (dbuf) cudaFree(dbuf);
+    if (tma_descs) cudaFree(tma_descs);
   }
 };
 
@@ -84,7 +92,8 @@ struct cftft_ring {
   int kind = 0;
   int coset_cw = -1;          // Fermat coset leaves: -1 auto, 0 off, 4/8/16 lane words
   int wave = -1;              // Fermat wave engine: -1 auto, 0 off, 1 on
-  int wide = -1;              // radix-64 coset leaves (coset_wide_kernel): -1 env CFTFT_WIDE (default off), 0, 1
+  int wide = -1;              // radix-64 coset leaves: -1 env CFTFT_WIDE, 0 off, 1 on (network waves on the TMA
+                              // kernel), 2 on (every wave on coset_wide_kernel)
   unsigned leaf_limit = 0;    // cftft_ring_set_leaf_limit (0: none)
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
@@ -221,6 +230,104 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   dp.wave_ops = reinterpret_cast<const u32*>(b + o_wo);
   dp.wave_slots = reinterpret_cast<const u32*>(b + o_ws);
   dp.final_rot = p.final_rot.empty() ? nullptr : reinterpret_cast<const u32*>(b + o_fr);
+  // radix-64 network waves on the TMA kernel (wave_tma.cuh): 64-slot full
+  // networks over 256-bit lanes with at least two cosets, one item per coset,
+  // stage-A rotations only where the kernel's compile-time mask has them
+  dp.tma_wave.assign(p.waves.size(), 0);
+  std::vector<fermat::TmaLeafDesc> descs;
+  dp.tma_desc_off.assign(p.waves.size(), 0);
+  for (size_t w = 0; w < p.waves.size(); ++w) {
+    const auto& wr = p.waves[w];
+    if (wr[2] != 2 || !wr[1]) continue;
+    bool ok = true;
+    u32 step = 0;
+    for (u64 i = wr[0]; i < wr[0] + wr[1] && ok; ++i) {
+      const DevClass& d = cls[p.leaves[i].cls];
+      ok = d.L == 64 && (d.wnet == 1 || d.wnet == 2) && d.kind == 1 && d.step >= 2 && (d.step & (d.step - 1)) == 0 &&
+           (step == 0 || d.step == step) && wr[3] == d.step;
+      step = d.step;
+      if (!ok) break;
+      const u32 mask = d.wnet == 1 ? fermat::kRotDif : fermat::kRotDit;
+      for (u32 o = 0; o < 192 && ok; ++o) {
+        const u32 wop = p.wave_ops[d.wop_begin + o];
+        if ((wop & 15u) != OP_ADDSUB) ok = false;
+        if (o < 96 && !((mask >> (o % 12)) & 1u) && (wop >> 16) != 0) ok = false;
+      }
+    }
+    if (!ok) continue;
+    dp.tma_wave[w] = 1;
+    dp.tma_step = step;
+    dp.tma_desc_off[w] = descs.size();
+    for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
+      const DevLeaf& lf = p.leaves[i];
+      const DevClass& d = cls[lf.cls];
+      fermat::TmaLeafDesc td{};
+      td.base = lf.base;
+      td.stride = lf.stride;
+      td.c0 = lf.c0;
+      td.wop_begin = d.wop_begin;
+      td.nload = d.nload;
+      td.nstore_wnet = d.nstore | (d.wnet << 16);
+      descs.push_back(td);
+    }
+  }
+  if (!descs.empty()) {
+    // Coset-major intermediate layout: an element written by a TMA wave whose
+    // every later read (until it is written again) is by a TMA wave is stored
+    // coset by coset (coset k = lanes k + step * pos, pos = 0..31, as one 1 KB
+    // chunk), so each slot's coset moves as one bulk copy; everything else --
+    // inputs, outputs, whatever another kernel or the fold reads -- keeps the
+    // natural lane order.  Per slot entry of wave_slots: bit 0 the input is
+    // coset-major, bit 1 the output is.
+    std::vector<std::uint8_t> lay(p.wave_slots.size(), 0);
+    struct Ev {
+      u32 wave;
+      bool tma, rd, wr;
+      u64 slot;  // index into wave_slots (TMA waves)
+    };
+    std::vector<std::vector<Ev>> ev(p.extent);
+    for (size_t w = 0; w < p.waves.size(); ++w) {
+      const auto& wr = p.waves[w];
+      for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
+        const DevLeaf& lf = p.leaves[i];
+        const LeafProgram& c = p.classes[lf.cls];
+        const u32 span = std::max(c.nload, c.nstore);
+        for (u32 k = 0; k < span; ++k) {
+          const u64 e = lf.base + (u64)k * lf.stride;
+          if (e >= ev.size()) continue;
+          ev[e].push_back(Ev{(u32)w, dp.tma_wave[w] != 0, k < c.nload, k < c.nstore, (u64)lf.c0 + 2ull * k});
+        }
+      }
+    }
+    for (auto& es : ev) {
+      std::uint8_t cur = 0;
+      for (size_t a = 0; a < es.size(); ++a) {
+        const Ev& x = es[a];
+        if (x.rd && x.tma) lay[x.slot] |= cur;
+        if (!x.wr) continue;
+        std::uint8_t out = 0;
+        if (x.tma) {
+          bool any = false, all = true;
+          for (size_t b = a + 1; b < es.size(); ++b) {
+            if (es[b].rd) {
+              any = true;
+              all = all && es[b].tma;
+            }
+            if (es[b].wr) break;
+          }
+          out = (any && all) ? 1 : 0;
+          lay[x.slot] |= (std::uint8_t)(out << 1);
+        }
+        cur = out;
+      }
+    }
+    CUDA_TRY(cudaMalloc(&dp.tma_descs, descs.size() * sizeof(fermat::TmaLeafDesc) + lay.size()));
+    CUDA_TRY(cudaMemcpyAsync(dp.tma_descs, descs.data(), descs.size() * sizeof(fermat::TmaLeafDesc),
+                             cudaMemcpyHostToDevice, st));
+    dp.tma_lay = static_cast<std::uint8_t*>(dp.tma_descs) + descs.size() * sizeof(fermat::TmaLeafDesc);
+    CUDA_TRY(cudaMemcpyAsync(dp.tma_lay, lay.data(), lay.size(), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
   (void)R;
   return CFTFT_OK;
 }
@@ -444,6 +551,53 @@ int grid_for(K kernel, int threads, size_t smem, u64 nleaves, unsigned* grid) {
   return CFTFT_OK;
 }
 
+// Dynamic shared memory attribute of a kernel, per device (cudaFuncSetAttribute
+// applies to the current device only).
+template <class K>
+int set_smem_bytes(K kernel, size_t bytes) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_kmu);
+  for (const auto& k : g_kinfo)
+    if (k.dev == dev && k.fn == (const void*)kernel && k.threads == -2 && k.smem >= bytes) return CFTFT_OK;
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  g_kinfo.push_back(KernelInfo{dev, (const void*)kernel, -2, bytes, 0});
+  return CFTFT_OK;
+}
+
+// TMA descriptors of the radix-64 coset kernel (wave_tma.cuh): a buffer of
+// `extent` elements seen as [element][row][word] with rows of `step` 256-bit
+// lanes (32 rows per coefficient) and 8-word x 32-row boxes (one coset).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int encode_fn(EncodeTiledFn* out) {
+  static EncodeTiledFn fn = nullptr;
+  static std::mutex m;
+  std::lock_guard<std::mutex> g(m);
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) return fail(CFTFT_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  *out = fn;
+  return CFTFT_OK;
+}
+int make_coset_map(CUtensorMap* tm, void* base, u64 stride, u64 extent, u32 step) {
+  EncodeTiledFn fn = nullptr;
+  if (int rc = encode_fn(&fn)) return rc;
+  const cuuint64_t gdim[3] = {8ull * step, 32ull, std::max<u64>(extent, 1)};
+  const cuuint64_t gstr[2] = {32ull * step, stride};
+  const cuuint32_t box[3] = {8u, 32u, 1u};
+  const cuuint32_t est[3] = {1u, 1u, 1u};
+  const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CFTFT_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return CFTFT_OK;
+}
+
 // Per-launch scratch (counters, tops arrays, the shadow buffer) comes from the
 // device's stream-ordered pool; keep freed blocks cached instead of returning
 // them to the driver at every synchronisation.
@@ -663,8 +817,27 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
           CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, fermat::coset_wide_kernel<8>,
                                                                  32 * fermat::kWideWarps, xsmem));
         }
-        for (const auto& wr : dp.host.waves) {
-          if (wr[2] == 2) {
+        CUtensorMap tm_view{}, tm_shadow{};
+        bool tma_maps = false;
+        for (size_t wi = 0; wi < dp.host.waves.size(); ++wi) {
+          const auto& wr = dp.host.waves[wi];
+          if (wr[2] == 2 && dp.tma_wave[wi] && R->wide != 2) {
+            if (!tma_maps) {
+              if (int e = make_coset_map(&tm_view, base, stride, dp.host.extent, dp.tma_step)) return e;
+              if (int e = make_coset_map(&tm_shadow, shadow ? (void*)shadow : (void*)base, stride, dp.host.extent,
+                                         dp.tma_step))
+                return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<0>, fermat::kTmaSmem)) return e;
+              tma_maps = true;
+            }
+            W.leaves = dp.leaves + wr[0];
+            W.nleaves = (u32)wr[1];
+            W.gpl = (u32)std::max<u64>(1, wr[3]);
+            W.tdesc = static_cast<const fermat::TmaLeafDesc*>(dp.tma_descs) + dp.tma_desc_off[wi];
+            W.tlay = dp.tma_lay;
+            const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
+            fermat::coset_tma_kernel<0><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+          } else if (wr[2] == 2) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];
             W.gpl = (u32)std::max<u64>(1, wr[3]);
@@ -1050,7 +1223,8 @@ int cftft_ring_set_coset(cftft_ring* ring, int lane_words) {
 
 int cftft_ring_set_wide(cftft_ring* ring, int wide) {
   if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
-  if (wide < -1 || wide > 1) return fail(CFTFT_INVALID_PARAMS, "wide must be -1 (environment), 0 or 1");
+  if (wide < -1 || wide > 2)
+    return fail(CFTFT_INVALID_PARAMS, "wide must be -1 (environment), 0, 1 (TMA kernel) or 2 (CTA kernel only)");
   std::lock_guard<std::mutex> g(ring->mu);
   if (ring->wide != wide) {
     ring->wide = wide;

@@ -45,6 +45,8 @@ struct WaveArgs {
   u32 gpl;              // work items per ticket: its most warp groups (Plan::waves)
   u32 logS, logLanes;   // tops-array lane interleave (fermat_leaf.cuh, tops_ix)
   u32 debug;            // CFTFT_DEBUG_SKIP bits (experiments; results wrong when set)
+  const void* tdesc;    // coset_tma_kernel: per-leaf descriptors of the wave (TmaLeafDesc)
+  const std::uint8_t* tlay;  // coset_tma_kernel: per slot entry of wslots, bit 0 input / bit 1 output coset-major
 };
 __device__ __forceinline__ u32 wave_tix(const WaveArgs& A, u32 p) {
   return ((p & ((1u << A.logS) - 1)) << (A.logLanes - A.logS)) | (p >> A.logS);
