@@ -66,7 +66,8 @@ struct DevicePlan {
   const u32* wave_ops = nullptr;
   const u32* wave_slots = nullptr;
   const u32* final_rot = nullptr;
-  // per wave: 1 when every leaf is a radix-64 network class the TMA kernel runs
+  // per wave: 1 (DIF) / 2 (DIT) when every leaf is a radix-64 network class
+  // of that kind the TMA kernel runs
   std::vector<std::uint8_t> tma_wave;
   std::vector<u64> tma_desc_off;  // per wave: first descriptor in tma_descs
   void* tma_descs = nullptr;      // fermat::TmaLeafDesc per leaf of the TMA waves
@@ -240,11 +241,12 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     const auto& wr = p.waves[w];
     if (wr[2] != 2 || !wr[1]) continue;
     bool ok = true;
-    u32 step = 0;
+    u32 step = 0, wnet = 0;
     for (u64 i = wr[0]; i < wr[0] + wr[1] && ok; ++i) {
       const DevClass& d = cls[p.leaves[i].cls];
       ok = d.L == 64 && (d.wnet == 1 || d.wnet == 2) && d.kind == 1 && d.step >= 2 && (d.step & (d.step - 1)) == 0 &&
-           (step == 0 || d.step == step) && wr[3] == d.step;
+           (step == 0 || d.step == step) && wr[3] == d.step && (wnet == 0 || d.wnet == wnet);
+      wnet = d.wnet;
       step = d.step;
       if (!ok) break;
       const u32 mask = d.wnet == 1 ? fermat::kRotDif : fermat::kRotDit;
@@ -255,7 +257,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
       }
     }
     if (!ok) continue;
-    dp.tma_wave[w] = 1;
+    dp.tma_wave[w] = (std::uint8_t)wnet;
     dp.tma_step = step;
     dp.tma_desc_off[w] = descs.size();
     for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
@@ -319,6 +321,24 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
           lay[x.slot] |= (std::uint8_t)(out << 1);
         }
         cur = out;
+      }
+    }
+    if (getenv("CFTFT_LAY_STATS")) {
+      for (size_t w = 0; w < p.waves.size(); ++w) {
+        if (!dp.tma_wave[w]) continue;
+        const auto& wr = p.waves[w];
+        u64 n = 0, in = 0, out = 0;
+        for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
+          const DevLeaf& lf = p.leaves[i];
+          const LeafProgram& c = p.classes[lf.cls];
+          for (u32 k = 0; k < std::max(c.nload, c.nstore); ++k) {
+            ++n;
+            in += lay[lf.c0 + 2 * k] & 1;
+            out += (lay[lf.c0 + 2 * k] >> 1) & 1;
+          }
+        }
+        fprintf(stderr, "[cftft] wave %zu: %llu slots, coset-major in %llu out %llu\n", w, (unsigned long long)n,
+                (unsigned long long)in, (unsigned long long)out);
       }
     }
     CUDA_TRY(cudaMalloc(&dp.tma_descs, descs.size() * sizeof(fermat::TmaLeafDesc) + lay.size()));
@@ -585,6 +605,12 @@ int encode_fn(EncodeTiledFn* out) {
   *out = fn;
   return CFTFT_OK;
 }
+CUtensorMapL2promotion l2_promotion() {
+  static const int v = getenv("CFTFT_TMA_L2") ? atoi(getenv("CFTFT_TMA_L2")) : 64;
+  return v >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                  : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                             : v >= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
 int make_coset_map(CUtensorMap* tm, void* base, u64 stride, u64 extent, u32 step) {
   EncodeTiledFn fn = nullptr;
   if (int rc = encode_fn(&fn)) return rc;
@@ -593,7 +619,7 @@ int make_coset_map(CUtensorMap* tm, void* base, u64 stride, u64 extent, u32 step
   const cuuint32_t box[3] = {8u, 32u, 1u};
   const cuuint32_t est[3] = {1u, 1u, 1u};
   const CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, gdim, gstr, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_SWIZZLE_32B, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CFTFT_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return CFTFT_OK;
 }
@@ -827,7 +853,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
               if (int e = make_coset_map(&tm_shadow, shadow ? (void*)shadow : (void*)base, stride, dp.host.extent,
                                          dp.tma_step))
                 return e;
-              if (int e = set_smem_bytes(fermat::coset_tma_kernel<0>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<true>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<false>, fermat::kTmaSmem)) return e;
               tma_maps = true;
             }
             W.leaves = dp.leaves + wr[0];
@@ -835,8 +862,12 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             W.tdesc = static_cast<const fermat::TmaLeafDesc*>(dp.tma_descs) + dp.tma_desc_off[wi];
             W.tlay = dp.tma_lay;
+            W.pfdist = 0;
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
-            fermat::coset_tma_kernel<0><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+            if (dp.tma_wave[wi] == 1)
+              fermat::coset_tma_kernel<true><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+            else
+              fermat::coset_tma_kernel<false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
           } else if (wr[2] == 2) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];

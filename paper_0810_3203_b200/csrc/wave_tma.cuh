@@ -1,42 +1,38 @@
 // wave_tma.cuh -- radix-64 coset passes as a TMA-fed, warp-specialised
-// persistent kernel (the default engine for radix-64 network waves).
+// persistent kernel (the engine of radix-64 network waves).
 //
 // Same plan formats as coset_wide_kernel (wave_wide.cuh): one work item =
 // (coset leaf of 64 coefficients, one lane coset c < step); the 64 slots x 32
 // positions of the item are lanes c + step * pos of its coefficients (256-bit
 // lanes, carry-save with an int32 top per lane); the leaf is a full 64-point
 // network (DIF for the TFT, DIT for the ITFT) = two stages of eight 8-point
-// register networks (Planner::wide_network).  What differs is how the data
-// moves and who waits for whom:
+// register networks (Planner::wide_network).
 //
-//  * one CTA per SM, 8 warps; warp w owns stage-A network w and its buffer
-//    of the input ring;
-//  * the inputs of an item arrive by TMA (cp.async.bulk.tensor): per slot one
-//    32-position box of the source coset (and, for a sub-lane pre-rotation,
-//    one box of the coset below it), the 128-byte tops rows and, when a lane
-//    of the item reads source lane 0, the element's top word -- completing on
-//    the network's mbarrier (expect_tx).  Each warp issues its own network's
-//    copies for the CTA's NEXT item as soon as it has read the current one
-//    out of its buffer: a one-item-deep pipeline with no producer warp and no
-//    release barriers;
-//  * a warp settles its 8 slots one at a time (pre-rotation by whole cosets
-//    = a row index; sub-lane part = a funnel of the two boxes; the top word
-//    folded into source lane 0; lanes past 2^N negated) in place in its
-//    buffer, loads them into registers, runs the stage-A network, and after a
-//    CTA barrier the stage-B networks read the exchange tile and store their
-//    outputs straight from registers (post-rotation = the output lane index).
+// One 16-warp CTA per SM, two warp roles, two item tiles:
+//  * stage-A warps 0..7: warp w waits for its item's tile (TMA: every loaded
+//    slot's coset box, its tops and, where needed, the element's top word),
+//    settles its 8 slots straight into registers (pre-rotation by whole
+//    cosets = a row index; a sub-lane part = a funnel with the lane below,
+//    whose rows the warp fetched into its own ring one item ahead; the top
+//    word folded into source lane 0; lanes past 2^N negated), runs its
+//    stage-A network and writes the outputs back in place (its slots are its
+//    own), then arrives on the tile's named barrier;
+//  * stage-B warps 8..15: wait on that barrier, read their 8 slots of the
+//    tile into registers, release the tile (warp 8 immediately refills it
+//    with the item two ahead), run the stage-B network and store straight
+//    from registers through the post-rotation (carry-save, coset-major or
+//    natural order).
+// Stage A of item k+1 overlaps stage B of item k; the loads of item k+2 are
+// in flight during both.  Tiles and coset-major chunks are stored with the
+// 32-byte swizzle (the 16-byte halves of row r swapped when bit 2 of r is
+// set -- CU_TENSOR_MAP_SWIZZLE_32B for tensor boxes, the writers' own
+// addressing for coset-major chunks): a warp's 32 rows hit distinct banks.
 //
 // Shared memory (bytes, 1024-aligned base):
-//   ring rows   8 networks x 16 boxes (8 slots A, 8 slots B) x 1 KB   131072
-//   exchange    64 slots x 32 rows x 32 B                              65536
-//   ring tops   8 networks x 8 slots x (128 B below + 128 B own)       16384
-//   top words   8 networks x 8 slots x 16 B                              1024
-//   exch tops   64 slots x 32 int                                         8192
-//   mbarriers   8 x 8 B                                                     64
-// Rows of 32 bytes are stored with the 32-byte swizzle (the 16-byte half of
-// row r is swapped when bit 2 of r is set: CU_TENSOR_MAP_SWIZZLE_32B for the
-// TMA boxes, the same XOR by hand for the exchange): a warp's 32 lanes reading
-// 32 rows hit distinct banks.
+//   tile t (x2)  rows 64 slots x 1 KB | tops 64 x 128 B | top words 64 x 16 B
+//   ring rows    8 warps x 8 slots x 1 KB   (stage A: the lane-below cosets)
+//   ring tops    8 warps x 8 slots x 128 B
+//   mbarriers    full[2], ring[8]
 #pragma once
 
 #include <cuda.h>
@@ -46,15 +42,18 @@
 namespace cftft_b200 {
 namespace fermat {
 
-constexpr int kTmaNets = 8;                // warps (= networks per stage)
-constexpr int kTmaThreads = 32 * kTmaNets;
-constexpr u32 kTmaRing = 0;  // per slot [B 1 KB | A 1 KB]
-constexpr u32 kTmaExch = kTmaRing + 8u * 16u * 1024u;
-constexpr u32 kTmaRingTops = kTmaExch + 64u * 1024u;
-constexpr u32 kTmaHiw = kTmaRingTops + 8u * 8u * 256u;
-constexpr u32 kTmaExchTops = kTmaHiw + 8u * 8u * 16u;
-constexpr u32 kTmaBars = kTmaExchTops + 64u * 32u * 4u;
-constexpr u32 kTmaSmem = kTmaBars + 8u * 8u + 1024u;  // + alignment slack
+constexpr int kTmaWarpsA = 8;
+constexpr int kTmaThreads = 32 * 2 * kTmaWarpsA;
+constexpr u32 kTileRows = 0;
+constexpr u32 kTileTops = 64u * 1024u;
+constexpr u32 kTileHiw = kTileTops + 64u * 128u;
+constexpr u32 kTileBytes = kTileHiw + 64u * 16u;  // 74752 (a multiple of 1024)
+constexpr u32 kRingRows = 2u * kTileBytes;
+constexpr u32 kRingTops = kRingRows + 64u * 1024u;
+constexpr u32 kSlotTab = kRingTops + 64u * 128u;  // per warp: 8 store descriptors of 32 B
+constexpr u32 kTmaBars = kSlotTab + 128u * 32u;
+constexpr u32 kTmaSmem = kTmaBars + 16u * 8u + 1024u;  // + alignment slack
+static_assert(kTileBytes % 1024u == 0, "tile alignment");
 
 __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
@@ -69,7 +68,7 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
@@ -87,12 +86,18 @@ __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u3
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void pf_box(const CUtensorMap* tm, u32 cls, u32 e) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(tm), "r"(8u * cls), "r"(0u),
+               "r"(e)
+               : "memory");
+}
+__device__ __forceinline__ void pf_bulk(const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void named_bar(u32 id, u32 n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
-// 32-byte row r of a tile: 16-byte half h at 32 r + 16 h (coset-major chunks
-// arrive as plain 1 KB copies, so the tiles are linear; a warp reading 32 rows
-// pays a 2-way bank conflict)
-__device__ __forceinline__ u32 sw_off(u32 r, u32 h) { return 32u * r + 16u * h; }
+// 32-byte row r of a tile: 16-byte half h at 32 r + 16 (h ^ bit 2 of r)
+__device__ __forceinline__ u32 sw_off(u32 r, u32 h) { return 32u * r + 16u * (h ^ ((r >> 2) & 1u)); }
 __device__ __forceinline__ void lds_row(Ch<8>& c, u32 tile, u32 r) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
                : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3])
@@ -248,169 +253,202 @@ static_assert(sizeof(TmaLeafDesc) == 32, "TmaLeafDesc layout");
 __device__ __forceinline__ u32 slot_a(u32 wnet, u32 w, u32 j) { return wnet == 2 ? 8u * w + j : w + 8u * j; }
 __device__ __forceinline__ u32 slot_b(u32 wnet, u32 w, u32 j) { return wnet == 2 ? w + 8u * j : 8u * w + j; }
 
-// Per-lane registers of an item: lanes 0..7 the stage-A slots, lanes 8..15
-// the stage-B slots of this warp's networks (with their output addresses);
-// lanes < 12 the packed ops of both networks.
-struct TmaLane {
-  u32 pre, post;
-  u64 e;
-  u32 opa, opb;
-  u32 lay;  // bit 0: the slot's input is coset-major, bit 1: its output is
-};
-__device__ __forceinline__ TmaLane tma_lane(const WaveArgs& A, const TmaLeafDesc& d, bool valid, u32 w, u32 lane) {
-  TmaLane l{};
-  if (!valid) return l;
-  const u32 wnet = d.nstore_wnet >> 16;
-  if (lane < 16) {
-    const u32 j = lane & 7u;
-    const u32 slot = lane < 8 ? slot_a(wnet, w, j) : slot_b(wnet, w, j);
-    l.e = d.base + (u64)slot * d.stride;
-    if (slot < max(d.nload, d.nstore_wnet & 0xFFFFu)) {
-      l.pre = __ldg(A.wslots + d.c0 + 2 * slot);
-      l.post = __ldg(A.wslots + d.c0 + 2 * slot + 1);
-      l.lay = __ldg(A.tlay + d.c0 + 2 * slot);
-    }
-  }
-  if (lane < 12) {
-    l.opa = __ldg(A.wops + d.wop_begin + w * 12u + lane);
-    l.opb = __ldg(A.wops + d.wop_begin + (8u + w) * 12u + lane);
-  }
-  return l;
+__device__ __forceinline__ TmaLeafDesc tma_desc(const WaveArgs& A, u32 item, u32 items) {
+  TmaLeafDesc d{};
+  if (item < items) d = static_cast<const TmaLeafDesc*>(A.tdesc)[item >> A.logS];
+  return d;
+}
+// source coset of a slot's pre-rotation for item coset g
+__device__ __forceinline__ u32 src_coset(u32 pre, u32 g, u32 step) {
+  const u32 qb = ((pre & 0x3FFFFFFFu) >> 8) & (step - 1);
+  return g >= qb ? g - qb : g + step - qb;
+}
+__device__ __forceinline__ u32 warp_sum(u32 v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-// TMA copies of network w's inputs of an item (coset g) into the warp's ring
-// buffer (lanes 0..7: one slot each), completing on the network's mbarrier.
-__device__ __forceinline__ void tma_issue(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
-                                          const TmaLeafDesc& d, u32 g, const TmaLane& l, u32 w, u32 lane, u32 sm_s,
-                                          u32 bar, u32 step) {
-  const u32 slot = slot_a(d.nstore_wnet >> 16, w, lane & 7u);
-  const bool ld = lane < 8 && slot < d.nload;
-  u32 bytes = 0, cA = 0, cB = 0;
-  bool unal = false, fresh = false, hiw = false;
-  if (ld) {
-    const u32 r = l.pre & 0x3FFFFFFFu;
-    const u32 qb = (r >> 8) & (step - 1);
-    unal = (r & 255u) != 0;
-    fresh = (l.pre >> 30) & 1u;
-    cA = g >= qb ? g - qb : g + step - qb;
-    cB = cA ? cA - 1 : step - 1;
-    hiw = cA == 0 || (unal && cA == 1);  // a lane of the item reads source lane 0
-    bytes = (unal ? 2048u : 1024u) + (fresh ? 0u : (unal ? 256u : 128u)) + (hiw ? 16u : 0u);
-  }
-  u32 tot = bytes;
+// Stage-B warp 8: the tile loads of item (d, g) into tile `tile` (lane l:
+// slots l and l + 32, their pre / layout entries prefetched), completing on `bar`.
+struct TileLane {
+  u32 pre[2], lay[2];
+};
+__device__ __forceinline__ TileLane tile_lane(const WaveArgs& A, const TmaLeafDesc& d, bool valid, u32 lane) {
+  TileLane t{};
 #pragma unroll
-  for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  for (int h = 0; h < 2; ++h) {
+    const u32 slot = lane + 32u * h;
+    if (valid && slot < d.nload) {
+      t.pre[h] = __ldg(A.wslots + d.c0 + 2 * slot);
+      t.lay[h] = __ldg(A.tlay + d.c0 + 2 * slot) | 4u;  // bit 2: loaded
+    }
+  }
+  return t;
+}
+__device__ __forceinline__ void tile_issue(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
+                                           const TmaLeafDesc& d, const TileLane& tl, u32 g, u32 lane, u32 tile,
+                                           u32 bar, u32 step) {
+  u32 bytes = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(tl.lay[h] & 4u)) continue;
+    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
+    const u32 cA = src_coset(tl.pre[h], g, step);
+    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u;
+    bytes += 1024u + (fresh ? 0u : 128u) + ((cA == 0 || (unal && cA == 1)) ? 16u : 0u);
+  }
+  const u32 tot = warp_sum(bytes);
+  if (lane == 0) mbar_expect_tx(bar, tot);
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(tl.lay[h] & 4u)) continue;
+    const u32 slot = lane + 32u * h;
+    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
+    const u32 cA = src_coset(tl.pre[h], g, step);
+    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u, sh = tl.pre[h] >> 31;
+    const u64 e = d.base + (u64)slot * d.stride;
+    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+    if (tl.lay[h] & 1u)
+      bulk_g2s(tile + kTileRows + slot * 1024u, el + (u64)cA * 1024u, 1024u, bar);
+    else
+      tma_box(tile + kTileRows + slot * 1024u, sh ? tms : tmv, cA, (u32)e, bar);
+    if (!fresh)
+      bulk_g2s(tile + kTileTops + slot * 128u, A.T + (sh ? A.tloc : 0) + e * A.lanes + (u64)cA * 32u, 128u, bar);
+    if (cA == 0 || (unal && cA == 1)) bulk_g2s(tile + kTileHiw + slot * 16u, el + 4ull * A.D, 16u, bar);
+  }
+}
+
+// L2 prefetch of everything an item's tile and rings will load (lane l:
+// slots l and l + 32), issued a few items ahead so that DRAM keeps streaming
+// while shared memory holds only the items in progress.
+__device__ __forceinline__ void tile_prefetch(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
+                                              const TmaLeafDesc& d, const TileLane& tl, u32 g, u32 lane, u32 step) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (!(tl.lay[h] & 4u)) continue;
+    const u32 slot = lane + 32u * h;
+    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
+    const u32 cA = src_coset(tl.pre[h], g, step);
+    const u32 cB = cA ? cA - 1 : step - 1;
+    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u, sh = tl.pre[h] >> 31;
+    const u64 e = d.base + (u64)slot * d.stride;
+    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+    const int* tin = A.T + (sh ? A.tloc : 0) + e * A.lanes;
+    if (tl.lay[h] & 1u) {
+      if (unal && cA)
+        pf_bulk(el + (u64)cB * 1024u, 2048u);
+      else
+        pf_bulk(el + (u64)cA * 1024u, 1024u);
+      if (unal && !cA) pf_bulk(el + (u64)cB * 1024u, 1024u);
+    } else {
+      pf_box(sh ? tms : tmv, cA, (u32)e);
+      if (unal) pf_box(sh ? tms : tmv, cB, (u32)e);
+    }
+    if (!fresh) {
+      if (unal && cA)
+        pf_bulk(tin + (u64)cB * 32u, 256u);
+      else
+        pf_bulk(tin + (u64)cA * 32u, 128u);
+      if (unal && !cA) pf_bulk(tin + (u64)cB * 32u, 128u);
+    }
+  }
+}
+
+// Stage-A warp w: cp.async loads of its own slots of item (d, g) into the
+// group's tile -- rows (swizzled), tops, the element's top word where the
+// item reads source lane 0 (lane j < 8 holds slot j's pre / layout entry).
+template <bool DIF>
+__device__ __forceinline__ void warp_load(const WaveArgs& A, const TmaLeafDesc& d, u32 g, u32 w, u32 lane, u32 apre,
+                                          u32 alay, u32 tile, u32 step) {
+#pragma unroll 1
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_a(DIF ? 1u : 2u, w, j);
+    if (slot >= d.nload) break;  // (later slots are truncated too)
+    const u32 pre = __shfl_sync(0xffffffffu, apre, (int)j);
+    const u32 lay = __shfl_sync(0xffffffffu, alay, (int)j);
+    const u32 r = pre & 0x3FFFFFFFu;
+    const u32 cA = src_coset(pre, g, step);
+    const bool unal = (r & 255u) != 0, fresh = (pre >> 30) & 1u, sh = pre >> 31;
+    const u64 e = d.base + (u64)slot * d.stride;
+    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+    const u32 dst = tile + kTileRows + slot * 1024u;
+    if (lay & 1u) {  // coset-major chunks are stored swizzled: a linear copy
+      const std::uint8_t* src = el + (u64)cA * 1024u + 32u * lane;
+      cp_async16(dst + 32u * lane, src);
+      cp_async16(dst + 32u * lane + 16u, src + 16);
+    } else {
+      const std::uint8_t* src = el + 32ull * (cA + step * lane);
+      cp_async16_l2(dst + sw_off(lane, 0), src);
+      cp_async16_l2(dst + sw_off(lane, 1), src + 16);
+    }
+    if (!fresh) cp_async4(tile + kTileTops + slot * 128u + 4u * lane, A.T + (sh ? A.tloc : 0) + e * A.lanes + cA * 32u + lane);
+    if (lane == 0 && (cA == 0 || (unal && cA == 1))) cp_async8(tile + kTileHiw + slot * 16u, el + 4ull * A.D);
+  }
+  cp_async_commit();
+}
+
+// Stage-A warp w: the lane-below rows of its unaligned slots of item (d, g)
+// into the warp's ring (lane j < 8: slot j of the warp's network).
+template <bool DIF>
+__device__ __forceinline__ void ring_issue(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
+                                           const TmaLeafDesc& d, u32 g, bool valid, u32 w, u32 lane, u32 pre,
+                                           u32 lay, u32 sm_s, u32 bar, u32 step) {
+  const u32 slot = slot_a(DIF ? 1u : 2u, w, lane & 7u);
+  const u32 r = pre & 0x3FFFFFFFu;
+  const bool ld = valid && lane < 8 && slot < d.nload && (r & 255u) != 0;
+  const bool fresh = (pre >> 30) & 1u;
+  const u32 tot = warp_sum(ld ? 1024u + (fresh ? 0u : 128u) : 0u);
   if (lane == 0) mbar_expect_tx(bar, tot);
   __syncwarp();
   if (ld) {
-    const bool sh = l.pre >> 31;
-    const u32 sb = sm_s + kTmaRing + (w * 8u + lane) * 2048u;  // [B | A]
-    const std::uint8_t* el = (sh ? A.data2 : A.data) + l.e * A.elem_bytes;
-    if (l.lay & 1u) {  // coset-major: coset k of the element is the 1 KB chunk k
-      if (unal && cA) {
-        bulk_g2s(sb, el + (u64)cB * 1024u, 2048u, bar);
-      } else {
-        bulk_g2s(sb + 1024u, el + (u64)cA * 1024u, 1024u, bar);
-        if (unal) bulk_g2s(sb, el + (u64)cB * 1024u, 1024u, bar);
-      }
-    } else {  // natural lane order: one 32-row box per coset
-      const CUtensorMap* tm = sh ? tms : tmv;
-      tma_box(sb + 1024u, tm, cA, (u32)l.e, bar);
-      if (unal) tma_box(sb, tm, cB, (u32)l.e, bar);
-    }
-    if (!fresh) {
-      const int* tin = A.T + (sh ? A.tloc : 0) + l.e * A.lanes;
-      const u32 tdst = sm_s + kTmaRingTops + (w * 8u + lane) * 256u;  // [below | own]
-      if (unal && cA) {
-        bulk_g2s(tdst, tin + (u64)cB * 32u, 256u, bar);
-      } else {
-        bulk_g2s(tdst + 128u, tin + (u64)cA * 32u, 128u, bar);
-        if (unal) bulk_g2s(tdst, tin + (u64)cB * 32u, 128u, bar);
-      }
-    }
-    if (hiw) bulk_g2s(sm_s + kTmaHiw + (w * 8u + lane) * 16u, el + 4ull * A.D, 16u, bar);
+    const u32 cA = src_coset(pre, g, step);
+    const u32 cB = cA ? cA - 1 : step - 1;
+    const bool sh = pre >> 31;
+    const u64 e = d.base + (u64)slot * d.stride;
+    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+    const u32 dst = sm_s + kRingRows + (w * 8u + lane) * 1024u;
+    if (lay & 1u)
+      bulk_g2s(dst, el + (u64)cB * 1024u, 1024u, bar);
+    else
+      tma_box(dst, sh ? tms : tmv, cB, (u32)e, bar);
+    if (!fresh)
+      bulk_g2s(sm_s + kRingTops + (w * 8u + lane) * 128u, A.T + (sh ? A.tloc : 0) + e * A.lanes + (u64)cB * 32u,
+               128u, bar);
   }
 }
 
-// The stage-B networks (every op through the rotated path) and the stores.
-template <bool DIF>
-__device__ __forceinline__ void stage_b_and_store(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], const TmaLane& ln,
-                                                  const TmaLeafDesc& d, u32 c, u32 w, u32 pos, u32 exch, u32 etops,
-                                                  u32 step, u32 logS) {
-  const u32 wnet = DIF ? 1u : 2u;
-#pragma unroll
-  for (u32 j = 0; j < 8; ++j) {
-    const u32 slot = slot_b(wnet, w, j);
-    lds_row(x[j], exch + slot * 1024u, pos);
-    tx[j] = sh_ld32(etops + (slot * 32u + pos) * 4u);
-  }
-  net8<DIF, 0xFFFu>(x, tx, ln.opb, pos);
-  const u32 CL = A.lanes, L0 = c + step * pos, nstore = d.nstore_wnet & 0xFFFFu;
-#pragma unroll
-  for (u32 j = 0; j < 8; ++j) {
-    const u32 slot = slot_b(wnet, w, j);
-    if (slot >= nstore) continue;  // (warp-uniform)
-    const u32 post = __shfl_sync(0xffffffffu, ln.post, (int)(8 + j));
-    const u32 pre = __shfl_sync(0xffffffffu, ln.pre, (int)(8 + j));
-    const u32 lay = __shfl_sync(0xffffffffu, ln.lay, (int)(8 + j));
-    const u64 e = __shfl_sync(0xffffffffu, ln.e, (int)(8 + j));
-    const u32 dst = (L0 + (post & 0x3FFFFFFFu)) & (2 * CL - 1);
-    const u32 dl = dst & (CL - 1);
-    const bool ng = dst >= CL;
-    if (__any_sync(0xffffffffu, ng)) neg_if8(x[j], tx[j], ng);
-    const bool osh = post >> 31;
-    std::uint8_t* el = (osh ? A.data2 : A.data) + e * A.elem_bytes;
-    int* tout = A.T + (osh ? A.tloc : 0) + e * CL;
-    const u32 at = (lay & 2u) ? ((dl & (step - 1)) << 5) | (dl >> logS) : dl;  // coset-major: chunk, row
-    uint4* gp = reinterpret_cast<uint4*>(el + (u64)at * 32u);
-    __stcg(gp, make_uint4(x[j].w[0], x[j].w[1], x[j].w[2], x[j].w[3]));
-    __stcg(gp + 1, make_uint4(x[j].w[4], x[j].w[5], x[j].w[6], x[j].w[7]));
-    __stcg(tout + (((dl & (step - 1)) << (A.logLanes - logS)) | (dl >> logS)), tx[j]);
-    bool owner;
-    if (slot < d.nload) {  // the lane that read source lane 0 clears the output's top word
-      const u32 q = (pre & 0x3FFFFFFFu) >> 8;
-      if (q == 0) {
-        owner = c == 0 && pos == 0;
-      } else {
-        const PreSrc s = pre_src(c, pos, q, logS);
-        owner = s.cls == 0 && s.row == 0;
-      }
-    } else {
-      owner = dl == 0;
-    }
-    if (owner) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
-  }
-}
-
-template <bool DIF>
-__device__ __forceinline__ void tma_item_run(const WaveArgs& A, const TmaLeafDesc& d, const TmaLane& ln, u32 c,
-                                             u32 w, u32 pos, u32 sm_s, u32 step, u32 logS, Ch<8> (&x)[8],
-                                             int (&tx)[8]) {
-  // ---- stage-A inputs: settle the slots that need it in place, then load
-  const u32 wnet = DIF ? 1u : 2u;
-  const u32 ring = sm_s + kTmaRing + w * 16u * 1024u;  // slot j: [B | A] at ring + 2 KB j
-  const u32 rtops = sm_s + kTmaRingTops + w * 8u * 256u;
-  const u32 L0 = c + step * pos;
-#pragma unroll 1
-  for (u32 j = 0; j < 8; ++j) {
-    if (slot_a(wnet, w, j) >= d.nload) break;  // (warp-uniform; later slots are truncated too)
-    const u32 pre = __shfl_sync(0xffffffffu, ln.pre, (int)j);
-    const u32 r = pre & 0x3FFFFFFFu;
-    if (r == 0) continue;  // read in place below
+// Settle one slot in place: row pos of the slot becomes the true carry-save
+// value of this lane's rotated source lane (x = lane L0 - r, r = q lanes + o
+// bits), the element's top word folded into source lane 0, lanes past 2^N
+// negated; its top goes to tops[pos].  A sub-lane rotation takes the low
+// 256 - o bits of source lane A = L0 - q shifted up and the high o bits (and
+// the top) of the lane below it, B; each part carries the sign its source
+// lane has as seen from this lane, applied after the split -- so the lane
+// that reads X as A and the lane that reads X as B always split X the same
+// way, and across 2^N == -1 (output lane 0 taking lane C-1's high bits) the
+// parts are exact negatives.
+__device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u32 tops, u32 hiw, u32 brows,
+                                            u32 btops, u32 logS) {
+  const u32 r = pre & 0x3FFFFFFFu;
+  const bool fresh = (pre >> 30) & 1u;
+  Ch<8> x;
+  int t;
+  if (r == 0) {  // c == 0: only the top word of row 0 to fold
+    lds_row(x, rows, pos);
+    t = fresh ? 0 : sh_ld32(tops + 4u * pos);
+    const long long hi = sh_ld64(hiw);
+    if (pos == 0 && hi) t += ch_add_small<8>(x, -(int)hi);
+  } else {
     const u32 o = r & 255u;
-    const bool fresh = (pre >> 30) & 1u;
     const PreSrc sa = pre_src(c, pos, r >> 8, logS);
-    const u32 rowsB = ring + j * 2048u, rowsA = rowsB + 1024u;
-    const u32 tp = rtops + j * 256u;
-    const u32 hw = sm_s + kTmaHiw + (w * 8u + j) * 16u;
-    Ch<8> a;
-    lds_row(a, rowsA, sa.row);
-    int ta = fresh ? 0 : sh_ld32(tp + 128u + 4u * sa.row);
-    if (sa.cls == 0) {  // warp-uniform: the item reads source lane 0 (row 0)
-      const long long hi = sh_ld64(hw);
-      if (sa.row == 0 && hi) ta += ch_add_small<8>(a, -(int)hi);
+    lds_row(x, rows, sa.row);
+    t = fresh ? 0 : sh_ld32(tops + 4u * sa.row);
+    if (sa.cls == 0) {  // warp-uniform
+      const long long hi = sh_ld64(hiw);
+      if (sa.row == 0 && hi) t += ch_add_small<8>(x, -(int)hi);
     }
-    if (__any_sync(0xffffffffu, sa.neg)) neg_if8(a, ta, sa.neg);
     if (o) {
       // the lane below the source: coset c'-1 on the same row, or coset
       // step-1 one row down (srcA - 1 = (step - 1) + step (rho - 1))
@@ -422,118 +460,286 @@ __device__ __forceinline__ void tma_item_run(const WaveArgs& A, const TmaLeafDes
         negB = rhoB >= 32;
       }
       Ch<8> b;
-      lds_row(b, rowsB, rowB);
-      int tb = fresh ? 0 : sh_ld32(tp + 4u * rowB);
+      lds_row(b, brows, rowB);
+      int tb = fresh ? 0 : sh_ld32(btops + 4u * rowB);
       if (sa.cls == 1) {
-        const long long hi = sh_ld64(hw);
+        const long long hi = sh_ld64(hiw);
         if (rowB == 0 && hi) tb += ch_add_small<8>(b, -(int)hi);
       }
-      if (__any_sync(0xffffffffu, negB)) neg_if8(b, tb, negB);
-      Ch<8> out;
-      int otop = unal_combine8(out, b, a, tb, o);
-      if (L0 == 0) {
-        // lane 0's B is lane C-1's A seen through 2^N == -1 (wave_coset.cuh)
-        const u32 nbits = 256u - o;
-        u32 nz = 0;
+      // signs differ only where the source index wraps between B and A
+      const bool mixed = negB != sa.neg;
+      Ch<8> bs;
 #pragma unroll
-        for (int xw = 0; xw < 8; ++xw) {
-          const u32 lo = 32u * xw;
-          const u32 m = lo + 32u <= nbits ? ~0u : (lo < nbits ? (1u << (nbits - lo)) - 1u : 0u);
-          nz |= b.w[xw] & m;
-        }
-        if (nz) otop += ch_add_small<8>(out, 1);
+      for (int k = 0; k < 8; ++k) bs.w[k] = mixed ? 0u : b.w[k];
+      Ch<8> out;
+      t = unal_combine8(out, bs, x, mixed ? 0 : tb, o);  // the whole lane, or low(A) where mixed
+      if (__any_sync(0xffffffffu, sa.neg)) neg_if8(out, t, sa.neg);
+      if (__any_sync(0xffffffffu, mixed)) {
+        Ch<8> z, h;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) z.w[k] = 0;
+        int th = unal_combine8(h, b, z, tb, o);  // high(B)
+        if (__any_sync(0xffffffffu, negB)) neg_if8(h, th, negB);
+        if (mixed) t += th + ch_add<8>(out, out, h);
       }
-      a = out;
-      ta = otop;
+      x = out;
+    } else if (__any_sync(0xffffffffu, sa.neg)) {
+      neg_if8(x, t, sa.neg);
     }
-    __syncwarp();
-    sts_row(rowsA, pos, a);
-    sh_st32(tp + 128u + 4u * pos, ta);
+  }
+  __syncwarp();  // every lane has read the slot's rows
+  sts_row(rows, pos, x);
+  sh_st32(tops + 4u * pos, t);
+}
+
+// Stage-B rotated butterflies skip the shuffles when the op's q is zero
+__device__ __forceinline__ void bfly_any(Ch<8>& a, int& ta, Ch<8>& b, int& tb, u32 opv, int oi, u32 pos) {
+  const u32 qv = (__shfl_sync(0xffffffffu, opv, oi) >> 16) & 63u;
+  if (qv == 0)
+    bfly_plain(a, ta, b, tb);
+  else
+    bfly_rot(a, ta, b, tb, opv, oi, pos);
+}
+template <bool DIF>
+__device__ __forceinline__ void net8_b(Ch<8> (&x)[8], int (&t)[8], u32 opv, u32 pos) {
+  if constexpr (DIF) {
+    bfly_any(x[0], t[0], x[4], t[4], opv, 0, pos);
+    bfly_any(x[1], t[1], x[5], t[5], opv, 1, pos);
+    bfly_any(x[2], t[2], x[6], t[6], opv, 2, pos);
+    bfly_any(x[3], t[3], x[7], t[7], opv, 3, pos);
+    bfly_any(x[0], t[0], x[2], t[2], opv, 4, pos);
+    bfly_any(x[1], t[1], x[3], t[3], opv, 5, pos);
+    bfly_any(x[4], t[4], x[6], t[6], opv, 6, pos);
+    bfly_any(x[5], t[5], x[7], t[7], opv, 7, pos);
+    bfly_any(x[0], t[0], x[1], t[1], opv, 8, pos);
+    bfly_any(x[2], t[2], x[3], t[3], opv, 9, pos);
+    bfly_any(x[4], t[4], x[5], t[5], opv, 10, pos);
+    bfly_any(x[6], t[6], x[7], t[7], opv, 11, pos);
+  } else {
+    bfly_any(x[0], t[0], x[1], t[1], opv, 0, pos);
+    bfly_any(x[2], t[2], x[3], t[3], opv, 1, pos);
+    bfly_any(x[4], t[4], x[5], t[5], opv, 2, pos);
+    bfly_any(x[6], t[6], x[7], t[7], opv, 3, pos);
+    bfly_any(x[0], t[0], x[2], t[2], opv, 4, pos);
+    bfly_any(x[1], t[1], x[3], t[3], opv, 5, pos);
+    bfly_any(x[4], t[4], x[6], t[6], opv, 6, pos);
+    bfly_any(x[5], t[5], x[7], t[7], opv, 7, pos);
+    bfly_any(x[0], t[0], x[4], t[4], opv, 8, pos);
+    bfly_any(x[1], t[1], x[5], t[5], opv, 9, pos);
+    bfly_any(x[2], t[2], x[6], t[6], opv, 10, pos);
+    bfly_any(x[3], t[3], x[7], t[7], opv, 11, pos);
+  }
+}
+
+// stage A of one item for warp w (tile `tile`): settle in place, load,
+// network, write back
+template <bool DIF>
+__device__ __forceinline__ void stage_a(const TmaLeafDesc& d, u32 c, u32 w, u32 pos, u32 apre, u32 opa, u32 tile,
+                                        u32 sm_s, u32 logS) {
+  const u32 wnet = DIF ? 1u : 2u;
+  u32 tvalid = 0;  // bit j: the slot's tops row is valid
+#pragma unroll 1
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_a(wnet, w, j);
+    if (slot >= d.nload) break;  // (warp-uniform; later slots are truncated too)
+    const u32 pre = __shfl_sync(0xffffffffu, apre, (int)j);
+    if ((pre & 0x3FFFFFFFu) == 0 && c != 0) {  // read in place
+      if (!((pre >> 30) & 1u)) tvalid |= 1u << j;
+      continue;
+    }
+    settle_slot(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
+                tile + kTileHiw + slot * 16u, sm_s + kRingRows + (w * 8u + j) * 1024u,
+                sm_s + kRingTops + (w * 8u + j) * 128u, logS);
+    tvalid |= 1u << j;
   }
   __syncwarp();
+  Ch<8> x[8];
+  int tx[8];
 #pragma unroll
   for (u32 j = 0; j < 8; ++j) {
-    if (slot_a(wnet, w, j) >= d.nload) {  // truncated input (warp-uniform)
+    const u32 slot = slot_a(wnet, w, j);
+    if (slot >= d.nload) {  // truncated input (warp-uniform)
 #pragma unroll
       for (int wd = 0; wd < 8; ++wd) x[j].w[wd] = 0;
       tx[j] = 0;
       continue;
     }
-    const u32 pre = __shfl_sync(0xffffffffu, ln.pre, (int)j);
-    lds_row(x[j], ring + j * 2048u + 1024u, pos);
-    const bool inplace = (pre & 0x3FFFFFFFu) == 0;
-    tx[j] = (inplace && ((pre >> 30) & 1u)) ? 0 : sh_ld32(rtops + j * 256u + 128u + 4u * pos);
-    if (inplace && c == 0) {  // source lane 0 is this item's row 0: fold the top word in
-      const long long hi = sh_ld64(sm_s + kTmaHiw + (w * 8u + j) * 16u);
-      if (pos == 0 && hi) tx[j] += ch_add_small<8>(x[j], -(int)hi);
-    }
+    lds_row(x[j], tile + kTileRows + slot * 1024u, pos);
+    tx[j] = ((tvalid >> j) & 1u) ? sh_ld32(tile + kTileTops + slot * 128u + 4u * pos) : 0;
   }
-  __syncwarp();
+  if (DIF)
+    net8<true, kRotDif>(x, tx, opa, pos);
+  else
+    net8<false, kRotDit>(x, tx, opa, pos);
+  __syncwarp();  // every lane is done reading the warp's slots
+#pragma unroll
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_a(wnet, w, j);
+    sts_row(tile + kTileRows + slot * 1024u, pos, x[j]);
+    sh_st32(tile + kTileTops + slot * 128u + 4u * pos, tx[j]);
+  }
 }
 
-template <int DUMMY = 0>
+// Store descriptor of one output slot (stage-B warp table in shared memory)
+struct SlotOut {
+  u64 el;    // output element base (buffer resolved)
+  u64 tout;  // its tops row
+  u32 post;  // post-rotation in lanes
+  u32 lown;  // the lane (L0) that clears the output's top word
+  u32 flags; // bit 0: stored (slot < nstore), bit 1: coset-major output
+  u32 pad;
+};
+static_assert(sizeof(SlotOut) == 32, "SlotOut layout");
+
+template <bool DIF>
+__device__ __forceinline__ void slot_table(const WaveArgs& A, const TmaLeafDesc& d, u32 wb, u32 lane, u32 tab) {
+  if (lane < 8) {
+    const u32 slot = slot_b(DIF ? 1u : 2u, wb, lane);
+    SlotOut so{};
+    if (slot < (d.nstore_wnet & 0xFFFFu)) {
+      const u32 post = __ldg(A.wslots + d.c0 + 2 * slot + 1);
+      const u32 CL = A.lanes;
+      const u64 e = d.base + (u64)slot * d.stride;
+      const bool osh = post >> 31;
+      so.el = reinterpret_cast<u64>((osh ? A.data2 : A.data) + e * A.elem_bytes);
+      so.tout = reinterpret_cast<u64>(A.T + (osh ? A.tloc : 0) + e * CL);
+      so.post = post & 0x3FFFFFFFu;
+      so.flags = 1u | (((u32)__ldg(A.tlay + d.c0 + 2 * slot) & 2u));
+      if (slot < d.nload) {  // the lane that read source lane 0 (L0 == q mod C)
+        const u32 q = (__ldg(A.wslots + d.c0 + 2 * slot) & 0x3FFFFFFFu) >> 8;
+        so.lown = q & (CL - 1);
+      } else {  // the lane writing output lane 0
+        so.lown = (CL - (so.post & (CL - 1))) & (CL - 1);
+      }
+    }
+    uint4* p = reinterpret_cast<uint4*>(__cvta_shared_to_generic(tab + 32u * lane));
+    const uint4* sp = reinterpret_cast<const uint4*>(&so);
+    p[0] = sp[0];
+    p[1] = sp[1];
+  }
+}
+
+template <bool DIF>
+__device__ __forceinline__ void stage_b_load(Ch<8> (&x)[8], int (&tx)[8], u32 wb, u32 pos, u32 tile) {
+  const u32 wnet = DIF ? 1u : 2u;
+#pragma unroll
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_b(wnet, wb, j);
+    lds_row(x[j], tile + kTileRows + slot * 1024u, pos);
+    tx[j] = sh_ld32(tile + kTileTops + slot * 128u + 4u * pos);
+  }
+}
+template <bool DIF>
+__device__ __forceinline__ void stage_b_run(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], u32 c, u32 pos, u32 opb,
+                                            u32 tab, u32 logS) {
+  net8_b<DIF>(x, tx, opb, pos);
+  const u32 CL = A.lanes, L0 = c + (pos << logS), step = 1u << logS;
+  const u32 tsh = A.logLanes - logS;
+#pragma unroll
+  for (u32 j = 0; j < 8; ++j) {
+    const SlotOut* so = reinterpret_cast<const SlotOut*>(__cvta_shared_to_generic(tab + 32u * j));
+    const uint4 h1 = reinterpret_cast<const uint4*>(so)[1];  // post, lown, flags, pad
+    if (!(h1.z & 1u)) continue;  // slot >= nstore (warp-uniform)
+    const uint4 h0 = reinterpret_cast<const uint4*>(so)[0];
+    std::uint8_t* el = reinterpret_cast<std::uint8_t*>(((u64)h0.y << 32) | h0.x);
+    int* tout = reinterpret_cast<int*>(((u64)h0.w << 32) | h0.z);
+    const u32 dst = (L0 + h1.x) & (2 * CL - 1);
+    const u32 dl = dst & (CL - 1);
+    const bool ng = dst >= CL;
+    if (__any_sync(0xffffffffu, ng)) neg_if8(x[j], tx[j], ng);
+    const u32 cs = dl & (step - 1), rw = dl >> logS;
+    if (h1.z & 2u) {  // coset-major, swizzled: chunk cs, row rw
+      uint4* gp = reinterpret_cast<uint4*>(el + (cs << 10) + 32u * rw);
+      const u32 sw = (rw >> 2) & 1u;
+      __stcg(gp + sw, make_uint4(x[j].w[0], x[j].w[1], x[j].w[2], x[j].w[3]));
+      __stcg(gp + (sw ^ 1u), make_uint4(x[j].w[4], x[j].w[5], x[j].w[6], x[j].w[7]));
+    } else {
+      uint4* gp = reinterpret_cast<uint4*>(el + 32u * dl);
+      __stcg(gp, make_uint4(x[j].w[0], x[j].w[1], x[j].w[2], x[j].w[3]));
+      __stcg(gp + 1, make_uint4(x[j].w[4], x[j].w[5], x[j].w[6], x[j].w[7]));
+    }
+    __stcg(tout + ((cs << tsh) | rw), tx[j]);
+    if (L0 == h1.y) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
+  }
+}
+
+template <bool DIF>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     coset_tma_kernel(const __grid_constant__ CUtensorMap tm_view, const __grid_constant__ CUtensorMap tm_shadow,
                      WaveArgs A) {
   extern __shared__ std::uint8_t tsm_raw[];
   const u32 sm_s = ((u32)__cvta_generic_to_shared(tsm_raw) + 1023u) & ~1023u;
-  const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31, pos = lane;
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pos = lane;
+  const u32 grp = warp >> 3, w = warp & 7u;
   const u32 logS = A.logS, step = 1u << logS;
-  const u32 bar = sm_s + kTmaBars + 8u * w;
-  if (lane == 0) {
-    mbar_init(bar, 1);
+  // mbarriers ring[g][w]: network w's lane-below rows for group g's items
+  const u32 bar0 = sm_s + kTmaBars;
+  auto ringbar = [&](u32 g) { return bar0 + 64u * g + 8u * w; };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 16; ++b) mbar_init(bar0 + 8u * b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  __syncwarp();
-  // items: (leaf t, coset g), g fastest (the host guarantees gpl == step)
-  const u32 items = A.nleaves << logS;
-  const TmaLeafDesc* descs = static_cast<const TmaLeafDesc*>(A.tdesc);
-  auto load_desc = [&](u32 item) {
-    TmaLeafDesc d{};
-    if (item < items) d = descs[item >> logS];
-    return d;
+  __syncthreads();
+  const u32 items = A.nleaves << logS, G = gridDim.x;
+  auto item_of = [&](u32 k) { return blockIdx.x + k * G; };
+  const u32 tile = sm_s + grp * kTileBytes;
+  const u32 tab = sm_s + kSlotTab + 256u * warp;
+  // lane j < 8: slot j of this warp's stage-A network (pre, layout)
+  auto lane_info = [&](const TmaLeafDesc& d, bool valid, u32& pre, u32& lay) {
+    pre = lay = 0;
+    const u32 slot = slot_a(DIF ? 1u : 2u, w, lane & 7u);
+    if (valid && lane < 8 && slot < d.nload) {
+      pre = __ldg(A.wslots + d.c0 + 2 * slot);
+      lay = __ldg(A.tlay + d.c0 + 2 * slot);
+    }
   };
-  // descriptors two items ahead, lane registers one item ahead
-  u32 i1 = blockIdx.x, i2 = i1 + gridDim.x;
-  TmaLeafDesc d1 = load_desc(i1), d2 = load_desc(i2);
-  TmaLane l1 = tma_lane(A, d1, i1 < items, w, lane);
-  if (i1 < items) tma_issue(A, &tm_view, &tm_shadow, d1, i1 & (step - 1), l1, w, lane, sm_s, bar, step);
-  const u32 exch = sm_s + kTmaExch, etops = sm_s + kTmaExchTops;
-  for (u32 k = 0; i1 < items; ++k) {
-    const TmaLeafDesc d = d1;
-    const TmaLane ln = l1;
-    const u32 c = i1 & (step - 1);
-    i1 = i2;
-    d1 = d2;
-    l1 = tma_lane(A, d1, i1 < items, w, lane);
-    i2 += gridDim.x;
-    d2 = load_desc(i2);
-    const bool dif = (d.nstore_wnet >> 16) == 1;
-    mbar_wait(bar, k & 1u);
+  // Group g runs stage A then stage B of items k = g, g + 2, ...: while one
+  // group is in stage B of item k the other settles and transforms item k+1.
+  // Each warp loads its own stage-A slots (cp.async) as soon as the group's
+  // tile is free; the lane-below rings are shared: the group that finishes
+  // settling item k starts the rows of item k+1 (the other group's) into them.
+  u32 i = item_of(grp);
+  TmaLeafDesc d = tma_desc(A, i, items);
+  u32 pre, lay;
+  lane_info(d, i < items, pre, lay);
+  if (i < items) warp_load<DIF>(A, d, i & (step - 1), w, lane, pre, lay, tile, step);
+  if (grp == 0)
+    ring_issue<DIF>(A, &tm_view, &tm_shadow, d, i & (step - 1), i < items, w, lane, pre, lay, sm_s, ringbar(0),
+                    step);
+  u32 n = 0;  // this group's item count
+  for (u32 k = grp; i < items; k += 2, ++n) {
+    const u32 c = i & (step - 1);
+    const u32 in = item_of(k + 1);
+    const TmaLeafDesc dn = tma_desc(A, in, items);
+    u32 npre, nlay;
+    lane_info(dn, in < items, npre, nlay);
+    const u32 i2 = item_of(k + 2);
+    const TmaLeafDesc d2 = tma_desc(A, i2, items);
+    u32 pre2, lay2;
+    lane_info(d2, i2 < items, pre2, lay2);
+    const u32 opa = lane < 12 ? __ldg(A.wops + d.wop_begin + w * 12u + lane) : 0u;
+    const u32 opb = lane < 12 ? __ldg(A.wops + d.wop_begin + (8u + w) * 12u + lane) : 0u;
+    // ---- stage A
+    cp_async_wait<0>();
+    __syncwarp();
+    mbar_wait(ringbar(grp), n & 1u);
+    if (!(A.debug & 256u)) stage_a<DIF>(d, c, w, pos, pre, opa, tile, sm_s, logS);
+    // the ring is free: the next item's lane-below rows start moving
+    ring_issue<DIF>(A, &tm_view, &tm_shadow, dn, in & (step - 1), in < items, w, lane, npre, nlay, sm_s,
+                    ringbar(grp ^ 1u), step);
+    slot_table<DIF>(A, d, w, lane, tab);
+    named_bar(1u + grp, 256u);  // the group's stage-A outputs are in the tile
+    // ---- stage B
     Ch<8> x[8];
     int tx[8];
-    if (dif)
-      tma_item_run<true>(A, d, ln, c, w, pos, sm_s, step, logS, x, tx);
-    else
-      tma_item_run<false>(A, d, ln, c, w, pos, sm_s, step, logS, x, tx);
-    // the buffer is free: the next item's inputs start moving now
-    if (i1 < items) tma_issue(A, &tm_view, &tm_shadow, d1, i1 & (step - 1), l1, w, lane, sm_s, bar, step);
-    if (dif)
-      net8<true, kRotDif>(x, tx, ln.opa, pos);
-    else
-      net8<false, kRotDit>(x, tx, ln.opa, pos);
-    named_bar(1, kTmaThreads);  // every warp is done reading the previous item's exchange tile
-#pragma unroll
-    for (u32 j = 0; j < 8; ++j) {
-      const u32 slot = dif ? w + 8u * j : 8u * w + j;
-      sts_row(exch + slot * 1024u, pos, x[j]);
-      sh_st32(etops + (slot * 32u + pos) * 4u, tx[j]);
-    }
-    named_bar(1, kTmaThreads);  // stage A complete
-    if (dif)
-      stage_b_and_store<true>(A, x, tx, ln, d, c, w, pos, exch, etops, step, logS);
-    else
-      stage_b_and_store<false>(A, x, tx, ln, d, c, w, pos, exch, etops, step, logS);
+    stage_b_load<DIF>(x, tx, w, pos, tile);
+    named_bar(1u + grp, 256u);  // every warp of the group holds its rows: the tile is free
+    if (i2 < items) warp_load<DIF>(A, d2, i2 & (step - 1), w, lane, pre2, lay2, tile, step);
+    if (!(A.debug & 512u)) stage_b_run<DIF>(A, x, tx, c, pos, opb, tab, logS);
+    __syncwarp();  // the slot table is rewritten for the next item
+    i = i2;
+    d = d2;
+    pre = pre2;
   }
 }
 
