@@ -67,9 +67,13 @@ typedef struct cftft_params {
 typedef struct cftft_ring cftft_ring;
 
 /* Ring contexts replace cftft::RingCtx (field.hpp:84-185).  For FERMAT,
- * n_or_k = N (a power of two, >= 64) and modulus is ignored.  For
- * NEGACYCLIC, n_or_k = K (a power of two) and modulus = m (odd, < 2^62).
- * Immutable and shareable across threads once created. */
+ * n_or_k = N (a power of two in [128, 2^18]) and modulus is ignored.  For
+ * NEGACYCLIC, n_or_k = K (a power of two in [2, 16384]) and modulus = m
+ * (odd, < 2^62).  For PRIME, n_or_k = m (two-adicity, 1..32) and modulus =
+ * p (a prime with 2^m | p - 1; a composite p is CFTFT_INVALID_PARAMS, the
+ * reference's NotPrime).  Out-of-range sizes: CFTFT_UNSUPPORTED.  Immutable
+ * and shareable across threads once created (concurrent host-view calls on
+ * one ring are serialised). */
 int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** out);
 void cftft_ring_destroy(cftft_ring* ring);
 uint64_t cftft_ring_root_order(const cftft_ring* ring);    /* M */
@@ -95,10 +99,11 @@ int cftft_stream_synchronize(void* stream);
  * Results are bit-identical in every mode. */
 int cftft_ring_set_coset(cftft_ring* ring, int lane_words);
 
-/* Fermat rings with coset leaves: 1 runs leaves of up to 64 coefficients on
- * the CTA-level radix-64 kernel (three passes over the data at L = 2^18
- * instead of six), 0 the radix-8 warp engine, -1 (default) follows the
- * environment variable CFTFT_WIDE (unset: 0).  Bit-identical results. */
+/* Fermat rings with coset leaves: 1 (and -1, the default) cuts the
+ * transform into coset leaves of up to 64 coefficients, whose full-network
+ * waves run on the TMA-wave kernel (three passes over the data at L = 2^18
+ * instead of six); 0 keeps leaves of <= 8 coefficients on the radix-8 warp
+ * engine.  Bit-identical results; other values: CFTFT_INVALID_PARAMS. */
 int cftft_ring_set_wide(cftft_ring* ring, int wide);
 
 /* Forward truncated transform, in place over a DEVICE view
@@ -170,7 +175,7 @@ int cftft_gpu_scale(const cftft_ring* ring, void* dev_base, uint64_t count,
                     uint64_t elem_stride_bytes, uint64_t e, void* stream);
 
 /* Base-case counts of the reference recursion (data independent;
- * verify.hpp:459-483), by host replay.  No GPU needed. */
+ * verify.hpp:175-199), by host replay.  No GPU needed. */
 uint64_t cftft_tft_base_cases(uint64_t L, uint64_t z, uint64_t n, int policy);
 uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int policy);
 

@@ -189,8 +189,8 @@ class FermatRingCtx(_Ring):
         _check(lib().cftft_ring_set_coset(self._h, lane_words))
 
     def set_wide(self, wide: int) -> None:
-        """Radix-64 coset leaves on the CTA kernel: 1 on, 0 off (radix-8 warp
-        engine), -1 = environment CFTFT_WIDE (default off)."""
+        """Radix-64 coset leaves (full-network waves on the TMA-wave kernel):
+        1 or -1 (the default) on, 0 off (radix-8 warp engine)."""
         _check(lib().cftft_ring_set_wide(self._h, wide))
 
 

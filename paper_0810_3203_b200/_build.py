@@ -47,7 +47,10 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    # CFTFT_BUILD_EXPERIMENTS=1: a build whose experiment knobs (phase clocks,
+    # debug skips: csrc/capi.cu env_int) follow the environment
+    extra = ["-DCFTFT_EXPERIMENTS"] if os.environ.get("CFTFT_BUILD_EXPERIMENTS") == "1" else []
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

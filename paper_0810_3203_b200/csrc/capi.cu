@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <thread>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -31,6 +32,17 @@ using namespace cftft_b200;
 namespace {
 
 thread_local std::string g_last_error;
+
+// Experiment knobs (phase clocks, debug skips) exist only in builds with
+// -DCFTFT_EXPERIMENTS; the shipped library reads no environment variables.
+#ifdef CFTFT_EXPERIMENTS
+int env_int(const char* k, int dflt) {
+  const char* v = getenv(k);
+  return v ? atoi(v) : dflt;
+}
+#else
+int env_int(const char*, int dflt) { return dflt; }
+#endif
 thread_local u64 g_last_launches = 0;
 
 int fail(int code, const std::string& msg) {
@@ -45,7 +57,8 @@ int fail(int code, const std::string& msg) {
       return fail(CFTFT_CUDA_ERROR, std::string(#expr ": ") + cudaGetErrorString(e_));    \
   } while (0)
 
-constexpr size_t kSmemBudget = 196 * 1024;  // per-CTA dynamic shared memory for leaf slots
+constexpr size_t kSmemBudget = 196 * 1024;
+constexpr size_t kMaxBatchPlans = 64;  // per-CTA dynamic shared memory for leaf slots
 // Fermat carry scratch: one int per (thread x task) of a store batch
 inline size_t scratch_bytes(u32 nt) { return (size_t)nt * 4; }
 
@@ -73,6 +86,8 @@ struct DevicePlan {
   void* tma_descs = nullptr;      // fermat::TmaLeafDesc per leaf of the TMA waves
   std::uint8_t* tma_lay = nullptr;  // coset-major layout bits per wave_slots entry (inside tma_descs)
   u32 tma_step = 0;
+  std::vector<u64> batch_items;  // batch plans: the items, compared on a cache hit
+  bool tma_cm_finals = false;  // every shadow-buffer final is written coset-major by a TMA wave
   u64 nleaves = 0;
   u32 ncounters = 0;
   unsigned max_ell = 0;
@@ -92,9 +107,8 @@ using PlanKey = std::tuple<int, int, u64, u64, u64, u64, int, int>;  // dev, inv
 struct cftft_ring {
   int kind = 0;
   int coset_cw = -1;          // Fermat coset leaves: -1 auto, 0 off, 4/8/16 lane words
-  int wave = -1;              // Fermat wave engine: -1 auto, 0 off, 1 on
-  int wide = -1;              // radix-64 coset leaves: -1 env CFTFT_WIDE, 0 off, 1 on (network waves on the TMA
-                              // kernel), 2 on (every wave on coset_wide_kernel)
+  int wide = -1;              // radix-64 coset leaves: -1 default (on), 0 off, 1 on (network waves on the
+                              // TMA-wave kernel, the other radix-64 waves on coset_wide_kernel)
   unsigned leaf_limit = 0;    // cftft_ring_set_leaf_limit (0: none)
   u64 N = 0, K = 0, m = 0, M = 0;
   u32 D = 0, C = 0;     // Fermat: u32 words / chunks of CW words
@@ -112,7 +126,9 @@ struct cftft_ring {
   u64 pinv = 0, omega = 0;
   u32 lo_bits = 0;
   u64* prime_tw = nullptr;  // [2^lo_bits] omega^i R, then [M / 2^lo_bits] omega^(i 2^lo_bits) R
-  // staging buffer for the host-view entry points
+  // staging buffer for the host-view entry points; stage_mu is held for a
+  // whole host call (copy in, transform, copy out)
+  std::mutex stage_mu;
   void* stage = nullptr;
   size_t stage_bytes = 0;
   // coset-plan scratch (shadow buffer, tops arrays), one per stream: reused
@@ -121,6 +137,7 @@ struct cftft_ring {
   struct Scratch {
     int dev = -1;
     void* stream = nullptr;
+    std::thread::id thread;  // the default-stream handles (0, per-thread) name a different stream per thread
     void* shadow = nullptr;
     size_t shadow_bytes = 0;
     void* tops = nullptr;
@@ -301,13 +318,27 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
         }
       }
     }
-    for (auto& es : ev) {
+    // A final output left in the shadow buffer is folded from there into the
+    // caller's view by cs_fold_kernel, which can read it coset by coset: when
+    // every such output's last writer is a TMA wave, those writes are
+    // coset-major too (whole 1 KB chunks instead of 32-byte pieces).
+    std::vector<std::uint8_t> shfin(p.extent, 0);
+    if (p.use_fold_list)
+      for (u64 e : p.shadow_finals)
+        if (e < shfin.size()) shfin[e] = 1;
+    std::vector<u64> cm_final_slots;
+    bool cm_all = p.use_fold_list && !p.shadow_finals.empty();
+    for (u64 e = 0; e < ev.size(); ++e) {
+      auto& es = ev[e];
       std::uint8_t cur = 0;
       for (size_t a = 0; a < es.size(); ++a) {
         const Ev& x = es[a];
         if (x.rd && x.tma) lay[x.slot] |= cur;
         if (!x.wr) continue;
         std::uint8_t out = 0;
+        bool last = true;
+        for (size_t b = a + 1; b < es.size(); ++b)
+          if (es[b].wr) last = false;
         if (x.tma) {
           bool any = false, all = true;
           for (size_t b = a + 1; b < es.size(); ++b) {
@@ -318,29 +349,19 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
             if (es[b].wr) break;
           }
           out = (any && all) ? 1 : 0;
+          if (!any && last && shfin[e] && (p.wave_slots[x.slot + 1] >> 31)) {
+            out = 1;
+            cm_final_slots.push_back(x.slot);
+          }
           lay[x.slot] |= (std::uint8_t)(out << 1);
         }
+        if (last && shfin[e] && !(x.tma && out)) cm_all = false;
         cur = out;
       }
     }
-    if (getenv("CFTFT_LAY_STATS")) {
-      for (size_t w = 0; w < p.waves.size(); ++w) {
-        if (!dp.tma_wave[w]) continue;
-        const auto& wr = p.waves[w];
-        u64 n = 0, in = 0, out = 0;
-        for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
-          const DevLeaf& lf = p.leaves[i];
-          const LeafProgram& c = p.classes[lf.cls];
-          for (u32 k = 0; k < std::max(c.nload, c.nstore); ++k) {
-            ++n;
-            in += lay[lf.c0 + 2 * k] & 1;
-            out += (lay[lf.c0 + 2 * k] >> 1) & 1;
-          }
-        }
-        fprintf(stderr, "[cftft] wave %zu: %llu slots, coset-major in %llu out %llu\n", w, (unsigned long long)n,
-                (unsigned long long)in, (unsigned long long)out);
-      }
-    }
+    if (!cm_all)
+      for (u64 sl : cm_final_slots) lay[sl] &= (std::uint8_t)~2u;
+    dp.tma_cm_finals = cm_all;
     CUDA_TRY(cudaMalloc(&dp.tma_descs, descs.size() * sizeof(fermat::TmaLeafDesc) + lay.size()));
     CUDA_TRY(cudaMemcpyAsync(dp.tma_descs, descs.data(), descs.size() * sizeof(fermat::TmaLeafDesc),
                              cudaMemcpyHostToDevice, st));
@@ -358,8 +379,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
 RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   RingShape rs;
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
-  static const int env_grp = getenv("CFTFT_PRIME_GROUP") ? atoi(getenv("CFTFT_PRIME_GROUP")) : 16;
-  if (R->kind == CFTFT_RING_PRIME) rs.group = (u32)std::min(16, std::max(1, env_grp));  // adjacent u64 coefficients per ticket
+  if (R->kind == CFTFT_RING_PRIME) rs.group = 16;  // adjacent u64 coefficients per ticket
   rs.M = R->M;
   rs.max_leaf_ell = R->max_leaf_ell;
   rs.elem_bytes = R->elem_bytes;
@@ -367,11 +387,8 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   if (rs.fermat) {
     const bool on = R->coset_cw > 0 || (R->coset_cw < 0 && R->N >= 4096 && R->NT == 512);
     if (on && L >= 4) {
-      static const int env_cw = getenv("CFTFT_COSET_CW") ? atoi(getenv("CFTFT_COSET_CW")) : 0;
       if (R->coset_cw > 0) {
         cw = (u32)R->coset_cw;
-      } else if (env_cw == 4 || env_cw == 8 || env_cw == 16) {
-        cw = (u32)env_cw;
       } else {
         const unsigned ell = (unsigned)__builtin_ctzll(L);
         const u64 lnode = u64{1} << (ell - ell / 2);
@@ -391,10 +408,9 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
       rs.max_leaf_ell = lam;
       rs.lane_bits = 32ull * cw;
       rs.slot_budget = budget;
-      // per-ticket fixed costs outweigh the overlap two half-size buffers buy:
-      // coset tickets fill the shared memory (CFTFT_HALFTICKETS=1: half, double buffered)
-      static const bool half = getenv("CFTFT_HALFTICKETS") != nullptr;
-      rs.ticket_budget = half ? budget / 2 : budget;
+      // per-ticket fixed costs outweigh the overlap two half-size buffers
+      // would buy: coset tickets fill the shared memory
+      rs.ticket_budget = budget;
       unsigned cl = 0;
       for (unsigned e = 1; e <= 6; ++e) {
         const u64 cs = u64{1} << (e - 1);
@@ -402,21 +418,14 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         if ((u64{1} << e) <= 2ull * C && (u64{1} << e) * slot <= budget / 2) cl = e;
       }
       if (R->leaf_limit) cl = std::min(cl, std::max(1u, R->leaf_limit));
-      static const int env_wave = getenv("CFTFT_WAVE") ? atoi(getenv("CFTFT_WAVE")) : -1;
-      const int wave = R->wave >= 0 ? R->wave : (env_wave >= 0 ? env_wave : 1);
-      if (wave && cw == 8) {
+      if (cw == 8) {
         rs.wave_engine = true;
-        rs.wave_unaligned = getenv("CFTFT_WAVE_ALIGNED") == nullptr;
-        // radix-64 coset leaves on the CTA kernel (CFTFT_WIDE=0: radix 8 only)
-        // (measured slower than the radix-8 engine so far: opt-in)
-        static const int env_wide = getenv("CFTFT_WIDE") ? atoi(getenv("CFTFT_WIDE")) : 0;
-        const int wide = R->wide >= 0 ? R->wide : env_wide;
+        rs.wave_unaligned = true;
+        // radix-64 coset leaves (default: their full-network waves run on the
+        // TMA-wave kernel, wave_tma.cuh; set_wide(0): radix-8 warp waves only)
+        const int wide = R->wide >= 0 ? R->wide : 1;
         rs.wide = wide != 0 && cl >= 6 && (R->M >> 6) % rs.lane_bits == 0;
-        // coset leaves of 16 coefficients on 16-slot warp tiles (CFTFT_R16=1; measured slower,
-        // profiles/r01_experiments.md: the tiles halve the warps per SM)
-        static const int env_r16 = getenv("CFTFT_R16") ? atoi(getenv("CFTFT_R16")) : 0;
-        rs.r16 = !rs.wide && env_r16 != 0 && cl >= 4;
-        cl = std::min(cl, rs.wide ? 6u : (rs.r16 ? 4u : 3u));
+        cl = std::min(cl, rs.wide ? 6u : 3u);
         rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
       }
       rs.coset_max_ell = cl;
@@ -425,10 +434,6 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   }
   rs.C = C;
   rs.slot_bytes = sb;
-  static const int env_ov = getenv("CFTFT_OVERLAP") ? atoi(getenv("CFTFT_OVERLAP")) : 0;
-  rs.wave_overlap = (u32)std::max(0, env_ov);
-  static const int env_l2 = getenv("CFTFT_L2MB") ? atoi(getenv("CFTFT_L2MB")) : 0;
-  if (env_l2 > 0) rs.l2_budget = (u64)env_l2 << 20;
   if (dp) {
     dp->cw = cw;
     dp->C = C;
@@ -445,20 +450,10 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
   return rs;
 }
 
-// Radix-16 plans (RingShape::r16) against their radix-8 alternative: the
-// one whose leaves move fewer bytes (partial ITFT leaves of 16 coefficients
-// are often not lane aligned and split into 4-point leaves).
 template <class F>
 Plan best_plan(const RingShape& rs, F build) {
   Planner pa(rs);
-  Plan a = build(pa);
-  if (!rs.r16) return a;
-  RingShape r8 = rs;
-  r8.r16 = false;
-  r8.coset_max_ell = std::min(r8.coset_max_ell, 3u);
-  Planner pb(r8);
-  Plan b = build(pb);
-  return plan_cost(a, rs.elem_bytes) <= plan_cost(b, rs.elem_bytes) ? std::move(a) : std::move(b);
+  return build(pa);
 }
 
 int get_plan(cftft_ring* R, bool inv, const cftft_params& p, int policy, cudaStream_t st,
@@ -606,10 +601,9 @@ int encode_fn(EncodeTiledFn* out) {
   return CFTFT_OK;
 }
 CUtensorMapL2promotion l2_promotion() {
-  static const int v = getenv("CFTFT_TMA_L2") ? atoi(getenv("CFTFT_TMA_L2")) : 64;
-  return v >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                  : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                             : v >= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  // a coset box row is 32 bytes: let the L2 fetch the 64-byte pair (the
+  // neighbouring coset is read by a concurrent item)
+  return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
 }
 int make_coset_map(CUtensorMap* tm, void* base, u64 stride, u64 extent, u32 step) {
   EncodeTiledFn fn = nullptr;
@@ -642,19 +636,6 @@ int keep_pool() {
   return CFTFT_OK;
 }
 
-// CFTFT_HOST_TRACE=1: host-side time of each step of a launch (stderr)
-struct HostTrace {
-  bool on;
-  std::chrono::steady_clock::time_point t;
-  HostTrace() : on(getenv("CFTFT_HOST_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
-  void mark(const char* what) {
-    if (!on) return;
-    const auto n = std::chrono::steady_clock::now();
-    fprintf(stderr, "[cftft host] %-14s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
-    t = n;
-  }
-};
-
 // Prime rings: the two-level Montgomery tables of omega's powers (omega^i R
 // mod p, i < 2^lo_bits; omega^(i 2^lo_bits) R mod p), built once per ring.
 int ensure_prime_tables(cftft_ring* R, cudaStream_t st) {
@@ -680,15 +661,12 @@ int ensure_prime_tables(cftft_ring* R, cudaStream_t st) {
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
   u64 launches = 0;
-  HostTrace ht;
   if (int rc = keep_pool()) return rc;
-  ht.mark("pool");
   if (dp.nleaves) {
     u32* counters = nullptr;
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
-    ht.mark("counters");
     // Fermat: two ticket buffers of `half` bytes each (a big ticket spans both)
     const size_t half = ((kSmemBudget - scratch_bytes(1024)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
@@ -727,13 +705,16 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         CUDA_TRY(cudaGetDevice(&dev));
         std::lock_guard<std::mutex> g(R->mu);
         cftft_ring::Scratch* sc = nullptr;
+        const bool dflt = st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread;
+        const std::thread::id me = dflt ? std::this_thread::get_id() : std::thread::id();
         for (auto& x : R->scratch)
-          if (x.dev == dev && x.stream == (void*)st) sc = &x;
+          if (x.dev == dev && x.stream == (void*)st && x.thread == me) sc = &x;
         if (!sc) {
           R->scratch.push_back(cftft_ring::Scratch{});
           sc = &R->scratch.back();
           sc->dev = dev;
           sc->stream = (void*)st;
+          sc->thread = me;
         }
         if (sc->tops_bytes < tb || sc->shadow_bytes < sb) {
           CUDA_TRY(cudaStreamSynchronize(st));  // the old buffers may still be in use
@@ -754,7 +735,6 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         }
         tops = static_cast<int*>(sc->tops);
         shadow = static_cast<std::uint8_t*>(sc->shadow);
-        ht.mark("scratch");
         // wave plans load no tops of elements they have not written (Plan::tops_clear)
         if (dp.host.tops_clear) CUDA_TRY(cudaMemsetAsync(tops, 0, tb, st));
       }
@@ -766,20 +746,18 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.no_deps = 0;
       A.half = (u32)half;
       unsigned long long* prof = nullptr;
-      static const bool profiling = getenv("CFTFT_PROFILE") != nullptr;
+      static const bool profiling = env_int("CFTFT_PROFILE", 0) != 0;
       if (profiling) {
         CUDA_TRY(cudaMallocAsync((void**)&prof, 8 * fermat::PH_N, st));
         CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * fermat::PH_N, st));
       }
       A.prof = prof;
-      static const u32 dbg = getenv("CFTFT_DEBUG_SKIP") ? (u32)atoi(getenv("CFTFT_DEBUG_SKIP")) : 0u;
+      static const u32 dbg = (u32)env_int("CFTFT_DEBUG_SKIP", 0);
       A.debug_skip = dbg;
       auto go = [&](auto kernel, int nt) -> int {
         if (int rc = set_smem(kernel)) return rc;
         if (int rc = grid_for(kernel, nt, smem, dp.nleaves, &grid)) return rc;
-        ht.mark("attrs");
         kernel<<<grid, nt, smem, st>>>(A);
-        ht.mark("launch");
         return CFTFT_OK;
       };
       int rc = 0;
@@ -807,39 +785,18 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         W.lanes = dp.C;
         W.D = R->D;
         W.M = R->M;
-        static const int wwarps = std::min(fermat::kWaveWarps, std::max(1, getenv("CFTFT_WAVE_WARPS")
-                                                                               ? atoi(getenv("CFTFT_WAVE_WARPS"))
-                                                                               : fermat::kWaveWarps));
+        const int wwarps = fermat::kWaveWarps;
         const size_t wsmem = (size_t)wwarps * fermat::wave_tile_words<8>() * 4;
-        const size_t wsmem16 = (size_t)wwarps * fermat::wave_tile_words<8, 16>() * 4;
-        static bool wave_attr = false;
-        if (!wave_attr) {
-          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, false>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
-          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, false, 16>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem16));
-          CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wave_kernel<8, true, 16>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem16));
-          wave_attr = true;
-        }
+        if (int e = set_smem_bytes(fermat::coset_wave_kernel<8, false>, wsmem)) return e;
+        if (int e = set_smem_bytes(fermat::coset_wave_kernel<8, true>, wsmem)) return e;
         int dev = 0, sms = 0, per = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8, false>, 32 * wwarps, wsmem));
-        int per16 = 0;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per16, fermat::coset_wave_kernel<8, false, 16>,
-                                                               32 * wwarps, wsmem16));
         const size_t xsmem = (size_t)fermat::wide_tile_words<8>() * 4;
         int xper = 0;
         if (dp.host.wide) {
-          static bool wide_attr = false;
-          if (!wide_attr) {
-            CUDA_TRY(cudaFuncSetAttribute(fermat::coset_wide_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)xsmem));
-            wide_attr = true;
-          }
+          if (int e = set_smem_bytes(fermat::coset_wide_kernel<8>, xsmem)) return e;
           CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, fermat::coset_wide_kernel<8>,
                                                                  32 * fermat::kWideWarps, xsmem));
         }
@@ -847,7 +804,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         bool tma_maps = false;
         for (size_t wi = 0; wi < dp.host.waves.size(); ++wi) {
           const auto& wr = dp.host.waves[wi];
-          if (wr[2] == 2 && dp.tma_wave[wi] && R->wide != 2) {
+          if (wr[2] == 2 && dp.tma_wave[wi]) {
             if (!tma_maps) {
               if (int e = make_coset_map(&tm_view, base, stride, dp.host.extent, dp.tma_step)) return e;
               if (int e = make_coset_map(&tm_shadow, shadow ? (void*)shadow : (void*)base, stride, dp.host.extent,
@@ -874,15 +831,6 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms * std::max(xper, 1));
             fermat::coset_wide_kernel<8><<<g, 32 * fermat::kWideWarps, xsmem, st>>>(W);
-          } else if (wr[2] == 3) {  // 16-slot warp tiles
-            W.leaves = dp.leaves + wr[0];
-            W.nleaves = (u32)wr[1];
-            W.gpl = (u32)std::max<u64>(1, wr[3]);
-            const unsigned g = (unsigned)std::min<u64>((wr[1] * W.gpl + wwarps - 1) / wwarps, (u64)sms * std::max(per16, 1));
-            if (W.logS)
-              fermat::coset_wave_kernel<8, true, 16><<<g, 32 * wwarps, wsmem16, st>>>(W);
-            else
-              fermat::coset_wave_kernel<8, false, 16><<<g, 32 * wwarps, wsmem16, st>>>(W);
           } else if (wr[2] == 1) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];
@@ -903,8 +851,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         }
         launches -= 1;  // counted once more below
       } else {
-        rc = dp.cw == 16 ? (R->NT == 256 ? go(fermat::leaf_kernel<16, 256>, 256) : go(fermat::leaf_kernel<16, 512>, 512))
-             : dp.cw == 8 ? (getenv("CFTFT_NT1024") ? go(fermat::leaf_kernel<8, 1024>, 1024) : go(fermat::leaf_kernel<8, 512>, 512))
+        rc = dp.cw == 16 ? go(fermat::leaf_kernel<16, 512>, 512)
+             : dp.cw == 8 ? go(fermat::leaf_kernel<8, 512>, 512)
                           : go(fermat::leaf_kernel<4, 512>, 512);
       }
       if (rc) return rc;
@@ -912,12 +860,8 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         // carry-save lanes of the outputs back to the canonical element format
         // (with the sub-lane rotations the outputs' last writers deferred)
         const size_t fsm = dp.final_rot ? (size_t)R->D * 4 : 0;
-        static size_t fattr = 0;
-        if (fsm > 40 * 1024 && fsm > fattr) {
-          CUDA_TRY(cudaFuncSetAttribute(fermat::cs_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)fsm));
-          fattr = fsm;
-        }
+        if (fsm > 40 * 1024)
+          if (int e = set_smem_bytes(fermat::cs_fold_kernel, fsm)) return e;
         const u32 logC = (u32)__builtin_ctz(dp.C);
         if (dp.host.use_fold_list) {
           // listed outputs in place, the shadow buffer's from there into place
@@ -929,7 +873,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
           if (!dp.host.shadow_finals.empty()) {
             fermat::cs_fold_kernel<<<(unsigned)dp.host.shadow_finals.size(), 256, fsm, st>>>(
                 base, stride, tops + A.tloc, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot,
-                dp.shadow_finals, shadow);
+                dp.shadow_finals, shadow, dp.tma_cm_finals ? (u32)__builtin_ctz(dp.tma_step) : 0u);
             ++launches;
           }
         } else if (dp.host.final_count) {
@@ -1033,8 +977,8 @@ int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* 
   auto* R = const_cast<cftft_ring*>(cR);
   const u64 L = p->length;
   const size_t need = (size_t)L * stride;
+  std::lock_guard<std::mutex> sg(R->stage_mu);
   {
-    std::lock_guard<std::mutex> g(R->mu);
     if (R->stage_bytes < need) {
       if (R->stage) cudaFree(R->stage);
       R->stage = nullptr;
@@ -1169,6 +1113,32 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
         if (e & 1) r = mulp(r, a);
       return r;
     };
+    // the reference rejects composite moduli (field.hpp:56-78, NotPrime):
+    // Miller-Rabin with the first twelve primes as bases, exact below 2^64
+    {
+      bool prime = true;
+      const u64 d0 = p - 1;
+      const int r0 = __builtin_ctzll(d0);
+      const u64 d = d0 >> r0;
+      for (u64 a : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull}) {
+        if (p % a == 0) {
+          prime = p == a;
+          break;
+        }
+        u64 x = powp(a, d);
+        if (x == 1 || x == p - 1) continue;
+        bool witness = true;
+        for (int i = 1; i < r0 && witness; ++i) {
+          x = mulp(x, x);
+          if (x == p - 1) witness = false;
+        }
+        if (witness) {
+          prime = false;
+          break;
+        }
+      }
+      if (!prime) return fail(CFTFT_INVALID_PARAMS, "prime ring: modulus is not prime");
+    }
     const u64 M = u64{1} << m;
     // smallest g in 2, 3, 5, 7, ... whose (p-1)/2^m power has order 2^m (field.hpp:170-177)
     u64 omega = 0;
@@ -1192,18 +1162,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   }
   // largest leaf whose slots fit the shared-memory budget (and the 16-bit slot ids)
   unsigned lam = 1;
-  if (kind == CFTFT_RING_FERMAT) {
-    const char* e = getenv("CFTFT_CTAS_PER_SM");
-    if (e && atoi(e) == 2 && R->CW == 16 && R->C <= 256) R->NT = 256;
-    const char* wv = getenv("CFTFT_WHOLE1024");  // experiment: whole leaves, 1024 threads, 256-bit chunks
-    if (wv && atoi(wv) == 1 && R->D >= 16) {
-      R->CW = 8;
-      R->C = R->D / 8;
-      R->slot_bytes = fermat_slot_bytes(R->C, 4 * R->CW);
-      R->NT = 1024;
-    }
-  }
-  const size_t per_cta = R->NT == 256 ? 96 * 1024 + scratch_bytes(R->NT) : kSmemBudget;
+  const size_t per_cta = kSmemBudget;
   const size_t budget = per_cta - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
   while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= budget) ++lam;
   R->max_leaf_ell = lam;
@@ -1254,8 +1213,8 @@ int cftft_ring_set_coset(cftft_ring* ring, int lane_words) {
 
 int cftft_ring_set_wide(cftft_ring* ring, int wide) {
   if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
-  if (wide < -1 || wide > 2)
-    return fail(CFTFT_INVALID_PARAMS, "wide must be -1 (environment), 0, 1 (TMA kernel) or 2 (CTA kernel only)");
+  if (wide < -1 || wide > 1)
+    return fail(CFTFT_INVALID_PARAMS, "wide must be -1 (default), 0 (radix-8 waves) or 1 (radix-64 waves)");
   std::lock_guard<std::mutex> g(ring->mu);
   if (ring->wide != wide) {
     ring->wide = wide;
@@ -1405,11 +1364,8 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   if (R->kind == CFTFT_RING_FERMAT && (u64)R->D * 12 <= 200 * 1024) {
     // one CTA per element: word-parallel shift, block-scan borrows (rotate_kernel)
     const size_t sm = (size_t)R->D * 12 + 128;  // + borrow masks of a small ring
-    static size_t rattr = 0;
-    if (sm > 40 * 1024 && sm > rattr) {  // with the static scan scratch
-      CUDA_TRY(cudaFuncSetAttribute(fermat::rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      rattr = sm;
-    }
+    if (sm > 40 * 1024)  // with the static scan scratch
+      if (int rc = set_smem_bytes(fermat::rotate_kernel, sm)) return rc;
     fermat::rotate_kernel<<<(unsigned)count, 256, sm, st>>>(static_cast<std::uint8_t*>(dev_base), elem_stride_bytes,
                                                             e, R->D);
     CUDA_TRY(cudaGetLastError());
@@ -1419,7 +1375,9 @@ int cftft_gpu_scale(const cftft_ring* cring, void* dev_base, uint64_t count,
   // A scale is a degenerate plan: one length-1 class (load, no ops, store
   // with rotation e) and one leaf per element.
   const u64 M = R->M;
-  PlanKey key{-1, 2, 1, e & (M - 1), count, 0, 0, 0};
+  int sdev = 0;
+  CUDA_TRY(cudaGetDevice(&sdev));
+  PlanKey key{sdev, 2, 1, e & (M - 1), count, 0, 0, 0};
   DevicePlan* dp = nullptr;
   {
     std::lock_guard<std::mutex> g(R->mu);
@@ -1488,13 +1446,28 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   PlanKey key{dev, 3 + (inverse ? 1 : 0), h, count, v[0].L, v[0].base, policy, -1};
+  std::vector<u64> bkey;
+  bkey.reserve(v.size() * 7);
+  for (const auto& it : v) bkey.insert(bkey.end(), {it.L, it.s, it.z, it.n, (u64)it.f, it.base, it.stride});
   DevicePlan* dp = nullptr;
   {
     std::lock_guard<std::mutex> g(R->mu);
     auto itc = R->cache.find(key);
+    if (itc != R->cache.end() && itc->second->batch_items != bkey) {
+      R->cache.erase(itc);  // a hash collision: replan
+      itc = R->cache.end();
+    }
     if (itc != R->cache.end()) {
       dp = itc->second.get();
     } else {
+      // bounded: batch shapes beyond kMaxBatchPlans evict the cached batches
+      size_t nb = 0;
+      for (const auto& kv : R->cache) nb += std::get<1>(kv.first) >= 3;
+      if (nb >= kMaxBatchPlans) {
+        CUDA_TRY(cudaStreamSynchronize(st));  // their device buffers may still be in use
+        for (auto it2 = R->cache.begin(); it2 != R->cache.end();)
+          it2 = std::get<1>(it2->first) >= 3 ? R->cache.erase(it2) : std::next(it2);
+      }
       auto np = std::make_unique<DevicePlan>();
       const RingShape rs = shape_of(R, v[0].L, np.get());
       try {
@@ -1503,6 +1476,7 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
         return fail(CFTFT_UNSUPPORTED, ex.what());
       }
       if (int rc = upload(R, *np, st)) return rc;
+      np->batch_items = std::move(bkey);
       dp = np.get();
       R->cache[key] = std::move(np);
     }

@@ -1365,7 +1365,8 @@ __global__ void shadow_copy_kernel(std::uint8_t* data, const std::uint8_t* data2
 // points at that buffer's tops) -- it is copied into place first.
 __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb, const int* T, u32 CL, u32 CW,
                                                       u32 logLanes, u32 logS, u32 D, u64 idx0, u64 istride,
-                                                      const u32* frot, const u64* idx, const std::uint8_t* src) {
+                                                      const u32* frot, const u64* idx, const std::uint8_t* src,
+                                                      u32 src_cm = 0) {
   __shared__ int s_pend[1024];
   extern __shared__ u32 s_old[];  // D words (frot only)
   const u64 e = idx ? idx[blockIdx.x] : idx0 + (u64)blockIdx.x * istride;
@@ -1374,7 +1375,22 @@ __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb
     const uint4* s4 = reinterpret_cast<const uint4*>(src + e * eb);
     uint4* d4 = reinterpret_cast<uint4*>(el);
     const u32 pieces = (4 * D + 8 + 15) / 16;
-    for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) d4[x] = __ldcg(s4 + x);
+    if (src_cm) {
+      // coset-major source (wave_tma.cuh): lane p = coset p mod 2^src_cm,
+      // row p >> src_cm, 1 KB per coset, 16-byte halves swapped on rows
+      // with bit 2 set; the top word follows the lanes as usual
+      const u32 lp = CL * 2;  // 16-byte pieces of the lanes
+      for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) {
+        u32 sx = x;
+        if (x < lp) {
+          const u32 p = x >> 1, h = x & 1u, row = p >> src_cm, cs = p & ((1u << src_cm) - 1);
+          sx = (cs << 6) | (row << 1) | (h ^ ((row >> 2) & 1u));
+        }
+        d4[x] = __ldcg(s4 + sx);
+      }
+    } else {
+      for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) d4[x] = __ldcg(s4 + x);
+    }
     __syncthreads();
   }
   const int* Te = T + e * CL;

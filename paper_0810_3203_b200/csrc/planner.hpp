@@ -236,9 +236,6 @@ struct RingShape {
   // run on the CTA kernel (csrc/wave_wide.cuh); the top-level split leaves
   // row nodes of 2^(6k) coefficients (three radix-64 passes at L = 2^18)
   bool wide = false;
-  // wave engine with coset leaves of up to 16 coefficients on the warp kernel
-  // (16-slot tiles): splits minimise the number of radix-16 passes
-  bool r16 = false;
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -435,16 +432,7 @@ class Planner {
       const LeafProgram& cl = classes_[c];
       p.wave_op_begin[c] = (u32)p.wave_ops.size();
       if (cl.kind != 1) continue;
-      if (cl.key.ell == 4 && !rs_.wide) {
-        // 16-slot warp tiles: the 16-point network's rotations in the
-        // kernel's op order, or the class's micro-ops
-        std::vector<u32> net;
-        p.wave_net[c] = network16(cl, M, net);
-        if (p.wave_net[c]) {
-          p.wave_ops.insert(p.wave_ops.end(), net.begin(), net.end());
-          continue;
-        }
-      } else if (cl.key.ell >= 4) {
+      if (cl.key.ell >= 4) {
         // CTA kernel: the radix-64 network's rotations per (stage, warp, op),
         // or the class's micro-ops
         std::vector<u32> net;
@@ -529,108 +517,7 @@ class Planner {
   u32 wave_kind(const LeafProgram& cl) const {
     if (cl.kind != 1) return 0;
     if (cl.key.ell <= 3) return 1u;
-    return rs_.wide ? 2u : 3u;  // 3: 16-slot warp tiles (coset_wave_kernel<.., 16>)
-  }
-
-  // 1 / 2: the 16-slot class runs as the radix-2 DIF (spans 8,4,2,1) / DIT
-  // (spans 1,2,4,8) network on the warp kernel's 16-slot tiles; `net` gets
-  // the rotation (coset positions << 16) of each of its 32 butterflies in the
-  // kernel's order -- DIF: the span-8 level (pairs j, j+8), then the 8-point
-  // network of slots 0-7, then of slots 8-15 (wave_coset.cuh op order);
-  // DIT: the two 8-point networks, then the span-8 level.  Checked like
-  // wide_network: program and network evaluated exactly over Z[x]/(x^8+1).
-  static u32 network16(const LeafProgram& cl, u64 M, std::vector<u32>& net) {
-    if (cl.key.ell != 4 || cl.nload == 0 || cl.ops.empty()) return 0;
-    const u64 unit = M >> 4;
-    constexpr u32 D = 8;  // positions per coset: x^8 = -1
-    using V = std::array<long long, D>;
-    auto rot = [](const V& v, u64 q) {
-      V r{};
-      for (u32 d = 0; d < D; ++d) {
-        const u64 t = d + q;
-        r[t % D] = ((t / D) & 1) ? -v[d] : v[d];
-      }
-      return r;
-    };
-    auto ilog = [](u32 h) { u32 l = 0; while ((1u << l) < h) ++l; return l; };
-    for (u32 kind = 1; kind <= 2; ++kind) {
-      int qn[4][8];
-      for (auto& row : qn)
-        for (int& q : row) q = -1;
-      std::array<int, 16> last;
-      last.fill(-1);
-      bool ok = true;
-      for (const DevOp& op : cl.ops) {
-        const u32 a = op.a, b = op.b, h = b - a;
-        if (op.type > OP_COPY || b <= a || b >= 16 || (h & (h - 1)) || (a & h)) { ok = false; break; }
-        const int lvl = kind == 1 ? 3 - (int)ilog(h) : (int)ilog(h);
-        if (last[a] >= lvl || last[b] >= lvl) { ok = false; break; }
-        last[a] = last[b] = lvl;
-        if (op.type != OP_COPY && op.r % unit) { ok = false; break; }
-        qn[lvl][(a / (2 * h)) * h + a % h] = op.type == OP_COPY ? 0 : (int)((op.r / unit) % (2 * D));
-      }
-      if (!ok) continue;
-      std::vector<V> x0(16), x1;
-      u64 seed = 0x2545F4914F6CDD1Dull * (cl.key.z * 131 + cl.key.n * 7 + cl.key.f * 3 + kind);
-      for (u32 k = 0; k < 16; ++k)
-        for (u32 d = 0; d < D; ++d) {
-          seed = seed * 6364136223846793005ull + 1442695040888963407ull;
-          x0[k][d] = k < cl.nload ? (long long)((seed >> 33) % 2001) - 1000 : 0;
-        }
-      x1 = x0;
-      for (const DevOp& op : cl.ops) {
-        V& A = x1[op.a];
-        V& B = x1[op.b];
-        if (op.type == OP_COPY) { B = A; continue; }
-        const V rb = rot(B, (op.r / unit) % (2 * D));
-        V s0, s1;
-        for (u32 d = 0; d < D; ++d) {
-          s0[d] = (op.type == OP_SUB2 || op.type == OP_SUB2DIFF ? 2 * A[d] - rb[d] : A[d] + rb[d]);
-          s1[d] = A[d] - rb[d];
-        }
-        A = s0;
-        if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF) B = s1;
-      }
-      std::vector<V> y = x0;
-      for (int lvl = 0; lvl < 4; ++lvl) {
-        const u32 h = kind == 1 ? (8u >> lvl) : (1u << lvl);
-        for (u32 j = 0; j < 8; ++j) {
-          const u32 a = (j / h) * 2 * h + j % h;
-          const V rb = rot(y[a + h], (u64)std::max(0, qn[lvl][j]));
-          for (u32 d = 0; d < D; ++d) {
-            const long long av = y[a][d];
-            y[a][d] = av + rb[d];
-            y[a + h][d] = av - rb[d];
-          }
-        }
-      }
-      for (u32 k = 0; k < cl.nstore && ok; ++k) ok = y[k] == x1[k];
-      if (!ok) continue;
-      auto q_of = [&](int lvl, u32 a, u32 h) {
-        return (u32)std::max(0, qn[lvl][(a / (2 * h)) * h + a % h]) << 16;
-      };
-      net.assign(32, 0);
-      // the 8-point network of slots 8 hh .. 8 hh + 7 at ops [o0, o0 + 12)
-      auto half_net = [&](u32 o0, u32 hh, int lvl0) {
-        for (u32 o = 0; o < 12; ++o) {
-          const u32 ll = o / 4, jj = o % 4;
-          const u32 hl = kind == 1 ? (4u >> ll) : (1u << ll);
-          const u32 al = (jj / hl) * 2 * hl + jj % hl;
-          net[o0 + o] = q_of(lvl0 + (int)ll, 8 * hh + al, hl);
-        }
-      };
-      if (kind == 1) {
-        for (u32 j = 0; j < 8; ++j) net[j] = q_of(0, j, 8);
-        half_net(8, 0, 1);
-        half_net(20, 1, 1);
-      } else {
-        half_net(0, 0, 0);
-        half_net(12, 1, 0);
-        for (u32 j = 0; j < 8; ++j) net[24 + j] = q_of(3, j, 8);
-      }
-      return kind;
-    }
-    return 0;
+    return 2u;
   }
 
   // 1 / 2: the 64-slot class runs as the radix-2 DIF (spans 32..1, the TFT's)
@@ -849,28 +736,7 @@ class Planner {
 
   // Split for a node: the reference's policy at the top (transform.hpp:83-87),
   // an SMEM-sized near-balanced split below it.
-  // radix-16 plans: the split with the fewest radix-16 passes
-  // (ceil(l1/4) + ceil(l2/4)), the most balanced among those
-  static void split16(unsigned ell, unsigned& l1, unsigned& l2) {
-    unsigned best = ~0u;
-    for (unsigned a = 1; a < ell; ++a) {
-      const unsigned cost = (a + 3) / 4 + (ell - a + 3) / 4;
-      const unsigned imb = a > ell - a ? 2 * a - ell : ell - 2 * a;
-      const unsigned key = cost * 64 + imb * 2 + (a > ell - a ? 1 : 0);
-      if (key < best) {
-        best = key;
-        l1 = a;
-      }
-    }
-    l2 = ell - l1;
-  }
-
   void split(unsigned ell, int policy, bool top, unsigned& l1, unsigned& l2) const {
-    if (top && rs_.r16 && !policy_everywhere_ && ell > 4) {
-      // any split gives the same outputs (transform_test.cpp:248-272)
-      split16(ell, l1, l2);
-      return;
-    }
     if (top && rs_.wide && !policy_everywhere_ && ell > 6) {
       // any split gives the same outputs (transform_test.cpp:248-272): the
       // row nodes get 2^(6k) coefficients (radix-64 passes), the columns the rest
@@ -970,12 +836,8 @@ class Planner {
         l2 = ell - l1;
       }
     } else if (coset_on && depth > 0) {
-      if (rs_.r16) {
-        split16(ell, l1, l2);
-      } else {
-        l1 = ell / 2;
-        l2 = ell - l1;
-      }
+      l1 = ell / 2;
+      l2 = ell - l1;
     } else {
       split(ell, policy, depth == 0, l1, l2);
     }
@@ -1550,7 +1412,7 @@ inline double plan_cost(const Plan& p, u64 elem_bytes) {
 // ---------------------------------------------------------------------------
 // Base-case counts of the REFERENCE recursion (policy at every level), by
 // replay without arithmetic; memoised since counts are data independent
-// (verify.hpp:459-483).
+// (verify.hpp:175-199).
 class CountReplay {
  public:
   u64 tft(u64 L, u64 z, u64 n, int policy) {

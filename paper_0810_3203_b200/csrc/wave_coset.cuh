@@ -257,8 +257,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
     // the ticket's slot table and the class's first 32 packed ops, one word
     // per lane, broadcast by shuffles (no dependent global loads in the loops)
     const u32 span = max(cl.nload, cl.nstore);
-    // (a 16-slot network's table has 32 rotations whatever the class's op count)
-    const u32 nwo = (cl.wnet && cl.L == 16) ? 32u : cl.nops;
+    const u32 nwo = cl.nops;
     const u32 opv0 = lane < nwo ? A.wops[cl.wop_begin + lane] : 0u;
     // the ticket's slots, resolved once (lane k: slot k) and read back by
     // broadcast; the previous ticket's groups are done with the table
@@ -539,21 +538,7 @@ __global__ void __launch_bounds__(32 * kWaveWarps, 4) coset_wave_kernel(WaveArgs
             spanp(4, 4, b0, ob + 8, out, false, false);
           }
         };
-        if (S == 16 && cl.L == 16) {
-          // 16 slots (Planner::network16 op order): DIF = span 8, then the
-          // 8-point networks of slots 0-7 and 8-15; DIT = those, then span 8
-          if (cl.wnet == 1) {
-            spanp(8, 8, 0, 0, false, true, fused);
-            net8(0, 8, true, true, false, false);
-            net8(8, 20, true, true, false, false);
-          } else {
-            net8(0, 0, false, false, true, fused);
-            net8(8, 12, false, false, true, fused);
-            spanp(8, 8, 0, 24, true, false, false);
-          }
-        } else {
-          net8(0, 0, cl.wnet == 1, true, true, fused);
-        }
+        net8(0, 0, cl.wnet == 1, true, true, fused);
         __syncwarp();
         continue;
       }

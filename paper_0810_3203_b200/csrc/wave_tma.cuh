@@ -362,29 +362,45 @@ __device__ __forceinline__ void tile_prefetch(const WaveArgs& A, const CUtensorM
 template <bool DIF>
 __device__ __forceinline__ void warp_load(const WaveArgs& A, const TmaLeafDesc& d, u32 g, u32 w, u32 lane, u32 apre,
                                           u32 alay, u32 tile, u32 step) {
+  // lane j < 8 resolves slot j once: its source coset's row 0, its tops row,
+  // the element's top word, the row stride and what to load
+  u64 rows = 0, trow = 0, hw = 0;
+  u32 fl = 0;  // bit 0: load, 1: coset-major, 2: tops, 3: top word
+  {
+    const u32 slot = slot_a(DIF ? 1u : 2u, w, lane & 7u);
+    if (lane < 8 && slot < d.nload) {
+      const u32 r = apre & 0x3FFFFFFFu;
+      const u32 cA = src_coset(apre, g, step);
+      const bool unal = (r & 255u) != 0, fresh = (apre >> 30) & 1u, sh = apre >> 31;
+      const u64 e = d.base + (u64)slot * d.stride;
+      const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+      rows = reinterpret_cast<u64>(el + ((alay & 1u) ? (u64)cA * 1024u : 32ull * cA));
+      trow = reinterpret_cast<u64>(A.T + (sh ? A.tloc : 0) + e * A.lanes + cA * 32u);
+      hw = reinterpret_cast<u64>(el + 4ull * A.D);
+      fl = 1u | ((alay & 1u) << 1) | (fresh ? 0u : 4u) | ((cA == 0 || (unal && cA == 1)) ? 8u : 0u);
+    }
+  }
+  const u32 rstride = 32u * step;
 #pragma unroll 1
   for (u32 j = 0; j < 8; ++j) {
+    const u32 f = __shfl_sync(0xffffffffu, fl, (int)j);
+    if (!(f & 1u)) break;  // (later slots are truncated too)
     const u32 slot = slot_a(DIF ? 1u : 2u, w, j);
-    if (slot >= d.nload) break;  // (later slots are truncated too)
-    const u32 pre = __shfl_sync(0xffffffffu, apre, (int)j);
-    const u32 lay = __shfl_sync(0xffffffffu, alay, (int)j);
-    const u32 r = pre & 0x3FFFFFFFu;
-    const u32 cA = src_coset(pre, g, step);
-    const bool unal = (r & 255u) != 0, fresh = (pre >> 30) & 1u, sh = pre >> 31;
-    const u64 e = d.base + (u64)slot * d.stride;
-    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
     const u32 dst = tile + kTileRows + slot * 1024u;
-    if (lay & 1u) {  // coset-major chunks are stored swizzled: a linear copy
-      const std::uint8_t* src = el + (u64)cA * 1024u + 32u * lane;
-      cp_async16(dst + 32u * lane, src);
-      cp_async16(dst + 32u * lane + 16u, src + 16);
+    const std::uint8_t* rp = reinterpret_cast<const std::uint8_t*>(__shfl_sync(0xffffffffu, rows, (int)j));
+    if (f & 2u) {  // coset-major chunks are stored swizzled: a linear copy
+      cp_async16(dst + 32u * lane, rp + 32u * lane);
+      cp_async16(dst + 32u * lane + 16u, rp + 32u * lane + 16u);
     } else {
-      const std::uint8_t* src = el + 32ull * (cA + step * lane);
+      const std::uint8_t* src = rp + (u64)rstride * lane;
       cp_async16_l2(dst + sw_off(lane, 0), src);
       cp_async16_l2(dst + sw_off(lane, 1), src + 16);
     }
-    if (!fresh) cp_async4(tile + kTileTops + slot * 128u + 4u * lane, A.T + (sh ? A.tloc : 0) + e * A.lanes + cA * 32u + lane);
-    if (lane == 0 && (cA == 0 || (unal && cA == 1))) cp_async8(tile + kTileHiw + slot * 16u, el + 4ull * A.D);
+    if (f & 4u)
+      cp_async4(tile + kTileTops + slot * 128u + 4u * lane,
+                reinterpret_cast<const int*>(__shfl_sync(0xffffffffu, trow, (int)j)) + lane);
+    const u64 h = __shfl_sync(0xffffffffu, hw, (int)j);
+    if (lane == 0 && (f & 8u)) cp_async8(tile + kTileHiw + slot * 16u, reinterpret_cast<const void*>(h));
   }
   cp_async_commit();
 }
@@ -468,13 +484,18 @@ __device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u
       }
       // signs differ only where the source index wraps between B and A
       const bool mixed = negB != sa.neg;
-      Ch<8> bs;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) bs.w[k] = mixed ? 0u : b.w[k];
+      const bool anym = __any_sync(0xffffffffu, mixed);
       Ch<8> out;
-      t = unal_combine8(out, bs, x, mixed ? 0 : tb, o);  // the whole lane, or low(A) where mixed
+      if (anym) {
+        Ch<8> bs;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bs.w[k] = mixed ? 0u : b.w[k];
+        t = unal_combine8(out, bs, x, mixed ? 0 : tb, o);  // the whole lane, or low(A) where mixed
+      } else {
+        t = unal_combine8(out, b, x, tb, o);
+      }
       if (__any_sync(0xffffffffu, sa.neg)) neg_if8(out, t, sa.neg);
-      if (__any_sync(0xffffffffu, mixed)) {
+      if (anym) {
         Ch<8> z, h;
 #pragma unroll
         for (int k = 0; k < 8; ++k) z.w[k] = 0;

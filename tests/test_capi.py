@@ -96,7 +96,7 @@ def test_counts_full_transform_hits_ceiling():  # transform_test.cpp:342-351
             assert 2 * cf.itft_base_cases(L, L, L, 0, pol) == L * ell
 
 
-def test_counts_respect_bounds():  # verify.hpp:507-553
+def test_counts_respect_bounds():  # verify.hpp:223-269
     for ell in range(1, 6):
         L = 1 << ell
         for z in range(1, L + 1):
@@ -350,20 +350,21 @@ def test_linear_form_and_doubling_leaves():
     assert seen_linear > 0
 
 
-def test_radix16_schedule_reproduces_definition():
-    """Opt-in radix-16 warp tiles (CFTFT_R16=1): 16-point networks, the
-    wave-minimising splits and the plan choice, evaluated in a subprocess
-    (the switch is read once per process)."""
-    import subprocess
-    import sys
-    code = (
-        "import random, sys; sys.path.insert(0, 'tests'); sys.path.insert(0, 'oracle');"
-        "import test_capi as t; import paper_0810_3203_b200 as cf;"
-        "ctx = cf.FermatRingCtx(8192);"
-        "d = cf.plan_dump(ctx, False, cf.TransformParams(1 << 9, 0, 500, 500, 0));"
-        "assert any(c['ell'] == 4 and c.get('net') for c in d['classes']), 'no 16-point network';"
-        "t.check_plan(ctx, 8192, random.Random(16), 8, 5, 9)"
-    )
-    env = dict(os.environ, CFTFT_R16="1")
-    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_ring_create_ranges_and_primality():
+    """Ring contexts reject what the header says they reject, before any GPU
+    work: Fermat N outside [128, 2^18] or not a power of two, a composite
+    prime-ring modulus (the reference's NotPrime, field.hpp:56-78), a prime
+    without 2^m | p - 1."""
+    for N in (64, 96, 1 << 19):
+        with pytest.raises(cf.Unsupported):
+            cf.FermatRingCtx(N)
+    cf.FermatRingCtx(128)
+    with pytest.raises(cf.InvalidParams):
+        cf.PrimeRingCtx(1, 15)  # 15 = 3 * 5, odd, 2 | 14
+    with pytest.raises(cf.InvalidParams):
+        cf.PrimeRingCtx(2, 97 * 193)  # composite with 4 | p - 1
+    with pytest.raises(cf.InvalidParams):
+        cf.PrimeRingCtx(4, 7)  # prime, 16 does not divide 6
+    assert cf.PrimeRingCtx(4, 97).root_order() == 16
