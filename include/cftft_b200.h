@@ -42,7 +42,8 @@ enum cftft_status {
   CFTFT_INVALID_PARAMS = 2, /* z, n, f outside the reference's contract      */
   CFTFT_CUDA_ERROR = 3,     /* CUDA runtime failure (no GPU, launch error)  */
   CFTFT_UNSUPPORTED = 4,    /* ring/stride the engine does not implement    */
-  CFTFT_NO_MEMORY = 5
+  CFTFT_NO_MEMORY = 5,
+  CFTFT_POISON_READ = 6     /* debug poison: a cell >= z was read (below)    */
 };
 
 /* CFTFT_RING_PRIME: the reference's own ring, Z/pZ for an odd prime p < 2^64
@@ -182,6 +183,21 @@ uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int po
 /* Launch statistics of the last transform issued on this thread: number of
  * kernels enqueued (for bench.py's gpu_launches). */
 uint64_t cftft_last_launch_count(void);
+
+/* cftft::fault::corrupt_tft_base (transform.hpp:53-56, 109): while set,
+ * every forward transform ends with a one-thread kernel that adds the ring's
+ * 1 to output x[0] (a corrupted butterfly), so verification sweeps must
+ * fail.  Process-global, like the reference's hook (cftft_cli.cpp:41). */
+void cftft_set_fault_injection(int on);
+int cftft_fault_injection(void);
+
+/* Debug poison (transform.hpp:58-70, poison_tail): while set, cftft_gpu_tft
+ * / cftft_gpu_itft run each transform twice, with two different
+ * non-canonical fills of the cells [z, L) (inputs [0, z) restored in
+ * between), and return CFTFT_POISON_READ if any specified output (x[0, n),
+ * plus x[n] for an ITFT with f = 1) differs: a cell the contract leaves
+ * unspecified was read before it was written.  Synchronous; debug only. */
+void cftft_set_debug_poison(int on);
 
 /* Debug: JSON description of the GPU schedule (leaves, waves, micro-ops) a
  * transform would run.  Pure host code (no GPU).  Returns the number of

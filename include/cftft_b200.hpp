@@ -43,6 +43,18 @@ struct CudaError : std::runtime_error {
 struct Unsupported : std::runtime_error {
   explicit Unsupported(const std::string& what) : std::runtime_error(what) {}
 };
+// debug poison (cftft_set_debug_poison): an output depended on a cell >= z
+struct PoisonRead : std::logic_error {
+  explicit PoisonRead(const std::string& what) : std::logic_error(what) {}
+};
+
+// cftft::fault::corrupt_tft_base (transform.hpp:53-56): the reference's hook
+// is a global flag; here it is the library's (forward transforms add 1 to
+// x[0] while set).
+namespace fault {
+inline void set_corrupt_tft_base(bool on) { cftft_set_fault_injection(on ? 1 : 0); }
+inline bool corrupt_tft_base() { return cftft_fault_injection() != 0; }
+}  // namespace fault
 
 inline void check(int rc) {
   if (rc == CFTFT_OK) return;
@@ -51,6 +63,7 @@ inline void check(int rc) {
     case CFTFT_BAD_LENGTH: throw BadLength(msg);
     case CFTFT_INVALID_PARAMS: throw InvalidParams(msg);
     case CFTFT_CUDA_ERROR: throw CudaError(msg);
+    case CFTFT_POISON_READ: throw PoisonRead(msg);
     default: throw Unsupported(msg);
   }
 }

@@ -39,7 +39,7 @@ __all__ = [
     "cf_tft", "cf_itft", "cf_tft_host", "cf_itft_host", "bit_reverse", "tft_bound",
     "itft_bound", "tft_base_cases", "itft_base_cases", "lib", "last_launch_count", "plan_dump", "PrimeRingCtx",
     "GOLDILOCKS",
-    "scale",
+    "scale", "set_fault_injection", "fault_injection", "set_debug_poison", "PoisonRead", "NoMemory",
 ]
 
 
@@ -76,6 +76,14 @@ class CudaError(RuntimeError):
 
 class Unsupported(RuntimeError):
     pass
+
+
+class NoMemory(MemoryError):
+    pass
+
+
+class PoisonRead(AssertionError):
+    """Debug poison (set_debug_poison): an output depended on a cell >= z."""
 
 
 class _Params(C.Structure):
@@ -129,6 +137,11 @@ def lib():
         L.cftft_plan_dump.restype = C.c_size_t
         L.cftft_last_error.restype = C.c_char_p
         L.cftft_version.restype = C.c_char_p
+        L.cftft_set_fault_injection.argtypes = [C.c_int]
+        L.cftft_set_fault_injection.restype = None
+        L.cftft_fault_injection.restype = C.c_int
+        L.cftft_set_debug_poison.argtypes = [C.c_int]
+        L.cftft_set_debug_poison.restype = None
         _lib = L
     return _lib
 
@@ -137,7 +150,8 @@ def _check(rc: int) -> None:
     if rc == 0:
         return
     msg = lib().cftft_last_error().decode()
-    raise {1: BadLength, 2: InvalidParams, 3: CudaError, 4: Unsupported}.get(rc, RuntimeError)(msg)
+    raise {1: BadLength, 2: InvalidParams, 3: CudaError, 4: Unsupported, 5: NoMemory,
+           6: PoisonRead}.get(rc, RuntimeError)(msg)
 
 
 class _Ring:
@@ -368,6 +382,23 @@ def tft_base_cases(L: int, z: int, n: int, policy=SplitPolicy.balanced) -> int:
 
 def itft_base_cases(L: int, z: int, n: int, f: int, policy=SplitPolicy.balanced) -> int:
     return lib().cftft_itft_base_cases(L, z, n, f, int(policy))
+
+
+def set_fault_injection(on: bool) -> None:
+    """fault::corrupt_tft_base (transform.hpp:53-56): while on, forward
+    transforms add the ring's 1 to x[0], so verification must fail."""
+    lib().cftft_set_fault_injection(1 if on else 0)
+
+
+def fault_injection() -> bool:
+    return bool(lib().cftft_fault_injection())
+
+
+def set_debug_poison(on: bool) -> None:
+    """poison_tail (transform.hpp:58-70) as a GPU debug mode: every device
+    transform runs twice with different fills of the cells >= z and raises
+    PoisonRead if a specified output differs."""
+    lib().cftft_set_debug_poison(1 if on else 0)
 
 
 def last_launch_count() -> int:

@@ -11,6 +11,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <atomic>
 #include <sstream>
 #include <thread>
 #include <string>
@@ -32,6 +33,8 @@ using namespace cftft_b200;
 namespace {
 
 thread_local std::string g_last_error;
+std::atomic<int> g_fault{0};   // cftft_set_fault_injection
+std::atomic<int> g_poison{0};  // cftft_set_debug_poison
 
 // Experiment knobs (phase clocks, debug skips) exist only in builds with
 // -DCFTFT_EXPERIMENTS; the shipped library reads no environment variables.
@@ -954,6 +957,24 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
   return CFTFT_OK;
 }
 
+// fault::corrupt_tft_base on the GPU: element 0 += 1 in the ring (Fermat:
+// N/64 limbs + top word, canonical; negacyclic: word 0 mod m; prime: mod p)
+__global__ void fault_add_one_kernel(std::uint8_t* el, int kind, u64 words, u64 m) {
+  u64* w = reinterpret_cast<u64*>(el);
+  if (kind == CFTFT_RING_FERMAT) {
+    const u64 limbs = words / 2;  // words = D (u32 words)
+    if (w[limbs]) {  // 2^N + 1 == 0
+      w[limbs] = 0;
+      return;
+    }
+    u64 i = 0;
+    while (i < limbs && ++w[i] == 0) ++i;
+    if (i == limbs) w[limbs] = 1;  // 2^N - 1 + 1
+  } else {
+    w[0] = (w[0] + 1 == m) ? 0 : w[0] + 1;
+  }
+}
+
 int transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* dev_base, u64 stride,
               int policy, uint64_t* count, void* stream) {
   if (int rc = validate(cR, inv, p, policy)) return rc;
@@ -967,7 +988,55 @@ int transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* dev_b
   auto st = static_cast<cudaStream_t>(stream);
   DevicePlan* dp = nullptr;
   if (int rc = get_plan(R, inv, *p, policy, st, &dp)) return rc;
-  return launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), stride, st, true);
+  auto* base = static_cast<std::uint8_t*>(dev_base);
+  auto run = [&]() -> int {
+    if (int rc = launch_plan(R, *dp, base, stride, st, true)) return rc;
+    if (!inv && g_fault.load()) {
+      // fault::corrupt_tft_base: x[0] += 1 in the ring
+      fault_add_one_kernel<<<1, 1, 0, st>>>(base, R->kind, R->kind == CFTFT_RING_NEGACYCLIC ? R->K : (u64)R->D,
+                                           R->m);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return CFTFT_OK;
+  };
+  if (!g_poison.load()) return run();
+  // debug poison: two runs with different fills of [z, L); the specified
+  // outputs must agree bit for bit
+  const u64 L = p->length, z = p->input_count;
+  const u64 o = inv ? p->output_count + (u64)p->want_next : p->output_count;
+  const size_t eb = R->elem_bytes;
+  void *save = nullptr, *out1 = nullptr;
+  CUDA_TRY(cudaMalloc(&save, (size_t)L * eb));
+  CUDA_TRY(cudaMalloc(&out1, (size_t)o * eb));
+  int rc = CFTFT_OK;
+  auto fail_free = [&](int code) {
+    cudaFree(save);
+    cudaFree(out1);
+    return code;
+  };
+  if (cudaMemcpy2DAsync(save, eb, base, stride, eb, z, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return fail_free(fail(CFTFT_CUDA_ERROR, "poison: save"));
+  for (int pass = 0; pass < 2 && !rc; ++pass) {
+    if (pass && cudaMemcpy2DAsync(base, stride, save, eb, eb, z, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return fail_free(fail(CFTFT_CUDA_ERROR, "poison: restore"));
+    if (L > z && cudaMemset2DAsync(base + z * stride, stride, pass ? 0xA5 : 0xFF, eb, L - z, st) != cudaSuccess)
+      return fail_free(fail(CFTFT_CUDA_ERROR, "poison: fill"));
+    rc = run();
+    if (!rc && !pass &&
+        cudaMemcpy2DAsync(out1, eb, base, stride, eb, o, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      rc = fail(CFTFT_CUDA_ERROR, "poison: keep");
+  }
+  if (rc) return fail_free(rc);
+  std::vector<std::uint8_t> a((size_t)o * eb), b((size_t)o * eb);
+  if (cudaMemcpy2DAsync(a.data(), eb, out1, eb, eb, o, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpy2DAsync(b.data(), eb, base, stride, eb, o, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return fail_free(fail(CFTFT_CUDA_ERROR, "poison: compare"));
+  for (u64 i = 0; i < o; ++i)
+    if (std::memcmp(a.data() + i * eb, b.data() + i * eb, eb) != 0)
+      return fail_free(fail(CFTFT_POISON_READ, "output " + std::to_string(i) +
+                                                   " depends on the cells >= z (read before written)"));
+  return fail_free(CFTFT_OK);
 }
 
 int host_transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* host_base,
@@ -1518,6 +1587,9 @@ uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int po
 }
 
 uint64_t cftft_last_launch_count(void) { return g_last_launches; }
+void cftft_set_fault_injection(int on) { g_fault.store(on ? 1 : 0); }
+int cftft_fault_injection(void) { return g_fault.load(); }
+void cftft_set_debug_poison(int on) { g_poison.store(on ? 1 : 0); }
 
 size_t cftft_plan_dump(const cftft_ring* ring, int inverse, const cftft_params* params, int policy,
                        char* buf, size_t cap) {
