@@ -43,7 +43,8 @@ enum cftft_status {
   CFTFT_CUDA_ERROR = 3,     /* CUDA runtime failure (no GPU, launch error)  */
   CFTFT_UNSUPPORTED = 4,    /* ring/stride the engine does not implement    */
   CFTFT_NO_MEMORY = 5,
-  CFTFT_POISON_READ = 6     /* debug poison: a cell >= z was read (below)    */
+  CFTFT_POISON_READ = 6,    /* debug poison: a cell >= z was read (below)    */
+  CFTFT_TOO_LARGE = 7       /* poly_mul: product longer than the root order  */
 };
 
 /* CFTFT_RING_PRIME: the reference's own ring, Z/pZ for an odd prime p < 2^64
@@ -167,6 +168,51 @@ int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, 
 
 /* Negacyclic rings: x[i] <- c * x[i] word-wise mod m (e.g. poly_mul's final
  * L^-1 scale, polymul.hpp:82-87). */
+/* The same with an extra factor on every product: Z/(2^N+1): 2^scale
+ * (scale < 2N; poly_mul's L^-1 = 2^(2N - ell)); negacyclic and prime rings:
+ * the scalar `scale` mod m / p.  cftft_gpu_pointwise is scale = 2^0 / 1. */
+int cftft_gpu_pointwise_scaled(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
+                               uint64_t elem_stride_bytes, uint64_t scale, void* stream);
+
+/* cftft::MulStats (polymul.hpp:39-43): exactly n pointwise products, the
+ * transform length L, and the base cases of all three transforms. */
+typedef struct cftft_mul_stats {
+  uint64_t pointwise_mults;
+  uint64_t transform_length;
+  uint64_t base_case_count;
+} cftft_mul_stats;
+
+/* cftft::poly_mul (polymul.hpp:48-95) on the GPU: g (zg elements) times h
+ * (zh elements), both DEVICE arrays at elem_stride_bytes, into dev_out
+ * (n = zg + zh - 1 canonical elements); the caller passes the supports
+ * (cftft_gpu_poly_support computes poly_support, polymul.hpp:26-30).  TFT,
+ * TFT, n pointwise products with the final L^-1 folded in, ITFT -- all on
+ * the GPU, asynchronous on `stream` (workspace is stream-ordered).  zg or
+ * zh = 0 gives the zero polynomial (nothing written, stats zero); n > M is
+ * CFTFT_TOO_LARGE (cftft::TooLarge, polymul.hpp:13-18). */
+int cftft_gpu_poly_mul(const cftft_ring* ring, const void* dev_g, uint64_t zg, const void* dev_h, uint64_t zh,
+                       void* dev_out, uint64_t elem_stride_bytes, int policy, cftft_mul_stats* stats,
+                       void* stream);
+/* poly_support (polymul.hpp:26-30): 1 + the index of the last nonzero
+ * element of a DEVICE array of len elements (0: zero polynomial).  Waits. */
+int cftft_gpu_poly_support(const cftft_ring* ring, const void* dev_a, uint64_t len, uint64_t elem_stride_bytes,
+                           uint64_t* support, void* stream);
+
+/* Schoenhage-Strassen packing: count coefficients of
+ * src_words little-endian u64 limbs each (contiguous) zero-extended into
+ * ring elements at elem_stride_bytes. */
+int cftft_gpu_pack_limbs(const cftft_ring* ring, void* dev_dst, uint64_t elem_stride_bytes, const void* dev_src,
+                         uint64_t src_words, uint64_t count, void* stream);
+
+/* Nussbaumer, negacyclic rings (Z/mZ)[y]/(y^K+1), y = x^s:
+ * split: f (K s residues) -> s elements A_j with word k = f[j + s k];
+ * join: h[j + s k] = (C_j + y C_{j+s})[k] mod m for j < s, from the 2s - 1
+ * product elements C (C_{j+s} = 0 past them). */
+int cftft_gpu_nussbaumer_split(const cftft_ring* ring, void* dev_dst, uint64_t elem_stride_bytes,
+                               const uint64_t* dev_f, uint64_t s, void* stream);
+int cftft_gpu_nussbaumer_join(const cftft_ring* ring, uint64_t* dev_h, const void* dev_c, uint64_t elem_stride_bytes,
+                              uint64_t s, void* stream);
+
 int cftft_gpu_mul_scalar(const cftft_ring* ring, void* dev_base, uint64_t count, uint64_t elem_stride_bytes,
                          uint64_t c, void* stream);
 

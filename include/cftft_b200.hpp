@@ -43,6 +43,10 @@ struct CudaError : std::runtime_error {
 struct Unsupported : std::runtime_error {
   explicit Unsupported(const std::string& what) : std::runtime_error(what) {}
 };
+// cftft::TooLarge (polymul.hpp:13-18): the product does not fit the root order
+struct TooLarge : std::length_error {
+  explicit TooLarge(const std::string& what) : std::length_error(what) {}
+};
 // debug poison (cftft_set_debug_poison): an output depended on a cell >= z
 struct PoisonRead : std::logic_error {
   explicit PoisonRead(const std::string& what) : std::logic_error(what) {}
@@ -64,6 +68,7 @@ inline void check(int rc) {
     case CFTFT_INVALID_PARAMS: throw InvalidParams(msg);
     case CFTFT_CUDA_ERROR: throw CudaError(msg);
     case CFTFT_POISON_READ: throw PoisonRead(msg);
+    case CFTFT_TOO_LARGE: throw TooLarge(msg);
     default: throw Unsupported(msg);
   }
 }
@@ -189,6 +194,66 @@ inline void cf_itft_host(const Ring& ring, const TransformParams& params, void* 
   check(cftft_itft_host(ring.handle(), &p, buffer, elem_stride_bytes, static_cast<int>(policy),
                         stats ? &count : nullptr));
   if (stats) stats->base_case_count += count;
+}
+
+/// The reference's own ring: Z/pZ, omega of order 2^m (field.hpp:84-185).
+class PrimeRing : public Ring {
+ public:
+  explicit PrimeRing(u64 p = 0xFFFFFFFF00000001ull, unsigned m = 32) : Ring(CFTFT_RING_PRIME, m, p) {}
+};
+
+// ---------------------------------------------------------------------------
+// poly_mul (polymul.hpp:26-95) over device memory
+
+struct MulStats {
+  u64 pointwise_mults = 0;   // exactly the product length, never the padded L
+  u64 transform_length = 0;  // L, or 0 when a zero input short-circuits
+  ButterflyStats butterflies;  // all three transforms combined
+};
+
+/// A polynomial on the device: coefficient i is element i of `view`
+/// (contiguous: view.stride() == 1).
+inline u64 poly_support(const Ring& ring, const DeviceView& a, void* stream = nullptr) {
+  uint64_t k = 0;
+  check(cftft_gpu_poly_support(ring.handle(), a.base(), a.size(), a.elem_stride_bytes() * a.stride(), &k, stream));
+  return k;
+}
+
+/// Smallest power-of-two transform length >= max(n, 2) within the root order.
+inline u64 choose_length(const Ring& ring, u64 n) {
+  if (n < 1) throw InvalidParams("choose_length requires n >= 1");
+  if (n > ring.root_order())
+    throw TooLarge("product length " + std::to_string(n) + " exceeds the available root order " +
+                   std::to_string(ring.root_order()));
+  u64 L = 2;
+  while (L < n) L <<= 1;
+  return L;
+}
+
+/// g * h into `out` (>= zg + zh - 1 elements; supports by poly_support);
+/// returns the product length n (0 for a zero input: nothing written).
+inline u64 poly_mul(const Ring& ring, const DeviceView& g, const DeviceView& h, DeviceView out,
+                    SplitPolicy policy = SplitPolicy::balanced, MulStats* stats = nullptr, void* stream = nullptr,
+                    bool synchronize = true) {
+  if (stats) *stats = MulStats{};
+  if (g.stride() != 1 || h.stride() != 1 || out.stride() != 1 ||
+      g.elem_stride_bytes() != out.elem_stride_bytes() || h.elem_stride_bytes() != out.elem_stride_bytes())
+    throw InvalidParams("poly_mul takes contiguous views of one element stride");
+  const u64 zg = poly_support(ring, g, stream), zh = poly_support(ring, h, stream);
+  if (zg == 0 || zh == 0) return 0;
+  const u64 n = zg + zh - 1;
+  choose_length(ring, n);
+  if (out.size() < n) throw InvalidParams("output view shorter than the product");
+  cftft_mul_stats cs{};
+  check(cftft_gpu_poly_mul(ring.handle(), g.base(), zg, h.base(), zh, out.base(), out.elem_stride_bytes(),
+                           static_cast<int>(policy), &cs, stream));
+  if (synchronize) check(cftft_stream_synchronize(stream));
+  if (stats) {
+    stats->pointwise_mults = cs.pointwise_mults;
+    stats->transform_length = cs.transform_length;
+    stats->butterflies.base_case_count = cs.base_case_count;
+  }
+  return n;
 }
 
 /// Bit reversal of the low ell bits (transform.hpp:73-80).

@@ -23,6 +23,7 @@
 #include "negacyclic_leaf.cuh"
 #include "prime_leaf.cuh"
 #include "pointwise.cuh"
+#include "polymul.cuh"
 #include "wave_coset.cuh"
 #include "wave_wide.cuh"
 #include "wave_tma.cuh"
@@ -1371,8 +1372,8 @@ int ensure_ntt_tables(cftft_ring* R, cudaStream_t st) {
 }
 }  // namespace
 
-int cftft_gpu_pointwise(const cftft_ring* cring, void* dev_a, const void* dev_b, uint64_t count,
-                        uint64_t elem_stride_bytes, void* stream) {
+int cftft_gpu_pointwise_scaled(const cftft_ring* cring, void* dev_a, const void* dev_b, uint64_t count,
+                               uint64_t elem_stride_bytes, uint64_t scale, void* stream) {
   if (!cring) return fail(CFTFT_INVALID_PARAMS, "null ring");
   if (int rc = check_stride(cring, elem_stride_bytes)) return rc;
   if (count == 0) return CFTFT_OK;
@@ -1381,11 +1382,20 @@ int cftft_gpu_pointwise(const cftft_ring* cring, void* dev_a, const void* dev_b,
   auto st = static_cast<cudaStream_t>(stream);
   if (R->kind == CFTFT_RING_NEGACYCLIC) {
     const size_t smem = 24 * R->K;
-    CUDA_TRY(cudaFuncSetAttribute(pointwise::nega_pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    if (smem > 48 * 1024)
+      if (int rc = set_smem_bytes(pointwise::nega_pointwise_kernel, smem)) return rc;
     pointwise::nega_pointwise_kernel<<<(unsigned)count, 256, smem, st>>>(
         static_cast<std::uint8_t*>(dev_a), static_cast<const std::uint8_t*>(dev_b), elem_stride_bytes, (u32)R->K,
-        R->m, 1);
+        R->m, scale % R->m);
+    g_last_launches = 1;
+    CUDA_TRY(cudaGetLastError());
+    return CFTFT_OK;
+  }
+  if (R->kind == CFTFT_RING_PRIME) {
+    const unsigned grid = (unsigned)std::min<u64>((count + 255) / 256, 148ull * 16);
+    polymul::prime_pointwise_kernel<<<grid, 256, 0, st>>>(static_cast<std::uint8_t*>(dev_a),
+                                                           static_cast<const std::uint8_t*>(dev_b),
+                                                           elem_stride_bytes, count, R->m, scale % R->m);
     g_last_launches = 1;
     CUDA_TRY(cudaGetLastError());
     return CFTFT_OK;
@@ -1401,11 +1411,140 @@ int cftft_gpu_pointwise(const cftft_ring* cring, void* dev_a, const void* dev_b,
   A.logn = (u32)__builtin_ctz(A.D16);
   A.D32 = R->D;
   A.tw = R->ntt_tw;
+  A.rot = (u32)(scale & (R->M - 1));
   const size_t smem = (size_t)2 * A.D16 * 8;
-  CUDA_TRY(cudaFuncSetAttribute(pointwise::fermat_pointwise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem));
+  if (smem > 48 * 1024)
+    if (int rc = set_smem_bytes(pointwise::fermat_pointwise_kernel, smem)) return rc;
   pointwise::fermat_pointwise_kernel<<<(unsigned)count, 512, smem, st>>>(A);
   g_last_launches = 1;
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int cftft_gpu_pointwise(const cftft_ring* ring, void* dev_a, const void* dev_b, uint64_t count,
+                        uint64_t elem_stride_bytes, void* stream) {
+  // the identity factor: 2^0 in Z/(2^N+1), 1 in the other rings
+  return cftft_gpu_pointwise_scaled(ring, dev_a, dev_b, count, elem_stride_bytes,
+                                    ring && ring->kind == CFTFT_RING_FERMAT ? 0 : 1, stream);
+}
+
+int cftft_gpu_poly_support(const cftft_ring* ring, const void* dev_a, uint64_t len, uint64_t elem_stride_bytes,
+                           uint64_t* support, void* stream) {
+  if (!ring || !support) return fail(CFTFT_INVALID_PARAMS, "null argument");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  *support = 0;
+  if (len == 0) return CFTFT_OK;
+  auto st = static_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof *d, st));
+  CUDA_TRY(cudaMemsetAsync(d, 0, sizeof *d, st));
+  const unsigned grid = (unsigned)std::min<u64>((len + 7) / 8, 148ull * 8);
+  polymul::support_kernel<<<grid, 256, 0, st>>>(static_cast<const std::uint8_t*>(dev_a), elem_stride_bytes, len,
+                                                 (u32)(ring->elem_bytes / 8), d);
+  unsigned long long h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaFreeAsync(d, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *support = h;
+  return CFTFT_OK;
+}
+
+int cftft_gpu_poly_mul(const cftft_ring* cring, const void* dev_g, uint64_t zg, const void* dev_h, uint64_t zh,
+                       void* dev_out, uint64_t elem_stride_bytes, int policy, cftft_mul_stats* stats,
+                       void* stream) {
+  if (!cring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (int rc = check_stride(cring, elem_stride_bytes)) return rc;
+  if (policy != CFTFT_BALANCED && policy != CFTFT_RADIX2) return fail(CFTFT_INVALID_PARAMS, "unknown split policy");
+  if (stats) *stats = cftft_mul_stats{0, 0, 0};
+  if (zg == 0 || zh == 0) return CFTFT_OK;  // the zero polynomial (polymul.hpp:55)
+  auto* R = const_cast<cftft_ring*>(cring);
+  auto st = static_cast<cudaStream_t>(stream);
+  const u64 n = zg + zh - 1;
+  // choose_length (polymul.hpp:33-37)
+  if (n > R->M)
+    return fail(CFTFT_TOO_LARGE, "product length " + std::to_string(n) + " exceeds the available root order " +
+                                     std::to_string(R->M));
+  u64 L = 2;
+  while (L < n) L <<= 1;
+  const size_t eb = R->elem_bytes, sz = (size_t)L * elem_stride_bytes;
+  std::uint8_t *g = nullptr, *h = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&g, 2 * sz, st));
+  h = g + sz;
+  int rc = CFTFT_OK;
+  uint64_t c1 = 0, c2 = 0, c3 = 0;
+  do {
+    if (cudaMemcpy2DAsync(g, elem_stride_bytes, dev_g, elem_stride_bytes, eb, zg, cudaMemcpyDeviceToDevice, st) ||
+        cudaMemcpy2DAsync(h, elem_stride_bytes, dev_h, elem_stride_bytes, eb, zh, cudaMemcpyDeviceToDevice, st)) {
+      rc = fail(CFTFT_CUDA_ERROR, "poly_mul: staging copies");
+      break;
+    }
+    const cftft_params pg{L, 0, zg, n, 0}, ph{L, 0, zh, n, 0}, pi{L, 0, n, n, 0};
+    if ((rc = transform(R, false, &pg, g, elem_stride_bytes, policy, &c1, st))) break;
+    if ((rc = transform(R, false, &ph, h, elem_stride_bytes, policy, &c2, st))) break;
+    // exactly n pointwise products (polymul.hpp:73-77) with the final L^-1
+    // (polymul.hpp:82-87) folded in: 2^(2N - ell) in Z/(2^N+1), L^-1 mod m / p
+    unsigned ell = 0;
+    while ((u64{1} << ell) < L) ++ell;
+    u64 scale = 0;
+    if (R->kind == CFTFT_RING_FERMAT) {
+      scale = R->M - ell;
+    } else {
+      const u64 mod = R->m;
+      auto mulm = [mod](u64 a, u64 b) { return (u64)((unsigned __int128)a * b % mod); };
+      // L^-1 = (2^-1)^ell, 2^-1 = (mod + 1) / 2 (mod odd)
+      u64 inv2 = (mod + 1) / 2, r = 1 % mod;
+      for (unsigned k = 0; k < ell; ++k) r = mulm(r, inv2);
+      scale = r;
+    }
+    if ((rc = cftft_gpu_pointwise_scaled(R, g, h, n, elem_stride_bytes, scale, st))) break;
+    if ((rc = transform(R, true, &pi, g, elem_stride_bytes, policy, &c3, st))) break;
+    if (cudaMemcpy2DAsync(dev_out, elem_stride_bytes, g, elem_stride_bytes, eb, n, cudaMemcpyDeviceToDevice, st)) {
+      rc = fail(CFTFT_CUDA_ERROR, "poly_mul: output copy");
+      break;
+    }
+  } while (false);
+  cudaFreeAsync(g, st);
+  if (rc) return rc;
+  if (stats) *stats = cftft_mul_stats{n, L, c1 + c2 + c3};
+  return CFTFT_OK;
+}
+
+int cftft_gpu_pack_limbs(const cftft_ring* ring, void* dev_dst, uint64_t elem_stride_bytes, const void* dev_src,
+                         uint64_t src_words, uint64_t count, void* stream) {
+  if (!ring) return fail(CFTFT_INVALID_PARAMS, "null ring");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  const u64 ew = ring->elem_bytes / 8;
+  if (src_words > (ring->kind == CFTFT_RING_FERMAT ? ring->N / 64 : ew))
+    return fail(CFTFT_INVALID_PARAMS, "source coefficients wider than the ring's elements");
+  if (count == 0) return CFTFT_OK;
+  if (count > 0x7FFFFFFFull) return fail(CFTFT_UNSUPPORTED, "too many elements for one launch");
+  polymul::pack_limbs_kernel<<<(unsigned)count, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<std::uint8_t*>(dev_dst), elem_stride_bytes, static_cast<const std::uint8_t*>(dev_src), src_words,
+      (u32)ew);
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int cftft_gpu_nussbaumer_split(const cftft_ring* ring, void* dev_dst, uint64_t elem_stride_bytes,
+                               const uint64_t* dev_f, uint64_t s, void* stream) {
+  if (!ring || ring->kind != CFTFT_RING_NEGACYCLIC) return fail(CFTFT_INVALID_PARAMS, "a negacyclic ring is needed");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  if (s == 0 || s > 0x7FFFFFFFull) return fail(CFTFT_INVALID_PARAMS, "bad split length");
+  const dim3 grid((unsigned)((s + 31) / 32), (unsigned)((ring->K + 31) / 32)), block(32, 8);
+  polymul::nuss_split_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<std::uint8_t*>(dev_dst), elem_stride_bytes, dev_f, (u32)ring->K, (u32)s);
+  CUDA_TRY(cudaGetLastError());
+  return CFTFT_OK;
+}
+
+int cftft_gpu_nussbaumer_join(const cftft_ring* ring, uint64_t* dev_h, const void* dev_c, uint64_t elem_stride_bytes,
+                              uint64_t s, void* stream) {
+  if (!ring || ring->kind != CFTFT_RING_NEGACYCLIC) return fail(CFTFT_INVALID_PARAMS, "a negacyclic ring is needed");
+  if (int rc = check_stride(ring, elem_stride_bytes)) return rc;
+  if (s == 0 || s > 0x7FFFFFFFull) return fail(CFTFT_INVALID_PARAMS, "bad split length");
+  const dim3 grid((unsigned)((s + 31) / 32), (unsigned)((ring->K + 31) / 32)), block(32, 8);
+  polymul::nuss_join_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+      dev_h, static_cast<const std::uint8_t*>(dev_c), elem_stride_bytes, (u32)ring->K, (u32)s, ring->m);
   CUDA_TRY(cudaGetLastError());
   return CFTFT_OK;
 }

@@ -125,6 +125,7 @@ struct FermatMulArgs {
   u32 D32;        // u32 words per element = N/32
   const u64* tw;  // psi^i (i < n), then omega_n^j (j < n/2), then the inverses
   u64 n_inv;      // 1/n mod p
+  u32 rot;        // extra factor 2^rot of every product (rot < 2N): poly_mul's L^-1 = 2^(2N - ell)
 };
 
 // In-place cyclic NTT of length n in shared memory: DIF (natural -> bit
@@ -221,15 +222,14 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
   long long pend = 0;
   if (topa != 0 || topb != 0) {
     // canonical inputs: top = 1 means 2^N == -1 (all limbs zero), so the
-    // product is -b, -a or 1; -x = ~x + 2 (mod 2^N + 1).
+    // product is -b, -a or 1: as negacyclic digit coefficients -x_i, or 1
     const bool one = topa != 0 && topb != 0;
-    const u32* other = reinterpret_cast<const u32*>(topa ? eb : ea);
-    if (t < chunks) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) wv[k] = one ? 0u : ~other[16 * t + k];
-      pend = (t == 0) ? (one ? 1 : 2) : 0;
+    const std::uint16_t* other = topa ? db : da;
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+      const u64 d = one ? (i == 0 ? 1u : 0u) : (u64)other[i];
+      xa[i] = one ? d : (d ? GP - d : 0);
     }
-    __syncthreads();  // all reads of a done before anything is written
+    __syncthreads();
   } else {
     for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
       xa[i] = g_mul((u64)da[i], psi[i]);
@@ -243,15 +243,28 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
     ntt_dit(xa, wi, n, A.logn);
     for (u32 i = threadIdx.x; i < n; i += blockDim.x) xa[i] = g_mul(xa[i], psii[i]);
     __syncthreads();
-    // fold the signed digit coefficients c_i (|c_i| < 2^45) into 512-bit chunks
+  }
+  {
+    // fold the signed digit coefficients c_i (|c_i| < 2^45) into 512-bit
+    // chunks; the extra factor 2^rot = x^q 2^r (x = 2^16, x^n = -1): digit i
+    // of the result takes coefficient i - q (negated past the wrap) times 2^r
+    const u32 q = A.rot >> 4, r = A.rot & 15u;
     if (t < chunks) {
       long long acc[17];
 #pragma unroll
       for (int k = 0; k < 17; ++k) acc[k] = 0;
 #pragma unroll
       for (int d = 0; d < 32; ++d) {
-        const u64 v = xa[32 * t + d];
-        const long long c = v > (GP >> 1) ? -(long long)(GP - v) : (long long)v;
+        int src = (int)(32 * t + d) - (int)(q % (2 * n));
+        bool neg = false;
+        while (src < 0) {
+          src += (int)n;
+          neg = !neg;
+        }
+        const u64 v = xa[src];
+        long long c = v > (GP >> 1) ? -(long long)(GP - v) : (long long)v;
+        if (neg) c = -c;
+        c *= (1ll << r);  // |c| < 2^60
         // c * 2^(16 d) -> word d/2, shifted by 16 (d odd)
         if (d & 1) {
           acc[d / 2] += (long long)((unsigned long long)(c & 0xFFFF) << 16);

@@ -8,9 +8,11 @@ multiplication pipelines built on it:
             N = k L / 2 the smallest size holding the output coefficients
             (PAPER.md:807)
 
-Everything runs on the GPU: the transforms (cf_tft / cf_itft), the pointwise
-ring products (cftft_gpu_pointwise), the final L^-1 scale, packing and
-recombination (torch tensor ops on device memory).
+Everything runs on the GPU through the C ABI (include/cftft_b200.h):
+cftft_gpu_poly_mul (two TFTs, the n pointwise products with L^-1 folded in,
+the ITFT), cftft_gpu_pack_limbs (SS packing), cftft_gpu_nussbaumer_split /
+_join (the x^(j+sk) <-> z^j y^k reshapes and the y C recombination).  torch
+only allocates device memory.
 """
 from __future__ import annotations
 
@@ -19,8 +21,8 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import (ButterflyStats, DeviceView, FermatRingCtx, InvalidParams, NegacyclicRingCtx, SplitPolicy,
-               TransformParams, _check, _stream_ptr, cf_itft, cf_tft, lib, scale)
+from . import (ButterflyStats, FermatRingCtx, InvalidParams, NegacyclicRingCtx, SplitPolicy, _check, _stream_ptr,
+               lib)
 
 
 class TooLarge(ValueError):
@@ -33,6 +35,39 @@ class MulStats:
     pointwise_mults: int = 0
     transform_length: int = 0
     butterflies: ButterflyStats = field(default_factory=ButterflyStats)
+
+
+class _CMulStats(C.Structure):
+    _fields_ = [("pointwise_mults", C.c_uint64), ("transform_length", C.c_uint64),
+                ("base_case_count", C.c_uint64)]
+
+
+def _bind():
+    L = lib()
+    if not getattr(L, "_polymul_bound", False):
+        vp, u64 = C.c_void_p, C.c_uint64
+        L.cftft_gpu_poly_mul.argtypes = [vp, vp, u64, vp, u64, vp, u64, C.c_int, C.POINTER(_CMulStats), vp]
+        L.cftft_gpu_poly_support.argtypes = [vp, vp, u64, u64, C.POINTER(u64), vp]
+        L.cftft_gpu_pointwise_scaled.argtypes = [vp, vp, vp, u64, u64, u64, vp]
+        L.cftft_gpu_pack_limbs.argtypes = [vp, vp, u64, vp, u64, u64, vp]
+        L.cftft_gpu_nussbaumer_split.argtypes = [vp, vp, u64, vp, u64, vp]
+        L.cftft_gpu_nussbaumer_join.argtypes = [vp, vp, vp, u64, u64, vp]
+        L._polymul_bound = True
+    return L
+
+
+def _call(rc: int) -> None:
+    if rc == 7:
+        raise TooLarge(lib().cftft_last_error().decode())
+    _check(rc)
+
+
+def poly_support(ctx, A: torch.Tensor, stream=None) -> int:
+    """1 + deg (trailing zero elements ignored), polymul.hpp:26-30."""
+    out = C.c_uint64()
+    _call(_bind().cftft_gpu_poly_support(ctx._h, C.c_void_p(A.data_ptr()), A.shape[0], A.shape[1] * 8,
+                                         C.byref(out), C.c_void_p(_stream_ptr(stream))))
+    return out.value
 
 
 def choose_length(ctx, n: int) -> int:
@@ -59,37 +94,31 @@ def mul_scalar(ctx, a: torch.Tensor, count: int, c: int, stream=None) -> None:
                                       C.c_void_p(_stream_ptr(stream))))
 
 
-def poly_mul(ctx, G: torch.Tensor, H: torch.Tensor, zg: int, zh: int, policy=SplitPolicy.balanced,
-             stats: MulStats | None = None) -> torch.Tensor:
-    """Product of two polynomials over the ring (polymul.hpp:48-95): G, H are
-    CUDA tensors of elements (rows) with supports zg, zh.  Returns the n =
-    zg + zh - 1 coefficients of the product (canonical elements)."""
+def poly_mul(ctx, G: torch.Tensor, H: torch.Tensor, zg: int | None = None, zh: int | None = None,
+             policy=SplitPolicy.balanced, stats: MulStats | None = None, stream=None) -> torch.Tensor:
+    """Product of two polynomials over the ring (polymul.hpp:48-95) through
+    cftft_gpu_poly_mul: G, H are CUDA tensors of elements (rows); supports
+    zg, zh default to poly_support.  Returns the n = zg + zh - 1
+    coefficients of the product (canonical elements)."""
     if stats is not None:
         stats.__init__()
+    if zg is None:
+        zg = poly_support(ctx, G, stream)
+    if zh is None:
+        zh = poly_support(ctx, H, stream)
     if zg == 0 or zh == 0:
         return G[:0]
     n = zg + zh - 1
-    L = choose_length(ctx, n)
-    W = ctx.element_words
-    g = torch.zeros((L, W), dtype=torch.int64, device=G.device)
-    h = torch.zeros((L, W), dtype=torch.int64, device=G.device)
-    g[:zg] = G[:zg]
-    h[:zh] = H[:zh]
-    bs = ButterflyStats()
-    cf_tft(ctx, TransformParams(L, 0, zg, n), DeviceView(g), policy, bs)
-    cf_tft(ctx, TransformParams(L, 0, zh, n), DeviceView(h), policy, bs)
-    pointwise(ctx, g, h, n)
-    cf_itft(ctx, TransformParams(L, 0, n, n, 0), DeviceView(g), policy, bs)
-    ell = L.bit_length() - 1
-    if isinstance(ctx, FermatRingCtx):
-        scale(ctx, DeviceView(g), n, ctx.root_order() - ell)  # 1/L = omega^(M - ell)
-    else:
-        mul_scalar(ctx, g, n, pow(L, -1, ctx.m))
+    out = torch.empty((n, ctx.element_words), dtype=torch.int64, device=G.device)
+    cs = _CMulStats()
+    _call(_bind().cftft_gpu_poly_mul(ctx._h, C.c_void_p(G.data_ptr()), zg, C.c_void_p(H.data_ptr()), zh,
+                                     C.c_void_p(out.data_ptr()), ctx.element_words * 8, int(policy), C.byref(cs),
+                                     C.c_void_p(_stream_ptr(stream))))
     if stats is not None:
-        stats.pointwise_mults = n
-        stats.transform_length = L
-        stats.butterflies = bs
-    return g[:n]
+        stats.pointwise_mults = cs.pointwise_mults
+        stats.transform_length = cs.transform_length
+        stats.butterflies = ButterflyStats(cs.base_case_count)
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -106,17 +135,17 @@ def nussbaumer_negacyclic_mul(f: torch.Tensor, g: torch.Tensor, m: int, K: int, 
     ctx = _RINGS.get(("negacyclic", K, m))
     if ctx is None:
         ctx = _RINGS[("negacyclic", K, m)] = NegacyclicRingCtx(K, m)
-    A = f.view(K, s).t().contiguous()  # A[j][k] = f[j + s k]
-    B = g.view(K, s).t().contiguous()
+    L = _bind()
+    eb = ctx.element_words * 8
+    f, g = f.contiguous(), g.contiguous()
+    A = torch.empty((s, K), dtype=torch.int64, device=f.device)
+    B = torch.empty((s, K), dtype=torch.int64, device=f.device)
+    _call(L.cftft_gpu_nussbaumer_split(ctx._h, C.c_void_p(A.data_ptr()), eb, C.c_void_p(f.data_ptr()), s, None))
+    _call(L.cftft_gpu_nussbaumer_split(ctx._h, C.c_void_p(B.data_ptr()), eb, C.c_void_p(g.data_ptr()), s, None))
     Cz = poly_mul(ctx, A, B, s, s, policy, stats)  # 2s - 1 elements of R
-    top = torch.zeros((s, K), dtype=torch.int64, device=f.device)
-    top[: s - 1] = Cz[s:]
-    # y * C: negacyclic shift by one word
-    yC = torch.roll(top, 1, dims=1)
-    yC[:, 0] = torch.where(yC[:, 0] == 0, yC[:, 0], m - yC[:, 0])
-    hb = Cz[:s] + yC
-    hb = torch.where(hb >= m, hb - m, hb)
-    return hb.t().contiguous().view(-1)
+    h = torch.empty(K * s, dtype=torch.int64, device=f.device)
+    _call(L.cftft_gpu_nussbaumer_join(ctx._h, C.c_void_p(h.data_ptr()), C.c_void_p(Cz.data_ptr()), eb, s, None))
+    return h
 
 
 # ---------------------------------------------------------------------------
@@ -161,9 +190,11 @@ def ss_mul(F: torch.Tensor, G: torch.Tensor, coeff_bits: int, policy=SplitPolicy
     ctx = _fermat_ring(N)
     W = ctx.element_words
     limbs = F.shape[1]
-    A = torch.zeros((zf, W), dtype=torch.int64, device=F.device)
-    B = torch.zeros((zg, W), dtype=torch.int64, device=F.device)
-    A[:, :limbs] = F
-    B[:, :limbs] = G
+    L = _bind()
+    A = torch.empty((zf, W), dtype=torch.int64, device=F.device)
+    B = torch.empty((zg, W), dtype=torch.int64, device=F.device)
+    Fc, Gc = F.contiguous(), G.contiguous()
+    _call(L.cftft_gpu_pack_limbs(ctx._h, C.c_void_p(A.data_ptr()), W * 8, C.c_void_p(Fc.data_ptr()), limbs, zf, None))
+    _call(L.cftft_gpu_pack_limbs(ctx._h, C.c_void_p(B.data_ptr()), W * 8, C.c_void_p(Gc.data_ptr()), limbs, zg, None))
     H = poly_mul(ctx, A, B, zf, zg, policy, stats)
     return H[:, : N // 64], N

@@ -51,6 +51,106 @@ static void validation() {
   EXPECT(throws<std::invalid_argument>([&] { cf::cf_tft(ring, {6, 0, 1, 1, 0}, v8); }));
   EXPECT(throws<cf::Unsupported>([] { cf::FermatRing bad(100); }));
   EXPECT(cf::bit_reverse(1, 3) == 4 && cf::bit_reverse(6, 3) == 3);
+  // choose_length / TooLarge (polymul.hpp:33-37, 13-18)
+  cf::PrimeRing small(97, 4);  // root order 16
+  EXPECT(cf::choose_length(small, 1) == 2 && cf::choose_length(small, 9) == 16);
+  EXPECT(throws<cf::TooLarge>([&] { cf::choose_length(small, 17); }));
+  EXPECT(throws<std::length_error>([&] { cf::choose_length(small, 17); }));
+  EXPECT(throws<cf::InvalidParams>([&] { cf::choose_length(small, 0); }));
+  EXPECT(throws<cf::InvalidParams>([] { cf::PrimeRing composite(97 * 193, 2); }));
+}
+
+// poly_mul on the GPU against a schoolbook product (polymul_test.cpp:11-19,
+// 81-162): the reference's own ring, then Z/(2^1024+1) with small
+// coefficients (exact integer products); exactly n pointwise products,
+// the zero polynomial, TooLarge.
+static void poly_mul_gpu() {
+  const std::uint64_t p = 0xFFFFFFFF00000001ull;
+  cf::PrimeRing ring(p, 32);
+  std::mt19937_64 rng(7);
+  const std::uint64_t zg = 300, zh = 257, len = 320;
+  std::vector<std::uint64_t> g(len, 0), h(len, 0);
+  for (std::uint64_t i = 0; i < zg; ++i) g[i] = rng() % p;
+  for (std::uint64_t i = 0; i < zh; ++i) h[i] = rng() % p;
+  g[zg - 1] = 5;  // nonzero leading coefficients: supports zg, zh
+  h[zh - 1] = 9;
+  const std::uint64_t n = zg + zh - 1;
+  std::vector<std::uint64_t> want(n, 0);
+  for (std::uint64_t i = 0; i < zg; ++i)
+    for (std::uint64_t j = 0; j < zh; ++j)
+      want[i + j] = (std::uint64_t)(((unsigned __int128)g[i] * h[j] + want[i + j]) % p);
+  std::uint64_t *dg = nullptr, *dh = nullptr, *dout = nullptr;
+  EXPECT(cudaMalloc(&dg, len * 8) == cudaSuccess && cudaMalloc(&dh, len * 8) == cudaSuccess &&
+         cudaMalloc(&dout, n * 8) == cudaSuccess);
+  EXPECT(cudaMemcpy(dg, g.data(), len * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+  EXPECT(cudaMemcpy(dh, h.data(), len * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+  cf::MulStats st;
+  const std::uint64_t got_n = cf::poly_mul(ring, cf::DeviceView(dg, 8, len), cf::DeviceView(dh, 8, len),
+                                           cf::DeviceView(dout, 8, n), cf::SplitPolicy::balanced, &st);
+  EXPECT(got_n == n);
+  EXPECT(st.pointwise_mults == n && st.transform_length == 1024);
+  EXPECT(st.butterflies.base_case_count == cftft_tft_base_cases(1024, zg, n, 0) +
+                                               cftft_tft_base_cases(1024, zh, n, 0) +
+                                               cftft_itft_base_cases(1024, n, n, 0, 0));
+  std::vector<std::uint64_t> out(n);
+  EXPECT(cudaMemcpy(out.data(), dout, n * 8, cudaMemcpyDeviceToHost) == cudaSuccess);
+  EXPECT(out == want);
+  // the zero polynomial: nothing written, stats zero
+  EXPECT(cudaMemset(dh, 0, len * 8) == cudaSuccess);
+  EXPECT(cf::poly_mul(ring, cf::DeviceView(dg, 8, len), cf::DeviceView(dh, 8, len), cf::DeviceView(dout, 8, n),
+                      cf::SplitPolicy::radix2, &st) == 0);
+  EXPECT(st.pointwise_mults == 0 && st.transform_length == 0);
+  // TooLarge: root order 16
+  cf::PrimeRing small(97, 4);
+  EXPECT(cudaMemcpy(dh, h.data(), len * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+  EXPECT(throws<cf::TooLarge>([&] {
+    cf::poly_mul(small, cf::DeviceView(dg, 8, 10), cf::DeviceView(dh, 8, 10), cf::DeviceView(dout, 8, 19));
+  }));
+  cudaFree(dg);
+  cudaFree(dh);
+  cudaFree(dout);
+
+  // Z/(2^1024+1): coefficients < 2^62, products exact below 2^1024
+  const std::uint64_t N = 1024;
+  cf::FermatRing fr(N);
+  const std::uint64_t eb = fr.element_bytes(), words = eb / 8, fz = 200;
+  std::vector<std::uint64_t> fg(fz * words, 0), fh(fz * words, 0);
+  std::vector<std::uint64_t> sg(fz), sh(fz);
+  for (std::uint64_t i = 0; i < fz; ++i) {
+    sg[i] = rng() >> 2;
+    sh[i] = rng() >> 2;
+    fg[i * words] = sg[i];
+    fh[i * words] = sh[i];
+  }
+  const std::uint64_t fn = 2 * fz - 1;
+  std::vector<unsigned __int128> acc(fn, 0);
+  std::vector<std::uint64_t> hi(fn, 0);
+  for (std::uint64_t i = 0; i < fz; ++i)
+    for (std::uint64_t j = 0; j < fz; ++j) {
+      const unsigned __int128 t = (unsigned __int128)sg[i] * sh[j];
+      const unsigned __int128 old = acc[i + j];
+      acc[i + j] += t;
+      if (acc[i + j] < old) ++hi[i + j];
+    }
+  void *fdg = nullptr, *fdh = nullptr, *fdo = nullptr;
+  EXPECT(cudaMalloc(&fdg, fz * eb) == cudaSuccess && cudaMalloc(&fdh, fz * eb) == cudaSuccess &&
+         cudaMalloc(&fdo, fn * eb) == cudaSuccess);
+  EXPECT(cudaMemcpy(fdg, fg.data(), fz * eb, cudaMemcpyHostToDevice) == cudaSuccess);
+  EXPECT(cudaMemcpy(fdh, fh.data(), fz * eb, cudaMemcpyHostToDevice) == cudaSuccess);
+  EXPECT(cf::poly_mul(fr, cf::DeviceView(fdg, eb, fz), cf::DeviceView(fdh, eb, fz), cf::DeviceView(fdo, eb, fn)) ==
+         fn);
+  std::vector<std::uint64_t> fo(fn * words);
+  EXPECT(cudaMemcpy(fo.data(), fdo, fn * eb, cudaMemcpyDeviceToHost) == cudaSuccess);
+  bool same = true;
+  for (std::uint64_t i = 0; i < fn; ++i) {
+    same &= fo[i * words] == (std::uint64_t)acc[i] && fo[i * words + 1] == (std::uint64_t)(acc[i] >> 64) &&
+            fo[i * words + 2] == hi[i];
+    for (std::uint64_t k = 3; k < words; ++k) same &= fo[i * words + k] == 0;
+  }
+  EXPECT(same);
+  cudaFree(fdg);
+  cudaFree(fdh);
+  cudaFree(fdo);
 }
 
 static void round_trip_gpu() {
@@ -100,7 +200,10 @@ static void round_trip_gpu() {
 
 int main(int argc, char** argv) {
   validation();
-  if (argc > 1 && std::string(argv[1]) == "--gpu") round_trip_gpu();
+  if (argc > 1 && std::string(argv[1]) == "--gpu") {
+    round_trip_gpu();
+    poly_mul_gpu();
+  }
   std::printf("%s (%d failures)\n", failures ? "FAIL" : "OK", failures);
   return failures ? 1 : 0;
 }
