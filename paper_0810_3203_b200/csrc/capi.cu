@@ -124,8 +124,8 @@ struct cftft_ring {
   unsigned max_leaf_fit = 1;
   std::mutex mu;
   std::map<PlanKey, std::unique_ptr<DevicePlan>> cache;
-  // Goldilocks twiddle tables of the Fermat pointwise multiplier
-  u64* ntt_tw = nullptr;
+  // NTT twiddle tables of the Fermat pointwise multiplier (pointwise.cuh)
+  u32* ntt_tw = nullptr;
   // prime rings: p (in m), -p^-1 mod 2^64, omega, two-level Montgomery tables
   u64 pinv = 0, omega = 0;
   u32 lo_bits = 0;
@@ -1315,58 +1315,51 @@ int cftft_itft_host(const cftft_ring* ring, const cftft_params* params, void* ho
 
 namespace {
 typedef unsigned __int128 hu128;
-constexpr u64 kGold = 0xFFFFFFFF00000001ull;
-u64 gmul(u64 a, u64 b) { return (u64)((hu128)a * b % kGold); }
-u64 gpow(u64 a, u64 e) {
-  u64 r = 1;
-  while (e) {
-    if (e & 1) r = gmul(r, a);
-    a = gmul(a, a);
-    e >>= 1;
-  }
-  return r;
-}
-// Twiddle table layout (see pointwise.cuh): [psi^i, i<n] [omega^j, j<n/2]
-// [unused n/2] [psi^-i / n, i<n] [omega^-j, j<n/2]
 int ensure_ntt_tables(cftft_ring* R, cudaStream_t st) {
   std::lock_guard<std::mutex> g(R->mu);
   if (R->ntt_tw) return CFTFT_OK;
   const u64 n = R->N / 16;
-  // the reference's root search over Goldilocks (field.hpp:170-177): 7^((p-1)/2^32)
-  const u64 w32 = gpow(7, (kGold - 1) >> 32);
-  const u64 psi = gpow(w32, (u64{1} << 32) / (2 * n));  // order 2n
-  const u64 om = gmul(psi, psi);                         // order n
-  const u64 psi_inv = gpow(psi, kGold - 2), om_inv = gpow(om, kGold - 2), n_inv = gpow(n % kGold, kGold - 2);
-  // [0, n) psi^i, [n, 3n/2) omega^j, [2n, 3n) psi^-i / n, [3n, 7n/2) omega^-j, then per-stage
-  // twiddles for the NTT levels (level ls: omega^(j 2^ls), j < n >> (ls+1), at n - (n >> ls)):
-  // forward at 7n/2, inverse at 9n/2 -- contiguous per level, so a warp's reads coalesce
-  std::vector<u64> h((size_t)(11 * n / 2), 0);
-  u64 x = 1, y = n_inv;
-  for (u64 i = 0; i < n; ++i) {
-    h[i] = x;
-    h[2 * n + i] = y;
-    x = gmul(x, psi);
-    y = gmul(y, psi_inv);
-  }
-  x = 1, y = 1;
-  for (u64 j = 0; j < n / 2; ++j) {
-    h[n + j] = x;
-    h[3 * n + j] = y;
-    x = gmul(x, om);
-    y = gmul(y, om_inv);
-  }
-  for (u64 ls = 0, off = 0; (n >> (ls + 1)) >= 1; off += n >> (ls + 1), ++ls) {
-    const u64 sf = gpow(om, u64{1} << ls), si = gpow(om_inv, u64{1} << ls);
-    u64 a = 1, b = 1;
-    for (u64 j = 0; j < (n >> (ls + 1)); ++j) {
-      h[7 * n / 2 + off + j] = a;
-      h[9 * n / 2 + off + j] = b;
-      a = gmul(a, sf);
-      b = gmul(b, si);
+  // 4 n entries of {w mod Q1, Shoup factor floor(w 2^32 / Q1), w mod Q2,
+  // Shoup} (pointwise.cuh; primitive root 3 for both primes): psi^i,
+  // psi^-i / n, the forward level twiddles (level ls: omega^(j 2^ls),
+  // j < n >> (ls+1), at n - (n >> ls)), the inverse ones
+  std::vector<u32> h((size_t)16 * n, 0);
+  const u32 primes[2] = {pointwise::Q1, pointwise::Q2};
+  for (int j = 0; j < 2; ++j) {
+    const u64 p = primes[j];
+    auto mul = [p](u64 a, u64 b) { return a * b % p; };
+    auto pw = [&](u64 a, u64 e) {
+      u64 r = 1;
+      for (; e; e >>= 1, a = mul(a, a))
+        if (e & 1) r = mul(r, a);
+      return r;
+    };
+    auto put = [&](u64 slot, u64 w) {
+      h[4 * slot + 2 * j] = (u32)w;
+      h[4 * slot + 2 * j + 1] = (u32)((w << 32) / p);
+    };
+    const u64 psi = pw(3, (p - 1) / (2 * n)), om = mul(psi, psi);
+    const u64 psi_inv = pw(psi, p - 2), om_inv = pw(om, p - 2), n_inv = pw(n % p, p - 2);
+    u64 x = 1, y = n_inv;
+    for (u64 i = 0; i < n; ++i) {
+      put(i, x);
+      put(n + i, y);
+      x = mul(x, psi);
+      y = mul(y, psi_inv);
+    }
+    for (u64 ls = 0, off = 0; (n >> (ls + 1)) >= 1; off += n >> (ls + 1), ++ls) {
+      const u64 sf = pw(om, u64{1} << ls), si = pw(om_inv, u64{1} << ls);
+      u64 a = 1, b = 1;
+      for (u64 k = 0; k < (n >> (ls + 1)); ++k) {
+        put(2 * n + off + k, a);
+        put(3 * n + off + k, b);
+        a = mul(a, sf);
+        b = mul(b, si);
+      }
     }
   }
-  CUDA_TRY(cudaMalloc((void**)&R->ntt_tw, h.size() * 8));
-  CUDA_TRY(cudaMemcpyAsync(R->ntt_tw, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMalloc((void**)&R->ntt_tw, h.size() * 4));
+  CUDA_TRY(cudaMemcpyAsync(R->ntt_tw, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return CFTFT_OK;
 }
@@ -1410,9 +1403,9 @@ int cftft_gpu_pointwise_scaled(const cftft_ring* cring, void* dev_a, const void*
   A.D16 = (u32)(R->N / 16);
   A.logn = (u32)__builtin_ctz(A.D16);
   A.D32 = R->D;
-  A.tw = R->ntt_tw;
+  A.tw = reinterpret_cast<const uint4*>(R->ntt_tw);
   A.rot = (u32)(scale & (R->M - 1));
-  const size_t smem = (size_t)2 * A.D16 * 8;
+  const size_t smem = (size_t)4 * pointwise::padded(A.D16) * 4;
   if (smem > 48 * 1024)
     if (int rc = set_smem_bytes(pointwise::fermat_pointwise_kernel, smem)) return rc;
   pointwise::fermat_pointwise_kernel<<<(unsigned)count, 512, smem, st>>>(A);

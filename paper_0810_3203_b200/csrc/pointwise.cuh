@@ -10,12 +10,10 @@
 //
 // Fermat R = Z/(2^N+1): a * b mod 2^N+1 is a NEGACYCLIC convolution of the
 // 16-bit digit vectors (2^(16 * N/16) = 2^N == -1).  One CTA per product runs
-// it as a weighted NTT over the Goldilocks field p = 2^64 - 2^32 + 1 (the
-// reference's default ring, field.hpp:84-98): digits < 2^16, so every
-// convolution coefficient lies in (-2^(44+1), 2^(44+1)) and is recovered
-// exactly from its residue mod p.  The coefficients are then folded into
-// 512-bit chunks with signed tops and carry-resolved like the transform
-// engine, and written in the engine's lazy element format.
+// it as psi-weighted NTTs modulo two 30-bit primes (native 32-bit Shoup /
+// Barrett arithmetic) and recovers every coefficient (|c| < n 2^32) by CRT;
+// the coefficients are then folded into 512-bit chunks and carry-resolved,
+// canonical output.
 #pragma once
 #include <cstdint>
 
@@ -92,28 +90,25 @@ __global__ void nega_scale_kernel(std::uint8_t* a, u64 stride, u64 count, u32 K,
 }
 
 // ---------------------------------------------------------------------------
-// Goldilocks field (p = 2^64 - 2^32 + 1)
+// Two NTT primes below 2^30 with roots of unity of every power-of-two order
+// up to 2^23: 998244353 = 119 2^23 + 1 and 469762049 = 7 2^26 + 1 (primitive
+// root 3 for both).  Their product (~2^58.7) exceeds twice the largest
+// negacyclic convolution coefficient of 16-bit digits, n 2^32 <= 2^45
+// (n = N/16 <= 8192), so each coefficient comes back exactly by CRT.
+constexpr u32 Q1 = 998244353u, Q2 = 469762049u;
 
-constexpr u64 GP = 0xFFFFFFFF00000001ull;
-
-__device__ __forceinline__ u64 g_add(u64 a, u64 b) {
-  const u64 s = a + b;
-  // overflow past 2^64 or >= p: subtract p (== add 2^32 - 1 mod 2^64)
-  if (s < a) return s + 0xFFFFFFFFull;
-  return s >= GP ? s - GP : s;
+// Shoup product x w mod p for a fixed w (wp = floor(w 2^32 / p)): x < 2^32,
+// result in [0, 2p)
+__device__ __forceinline__ u32 shoup(u32 x, u32 w, u32 wp, u32 p) {
+  const u32 q = __umulhi(x, wp);
+  return x * w - q * p;
 }
-__device__ __forceinline__ u64 g_sub(u64 a, u64 b) { return a >= b ? a - b : a + (GP - b); }
-__device__ __forceinline__ u64 g_mul(u64 a, u64 b) {
-  const u64 lo = a * b, hi = __umul64hi(a, b);
-  // x = hi 2^64 + lo; 2^64 == 2^32 - 1, 2^96 == -1 (field.hpp:154-167 restated)
-  const u64 hh = hi >> 32, hl = hi & 0xFFFFFFFFull;
-  u64 t = lo - hh;
-  if (lo < hh) t -= 0xFFFFFFFFull;
-  const u64 s = hl * 0xFFFFFFFFull;
-  u64 r = t + s;
-  if (r < t) r += 0xFFFFFFFFull;
-  if (r >= GP) r -= GP;
-  return r;
+// x y mod p for variable x, y < 2^31 (Barrett with m64 = floor(2^64 / p)):
+// result in [0, 2p)
+__device__ __forceinline__ u32 mulmod_b(u32 x, u32 y, u32 p, u64 m64) {
+  const u64 t = (u64)x * y;
+  const u64 q = __umul64hi(t, m64);
+  return (u32)(t - q * p);
 }
 
 struct FermatMulArgs {
@@ -123,45 +118,126 @@ struct FermatMulArgs {
   u32 D16;        // digits (16-bit) per element = N/16 = NTT length n
   u32 logn;
   u32 D32;        // u32 words per element = N/32
-  const u64* tw;  // psi^i (i < n), then omega_n^j (j < n/2), then the inverses
-  u64 n_inv;      // 1/n mod p
+  const uint4* tw;  // 4 n entries {w mod Q1, its Shoup factor, w mod Q2, its Shoup}: psi^i, psi^-i / n,
+                    // the forward level twiddles (level ls: omega^(j 2^ls), j < n >> (ls+1), at
+                    // n - (n >> ls)), the inverse ones
   u32 rot;        // extra factor 2^rot of every product (rot < 2N): poly_mul's L^-1 = 2^(2N - ell)
 };
 
-// In-place cyclic NTT of length n in shared memory: DIF (natural -> bit
-// reversed) for the forward transform, DIT (bit reversed -> natural) for the
-// inverse; w = omega_n^j table (n/2 entries) in shared memory.
-// ws: per-level twiddle tables in global memory (level ls: omega^(j 2^ls),
-// j < n >> (ls+1), at n - (n >> ls)) -- contiguous in j, so a warp's reads
-// coalesce (the strided w[j << ls] of one table was a 32-way shared-memory
-// bank conflict in the middle levels).
-__device__ __forceinline__ void ntt_dif(u64* x, const u64* ws, u32 n, u32 logn) {
-  for (u32 h = n >> 1, ls = 0; h >= 1; h >>= 1, ++ls) {
-    const u32 lh = logn - 1 - ls;
-    const u64* w = ws + (n - (n >> ls));
-    for (u32 t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
-      const u32 grp = t >> lh, j = t & (h - 1);
-      const u32 i0 = grp * 2 * h + j, i1 = i0 + h;
-      const u64 u = x[i0], v = x[i1];
-      x[i0] = g_add(u, v);
-      x[i1] = g_mul(g_sub(u, v), __ldg(w + j));
-    }
-    __syncthreads();
-  }
+// Both primes' arrays of one operand advance together (independent work per
+// thread); values stay lazily in [0, 2p) (Harvey's butterflies, p < 2^30).
+template <u32 Q>
+__device__ __forceinline__ void bf_dif(u32& u, u32& v, u32 w, u32 wp) {
+  const u32 s = u + v, d = u - v + 2 * Q;
+  u = s >= 2 * Q ? s - 2 * Q : s;
+  v = shoup(d, w, wp, Q);
 }
-__device__ __forceinline__ void ntt_dit(u64* x, const u64* ws, u32 n, u32 logn) {
-  for (u32 h = 1, ls = logn - 1; h < n; h <<= 1, --ls) {
-    const u32 lh = logn - 1 - ls;
-    const u64* w = ws + (n - (n >> ls));
-    for (u32 t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
-      const u32 grp = t >> lh, j = t & (h - 1);
-      const u32 i0 = grp * 2 * h + j, i1 = i0 + h;
-      const u64 u = x[i0], v = g_mul(x[i1], __ldg(w + j));
-      x[i0] = g_add(u, v);
-      x[i1] = g_sub(u, v);
+template <u32 Q>
+__device__ __forceinline__ void bf_dit(u32& u, u32& v, u32 w, u32 wp) {
+  const u32 t = shoup(v, w, wp, Q);
+  const u32 s = u + t, d = u - t + 2 * Q;
+  u = s >= 2 * Q ? s - 2 * Q : s;
+  v = d >= 2 * Q ? d - 2 * Q : d;
+}
+// Shared arrays are padded one word per eight (index i at i + i/8): the
+// radix-8 passes' strided sets then hit distinct banks for every span.
+__device__ __forceinline__ u32 pd(u32 i) { return i + (i >> 3); }
+__host__ __device__ constexpr u32 padded(u32 n) { return n + (n >> 3); }
+
+// one radix-2 level (the passes' tail when log n is not a multiple of 3)
+template <bool DIF>
+__device__ __forceinline__ void level2(u32* x1, u32* x2, const uint4* tw, u32 n, u32 logn, u32 ls) {
+  const u32 h = n >> (ls + 1), lh = logn - 1 - ls, off = n - (n >> ls);
+  const uint4* tl = tw + (DIF ? 2 * n : 3 * n) + off;
+  for (u32 t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+    const u32 grp = t >> lh, j = t & (h - 1);
+    const u32 i0 = pd(grp * 2 * h + j), i1 = pd(grp * 2 * h + j + h);
+    u32 a = x1[i0], b = x1[i1], c = x2[i0], d = x2[i1];
+    const uint4 w = __ldg(tl + j);
+    if (DIF) {
+      bf_dif<Q1>(a, b, w.x, w.y);
+      bf_dif<Q2>(c, d, w.z, w.w);
+    } else {
+      bf_dit<Q1>(a, b, w.x, w.y);
+      bf_dit<Q2>(c, d, w.z, w.w);
     }
-    __syncthreads();
+    x1[i0] = a;
+    x1[i1] = b;
+    x2[i0] = c;
+    x2[i1] = d;
   }
+  __syncthreads();
+}
+// Three levels in registers: the sets {base + m q, m < 8} (q the smallest
+// span of the three) are closed under them.  DIF: spans 4q, 2q, q (levels
+// ls, ls+1, ls+2); DIT: spans q, 2q, 4q (levels ls+2, ls+1, ls).  The
+// twiddles a set needs: four at the 4q level, two at 2q, one at q.
+template <bool DIF>
+__device__ __forceinline__ void pass8(u32* x1, u32* x2, const uint4* tw, u32 n, u32 logn, u32 ls) {
+  const u32 logq = logn - ls - 3, q = 1u << logq;
+  const uint4* tl = tw + (DIF ? 2 * n : 3 * n);
+  const u32 o0 = n - (n >> ls), o1 = n - (n >> (ls + 1)), o2 = n - (n >> (ls + 2));
+  for (u32 st = threadIdx.x; st < (n >> 3); st += blockDim.x) {
+    const u32 g = st >> logq, r = st & (q - 1), base = (g << (logq + 3)) + r;
+    u32 v1[8], v2[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      v1[m] = x1[pd(base + m * q)];
+      v2[m] = x2[pd(base + m * q)];
+    }
+    uint4 w[7];  // [0..3] the 4q level, [4..5] 2q, [6] q
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      w[k] = __ldg(tl + (k < 4 ? o0 + r + k * q : (k < 6 ? o1 + r + (k - 4) * q : o2 + r)));
+    auto bf = [&](int k, int m0, int m1) {
+      if (DIF) {
+        bf_dif<Q1>(v1[m0], v1[m1], w[k].x, w[k].y);
+        bf_dif<Q2>(v2[m0], v2[m1], w[k].z, w[k].w);
+      } else {
+        bf_dit<Q1>(v1[m0], v1[m1], w[k].x, w[k].y);
+        bf_dit<Q2>(v2[m0], v2[m1], w[k].z, w[k].w);
+      }
+    };
+    if (DIF) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) bf(m, m, m + 4);
+#pragma unroll
+      for (int m = 0; m < 8; m += 4) {
+        bf(4, m, m + 2);
+        bf(5, m + 1, m + 3);
+      }
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) bf(6, m, m + 1);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 8; m += 2) bf(6, m, m + 1);
+#pragma unroll
+      for (int m = 0; m < 8; m += 4) {
+        bf(4, m, m + 2);
+        bf(5, m + 1, m + 3);
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) bf(m, m, m + 4);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      x1[pd(base + m * q)] = v1[m];
+      x2[pd(base + m * q)] = v2[m];
+    }
+  }
+  __syncthreads();
+}
+// cyclic NTTs of length n = 2^logn: DIF natural -> bit reversed (levels 0,
+// 1, ...), DIT bit reversed -> natural (levels logn-1, ..., 0)
+__device__ __forceinline__ void ntt_dif2(u32* x1, u32* x2, const uint4* tw, u32 n, u32 logn) {
+  u32 ls = 0;
+  for (; ls + 3 <= logn; ls += 3) pass8<true>(x1, x2, tw, n, logn, ls);
+  for (; ls < logn; ++ls) level2<true>(x1, x2, tw, n, logn, ls);
+}
+__device__ __forceinline__ void ntt_dit2(u32* x1, u32* x2, const uint4* tw, u32 n, u32 logn) {
+  int ls = (int)logn - 1;
+  for (; ls >= 0 && (u32)ls + 1 > (logn / 3) * 3; --ls) level2<false>(x1, x2, tw, n, logn, (u32)ls);
+  for (; ls >= 2; ls -= 3) pass8<false>(x1, x2, tw, n, logn, (u32)ls - 2);
 }
 
 // Adds each chunk's pending signed carry `pend` into the chunked value (chunk
@@ -198,26 +274,31 @@ __device__ __forceinline__ long long ripple(u32 (&wv)[16], long long* sh, u32 t,
   return r;
 }
 
-// One CTA per product: a[e] <- a[e] * b[e] mod 2^N + 1, canonical output
-// (lo in [0, 2^N), top word 1 only for 2^N == -1), as the transforms expect.
+// One CTA per product: a[e] <- a[e] * b[e] * 2^rot mod 2^N + 1, canonical
+// output (lo in [0, 2^N), top word 1 only for 2^N == -1).  The digit
+// vectors' negacyclic convolution runs as psi-weighted cyclic NTTs modulo Q1
+// and Q2 in shared memory (four u32 arrays of n), then CRT to signed 64-bit
+// coefficients, digit shift by rot, folding into 512-bit chunks and carry
+// resolution.
 __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) {
-  extern __shared__ __align__(16) u64 s_f[];
+  extern __shared__ __align__(16) u32 s_f[];
   const u32 n = A.D16;
-  u64* xa = s_f;
-  u64* xb = s_f + n;
-  const u64* w = A.tw + 7 * (u64)n / 2;   // per-level omega^(j 2^ls) (ntt_dif)
-  const u64* wi = A.tw + 9 * (u64)n / 2;  // per-level omega^-(j 2^ls) (ntt_dit)
+  const u32 np = padded(n);
+  u32* a1 = s_f;
+  u32* a2 = s_f + np;
+  u32* b1 = s_f + 2 * np;
+  u32* b2 = s_f + 3 * np;
+  long long* cf = reinterpret_cast<long long*>(b1);  // signed coefficients, once b is consumed
+  const uint4* tw = A.tw;
   std::uint8_t* ea = A.a + (u64)blockIdx.x * A.stride;
   const std::uint8_t* eb = A.b + (u64)blockIdx.x * A.stride;
-  const u64* psi = A.tw;                 // psi^i
-  const u64* psii = A.tw + n + n;        // psi^-i * (1/n)
   const std::uint16_t* da = reinterpret_cast<const std::uint16_t*>(ea);
   const std::uint16_t* db = reinterpret_cast<const std::uint16_t*>(eb);
   const long long topa = *reinterpret_cast<const long long*>(ea + (u64)A.D32 * 4);
   const long long topb = *reinterpret_cast<const long long*>(eb + (u64)A.D32 * 4);
   const u32 chunks = n / 32;  // thread t owns words [16t, 16t+16)
   const u32 t = threadIdx.x;
-  long long* carry = reinterpret_cast<long long*>(xb);  // scratch once xb is consumed
+  long long* carry = reinterpret_cast<long long*>(a1);  // scratch once the coefficients are out
   u32 wv[16];
   long long pend = 0;
   if (topa != 0 || topb != 0) {
@@ -225,23 +306,47 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
     // product is -b, -a or 1: as negacyclic digit coefficients -x_i, or 1
     const bool one = topa != 0 && topb != 0;
     const std::uint16_t* other = topa ? db : da;
-    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-      const u64 d = one ? (i == 0 ? 1u : 0u) : (u64)other[i];
-      xa[i] = one ? d : (d ? GP - d : 0);
-    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x)
+      cf[i] = one ? (i == 0 ? 1 : 0) : -(long long)other[i];
     __syncthreads();
   } else {
     for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
-      xa[i] = g_mul((u64)da[i], psi[i]);
-      xb[i] = g_mul((u64)db[i], psi[i]);
+      const u32 x = da[i], y = db[i], k = pd(i);
+      const uint4 ps = __ldg(tw + i);
+      a1[k] = shoup(x, ps.x, ps.y, Q1);
+      a2[k] = shoup(x, ps.z, ps.w, Q2);
+      b1[k] = shoup(y, ps.x, ps.y, Q1);
+      b2[k] = shoup(y, ps.z, ps.w, Q2);
     }
     __syncthreads();
-    ntt_dif(xa, w, n, A.logn);
-    ntt_dif(xb, w, n, A.logn);
-    for (u32 i = threadIdx.x; i < n; i += blockDim.x) xa[i] = g_mul(xa[i], xb[i]);
+    ntt_dif2(a1, a2, tw, n, A.logn);
+    ntt_dif2(b1, b2, tw, n, A.logn);
+    constexpr u64 M1 = ~0ull / Q1, M2 = ~0ull / Q2;
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+      const u32 k = pd(i);
+      a1[k] = mulmod_b(a1[k], b1[k], Q1, M1);
+      a2[k] = mulmod_b(a2[k], b2[k], Q2, M2);
+    }
     __syncthreads();
-    ntt_dit(xa, wi, n, A.logn);
-    for (u32 i = threadIdx.x; i < n; i += blockDim.x) xa[i] = g_mul(xa[i], psii[i]);
+    ntt_dit2(a1, a2, tw, n, A.logn);
+    // unweight (psi^-i / n), CRT: c = r1 + Q1 ((r2 - r1) Q1^-1 mod Q2), signed
+    constexpr u32 INV = 208783132u;               // Q1^-1 mod Q2
+    constexpr u32 INVP = (u32)(((u64)INV << 32) / Q2);
+    constexpr u64 P = (u64)Q1 * Q2;
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint4 ip = __ldg(tw + n + i);
+      u32 r1 = shoup(a1[pd(i)], ip.x, ip.y, Q1);
+      u32 r2 = shoup(a2[pd(i)], ip.z, ip.w, Q2);
+      r1 = r1 >= Q1 ? r1 - Q1 : r1;
+      r2 = r2 >= Q2 ? r2 - Q2 : r2;
+      u32 r1m = r1 >= Q2 ? r1 - Q2 : r1;
+      r1m = r1m >= Q2 ? r1m - Q2 : r1m;
+      u32 k = shoup(r2 + Q2 - r1m, INV, INVP, Q2);
+      k = k >= Q2 ? k - Q2 : k;
+      const u64 c = r1 + (u64)Q1 * k;
+      cf[i] = c > P / 2 ? (long long)c - (long long)P : (long long)c;
+    }
     __syncthreads();
   }
   {
@@ -261,8 +366,7 @@ __global__ void __launch_bounds__(512) fermat_pointwise_kernel(FermatMulArgs A) 
           src += (int)n;
           neg = !neg;
         }
-        const u64 v = xa[src];
-        long long c = v > (GP >> 1) ? -(long long)(GP - v) : (long long)v;
+        long long c = cf[src];
         if (neg) c = -c;
         c *= (1ll << r);  // |c| < 2^60
         // c * 2^(16 d) -> word d/2, shifted by 16 (d odd)
