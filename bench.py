@@ -90,13 +90,40 @@ def hbm_peak():
 
 
 def load_traffic(cfg: str):
-    """dram bytes per launch from the committed ncu summary, if any."""
+    """The committed ncu DRAM traffic of a config (tools/traffic.py), only when
+    it was measured on this very build (sha256 of the loaded library)."""
+    import hashlib
+
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(cfg)
+            t = json.load(fh).get(cfg)
+        lib = os.path.join(ROOT, "paper_0810_3203_b200", "lib", "libcftft_b200.so")
+        if not isinstance(t, dict):
+            return None, "no ncu traffic for this config"
+        if hashlib.sha256(open(lib, "rb").read()).hexdigest() != t.get("so_sha256"):
+            return None, "profiles/traffic.json is from another build of the library (stale): not reported"
+        return t, "ncu dram__bytes_read.sum + dram__bytes_write.sum, this build (profiles/traffic.json)"
     except Exception:
-        return None
+        return None, "no profiles/traffic.json"
+
+
+def kernel_roofline(records, steps, peak):
+    """Per kernel name: launches, ms and algorithmic GB/s per step from the
+    library's launch timing (CUDA events on the launching stream, inside the
+    timed region); the dominant kernel is the one with the most time."""
+    agg = {}
+    for name, byts, ms in records:
+        a = agg.setdefault(name, [0, 0, 0.0])
+        a[0] += 1
+        a[1] += byts
+        a[2] += ms
+    table = {name: {"launches_per_step": c / steps, "ms_per_step": ms / steps,
+                    "algorithmic_bytes_per_launch": b / c, "gbs": b / (ms / 1e3) / 1e9 if ms else None,
+                    "frac": (b / (ms / 1e3) / 1e9) / peak if ms else None}
+             for name, (c, b, ms) in agg.items()}
+    dom = max(table, key=lambda k: table[k]["ms_per_step"]) if table else None
+    return dom, table
 
 
 class ClockSampler:
@@ -247,6 +274,37 @@ def cpu_sample_round_trip(N, L, z, n, buf, threads, every):
 
 
 CPU_SAMPLE_EVERY = 8  # 1/8 of the sub-transforms: ~2 s per step on 8 cores at C5
+CPU_SAMPLE_EVERY_1T = 64  # single-thread sample: 1/64 of the sub-transforms
+
+
+def cpu0_reference(L: int, z: int, n: int):
+    """SURVEY.md §8d CPU-0 (context only): the unmodified reference cf_tft /
+    cf_itft (oracle/_ref, built from /root/reference/proj/include) over its own
+    Goldilocks ring at the same (L, z, n) on one core; GB/s with its 8-byte
+    coefficients.  None when oracle/_ref is absent."""
+    import ctypes as C
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    if not po.ref_available():
+        return None
+    P, m = 0xFFFFFFFF00000001, 32
+    rng = np.random.default_rng(po.mix_seed(42, 7))
+    buf = np.zeros(L, dtype=np.uint64)
+    buf[:z] = rng.integers(0, P, size=z, dtype=np.uint64)
+    ptr = buf.ctypes.data_as(po.U64P)
+    c = C.c_uint64(0)
+    t = time.perf_counter()
+    po.ref().ref_tft(P, m, L, 0, z, n, ptr, L, 0, 1, 0, C.byref(c))
+    po.ref().ref_itft(P, m, L, 0, n, n, 0, ptr, L, 0, 1, 0, C.byref(c))
+    secs = time.perf_counter() - t
+    byts = tft_bytes(64, L, z, n) + itft_bytes(64, L, n, n, 0)
+    return {"value": byts / secs / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference", "seconds": secs,
+            "sample": f"the whole TFT+ITFT over Z/pZ (p = 2^64 - 2^32 + 1), L={L}, z=n={z}: a different ring "
+                      "(8-byte coefficients), context only"}
 
 
 # ---------------------------------------------------------------------------
@@ -385,6 +443,26 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
                "note": "per rank: pinned column slab in, round trip (transforms + NVLink transposes), column slab "
                        "out; triple-buffered streams overlap consecutive steps"}
     if rank == 0:
+        dom, table = kernel_roofline(timed, args.steps, peak)
+        traffic, traffic_note = load_traffic(args.config)
+        dk = table.get(dom, {})
+        tk = (traffic or {}).get("per_kernel", {}).get(dom, {})
+        roofline = {
+            "bound": "hbm", "kernel": dom, "achieved": dk.get("gbs"), "peak": peak, "unit": "GB/s",
+            "frac": dk.get("frac"), "peak_kind": peak_kind,
+            "traffic": tk.get("dram_bytes_per_launch"),
+            "traffic_note": traffic_note,
+            "algorithmic_bytes_per_launch": dk.get("algorithmic_bytes_per_launch"),
+            "kernel_ms_per_step": dk.get("ms_per_step"), "launches_per_step": dk.get("launches_per_step"),
+            "kernel_share_of_step": dk.get("ms_per_step", 0) / ms_per_step if dk else None,
+            "ncu_share_of_step": tk.get("share_of_step"),
+            "timing": "library launch timing: CUDA events around every launch on its stream, inside the timed "
+                      "region; algorithmic bytes = coefficients the launch's leaves read + write x N/8",
+            "step": {"achieved": kernel_gbs, "frac": kernel_gbs / peak,
+                     "traffic": (traffic or {}).get("step_dram_bytes"),
+                     "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
+            "kernels": table,
+        }
         line = {
             "metric": f"TFT+ITFT GB/s ({args.config}: {desc})",
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -399,7 +477,7 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
                          "frac": value / world / peak, "peak_kind": peak_kind, "traffic": None,
                          "per": "GPU", "nvlink_bytes_per_gpu_per_step": xfer,
                          "nvlink_gbs_per_gpu": xfer / (total_ms / args.steps / 1e3) / 1e9,
-                         "nvlink_peak_gbs": 770.0},
+                         "nvlink_peak_gbs": 900.0},
             "cpu_baseline": None,
             "e2e": e2e,
             "gpu_launches": eng.launches - l0,
@@ -626,12 +704,16 @@ def main():
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     sampler.begin()
+    cf.launch_timing_read()  # (drop anything logged before)
+    cf.set_launch_timing(True)
     g0.record(stream)
     launches = 0
     for k in range(args.steps):
         launches += step(evs[k])
     g1.record(stream)
     barrier()
+    cf.set_launch_timing(False)
+    timed = cf.launch_timing_read()
     sampler.end()
     clocks = sampler.stop()
     total_ms = g0.elapsed_time(g1)
@@ -707,9 +789,38 @@ def main():
                "sample": f"every {CPU_SAMPLE_EVERY}th top-level Bailey sub-transform of the {args.config} "
                          f"TFT and ITFT ({sb / 1e9:.2f} GB algorithmic, {secs:.1f} s) in place on the full "
                          f"seeded buffer, oracle port on {threads} host threads, {model}"}
+        # CPU-1 single thread (the reference's methodology)
+        secs1, sb1 = cpu_sample_round_trip(N, L, z, n, hb, 1, CPU_SAMPLE_EVERY_1T)
+        cpu["single_thread"] = {
+            "value": sb1 / secs1 / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"every {CPU_SAMPLE_EVERY_1T}th top-level Bailey sub-transform ({sb1 / 1e9:.2f} GB "
+                      f"algorithmic, {secs1:.1f} s), one host thread"}
         del hb
+        # CPU-0 context: the UNMODIFIED reference over its own ring (Goldilocks,
+        # 8-byte coefficients) at this config's (L, z, n), one core
+        cpu["cpu0_reference_goldilocks"] = cpu0_reference(L, z, n)
 
     if rank == 0:
+        dom, table = kernel_roofline(timed, args.steps, peak)
+        traffic, traffic_note = load_traffic(args.config)
+        dk = table.get(dom, {})
+        tk = (traffic or {}).get("per_kernel", {}).get(dom, {})
+        roofline = {
+            "bound": "hbm", "kernel": dom, "achieved": dk.get("gbs"), "peak": peak, "unit": "GB/s",
+            "frac": dk.get("frac"), "peak_kind": peak_kind,
+            "traffic": tk.get("dram_bytes_per_launch"),
+            "traffic_note": traffic_note,
+            "algorithmic_bytes_per_launch": dk.get("algorithmic_bytes_per_launch"),
+            "kernel_ms_per_step": dk.get("ms_per_step"), "launches_per_step": dk.get("launches_per_step"),
+            "kernel_share_of_step": dk.get("ms_per_step", 0) / ms_per_step if dk else None,
+            "ncu_share_of_step": tk.get("share_of_step"),
+            "timing": "library launch timing: CUDA events around every launch on its stream, inside the timed "
+                      "region; algorithmic bytes = coefficients the launch's leaves read + write x N/8",
+            "step": {"achieved": kernel_gbs, "frac": kernel_gbs / peak,
+                     "traffic": (traffic or {}).get("step_dram_bytes"),
+                     "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
+            "kernels": table,
+        }
         line = {
             "metric": f"TFT+ITFT GB/s ({args.config}: {desc})",
             "value": value,
@@ -728,11 +839,7 @@ def main():
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": "inputs (3.3 GB at C5) far exceed the 126 MB L2; no flush needed"
                        if args.config == "C5" else "see DESIGN.md"},
-            "roofline": {"bound": "hbm", "achieved": kernel_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": kernel_gbs / peak, "peak_kind": peak_kind,
-                         "traffic": load_traffic(args.config),
-                         "kernel": "coset_wave_kernel + leaf_kernel waves (all kernels of the step)",
-                         "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -237,6 +237,20 @@ uint64_t cftft_last_launch_count(void);
 void cftft_set_fault_injection(int on);
 int cftft_fault_injection(void);
 
+/* Launch timing for the bench (roofline of the dominant kernel): while set,
+ * every kernel of a transform is bracketed by CUDA events on its launching
+ * stream and logged with its ALGORITHMIC bytes (coefficients its leaves read
+ * plus write, times the coefficient's information bytes: N/8, 8 K, 8).
+ * cftft_launch_timing_read waits for the logged launches of the calling
+ * thread, copies up to max records and returns how many there were. */
+typedef struct cftft_launch_record {
+  char kernel[40];
+  uint64_t algorithmic_bytes;
+  float ms;
+} cftft_launch_record;
+void cftft_set_launch_timing(int on);
+uint64_t cftft_launch_timing_read(cftft_launch_record* out, uint64_t max);
+
 /* Debug poison (transform.hpp:58-70, poison_tail): while set, cftft_gpu_tft
  * / cftft_gpu_itft run each transform twice, with two different
  * non-canonical fills of the cells [z, L) (inputs [0, z) restored in

@@ -40,6 +40,7 @@ __all__ = [
     "itft_bound", "tft_base_cases", "itft_base_cases", "lib", "last_launch_count", "plan_dump", "PrimeRingCtx",
     "GOLDILOCKS",
     "scale", "set_fault_injection", "fault_injection", "set_debug_poison", "PoisonRead", "NoMemory",
+    "set_launch_timing", "launch_timing_read",
 ]
 
 
@@ -97,6 +98,10 @@ class _Sub(C.Structure):
                 ("base", C.c_uint64), ("stride", C.c_uint64)]
 
 
+class _LaunchRec(C.Structure):
+    _fields_ = [("kernel", C.c_char * 40), ("algorithmic_bytes", C.c_uint64), ("ms", C.c_float)]
+
+
 _lib = None
 
 
@@ -142,6 +147,10 @@ def lib():
         L.cftft_fault_injection.restype = C.c_int
         L.cftft_set_debug_poison.argtypes = [C.c_int]
         L.cftft_set_debug_poison.restype = None
+        L.cftft_set_launch_timing.argtypes = [C.c_int]
+        L.cftft_set_launch_timing.restype = None
+        L.cftft_launch_timing_read.argtypes = [C.POINTER(_LaunchRec), u64]
+        L.cftft_launch_timing_read.restype = u64
         _lib = L
     return _lib
 
@@ -399,6 +408,19 @@ def set_debug_poison(on: bool) -> None:
     transform runs twice with different fills of the cells >= z and raises
     PoisonRead if a specified output differs."""
     lib().cftft_set_debug_poison(1 if on else 0)
+
+
+def set_launch_timing(on: bool) -> None:
+    """CUDA events around every kernel of the transforms (bench roofline)."""
+    lib().cftft_set_launch_timing(1 if on else 0)
+
+
+def launch_timing_read() -> list:
+    """Waits for the logged launches of this thread: [(kernel, algorithmic
+    bytes, ms)], and forgets them."""
+    buf = (_LaunchRec * 4096)()
+    n = lib().cftft_launch_timing_read(buf, 4096)
+    return [(buf[i].kernel.decode(), buf[i].algorithmic_bytes, buf[i].ms) for i in range(min(n, 4096))]
 
 
 def last_launch_count() -> int:

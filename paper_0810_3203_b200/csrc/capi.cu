@@ -35,6 +35,46 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<int> g_fault{0};   // cftft_set_fault_injection
+std::atomic<int> g_timing{0};  // cftft_set_launch_timing
+// Launch timing (cftft_set_launch_timing): CUDA events on the launching
+// stream around each kernel of the transforms, with the launch's algorithmic
+// bytes (coefficients read + written x information bytes per coefficient).
+struct TimedLaunch {
+  const char* kernel;
+  u64 bytes;
+  cudaEvent_t e0, e1;
+};
+thread_local std::vector<TimedLaunch> g_timed;
+thread_local std::vector<cudaEvent_t> g_event_pool;
+cudaEvent_t pooled_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+// RAII around one launch; a no-op unless timing is on
+struct LaunchTimer {
+  cudaStream_t st;
+  bool on;
+  TimedLaunch rec{};
+  LaunchTimer(const char* kernel, u64 bytes, cudaStream_t s) : st(s), on(g_timing.load() != 0) {
+    if (!on) return;
+    rec.kernel = kernel;
+    rec.bytes = bytes;
+    rec.e0 = pooled_event();
+    rec.e1 = pooled_event();
+    cudaEventRecord(rec.e0, st);
+  }
+  ~LaunchTimer() {
+    if (!on) return;
+    cudaEventRecord(rec.e1, st);
+    g_timed.push_back(rec);
+  }
+};
 std::atomic<int> g_poison{0};  // cftft_set_debug_poison
 
 // Experiment knobs (phase clocks, debug skips) exist only in builds with
@@ -91,6 +131,7 @@ struct DevicePlan {
   std::uint8_t* tma_lay = nullptr;  // coset-major layout bits per wave_slots entry (inside tma_descs)
   u32 tma_step = 0;
   std::vector<u64> batch_items;  // batch plans: the items, compared on a cache hit
+  std::vector<u64> wave_loads;   // per wave: coefficients read + written by its leaves (launch timing)
   bool tma_cm_finals = false;  // every shadow-buffer final is written coset-major by a TMA wave
   u64 nleaves = 0;
   u32 ncounters = 0;
@@ -255,6 +296,10 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   // radix-64 network waves on the TMA kernel (wave_tma.cuh): 64-slot full
   // networks over 256-bit lanes with at least two cosets, one item per coset,
   // stage-A rotations only where the kernel's compile-time mask has them
+  dp.wave_loads.assign(p.waves.size(), 0);
+  for (size_t w = 0; w < p.waves.size(); ++w)
+    for (u64 i = p.waves[w][0]; i < p.waves[w][0] + p.waves[w][1]; ++i)
+      dp.wave_loads[w] += (u64)cls[p.leaves[i].cls].nload + cls[p.leaves[i].cls].nstore;
   dp.tma_wave.assign(p.waves.size(), 0);
   std::vector<fermat::TmaLeafDesc> descs;
   dp.tma_desc_off.assign(p.waves.size(), 0);
@@ -662,6 +707,11 @@ int ensure_prime_tables(cftft_ring* R, cudaStream_t st) {
   return CFTFT_OK;
 }
 
+// information bytes of one coefficient (N/8, 8 K, 8)
+u64 info_bytes(const cftft_ring* R) {
+  return R->kind == CFTFT_RING_FERMAT ? R->N / 8 : (R->kind == CFTFT_RING_NEGACYCLIC ? 8 * R->K : 8);
+}
+
 int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, cudaStream_t st,
                 bool canonicalize) {
   u64 launches = 0;
@@ -808,6 +858,11 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         bool tma_maps = false;
         for (size_t wi = 0; wi < dp.host.waves.size(); ++wi) {
           const auto& wr = dp.host.waves[wi];
+          const char* kname = (wr[2] == 2 && dp.tma_wave[wi]) ? "coset_tma_kernel"
+                              : wr[2] == 2                   ? "coset_wide_kernel"
+                              : wr[2] == 1                   ? "coset_wave_kernel"
+                                                             : "leaf_kernel";
+          LaunchTimer lt(kname, dp.wave_loads[wi] * info_bytes(R), st);
           if (wr[2] == 2 && dp.tma_wave[wi]) {
             if (!tma_maps) {
               if (int e = make_coset_map(&tm_view, base, stride, dp.host.extent, dp.tma_step)) return e;
@@ -870,17 +925,20 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         if (dp.host.use_fold_list) {
           // listed outputs in place, the shadow buffer's from there into place
           if (!dp.host.fold_list.empty()) {
+            LaunchTimer lt("cs_fold_kernel", 2 * dp.host.fold_list.size() * info_bytes(R), st);
             fermat::cs_fold_kernel<<<(unsigned)dp.host.fold_list.size(), 256, fsm, st>>>(
                 base, stride, tops, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot, dp.fold_list, nullptr);
             ++launches;
           }
           if (!dp.host.shadow_finals.empty()) {
+            LaunchTimer lt("cs_fold_kernel", 2 * dp.host.shadow_finals.size() * info_bytes(R), st);
             fermat::cs_fold_kernel<<<(unsigned)dp.host.shadow_finals.size(), 256, fsm, st>>>(
                 base, stride, tops + A.tloc, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot,
                 dp.shadow_finals, shadow, dp.tma_cm_finals ? (u32)__builtin_ctz(dp.tma_step) : 0u);
             ++launches;
           }
         } else if (dp.host.final_count) {
+          LaunchTimer lt("cs_fold_kernel", 2 * dp.host.final_count * info_bytes(R), st);
           fermat::cs_fold_kernel<<<(unsigned)dp.host.final_count, 256, fsm, st>>>(
               base, stride, tops, dp.C, dp.cw, logC, dp.logS, R->D, 0, 1, dp.final_rot, nullptr, nullptr);
           ++launches;
@@ -1720,6 +1778,26 @@ uint64_t cftft_itft_base_cases(uint64_t L, uint64_t z, uint64_t n, int f, int po
 
 uint64_t cftft_last_launch_count(void) { return g_last_launches; }
 void cftft_set_fault_injection(int on) { g_fault.store(on ? 1 : 0); }
+void cftft_set_launch_timing(int on) { g_timing.store(on ? 1 : 0); }
+uint64_t cftft_launch_timing_read(cftft_launch_record* out, uint64_t max) {
+  // waits for the recorded launches; returns (and forgets) this thread's records
+  const u64 n = g_timed.size();
+  for (u64 i = 0; i < n; ++i) {
+    TimedLaunch& t = g_timed[i];
+    float ms = 0.f;
+    cudaEventSynchronize(t.e1);
+    cudaEventElapsedTime(&ms, t.e0, t.e1);
+    if (out && i < max) {
+      std::snprintf(out[i].kernel, sizeof out[i].kernel, "%s", t.kernel);
+      out[i].algorithmic_bytes = t.bytes;
+      out[i].ms = ms;
+    }
+    g_event_pool.push_back(t.e0);
+    g_event_pool.push_back(t.e1);
+  }
+  g_timed.clear();
+  return n;
+}
 int cftft_fault_injection(void) { return g_fault.load(); }
 void cftft_set_debug_poison(int on) { g_poison.store(on ? 1 : 0); }
 
