@@ -386,11 +386,15 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
     l0 = eng.launches
     barrier()
     sampler.begin()
+    cf.launch_timing_read()
+    cf.set_launch_timing(True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     barrier()
+    cf.set_launch_timing(False)
+    timed = cf.launch_timing_read()
     sampler.end()
     clocks = sampler.stop()
     t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
@@ -444,23 +448,19 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
                        "out; triple-buffered streams overlap consecutive steps"}
     if rank == 0:
         dom, table = kernel_roofline(timed, args.steps, peak)
-        traffic, traffic_note = load_traffic(args.config)
         dk = table.get(dom, {})
-        tk = (traffic or {}).get("per_kernel", {}).get(dom, {})
         roofline = {
             "bound": "hbm", "kernel": dom, "achieved": dk.get("gbs"), "peak": peak, "unit": "GB/s",
-            "frac": dk.get("frac"), "peak_kind": peak_kind,
-            "traffic": tk.get("dram_bytes_per_launch"),
-            "traffic_note": traffic_note,
+            "frac": dk.get("frac"), "peak_kind": peak_kind, "traffic": None,
+            "traffic_note": "no ncu capture of the multi-rank path (ncu runs one GPU, one rank)",
             "algorithmic_bytes_per_launch": dk.get("algorithmic_bytes_per_launch"),
             "kernel_ms_per_step": dk.get("ms_per_step"), "launches_per_step": dk.get("launches_per_step"),
-            "kernel_share_of_step": dk.get("ms_per_step", 0) / ms_per_step if dk else None,
-            "ncu_share_of_step": tk.get("share_of_step"),
-            "timing": "library launch timing: CUDA events around every launch on its stream, inside the timed "
-                      "region; algorithmic bytes = coefficients the launch's leaves read + write x N/8",
-            "step": {"achieved": kernel_gbs, "frac": kernel_gbs / peak,
-                     "traffic": (traffic or {}).get("step_dram_bytes"),
-                     "tft_ms": t_tft / args.steps, "itft_ms": t_itft / args.steps},
+            "kernel_share_of_step": dk.get("ms_per_step", 0) / (total_ms / args.steps) if dk else None,
+            "per": "GPU (rank 0's launches)",
+            "step": {"achieved": value / world, "frac": value / world / peak},
+            "nvlink_bytes_per_gpu_per_step": xfer,
+            "nvlink_gbs_per_gpu": xfer / (total_ms / args.steps / 1e3) / 1e9,
+            "nvlink_peak_gbs": 900.0,
             "kernels": table,
         }
         line = {
@@ -473,11 +473,7 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
                        "coeff_bytes": N // 8, "algorithmic_bytes_per_step": byts,
                        "parallelism": f"column/row slabs over {world} GPUs, NCCL all-to-all transpose",
                        "l2": "inputs far exceed L2"},
-            "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
-                         "frac": value / world / peak, "peak_kind": peak_kind, "traffic": None,
-                         "per": "GPU", "nvlink_bytes_per_gpu_per_step": xfer,
-                         "nvlink_gbs_per_gpu": xfer / (total_ms / args.steps / 1e3) / 1e9,
-                         "nvlink_peak_gbs": 900.0},
+            "roofline": roofline,
             "cpu_baseline": None,
             "e2e": e2e,
             "gpu_launches": eng.launches - l0,

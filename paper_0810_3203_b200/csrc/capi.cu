@@ -425,7 +425,9 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
 // Planning geometry of one transform of length L.  Fermat: coset leaves use
 // lanes of `cw` words, chosen so that the reference's top-level split yields
 // sub-transforms whose internal rotations are whole lanes (M / sqrt(L) bits).
-RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
+// allow_wide = false: radix-8 waves only (batch plans: sub-transforms of one
+// pass are at most sqrt(L) long, where radix-64 leaves do not pay)
+RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp, bool allow_wide = true) {
   RingShape rs;
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
   if (R->kind == CFTFT_RING_PRIME) rs.group = 16;  // adjacent u64 coefficients per ticket
@@ -472,7 +474,7 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp) {
         rs.wave_unaligned = true;
         // radix-64 coset leaves (default: their full-network waves run on the
         // TMA-wave kernel, wave_tma.cuh; set_wide(0): radix-8 warp waves only)
-        const int wide = R->wide >= 0 ? R->wide : 1;
+        const int wide = !allow_wide ? 0 : (R->wide >= 0 ? R->wide : 1);
         rs.wide = wide != 0 && cl >= 6 && (R->M >> 6) % rs.lane_bits == 0;
         cl = std::min(cl, rs.wide ? 6u : 3u);
         rs.max_leaf_ell = std::min(rs.max_leaf_ell, 3u);
@@ -1728,7 +1730,7 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
           it2 = std::get<1>(it2->first) >= 3 ? R->cache.erase(it2) : std::next(it2);
       }
       auto np = std::make_unique<DevicePlan>();
-      const RingShape rs = shape_of(R, v[0].L, np.get());
+      const RingShape rs = shape_of(R, v[0].L, np.get(), false);
       try {
         np->host = best_plan(rs, [&](Planner& pl) { return pl.build_batch(inverse != 0, v, policy); });
       } catch (const std::exception& ex) {
@@ -1741,7 +1743,8 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
     }
   }
   int rc = launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, st, false);
-  if (rc || !canonicalize || R->kind != CFTFT_RING_FERMAT) return rc;
+  // coset plans end in the carry-save fold: their outputs are canonical already
+  if (rc || !canonicalize || R->kind != CFTFT_RING_FERMAT || dp->host.coset) return rc;
   for (u64 k = 0; k < count; ++k) {
     const u64 outs = v[k].n + (u64)v[k].f;
     std::uint8_t* b = static_cast<std::uint8_t*>(dev_base) + v[k].base * elem_stride_bytes;

@@ -70,18 +70,13 @@ class GpuEngine:
         self.launches = 0
 
     def batch(self, inverse: bool, subs, slab: torch.Tensor) -> None:
+        """One batched launch; outputs canonical (coset plans end in their
+        carry-save fold, whole-leaf plans get a canonicalising pass)."""
         from . import last_launch_count, run_batch
 
         if subs:
-            run_batch(self.ctx, inverse, subs, slab, self.policy)
+            run_batch(self.ctx, inverse, subs, slab, self.policy, canonicalize=True)
             self.launches += last_launch_count()
-
-    def canonicalize(self, slab: torch.Tensor, count: int) -> None:
-        from . import canonicalize
-
-        if count > 0:
-            canonicalize(self.ctx, slab, count)
-            self.launches += 1
 
 
 class DistGeometry:
@@ -165,7 +160,6 @@ class DistTFT:
         subs = [Sub(g.L2, s_row, g.z2e, g.L2 if u < g.n1 else g.n2, 0, (u - r0) * g.L2, 1)
                 for u in range(r0, r1)]
         self.engine.batch(False, subs, rowslab)
-        self.engine.canonicalize(rowslab, self._valid_in_rows(r0, r1, g.n))
         return rowslab
 
     def _valid_in_rows(self, r0: int, r1: int, count: int) -> int:
@@ -258,7 +252,6 @@ class DistTFT:
             if u < n2:
                 subs.append(Sub(g.L1, self.s + u * g.col_step, z1 + 1 if u < lo else z1, n1 + 1, 0, c, W))
         self.engine.batch(True, subs, colslab)
-        self.engine.canonicalize(colslab, min(colslab.shape[0], (n1 + 1) * W))
 
     def _phase3(self, g, colslab, rowslab, s_row):
         """Row n1 (transform.hpp:227-230): gather its right part from the column
