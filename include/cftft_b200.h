@@ -221,6 +221,31 @@ int cftft_gpu_mul_scalar(const cftft_ring* ring, void* dev_base, uint64_t count,
 int cftft_gpu_scale(const cftft_ring* ring, void* dev_base, uint64_t count,
                     uint64_t elem_stride_bytes, uint64_t e, void* stream);
 
+/* Multi-GPU transforms: one transform partitioned over the
+ * ranks of an NCCL communicator, one GPU per rank.  Rank p owns top-level
+ * columns [c0, c1) of the Bailey split L = L1 x L2 (a "column slab": L1 x
+ * (c1 - c0) elements, element (r, c) at r (c1 - c0) + c) and rows [r0, r1)
+ * of the active rows (a "row slab": (r1 - r0) x L2, each row contiguous).
+ * cftft_gpu_dist_tft: column slab (inputs x[r L2 + c] for the rank's
+ * columns) -> column TFTs -> NCCL transpose -> row TFTs -> row slab (the
+ * first n outputs, in the reference's bit-reversed order, row by row).
+ * cftft_gpu_dist_itft: row slab (x[0, n) transformed values, x[n, z) L a)
+ * -> phases i-iv with the transposes and the phase-iii row exchange ->
+ * column slab (L a[0, n), plus x[n] if f = 1).  Asynchronous on `stream`;
+ * every rank calls with the same parameters.  NCCL is loaded at run time
+ * (libnccl.so.2). */
+typedef struct cftft_dist cftft_dist;
+int cftft_nccl_unique_id(void* out128);  /* ncclGetUniqueId: rank 0 makes it, all ranks get a copy */
+int cftft_dist_create(const cftft_ring* ring, int rank, int world, const void* nccl_id128, cftft_dist** out);
+int cftft_dist_create_from_comm(const cftft_ring* ring, void* nccl_comm, cftft_dist** out);
+void cftft_dist_destroy(cftft_dist* d);
+/* this rank's slabs: out[8] = {c0, c1, r0, r1, L1, L2, column-slab elements, row-slab elements} */
+int cftft_dist_geometry(const cftft_dist* d, const cftft_params* params, int inverse, int policy, uint64_t* out);
+int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* params, void* dev_colslab, void* dev_rowslab,
+                       uint64_t elem_stride_bytes, int policy, void* stream);
+int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* params, void* dev_rowslab, void* dev_colslab,
+                        uint64_t elem_stride_bytes, int policy, void* stream);
+
 /* Base-case counts of the reference recursion (data independent;
  * verify.hpp:175-199), by host replay.  No GPU needed. */
 uint64_t cftft_tft_base_cases(uint64_t L, uint64_t z, uint64_t n, int policy);

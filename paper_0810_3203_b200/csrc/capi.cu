@@ -24,6 +24,7 @@
 #include "prime_leaf.cuh"
 #include "pointwise.cuh"
 #include "polymul.cuh"
+#include "dist.cuh"
 #include "wave_coset.cuh"
 #include "wave_wide.cuh"
 #include "wave_tma.cuh"
@@ -1833,3 +1834,289 @@ const char* cftft_last_error(void) { return g_last_error.c_str(); }
 const char* cftft_version(void) { return "cftft-b200 0.1 (sm_100a)"; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU transforms (dist.cuh): one transform partitioned over an NCCL
+// communicator's ranks.
+
+struct cftft_dist {
+  const cftft_ring* ring = nullptr;
+  ncclComm_t comm = nullptr;
+  bool owns = false;
+  int rank = 0, world = 1, device = 0;
+};
+
+namespace {
+#define NCCL_TRY(expr)                                                                                  \
+  do {                                                                                                  \
+    ncclResult_t r_ = (expr);                                                                           \
+    if (r_ != ncclSuccess)                                                                              \
+      return fail(CFTFT_CUDA_ERROR, std::string(#expr ": ") +                                           \
+                                        (dist::nccl().GetErrorString ? dist::nccl().GetErrorString(r_) \
+                                                                     : "nccl error"));                  \
+  } while (0)
+
+cftft_subtransform sub(u64 L, u64 s, u64 z, u64 n, int f, u64 base, u64 stride) {
+  cftft_subtransform t{};
+  t.length = L;
+  t.twiddle_exp = s;
+  t.input_count = z;
+  t.output_count = n;
+  t.want_next = f;
+  t.base = base;
+  t.stride = stride;
+  return t;
+}
+int run_subs(const cftft_dist* d, int inverse, const std::vector<cftft_subtransform>& v, void* slab, u64 esb,
+             int policy, cudaStream_t st) {
+  if (v.empty()) return CFTFT_OK;
+  return cftft_gpu_batch(d->ring, inverse, v.data(), v.size(), slab, esb, policy, 1, st);
+}
+// device copy of a small u64 table (stream ordered; freed after use)
+int dev_table(const std::vector<u64>& h, u64** out, cudaStream_t st) {
+  CUDA_TRY(cudaMallocAsync((void**)out, h.size() * 8, st));
+  CUDA_TRY(cudaMemcpyAsync(*out, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  return CFTFT_OK;
+}
+int check_dist(const cftft_dist* d, const cftft_params* p, int inverse, int policy, u64 esb) {
+  if (!d || !d->ring || !p) return fail(CFTFT_INVALID_PARAMS, "null argument");
+  if (int rc = validate(d->ring, inverse != 0, p, policy)) return rc;
+  if (int rc = check_stride(d->ring, esb)) return rc;
+  if (esb % 16) return fail(CFTFT_UNSUPPORTED, "distributed slabs need a 16-byte element stride");
+  return CFTFT_OK;
+}
+}  // namespace
+
+int cftft_nccl_unique_id(void* out) {
+  if (!out) return fail(CFTFT_INVALID_PARAMS, "null id buffer");
+  auto& n = dist::nccl();
+  if (!n.ok()) return fail(CFTFT_UNSUPPORTED, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  NCCL_TRY(n.GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof id);
+  return CFTFT_OK;
+}
+
+int cftft_dist_create(const cftft_ring* ring, int rank, int world, const void* nccl_id, cftft_dist** out) {
+  if (!ring || !nccl_id || !out || world < 1 || rank < 0 || rank >= world)
+    return fail(CFTFT_INVALID_PARAMS, "bad distributed context arguments");
+  auto& n = dist::nccl();
+  if (!n.ok()) return fail(CFTFT_UNSUPPORTED, "libnccl.so.2 not found");
+  auto d = std::make_unique<cftft_dist>();
+  d->ring = ring;
+  d->rank = rank;
+  d->world = world;
+  CUDA_TRY(cudaGetDevice(&d->device));
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof id);
+  NCCL_TRY(n.CommInitRank(&d->comm, world, id, rank));
+  d->owns = true;
+  *out = d.release();
+  return CFTFT_OK;
+}
+
+int cftft_dist_create_from_comm(const cftft_ring* ring, void* nccl_comm, cftft_dist** out) {
+  if (!ring || !nccl_comm || !out) return fail(CFTFT_INVALID_PARAMS, "bad distributed context arguments");
+  auto& n = dist::nccl();
+  if (!n.ok() || !n.CommCount || !n.CommUserRank) return fail(CFTFT_UNSUPPORTED, "libnccl.so.2 not found");
+  auto d = std::make_unique<cftft_dist>();
+  d->ring = ring;
+  d->comm = static_cast<ncclComm_t>(nccl_comm);
+  NCCL_TRY(n.CommCount(d->comm, &d->world));
+  NCCL_TRY(n.CommUserRank(d->comm, &d->rank));
+  CUDA_TRY(cudaGetDevice(&d->device));
+  *out = d.release();
+  return CFTFT_OK;
+}
+
+void cftft_dist_destroy(cftft_dist* d) {
+  if (!d) return;
+  if (d->owns && d->comm && dist::nccl().CommDestroy) dist::nccl().CommDestroy(d->comm);
+  delete d;
+}
+
+int cftft_dist_geometry(const cftft_dist* d, const cftft_params* p, int inverse, int policy, uint64_t* out) {
+  if (!d || !p || !out) return fail(CFTFT_INVALID_PARAMS, "null argument");
+  if (int rc = validate(d->ring, inverse != 0, p, policy)) return rc;
+  const dist::Geometry g(d->ring->M, p->length, p->input_count, p->output_count, (u64)d->world, policy,
+                         inverse != 0, inverse ? p->want_next : 0);
+  const u64 r = (u64)d->rank;
+  const u64 v[8] = {g.c0[r], g.c1[r], g.r0[r], g.r1[r], g.L1, g.L2, g.L1 * g.width(r), g.nrows(r) * g.L2};
+  std::memcpy(out, v, sizeof v);
+  return CFTFT_OK;
+}
+
+int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab, void* rowslab,
+                       uint64_t esb, int policy, void* stream) {
+  if (int rc = check_dist(d, p, 0, policy, esb)) return rc;
+  auto& nc = dist::nccl();
+  auto st = static_cast<cudaStream_t>(stream);
+  const cftft_ring* R = d->ring;
+  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, false, 0);
+  const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me), nr = g.nrows(me);
+  const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
+  // 1. column TFTs (transform.hpp:175-180)
+  std::vector<cftft_subtransform> v;
+  for (u64 c = 0; c < W; ++c) {
+    const u64 u = g.c0[me] + c;
+    if (u >= g.z2e) continue;
+    v.push_back(sub(g.L1, (s + u * g.col_step) & (R->M - 1), u < g.z2 ? g.z1 + 1 : g.z1, g.n1c, 0, c, W));
+  }
+  if (int rc = run_subs(d, 0, v, colslab, esb, policy, st)) return rc;
+  // 2. transpose: rows R_q of my columns to rank q (contiguous in the column slab)
+  std::vector<u64> qoff(P), qc0(P), qw(P);
+  u64 tot = 0;
+  for (u64 q = 0; q < P; ++q) {
+    qoff[q] = tot;
+    qc0[q] = g.c0[q];
+    qw[q] = g.width(q);
+    tot += nr * g.width(q);
+  }
+  std::uint8_t* recv = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&recv, std::max<u64>(1, tot) * esb, st));
+  NCCL_TRY(nc.GroupStart());
+  for (u64 q = 0; q < P; ++q) {
+    const u64 cnt_s = g.nrows(q) * W * esb, cnt_r = nr * g.width(q) * esb;
+    if (cnt_s)
+      NCCL_TRY(nc.Send(static_cast<std::uint8_t*>(colslab) + g.r0[q] * W * esb, cnt_s, ncclUint8, (int)q, d->comm, st));
+    if (cnt_r) NCCL_TRY(nc.Recv(recv + qoff[q] * esb, cnt_r, ncclUint8, (int)q, d->comm, st));
+  }
+  NCCL_TRY(nc.GroupEnd());
+  // 3. unpack into the row slab, row TFTs (transform.hpp:182-185)
+  if (nr) {
+    std::vector<u64> tab(qoff);
+    tab.insert(tab.end(), qc0.begin(), qc0.end());
+    tab.insert(tab.end(), qw.begin(), qw.end());
+    u64* dt = nullptr;
+    if (int rc = dev_table(tab, &dt, st)) return rc;
+    dist::unpack_rows_kernel<<<(unsigned)(nr * P), 256, 0, st>>>(static_cast<std::uint8_t*>(rowslab), recv, esb, nr,
+                                                                  g.L2, dt, dt + P, dt + 2 * P, (u32)P);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(dt, st));
+  }
+  CUDA_TRY(cudaFreeAsync(recv, st));
+  v.clear();
+  for (u64 u = g.r0[me]; u < g.r1[me]; ++u)
+    v.push_back(sub(g.L2, s_row, g.z2e, u < g.n1 ? g.L2 : g.n2, 0, (u - g.r0[me]) * g.L2, 1));
+  return run_subs(d, 0, v, rowslab, esb, policy, st);
+}
+
+int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowslab, void* colslab,
+                        uint64_t esb, int policy, void* stream) {
+  if (int rc = check_dist(d, p, 1, policy, esb)) return rc;
+  auto& nc = dist::nccl();
+  auto st = static_cast<cudaStream_t>(stream);
+  const cftft_ring* R = d->ring;
+  const int f = p->want_next;
+  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, true, f);
+  const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me);
+  const u64 r0 = g.r0[me], r1 = g.r1[me], c0 = g.c0[me];
+  const u64 n1 = g.n1, n2 = g.n2, z1 = g.z1, z2e = g.z2e;
+  const u64 fm = (n2 + (u64)f) > 0 ? 1 : 0, lo = std::min(n2, g.z2), hi = std::max(n2, g.z2);
+  const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
+  auto* rs = static_cast<std::uint8_t*>(rowslab);
+  auto* cs = static_cast<std::uint8_t*>(colslab);
+  // i. full rows u < n1 (transform.hpp:215-216)
+  std::vector<cftft_subtransform> v;
+  for (u64 u = r0; u < std::min(r1, n1); ++u) v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
+  if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
+  // rows [0, zrows) to the column owners: my rows' columns [c0_q, c1_q) packed
+  // per destination; rank q's rows arrive in global row order, straight into
+  // the column slab (rows [0, zrows) of it)
+  {
+    const u64 mine = r0 < g.zrows ? std::min(r1, g.zrows) - r0 : 0;
+    std::vector<u64> qoff(P), qc0(P), qw(P);
+    u64 tot = 0;
+    for (u64 q = 0; q < P; ++q) {
+      qoff[q] = tot;
+      qc0[q] = g.c0[q];
+      qw[q] = g.width(q);
+      tot += mine * g.width(q);
+    }
+    std::uint8_t* send = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&send, std::max<u64>(1, tot) * esb, st));
+    if (mine) {
+      std::vector<u64> tab(qoff);
+      tab.insert(tab.end(), qc0.begin(), qc0.end());
+      tab.insert(tab.end(), qw.begin(), qw.end());
+      u64* dt = nullptr;
+      if (int rc = dev_table(tab, &dt, st)) return rc;
+      dist::pack_rows_kernel<<<(unsigned)(mine * P), 256, 0, st>>>(send, rs, esb, mine, g.L2, dt, dt + P, dt + 2 * P,
+                                                                    (u32)P);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaFreeAsync(dt, st));
+    }
+    NCCL_TRY(nc.GroupStart());
+    for (u64 q = 0; q < P; ++q) {
+      const u64 cnt_s = mine * g.width(q) * esb;
+      const u64 qa = g.r0[q], qb = std::min(g.r1[q], g.zrows);
+      const u64 cnt_r = (qb > qa ? qb - qa : 0) * W * esb;
+      if (cnt_s) NCCL_TRY(nc.Send(send + qoff[q] * esb, cnt_s, ncclUint8, (int)q, d->comm, st));
+      if (cnt_r) NCCL_TRY(nc.Recv(cs + qa * W * esb, cnt_r, ncclUint8, (int)q, d->comm, st));
+    }
+    NCCL_TRY(nc.GroupEnd());
+    CUDA_TRY(cudaFreeAsync(send, st));
+  }
+  // ii. right columns [n2, z2') (transform.hpp:219-224)
+  v.clear();
+  for (u64 c = 0; c < W; ++c) {
+    const u64 u = c0 + c;
+    if (n2 <= u && u < z2e)
+      v.push_back(sub(g.L1, (s + u * g.col_step) & (R->M - 1), u < hi ? z1 + 1 : z1, n1, (int)fm, c, W));
+  }
+  if (int rc = run_subs(d, 1, v, colslab, esb, policy, st)) return rc;
+  // iii. row n1 (transform.hpp:227-230): gather, transform on its owner, scatter
+  if (fm) {
+    u64 owner = 0;
+    for (u64 q = 0; q < P; ++q)
+      if (g.r0[q] <= n1 && n1 < g.r1[q]) owner = q;
+    std::uint8_t* row = me == owner ? rs + (n1 - g.r0[owner]) * g.L2 * esb : nullptr;
+    NCCL_TRY(nc.GroupStart());
+    {
+      const u64 a = std::max(n2, c0), b = std::min(z2e, g.c1[me]);
+      if (b > a) {
+        if (me == owner) {
+          CUDA_TRY(cudaMemcpyAsync(row + a * esb, cs + (n1 * W + (a - c0)) * esb, (b - a) * esb,
+                                   cudaMemcpyDeviceToDevice, st));
+        } else {
+          NCCL_TRY(nc.Send(cs + (n1 * W + (a - c0)) * esb, (b - a) * esb, ncclUint8, (int)owner, d->comm, st));
+        }
+      }
+      if (me == owner)
+        for (u64 q = 0; q < P; ++q) {
+          const u64 aa = std::max(n2, g.c0[q]), bb = std::min(z2e, g.c1[q]);
+          if (q != me && bb > aa) NCCL_TRY(nc.Recv(row + aa * esb, (bb - aa) * esb, ncclUint8, (int)q, d->comm, st));
+        }
+    }
+    NCCL_TRY(nc.GroupEnd());
+    if (me == owner) {
+      v.assign(1, sub(g.L2, s_row, z2e, n2, f, (n1 - g.r0[owner]) * g.L2, 1));
+      if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
+    }
+    const u64 outs = n2 + (u64)f;
+    NCCL_TRY(nc.GroupStart());
+    {
+      const u64 aa = c0, bb = std::min(outs, g.c1[me]);
+      if (bb > aa) {
+        if (me == owner) {
+          CUDA_TRY(cudaMemcpyAsync(cs + n1 * W * esb, row + aa * esb, (bb - aa) * esb, cudaMemcpyDeviceToDevice, st));
+        } else {
+          NCCL_TRY(nc.Recv(cs + n1 * W * esb, (bb - aa) * esb, ncclUint8, (int)owner, d->comm, st));
+        }
+      }
+      if (me == owner)
+        for (u64 q = 0; q < P; ++q) {
+          const u64 qa = g.c0[q], qb = std::min(outs, g.c1[q]);
+          if (q != me && qb > qa) NCCL_TRY(nc.Send(row + qa * esb, (qb - qa) * esb, ncclUint8, (int)q, d->comm, st));
+        }
+    }
+    NCCL_TRY(nc.GroupEnd());
+  }
+  // iv. left columns [0, n2) (transform.hpp:233-238)
+  v.clear();
+  for (u64 c = 0; c < W; ++c) {
+    const u64 u = c0 + c;
+    if (u < n2) v.push_back(sub(g.L1, (s + u * g.col_step) & (R->M - 1), u < lo ? z1 + 1 : z1, n1 + 1, 0, c, W));
+  }
+  return run_subs(d, 1, v, colslab, esb, policy, st);
+}

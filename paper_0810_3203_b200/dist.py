@@ -306,3 +306,85 @@ class DistTFT:
         dist.all_to_all_single(recv, send.contiguous(), recv_splits, send_splits, group=self.group)
         if bb > aa:
             colslab[n1 * W + (aa - c0): n1 * W + (bb - c0)] = recv
+
+
+# ---------------------------------------------------------------------------
+# The native path: the same partition in the library (csrc/dist.cuh) over an
+# NCCL communicator of its own (cftft_gpu_dist_tft / cftft_gpu_dist_itft).
+
+
+class NcclDist:
+    """A distributed context of the C ABI for the current torch.distributed
+    group: rank 0 makes an NCCL unique id, the group broadcasts it, every rank
+    joins the library's communicator on its current CUDA device."""
+
+    def __init__(self, ctx, group=None, policy: int = 0):
+        import ctypes as C
+
+        from . import _check, lib
+
+        self.ctx, self.policy = ctx, policy
+        L = lib()
+        vp = C.c_void_p
+        if not getattr(L, "_dist_bound", False):
+            L.cftft_nccl_unique_id.argtypes = [vp]
+            L.cftft_dist_create.argtypes = [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]
+            L.cftft_dist_destroy.argtypes = [vp]
+            L.cftft_dist_destroy.restype = None
+            L.cftft_dist_geometry.argtypes = [vp, vp, C.c_int, C.c_int, C.POINTER(C.c_uint64)]
+            for fn in ("cftft_gpu_dist_tft", "cftft_gpu_dist_itft"):
+                getattr(L, fn).argtypes = [vp, vp, vp, vp, C.c_uint64, C.c_int, vp]
+            L._dist_bound = True
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        idbuf = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            _check(L.cftft_nccl_unique_id(C.cast(idbuf, vp)))
+        t = torch.tensor(list(idbuf), dtype=torch.uint8,
+                         device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        for i, b in enumerate(t.cpu().tolist()):
+            idbuf[i] = b
+        h = vp()
+        _check(L.cftft_dist_create(ctx._h, self.rank, self.world, C.cast(idbuf, vp), C.byref(h)))
+        self._h = h
+        self.launches = 0
+
+    def __del__(self):
+        try:
+            from . import lib
+
+            lib().cftft_dist_destroy(self._h)
+        except Exception:
+            pass
+
+    def geometry(self, params, inverse: bool = False) -> dict:
+        """{c0, c1, r0, r1, L1, L2, col_elems, row_elems} of this rank."""
+        import ctypes as C
+
+        from . import _check, _params, lib
+
+        p = _params(params)
+        out = (C.c_uint64 * 8)()
+        _check(lib().cftft_dist_geometry(self._h, C.byref(p), 1 if inverse else 0, self.policy, out))
+        return dict(zip(("c0", "c1", "r0", "r1", "L1", "L2", "col_elems", "row_elems"), list(out)))
+
+    def tft(self, params, colslab: torch.Tensor, rowslab: torch.Tensor, stream=None) -> None:
+        import ctypes as C
+
+        from . import _check, _params, _stream_ptr, lib
+
+        p = _params(params)
+        _check(lib().cftft_gpu_dist_tft(self._h, C.byref(p), C.c_void_p(colslab.data_ptr()),
+                                        C.c_void_p(rowslab.data_ptr()), colslab.shape[1] * 8, self.policy,
+                                        C.c_void_p(_stream_ptr(stream))))
+
+    def itft(self, params, rowslab: torch.Tensor, colslab: torch.Tensor, stream=None) -> None:
+        import ctypes as C
+
+        from . import _check, _params, _stream_ptr, lib
+
+        p = _params(params)
+        _check(lib().cftft_gpu_dist_itft(self._h, C.byref(p), C.c_void_p(rowslab.data_ptr()),
+                                         C.c_void_p(colslab.data_ptr()), rowslab.shape[1] * 8, self.policy,
+                                         C.c_void_p(_stream_ptr(stream))))

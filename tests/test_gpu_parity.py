@@ -256,6 +256,79 @@ def test_dist_path_on_one_gpu():
             dist.destroy_process_group()
 
 
+def _nccl_group():
+    import socket
+
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+
+
+def test_native_dist_path_on_one_gpu():
+    """cftft_gpu_dist_tft / _itft (the C ABI's multi-GPU transforms over the
+    library's own NCCL communicator) on a one-rank group: the column slab is
+    the whole row-major array, the row slab its first rows; bit-exact against
+    the oracle (TFT) and the single-GPU transform (ITFT with f = 1), and the
+    C5 round trip."""
+    import torch.distributed as dist
+
+    from paper_0810_3203_b200.dist import NcclDist
+
+    try:
+        _nccl_group()
+        for N, L, z, n in ((4096, 4096, 3000, 3100), (32768, 1 << 16, 40000, 40000)):
+            ctx = cf.FermatRingCtx(N)
+            ring = po.Ring.fermat(N)
+            W = ctx.element_words
+            lim = N // 64
+            nd = NcclDist(ctx)
+            full = fermat_inputs(N, L, z, W, 78)
+            full[z:] = 0
+            want = full.copy()
+            ring.tft(want, L, 0, z, n, threads=8)
+            geo = nd.geometry(cf.TransformParams(L, 0, z, n))
+            assert geo["c0"] == 0 and geo["c1"] == geo["L2"] and geo["L1"] * geo["L2"] == L
+            col = to_dev(full)
+            rows = torch.zeros((geo["row_elems"], W), dtype=torch.int64, device="cuda")
+            nd.tft(cf.TransformParams(L, 0, z, n), col, rows)
+            got = from_dev(rows)
+            assert np.array_equal(got[:n, : lim + 1], want[:n, : lim + 1]), (N, L, z, n)
+            # ITFT (z, n - 1, f = 1) vs the single-GPU engine on the same inputs
+            ni = n - 1
+            gi = nd.geometry(cf.TransformParams(L, 0, n, ni, 1), inverse=True)
+            rin = torch.zeros((gi["row_elems"], W), dtype=torch.int64, device="cuda")
+            rin[: min(gi["row_elems"], rows.shape[0])] = rows[: min(gi["row_elems"], rows.shape[0])]
+            back = torch.zeros_like(col)
+            nd.itft(cf.TransformParams(L, 0, n, ni, 1), rin, back)
+            ref = torch.zeros_like(col)
+            ref[: rows.shape[0]] = rows
+            cf.cf_itft(ctx, cf.TransformParams(L, 0, n, ni, 1), cf.DeviceView(ref))
+            assert np.array_equal(from_dev(back)[: ni + 1, : lim + 1], from_dev(ref)[: ni + 1, : lim + 1])
+        # C5 round trip through the native path
+        N, L, z = 131072, 1 << 18, 200000
+        ctx = cf.FermatRingCtx(N)
+        W, lim = ctx.element_words, N // 64
+        nd = NcclDist(ctx)
+        a = fermat_inputs(N, L, z, W, 5)
+        a[z:] = 0
+        col = to_dev(a)
+        geo = nd.geometry(cf.TransformParams(L, 0, z, z))
+        rows = torch.empty((geo["row_elems"], W), dtype=torch.int64, device="cuda")
+        nd.tft(cf.TransformParams(L, 0, z, z), col, rows)
+        nd.itft(cf.TransformParams(L, 0, z, z, 0), rows, col)
+        cf.scale(ctx, cf.DeviceView(col), z, 2 * N - 18)
+        assert np.array_equal(from_dev(col)[:z, : lim + 1], a[:z, : lim + 1])
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
 # ---- coset leaves (carry-save lanes) ---------------------------------------------
 
 @pytest.mark.parametrize("N,cw", [(1024, 4), (2048, 8), (4096, 4), (8192, 16)])
