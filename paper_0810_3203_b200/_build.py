@@ -83,3 +83,23 @@ def build_api_test(force: bool = False) -> str:
         raise RuntimeError("api_test build failed:\n" + r.stdout + r.stderr)
     os.replace(API_TEST + ".tmp", API_TEST)
     return API_TEST
+
+
+CLI_SRC = os.path.join(PKG, "cli", "cftft_cli.cpp")
+CLI = os.path.join(LIBDIR, "cftft")
+
+
+def build_cli(force: bool = False) -> str:
+    """The command-line workbench (cli/cftft_cli.cpp: verify / count / bench /
+    compare, the reference CLI's contract), linked against the in-tree
+    library with an $ORIGIN rpath."""
+    if not force and os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(CLI_SRC),
+                                                                          os.path.getmtime(LIB)):
+        return CLI
+    cmd = [_nvcc(), "-std=c++17", "-O2", "-o", CLI + ".tmp", CLI_SRC, "-L", LIBDIR, "-lcftft_b200",
+           "-Xlinker", "-rpath=$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("cli build failed:\n" + r.stdout + r.stderr)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI

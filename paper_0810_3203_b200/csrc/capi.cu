@@ -1021,7 +1021,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
 
 // fault::corrupt_tft_base on the GPU: element 0 += 1 in the ring (Fermat:
 // N/64 limbs + top word, canonical; negacyclic: word 0 mod m; prime: mod p)
-__global__ void fault_add_one_kernel(std::uint8_t* el, int kind, u64 words, u64 m) {
+__device__ void fault_add_one_kernel_body(std::uint8_t* el, int kind, u64 words, u64 m) {
   u64* w = reinterpret_cast<u64*>(el);
   if (kind == CFTFT_RING_FERMAT) {
     const u64 limbs = words / 2;  // words = D (u32 words)
@@ -1035,6 +1035,15 @@ __global__ void fault_add_one_kernel(std::uint8_t* el, int kind, u64 words, u64 
   } else {
     w[0] = (w[0] + 1 == m) ? 0 : w[0] + 1;
   }
+}
+
+__global__ void fault_add_one_kernel(std::uint8_t* el, int kind, u64 words, u64 m) {
+  fault_add_one_kernel_body(el, kind, words, m);
+}
+__global__ void fault_add_one_items_kernel(std::uint8_t* base, u64 esb, const u64* idx, u64 count, int kind,
+                                           u64 words, u64 m) {
+  const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  if (i < count) fault_add_one_kernel_body(base + idx[i] * esb, kind, words, m);
 }
 
 int transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* dev_base, u64 stride,
@@ -1744,8 +1753,32 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
     }
   }
   int rc = launch_plan(R, *dp, static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, st, false);
+  if (rc) return rc;
+  if (!inverse && g_fault.load()) {
+    // fault::corrupt_tft_base: every forward sub-transform's x[0] += 1
+    std::vector<u64> idx(count);
+    for (u64 k = 0; k < count; ++k) idx[k] = v[k].base;
+    u64* di = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&di, count * 8, st));
+    CUDA_TRY(cudaMemcpyAsync(di, idx.data(), count * 8, cudaMemcpyHostToDevice, st));
+    // (batch outputs of whole-leaf plans are canonicalised first below)
+    if (canonicalize && R->kind == CFTFT_RING_FERMAT && !dp->host.coset) {
+      for (u64 k = 0; k < count; ++k) {
+        const u64 outs = v[k].n + (u64)v[k].f;
+        std::uint8_t* b = static_cast<std::uint8_t*>(dev_base) + v[k].base * elem_stride_bytes;
+        fermat::canonicalize_kernel<<<(unsigned)((outs + 255) / 256), 256, 0, st>>>(
+            b, elem_stride_bytes * v[k].stride, outs, R->D);
+      }
+    }
+    fault_add_one_items_kernel<<<(unsigned)((count + 127) / 128), 128, 0, st>>>(
+        static_cast<std::uint8_t*>(dev_base), elem_stride_bytes, di, count, R->kind,
+        R->kind == CFTFT_RING_NEGACYCLIC ? R->K : (u64)R->D, R->m);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(di, st));
+    return CFTFT_OK;
+  }
   // coset plans end in the carry-save fold: their outputs are canonical already
-  if (rc || !canonicalize || R->kind != CFTFT_RING_FERMAT || dp->host.coset) return rc;
+  if (!canonicalize || R->kind != CFTFT_RING_FERMAT || dp->host.coset) return rc;
   for (u64 k = 0; k < count; ++k) {
     const u64 outs = v[k].n + (u64)v[k].f;
     std::uint8_t* b = static_cast<std::uint8_t*>(dev_base) + v[k].base * elem_stride_bytes;
