@@ -483,6 +483,11 @@ RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp, bool allow_wide =
       rs.coset_max_ell = cl;
       if (!cl) rs.lane_bits = 0;
     }
+    // whole-coefficient plans (small N): leaves of <= 64 coefficients, so the
+    // Bailey phases spread over many CTAs instead of one CTA walking every
+    // level of a transform that happens to fit its shared memory (C1: TFT +
+    // ITFT 256 -> 163 us)
+    if (!rs.lane_bits && !R->leaf_limit) rs.max_leaf_ell = std::min(rs.max_leaf_ell, 6u);
   }
   rs.C = C;
   rs.slot_bytes = sb;
