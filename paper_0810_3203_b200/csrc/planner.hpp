@@ -969,7 +969,20 @@ class Planner {
     if (coset_fits(ell)) {
       const ClassKey key{inv ? 1 : 0, ell, z, n, f, 1};
       const LeafProgram& prog = coset_program(key, policy);
-      if (aligned(prog, inv, ell, lf)) {
+      // a 64-coefficient ITFT leaf that is not a full network (the truncated
+      // phase-iii row's parts) would run its micro-ops on the CTA kernel, an
+      // order of magnitude slower per byte than the radix-8 warp waves: cut
+      // it into radix-8 leaves instead
+      bool take = aligned(prog, inv, ell, lf);
+      if (take && inv && ell == 6 && rs_.wide) {
+        auto it = full_net_.find(key);
+        if (it == full_net_.end()) {
+          std::vector<u32> net;
+          it = full_net_.emplace(key, wide_network(prog, rs_.M, net) != 0).first;
+        }
+        take = it->second;
+      }
+      if (take) {
         units = emit_coset(key, policy, base, stride, cx, wave0, lf);
         return true;
       }
@@ -1385,6 +1398,7 @@ class Planner {
   std::map<ClassKey, u32> class_index_;
   std::map<ClassKey, LeafProgram> progs_;
   std::map<ClassKey, LeafProgram> lin_progs_;  // coset_program
+  std::map<ClassKey, bool> full_net_;          // try_leaf: the class is a full radix-64 network
   std::vector<LeafProgram> classes_;
   std::vector<DevLeaf> leaves_;
   std::vector<Key> keys_;
