@@ -309,13 +309,20 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     if (wr[2] != 2 || !wr[1]) continue;
     bool ok = true;
     u32 step = 0, wnet = 0;
+    auto is_prog = [&](u32 ci) {
+      return cls[ci].wnet == 0 && ci < p.wave_prog.size() && p.wave_prog[ci] != kNoDep;
+    };
     for (u64 i = wr[0]; i < wr[0] + wr[1] && ok; ++i) {
-      const DevClass& d = cls[p.leaves[i].cls];
-      ok = d.L == 64 && (d.wnet == 1 || d.wnet == 2) && d.kind == 1 && d.step >= 2 && (d.step & (d.step - 1)) == 0 &&
-           (step == 0 || d.step == step) && wr[3] == d.step && (wnet == 0 || d.wnet == wnet);
-      wnet = d.wnet;
+      const u32 ci = p.leaves[i].cls;
+      const DevClass& d = cls[ci];
+      const bool prog = is_prog(ci);
+      ok = d.L == 64 && (d.wnet == 1 || d.wnet == 2 || prog) && d.kind == 1 && d.step >= 2 &&
+           (d.step & (d.step - 1)) == 0 && (step == 0 || d.step == step) && wr[3] == d.step &&
+           (prog || wnet == 0 || d.wnet == wnet);
       step = d.step;
       if (!ok) break;
+      if (prog) continue;  // phase programs run in either kernel
+      wnet = d.wnet;
       const u32 mask = d.wnet == 1 ? fermat::kRotDif : fermat::kRotDit;
       for (u32 o = 0; o < 192 && ok; ++o) {
         const u32 wop = p.wave_ops[d.wop_begin + o];
@@ -324,19 +331,23 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
       }
     }
     if (!ok) continue;
-    dp.tma_wave[w] = (std::uint8_t)wnet;
+    // bits 0-1: the kernel's network kind (programs only: DIT); bit 2: phase programs
+    bool any_prog = false;
+    for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) any_prog = any_prog || is_prog(p.leaves[i].cls);
+    dp.tma_wave[w] = (std::uint8_t)((wnet ? wnet : 2u) | (any_prog ? 4u : 0u));
     dp.tma_step = step;
     dp.tma_desc_off[w] = descs.size();
     for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
       const DevLeaf& lf = p.leaves[i];
       const DevClass& d = cls[lf.cls];
+      const bool prog = is_prog(lf.cls);
       fermat::TmaLeafDesc td{};
       td.base = lf.base;
       td.stride = lf.stride;
       td.c0 = lf.c0;
-      td.wop_begin = d.wop_begin;
+      td.wop_begin = prog ? p.wave_prog[lf.cls] : d.wop_begin;
       td.nload = d.nload;
-      td.nstore_wnet = d.nstore | (d.wnet << 16);
+      td.nstore_wnet = d.nstore | ((prog ? 3u : d.wnet) << 16);
       descs.push_back(td);
     }
   }
@@ -877,8 +888,10 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
               if (int e = make_coset_map(&tm_shadow, shadow ? (void*)shadow : (void*)base, stride, dp.host.extent,
                                          dp.tma_step))
                 return e;
-              if (int e = set_smem_bytes(fermat::coset_tma_kernel<true>, fermat::kTmaSmem)) return e;
-              if (int e = set_smem_bytes(fermat::coset_tma_kernel<false>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<true, false>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<false, false>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<true, true>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<false, true>, fermat::kTmaSmem)) return e;
               tma_maps = true;
             }
             W.leaves = dp.leaves + wr[0];
@@ -888,10 +901,20 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.tlay = dp.tma_lay;
             W.pfdist = 0;
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
-            if (dp.tma_wave[wi] == 1)
-              fermat::coset_tma_kernel<true><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
-            else
-              fermat::coset_tma_kernel<false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+            switch (dp.tma_wave[wi]) {
+              case 1:
+                fermat::coset_tma_kernel<true, false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                break;
+              case 2:
+                fermat::coset_tma_kernel<false, false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                break;
+              case 5:
+                fermat::coset_tma_kernel<true, true><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                break;
+              default:
+                fermat::coset_tma_kernel<false, true><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                break;
+            }
           } else if (wr[2] == 2) {
             W.leaves = dp.leaves + wr[0];
             W.nleaves = (u32)wr[1];

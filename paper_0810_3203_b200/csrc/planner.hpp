@@ -192,6 +192,9 @@ struct Plan {
   std::vector<u32> wave_ops;
   std::vector<u32> wave_op_begin;  // per class
   std::vector<u32> wave_net;       // per class, DevClass::wnet
+  // per class: its TMA phase program in wave_ops (Planner::tma_program), or
+  // kNoDep (64-slot classes that are not full networks)
+  std::vector<u32> wave_prog;
   // wave engine, coset tickets: per slot {pre bits | fresh << 30 | in-buffer << 31,
   // post lanes | final output << 30 | out-buffer << 31}, at DevLeaf::c0 (reused as the offset);
   // fresh: the element was never written by the plan before (its tops are zero, not loaded);
@@ -236,6 +239,9 @@ struct RingShape {
   // run on the CTA kernel (csrc/wave_wide.cuh); the top-level split leaves
   // row nodes of 2^(6k) coefficients (three radix-64 passes at L = 2^18)
   bool wide = false;
+  // 64-slot ITFT classes that are not full networks stay radix-64 leaves when
+  // they have a phase program (the TMA kernel runs them in one pass)
+  bool tma_programs = true;
 };
 
 // Fermat shared-memory slot: cs chunks of lane_bytes, an int32 top per chunk,
@@ -428,6 +434,7 @@ class Planner {
     p.wave_ops.clear();
     p.wave_op_begin.assign(classes_.size(), 0);
     p.wave_net.assign(classes_.size(), 0);
+    p.wave_prog.assign(classes_.size(), kNoDep);
     for (size_t c = 0; c < classes_.size(); ++c) {
       const LeafProgram& cl = classes_[c];
       p.wave_op_begin[c] = (u32)p.wave_ops.size();
@@ -447,6 +454,11 @@ class Planner {
       for (const auto& op : cl.ops) {
         const u64 q = op.type == OP_COPY ? 0 : (op.r / lb) / cl.step;
         p.wave_ops.push_back((u32)op.type | ((u32)op.a << 4) | ((u32)op.b << 10) | ((u32)q << 16));
+      }
+      std::vector<u32> prog;
+      if (cl.key.ell == 6 && tma_program(cl, lb, prog)) {
+        p.wave_prog[c] = (u32)p.wave_ops.size();
+        p.wave_ops.insert(p.wave_ops.end(), prog.begin(), prog.end());
       }
     }
     p.wave_slots.clear();
@@ -616,6 +628,112 @@ class Planner {
       return kind;
     }
     return 0;
+  }
+
+  // A 64-slot coset class that is not a full network (the truncated ITFT
+  // leaves: the reference's phases i..iv over an 8 x 8 grid, slot 8r + c,
+  // transform.hpp:215-238) as a phase program for the TMA kernel's warp
+  // groups (wave_tma.cuh, prog_ops): each op lies inside one row or one
+  // column of the grid; in a row phase warp w runs the ops of row w, in a
+  // column phase those of column w, in level order; a phase starts when the
+  // previous one is done on every warp.  Phases alternate row / column; an
+  // op goes to the first phase of its kind after the phases of every earlier
+  // op on its slots (the same phase when that op is of its kind: then it is
+  // the same warp's).  Layout: word 0 = phase count P | network rows << 8,
+  // words 1 + 8p + w = (first op << 16) | op count of warp w in phase p
+  // (offsets from word 0), words 1 + 8P + 12w: row w's network ops, then the
+  // ops packed as in wave_ops (bit 22: runs paired with the next op).  Returns false when an op spans rows
+  // and columns, reads a slot nothing has defined (slots >= nload are never
+  // loaded), or needs more than 8 phases.
+  static bool tma_program(const LeafProgram& cl, u64 lane_bits, std::vector<u32>& out) {
+    if (cl.key.ell != 6 || cl.kind != 1 || cl.nload == 0 || cl.ops.empty()) return false;
+    constexpr int kMaxPhases = 8;
+    std::array<int, 64> lastp;  // phase of the last op on the slot (-1: none)
+    lastp.fill(-1);
+    std::array<bool, 64> defined{};
+    for (u32 k = 0; k < 64; ++k) defined[k] = k < cl.nload;
+    const int t0 = (cl.ops[0].a % 8 != cl.ops[0].b % 8) ? 0 : 1;  // kind of phase 0 (0 rows, 1 columns)
+    std::vector<std::array<std::vector<u32>, 8>> ph;
+    for (const DevOp& op : cl.ops) {
+      const u32 a = op.a, b = op.b;
+      if (a >= 64 || b >= 64) return false;
+      int kind;
+      if (a == b && (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF || op.type == OP_COPY)) return false;
+      if (a == b)  // a <- a +- R(a): either kind; stay in the slot's last phase
+        kind = lastp[a] < 0 ? t0 : (((lastp[a] & 1) == 0) ? t0 : 1 - t0);
+      else if (a / 8 == b / 8)
+        kind = 0;
+      else if (a % 8 == b % 8)
+        kind = 1;
+      else
+        return false;
+      if (!defined[a] || (op.type != OP_COPY && !defined[b])) return false;
+      if (op.type != OP_COPY && op.type != OP_ADDSUB && op.type != OP_ADD && op.type != OP_SUB2 &&
+          op.type != OP_SUB2DIFF)
+        return false;
+      const u32 owner = kind == 0 ? a / 8 : a % 8;
+      int p = (kind == t0) ? 0 : 1;
+      for (u32 s : {a, b}) {
+        if (lastp[s] < 0) continue;
+        const int q = lastp[s];
+        const int qk = ((q & 1) == 0) ? t0 : 1 - t0;
+        const int need = qk == kind ? q : q + 1;
+        while (p < need) p += 2;
+      }
+      if (p >= kMaxPhases) return false;
+      if ((int)ph.size() <= p) ph.resize(p + 1);
+      const u64 q = op.type == OP_COPY ? 0 : (op.r / lane_bits) / cl.step;
+      ph[p][owner].push_back((u32)op.type | (a << 4) | (b << 10) | ((u32)q << 16));
+      lastp[a] = lastp[b] = p;
+      defined[b] = defined[b] || op.type == OP_ADDSUB || op.type == OP_SUB2DIFF || op.type == OP_COPY;
+    }
+    for (u32 k = 0; k < cl.nstore; ++k)
+      if (!defined[k]) return false;
+    const u32 P = (u32)ph.size();
+    // phase 0 rows that are full 8-point DIT networks (the ITFT's phase i) run
+    // in registers on the DIT kernel (stage_a: ADDSUB on the network's pairs,
+    // rotations only where kRotDit has them); their ops stay in the list for
+    // the DIF kernel
+    static const u32 pr[12][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}, {0, 2}, {1, 3},
+                                  {4, 6}, {5, 7}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
+    constexpr u32 kRotDitMask = (1u << 5) | (1u << 7) | (1u << 9) | (1u << 10) | (1u << 11);
+    u32 netmask = 0;
+    for (u32 w = 0; w < 8 && t0 == 0 && P > 0; ++w) {
+      const auto& v = ph[0][w];
+      bool net = v.size() == 12;
+      for (u32 j = 0; j < 12 && net; ++j) {
+        const u32 wop = v[j];
+        net = (wop & 15u) == OP_ADDSUB && ((wop >> 4) & 63u) == 8 * w + pr[j][0] &&
+              ((wop >> 10) & 63u) == 8 * w + pr[j][1] && (((kRotDitMask >> j) & 1u) || (wop >> 16) == 0);
+      }
+      if (net) netmask |= 1u << w;
+    }
+    // pairs: an ADDSUB followed by an ADDSUB on other slots (bit 22 on the
+    // first) run together (two independent carry chains), within a 32-op chunk
+    for (auto& phase : ph)
+      for (auto& v : phase)
+        for (size_t k = 0; k + 1 < v.size();) {
+          const u32 x = v[k], y = v[k + 1];
+          const u32 xa = (x >> 4) & 63u, xb = (x >> 10) & 63u, ya = (y >> 4) & 63u, yb = (y >> 10) & 63u;
+          if ((k & 31) != 31 && (x & 15u) == OP_ADDSUB && (y & 15u) == OP_ADDSUB && xa != ya && xa != yb &&
+              xb != ya && xb != yb) {
+            v[k] |= 1u << 22;
+            k += 2;
+          } else {
+            k += 1;
+          }
+        }
+    out.assign(1 + 8 * P + 96, 0);
+    out[0] = P | (netmask << 8);
+    for (u32 w = 0; w < 8; ++w)
+      if ((netmask >> w) & 1u)
+        for (u32 j = 0; j < 12; ++j) out[1 + 8 * P + 12 * w + j] = ph[0][w][j] & ~(1u << 22);
+    for (u32 p = 0; p < P; ++p)
+      for (u32 w = 0; w < 8; ++w) {
+        out[1 + 8 * p + w] = ((u32)out.size() << 16) | (u32)ph[p][w].size();
+        out.insert(out.end(), ph[p][w].begin(), ph[p][w].end());
+      }
+    return out.size() < 65536;
   }
 
   // 1 / 2: the class runs as the full 8-point network of ADDSUB butterflies
@@ -969,16 +1087,23 @@ class Planner {
     if (coset_fits(ell)) {
       const ClassKey key{inv ? 1 : 0, ell, z, n, f, 1};
       const LeafProgram& prog = coset_program(key, policy);
-      // a 64-coefficient ITFT leaf that is not a full network (the truncated
-      // phase-iii row's parts) would run its micro-ops on the CTA kernel, an
-      // order of magnitude slower per byte than the radix-8 warp waves: cut
-      // it into radix-8 leaves instead
+      // a 64-coefficient ITFT leaf that is neither a full network nor a
+      // phase program for the TMA kernel (tma_program) would run its
+      // micro-ops on the CTA kernel, an order of magnitude slower per byte
+      // than the radix-8 warp waves: cut it into radix-8 leaves instead
       bool take = aligned(prog, inv, ell, lf);
       if (take && inv && ell == 6 && rs_.wide) {
         auto it = full_net_.find(key);
         if (it == full_net_.end()) {
           std::vector<u32> net;
-          it = full_net_.emplace(key, wide_network(prog, rs_.M, net) != 0).first;
+          bool ok = wide_network(prog, rs_.M, net) != 0;
+          if (!ok && rs_.tma_programs) {
+            LeafProgram cp = prog;  // the class's coset geometry (class_of)
+            cp.kind = 1;
+            cp.step = (u32)(lanes2() >> ell);
+            ok = cp.step >= 2 && tma_program(cp, rs_.lane_bits, net);
+          }
+          it = full_net_.emplace(key, ok).first;
         }
         take = it->second;
       }
@@ -1083,8 +1208,69 @@ class Planner {
     const u64 inner = rs_.M >> k.ell;
     bool al = true;
     for (const auto& op : src.ops) al = al && (op.type == OP_COPY || op.r % inner == 0);
-    const bool use = !al && rs_.wave_engine && rs_.wave_unaligned && rs_.fermat && linearize(src, lin);
+    const bool use = !al && rs_.wave_engine && rs_.wave_unaligned && rs_.fermat &&
+                     (linearize(src, lin) || realign(src, lin));
     return lin_progs_.emplace(k, use ? lin : src).first->second;
+  }
+
+  // Sub-unit offsets: the same program with every op rotation a multiple of
+  // the leaf's unit U = M >> ell, when offsets d_k (true value of slot k =
+  // omega^d_k * stored) absorb the rest.  The ITFT's divisions by 2 (omega =
+  // 2 in the Fermat ring, 2^-1 = omega^(M-1)) leave chains such as
+  // x <- 2x - omega^(2U-3) y, x <- 2x - omega^(4U-2) y', ... (the row n1 of
+  // a truncated 64-point ITFT, transform.hpp:227-230): x starts with an
+  // offset of -4 (taken by its load's pre-rotation, any bits on the TMA and
+  // warp kernels) and each step is computed as omega (x - omega^(r-1) y),
+  // raising the offset by one.  Per op, in order: the exact form when it is
+  // aligned; else a slot still holding its loaded value takes the offset
+  // that aligns it (its pre-rotation changes); else SUB2 as the shifted
+  // subtraction.  Loads and stores absorb the offsets (pre - d, post + d).
+  bool realign(const LeafProgram& src, LeafProgram& dst) const {
+    const u64 M = rs_.M, U = M >> src.key.ell, H = M / 2;
+    const u32 L = 1u << src.key.ell;
+    if (U < 2) return false;
+    std::vector<u64> d(L, 0), dload(L, 0);
+    std::vector<char> fresh(L, 0);  // loaded, not yet read or written by an op
+    for (u32 k = 0; k < src.nload; ++k) fresh[k] = 1;
+    dst = src;
+    for (auto& op : dst.ops) {
+      const u32 a = op.a, b = op.b;
+      if (op.type == OP_COPY) {
+        d[b] = d[a];
+        fresh[a] = fresh[b] = 0;
+        continue;
+      }
+      if (op.type != OP_ADD && op.type != OP_ADDSUB && op.type != OP_SUB2 && op.type != OP_SUB2DIFF) return false;
+      u64 rr = (op.r + d[b] - d[a]) & (M - 1);
+      if (rr % U) {
+        if (fresh[a] && a != b) {
+          const u64 m = rr % U;  // d_a += m
+          d[a] = (d[a] + m) & (M - 1);
+          dload[a] = d[a];
+          rr -= m;
+        } else if (fresh[b] && a != b) {
+          const u64 m = rr % U;  // d_b -= m
+          d[b] = (d[b] - m) & (M - 1);
+          dload[b] = d[b];
+          rr -= m;
+        } else if (op.type == OP_SUB2 && ((rr + M - 1) & (M - 1)) % U == 0) {
+          // 2x - R y = omega (x - omega^-1 R y): an ADD of -omega^(r-1) y, offset + 1
+          op.type = OP_ADD;
+          op.r = (rr + M - 1 + H) & (M - 1);
+          d[a] = (d[a] + 1) & (M - 1);
+          fresh[a] = fresh[b] = 0;
+          continue;
+        } else {
+          return false;
+        }
+      }
+      op.r = rr;
+      if (op.type == OP_ADDSUB || op.type == OP_SUB2DIFF) d[b] = d[a];
+      fresh[a] = fresh[b] = 0;
+    }
+    for (u32 k = 0; k < dst.nload; ++k) dst.pre[k].b = (dst.pre[k].b - dload[k]) & (M - 1);
+    for (u32 k = 0; k < dst.nstore; ++k) dst.post[k].b = (dst.post[k].b + d[k]) & (M - 1);
+    return true;
   }
 
   // A one-output program whose output is a sum of +-omega^e multiples of its

@@ -650,10 +650,10 @@ __device__ __forceinline__ void stage_b_load(Ch<8> (&x)[8], int (&tx)[8], u32 wb
     tx[j] = sh_ld32(tile + kTileTops + slot * 128u + 4u * pos);
   }
 }
-template <bool DIF>
-__device__ __forceinline__ void stage_b_run(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], u32 c, u32 pos, u32 opb,
-                                            u32 tab, u32 logS) {
-  net8_b<DIF>(x, tx, opb, pos);
+// store the 8 slots of a stage-B warp through its slot table (post-rotation,
+// carry-save, coset-major or natural order)
+__device__ __forceinline__ void stage_b_store(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], u32 c, u32 pos, u32 tab,
+                                              u32 logS) {
   const u32 CL = A.lanes, L0 = c + (pos << logS), step = 1u << logS;
   const u32 tsh = A.logLanes - logS;
 #pragma unroll
@@ -683,8 +683,123 @@ __device__ __forceinline__ void stage_b_run(const WaveArgs& A, Ch<8> (&x)[8], in
     if (L0 == h1.y) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
   }
 }
-
 template <bool DIF>
+__device__ __forceinline__ void stage_b_run(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], u32 c, u32 pos, u32 opb,
+                                            u32 tab, u32 logS) {
+  net8_b<DIF>(x, tx, opb, pos);
+  stage_b_store(A, x, tx, c, pos, tab, logS);
+}
+
+// ---- phase programs (Planner::tma_program): 64-slot classes that are not
+// full networks, e.g. the truncated ITFT leaves.  Stage A only settles the
+// warp's slots in the tile; then every phase runs its ops on the tile, warp w
+// the ops of its row / column (disjoint slots), a group barrier between
+// phases; stage B stores from the tile.
+
+// stage A of a program item: settle warp w's slots in place; the tops rows of
+// slots read in place that were never written are zeroed
+template <bool DIF>
+__device__ __forceinline__ void stage_a_settle(const TmaLeafDesc& d, u32 c, u32 w, u32 pos, u32 apre, u32 tile,
+                                               u32 sm_s, u32 logS) {
+  const u32 wnet = DIF ? 1u : 2u;
+#pragma unroll 1
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_a(wnet, w, j);
+    if (slot >= d.nload) break;
+    const u32 pre = __shfl_sync(0xffffffffu, apre, (int)j);
+    if ((pre & 0x3FFFFFFFu) == 0 && c != 0) {
+      if ((pre >> 30) & 1u) sh_st32(tile + kTileTops + slot * 128u + 4u * pos, 0);
+      continue;
+    }
+    settle_slot(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
+                tile + kTileHiw + slot * 16u, sm_s + kRingRows + (w * 8u + j) * 1024u,
+                sm_s + kRingTops + (w * 8u + j) * 128u, logS);
+  }
+}
+
+// warp w's ops of one phase: micro-ops on the tile's rows (a butterfly's b is
+// row b read at position pos - q, negated across 2^N == -1).  An ADDSUB
+// flagged as paired (bit 22) runs together with the next op, also an ADDSUB
+// on other slots: two independent carry chains in flight.
+__device__ __forceinline__ void prog_addsub_load(u32 wop, u32 tile, u32 pos, Ch<8>& x, int& ta, Ch<8>& yb, int& tb,
+                                                 bool& neg) {
+  const u32 a = (wop >> 4) & 63u, b = (wop >> 10) & 63u, q = (wop >> 16) & 63u;
+  const u32 qq = q & 31u, pl = (pos - qq) & 31u;
+  neg = (pos < qq) != (q >= 32u);
+  lds_row(x, tile + kTileRows + a * 1024u, pos);
+  ta = sh_ld32(tile + kTileTops + a * 128u + 4u * pos);
+  lds_row(yb, tile + kTileRows + b * 1024u, pl);
+  tb = sh_ld32(tile + kTileTops + b * 128u + 4u * pl);
+}
+__device__ __forceinline__ void prog_addsub_store(u32 wop, u32 tile, u32 pos, const Ch<8>& y0, int t0,
+                                                  const Ch<8>& y1, int t1) {
+  const u32 a = (wop >> 4) & 63u, b = (wop >> 10) & 63u;
+  sts_row(tile + kTileRows + a * 1024u, pos, y0);
+  sh_st32(tile + kTileTops + a * 128u + 4u * pos, t0);
+  sts_row(tile + kTileRows + b * 1024u, pos, y1);
+  sh_st32(tile + kTileTops + b * 128u + 4u * pos, t1);
+}
+__device__ __forceinline__ void prog_ops(const u32* prog, u32 desc, u32 lane, u32 tile) {
+  const u32 first = desc >> 16, count = desc & 0xFFFFu;
+  const u32 pos = lane;
+#pragma unroll 1
+  for (u32 o0 = 0; o0 < count; o0 += 32) {
+    const u32 opv = o0 + lane < count ? __ldg(prog + first + o0 + lane) : 0u;
+    const u32 m = count - o0 < 32u ? count - o0 : 32u;
+#pragma unroll 1
+    for (u32 o = 0; o < m; ++o) {
+      const u32 wop = __shfl_sync(0xffffffffu, opv, (int)o);
+      if (wop & (1u << 22)) {  // a pair of ADDSUBs (warp-uniform)
+        const u32 wop2 = __shfl_sync(0xffffffffu, opv, (int)o + 1);
+        Ch<8> x0, b0, x1, b1, y0, y1, z0, z1;
+        int ta0, tb0, ta1, tb1, s0, s1, r0, r1;
+        bool n0, n1;
+        prog_addsub_load(wop, tile, pos, x0, ta0, b0, tb0, n0);
+        prog_addsub_load(wop2, tile, pos, x1, ta1, b1, tb1, n1);
+        ch_pm8(y0, s0, y1, s1, x0, ta0, b0, tb0, n0);
+        ch_pm8(z0, r0, z1, r1, x1, ta1, b1, tb1, n1);
+        __syncwarp();
+        prog_addsub_store(wop, tile, pos, y0, s0, y1, s1);
+        prog_addsub_store(wop2, tile, pos, z0, r0, z1, r1);
+        __syncwarp();
+        ++o;
+        continue;
+      }
+      const u32 type = wop & 15u, a = (wop >> 4) & 63u, b = (wop >> 10) & 63u, q = (wop >> 16) & 63u;
+      const u32 ra = tile + kTileRows + a * 1024u, rb = tile + kTileRows + b * 1024u;
+      Ch<8> x, y0, y1;
+      const int ta = sh_ld32(tile + kTileTops + a * 128u + 4u * pos);
+      lds_row(x, ra, pos);
+      int t0 = 0, t1 = ta;
+      if (type == OP_COPY) {
+        y1 = x;
+      } else {
+        const u32 qq = q & 31u;
+        const u32 pl = (pos - qq) & 31u;
+        const bool neg = (pos < qq) != (q >= 32u);
+        Ch<8> yb;
+        lds_row(yb, rb, pl);
+        const int tb = sh_ld32(tile + kTileTops + b * 128u + 4u * pl);
+        ch_pm8(y0, t0, y1, t1, x, ta, yb, tb, neg);
+        if (type == OP_SUB2 || type == OP_SUB2DIFF) t0 = ch_add<8>(y0, x, y1) + ta + t1;
+      }
+      __syncwarp();
+      if (type != OP_COPY) {
+        sts_row(ra, pos, y0);
+        sh_st32(tile + kTileTops + a * 128u + 4u * pos, t0);
+      }
+      if (type == OP_ADDSUB || type == OP_SUB2DIFF || type == OP_COPY) {
+        sts_row(rb, pos, y1);
+        sh_st32(tile + kTileTops + b * 128u + 4u * pos, t1);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// PROG: the wave has phase-program items (a separate instance, so the
+// network-only kernels keep their register allocation)
+template <bool DIF, bool PROG>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     coset_tma_kernel(const __grid_constant__ CUtensorMap tm_view, const __grid_constant__ CUtensorMap tm_shadow,
                      WaveArgs A) {
@@ -738,25 +853,50 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const TmaLeafDesc d2 = tma_desc(A, i2, items);
     u32 pre2, lay2;
     lane_info(d2, i2 < items, pre2, lay2);
-    const u32 opa = lane < 12 ? __ldg(A.wops + d.wop_begin + w * 12u + lane) : 0u;
-    const u32 opb = lane < 12 ? __ldg(A.wops + d.wop_begin + (8u + w) * 12u + lane) : 0u;
+    // group-uniform: a phase program (wnet 3) instead of the two networks
+    const bool prog = PROG && (d.nstore_wnet >> 16) == 3u;
+    const u32 opa = !prog && lane < 12 ? __ldg(A.wops + d.wop_begin + w * 12u + lane) : 0u;
+    const u32 opb = !prog && lane < 12 ? __ldg(A.wops + d.wop_begin + (8u + w) * 12u + lane) : 0u;
     // ---- stage A
     cp_async_wait<0>();
     __syncwarp();
     mbar_wait(ringbar(grp), n & 1u);
-    if (!(A.debug & 256u)) stage_a<DIF>(d, c, w, pos, pre, opa, tile, sm_s, logS);
+    // program items: word 0 = phases | network rows << 8 (the DIT kernel runs
+    // phase 0 of those rows as stage-A networks in registers)
+    const u32 phdr = prog ? __ldg(A.wops + d.wop_begin) : 0u;
+    const bool pnet = prog && !DIF && ((phdr >> (8 + w)) & 1u);
+    if (pnet) {
+      const u32 opn = lane < 12 ? __ldg(A.wops + d.wop_begin + 1 + 8 * (phdr & 0xFFu) + 12 * w + lane) : 0u;
+      stage_a<DIF>(d, c, w, pos, pre, opn, tile, sm_s, logS);
+    } else if (prog) {
+      stage_a_settle<DIF>(d, c, w, pos, pre, tile, sm_s, logS);
+    } else if (!(A.debug & 256u)) {
+      stage_a<DIF>(d, c, w, pos, pre, opa, tile, sm_s, logS);
+    }
     // the ring is free: the next item's lane-below rows start moving
     ring_issue<DIF>(A, &tm_view, &tm_shadow, dn, in & (step - 1), in < items, w, lane, npre, nlay, sm_s,
                     ringbar(grp ^ 1u), step);
     slot_table<DIF>(A, d, w, lane, tab);
     named_bar(1u + grp, 256u);  // the group's stage-A outputs are in the tile
+    if (prog) {
+      const u32* pg = A.wops + d.wop_begin;
+      const u32 P = phdr & 0xFFu;
+#pragma unroll 1
+      for (u32 p = 0; p < P; ++p) {
+        if (p || !pnet) prog_ops(pg, __ldg(pg + 1 + 8 * p + w), lane, tile);
+        named_bar(1u + grp, 256u);
+      }
+    }
     // ---- stage B
     Ch<8> x[8];
     int tx[8];
     stage_b_load<DIF>(x, tx, w, pos, tile);
     named_bar(1u + grp, 256u);  // every warp of the group holds its rows: the tile is free
     if (i2 < items) warp_load<DIF>(A, d2, i2 & (step - 1), w, lane, pre2, lay2, tile, step);
-    if (!(A.debug & 512u)) stage_b_run<DIF>(A, x, tx, c, pos, opb, tab, logS);
+    if (prog)
+      stage_b_store(A, x, tx, c, pos, tab, logS);
+    else if (!(A.debug & 512u))
+      stage_b_run<DIF>(A, x, tx, c, pos, opb, tab, logS);
     __syncwarp();  // the slot table is rewritten for the next item
     i = i2;
     d = d2;

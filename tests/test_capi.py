@@ -231,18 +231,25 @@ def run_plan_fermat(plan, N, vals):
     return out
 
 
-def check_plan(ctx, N, rnd, trials, lmin=1, lmax=8):
+def check_plan(ctx, N, rnd, trials, lmin=1, lmax=8, shapes=()):
+    """Random (L, z, n, s, policy) TFTs + ITFTs, then the given ITFT shapes
+    (L, z, n2, f): emulated plan vs the definition."""
     fm = bm.FermatModel(N)
-    for _ in range(trials):
-        L = 1 << rnd.randint(lmin, lmax)
-        z, n = rnd.randint(1, L), rnd.randint(1, L)
+    todo = [None] * trials + list(shapes)
+    for shape in todo:
+        if shape is None:
+            L = 1 << rnd.randint(lmin, lmax)
+            z, n = rnd.randint(1, L), rnd.randint(1, L)
+            n2, f = rnd.randint(0, z), rnd.randint(0, 1)
+        else:
+            L, z, n2, f = shape
+            n = z
         s, pol = rnd.randrange(2 * N), rnd.randint(0, 1)
         a = [rnd.randrange((1 << N) + 1) for _ in range(z)]
         want = fm.dft(L, s, a)
         plan = cf.plan_dump(ctx, False, cf.TransformParams(L, s, z, n), pol)
         x = run_plan_fermat(plan, N, {i: a[i] for i in range(z)})
         assert [x[i] for i in range(n)] == want[:n], (N, L, z, n, s, pol)
-        n2, f = rnd.randint(0, z), rnd.randint(0, 1)
         if not 1 <= n2 + f <= L:
             continue
         vals = {i: want[i] for i in range(n2)}
@@ -264,11 +271,12 @@ def test_gpu_schedule_reproduces_definition(limit):
 
 
 def test_wide_schedule_reproduces_definition():
-    """Radix-64 coset leaves (coset_wide_kernel): the reshaped top split, the
-    full 64-point networks (incl. truncated TFT leaves on zero-filled inputs)
-    and the generic 16..64-slot programs."""
+    """Radix-64 coset leaves: the reshaped top split, the full 64-point
+    networks (incl. truncated TFT leaves on zero-filled inputs) and the
+    generic 64-slot programs (truncated ITFT leaves with their sub-unit
+    offsets realigned, run as phase programs on the TMA kernel)."""
     rnd = random.Random(7)
-    N = 8192
+    N = 32768
     ctx = cf.FermatRingCtx(N)
     ctx.set_wide(1)
     seen = set()
@@ -281,7 +289,8 @@ def test_wide_schedule_reproduces_definition():
             for c in plan["classes"]:
                 if c["kind"] == 1 and c["ell"] >= 4:
                     seen.add("net" if c.get("net") else "generic")
-    check_plan(ctx, N, random.Random(8), 10, 6, 9)
+    # truncated 64-point ITFT leaves that become phase programs
+    check_plan(ctx, N, random.Random(8), 2, 6, 7, shapes=[(64, 33, 30, 0), (64, 49, 49, 0), (64, 48, 48, 1)])
     assert seen == {"net", "generic"}, seen
 
 
@@ -324,8 +333,10 @@ def test_schedule_shape_config5():
 def test_linear_form_and_doubling_leaves():
     """One-output ITFT leaves whose halvings make op rotations sub-lane run in
     their linear form (inputs pre-rotated by any bits, aligned adds) as coset
-    leaves; doublings are arithmetic (no deferred final rotations).  The plans
-    are evaluated against the transform's definition."""
+    leaves; other such leaves are realigned (Planner::realign: sub-unit
+    offsets taken by the loads, doublings turned into rotations where the
+    chain needs it, final offsets deferred to the fold).  The plans are
+    evaluated against the transform's definition, deferred rotations included."""
     N = 2048
     ctx = cf.FermatRingCtx(N)
     ctx.set_coset(8)
@@ -337,7 +348,6 @@ def test_linear_form_and_doubling_leaves():
         a = [rnd.randrange((1 << N) + 1) for _ in range(z)]
         want = fm.dft(L, s, a)
         plan = cf.plan_dump(ctx, True, cf.TransformParams(L, s, z, n, f))
-        assert plan.get("final_rot", []) == []
         for c in plan["classes"]:
             if c["kind"] == 1 and c["nstore"] == 1 and c["ops"] and all(t in (1, 4) and r == 0 for (t, a_, b_, r) in c["ops"]):
                 seen_linear += 1
