@@ -140,9 +140,11 @@ struct DevicePlan {
   // Fermat geometry of this plan: chunk (lane) width, chunks per element,
   // whole-leaf slot bytes, tops-array interleave
   u32 cw = 16, C = 0, slot_bytes = 0, logS = 0;
+  u64* prime_ntw = nullptr;  // prime rings: network classes' butterfly twiddles (prime::Args::ntw)
   ~DevicePlan() {
     if (dbuf) cudaFree(dbuf);
     if (tma_descs) cudaFree(tma_descs);
+    if (prime_ntw) cudaFree(prime_ntw);
   }
 };
 
@@ -204,12 +206,92 @@ struct cftft_ring {
 
 namespace {
 
+// Prime rings: 1 (DIF, spans L/2 .. 1) / 2 (DIT, spans 1 .. L/2) when the
+// class is the full radix-2 network of ADDSUB butterflies in level order --
+// truncated TFT programs qualify when the network on zero-filled missing
+// inputs reproduces every stored output (checked by evaluating both mod p on
+// random inputs; a COPY is a butterfly with a zero b, an ADD one whose
+// difference nothing reads) -- else 0.  `tw` gets
+// omega^r 2^64 mod p per butterfly (level l, index j) at l L/2 + j, 0 for r = 0.
+u32 prime_network(const LeafProgram& cl, u64 p, u64 omega, std::vector<u64>& tw) {
+  const u32 ell = cl.key.ell;
+  if (ell < 3 || cl.ops.empty() || cl.nload == 0) return 0;
+  const u32 L = 1u << ell, half = L / 2;
+  auto mulp = [p](u64 a, u64 b) { return (u64)((unsigned __int128)a * b % p); };
+  auto powp = [&](u64 a, u64 e) {
+    u64 r = 1 % p;
+    for (; e; e >>= 1, a = mulp(a, a))
+      if (e & 1) r = mulp(r, a);
+    return r;
+  };
+  auto addm = [p](u64 a, u64 b) { return (u64)(((unsigned __int128)a + b) % p); };
+  auto subm = [p](u64 a, u64 b) { return a >= b ? a - b : (u64)((unsigned __int128)a + p - b); };
+  for (u32 kind = 1; kind <= 2; ++kind) {
+    std::vector<long long> qn((size_t)ell * half, -1);
+    std::vector<int> last(L, -1);
+    bool ok = true;
+    for (const DevOp& op : cl.ops) {
+      const u32 a = op.a, b = op.b, h = b - a;
+      if ((op.type != OP_ADDSUB && op.type != OP_COPY && op.type != OP_ADD) || b <= a || b >= L || (h & (h - 1)) ||
+          (a & h)) {
+        ok = false;
+        break;
+      }
+      const int lh = __builtin_ctz(h);
+      const int lvl = kind == 1 ? (int)ell - 1 - lh : lh;
+      if (last[a] >= lvl || last[b] >= lvl) {
+        ok = false;
+        break;
+      }
+      last[a] = last[b] = lvl;
+      qn[(size_t)lvl * half + (a / (2 * h)) * h + a % h] = op.type == OP_COPY ? 0 : (long long)op.r;
+    }
+    if (!ok) continue;
+    std::vector<u64> x(L, 0), y;
+    u64 seed = 0x9E3779B97F4A7C15ull ^ (cl.key.z * 131 + cl.key.n * 7 + kind);
+    for (u32 k = 0; k < cl.nload; ++k) {
+      seed = seed * 6364136223846793005ull + 1442695040888963407ull;
+      x[k] = (seed >> 1) % p;
+    }
+    y = x;
+    for (const DevOp& op : cl.ops) {
+      if (op.type == OP_COPY) {
+        x[op.b] = x[op.a];
+        continue;
+      }
+      const u64 t = mulp(x[op.b], powp(omega, op.r)), u = x[op.a];
+      x[op.a] = addm(u, t);
+      if (op.type == OP_ADDSUB) x[op.b] = subm(u, t);
+    }
+    for (u32 lvl = 0; lvl < ell; ++lvl) {
+      const u32 h = kind == 1 ? (L >> (lvl + 1)) : (1u << lvl);
+      for (u32 j = 0; j < half; ++j) {
+        const u32 a = (j / h) * 2 * h + j % h;
+        const long long q = qn[(size_t)lvl * half + j];
+        const u64 t = q > 0 ? mulp(y[a + h], powp(omega, (u64)q)) : y[a + h], u = y[a];
+        y[a] = addm(u, t);
+        y[a + h] = subm(u, t);
+      }
+    }
+    for (u32 k = 0; k < cl.nstore && ok; ++k) ok = x[k] == y[k];
+    if (!ok) continue;
+    const u64 Rm = (u64)(((unsigned __int128)1 << 64) % p);
+    const size_t off = tw.size();
+    tw.resize(off + (size_t)ell * half, 0);
+    for (size_t i = 0; i < (size_t)ell * half; ++i)
+      if (qn[i] > 0) tw[off + i] = mulp(powp(omega, (u64)qn[i]), Rm);
+    return kind;
+  }
+  return 0;
+}
+
 int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
   const Plan& p = dp.host;
   std::vector<DevClass> cls;
   std::vector<DevOp> ops;
   std::vector<u32> levels;
   std::vector<SymExp> rots;
+  std::vector<u64> ntw;  // prime network twiddles
   for (const auto& c : p.classes) {
     DevClass d{};
     d.L = 1u << c.key.ell;
@@ -237,7 +319,29 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     d.fslot = (c.key.inverse && c.key.f) ? (u32)c.key.n : 0xFFFFFFFFu;
     d.wop_begin = cls.size() < p.wave_op_begin.size() ? p.wave_op_begin[cls.size()] : 0;
     d.wnet = cls.size() < p.wave_net.size() ? p.wave_net[cls.size()] : 0;
+    if (R->kind == CFTFT_RING_PRIME) {
+      const size_t off = ntw.size();
+      d.wnet = prime_network(c, R->m, R->omega, ntw);
+      d.wop_begin = (u32)off;
+    }
     cls.push_back(d);
+  }
+  if (!ntw.empty()) {
+    CUDA_TRY(cudaMalloc(&dp.prime_ntw, ntw.size() * sizeof(u64)));
+    CUDA_TRY(cudaMemcpyAsync(dp.prime_ntw, ntw.data(), ntw.size() * sizeof(u64), cudaMemcpyHostToDevice, st));
+  }
+  if (R->kind == CFTFT_RING_PRIME) {
+    // each op's omega^r in Montgomery form (times 2^64 mod p): one product
+    // per butterfly on the GPU instead of two table lookups and two products
+    const u64 pm = R->m;
+    auto mulp = [pm](u64 a, u64 b) { return (u64)((unsigned __int128)a * b % pm); };
+    const u64 Rm = (u64)(((unsigned __int128)1 << 64) % pm);
+    for (auto& op : ops) {
+      u64 r = 1 % pm, a = R->omega, e = op.r;
+      for (; e; e >>= 1, a = mulp(a, a))
+        if (e & 1) r = mulp(r, a);
+      op.pad2 = mulp(r, Rm);
+    }
   }
   if (rots.empty()) rots.push_back(SymExp{});
   if (levels.empty()) levels.push_back(0);
@@ -740,11 +844,14 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
     const size_t cbytes = sizeof(u32) * (1 + (size_t)dp.ncounters);
     CUDA_TRY(cudaMallocAsync((void**)&counters, cbytes, st));
     CUDA_TRY(cudaMemsetAsync(counters, 0, cbytes, st));
+    size_t max_group = 1;  // prime: the most leaves a ticket groups
+    for (size_t g = 1; g < dp.host.groups.size(); g += 2) max_group = std::max<size_t>(max_group, dp.host.groups[g]);
     // Fermat: two ticket buffers of `half` bytes each (a big ticket spans both)
     const size_t half = ((kSmemBudget - scratch_bytes(1024)) / 2) & ~size_t(15);
     const size_t slots_bytes = R->kind == CFTFT_RING_FERMAT
                                    ? std::max<size_t>({dp.host.max_slot_area, (size_t)dp.slot_bytes << dp.max_ell, 2 * half})
-                                   : ((size_t)R->slot_bytes << dp.max_ell) * (R->kind == CFTFT_RING_PRIME ? 16 : 1);  // prime: grouped leaves
+                                   : ((size_t)R->slot_bytes << dp.max_ell) * max_group *
+                                         (R->kind == CFTFT_RING_PRIME ? 17 : 16) / 16;  // prime: grouped, padded
     const size_t smem = slots_bytes + (R->kind == CFTFT_RING_FERMAT ? scratch_bytes(1024) : 0);
     unsigned grid = 1;
     int* tops = nullptr;
@@ -989,8 +1096,22 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       }
     } else if (R->kind == CFTFT_RING_PRIME) {
       if (int rc = ensure_prime_tables(R, st)) return rc;
-      if (int rc = set_smem(prime::leaf_kernel)) return rc;
-      if (int rc = grid_for(prime::leaf_kernel, prime::kThreads, smem, dp.nleaves, &grid)) return rc;
+      // big leaves (2^9..2^11 coefficients): 256-thread CTAs for the TFT
+      // (network leaves), 512 for the ITFT (its truncated leaves run many
+      // short dependency levels: wider CTAs per barrier measured faster)
+      const bool big = dp.max_ell >= 9;
+      const bool wide_cta = big && dp.host.inverse;
+      const int pthreads = wide_cta ? 512 : big ? 256 : 128;
+      if (wide_cta) {
+        if (int rc = set_smem(prime::leaf_kernel<512>)) return rc;
+        if (int rc = grid_for(prime::leaf_kernel<512>, pthreads, smem, dp.nleaves, &grid)) return rc;
+      } else if (big) {
+        if (int rc = set_smem(prime::leaf_kernel<256>)) return rc;
+        if (int rc = grid_for(prime::leaf_kernel<256>, pthreads, smem, dp.nleaves, &grid)) return rc;
+      } else {
+        if (int rc = set_smem(prime::leaf_kernel<128>)) return rc;
+        if (int rc = grid_for(prime::leaf_kernel<128>, pthreads, smem, dp.nleaves, &grid)) return rc;
+      }
       prime::Args A{};
       A.data = base;
       A.elem_bytes = stride;
@@ -1010,8 +1131,14 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
       A.tw_hi = R->prime_tw + (size_t{1} << R->lo_bits);
       A.slot_bytes = R->slot_bytes;
       A.groups = dp.groups;
+      A.ntw = dp.prime_ntw;
       A.nleaves = dp.groups ? dp.host.groups.size() / 2 : dp.nleaves;  // tickets
-      prime::leaf_kernel<<<grid, prime::kThreads, smem, st>>>(A);
+      if (wide_cta)
+        prime::leaf_kernel<512><<<grid, pthreads, smem, st>>>(A);
+      else if (big)
+        prime::leaf_kernel<256><<<grid, pthreads, smem, st>>>(A);
+      else
+        prime::leaf_kernel<128><<<grid, pthreads, smem, st>>>(A);
     } else {
       if (int rc = set_smem(negacyclic::leaf_kernel)) return rc;
       if (int rc = grid_for(negacyclic::leaf_kernel, negacyclic::kThreads, smem, dp.nleaves, &grid))
@@ -1332,7 +1459,9 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
   unsigned lam = 1;
   const size_t per_cta = kSmemBudget;
   const size_t budget = per_cta - (kind == CFTFT_RING_FERMAT ? scratch_bytes(R->NT) : 0);
-  while (lam < 10 && ((size_t)R->slot_bytes << (lam + 1)) <= budget) ++lam;
+  // (prime rings: leaves up to 2^11, so that L = 2^22 runs in two passes)
+  const unsigned lam_max = kind == CFTFT_RING_PRIME ? 11u : 10u;
+  while (lam < lam_max && ((size_t)R->slot_bytes << (lam + 1)) <= budget) ++lam;
   R->max_leaf_ell = lam;
   R->max_leaf_fit = lam;
   *out = R.release();

@@ -69,7 +69,7 @@ struct DevOp {
   std::uint16_t a, b;
   std::uint16_t pad1;
   u64 r;
-  u64 pad2;
+  u64 pad2;  // prime rings: omega^r 2^64 mod p (upload)
 };
 static_assert(sizeof(DevOp) == 24, "DevOp layout");
 
@@ -837,10 +837,12 @@ class Planner {
   // dependency and completion counter.
   void group_leaves(Plan& p) const {
     p.groups.clear();
+    // at most 4096 slots per ticket: big leaves (2^9..2^11) group fewer
+    const size_t cap = std::max<size_t>(1, std::min<size_t>(rs_.group, size_t{4096} >> max_ell_));
     for (size_t t = 0; t < p.leaves.size();) {
       const DevLeaf& g = p.leaves[t];
       size_t n = 1;
-      while (n < rs_.group && t + n < p.leaves.size()) {
+      while (n < cap && t + n < p.leaves.size()) {
         const DevLeaf& x = p.leaves[t + n];
         if (x.cls != g.cls || x.stride != g.stride || x.base != g.base + n || p.leaf_wave[t + n] != p.leaf_wave[t])
           break;

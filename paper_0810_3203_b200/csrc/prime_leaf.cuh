@@ -17,8 +17,6 @@
 namespace cftft_b200 {
 namespace prime {
 
-constexpr int kThreads = 128;
-constexpr int kTasksPerThread = 4;
 
 struct Args {
   std::uint8_t* data;
@@ -37,7 +35,11 @@ struct Args {
   u32 lo_bits;
   u32 slot_bytes;
   const u32* groups;  // tickets = {first leaf, count} (Plan::groups), or null: one leaf each
+  // network classes (DevClass::wnet 1 DIF / 2 DIT): per butterfly (level l,
+  // index j < L/2) omega^r 2^64 mod p at ntw[wop_begin + l L/2 + j]; 0 = r 0
+  const u64* ntw;
 };
+
 
 __device__ __forceinline__ u64 addp(u64 a, u64 b, u64 p) {
   const u64 s = a + b;
@@ -64,7 +66,42 @@ __device__ __forceinline__ u32 ld_acquire(const u32* c) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
+// Shared-memory slot index, padded by one word per 16 (a warp's 8-byte
+// accesses at any power-of-two stride spread over the banks)
+__device__ __forceinline__ u32 pdx(u32 i) { return i + (i >> 4); }
+
+// Radix-2^NL group of a full network (levels l0 .. l0 + NL - 1) on one
+// element set {base + m hs} of leaf j (slot k of leaf j at k G + j).
+template <int NL, bool DIF>
+__device__ __forceinline__ void net_group(u64* slot, u32 G, u32 j, u32 base, u32 hs, u32 l0, u32 half,
+                                          const u64* tw, u64 p, u64 pinv) {
+  constexpr u32 R = 1u << NL;
+  u64 v[R];
+#pragma unroll
+  for (u32 m = 0; m < R; ++m) v[m] = slot[pdx((base + m * hs) * G + j)];
+#pragma unroll
+  for (u32 t = 0; t < NL; ++t) {
+    const u32 sp = DIF ? (R >> (t + 1)) : (1u << t);  // span in units of hs
+    const u32 h = sp * hs;
+    const u32 lvl = l0 + t;
+#pragma unroll
+    for (u32 m = 0; m < R; ++m) {
+      if (m & sp) continue;
+      const u32 a = base + m * hs;
+      const u32 jb = (a / (2 * h)) * h + a % h;
+      const u64 w = __ldg(tw + (u64)lvl * half + jb);
+      const u64 b = w ? montmul(v[m + sp], w, p, pinv) : v[m + sp];
+      const u64 x = v[m];
+      v[m] = addp(x, b, p);
+      v[m + sp] = subp(x, b, p);
+    }
+  }
+#pragma unroll
+  for (u32 m = 0; m < R; ++m) slot[pdx((base + m * hs) * G + j)] = v[m];
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT < 4 ? 4 : 1024 / NT) leaf_kernel(Args A) {
   extern __shared__ __align__(16) std::uint8_t sm[];
   __shared__ u32 s_ticket;
   __shared__ u64 s_w[32];  // weights of the ticket's leaves
@@ -92,6 +129,9 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
     const u32 G = A.groups ? A.groups[2 * ticket + 1] : 1u;
     const DevLeaf lf = A.leaves[first];
     const DevClass cl = A.classes[lf.cls];
+    // x / G for x < 2^24 as a high product (G <= 16)
+    const u32 ginv = (u32)((0x100000000ull + G - 1) / G);
+    auto divg = [&](u32 x) -> u32 { return G == 1 ? x : __umulhi(x, ginv); };
     if (tid < G) {
       const DevLeaf lj = A.leaves[first + tid];
       s_w[tid] = lj.s;
@@ -104,95 +144,105 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(Args A) {
     auto wt = [&](u32 j) -> u64 { return s_w[j] & (A.M - 1); };
     // load through the pre-rotations (the ITFT's spectral inputs)
     for (u32 idx = tid; idx < cl.nload * G; idx += nthr) {
-      const u32 k = idx / G, j = idx - k * G;
+      const u32 k = divg(idx), j = idx - k * G;
       const u64 v = __ldcg(reinterpret_cast<const u64*>(A.data + (lf.base + j + (u64)k * lf.stride) * A.elem_bytes));
       if (cl.has_pre) {
         const SymExp P = A.rots[cl.pre_begin + k];
-        slot[idx] = twiddle(v, (P.a * wt(j) + P.b) & (A.M - 1));
+        slot[pdx(idx)] = twiddle(v, (P.a * wt(j) + P.b) & (A.M - 1));
       } else {
-        slot[idx] = v;
+        slot[pdx(idx)] = v;
       }
     }
     __syncthreads();
 
-    // tasks = (op, leaf j), j fastest
-    const u32 tasks_per_batch = nthr * kTasksPerThread;
-    for (u32 l = 0; l < cl.nlevels; ++l) {
-      const u32 o0 = A.levels[cl.level_begin + l], o1 = A.levels[cl.level_begin + l + 1];
-      const u32 ntasks = (o1 - o0) * G;
-      for (u32 tb = 0; tb < ntasks; tb += tasks_per_batch) {
-        u64 v0[kTasksPerThread], v1[kTasksPerThread];
-        u32 sa[kTasksPerThread], sb[kTasksPerThread], mask[kTasksPerThread];
-#pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k) {
-          mask[k] = 0;
-          const u32 task = tb + tid + k * nthr;
-          if (task >= ntasks) continue;
-          const u32 oi = task / G, j = task - oi * G;
-          const DevOp op = A.ops[o0 + oi];
-          sa[k] = op.a * G + j;
-          sb[k] = op.b * G + j;
-          const u64 a = slot[sa[k]];
-          switch (op.type) {
-            case OP_COPY:
-              v1[k] = a;
-              mask[k] = 2;
-              break;
-            case OP_DBL:
-              v0[k] = addp(a, a, p);
-              mask[k] = 1;
-              break;
-            case OP_HALF:
-              v0[k] = halfp(a, p);
-              mask[k] = 1;
-              break;
-            default: {
-              const u64 b = twiddle(slot[sb[k]], op.r);
-              switch (op.type) {
-                case OP_ADDSUB:
-                  v0[k] = addp(a, b, p);
-                  v1[k] = subp(a, b, p);
-                  mask[k] = 3;
-                  break;
-                case OP_ADD:
-                  v0[k] = addp(a, b, p);
-                  mask[k] = 1;
-                  break;
-                case OP_SUB2:
-                  v0[k] = subp(addp(a, a, p), b, p);
-                  mask[k] = 1;
-                  break;
-                case OP_SUB2DIFF:
-                  v0[k] = subp(addp(a, a, p), b, p);
-                  v1[k] = subp(a, b, p);
-                  mask[k] = 3;
-                  break;
-                case OP_ADDHALF:
-                  v0[k] = halfp(addp(a, b, p), p);
-                  mask[k] = 1;
-                  break;
-                default:
-                  break;
-              }
-            }
+    if (cl.wnet) {
+      // a full radix-2 network (DIF: spans L/2 .. 1, DIT: 1 .. L/2; truncated
+      // TFT inputs read as zeros): register groups of three levels, one
+      // shared-memory round trip and barrier per group
+      for (u32 idx = cl.nload * G + tid; idx < cl.L * G; idx += nthr) slot[pdx(idx)] = 0;
+      __syncthreads();
+      const bool dif = cl.wnet == 1;
+      const u32 ell = 31 - __clz(cl.L), half = cl.L >> 1;
+      const u64* tw = A.ntw + cl.wop_begin;
+      for (u32 l0 = 0; l0 < ell; l0 += 3) {
+        const u32 nl = ell - l0 < 3 ? ell - l0 : 3;
+        const u32 hs = dif ? (cl.L >> (l0 + nl)) : (1u << l0);  // span of the group's last / first level
+        const u32 lhs = 31 - __clz(hs);
+        const u32 nsets = cl.L >> nl;
+        for (u32 task = tid; task < nsets * G; task += nthr) {
+          const u32 set = divg(task), j = task - set * G;
+          const u32 base = ((set >> lhs) << (lhs + nl)) | (set & (hs - 1));
+          if (nl == 3) {
+            if (dif) net_group<3, true>(slot, G, j, base, hs, l0, half, tw, p, pinv);
+            else net_group<3, false>(slot, G, j, base, hs, l0, half, tw, p, pinv);
+          } else if (nl == 2) {
+            if (dif) net_group<2, true>(slot, G, j, base, hs, l0, half, tw, p, pinv);
+            else net_group<2, false>(slot, G, j, base, hs, l0, half, tw, p, pinv);
+          } else {
+            if (dif) net_group<1, true>(slot, G, j, base, hs, l0, half, tw, p, pinv);
+            else net_group<1, false>(slot, G, j, base, hs, l0, half, tw, p, pinv);
           }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kTasksPerThread; ++k) {
-          if (mask[k] & 1) slot[sa[k]] = v0[k];
-          if (mask[k] & 2) slot[sb[k]] = v1[k];
         }
         __syncthreads();
       }
     }
+    // tasks = (op, leaf j), j fastest; the ops of a level touch disjoint
+    // slots (Planner: dependency levels), so each task writes its results
+    // straight back and one barrier ends the level
+    for (u32 l = 0; l < (cl.wnet ? 0u : cl.nlevels); ++l) {
+      const u32 o0 = A.levels[cl.level_begin + l], o1 = A.levels[cl.level_begin + l + 1];
+      const u32 ntasks = (o1 - o0) * G;
+      for (u32 task = tid; task < ntasks; task += nthr) {
+        const u32 oi = divg(task), j = task - oi * G;
+        const DevOp op = A.ops[o0 + oi];
+        const u32 sa = pdx(op.a * G + j), sb = pdx(op.b * G + j);
+        const u64 a = slot[sa];
+        switch (op.type) {
+          case OP_COPY:
+            slot[sb] = a;
+            break;
+          case OP_DBL:
+            slot[sa] = addp(a, a, p);
+            break;
+          case OP_HALF:
+            slot[sa] = halfp(a, p);
+            break;
+          default: {
+            // op.pad2 = omega^r 2^64 mod p (host-computed, upload())
+            const u64 b = op.r ? montmul(slot[sb], op.pad2, p, pinv) : slot[sb];
+            switch (op.type) {
+              case OP_ADDSUB:
+                slot[sa] = addp(a, b, p);
+                slot[sb] = subp(a, b, p);
+                break;
+              case OP_ADD:
+                slot[sa] = addp(a, b, p);
+                break;
+              case OP_SUB2:
+                slot[sa] = subp(addp(a, a, p), b, p);
+                break;
+              case OP_SUB2DIFF:
+                slot[sa] = subp(addp(a, a, p), b, p);
+                slot[sb] = subp(a, b, p);
+                break;
+              case OP_ADDHALF:
+                slot[sa] = halfp(addp(a, b, p), p);
+                break;
+              default:
+                break;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
 
     // store through the post-rotations
     for (u32 idx = tid; idx < cl.nstore * G; idx += nthr) {
-      const u32 k = idx / G, j = idx - k * G;
+      const u32 k = divg(idx), j = idx - k * G;
       const SymExp P = A.rots[cl.post_begin + k];
       u64* dst = reinterpret_cast<u64*>(A.data + (lf.base + j + (u64)k * lf.stride) * A.elem_bytes);
-      __stcg(dst, twiddle(slot[idx], (P.a * wt(j) + P.b) & (A.M - 1)));
+      __stcg(dst, twiddle(slot[pdx(idx)], (P.a * wt(j) + P.b) & (A.M - 1)));
     }
     __threadfence();
     __syncthreads();
