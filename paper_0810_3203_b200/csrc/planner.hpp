@@ -708,14 +708,16 @@ class Planner {
       }
       if (net) netmask |= 1u << w;
     }
-    // pairs: an ADDSUB followed by an ADDSUB on other slots (bit 22 on the
-    // first) run together (two independent carry chains), within a 32-op chunk
+    // pairs: an ADDSUB (ADD) followed by an ADDSUB (ADD) on other slots (bit
+    // 22 on the first) run together (two independent carry chains), within a
+    // 32-op chunk
     for (auto& phase : ph)
       for (auto& v : phase)
         for (size_t k = 0; k + 1 < v.size();) {
           const u32 x = v[k], y = v[k + 1];
           const u32 xa = (x >> 4) & 63u, xb = (x >> 10) & 63u, ya = (y >> 4) & 63u, yb = (y >> 10) & 63u;
-          if ((k & 31) != 31 && (x & 15u) == OP_ADDSUB && (y & 15u) == OP_ADDSUB && xa != ya && xa != yb &&
+          const u32 tx = x & 15u, ty = y & 15u;
+          if ((k & 31) != 31 && tx == ty && (tx == OP_ADDSUB || tx == OP_ADD) && xa != ya && xa != yb &&
               xb != ya && xb != yb) {
             v[k] |= 1u << 22;
             k += 2;

@@ -749,7 +749,7 @@ __device__ __forceinline__ void prog_ops(const u32* prog, u32 desc, u32 lane, u3
 #pragma unroll 1
     for (u32 o = 0; o < m; ++o) {
       const u32 wop = __shfl_sync(0xffffffffu, opv, (int)o);
-      if (wop & (1u << 22)) {  // a pair of ADDSUBs (warp-uniform)
+      if (wop & (1u << 22)) {  // a pair of ADDSUBs or of ADDs (warp-uniform)
         const u32 wop2 = __shfl_sync(0xffffffffu, opv, (int)o + 1);
         Ch<8> x0, b0, x1, b1, y0, y1, z0, z1;
         int ta0, tb0, ta1, tb1, s0, s1, r0, r1;
@@ -759,8 +759,16 @@ __device__ __forceinline__ void prog_ops(const u32* prog, u32 desc, u32 lane, u3
         ch_pm8(y0, s0, y1, s1, x0, ta0, b0, tb0, n0);
         ch_pm8(z0, r0, z1, r1, x1, ta1, b1, tb1, n1);
         __syncwarp();
-        prog_addsub_store(wop, tile, pos, y0, s0, y1, s1);
-        prog_addsub_store(wop2, tile, pos, z0, r0, z1, r1);
+        if ((wop & 15u) == OP_ADDSUB) {
+          prog_addsub_store(wop, tile, pos, y0, s0, y1, s1);
+          prog_addsub_store(wop2, tile, pos, z0, r0, z1, r1);
+        } else {  // ADD: a only
+          const u32 a0 = (wop >> 4) & 63u, a1 = (wop2 >> 4) & 63u;
+          sts_row(tile + kTileRows + a0 * 1024u, pos, y0);
+          sh_st32(tile + kTileTops + a0 * 128u + 4u * pos, s0);
+          sts_row(tile + kTileRows + a1 * 1024u, pos, z0);
+          sh_st32(tile + kTileTops + a1 * 128u + 4u * pos, r0);
+        }
         __syncwarp();
         ++o;
         continue;
@@ -883,7 +891,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const u32 P = phdr & 0xFFu;
 #pragma unroll 1
       for (u32 p = 0; p < P; ++p) {
-        if (p || !pnet) prog_ops(pg, __ldg(pg + 1 + 8 * p + w), lane, tile);
+        if ((p || !pnet) && !((A.debug & 1024u) && p >= 2)) prog_ops(pg, __ldg(pg + 1 + 8 * p + w), lane, tile);
         named_bar(1u + grp, 256u);
       }
     }
