@@ -1380,7 +1380,7 @@ int cftft_ring_create(int kind, uint64_t n_or_k, uint64_t modulus, cftft_ring** 
     R->N = N;
     R->M = 2 * N;
     R->D = (u32)(N / 32);
-    R->CW = R->D >= 16 ? 16 : R->D;
+    R->CW = R->D >= 16 ? (R->D <= 64 ? 4 : 16) : R->D;
     R->C = R->D / R->CW;
     R->slot_bytes = fermat_slot_bytes(R->C, 4 * R->CW);
     R->elem_bytes = ((N / 8 + 8) + 15) & ~u64(15);
