@@ -1258,8 +1258,11 @@ int transform(const cftft_ring* cR, bool inv, const cftft_params* p, void* dev_b
       cudaMemcpy2DAsync(b.data(), eb, base, stride, eb, o, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return fail_free(fail(CFTFT_CUDA_ERROR, "poison: compare"));
+  // (a Fermat element is its lanes and top word; the bytes that pad it to a
+  // multiple of 16 are not part of the value)
+  const size_t vb = R->kind == CFTFT_RING_FERMAT ? (size_t)R->D * 4 + 8 : eb;
   for (u64 i = 0; i < o; ++i)
-    if (std::memcmp(a.data() + i * eb, b.data() + i * eb, eb) != 0)
+    if (std::memcmp(a.data() + i * eb, b.data() + i * eb, vb) != 0)
       return fail_free(fail(CFTFT_POISON_READ, "output " + std::to_string(i) +
                                                    " depends on the cells >= z (read before written)"));
   return fail_free(CFTFT_OK);

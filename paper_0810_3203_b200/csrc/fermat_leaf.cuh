@@ -1371,35 +1371,55 @@ __global__ void __launch_bounds__(256) cs_fold_kernel(std::uint8_t* data, u64 eb
   extern __shared__ u32 s_old[];  // D words (frot only)
   const u64 e = idx ? idx[blockIdx.x] : idx0 + (u64)blockIdx.x * istride;
   std::uint8_t* el = data + e * eb;
-  if (src) {
+  const int* Te = T + e * CL;
+  auto tix = [&](u32 p) { return ((p & ((1u << logS) - 1)) << (logLanes - logS)) | (p >> logS); };
+  bool fused = false;  // pass 1 done while copying
+  if (src && CW == 8) {
+    // 256-bit lanes: every lane is read from the source once, takes its
+    // carry-in in registers and is written into place (no second visit).
+    // Coset-major source (wave_tma.cuh): lane p = coset p mod 2^src_cm, row
+    // p >> src_cm, 1 KB per coset, 16-byte halves swapped on rows with bit 2
+    // set; the top word follows the lanes as usual.  (Reading in source order
+    // and scattering the writes, or staging through shared memory, measured
+    // slower: profiles/r02_experiments.md.)
+    const std::uint8_t* se = src + e * eb;
+    const long long hsrc = *reinterpret_cast<const long long*>(se + (u64)D * 4);
+    for (u32 p = threadIdx.x; p < CL; p += blockDim.x) {
+      u32 off = 32u * p, sw = 0;
+      if (src_cm) {
+        const u32 row = p >> src_cm, cs = p & ((1u << src_cm) - 1);
+        off = (cs << 10) | (row << 5);
+        sw = (row >> 2) & 1u;
+      }
+      const uint4* sp = reinterpret_cast<const uint4*>(se + off);
+      const uint4 lo = __ldcg(sp + sw), hi = __ldcg(sp + (sw ^ 1u));
+      u32 v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      const long long cin = p ? (long long)Te[tix(p - 1)] : -((long long)Te[tix(CL - 1)] + hsrc);
+      long long c = cin;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long x = (long long)v[k] + c;
+        v[k] = (u32)x;
+        c = x >> 32;
+      }
+      uint4* dp = reinterpret_cast<uint4*>(el + 32u * p);
+      dp[0] = make_uint4(v[0], v[1], v[2], v[3]);
+      dp[1] = make_uint4(v[4], v[5], v[6], v[7]);
+      s_pend[p] = (int)c;
+    }
+    fused = true;
+  } else if (src) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src + e * eb);
     uint4* d4 = reinterpret_cast<uint4*>(el);
     const u32 pieces = (4 * D + 8 + 15) / 16;
-    if (src_cm) {
-      // coset-major source (wave_tma.cuh): lane p = coset p mod 2^src_cm,
-      // row p >> src_cm, 1 KB per coset, 16-byte halves swapped on rows
-      // with bit 2 set; the top word follows the lanes as usual
-      const u32 lp = CL * 2;  // 16-byte pieces of the lanes
-      for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) {
-        u32 sx = x;
-        if (x < lp) {
-          const u32 p = x >> 1, h = x & 1u, row = p >> src_cm, cs = p & ((1u << src_cm) - 1);
-          sx = (cs << 6) | (row << 1) | (h ^ ((row >> 2) & 1u));
-        }
-        d4[x] = __ldcg(s4 + sx);
-      }
-    } else {
-      for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) d4[x] = __ldcg(s4 + x);
-    }
+    for (u32 x = threadIdx.x; x < pieces; x += blockDim.x) d4[x] = __ldcg(s4 + x);
     __syncthreads();
   }
-  const int* Te = T + e * CL;
   long long* hip = reinterpret_cast<long long*>(el + (u64)D * 4);
   u32* w = reinterpret_cast<u32*>(el);
   const u32 o = frot ? frot[e] : 0u;
-  auto tix = [&](u32 p) { return ((p & ((1u << logS) - 1)) << (logLanes - logS)) | (p >> logS); };
   // pass 1: every lane takes its carry-in
-  for (u32 p = threadIdx.x; p < CL; p += blockDim.x) {
+  for (u32 p = threadIdx.x; !fused && p < CL; p += blockDim.x) {
     long long cin;
     if (p) {
       cin = Te[tix(p - 1)];
