@@ -127,6 +127,7 @@ struct DevicePlan {
   // per wave: 1 (DIF) / 2 (DIT) when every leaf is a radix-64 network class
   // of that kind the TMA kernel runs
   std::vector<std::uint8_t> tma_wave;
+  std::vector<std::uint8_t> tma_aligned;  // per wave: no loaded slot has a sub-lane pre-rotation
   std::vector<u64> tma_desc_off;  // per wave: first descriptor in tma_descs
   void* tma_descs = nullptr;      // fermat::TmaLeafDesc per leaf of the TMA waves
   std::uint8_t* tma_lay = nullptr;  // coset-major layout bits per wave_slots entry (inside tma_descs)
@@ -406,6 +407,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     for (u64 i = p.waves[w][0]; i < p.waves[w][0] + p.waves[w][1]; ++i)
       dp.wave_loads[w] += (u64)cls[p.leaves[i].cls].nload + cls[p.leaves[i].cls].nstore;
   dp.tma_wave.assign(p.waves.size(), 0);
+  dp.tma_aligned.assign(p.waves.size(), 0);
   std::vector<fermat::TmaLeafDesc> descs;
   dp.tma_desc_off.assign(p.waves.size(), 0);
   for (size_t w = 0; w < p.waves.size(); ++w) {
@@ -441,10 +443,13 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
     dp.tma_wave[w] = (std::uint8_t)((wnet ? wnet : 2u) | (any_prog ? 4u : 0u));
     dp.tma_step = step;
     dp.tma_desc_off[w] = descs.size();
+    dp.tma_aligned[w] = 1;
     for (u64 i = wr[0]; i < wr[0] + wr[1]; ++i) {
       const DevLeaf& lf = p.leaves[i];
       const DevClass& d = cls[lf.cls];
       const bool prog = is_prog(lf.cls);
+      for (u32 k = 0; k < d.nload; ++k)
+        if (p.wave_slots[lf.c0 + 2ull * k] & 255u) dp.tma_aligned[w] = 0;
       fermat::TmaLeafDesc td{};
       td.base = lf.base;
       td.stride = lf.stride;
@@ -1006,7 +1011,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             W.tdesc = static_cast<const fermat::TmaLeafDesc*>(dp.tma_descs) + dp.tma_desc_off[wi];
             W.tlay = dp.tma_lay;
-            W.pfdist = 0;
+            W.tflags = dp.tma_aligned[wi] ? 1u : 0u;
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
             switch (dp.tma_wave[wi]) {
               case 1:

@@ -625,6 +625,28 @@ class Planner {
             const u32 j = (a / (2 * h)) * h + a % h;
             net[(st * 8 + w) * 12 + o] = (u32)std::max(0, qn[lvl][j]) << 16;
           }
+      // Stage B re-gauged (wave_tma.cuh, net8_g): slot j of a stage-B network
+      // is read as x^{g_j} * slot j (a row index and a sign), the g_j chosen
+      // so that seven butterflies need no rotation (both outputs of a
+      // butterfly keep a's gauge; q' = q + G_a - G_b); bits 4..9 of op j < 8:
+      // g_j, bits 10..15 of the other five ops: the residual rotation.
+      for (u32 w = 0; w < 8; ++w) {
+        u32* e = &net[(8 + w) * 12];
+        u32 q[12], g[8], res[12] = {};
+        for (u32 o = 0; o < 12; ++o) q[o] = (e[o] >> 16) & 63u;
+        g[0] = 0;
+        if (kind == 1) {  // DIF: pairs (k, k+4), then (0,2) (1,3) (4,6) (5,7), then (2k, 2k+1)
+          g[1] = q[8]; g[2] = q[4]; g[3] = g[1] + q[5]; g[4] = q[0];
+          g[5] = g[1] + q[1]; g[6] = g[2] + q[2]; g[7] = g[3] + q[3];
+          res[6] = q[6] - q[4]; res[7] = q[7] - q[5];
+        } else {          // DIT: pairs (2k, 2k+1), then (0,2) (1,3) (4,6) (5,7), then (k, k+4)
+          g[1] = q[0]; g[2] = q[4]; g[3] = g[2] + q[1]; g[4] = q[8];
+          g[5] = g[4] + q[2]; g[6] = g[4] + q[6]; g[7] = g[6] + q[3];
+          res[5] = q[5] - q[4]; res[7] = q[7] - q[6];
+        }
+        for (u32 o = 9; o < 12; ++o) res[o] = q[o] - q[8];
+        for (u32 o = 0; o < 12; ++o) e[o] |= (o < 8 ? (g[o] & 63u) << 4 : 0u) | ((res[o] & 63u) << 10);
+      }
       return kind;
     }
     return 0;

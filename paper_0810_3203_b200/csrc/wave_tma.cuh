@@ -8,31 +8,33 @@
 // network (DIF for the TFT, DIT for the ITFT) = two stages of eight 8-point
 // register networks (Planner::wide_network).
 //
-// One 16-warp CTA per SM, two warp roles, two item tiles:
-//  * stage-A warps 0..7: warp w waits for its item's tile (TMA: every loaded
-//    slot's coset box, its tops and, where needed, the element's top word),
-//    settles its 8 slots straight into registers (pre-rotation by whole
-//    cosets = a row index; a sub-lane part = a funnel with the lane below,
-//    whose rows the warp fetched into its own ring one item ahead; the top
-//    word folded into source lane 0; lanes past 2^N negated), runs its
-//    stage-A network and writes the outputs back in place (its slots are its
-//    own), then arrives on the tile's named barrier;
-//  * stage-B warps 8..15: wait on that barrier, read their 8 slots of the
-//    tile into registers, release the tile (warp 8 immediately refills it
-//    with the item two ahead), run the stage-B network and store straight
-//    from registers through the post-rotation (carry-save, coset-major or
-//    natural order).
-// Stage A of item k+1 overlaps stage B of item k; the loads of item k+2 are
-// in flight during both.  Tiles and coset-major chunks are stored with the
-// 32-byte swizzle (the 16-byte halves of row r swapped when bit 2 of r is
-// set -- CU_TENSOR_MAP_SWIZZLE_32B for tensor boxes, the writers' own
-// addressing for coset-major chunks): a warp's 32 rows hit distinct banks.
+// One 16-warp CTA per SM, two groups of 8 warps, each with its own item tile:
+// group g runs stage A then stage B of items k = g (mod 2), so one group's
+// stage B overlaps the other's stage A.  Per item, warp w of the group
+//  * stage A: waits for its own cp.async loads (its 8 stage-A slots: rows,
+//    tops, the element's top word) and the lane-below rows of unaligned slots
+//    (TMA bulk copies / tensor boxes into a per-network ring, issued one item
+//    ahead), settles each slot in place (pre-rotation by whole cosets = a row
+//    index; a sub-lane part = a funnel with the lane below; the top word
+//    folded into source lane 0; lanes past 2^N negated), runs its 8-point
+//    network in registers and writes the outputs back into its own slots;
+//  * stage B (after the group's named barrier): reads its 8 slots re-gauged
+//    (a rotation by whole coset positions is a row index and a sign, so only
+//    five of the twelve butterflies shuffle: net8_g), releases the tile and
+//    starts the loads of the group's next item into it, runs the network and
+//    stores straight from registers through the post-rotation (carry-save,
+//    coset-major or natural order).
+// Tiles and coset-major chunks are stored with the 32-byte swizzle (the
+// 16-byte halves of row r swapped when bit 2 of r is set -- the writers' own
+// addressing, CU_TENSOR_MAP_SWIZZLE_32B for tensor boxes): a warp's 32 rows
+// hit distinct banks.
 //
 // Shared memory (bytes, 1024-aligned base):
 //   tile t (x2)  rows 64 slots x 1 KB | tops 64 x 128 B | top words 64 x 16 B
 //   ring rows    8 warps x 8 slots x 1 KB   (stage A: the lane-below cosets)
 //   ring tops    8 warps x 8 slots x 128 B
-//   mbarriers    full[2], ring[8]
+//   store tables 16 warps x 8 descriptors of 32 B
+//   mbarriers    ring[2][8]
 #pragma once
 
 #include <cuda.h>
@@ -42,6 +44,9 @@
 namespace cftft_b200 {
 namespace fermat {
 
+#ifndef CFTFT_VAR
+#define CFTFT_VAR 0
+#endif
 constexpr int kTmaWarpsA = 8;
 constexpr int kTmaThreads = 32 * 2 * kTmaWarpsA;
 constexpr u32 kTileRows = 0;
@@ -85,14 +90,6 @@ __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u3
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
-}
-__device__ __forceinline__ void pf_box(const CUtensorMap* tm, u32 cls, u32 e) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(tm), "r"(8u * cls), "r"(0u),
-               "r"(e)
-               : "memory");
-}
-__device__ __forceinline__ void pf_bulk(const void* src, u32 bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void named_bar(u32 id, u32 n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
@@ -269,138 +266,60 @@ __device__ __forceinline__ u32 warp_sum(u32 v) {
   return v;
 }
 
-// Stage-B warp 8: the tile loads of item (d, g) into tile `tile` (lane l:
-// slots l and l + 32, their pre / layout entries prefetched), completing on `bar`.
-struct TileLane {
-  u32 pre[2], lay[2];
-};
-__device__ __forceinline__ TileLane tile_lane(const WaveArgs& A, const TmaLeafDesc& d, bool valid, u32 lane) {
-  TileLane t{};
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const u32 slot = lane + 32u * h;
-    if (valid && slot < d.nload) {
-      t.pre[h] = __ldg(A.wslots + d.c0 + 2 * slot);
-      t.lay[h] = __ldg(A.tlay + d.c0 + 2 * slot) | 4u;  // bit 2: loaded
-    }
-  }
-  return t;
-}
-__device__ __forceinline__ void tile_issue(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
-                                           const TmaLeafDesc& d, const TileLane& tl, u32 g, u32 lane, u32 tile,
-                                           u32 bar, u32 step) {
-  u32 bytes = 0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (!(tl.lay[h] & 4u)) continue;
-    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
-    const u32 cA = src_coset(tl.pre[h], g, step);
-    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u;
-    bytes += 1024u + (fresh ? 0u : 128u) + ((cA == 0 || (unal && cA == 1)) ? 16u : 0u);
-  }
-  const u32 tot = warp_sum(bytes);
-  if (lane == 0) mbar_expect_tx(bar, tot);
-  __syncwarp();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (!(tl.lay[h] & 4u)) continue;
-    const u32 slot = lane + 32u * h;
-    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
-    const u32 cA = src_coset(tl.pre[h], g, step);
-    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u, sh = tl.pre[h] >> 31;
-    const u64 e = d.base + (u64)slot * d.stride;
-    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
-    if (tl.lay[h] & 1u)
-      bulk_g2s(tile + kTileRows + slot * 1024u, el + (u64)cA * 1024u, 1024u, bar);
-    else
-      tma_box(tile + kTileRows + slot * 1024u, sh ? tms : tmv, cA, (u32)e, bar);
-    if (!fresh)
-      bulk_g2s(tile + kTileTops + slot * 128u, A.T + (sh ? A.tloc : 0) + e * A.lanes + (u64)cA * 32u, 128u, bar);
-    if (cA == 0 || (unal && cA == 1)) bulk_g2s(tile + kTileHiw + slot * 16u, el + 4ull * A.D, 16u, bar);
-  }
-}
-
-// L2 prefetch of everything an item's tile and rings will load (lane l:
-// slots l and l + 32), issued a few items ahead so that DRAM keeps streaming
-// while shared memory holds only the items in progress.
-__device__ __forceinline__ void tile_prefetch(const WaveArgs& A, const CUtensorMap* tmv, const CUtensorMap* tms,
-                                              const TmaLeafDesc& d, const TileLane& tl, u32 g, u32 lane, u32 step) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (!(tl.lay[h] & 4u)) continue;
-    const u32 slot = lane + 32u * h;
-    const u32 r = tl.pre[h] & 0x3FFFFFFFu;
-    const u32 cA = src_coset(tl.pre[h], g, step);
-    const u32 cB = cA ? cA - 1 : step - 1;
-    const bool unal = (r & 255u) != 0, fresh = (tl.pre[h] >> 30) & 1u, sh = tl.pre[h] >> 31;
-    const u64 e = d.base + (u64)slot * d.stride;
-    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
-    const int* tin = A.T + (sh ? A.tloc : 0) + e * A.lanes;
-    if (tl.lay[h] & 1u) {
-      if (unal && cA)
-        pf_bulk(el + (u64)cB * 1024u, 2048u);
-      else
-        pf_bulk(el + (u64)cA * 1024u, 1024u);
-      if (unal && !cA) pf_bulk(el + (u64)cB * 1024u, 1024u);
-    } else {
-      pf_box(sh ? tms : tmv, cA, (u32)e);
-      if (unal) pf_box(sh ? tms : tmv, cB, (u32)e);
-    }
-    if (!fresh) {
-      if (unal && cA)
-        pf_bulk(tin + (u64)cB * 32u, 256u);
-      else
-        pf_bulk(tin + (u64)cA * 32u, 128u);
-      if (unal && !cA) pf_bulk(tin + (u64)cB * 32u, 128u);
-    }
-  }
-}
-
 // Stage-A warp w: cp.async loads of its own slots of item (d, g) into the
 // group's tile -- rows (swizzled), tops, the element's top word where the
 // item reads source lane 0 (lane j < 8 holds slot j's pre / layout entry).
+// Lanes 4j .. 4j+3 resolve slot j: for natural-layout rows lane 4j + 2b + h
+// copies the 16-byte half h of rows 2i + b (i < 16), so one instruction moves
+// whole 32-byte sectors (two lanes per row); coset-major chunks are copied by
+// the whole warp, 512 contiguous bytes per instruction.
 template <bool DIF>
 __device__ __forceinline__ void warp_load(const WaveArgs& A, const TmaLeafDesc& d, u32 g, u32 w, u32 lane, u32 apre,
-                                          u32 alay, u32 tile, u32 step) {
-  // lane j < 8 resolves slot j once: its source coset's row 0, its tops row,
-  // the element's top word, the row stride and what to load
-  u64 rows = 0, trow = 0, hw = 0;
-  u32 fl = 0;  // bit 0: load, 1: coset-major, 2: tops, 3: top word
-  {
-    const u32 slot = slot_a(DIF ? 1u : 2u, w, lane & 7u);
-    if (lane < 8 && slot < d.nload) {
-      const u32 r = apre & 0x3FFFFFFFu;
-      const u32 cA = src_coset(apre, g, step);
-      const bool unal = (r & 255u) != 0, fresh = (apre >> 30) & 1u, sh = apre >> 31;
-      const u64 e = d.base + (u64)slot * d.stride;
-      const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
-      rows = reinterpret_cast<u64>(el + ((alay & 1u) ? (u64)cA * 1024u : 32ull * cA));
-      trow = reinterpret_cast<u64>(A.T + (sh ? A.tloc : 0) + e * A.lanes + cA * 32u);
-      hw = reinterpret_cast<u64>(el + 4ull * A.D);
-      fl = 1u | ((alay & 1u) << 1) | (fresh ? 0u : 4u) | ((cA == 0 || (unal && cA == 1)) ? 8u : 0u);
-    }
-  }
-  const u32 rstride = 32u * step;
-#pragma unroll 1
-  for (u32 j = 0; j < 8; ++j) {
-    const u32 f = __shfl_sync(0xffffffffu, fl, (int)j);
-    if (!(f & 1u)) break;  // (later slots are truncated too)
-    const u32 slot = slot_a(DIF ? 1u : 2u, w, j);
-    const u32 dst = tile + kTileRows + slot * 1024u;
-    const std::uint8_t* rp = reinterpret_cast<const std::uint8_t*>(__shfl_sync(0xffffffffu, rows, (int)j));
-    if (f & 2u) {  // coset-major chunks are stored swizzled: a linear copy
-      cp_async16(dst + 32u * lane, rp + 32u * lane);
-      cp_async16(dst + 32u * lane + 16u, rp + 32u * lane + 16u);
+                                           u32 alay, u32 tile, u32 step) {
+  const u32 j = lane >> 2, qd = lane & 3u, b = qd >> 1, h = qd & 1u;
+  const u32 pre = __shfl_sync(0xffffffffu, apre, (int)j), lay = __shfl_sync(0xffffffffu, alay, (int)j);
+  const u32 slot = slot_a(DIF ? 1u : 2u, w, j);
+  u64 chunk = 0;  // coset-major slots: the source chunk (copied by the whole warp below)
+  if (slot < d.nload) {
+    const u32 r = pre & 0x3FFFFFFFu;
+    const u32 cA = src_coset(pre, g, step);
+    const bool unal = (r & 255u) != 0, fresh = (pre >> 30) & 1u, sh = pre >> 31;
+    const u64 e = d.base + (u64)slot * d.stride;
+    const std::uint8_t* el = (sh ? A.data2 : A.data) + e * A.elem_bytes;
+    if (lay & 1u) {
+      chunk = reinterpret_cast<u64>(el + (u64)cA * 1024u);
     } else {
-      const std::uint8_t* src = rp + (u64)rstride * lane;
-      cp_async16_l2(dst + sw_off(lane, 0), src);
-      cp_async16_l2(dst + sw_off(lane, 1), src + 16);
+      const u32 dst = tile + kTileRows + slot * 1024u + 32u * b;
+      const std::uint8_t* src = el + 32ull * cA + (u64)(32u * step) * b + 16u * h;
+      const u64 inc = 64ull * step;
+      const u32 d0 = dst + 16u * h, d1 = dst + 16u * (h ^ 1u);
+#pragma unroll
+      for (u32 i = 0; i < 16; ++i) {
+        cp_async16_l2(((i >> 1) & 1u ? d1 : d0) + 64u * i, src);
+        src += inc;
+      }
     }
-    if (f & 4u)
-      cp_async4(tile + kTileTops + slot * 128u + 4u * lane,
-                reinterpret_cast<const int*>(__shfl_sync(0xffffffffu, trow, (int)j)) + lane);
-    const u64 h = __shfl_sync(0xffffffffu, hw, (int)j);
-    if (lane == 0 && (f & 8u)) cp_async8(tile + kTileHiw + slot * 16u, reinterpret_cast<const void*>(h));
+    if (!fresh) {
+      const int* tr = A.T + (sh ? A.tloc : 0) + e * A.lanes + cA * 32u + 8u * qd;
+      const u32 td = tile + kTileTops + slot * 128u + 32u * qd;
+      cp_async16(td, tr);
+      cp_async16(td + 16u, tr + 4);
+    }
+    if (qd == 0 && (cA == 0 || (unal && cA == 1))) cp_async8(tile + kTileHiw + slot * 16u, el + 4ull * A.D);
+  }
+  // coset-major chunks are stored swizzled: a linear copy, 512 contiguous
+  // bytes per instruction
+  const u32 cm = __ballot_sync(0xffffffffu, chunk != 0);
+  if (cm) {
+#pragma unroll
+    for (u32 k = 0; k < 8; ++k) {
+      const u64 cp = __shfl_sync(0xffffffffu, chunk, (int)(4u * k));
+      if (!cp) continue;  // (warp-uniform)
+      const u32 dst = tile + kTileRows + slot_a(DIF ? 1u : 2u, w, k) * 1024u + 16u * lane;
+      const std::uint8_t* src = reinterpret_cast<const std::uint8_t*>(cp) + 16u * lane;
+      cp_async16(dst, src);
+      cp_async16(dst + 512u, src + 512u);
+    }
   }
   cp_async_commit();
 }
@@ -451,6 +370,22 @@ __device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u
   const bool fresh = (pre >> 30) & 1u;
   Ch<8> x;
   int t;
+#if CFTFT_VAR & 1
+  if (r < 256u && c >= 2) {
+    // the common unaligned case (warp-uniform): no whole-lane rotation and no
+    // lane-0 neighbourhood -- source lane = this lane, the lane below it =
+    // the ring's row of the same position, no signs, no top word
+    Ch<8> b;
+    lds_row(x, rows, pos);
+    lds_row(b, brows, pos);
+    const int tb = fresh ? 0 : sh_ld32(btops + 4u * pos);
+    Ch<8> out;
+    t = unal_combine8(out, b, x, tb, r);
+    sts_row(rows, pos, out);
+    sh_st32(tops + 4u * pos, t);
+    return;
+  }
+#endif
   if (r == 0) {  // c == 0: only the top word of row 0 to fold
     lds_row(x, rows, pos);
     t = fresh ? 0 : sh_ld32(tops + 4u * pos);
@@ -513,42 +448,84 @@ __device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u
   sh_st32(tops + 4u * pos, t);
 }
 
-// Stage-B rotated butterflies skip the shuffles when the op's q is zero
-__device__ __forceinline__ void bfly_any(Ch<8>& a, int& ta, Ch<8>& b, int& tb, u32 opv, int oi, u32 pos) {
-  const u32 qv = (__shfl_sync(0xffffffffu, opv, oi) >> 16) & 63u;
-  if (qv == 0)
-    bfly_plain(a, ta, b, tb);
-  else
-    bfly_rot(a, ta, b, tb, opv, oi, pos);
+// ---- stage B with re-gauged inputs.  A rotation of a whole slot by g coset
+// positions is a row index (and a per-lane sign) when the slot is read from
+// the tile, so stage B reads slot j as x^{g_j} * slot j with the g_j chosen
+// (Planner::wide_network, bits 4..9 of op j < 8) such that seven of the twelve
+// butterflies need no rotation at all; the other five (the ops of kRotDif /
+// kRotDit) keep a residual rotation (bits 10..15).  Signs are carried per slot
+// (sg bit j: this lane's row of slot j is held negated) and folded into the
+// butterflies' +- (ch_pm8): both outputs of a butterfly take a's gauge and
+// sign, every chain ends in slot 0 (g_0 = 0), so the outputs are the plain
+// network's.
+template <bool DIF>
+__device__ __forceinline__ void stage_b_load_g(Ch<8> (&x)[8], int (&tx)[8], u32& sg, u32 wb, u32 pos, u32 opb,
+                                               u32 tile) {
+  const u32 wnet = DIF ? 1u : 2u;
+  sg = 0;
+#pragma unroll
+  for (u32 j = 0; j < 8; ++j) {
+    const u32 slot = slot_b(wnet, wb, j);
+    const u32 g = (__shfl_sync(0xffffffffu, opb, (int)j) >> 4) & 63u;
+    const u32 gq = g & 31u, row = (pos - gq) & 31u;
+    sg |= (u32)((pos < gq) != (g >= 32u)) << j;
+    lds_row(x[j], tile + kTileRows + slot * 1024u, row);
+    tx[j] = sh_ld32(tile + kTileTops + slot * 128u + 4u * row);
+  }
+}
+template <u32 MASK, int J, int IA, int IB>
+__device__ __forceinline__ void bfly_g(Ch<8> (&x)[8], int (&t)[8], u32& sg, u32 opv, u32 pos) {
+  Ch<8> y0, y1;
+  int t0, t1;
+  if constexpr ((MASK >> J) & 1u) {
+    const u32 qv = (__shfl_sync(0xffffffffu, opv, J) >> 10) & 63u;
+    const u32 qq = qv & 31u;
+    const u32 pl = (pos - qq) & 31u;
+    Ch<8> bp;
+#pragma unroll
+    for (int wd = 0; wd < 8; ++wd) bp.w[wd] = __shfl_sync(0xffffffffu, x[IB].w[wd], (int)pl);
+    const int tbp = __shfl_sync(0xffffffffu, t[IB], (int)pl);
+    const u32 sb = __shfl_sync(0xffffffffu, sg, (int)pl) >> IB;
+    const bool neg = (((sg >> IA) ^ sb) & 1u) != (u32)((pos < qq) != (qv >= 32u));
+    ch_pm8(y0, t0, y1, t1, x[IA], t[IA], bp, tbp, neg);
+  } else {
+    const bool neg = ((sg >> IA) ^ (sg >> IB)) & 1u;
+    ch_pm8(y0, t0, y1, t1, x[IA], t[IA], x[IB], t[IB], neg);
+  }
+  x[IA] = y0;
+  t[IA] = t0;
+  x[IB] = y1;
+  t[IB] = t1;
+  sg = (sg & ~(1u << IB)) | (((sg >> IA) & 1u) << IB);
 }
 template <bool DIF>
-__device__ __forceinline__ void net8_b(Ch<8> (&x)[8], int (&t)[8], u32 opv, u32 pos) {
+__device__ __forceinline__ void net8_g(Ch<8> (&x)[8], int (&t)[8], u32& sg, u32 opv, u32 pos) {
   if constexpr (DIF) {
-    bfly_any(x[0], t[0], x[4], t[4], opv, 0, pos);
-    bfly_any(x[1], t[1], x[5], t[5], opv, 1, pos);
-    bfly_any(x[2], t[2], x[6], t[6], opv, 2, pos);
-    bfly_any(x[3], t[3], x[7], t[7], opv, 3, pos);
-    bfly_any(x[0], t[0], x[2], t[2], opv, 4, pos);
-    bfly_any(x[1], t[1], x[3], t[3], opv, 5, pos);
-    bfly_any(x[4], t[4], x[6], t[6], opv, 6, pos);
-    bfly_any(x[5], t[5], x[7], t[7], opv, 7, pos);
-    bfly_any(x[0], t[0], x[1], t[1], opv, 8, pos);
-    bfly_any(x[2], t[2], x[3], t[3], opv, 9, pos);
-    bfly_any(x[4], t[4], x[5], t[5], opv, 10, pos);
-    bfly_any(x[6], t[6], x[7], t[7], opv, 11, pos);
+    bfly_g<kRotDif, 0, 0, 4>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 1, 1, 5>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 2, 2, 6>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 3, 3, 7>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 4, 0, 2>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 5, 1, 3>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 6, 4, 6>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 7, 5, 7>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 8, 0, 1>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 9, 2, 3>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 10, 4, 5>(x, t, sg, opv, pos);
+    bfly_g<kRotDif, 11, 6, 7>(x, t, sg, opv, pos);
   } else {
-    bfly_any(x[0], t[0], x[1], t[1], opv, 0, pos);
-    bfly_any(x[2], t[2], x[3], t[3], opv, 1, pos);
-    bfly_any(x[4], t[4], x[5], t[5], opv, 2, pos);
-    bfly_any(x[6], t[6], x[7], t[7], opv, 3, pos);
-    bfly_any(x[0], t[0], x[2], t[2], opv, 4, pos);
-    bfly_any(x[1], t[1], x[3], t[3], opv, 5, pos);
-    bfly_any(x[4], t[4], x[6], t[6], opv, 6, pos);
-    bfly_any(x[5], t[5], x[7], t[7], opv, 7, pos);
-    bfly_any(x[0], t[0], x[4], t[4], opv, 8, pos);
-    bfly_any(x[1], t[1], x[5], t[5], opv, 9, pos);
-    bfly_any(x[2], t[2], x[6], t[6], opv, 10, pos);
-    bfly_any(x[3], t[3], x[7], t[7], opv, 11, pos);
+    bfly_g<kRotDit, 0, 0, 1>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 1, 2, 3>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 2, 4, 5>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 3, 6, 7>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 4, 0, 2>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 5, 1, 3>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 6, 4, 6>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 7, 5, 7>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 8, 0, 4>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 9, 1, 5>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 10, 2, 6>(x, t, sg, opv, pos);
+    bfly_g<kRotDit, 11, 3, 7>(x, t, sg, opv, pos);
   }
 }
 
@@ -683,13 +660,6 @@ __device__ __forceinline__ void stage_b_store(const WaveArgs& A, Ch<8> (&x)[8], 
     if (L0 == h1.y) __stcg(reinterpret_cast<long long*>(el + 4ull * A.D), 0ll);
   }
 }
-template <bool DIF>
-__device__ __forceinline__ void stage_b_run(const WaveArgs& A, Ch<8> (&x)[8], int (&tx)[8], u32 c, u32 pos, u32 opb,
-                                            u32 tab, u32 logS) {
-  net8_b<DIF>(x, tx, opb, pos);
-  stage_b_store(A, x, tx, c, pos, tab, logS);
-}
-
 // ---- phase programs (Planner::tma_program): 64-slot classes that are not
 // full networks, e.g. the truncated ITFT leaves.  Stage A only settles the
 // warp's slots in the tile; then every phase runs its ops on the tile, warp w
@@ -847,7 +817,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   u32 pre, lay;
   lane_info(d, i < items, pre, lay);
   if (i < items) warp_load<DIF>(A, d, i & (step - 1), w, lane, pre, lay, tile, step);
-  if (grp == 0)
+  // waves without sub-lane pre-rotations never touch the lane-below rings
+  const bool ringed = !((CFTFT_VAR & 2) && (A.tflags & 1u));
+  if (grp == 0 && ringed)
     ring_issue<DIF>(A, &tm_view, &tm_shadow, d, i & (step - 1), i < items, w, lane, pre, lay, sm_s, ringbar(0),
                     step);
   u32 n = 0;  // this group's item count
@@ -868,7 +840,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     // ---- stage A
     cp_async_wait<0>();
     __syncwarp();
-    mbar_wait(ringbar(grp), n & 1u);
+    if (ringed) mbar_wait(ringbar(grp), n & 1u);
     // program items: word 0 = phases | network rows << 8 (the DIT kernel runs
     // phase 0 of those rows as stage-A networks in registers)
     const u32 phdr = prog ? __ldg(A.wops + d.wop_begin) : 0u;
@@ -882,8 +854,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       stage_a<DIF>(d, c, w, pos, pre, opa, tile, sm_s, logS);
     }
     // the ring is free: the next item's lane-below rows start moving
-    ring_issue<DIF>(A, &tm_view, &tm_shadow, dn, in & (step - 1), in < items, w, lane, npre, nlay, sm_s,
-                    ringbar(grp ^ 1u), step);
+    if (ringed)
+      ring_issue<DIF>(A, &tm_view, &tm_shadow, dn, in & (step - 1), in < items, w, lane, npre, nlay, sm_s,
+                      ringbar(grp ^ 1u), step);
     slot_table<DIF>(A, d, w, lane, tab);
     named_bar(1u + grp, 256u);  // the group's stage-A outputs are in the tile
     if (prog) {
@@ -898,13 +871,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     // ---- stage B
     Ch<8> x[8];
     int tx[8];
-    stage_b_load<DIF>(x, tx, w, pos, tile);
+    u32 sg = 0;
+    if (prog)
+      stage_b_load<DIF>(x, tx, w, pos, tile);
+    else
+      stage_b_load_g<DIF>(x, tx, sg, w, pos, opb, tile);
     named_bar(1u + grp, 256u);  // every warp of the group holds its rows: the tile is free
     if (i2 < items) warp_load<DIF>(A, d2, i2 & (step - 1), w, lane, pre2, lay2, tile, step);
     if (prog)
       stage_b_store(A, x, tx, c, pos, tab, logS);
-    else if (!(A.debug & 512u))
-      stage_b_run<DIF>(A, x, tx, c, pos, opb, tab, logS);
+    else if (!(A.debug & 512u)) {
+      net8_g<DIF>(x, tx, sg, opb, pos);
+      stage_b_store(A, x, tx, c, pos, tab, logS);
+    }
     __syncwarp();  // the slot table is rewritten for the next item
     i = i2;
     d = d2;
