@@ -91,19 +91,19 @@ def hbm_peak():
 
 def load_traffic(cfg: str):
     """The committed ncu DRAM traffic of a config (tools/traffic.py), only when
-    it was measured on this very build (sha256 of the loaded library)."""
-    import hashlib
+    it was measured on a build of these very sources (sha256 over csrc/ and
+    include/: the .so bytes themselves differ from one nvcc run to the next)."""
+    from paper_0810_3203_b200._build import source_sha256
 
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as fh:
             t = json.load(fh).get(cfg)
-        lib = os.path.join(ROOT, "paper_0810_3203_b200", "lib", "libcftft_b200.so")
         if not isinstance(t, dict):
             return None, "no ncu traffic for this config"
-        if hashlib.sha256(open(lib, "rb").read()).hexdigest() != t.get("so_sha256"):
-            return None, "profiles/traffic.json is from another build of the library (stale): not reported"
-        return t, "ncu dram__bytes_read.sum + dram__bytes_write.sum, this build (profiles/traffic.json)"
+        if source_sha256() != t.get("source_sha256"):
+            return None, "profiles/traffic.json is from other library sources (stale): not reported"
+        return t, "ncu dram__bytes_read.sum + dram__bytes_write.sum, these sources (profiles/traffic.json)"
     except Exception:
         return None, "no profiles/traffic.json"
 

@@ -43,6 +43,23 @@ def _stale() -> bool:
     return False
 
 
+def source_sha256() -> str:
+    """sha256 over the library's sources (csrc/ and include/, sorted by name):
+    identifies a build independently of the .so bytes, which nvcc does not
+    reproduce from one run to the next."""
+    import hashlib
+
+    h = hashlib.sha256()
+    inc = os.path.join(os.path.dirname(PKG), "include")
+    for d in (CSRC, inc):
+        for f in sorted(os.listdir(d)):
+            if f.endswith((".cu", ".cuh", ".hpp", ".h")):
+                h.update(f.encode())
+                with open(os.path.join(d, f), "rb") as fh:
+                    h.update(fh.read())
+    return h.hexdigest()
+
+
 def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB

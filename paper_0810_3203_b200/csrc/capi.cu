@@ -1001,6 +1001,7 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
                                          dp.tma_step))
                 return e;
               if (int e = set_smem_bytes(fermat::coset_tma_kernel<true, false>, fermat::kTmaSmem)) return e;
+              if (int e = set_smem_bytes(fermat::coset_tma_kernel<true, false, true>, fermat::kTmaSmem)) return e;
               if (int e = set_smem_bytes(fermat::coset_tma_kernel<false, false>, fermat::kTmaSmem)) return e;
               if (int e = set_smem_bytes(fermat::coset_tma_kernel<true, true>, fermat::kTmaSmem)) return e;
               if (int e = set_smem_bytes(fermat::coset_tma_kernel<false, true>, fermat::kTmaSmem)) return e;
@@ -1011,11 +1012,13 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             W.tdesc = static_cast<const fermat::TmaLeafDesc*>(dp.tma_descs) + dp.tma_desc_off[wi];
             W.tlay = dp.tma_lay;
-            W.tflags = dp.tma_aligned[wi] ? 1u : 0u;
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
             switch (dp.tma_wave[wi]) {
               case 1:
-                fermat::coset_tma_kernel<true, false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                if (dp.tma_aligned[wi])
+                  fermat::coset_tma_kernel<true, false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
+                else
+                  fermat::coset_tma_kernel<true, false, true><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);
                 break;
               case 2:
                 fermat::coset_tma_kernel<false, false><<<g, fermat::kTmaThreads, fermat::kTmaSmem, st>>>(tm_view, tm_shadow, W);

@@ -47,7 +47,6 @@ struct WaveArgs {
   u32 debug;            // CFTFT_DEBUG_SKIP bits (experiments; results wrong when set)
   const void* tdesc;    // coset_tma_kernel: per-leaf descriptors of the wave (TmaLeafDesc)
   const std::uint8_t* tlay;  // coset_tma_kernel: per slot entry of wslots, bit 0 input / bit 1 output coset-major
-  u32 tflags;                // coset_tma_kernel: bit 0 = no loaded slot of the wave has a sub-lane pre-rotation
 };
 __device__ __forceinline__ u32 wave_tix(const WaveArgs& A, u32 p) {
   return ((p & ((1u << A.logS) - 1)) << (A.logLanes - A.logS)) | (p >> A.logS);

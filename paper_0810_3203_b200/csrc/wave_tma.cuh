@@ -44,9 +44,6 @@
 namespace cftft_b200 {
 namespace fermat {
 
-#ifndef CFTFT_VAR
-#define CFTFT_VAR 0
-#endif
 constexpr int kTmaWarpsA = 8;
 constexpr int kTmaThreads = 32 * 2 * kTmaWarpsA;
 constexpr u32 kTileRows = 0;
@@ -364,17 +361,18 @@ __device__ __forceinline__ void ring_issue(const WaveArgs& A, const CUtensorMap*
 // that reads X as A and the lane that reads X as B always split X the same
 // way, and across 2^N == -1 (output lane 0 taking lane C-1's high bits) the
 // parts are exact negatives.
+template <bool FAST>
 __device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u32 tops, u32 hiw, u32 brows,
                                             u32 btops, u32 logS) {
   const u32 r = pre & 0x3FFFFFFFu;
   const bool fresh = (pre >> 30) & 1u;
   Ch<8> x;
   int t;
-#if CFTFT_VAR & 1
-  if (r < 256u && c >= 2) {
-    // the common unaligned case (warp-uniform): no whole-lane rotation and no
-    // lane-0 neighbourhood -- source lane = this lane, the lane below it =
-    // the ring's row of the same position, no signs, no top word
+  if (FAST && r < 256u && c >= 2) {
+    // the common case of the TFT's unaligned waves (warp-uniform; FAST: the
+    // kernel instance those waves run): no whole-lane rotation and no lane-0
+    // neighbourhood -- source lane = this lane, the lane below it = the
+    // ring's row of the same position, no signs, no top word
     Ch<8> b;
     lds_row(x, rows, pos);
     lds_row(b, brows, pos);
@@ -385,7 +383,6 @@ __device__ __forceinline__ void settle_slot(u32 pre, u32 c, u32 pos, u32 rows, u
     sh_st32(tops + 4u * pos, t);
     return;
   }
-#endif
   if (r == 0) {  // c == 0: only the top word of row 0 to fold
     lds_row(x, rows, pos);
     t = fresh ? 0 : sh_ld32(tops + 4u * pos);
@@ -531,9 +528,9 @@ __device__ __forceinline__ void net8_g(Ch<8> (&x)[8], int (&t)[8], u32& sg, u32 
 
 // stage A of one item for warp w (tile `tile`): settle in place, load,
 // network, write back
-template <bool DIF>
+template <bool DIF, bool FAST, class Settled>
 __device__ __forceinline__ void stage_a(const TmaLeafDesc& d, u32 c, u32 w, u32 pos, u32 apre, u32 opa, u32 tile,
-                                        u32 sm_s, u32 logS) {
+                                        u32 sm_s, u32 logS, Settled settled) {
   const u32 wnet = DIF ? 1u : 2u;
   u32 tvalid = 0;  // bit j: the slot's tops row is valid
 #pragma unroll 1
@@ -545,12 +542,13 @@ __device__ __forceinline__ void stage_a(const TmaLeafDesc& d, u32 c, u32 w, u32 
       if (!((pre >> 30) & 1u)) tvalid |= 1u << j;
       continue;
     }
-    settle_slot(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
+    settle_slot<FAST>(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
                 tile + kTileHiw + slot * 16u, sm_s + kRingRows + (w * 8u + j) * 1024u,
                 sm_s + kRingTops + (w * 8u + j) * 128u, logS);
     tvalid |= 1u << j;
   }
   __syncwarp();
+  settled();  // the warp's ring is free
   Ch<8> x[8];
   int tx[8];
 #pragma unroll
@@ -681,7 +679,7 @@ __device__ __forceinline__ void stage_a_settle(const TmaLeafDesc& d, u32 c, u32 
       if ((pre >> 30) & 1u) sh_st32(tile + kTileTops + slot * 128u + 4u * pos, 0);
       continue;
     }
-    settle_slot(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
+    settle_slot<false>(pre, c, pos, tile + kTileRows + slot * 1024u, tile + kTileTops + slot * 128u,
                 tile + kTileHiw + slot * 16u, sm_s + kRingRows + (w * 8u + j) * 1024u,
                 sm_s + kRingTops + (w * 8u + j) * 128u, logS);
   }
@@ -777,7 +775,9 @@ __device__ __forceinline__ void prog_ops(const u32* prog, u32 desc, u32 lane, u3
 
 // PROG: the wave has phase-program items (a separate instance, so the
 // network-only kernels keep their register allocation)
-template <bool DIF, bool PROG>
+// UNAL: the instance of the TFT's network waves with sub-lane pre-rotations
+// (settle_slot's fast path)
+template <bool DIF, bool PROG, bool UNAL = false>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     coset_tma_kernel(const __grid_constant__ CUtensorMap tm_view, const __grid_constant__ CUtensorMap tm_shadow,
                      WaveArgs A) {
@@ -817,9 +817,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   u32 pre, lay;
   lane_info(d, i < items, pre, lay);
   if (i < items) warp_load<DIF>(A, d, i & (step - 1), w, lane, pre, lay, tile, step);
-  // waves without sub-lane pre-rotations never touch the lane-below rings
-  const bool ringed = !((CFTFT_VAR & 2) && (A.tflags & 1u));
-  if (grp == 0 && ringed)
+  if (grp == 0)
     ring_issue<DIF>(A, &tm_view, &tm_shadow, d, i & (step - 1), i < items, w, lane, pre, lay, sm_s, ringbar(0),
                     step);
   u32 n = 0;  // this group's item count
@@ -840,23 +838,30 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     // ---- stage A
     cp_async_wait<0>();
     __syncwarp();
-    if (ringed) mbar_wait(ringbar(grp), n & 1u);
+    mbar_wait(ringbar(grp), n & 1u);
     // program items: word 0 = phases | network rows << 8 (the DIT kernel runs
     // phase 0 of those rows as stage-A networks in registers)
     const u32 phdr = prog ? __ldg(A.wops + d.wop_begin) : 0u;
     const bool pnet = prog && !DIF && ((phdr >> (8 + w)) & 1u);
-    if (pnet) {
-      const u32 opn = lane < 12 ? __ldg(A.wops + d.wop_begin + 1 + 8 * (phdr & 0xFFu) + 12 * w + lane) : 0u;
-      stage_a<DIF>(d, c, w, pos, pre, opn, tile, sm_s, logS);
-    } else if (prog) {
-      stage_a_settle<DIF>(d, c, w, pos, pre, tile, sm_s, logS);
-    } else if (!(A.debug & 256u)) {
-      stage_a<DIF>(d, c, w, pos, pre, opa, tile, sm_s, logS);
-    }
-    // the ring is free: the next item's lane-below rows start moving
-    if (ringed)
+    // As soon as the warp has settled its slots its ring is free: the next
+    // item's lane-below rows (the other group's) start moving, and that
+    // group's stage A may begin -- this hand-off also keeps the two groups
+    // half an item apart.
+    auto ring_next = [&]() {
       ring_issue<DIF>(A, &tm_view, &tm_shadow, dn, in & (step - 1), in < items, w, lane, npre, nlay, sm_s,
                       ringbar(grp ^ 1u), step);
+    };
+    if (pnet) {
+      const u32 opn = lane < 12 ? __ldg(A.wops + d.wop_begin + 1 + 8 * (phdr & 0xFFu) + 12 * w + lane) : 0u;
+      stage_a<DIF, false>(d, c, w, pos, pre, opn, tile, sm_s, logS, ring_next);
+    } else if (prog) {
+      stage_a_settle<DIF>(d, c, w, pos, pre, tile, sm_s, logS);
+      ring_next();
+    } else if (A.debug & 256u) {
+      ring_next();
+    } else {
+      stage_a<DIF, UNAL>(d, c, w, pos, pre, opa, tile, sm_s, logS, ring_next);
+    }
     slot_table<DIF>(A, d, w, lane, tab);
     named_bar(1u + grp, 256u);  // the group's stage-A outputs are in the tile
     if (prog) {

@@ -1,18 +1,18 @@
 """profiles/traffic.json from an ncu launch list of one TFT + one ITFT of a
 config (the `--metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum` pass): per kernel name, the DRAM bytes per launch;
-the whole step's DRAM bytes; and the sha256 of the library that ran, so that
-bench.py reports the figures only for the same build.
+the whole step's DRAM bytes; and the sha256 of the library's sources, so that
+bench.py reports the figures only for a build of the same sources.
 
 usage: python tools/traffic.py CONFIG launches.csv [more.csv ...]"""
 import csv
-import hashlib
 import json
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_0810_3203_b200", "lib", "libcftft_b200.so")
+sys.path.insert(0, ROOT)
+from paper_0810_3203_b200._build import source_sha256  # noqa: E402
 
 
 def launches(path):
@@ -47,7 +47,7 @@ def main():
     except Exception:
         allc = {}
     allc = {k: v for k, v in allc.items() if isinstance(v, dict)}
-    allc[cfg] = {"so_sha256": hashlib.sha256(open(LIB, "rb").read()).hexdigest(),
+    allc[cfg] = {"source_sha256": source_sha256(),
                  "step_dram_bytes": step, "step_ms_serialised": step_ms, "per_kernel": per,
                  "source": [os.path.relpath(p, ROOT) for p in paths],
                  "note": "ncu --clock-control none, one TFT + one ITFT: per-launch times are cold-cache and "
