@@ -360,7 +360,7 @@ def run_distributed(args, cf, po, dist, ctx, N, L, z, n, desc, rank, world, loca
     nd = NcclDist(ctx)
     pt, pi = cf.TransformParams(L, 0, z, n), cf.TransformParams(L, 0, n, n, 0)
     geo_f, geo_i = nd.geometry(pt), nd.geometry(pi, inverse=True)
-    g = DistGeometry(M, L, z, n, world)
+    g = DistGeometry(M, L, z, n, world, l1=int(geo_f["L1"]).bit_length() - 1)
     rows_local = geo_f["col_elems"]
     # this rank's column slab: seeded uniform limbs in rows < z1 + 1 (inputs)
     rng = np.random.default_rng(po.mix_seed(42, 5 + rank))

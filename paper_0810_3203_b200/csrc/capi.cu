@@ -546,8 +546,7 @@ int upload(cftft_ring* R, DevicePlan& dp, cudaStream_t st) {
 // Planning geometry of one transform of length L.  Fermat: coset leaves use
 // lanes of `cw` words, chosen so that the reference's top-level split yields
 // sub-transforms whose internal rotations are whole lanes (M / sqrt(L) bits).
-// allow_wide = false: radix-8 waves only (batch plans: sub-transforms of one
-// pass are at most sqrt(L) long, where radix-64 leaves do not pay)
+// allow_wide = false: radix-8 waves only
 RingShape shape_of(const cftft_ring* R, u64 L, DevicePlan* dp, bool allow_wide = true) {
   RingShape rs;
   rs.fermat = (R->kind == CFTFT_RING_FERMAT);
@@ -1012,6 +1011,11 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
             W.gpl = (u32)std::max<u64>(1, wr[3]);
             W.tdesc = static_cast<const fermat::TmaLeafDesc*>(dp.tma_descs) + dp.tma_desc_off[wi];
             W.tlay = dp.tma_lay;
+            // waves with sub-lane pre-rotations read every coset twice (as rows and
+            // as the next coset's lane-below rows): runs of adjacent cosets per CTA
+            // keep the second read in L2 (measured: 8 for the TFT's waves, 2 for
+            // the ITFT's network waves, none for aligned and program waves)
+            W.runlog = dp.tma_aligned[wi] ? 0u : dp.tma_wave[wi] == 1 ? 3u : dp.tma_wave[wi] == 2 ? 1u : 0u;
             const unsigned g = (unsigned)std::min<u64>(wr[1] * W.gpl, (u64)sms);
             switch (dp.tma_wave[wi]) {
               case 1:
@@ -1908,7 +1912,9 @@ int cftft_gpu_batch(const cftft_ring* cring, int inverse, const cftft_subtransfo
           it2 = std::get<1>(it2->first) >= 3 ? R->cache.erase(it2) : std::next(it2);
       }
       auto np = std::make_unique<DevicePlan>();
-      const RingShape rs = shape_of(R, v[0].L, np.get(), false);
+      // radix-64 leaves where the sub-transforms have them (the multi-GPU
+      // slabs of a wide ring: columns of 64, rows of L / 64)
+      const RingShape rs = shape_of(R, v[0].L, np.get(), true);
       try {
         np->host = best_plan(rs, [&](Planner& pl) { return pl.build_batch(inverse != 0, v, policy); });
       } catch (const std::exception& ex) {
@@ -2079,6 +2085,19 @@ int dev_table(const std::vector<u64>& h, u64** out, cudaStream_t st) {
   CUDA_TRY(cudaMemcpyAsync(*out, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
   return CFTFT_OK;
 }
+// the ring's transforms of length L run radix-64 coset leaves: the slabs take
+// the (6, ell - 6) split of the single-GPU plan
+int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    return 148;
+  return sms;
+}
+bool dist_wide(const cftft_ring* R, u64 L) {
+  DevicePlan geo;
+  return shape_of(R, L, &geo).wide;
+}
 int check_dist(const cftft_dist* d, const cftft_params* p, int inverse, int policy, u64 esb) {
   if (!d || !d->ring || !p) return fail(CFTFT_INVALID_PARAMS, "null argument");
   if (int rc = validate(d->ring, inverse != 0, p, policy)) return rc;
@@ -2140,7 +2159,7 @@ int cftft_dist_geometry(const cftft_dist* d, const cftft_params* p, int inverse,
   if (!d || !p || !out) return fail(CFTFT_INVALID_PARAMS, "null argument");
   if (int rc = validate(d->ring, inverse != 0, p, policy)) return rc;
   const dist::Geometry g(d->ring->M, p->length, p->input_count, p->output_count, (u64)d->world, policy,
-                         inverse != 0, inverse ? p->want_next : 0);
+                         inverse != 0, inverse ? p->want_next : 0, dist_wide(d->ring, p->length));
   const u64 r = (u64)d->rank;
   const u64 v[8] = {g.c0[r], g.c1[r], g.r0[r], g.r1[r], g.L1, g.L2, g.L1 * g.width(r), g.nrows(r) * g.L2};
   std::memcpy(out, v, sizeof v);
@@ -2153,7 +2172,8 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
   auto& nc = dist::nccl();
   auto st = static_cast<cudaStream_t>(stream);
   const cftft_ring* R = d->ring;
-  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, false, 0);
+  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, false, 0,
+                         dist_wide(R, p->length));
   const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me), nr = g.nrows(me);
   const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
   // 1. column TFTs (transform.hpp:175-180)
@@ -2190,7 +2210,7 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
     tab.insert(tab.end(), qw.begin(), qw.end());
     u64* dt = nullptr;
     if (int rc = dev_table(tab, &dt, st)) return rc;
-    dist::unpack_rows_kernel<<<(unsigned)(nr * P), 256, 0, st>>>(static_cast<std::uint8_t*>(rowslab), recv, esb, nr,
+    dist::unpack_rows_kernel<<<dist::copy_grid(nr * P, sm_count()), 256, 0, st>>>(static_cast<std::uint8_t*>(rowslab), recv, esb, nr,
                                                                   g.L2, dt, dt + P, dt + 2 * P, (u32)P);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(dt, st));
@@ -2209,7 +2229,8 @@ int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowsla
   auto st = static_cast<cudaStream_t>(stream);
   const cftft_ring* R = d->ring;
   const int f = p->want_next;
-  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, true, f);
+  const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, true, f,
+                         dist_wide(R, p->length));
   const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me);
   const u64 r0 = g.r0[me], r1 = g.r1[me], c0 = g.c0[me];
   const u64 n1 = g.n1, n2 = g.n2, z1 = g.z1, z2e = g.z2e;
@@ -2242,7 +2263,7 @@ int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowsla
       tab.insert(tab.end(), qw.begin(), qw.end());
       u64* dt = nullptr;
       if (int rc = dev_table(tab, &dt, st)) return rc;
-      dist::pack_rows_kernel<<<(unsigned)(mine * P), 256, 0, st>>>(send, rs, esb, mine, g.L2, dt, dt + P, dt + 2 * P,
+      dist::pack_rows_kernel<<<dist::copy_grid(mine * P, sm_count()), 256, 0, st>>>(send, rs, esb, mine, g.L2, dt, dt + P, dt + 2 * P,
                                                                     (u32)P);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaFreeAsync(dt, st));

@@ -79,11 +79,14 @@ struct Geometry {
   unsigned l1, l2;
   u64 L1, L2, n1, n2, n1c, z1, z2, z2e, zrows, col_step, R;
   std::vector<u64> c0, c1, r0, r1;
-  Geometry(u64 M_, u64 L_, u64 z_, u64 n_, u64 world_, int policy, bool inverse, int f)
+  // wide: the ring runs radix-64 coset leaves (shape_of): columns of 64
+  // coefficients (one radix-64 pass) and rows of L / 64 (the single-GPU
+  // plan's own top split) instead of the balanced split
+  Geometry(u64 M_, u64 L_, u64 z_, u64 n_, u64 world_, int policy, bool inverse, int f, bool wide = false)
       : M(M_), L(L_), z(z_), n(n_), world(world_) {
     unsigned ell = 0;
     while ((u64{1} << ell) < L) ++ell;
-    l1 = policy ? 1 : ell / 2;
+    l1 = policy ? 1 : (wide && ell >= 12) ? 6 : ell / 2;
     l2 = ell - l1;
     L1 = u64{1} << l1;
     L2 = u64{1} << l2;
@@ -117,13 +120,21 @@ struct Geometry {
 // recv blocks [q][nr][W_q] -> row slab [nr][L2] (columns [c0_q, c1_q) of every row)
 __global__ void unpack_rows_kernel(std::uint8_t* rowslab, const std::uint8_t* recv, u64 eb, u64 nr, u64 L2,
                                    const u64* qoff, const u64* qc0, const u64* qw, u32 world) {
-  // one CTA per (row, source rank); 16-byte pieces
+  // CTAs (x, y): x = (row, source rank), y strides over the row's 16-byte
+  // pieces (a few long rows still fill the machine)
   const u64 r = blockIdx.x / world, q = blockIdx.x % world;
   const u64 w = qw[q];
   const uint4* src = reinterpret_cast<const uint4*>(recv + (qoff[q] + r * w) * eb);
   uint4* dst = reinterpret_cast<uint4*>(rowslab + (r * L2 + qc0[q]) * eb);
   const u64 pieces = w * eb / 16;
-  for (u64 i = threadIdx.x; i < pieces; i += blockDim.x) dst[i] = __ldcs(src + i);
+  for (u64 i = (u64)blockIdx.y * blockDim.x + threadIdx.x; i < pieces; i += (u64)gridDim.y * blockDim.x)
+    dst[i] = __ldcs(src + i);
+}
+// grid of the two copies: about 8 CTAs per SM in all
+inline dim3 copy_grid(u64 rows_times_world, int sms) {
+  const u64 want = 8ull * (u64)sms;
+  const u64 y = rows_times_world >= want ? 1 : (want + rows_times_world - 1) / rows_times_world;
+  return dim3((unsigned)rows_times_world, (unsigned)std::min<u64>(y, 65535), 1);
 }
 // row slab [mine][L2] columns [c0_q, c1_q) -> send blocks [q][mine][W_q]
 __global__ void pack_rows_kernel(std::uint8_t* send, const std::uint8_t* rowslab, u64 eb, u64 mine, u64 L2,
@@ -133,7 +144,8 @@ __global__ void pack_rows_kernel(std::uint8_t* send, const std::uint8_t* rowslab
   const uint4* src = reinterpret_cast<const uint4*>(rowslab + (r * L2 + qc0[q]) * eb);
   uint4* dst = reinterpret_cast<uint4*>(send + (qoff[q] + r * w) * eb);
   const u64 pieces = w * eb / 16;
-  for (u64 i = threadIdx.x; i < pieces; i += blockDim.x) dst[i] = __ldcs(src + i);
+  for (u64 i = (u64)blockIdx.y * blockDim.x + threadIdx.x; i < pieces; i += (u64)gridDim.y * blockDim.x)
+    dst[i] = __ldcs(src + i);
   (void)mine;
 }
 

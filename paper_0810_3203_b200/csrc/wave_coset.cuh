@@ -47,6 +47,7 @@ struct WaveArgs {
   u32 debug;            // CFTFT_DEBUG_SKIP bits (experiments; results wrong when set)
   const void* tdesc;    // coset_tma_kernel: per-leaf descriptors of the wave (TmaLeafDesc)
   const std::uint8_t* tlay;  // coset_tma_kernel: per slot entry of wslots, bit 0 input / bit 1 output coset-major
+  u32 runlog;                // coset_tma_kernel: a CTA takes runs of 2^runlog consecutive items
 };
 __device__ __forceinline__ u32 wave_tix(const WaveArgs& A, u32 p) {
   return ((p & ((1u << A.logS) - 1)) << (A.logLanes - A.logS)) | (p >> A.logS);

@@ -795,7 +795,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
   __syncthreads();
   const u32 items = A.nleaves << logS, G = gridDim.x;
-  auto item_of = [&](u32 k) { return blockIdx.x + k * G; };
+  // Runs of 2^runlog consecutive items (cosets of one leaf) per CTA and
+  // round: the lane-below rows of an item are the rows its neighbour item
+  // loads, so with runs they are in L2 (the host picks the run per wave).
+  const u32 runlog = A.runlog, runmask = (1u << runlog) - 1u;
+  auto item_of = [&](u32 k) { return (blockIdx.x << runlog) + (k & runmask) + (k >> runlog) * (G << runlog); };
   const u32 tile = sm_s + grp * kTileBytes;
   const u32 tab = sm_s + kSlotTab + 256u * warp;
   // lane j < 8: slot j of this warp's stage-A network (pre, layout)

@@ -83,11 +83,14 @@ class DistGeometry:
     """Partition of one (L, z, n[, f]) transform over `world` ranks."""
 
     def __init__(self, M: int, L: int, z: int, n: int, world: int, policy: int = 0, inverse: bool = False,
-                 f: int = 0):
+                 f: int = 0, l1: int | None = None):
+        """l1: log2 of the column length when it is not the policy's split (the
+        native path takes columns of 64 on rings that run radix-64 leaves:
+        cftft_dist_geometry reports L1)."""
         self.M, self.L, self.z, self.n, self.world = M, L, z, n, world
         ell = L.bit_length() - 1
         self.ell = ell
-        self.l1, self.l2 = _split(ell, policy)
+        self.l1, self.l2 = _split(ell, policy) if l1 is None else (l1, ell - l1)
         self.L1, self.L2 = 1 << self.l1, 1 << self.l2
         L2 = self.L2
         self.n2, self.n1 = n & (L2 - 1), n >> self.l2
