@@ -233,7 +233,15 @@ int cftft_gpu_scale(const cftft_ring* ring, void* dev_base, uint64_t count,
  * -> phases i-iv with the transposes and the phase-iii row exchange ->
  * column slab (L a[0, n), plus x[n] if f = 1).  Asynchronous on `stream`;
  * every rank calls with the same parameters.  NCCL is loaded at run time
- * (libnccl.so.2). */
+ * (libnccl.so.2).
+ * The split L1 x L2 is the library's: the policy's (transform.hpp:150-152),
+ * except that rings whose single-GPU plans run radix-64 leaves take columns
+ * of L1 = 64 (outputs do not depend on the split); cftft_dist_geometry
+ * reports it together with the slabs.  Each transpose piece (one row's
+ * columns of one rank) is contiguous on both sides and moves by one
+ * ncclSend / ncclRecv straight into place; the column pass (TFT) and the
+ * full-row pass (ITFT) run in chunks, a chunk's transpose on the context's
+ * own stream overlapping the next chunk's transforms. */
 typedef struct cftft_dist cftft_dist;
 int cftft_nccl_unique_id(void* out128);  /* ncclGetUniqueId: rank 0 makes it, all ranks get a copy */
 int cftft_dist_create(const cftft_ring* ring, int rank, int world, const void* nccl_id128, cftft_dist** out);

@@ -2051,6 +2051,8 @@ struct cftft_dist {
   ncclComm_t comm = nullptr;
   bool owns = false;
   int rank = 0, world = 1, device = 0;
+  cudaStream_t comm_stream = nullptr;  // the TFT's transposes run here, behind the column chunks
+  cudaEvent_t ev = nullptr;
 };
 
 namespace {
@@ -2079,21 +2081,11 @@ int run_subs(const cftft_dist* d, int inverse, const std::vector<cftft_subtransf
   if (v.empty()) return CFTFT_OK;
   return cftft_gpu_batch(d->ring, inverse, v.data(), v.size(), slab, esb, policy, 1, st);
 }
-// device copy of a small u64 table (stream ordered; freed after use)
-int dev_table(const std::vector<u64>& h, u64** out, cudaStream_t st) {
-  CUDA_TRY(cudaMallocAsync((void**)out, h.size() * 8, st));
-  CUDA_TRY(cudaMemcpyAsync(*out, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
-  return CFTFT_OK;
-}
 // the ring's transforms of length L run radix-64 coset leaves: the slabs take
 // the (6, ell - 6) split of the single-GPU plan
-int sm_count() {
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-    return 148;
-  return sms;
-}
+// column chunks of the distributed TFT (chunk k's transpose overlaps chunk
+// k+1's column pass): a few, each still a full machine's worth of columns
+u64 dist_chunks(u64 W) { return std::max<u64>(1, std::min<u64>(4, W / 256)); }
 bool dist_wide(const cftft_ring* R, u64 L) {
   DevicePlan geo;
   return shape_of(R, L, &geo).wide;
@@ -2131,6 +2123,8 @@ int cftft_dist_create(const cftft_ring* ring, int rank, int world, const void* n
   std::memcpy(&id, nccl_id, sizeof id);
   NCCL_TRY(n.CommInitRank(&d->comm, world, id, rank));
   d->owns = true;
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->comm_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&d->ev, cudaEventDisableTiming));
   *out = d.release();
   return CFTFT_OK;
 }
@@ -2145,6 +2139,8 @@ int cftft_dist_create_from_comm(const cftft_ring* ring, void* nccl_comm, cftft_d
   NCCL_TRY(n.CommCount(d->comm, &d->world));
   NCCL_TRY(n.CommUserRank(d->comm, &d->rank));
   CUDA_TRY(cudaGetDevice(&d->device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->comm_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&d->ev, cudaEventDisableTiming));
   *out = d.release();
   return CFTFT_OK;
 }
@@ -2152,6 +2148,8 @@ int cftft_dist_create_from_comm(const cftft_ring* ring, void* nccl_comm, cftft_d
 void cftft_dist_destroy(cftft_dist* d) {
   if (!d) return;
   if (d->owns && d->comm && dist::nccl().CommDestroy) dist::nccl().CommDestroy(d->comm);
+  if (d->comm_stream) cudaStreamDestroy(d->comm_stream);
+  if (d->ev) cudaEventDestroy(d->ev);
   delete d;
 }
 
@@ -2176,46 +2174,43 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
                          dist_wide(R, p->length));
   const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me), nr = g.nrows(me);
   const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
-  // 1. column TFTs (transform.hpp:175-180)
+  // 1. column TFTs (transform.hpp:175-180) in chunks of adjacent columns, and
+  // 2. the transpose of each chunk behind it on the communicator's stream:
+  //    row r of R_q, the chunk's columns -> rank q, received straight into
+  //    place in q's row slab (the piece is contiguous on both sides: no pack
+  //    or unpack pass, no staging buffer).  Chunk k's sends overlap chunk
+  //    k+1's column pass; ranks issue the same chunks in the same order.
+  const u64 K = dist_chunks(g.L2 / P);  // the same on every rank
+  cudaStream_t cst = d->comm_stream;
+  cudaEvent_t ev = d->ev;
   std::vector<cftft_subtransform> v;
-  for (u64 c = 0; c < W; ++c) {
-    const u64 u = g.c0[me] + c;
-    if (u >= g.z2e) continue;
-    v.push_back(sub(g.L1, (s + u * g.col_step) & (R->M - 1), u < g.z2 ? g.z1 + 1 : g.z1, g.n1c, 0, c, W));
+  for (u64 k = 0; k < K; ++k) {
+    const u64 a = W * k / K, b = W * (k + 1) / K;
+    v.clear();
+    for (u64 c = a; c < b; ++c) {
+      const u64 u = g.c0[me] + c;
+      if (u >= g.z2e) continue;
+      v.push_back(sub(g.L1, (s + u * g.col_step) & (R->M - 1), u < g.z2 ? g.z1 + 1 : g.z1, g.n1c, 0, c, W));
+    }
+    if (int rc = run_subs(d, 0, v, colslab, esb, policy, st)) return rc;
+    CUDA_TRY(cudaEventRecord(ev, st));
+    CUDA_TRY(cudaStreamWaitEvent(cst, ev, 0));
+    NCCL_TRY(nc.GroupStart());
+    for (u64 q = 0; q < P; ++q) {
+      // my chunk [a, b) of every row of R_q; every peer's chunk of my rows
+      const u64 qa = g.width(q) * k / K, qb = g.width(q) * (k + 1) / K;
+      for (u64 r = g.r0[q]; r < g.r1[q] && b > a; ++r)
+        NCCL_TRY(nc.Send(static_cast<std::uint8_t*>(colslab) + (r * W + a) * esb, (b - a) * esb, ncclUint8, (int)q,
+                         d->comm, cst));
+      for (u64 r = 0; r < nr && qb > qa; ++r)
+        NCCL_TRY(nc.Recv(static_cast<std::uint8_t*>(rowslab) + (r * g.L2 + g.c0[q] + qa) * esb, (qb - qa) * esb,
+                         ncclUint8, (int)q, d->comm, cst));
+    }
+    NCCL_TRY(nc.GroupEnd());
   }
-  if (int rc = run_subs(d, 0, v, colslab, esb, policy, st)) return rc;
-  // 2. transpose: rows R_q of my columns to rank q (contiguous in the column slab)
-  std::vector<u64> qoff(P), qc0(P), qw(P);
-  u64 tot = 0;
-  for (u64 q = 0; q < P; ++q) {
-    qoff[q] = tot;
-    qc0[q] = g.c0[q];
-    qw[q] = g.width(q);
-    tot += nr * g.width(q);
-  }
-  std::uint8_t* recv = nullptr;
-  CUDA_TRY(cudaMallocAsync((void**)&recv, std::max<u64>(1, tot) * esb, st));
-  NCCL_TRY(nc.GroupStart());
-  for (u64 q = 0; q < P; ++q) {
-    const u64 cnt_s = g.nrows(q) * W * esb, cnt_r = nr * g.width(q) * esb;
-    if (cnt_s)
-      NCCL_TRY(nc.Send(static_cast<std::uint8_t*>(colslab) + g.r0[q] * W * esb, cnt_s, ncclUint8, (int)q, d->comm, st));
-    if (cnt_r) NCCL_TRY(nc.Recv(recv + qoff[q] * esb, cnt_r, ncclUint8, (int)q, d->comm, st));
-  }
-  NCCL_TRY(nc.GroupEnd());
-  // 3. unpack into the row slab, row TFTs (transform.hpp:182-185)
-  if (nr) {
-    std::vector<u64> tab(qoff);
-    tab.insert(tab.end(), qc0.begin(), qc0.end());
-    tab.insert(tab.end(), qw.begin(), qw.end());
-    u64* dt = nullptr;
-    if (int rc = dev_table(tab, &dt, st)) return rc;
-    dist::unpack_rows_kernel<<<dist::copy_grid(nr * P, sm_count()), 256, 0, st>>>(static_cast<std::uint8_t*>(rowslab), recv, esb, nr,
-                                                                  g.L2, dt, dt + P, dt + 2 * P, (u32)P);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaFreeAsync(dt, st));
-  }
-  CUDA_TRY(cudaFreeAsync(recv, st));
+  CUDA_TRY(cudaEventRecord(ev, cst));
+  CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+  // 3. row TFTs (transform.hpp:182-185)
   v.clear();
   for (u64 u = g.r0[me]; u < g.r1[me]; ++u)
     v.push_back(sub(g.L2, s_row, g.z2e, u < g.n1 ? g.L2 : g.n2, 0, (u - g.r0[me]) * g.L2, 1));
@@ -2238,46 +2233,52 @@ int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowsla
   const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
   auto* rs = static_cast<std::uint8_t*>(rowslab);
   auto* cs = static_cast<std::uint8_t*>(colslab);
-  // i. full rows u < n1 (transform.hpp:215-216)
+  // i. full rows u < n1 (transform.hpp:215-216), in chunks of rows; each
+  // chunk's rows then go to the column owners on the communicator's stream
+  // while the next chunk is transformed: the columns [c0_q, c1_q) of a row
+  // leave as they lie (contiguous in the row), rank q's rows arrive in
+  // global row order, straight into the column slab.  Every rank cuts every
+  // rank's rows [r0_q, min(r1_q, zrows)) the same way.
   std::vector<cftft_subtransform> v;
-  for (u64 u = r0; u < std::min(r1, n1); ++u) v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
-  if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
-  // rows [0, zrows) to the column owners: my rows' columns [c0_q, c1_q) packed
-  // per destination; rank q's rows arrive in global row order, straight into
-  // the column slab (rows [0, zrows) of it)
   {
-    const u64 mine = r0 < g.zrows ? std::min(r1, g.zrows) - r0 : 0;
-    std::vector<u64> qoff(P), qc0(P), qw(P);
-    u64 tot = 0;
+    cudaStream_t cst = d->comm_stream;
+    cudaEvent_t ev = d->ev;
+    u64 K = 1;  // chunks: at most 4, at least one row of the longest slab each
     for (u64 q = 0; q < P; ++q) {
-      qoff[q] = tot;
-      qc0[q] = g.c0[q];
-      qw[q] = g.width(q);
-      tot += mine * g.width(q);
+      const u64 m = g.r0[q] < g.zrows ? std::min(g.r1[q], g.zrows) - g.r0[q] : 0;
+      K = std::max(K, std::min<u64>(4, m));
     }
-    std::uint8_t* send = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&send, std::max<u64>(1, tot) * esb, st));
-    if (mine) {
-      std::vector<u64> tab(qoff);
-      tab.insert(tab.end(), qc0.begin(), qc0.end());
-      tab.insert(tab.end(), qw.begin(), qw.end());
-      u64* dt = nullptr;
-      if (int rc = dev_table(tab, &dt, st)) return rc;
-      dist::pack_rows_kernel<<<dist::copy_grid(mine * P, sm_count()), 256, 0, st>>>(send, rs, esb, mine, g.L2, dt, dt + P, dt + 2 * P,
-                                                                    (u32)P);
-      CUDA_TRY(cudaGetLastError());
-      CUDA_TRY(cudaFreeAsync(dt, st));
+    auto cut = [&](u64 q, u64 k, u64& a, u64& b) {  // global rows of chunk k of rank q
+      const u64 lo_r = g.r0[q], m = lo_r < g.zrows ? std::min(g.r1[q], g.zrows) - lo_r : 0;
+      a = lo_r + m * k / K;
+      b = lo_r + m * (k + 1) / K;
+    };
+    // rows of mine at or past zrows (none are sent) still take phase i
+    v.clear();
+    for (u64 u = std::max(r0, std::min(r1, g.zrows)); u < std::min(r1, n1); ++u)
+      v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
+    if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
+    for (u64 k = 0; k < K; ++k) {
+      u64 a, b;
+      cut(me, k, a, b);
+      v.clear();
+      for (u64 u = a; u < std::min(b, n1); ++u) v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
+      if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
+      CUDA_TRY(cudaEventRecord(ev, st));
+      CUDA_TRY(cudaStreamWaitEvent(cst, ev, 0));
+      NCCL_TRY(nc.GroupStart());
+      for (u64 q = 0; q < P; ++q) {
+        u64 qa, qb;
+        cut(q, k, qa, qb);
+        for (u64 u = a; u < b && g.width(q); ++u)
+          NCCL_TRY(nc.Send(rs + ((u - r0) * g.L2 + g.c0[q]) * esb, g.width(q) * esb, ncclUint8, (int)q, d->comm, cst));
+        for (u64 u = qa; u < qb && W; ++u)
+          NCCL_TRY(nc.Recv(cs + u * W * esb, W * esb, ncclUint8, (int)q, d->comm, cst));
+      }
+      NCCL_TRY(nc.GroupEnd());
     }
-    NCCL_TRY(nc.GroupStart());
-    for (u64 q = 0; q < P; ++q) {
-      const u64 cnt_s = mine * g.width(q) * esb;
-      const u64 qa = g.r0[q], qb = std::min(g.r1[q], g.zrows);
-      const u64 cnt_r = (qb > qa ? qb - qa : 0) * W * esb;
-      if (cnt_s) NCCL_TRY(nc.Send(send + qoff[q] * esb, cnt_s, ncclUint8, (int)q, d->comm, st));
-      if (cnt_r) NCCL_TRY(nc.Recv(cs + qa * W * esb, cnt_r, ncclUint8, (int)q, d->comm, st));
-    }
-    NCCL_TRY(nc.GroupEnd());
-    CUDA_TRY(cudaFreeAsync(send, st));
+    CUDA_TRY(cudaEventRecord(ev, cst));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
   }
   // ii. right columns [n2, z2') (transform.hpp:219-224)
   v.clear();

@@ -117,37 +117,6 @@ struct Geometry {
   u64 nrows(u64 p) const { return r1[p] - r0[p]; }
 };
 
-// recv blocks [q][nr][W_q] -> row slab [nr][L2] (columns [c0_q, c1_q) of every row)
-__global__ void unpack_rows_kernel(std::uint8_t* rowslab, const std::uint8_t* recv, u64 eb, u64 nr, u64 L2,
-                                   const u64* qoff, const u64* qc0, const u64* qw, u32 world) {
-  // CTAs (x, y): x = (row, source rank), y strides over the row's 16-byte
-  // pieces (a few long rows still fill the machine)
-  const u64 r = blockIdx.x / world, q = blockIdx.x % world;
-  const u64 w = qw[q];
-  const uint4* src = reinterpret_cast<const uint4*>(recv + (qoff[q] + r * w) * eb);
-  uint4* dst = reinterpret_cast<uint4*>(rowslab + (r * L2 + qc0[q]) * eb);
-  const u64 pieces = w * eb / 16;
-  for (u64 i = (u64)blockIdx.y * blockDim.x + threadIdx.x; i < pieces; i += (u64)gridDim.y * blockDim.x)
-    dst[i] = __ldcs(src + i);
-}
-// grid of the two copies: about 8 CTAs per SM in all
-inline dim3 copy_grid(u64 rows_times_world, int sms) {
-  const u64 want = 8ull * (u64)sms;
-  const u64 y = rows_times_world >= want ? 1 : (want + rows_times_world - 1) / rows_times_world;
-  return dim3((unsigned)rows_times_world, (unsigned)std::min<u64>(y, 65535), 1);
-}
-// row slab [mine][L2] columns [c0_q, c1_q) -> send blocks [q][mine][W_q]
-__global__ void pack_rows_kernel(std::uint8_t* send, const std::uint8_t* rowslab, u64 eb, u64 mine, u64 L2,
-                                 const u64* qoff, const u64* qc0, const u64* qw, u32 world) {
-  const u64 r = blockIdx.x / world, q = blockIdx.x % world;
-  const u64 w = qw[q];
-  const uint4* src = reinterpret_cast<const uint4*>(rowslab + (r * L2 + qc0[q]) * eb);
-  uint4* dst = reinterpret_cast<uint4*>(send + (qoff[q] + r * w) * eb);
-  const u64 pieces = w * eb / 16;
-  for (u64 i = (u64)blockIdx.y * blockDim.x + threadIdx.x; i < pieces; i += (u64)gridDim.y * blockDim.x)
-    dst[i] = __ldcs(src + i);
-  (void)mine;
-}
 
 }  // namespace dist
 }  // namespace cftft_b200
