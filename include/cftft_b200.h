@@ -249,6 +249,14 @@ int cftft_dist_create_from_comm(const cftft_ring* ring, void* nccl_comm, cftft_d
 void cftft_dist_destroy(cftft_dist* d);
 /* this rank's slabs: out[8] = {c0, c1, r0, r1, L1, L2, column-slab elements, row-slab elements} */
 int cftft_dist_geometry(const cftft_dist* d, const cftft_params* params, int inverse, int policy, uint64_t* out);
+/* Debug (pure host code, no GPU, no NCCL): the transpose schedule rank `rank`
+ * of `world` hands to NCCL for one transform over a ring of root order M --
+ * records of 6 words {chunk, 1 = send / 0 = recv, peer, 0 = column slab / 1 =
+ * row slab, element offset, element count}, in issue order; the pieces of one
+ * chunk form one NCCL group.  `wide` = the ring runs radix-64 leaves (columns
+ * of 64).  Returns the number of words (writes at most cap). */
+size_t cftft_dist_schedule(uint64_t M, const cftft_params* params, int inverse, int policy, int wide, int world,
+                           int rank, uint64_t* out, size_t cap);
 int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* params, void* dev_colslab, void* dev_rowslab,
                        uint64_t elem_stride_bytes, int policy, void* stream);
 int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* params, void* dev_rowslab, void* dev_colslab,

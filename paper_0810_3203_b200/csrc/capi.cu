@@ -2083,9 +2083,21 @@ int run_subs(const cftft_dist* d, int inverse, const std::vector<cftft_subtransf
 }
 // the ring's transforms of length L run radix-64 coset leaves: the slabs take
 // the (6, ell - 6) split of the single-GPU plan
-// column chunks of the distributed TFT (chunk k's transpose overlaps chunk
-// k+1's column pass): a few, each still a full machine's worth of columns
-u64 dist_chunks(u64 W) { return std::max<u64>(1, std::min<u64>(4, W / 256)); }
+// one NCCL group of transpose pieces (dist.cuh) on stream st
+int run_pieces(const cftft_dist* d, const std::vector<dist::Piece>& v, void* colslab, void* rowslab, u64 esb,
+               cudaStream_t st) {
+  auto& nc = dist::nccl();
+  NCCL_TRY(nc.GroupStart());
+  for (const dist::Piece& pc : v) {
+    std::uint8_t* at = static_cast<std::uint8_t*>(pc.buf ? rowslab : colslab) + pc.off * esb;
+    if (pc.send)
+      NCCL_TRY(nc.Send(at, pc.count * esb, ncclUint8, (int)pc.peer, d->comm, st));
+    else
+      NCCL_TRY(nc.Recv(at, pc.count * esb, ncclUint8, (int)pc.peer, d->comm, st));
+  }
+  NCCL_TRY(nc.GroupEnd());
+  return CFTFT_OK;
+}
 bool dist_wide(const cftft_ring* R, u64 L) {
   DevicePlan geo;
   return shape_of(R, L, &geo).wide;
@@ -2164,6 +2176,24 @@ int cftft_dist_geometry(const cftft_dist* d, const cftft_params* p, int inverse,
   return CFTFT_OK;
 }
 
+size_t cftft_dist_schedule(uint64_t M, const cftft_params* p, int inverse, int policy, int wide, int world,
+                           int rank, uint64_t* out, size_t cap) {
+  if (!p || world < 1 || rank < 0 || rank >= world) return 0;
+  const dist::Geometry g(M, p->length, p->input_count, p->output_count, (u64)world, policy, inverse != 0,
+                         inverse ? p->want_next : 0, wide != 0);
+  const u64 K = inverse ? dist::itft_chunks(g) : dist::tft_chunks(g);
+  size_t n = 0;
+  for (u64 k = 0; k < K; ++k) {
+    const auto v = inverse ? dist::itft_transpose(g, (u64)rank, k) : dist::tft_transpose(g, (u64)rank, k);
+    for (const dist::Piece& pc : v) {
+      const u64 rec[6] = {k, pc.send, pc.peer, pc.buf, pc.off, pc.count};
+      if (out && n + 6 <= cap) std::memcpy(out + n, rec, sizeof rec);
+      n += 6;
+    }
+  }
+  return n;
+}
+
 int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab, void* rowslab,
                        uint64_t esb, int policy, void* stream) {
   if (int rc = check_dist(d, p, 0, policy, esb)) return rc;
@@ -2172,7 +2202,7 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
   const cftft_ring* R = d->ring;
   const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, false, 0,
                          dist_wide(R, p->length));
-  const u64 P = (u64)d->world, me = (u64)d->rank, W = g.width(me), nr = g.nrows(me);
+  const u64 me = (u64)d->rank, W = g.width(me);
   const u64 s = p->twiddle_exp & (R->M - 1), s_row = (s << g.l1) & (R->M - 1);
   // 1. column TFTs (transform.hpp:175-180) in chunks of adjacent columns, and
   // 2. the transpose of each chunk behind it on the communicator's stream:
@@ -2180,12 +2210,13 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
   //    place in q's row slab (the piece is contiguous on both sides: no pack
   //    or unpack pass, no staging buffer).  Chunk k's sends overlap chunk
   //    k+1's column pass; ranks issue the same chunks in the same order.
-  const u64 K = dist_chunks(g.L2 / P);  // the same on every rank
+  const u64 K = dist::tft_chunks(g);
   cudaStream_t cst = d->comm_stream;
   cudaEvent_t ev = d->ev;
   std::vector<cftft_subtransform> v;
   for (u64 k = 0; k < K; ++k) {
-    const u64 a = W * k / K, b = W * (k + 1) / K;
+    u64 a, b;
+    dist::tft_chunk_cols(g, me, k, a, b);
     v.clear();
     for (u64 c = a; c < b; ++c) {
       const u64 u = g.c0[me] + c;
@@ -2195,18 +2226,7 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
     if (int rc = run_subs(d, 0, v, colslab, esb, policy, st)) return rc;
     CUDA_TRY(cudaEventRecord(ev, st));
     CUDA_TRY(cudaStreamWaitEvent(cst, ev, 0));
-    NCCL_TRY(nc.GroupStart());
-    for (u64 q = 0; q < P; ++q) {
-      // my chunk [a, b) of every row of R_q; every peer's chunk of my rows
-      const u64 qa = g.width(q) * k / K, qb = g.width(q) * (k + 1) / K;
-      for (u64 r = g.r0[q]; r < g.r1[q] && b > a; ++r)
-        NCCL_TRY(nc.Send(static_cast<std::uint8_t*>(colslab) + (r * W + a) * esb, (b - a) * esb, ncclUint8, (int)q,
-                         d->comm, cst));
-      for (u64 r = 0; r < nr && qb > qa; ++r)
-        NCCL_TRY(nc.Recv(static_cast<std::uint8_t*>(rowslab) + (r * g.L2 + g.c0[q] + qa) * esb, (qb - qa) * esb,
-                         ncclUint8, (int)q, d->comm, cst));
-    }
-    NCCL_TRY(nc.GroupEnd());
+    if (int rc = run_pieces(d, dist::tft_transpose(g, me, k), colslab, rowslab, esb, cst)) return rc;
   }
   CUDA_TRY(cudaEventRecord(ev, cst));
   CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
@@ -2243,39 +2263,20 @@ int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowsla
   {
     cudaStream_t cst = d->comm_stream;
     cudaEvent_t ev = d->ev;
-    u64 K = 1;  // chunks: at most 4, at least one row of the longest slab each
-    for (u64 q = 0; q < P; ++q) {
-      const u64 m = g.r0[q] < g.zrows ? std::min(g.r1[q], g.zrows) - g.r0[q] : 0;
-      K = std::max(K, std::min<u64>(4, m));
-    }
-    auto cut = [&](u64 q, u64 k, u64& a, u64& b) {  // global rows of chunk k of rank q
-      const u64 lo_r = g.r0[q], m = lo_r < g.zrows ? std::min(g.r1[q], g.zrows) - lo_r : 0;
-      a = lo_r + m * k / K;
-      b = lo_r + m * (k + 1) / K;
-    };
+    const u64 K = dist::itft_chunks(g);
     // rows of mine at or past zrows (none are sent) still take phase i
-    v.clear();
     for (u64 u = std::max(r0, std::min(r1, g.zrows)); u < std::min(r1, n1); ++u)
       v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
     if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
     for (u64 k = 0; k < K; ++k) {
       u64 a, b;
-      cut(me, k, a, b);
+      dist::itft_chunk_rows(g, me, k, a, b);
       v.clear();
       for (u64 u = a; u < std::min(b, n1); ++u) v.push_back(sub(g.L2, s_row, g.L2, g.L2, 0, (u - r0) * g.L2, 1));
       if (int rc = run_subs(d, 1, v, rowslab, esb, policy, st)) return rc;
       CUDA_TRY(cudaEventRecord(ev, st));
       CUDA_TRY(cudaStreamWaitEvent(cst, ev, 0));
-      NCCL_TRY(nc.GroupStart());
-      for (u64 q = 0; q < P; ++q) {
-        u64 qa, qb;
-        cut(q, k, qa, qb);
-        for (u64 u = a; u < b && g.width(q); ++u)
-          NCCL_TRY(nc.Send(rs + ((u - r0) * g.L2 + g.c0[q]) * esb, g.width(q) * esb, ncclUint8, (int)q, d->comm, cst));
-        for (u64 u = qa; u < qb && W; ++u)
-          NCCL_TRY(nc.Recv(cs + u * W * esb, W * esb, ncclUint8, (int)q, d->comm, cst));
-      }
-      NCCL_TRY(nc.GroupEnd());
+      if (int rc = run_pieces(d, dist::itft_transpose(g, me, k), colslab, rowslab, esb, cst)) return rc;
     }
     CUDA_TRY(cudaEventRecord(ev, cst));
     CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));

@@ -117,6 +117,70 @@ struct Geometry {
   u64 nrows(u64 p) const { return r1[p] - r0[p]; }
 };
 
+// ---- transpose schedules (pure host code: what cftft_gpu_dist_tft / _itft
+// hand to NCCL, and what tests/test_dist.py replays over simulated ranks).
+// One transpose = a few chunks; the pieces of a chunk form one NCCL group, in
+// this order; piece = one row's columns of one rank, contiguous on both sides.
+struct Piece {
+  u64 send;   // 1: ncclSend, 0: ncclRecv
+  u64 peer;
+  u64 buf;    // 0: column slab, 1: row slab
+  u64 off;    // element offset into the slab
+  u64 count;  // elements
+};
+// chunks of the distributed TFT (chunk k's transpose overlaps chunk k+1's
+// column pass): a few, each still a machine's worth of columns; the same on
+// every rank
+inline u64 tft_chunks(const Geometry& g) { return std::max<u64>(1, std::min<u64>(4, (g.L2 / g.world) / 256)); }
+// rank p's columns of chunk k: [a, b) of its slab
+inline void tft_chunk_cols(const Geometry& g, u64 p, u64 k, u64& a, u64& b) {
+  const u64 K = tft_chunks(g), W = g.width(p);
+  a = W * k / K;
+  b = W * (k + 1) / K;
+}
+// TFT: row r of R_q, my chunk's columns -> rank q, straight into q's row slab
+inline std::vector<Piece> tft_transpose(const Geometry& g, u64 me, u64 k) {
+  std::vector<Piece> v;
+  const u64 W = g.width(me), nr = g.nrows(me);
+  u64 a, b;
+  tft_chunk_cols(g, me, k, a, b);
+  for (u64 q = 0; q < g.world; ++q) {
+    u64 qa, qb;
+    tft_chunk_cols(g, q, k, qa, qb);
+    for (u64 r = g.r0[q]; r < g.r1[q] && b > a; ++r) v.push_back(Piece{1, q, 0, r * W + a, b - a});
+    for (u64 r = 0; r < nr && qb > qa; ++r) v.push_back(Piece{0, q, 1, r * g.L2 + g.c0[q] + qa, qb - qa});
+  }
+  return v;
+}
+// ITFT: rows [0, zrows) to the column owners, in chunks of rows; every rank
+// cuts every rank's rows [r0_q, min(r1_q, zrows)) the same way
+inline u64 itft_chunks(const Geometry& g) {
+  u64 K = 1;
+  for (u64 q = 0; q < g.world; ++q) {
+    const u64 m = g.r0[q] < g.zrows ? std::min(g.r1[q], g.zrows) - g.r0[q] : 0;
+    K = std::max(K, std::min<u64>(4, m));
+  }
+  return K;
+}
+inline void itft_chunk_rows(const Geometry& g, u64 q, u64 k, u64& a, u64& b) {  // global rows
+  const u64 K = itft_chunks(g), lo = g.r0[q], m = lo < g.zrows ? std::min(g.r1[q], g.zrows) - lo : 0;
+  a = lo + m * k / K;
+  b = lo + m * (k + 1) / K;
+}
+inline std::vector<Piece> itft_transpose(const Geometry& g, u64 me, u64 k) {
+  std::vector<Piece> v;
+  const u64 W = g.width(me);
+  u64 a, b;
+  itft_chunk_rows(g, me, k, a, b);
+  for (u64 q = 0; q < g.world; ++q) {
+    u64 qa, qb;
+    itft_chunk_rows(g, q, k, qa, qb);
+    for (u64 u = a; u < b && g.width(q); ++u)
+      v.push_back(Piece{1, q, 1, (u - g.r0[me]) * g.L2 + g.c0[q], g.width(q)});
+    for (u64 u = qa; u < qb && W; ++u) v.push_back(Piece{0, q, 0, u * W, W});
+  }
+  return v;
+}
 
 }  // namespace dist
 }  // namespace cftft_b200

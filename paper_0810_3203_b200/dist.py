@@ -316,6 +316,27 @@ class DistTFT:
 # NCCL communicator of its own (cftft_gpu_dist_tft / cftft_gpu_dist_itft).
 
 
+def native_schedule(M: int, L: int, z: int, n: int, f: int, world: int, rank: int, inverse: bool = False,
+                    policy: int = 0, wide: bool = False):
+    """cftft_dist_schedule: the transpose pieces rank `rank` hands to NCCL, as
+    tuples (chunk, send, peer, buf, offset, count) in issue order (pure host
+    code; tests replay it over simulated ranks)."""
+    import ctypes as C
+
+    from . import _Params, lib
+
+    Lb = lib()
+    Lb.cftft_dist_schedule.argtypes = [C.c_uint64, C.POINTER(_Params), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_uint64), C.c_size_t]
+    Lb.cftft_dist_schedule.restype = C.c_size_t
+    p = _Params(L, 0, z, n, f if inverse else 0)
+    need = Lb.cftft_dist_schedule(M, C.byref(p), int(inverse), policy, int(wide), world, rank, None, 0)
+    buf = (C.c_uint64 * max(1, need))()
+    got = Lb.cftft_dist_schedule(M, C.byref(p), int(inverse), policy, int(wide), world, rank, buf, need)
+    assert got == need
+    return [tuple(buf[i:i + 6]) for i in range(0, need, 6)]
+
+
 class NcclDist:
     """A distributed context of the C ABI for the current torch.distributed
     group: rank 0 makes an NCCL unique id, the group broadcasts it, every rank

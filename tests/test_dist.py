@@ -133,3 +133,69 @@ def test_geometry_config5():
         assert sum(b - a for a, b in g.cols) == 512
         assert sum(b - a for a, b in g.rows) == 391  # only active rows are distributed
         assert max(b - a for a, b in g.rows) - min(b - a for a, b in g.rows) <= 1
+
+
+@pytest.mark.parametrize("wide", [False, True])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("L,z,n,f", [(1 << 12, 3000, 3100, 0), (1 << 12, 4096, 4096, 0), (1 << 12, 700, 650, 1),
+                                     (1 << 14, 10001, 9999, 1), (1 << 18, 200000, 200000, 0)])
+def test_native_transpose_schedules_over_simulated_ranks(L, z, n, f, P, wide):
+    """The send / receive pieces cftft_gpu_dist_tft / _itft hand to NCCL
+    (cftft_dist_schedule, pure host code), replayed over P simulated ranks:
+    NCCL pairs the i-th send from a to b with the i-th receive at b from a
+    within a group (= one chunk).  Every pair must agree in count, and the
+    pieces must put element (r, c) of the L1 x L2 matrix where the other
+    slab layout wants it -- for the TFT (column slabs -> row slabs, all
+    active rows) and for the ITFT (row slabs -> column slabs, rows < zrows)."""
+    from paper_0810_3203_b200.dist import DistGeometry, native_schedule
+
+    M = 2 * L
+    ell = L.bit_length() - 1
+    l1 = 6 if (wide and ell >= 12) else None
+    for inverse in (False, True):
+        zz, nn = (z, n) if not inverse else (max(z, n), n)  # an ITFT needs z >= n
+        g = DistGeometry(M, L, zz, nn, P, inverse=inverse, f=f if inverse else 0, l1=l1)
+        L2 = g.L2
+        # slabs hold global element ids r * L2 + c (column slab: [L1][W]; row slab: [nrows][L2])
+        col = [np.full(g.L1 * g.width(p), -1, dtype=np.int64) for p in range(P)]
+        row = [np.full(max(1, g.nrows(p)) * L2, -1, dtype=np.int64) for p in range(P)]
+        for p in range(P):
+            c0, c1 = g.cols[p]
+            r0, r1 = g.rows[p]
+            if not inverse:
+                col[p][:] = (np.arange(g.L1)[:, None] * L2 + np.arange(c0, c1)[None, :]).ravel()
+            elif r1 > r0:
+                row[p][: (r1 - r0) * L2] = (np.arange(r0, r1)[:, None] * L2 + np.arange(L2)[None, :]).ravel()
+        sched = [native_schedule(M, L, zz, nn, f, P, p, inverse=inverse, wide=wide) for p in range(P)]
+        chunks = 1 + max((rec[0] for s in sched for rec in s), default=0)
+        assert chunks <= 4
+        for k in range(chunks):
+            queues = {}
+            for p in range(P):  # every rank's sends of the group, in issue order
+                for (ck, send, peer, buf, off, cnt) in sched[p]:
+                    if ck == k and send:
+                        src = (row if buf else col)[p]
+                        assert off + cnt <= src.size
+                        queues.setdefault((p, peer), []).append(src[off: off + cnt].copy())
+            for p in range(P):  # matched with the receives, in issue order
+                for (ck, send, peer, buf, off, cnt) in sched[p]:
+                    if ck == k and not send:
+                        q = queues.get((peer, p))
+                        assert q, "a receive without a matching send"
+                        data = q.pop(0)
+                        assert data.size == cnt, "send / receive sizes differ"
+                        dst = (row if buf else col)[p]
+                        assert off + cnt <= dst.size
+                        dst[off: off + cnt] = data
+            assert all(not q for q in queues.values()), "a send without a matching receive"
+        for p in range(P):
+            c0, c1 = g.cols[p]
+            r0, r1 = g.rows[p]
+            if not inverse:  # every active row, all L2 columns
+                want = (np.arange(r0, r1)[:, None] * L2 + np.arange(L2)[None, :]).ravel()
+                assert np.array_equal(row[p][: want.size], want), (P, p, "TFT row slab")
+            else:            # rows [0, zrows) of my columns
+                zr = g.zrows
+                want = np.arange(zr)[:, None] * L2 + np.arange(c0, c1)[None, :]
+                got = col[p].reshape(g.L1, c1 - c0)[:zr]
+                assert np.array_equal(got, want), (P, p, "ITFT column slab")
