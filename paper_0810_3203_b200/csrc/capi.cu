@@ -36,6 +36,7 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<int> g_fault{0};   // cftft_set_fault_injection
+thread_local int t_sm_reserve = 0;  // SMs the wave launches leave free (set by the multi-GPU transforms)
 std::atomic<int> g_timing{0};  // cftft_set_launch_timing
 // Launch timing (cftft_set_launch_timing): CUDA events on the launching
 // stream around each kernel of the transforms, with the launch's algorithmic
@@ -976,6 +977,9 @@ int launch_plan(cftft_ring* R, DevicePlan& dp, std::uint8_t* base, u64 stride, c
         int dev = 0, sms = 0, per = 0;
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        // the multi-GPU transforms leave a few SMs to NCCL's kernels, which run on
+        // the context's stream next to these persistent CTAs (t_sm_reserve)
+        sms = std::max(1, sms - t_sm_reserve);
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fermat::coset_wave_kernel<8, false>, 32 * wwarps, wsmem));
         const size_t xsmem = (size_t)fermat::wide_tile_words<8>() * 4;
         int xper = 0;
@@ -2083,6 +2087,17 @@ int run_subs(const cftft_dist* d, int inverse, const std::vector<cftft_subtransf
 }
 // the ring's transforms of length L run radix-64 coset leaves: the slabs take
 // the (6, ell - 6) split of the single-GPU plan
+// While a chunk's transpose runs on the context's stream the next chunk's
+// persistent wave CTAs would hold every SM; they leave this many free, so
+// NCCL's send / receive kernels start at once instead of in the gaps
+// between launches.  (One rank: NCCL's self-copies gain nothing from it --
+// measured 989 -> 975 GB/s -- so nothing is reserved there.)
+constexpr int kDistSmReserve = 8;
+struct SmReserve {
+  int old;
+  explicit SmReserve(int n) : old(t_sm_reserve) { t_sm_reserve = n; }
+  ~SmReserve() { t_sm_reserve = old; }
+};
 // one NCCL group of transpose pieces (dist.cuh) on stream st
 int run_pieces(const cftft_dist* d, const std::vector<dist::Piece>& v, void* colslab, void* rowslab, u64 esb,
                cudaStream_t st) {
@@ -2197,7 +2212,7 @@ size_t cftft_dist_schedule(uint64_t M, const cftft_params* p, int inverse, int p
 int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab, void* rowslab,
                        uint64_t esb, int policy, void* stream) {
   if (int rc = check_dist(d, p, 0, policy, esb)) return rc;
-  auto& nc = dist::nccl();
+  SmReserve reserve(d->world > 1 ? kDistSmReserve : 0);
   auto st = static_cast<cudaStream_t>(stream);
   const cftft_ring* R = d->ring;
   const dist::Geometry g(R->M, p->length, p->input_count, p->output_count, (u64)d->world, policy, false, 0,
@@ -2240,6 +2255,7 @@ int cftft_gpu_dist_tft(const cftft_dist* d, const cftft_params* p, void* colslab
 int cftft_gpu_dist_itft(const cftft_dist* d, const cftft_params* p, void* rowslab, void* colslab,
                         uint64_t esb, int policy, void* stream) {
   if (int rc = check_dist(d, p, 1, policy, esb)) return rc;
+  SmReserve reserve(d->world > 1 ? kDistSmReserve : 0);
   auto& nc = dist::nccl();
   auto st = static_cast<cudaStream_t>(stream);
   const cftft_ring* R = d->ring;
