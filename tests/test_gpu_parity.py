@@ -465,3 +465,73 @@ def test_fermat_sparse_values_carry_chains(N):
             a = int(buf[i, 0]) + (int(buf[i, lim]) << N)
             have = sum(int(got[i, j]) << (64 * j) for j in range(lim)) + (int(got[i, lim]) << N)
             assert have == (L * a) % mod, (N, L, i)
+
+
+# ---- one ring shared by two host threads -------------------------------------------
+
+def test_ring_shared_by_two_threads_and_streams():
+    """A ring context is shareable (include/cftft_b200.h): two host threads run
+    transforms on ONE ring at the same time, each on its own stream with its
+    own device view (coset plans keep scratch per stream), then each through
+    the host-buffer entry points (one staging buffer per ring, serialised by
+    the library).  Every result must equal the serial result of the same
+    transform, many times over."""
+    import threading
+
+    N, L = 32768, 1 << 12  # coset plans (two radix-64 passes): shadow buffer and tops per stream
+    ctx = cf.FermatRingCtx(N)
+    W, lim = ctx.element_words, N // 64
+    shapes = [(3000, 3100, 0), (4096, 4096, 0), (2500, 2049, 0), (3500, 3300, 1)]
+    inputs = [fermat_inputs(N, L, z, W, 900 + k) for k, (z, n, f) in enumerate(shapes)]
+    # serial expectations through the same library (its parity with the oracle
+    # is the other tests' business): TFT outputs, then the ITFT of those
+    want_t, want_i = [], []
+    for (z, n, f), buf in zip(shapes, inputs):
+        d = to_dev(buf)
+        cf.cf_tft(ctx, cf.TransformParams(L, 0, z, n), cf.DeviceView(d))
+        want_t.append(from_dev(d)[:n, : lim + 1].copy())
+        ni = n - f
+        d[n:] = 0
+        cf.cf_itft(ctx, cf.TransformParams(L, 0, n, ni, f), cf.DeviceView(d))
+        want_i.append(from_dev(d)[: ni + f, : lim + 1].copy())
+    errors = []
+
+    def worker(tid, host_api):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            for rep in range(6):
+                k = (tid + rep) % len(shapes)
+                z, n, f = shapes[k]
+                ni = n - f
+                if host_api:
+                    buf = inputs[k].copy()
+                    cf.cf_tft_host(ctx, cf.TransformParams(L, 0, z, n), buf)
+                    got_t = buf[:n, : lim + 1].copy()
+                    buf[n:] = 0
+                    cf.cf_itft_host(ctx, cf.TransformParams(L, 0, n, ni, f), buf)
+                    got_i = buf[: ni + f, : lim + 1]
+                else:
+                    with torch.cuda.stream(stream):
+                        d = to_dev(inputs[k])
+                        cf.cf_tft(ctx, cf.TransformParams(L, 0, z, n), cf.DeviceView(d), stream=stream)
+                        stream.synchronize()
+                        got_t = from_dev(d)[:n, : lim + 1].copy()
+                        d[n:] = 0
+                        cf.cf_itft(ctx, cf.TransformParams(L, 0, n, ni, f), cf.DeviceView(d), stream=stream)
+                        stream.synchronize()
+                        got_i = from_dev(d)[: ni + f, : lim + 1]
+                if not np.array_equal(got_t, want_t[k]):
+                    errors.append((tid, rep, k, "tft", host_api))
+                if not np.array_equal(got_i, want_i[k]):
+                    errors.append((tid, rep, k, "itft", host_api))
+        except Exception as ex:  # noqa: BLE001
+            errors.append((tid, repr(ex)))
+
+    for host_api in (False, True):
+        ts = [threading.Thread(target=worker, args=(t, host_api)) for t in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    assert not errors, errors
