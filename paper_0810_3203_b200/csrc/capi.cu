@@ -1345,6 +1345,16 @@ void json_plan(std::ostringstream& os, const Plan& p, u64 lane_bits) {
       os << ",\"net\":[";
       for (u32 i = 0; i < nn; ++i) os << (i ? "," : "") << (p.wave_ops[p.wave_op_begin[c] + i] >> 16);
       os << "]";
+      if (k.key.ell == 6) {
+        // stage B re-gauged (Planner::wide_network): per (warp, op) the input
+        // gauge g (ops 0..7) and the residual rotation, as {g, res}
+        os << ",\"net_g\":[";
+        for (u32 i = 96; i < 192; ++i) {
+          const u32 wd = p.wave_ops[p.wave_op_begin[c] + i];
+          os << (i > 96 ? "," : "") << "[" << ((wd >> 4) & 63u) << "," << ((wd >> 10) & 63u) << "]";
+        }
+        os << "]";
+      }
     }
     os << ",\"levels\":[";
     for (size_t l = 0; l < k.level_begin.size(); ++l) os << (l ? "," : "") << k.level_begin[l];

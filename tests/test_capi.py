@@ -378,3 +378,48 @@ def test_ring_create_ranges_and_primality():
     with pytest.raises(cf.InvalidParams):
         cf.PrimeRingCtx(4, 7)  # prime, 16 does not divide 6
     assert cf.PrimeRingCtx(4, 97).root_order() == 16
+
+
+def test_regauged_stage_b_equals_the_plain_network():
+    """Stage B of the radix-64 kernel reads its slots re-gauged (wave_tma.cuh,
+    net8_g): slot j as 2^(g_j unit) * slot j, seven butterflies without any
+    rotation, five with a residual one.  With the planner's gauges and
+    residuals (plan_dump's net_g) that must be the plain network -- 12
+    butterflies (a, b) <- (a + 2^(q unit) b, a - 2^(q unit) b) -- output for
+    output, over Z/(2^N+1), for every stage-B network of every radix-64 class
+    of the C2- and C5-shaped plans."""
+    rnd = random.Random(77)
+    rot_dif, rot_dit = {6, 7, 9, 10, 11}, {5, 7, 9, 10, 11}
+    seen = 0
+    for N, L, z, n in ((32768, 1 << 16, 40000, 50001), (131072, 1 << 18, 200000, 200000)):
+        ctx = cf.FermatRingCtx(N)
+        P, M = (1 << N) + 1, 2 * N
+        unit = M >> 6
+        for inv in (False, True):
+            prm = cf.TransformParams(L, 0, max(z, n) if inv else z, n, 0) if inv else cf.TransformParams(L, 0, z, n)
+            plan = cf.plan_dump(ctx, inv, prm)
+            for c in plan["classes"]:
+                if c["ell"] != 6 or not c.get("net_g"):
+                    continue
+                dif = c["wnet"] == 1
+                mask = rot_dif if dif else rot_dit
+                for w in range(8):
+                    q = c["net"][(8 + w) * 12: (9 + w) * 12]
+                    gr = c["net_g"][w * 12: (w + 1) * 12]
+                    x = [rnd.randrange(P) for _ in range(8)]
+                    y = [(x[j] * pow(2, (gr[j][0] * unit) % M, P)) % P for j in range(8)]
+                    assert gr[0][0] == 0
+                    for o in range(12):
+                        ll, jj = divmod(o, 4)
+                        hl = (4 >> ll) if dif else (1 << ll)
+                        a = (jj // hl) * 2 * hl + jj % hl
+                        b = a + hl
+                        xb = (x[b] * pow(2, (q[o] * unit) % M, P)) % P
+                        x[a], x[b] = (x[a] + xb) % P, (x[a] - xb) % P
+                        if o not in mask:
+                            assert gr[o][1] == 0, "a residual rotation outside the kernel's mask"
+                        yb = (y[b] * pow(2, (gr[o][1] * unit) % M, P)) % P
+                        y[a], y[b] = (y[a] + yb) % P, (y[a] - yb) % P
+                    assert x == y, (N, inv, w)
+                    seen += 1
+    assert seen >= 32
