@@ -839,6 +839,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const bool prog = PROG && (d.nstore_wnet >> 16) == 3u;
     const u32 opa = !prog && lane < 12 ? __ldg(A.wops + d.wop_begin + w * 12u + lane) : 0u;
     const u32 opb = !prog && lane < 12 ? __ldg(A.wops + d.wop_begin + (8u + w) * 12u + lane) : 0u;
+    // (the store table first: off the path between stage A and stage B, and
+    // it overlaps the wait for the loads)
+    slot_table<DIF>(A, d, w, lane, tab);
     // ---- stage A
     cp_async_wait<0>();
     __syncwarp();
@@ -866,7 +869,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     } else {
       stage_a<DIF, UNAL>(d, c, w, pos, pre, opa, tile, sm_s, logS, ring_next);
     }
-    slot_table<DIF>(A, d, w, lane, tab);
     named_bar(1u + grp, 256u);  // the group's stage-A outputs are in the tile
     if (prog) {
       const u32* pg = A.wops + d.wop_begin;
