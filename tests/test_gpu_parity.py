@@ -319,6 +319,8 @@ def test_native_dist_path_on_one_gpu():
         a[z:] = 0
         col = to_dev(a)
         geo = nd.geometry(cf.TransformParams(L, 0, z, z))
+        # a ring that runs radix-64 leaves takes the single-GPU plan's own split
+        assert geo["L1"] == 64 and geo["L2"] == L // 64
         rows = torch.empty((geo["row_elems"], W), dtype=torch.int64, device="cuda")
         nd.tft(cf.TransformParams(L, 0, z, z), col, rows)
         nd.itft(cf.TransformParams(L, 0, z, z, 0), rows, col)
